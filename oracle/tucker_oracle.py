@@ -1,0 +1,397 @@
+"""fp64 CPU oracle for the HOOI / Multislice-Projection hot path.
+
+TEST INFRASTRUCTURE ONLY.  Only ``tests/``, ``__graft_entry__.smoke()`` and
+``bench.py``'s ``cpu_baseline`` / ``--impl reference`` legs may import this
+module.  The product path (``paper_0711_2023_b200`` + ``libtucker.so``) never
+imports, links or executes it, and it shares no code with that path.
+
+Every function is a plain restatement of PAPER.md (``P:<line>``) in float64 with
+numpy/scipy primitives (sparse x dense product, tensordot, matmul, ``eigh``).
+There is no blocking, fusion or reordering beyond what the definitions state.
+Readings of ambiguous passages are the SURVEY.md §8(c) ledger entries A1-A18,
+restated in DESIGN.md.
+
+Parity status per function:
+  unfold, ttm, tucker_operator, fit_dense   pinned (tests/test_oracle_pins.py)
+  ttm_chain_unfold                           pinned (brute force P8, Kronecker law)
+  leading_eigenvectors                       pinned (SPEC worked examples, residual)
+  hooi_sweep / run_hooi                      pinned (P1, P2, P4, P10, P12)
+  mp_gram / mp_gram_slices / run_mp          pinned (P1, P4, P6, P9, P12)
+  core / fit_from_core                       pinned (P2, P7)
+  hosvd, pseudo_hosvd                        pinned (P5, P6, P12)
+"""
+from __future__ import annotations
+
+import numpy as np
+import scipy.sparse as sp
+
+# ---------------------------------------------------------------------------
+# Dense notation (§3)
+# ---------------------------------------------------------------------------
+
+
+def unfold(X: np.ndarray, n: int) -> np.ndarray:
+    """Mode-n matricization X_(n) (Eqs. 3-6).
+
+    Columns are mode-n fibers, ordered with the lower-numbered remaining modes
+    varying fastest (Eq. 3: X_(1) = [x_:11 x_:21 ... x_:I2I3]).  Reading A9
+    extends the rule to every mode.  `n` is 0-based here.
+    """
+    return np.moveaxis(X, n, 0).reshape(X.shape[n], -1, order="F")
+
+
+def fold(M: np.ndarray, n: int, dims) -> np.ndarray:
+    """Inverse of :func:`unfold`."""
+    rest = [d for i, d in enumerate(dims) if i != n]
+    return np.moveaxis(M.reshape([dims[n]] + rest, order="F"), 0, n)
+
+
+def ttm(X: np.ndarray, A: np.ndarray, n: int) -> np.ndarray:
+    """n-mode product Y = X x_n A, Eq. 1:
+    y_{..j..} = sum_{i_n} x_{..i_n..} a_{j i_n}.  Uses Y_(n) = A X_(n)."""
+    dims = list(X.shape)
+    dims[n] = A.shape[0]
+    return fold(A @ unfold(X, n), n, dims)
+
+
+def tucker_operator(G: np.ndarray, factors) -> np.ndarray:
+    """[[G; A1..AN]] = G x_1 A1 x_2 ... x_N AN, Eq. 7."""
+    Y = G
+    for n, A in enumerate(factors):
+        Y = ttm(Y, A, n)
+    return Y
+
+
+def fit_dense(X: np.ndarray, Xhat: np.ndarray) -> float:
+    """fit = 1 - ||X - Xhat||_F / ||X||_F, Eq. 9."""
+    nx = np.linalg.norm(X.ravel())
+    if nx == 0:
+        raise ValueError("fit undefined for a zero tensor (S:95)")
+    return float(1.0 - np.linalg.norm((X - Xhat).ravel()) / nx)
+
+
+# ---------------------------------------------------------------------------
+# Sparse tensor container (COO: one <i,j,k,x> per nonzero)
+# ---------------------------------------------------------------------------
+
+
+class SparseTensor:
+    """Order-N COO tensor in float64 (0-based indices)."""
+
+    def __init__(self, dims, idx, vals):
+        self.dims = tuple(int(d) for d in dims)
+        self.N = len(self.dims)
+        self.idx = [np.asarray(a, dtype=np.int64) for a in idx]
+        self.vals = np.asarray(vals, dtype=np.float64)
+        assert len(self.idx) == self.N
+        keep = self.vals != 0.0  # explicit zeros are dropped
+        if not keep.all():
+            self.idx = [a[keep] for a in self.idx]
+            self.vals = self.vals[keep]
+
+    @classmethod
+    def from_dense(cls, X: np.ndarray) -> "SparseTensor":
+        nz = np.nonzero(X)
+        return cls(X.shape, nz, X[nz])
+
+    def to_dense(self) -> np.ndarray:
+        X = np.zeros(self.dims)
+        np.add.at(X, tuple(self.idx), self.vals)
+        return X
+
+    def norm2(self) -> float:
+        """||X||_F^2."""
+        return float(np.dot(self.vals, self.vals))
+
+    def matrix(self, rows: list[int], col: int) -> sp.csr_matrix:
+        """The sparse matrix whose row is the linear index over `rows` modes
+        (lowest mode fastest) and whose column is the index in mode `col`."""
+        r = np.zeros_like(self.vals, dtype=np.int64)
+        stride = 1
+        for m in rows:
+            r += self.idx[m] * stride
+            stride *= self.dims[m]
+        return sp.csr_matrix((self.vals, (r, self.idx[col])), shape=(stride, self.dims[col]))
+
+
+# ---------------------------------------------------------------------------
+# HOOI projection: Z = [[X; A1^T, ..., I_n, ..., AN^T]] (Fig. 4)
+# ---------------------------------------------------------------------------
+
+
+def ttm_chain(T: SparseTensor, U, n: int) -> np.ndarray:
+    """Dense tensor Z = X x_{m != n} U_m^T (Fig. 4 `Z <- [[X; A(1)T..I_n..A(N)T]]`).
+
+    Axis m of the result has size J_m for m != n and I_n for m == n.
+    The first product is sparse x dense (Eq. 1 over the nonzeros), the rest are
+    dense n-mode products (Eq. 1).  Product order is irrelevant mathematically
+    (the n-mode products in distinct modes commute); the smallest J goes first
+    only to bound memory.
+    """
+    others = sorted((m for m in range(T.N) if m != n), key=lambda m: U[m].shape[1])
+    m0 = others[0]
+    rest_modes = [m for m in range(T.N) if m != m0]
+    # X x_{m0} U_{m0}^T : rows = linear index over rest_modes (lowest fastest)
+    Z = T.matrix(rest_modes, m0) @ np.asarray(U[m0], dtype=np.float64)
+    shape_rest = [T.dims[m] for m in rest_modes]
+    Z = Z.reshape(shape_rest + [U[m0].shape[1]], order="F")
+    # axes currently: rest_modes..., m0 -> move m0 back into its slot
+    Z = np.moveaxis(Z, -1, m0)
+    for m in others[1:]:
+        Z = ttm(Z, np.asarray(U[m], dtype=np.float64).T, m)
+    return Z
+
+
+def ttm_chain_unfold(T: SparseTensor, U, n: int) -> np.ndarray:
+    """Y_(n) = Z_(n), I_n x prod_{m != n} J_m, Kolda column order (Eqs. 3-6)."""
+    return unfold(ttm_chain(T, U, n), n)
+
+
+def leading_eigenvectors(S: np.ndarray, J: int):
+    """J leading eigenvectors of symmetric S (Fig. 4 `A(n) <- J_n leading
+    eigenvectors of Z_(n) Z_(n)^T`), descending eigenvalue order, each column
+    sign-canonicalised (largest-magnitude entry positive, ties -> lowest
+    index).  Reading A2: the eigenvectors of M (not of M M^T).
+    Returns (U, w_all_descending)."""
+    S = np.asarray(S, dtype=np.float64)
+    w, V = np.linalg.eigh(0.5 * (S + S.T))
+    order = np.argsort(-w, kind="stable")
+    w = w[order]
+    V = V[:, order[:J]].copy()
+    for j in range(V.shape[1]):
+        k = int(np.argmax(np.abs(V[:, j])))  # argmax returns lowest index on ties
+        if V[k, j] < 0:
+            V[:, j] = -V[:, j]
+    return V, w
+
+
+def eig_diag(w: np.ndarray, J: int) -> dict:
+    """lambda_1, lambda_J, lambda_{J+1}, relative gap and kappa (§8(c) item 6)."""
+    lJ = w[J - 1]
+    lJ1 = w[J] if J < w.size else 0.0
+    gap = lJ - lJ1
+    return dict(l1=float(w[0]), lJ=float(lJ), lJ1=float(lJ1),
+                rel_gap=float(gap / lJ) if lJ != 0 else 0.0,
+                kappa=float(w[0] / gap) if gap > 0 else float("inf"))
+
+
+def hooi_sweep(T: SparseTensor, U, core, diag=None):
+    """One pass of Fig. 4's main loop body: for n = 1..N in order,
+    Z <- [[X; A(1)T..I_n..A(N)T]], A(n) <- J_n leading eigenvectors of
+    Z_(n) Z_(n)^T.  Gauss-Seidel: later modes use the freshly updated factors.
+    Returns (U_new, Y_last) where Y_last = Z_(N) of the final mode."""
+    U = [np.asarray(u, dtype=np.float64) for u in U]
+    Y = None
+    for n in range(T.N):
+        Y = ttm_chain_unfold(T, U, n)
+        S = Y @ Y.T
+        U[n], w = leading_eigenvectors(S, core[n])
+        if diag is not None:
+            diag.append(dict(mode=n, **eig_diag(w, core[n])))
+    return U, Y
+
+
+# ---------------------------------------------------------------------------
+# Multislice Projection (Fig. 7, Fig. 8, Appendix)
+# ---------------------------------------------------------------------------
+
+
+def mp_term_unfold(T: SparseTensor, Um: np.ndarray, n: int, m: int) -> np.ndarray:
+    """W = (X x_m U_m^T)_(n): I_n x (J_m * prod_{k not in {n,m}} I_k), Kolda order.
+
+    Its column block for one slice s (all modes other than n, m fixed) is
+    P_s = X_s U_m, where X_s is the I_n x I_m slice (orientation as in Fig. 7:
+    X_{::i} B for n=1, m=2)."""
+    rest = [k for k in range(T.N) if k != m]
+    Z = T.matrix(rest, m) @ np.asarray(Um, dtype=np.float64)
+    Z = Z.reshape([T.dims[k] for k in rest] + [Um.shape[1]], order="F")
+    Z = np.moveaxis(Z, -1, m)
+    return unfold(Z, n)
+
+
+def mp_gram(T: SparseTensor, U, n: int) -> np.ndarray:
+    """M_n = sum_{m != n} sum_{slices s fixing all modes not in {n,m}} (X_s U_m)(X_s U_m)^T.
+
+    Fig. 7 (order 3) / Fig. 8 (order 4) main-loop M_n; Appendix
+    (``M1 = M1 + ((X2_slice*C)*(C'*X2_slice'))``).  Reading A1: this is a SUM of
+    single-mode projections, not HOOI's chain.  The slice sum equals W W^T with
+    W the column concatenation of the P_s blocks (pinned against
+    :func:`mp_gram_slices`, P9)."""
+    M = np.zeros((T.dims[n], T.dims[n]))
+    for m in range(T.N):
+        if m == n:
+            continue
+        W = mp_term_unfold(T, U[m], n, m)
+        M += W @ W.T
+    return M
+
+
+def mp_gram_slices(T: SparseTensor, U, n: int) -> np.ndarray:
+    """Literal slice loop of Figs. 7/8 (small inputs only): for each m != n and
+    each slice s fixing the modes not in {n, m}, M_n += X_s U_m U_m^T X_s^T."""
+    M = np.zeros((T.dims[n], T.dims[n]))
+    for m in range(T.N):
+        if m == n:
+            continue
+        Um = np.asarray(U[m], dtype=np.float64)
+        fixed = [k for k in range(T.N) if k not in (n, m)]
+        key = np.zeros_like(T.vals, dtype=np.int64)
+        for k in fixed:
+            key = key * T.dims[k] + T.idx[k]
+        for s in np.unique(key):
+            sel = key == s
+            Xs = sp.csr_matrix((T.vals[sel], (T.idx[n][sel], T.idx[m][sel])),
+                               shape=(T.dims[n], T.dims[m]))
+            P = Xs @ Um
+            M += P @ P.T
+    return M
+
+
+def mp_sweep(T: SparseTensor, U, core, diag=None):
+    """One pass of Fig. 7/8's main loop: for n = 1..N, M_n as above with the
+    freshest factors (Appendix: M2 uses the new A), then A(n) <- J_n leading
+    eigenvectors of M_n (reading A2: of M_n itself)."""
+    U = [np.asarray(u, dtype=np.float64) for u in U]
+    for n in range(T.N):
+        M = mp_gram(T, U, n)
+        U[n], w = leading_eigenvectors(M, core[n])
+        if diag is not None:
+            diag.append(dict(mode=n, **eig_diag(w, core[n])))
+    return U
+
+
+# ---------------------------------------------------------------------------
+# Core and fit (Fig. 4 last step P:629-631, Appendix, Eq. 9)
+# ---------------------------------------------------------------------------
+
+
+def core(T: SparseTensor, U) -> np.ndarray:
+    """G = [[X; A(1)T, ..., A(N)T]] (Figs. 1-8 final step): dense J_1 x..x J_N."""
+    Z = ttm_chain(T, U, T.N - 1)
+    return ttm(Z, np.asarray(U[T.N - 1], dtype=np.float64).T, T.N - 1)
+
+
+def fit_from_core(normX2: float, G: np.ndarray) -> float:
+    """Eq. 9 via ||X - Xhat||^2 = ||X||^2 - ||G||^2 for orthonormal factors and
+    G = [[X; U^T]] (reading A7/A8: (1 - fit)^2 = 1 - ||G||^2/||X||^2)."""
+    g2 = float(np.dot(G.ravel(), G.ravel()))
+    return 1.0 - np.sqrt(max(0.0, normX2 - g2)) / np.sqrt(normX2)
+
+
+def fit_residual(T: SparseTensor, G: np.ndarray, U) -> float:
+    """Eq. 9 by the dense residual (Appendix); small inputs only."""
+    X = T.to_dense()
+    return fit_dense(X, tucker_operator(G, [np.asarray(u, dtype=np.float64) for u in U]))
+
+
+# ---------------------------------------------------------------------------
+# Initialisations (NEXT 1) and drivers
+# ---------------------------------------------------------------------------
+
+
+def hosvd_factor(T: SparseTensor, n: int, J: int) -> np.ndarray:
+    """A(n) <- J_n leading eigenvectors of X_(n) X_(n)^T (Fig. 2)."""
+    others = [m for m in range(T.N) if m != n]
+    Xn = T.matrix(others, n).T.tocsr()  # I_n x prod(others)
+    S = (Xn @ Xn.T).toarray()
+    return leading_eigenvectors(S, J)[0]
+
+
+def pseudo_hosvd_gram(T: SparseTensor, n: int) -> np.ndarray:
+    """MP's initial M_n (Fig. 7, Fig. 8):
+    sum over the other modes m of sum_s X_s X_s^T for slices fixing modes not
+    in {n, m}; each term equals X_(n) X_(n)^T (pin P6)."""
+    M = np.zeros((T.dims[n], T.dims[n]))
+    for m in range(T.N):
+        if m == n:
+            continue
+        fixed = [k for k in range(T.N) if k not in (n, m)]
+        # rows: i_n ; cols: (i_m, fixed...) -- the concatenation of the X_s blocks
+        Xn = T.matrix([m] + fixed, n).T.tocsr()
+        M += (Xn @ Xn.T).toarray()
+    return M
+
+
+def run_hooi(T: SparseTensor, U0, core_dims, sweeps: int, diag=None):
+    """Fixed-sweep HOOI from given factors (reading A5/A6); U0[0] is unused
+    (Fig. 3 caption P:598-602).  Returns dict(U, G, fits)."""
+    U = [np.asarray(u, dtype=np.float64) for u in U0]
+    nx2 = T.norm2()
+    fits = []
+    for _ in range(sweeps):
+        U, _Y = hooi_sweep(T, U, core_dims, diag)
+        fits.append(fit_from_core(nx2, core(T, U)))
+    G = core(T, U)
+    return dict(U=U, G=G, fits=fits, fit=fit_from_core(nx2, G))
+
+
+def run_mp(T: SparseTensor, U0, core_dims, sweeps: int, diag=None):
+    """Fixed-sweep MP from given factors; U0[0] is unused (Appendix
+    uses B, C only to form M1)."""
+    U = [np.asarray(u, dtype=np.float64) for u in U0]
+    nx2 = T.norm2()
+    fits = []
+    for _ in range(sweeps):
+        U = mp_sweep(T, U, core_dims, diag)
+        fits.append(fit_from_core(nx2, core(T, U)))
+    G = core(T, U)
+    return dict(U=U, G=G, fits=fits, fit=fit_from_core(nx2, G))
+
+
+def run_hooi_converged(T: SparseTensor, core_dims, tol=1e-4, maxit=50):
+    """The paper's HOOI: HO-SVD init of modes 2..N (Fig. 4), then
+    sweeps until Delta_fit < 1e-4 or 50 iterations (Eq. 10)."""
+    U = [None] + [hosvd_factor(T, n, core_dims[n]) for n in range(1, T.N)]
+    U[0] = np.zeros((T.dims[0], core_dims[0]))
+    nx2 = T.norm2()
+    old, fit, it = 0.0, 0.0, 0
+    for it in range(1, maxit + 1):
+        U, _ = hooi_sweep(T, U, core_dims)
+        fit = fit_from_core(nx2, core(T, U))
+        if fit - old < tol:
+            break
+        old = fit
+    return dict(U=U, fit=fit, iters=it)
+
+
+def run_mp_converged(T: SparseTensor, core_dims, tol=1e-4, maxit=50):
+    """The paper's MP: pseudo HO-SVD init of modes 2..N (Fig. 7/8), then the
+    main loop until (fit - old_fit) < 1e-4 or 50 loops (Appendix)."""
+    U = [np.zeros((T.dims[0], core_dims[0]))] + [
+        leading_eigenvectors(pseudo_hosvd_gram(T, n), core_dims[n])[0] for n in range(1, T.N)]
+    nx2 = T.norm2()
+    old, fit, it = 0.0, 0.0, 0
+    for it in range(1, maxit + 1):
+        U = mp_sweep(T, U, core_dims)
+        fit = fit_from_core(nx2, core(T, U))
+        if fit - old < tol:
+            break
+        old = fit
+    return dict(U=U, fit=fit, iters=it)
+
+
+def run_hosvd(T: SparseTensor, core_dims):
+    """HO-SVD (Fig. 2): every factor from X alone, then the core and fit."""
+    U = [hosvd_factor(T, n, core_dims[n]) for n in range(T.N)]
+    return dict(U=U, fit=fit_from_core(T.norm2(), core(T, U)))
+
+
+# ---------------------------------------------------------------------------
+# Parity metrics (north star tolerances)
+# ---------------------------------------------------------------------------
+
+
+def projector_distance(U: np.ndarray, V: np.ndarray) -> float:
+    """||U U^T - V V^T||_F (sign- and rotation-invariant) for orthonormal U, V,
+    computed without the I x I projectors and without cancellation:
+    ||U U^T - V V^T||^2 = J_u + J_v - 2||U^T V||^2 = ||U - V V^T U||^2 + ||V - U U^T V||^2."""
+    U = np.asarray(U, dtype=np.float64)
+    V = np.asarray(V, dtype=np.float64)
+    a = U - V @ (V.T @ U)
+    b = V - U @ (U.T @ V)
+    return float(np.sqrt(np.sum(a * a) + np.sum(b * b)))
+
+
+def rel_frobenius(A: np.ndarray, B: np.ndarray) -> float:
+    B = np.asarray(B, dtype=np.float64)
+    return float(np.linalg.norm(np.asarray(A, dtype=np.float64) - B) / np.linalg.norm(B))
