@@ -1,0 +1,169 @@
+/*
+ * tucker.h -- C-ABI of libtucker.so, the B200 (sm_100a) hot path shared by HOOI
+ * and Multislice Projection (MP) from arxiv/paper_0711_2023.
+ *
+ * Citations: P:<line> = PAPER.md line.  Operation set: SURVEY.md §8(b).
+ *
+ * Conventions (all entry points)
+ *   - order N, dims I_1..I_N, core J_1..J_N (Eq. 8): "Tucker
+ *     decomposition X ~ [[G; A(1)..A(N)]]", A(n) is I_n x J_n with orthonormal
+ *     columns.
+ *   - Indices are 0-BASED int32 (the paper's text files are 1-based).
+ *   - Nonzero values are fp32; explicit zeros are accepted and dropped.
+ *   - Factor matrices are fp32, ROW-MAJOR I_n x J_n (element (i,j) at i*J_n+j).
+ *   - The core G is fp32, mode-1 fastest: G(j1..jN) at j1 + J1*(j2 + J2*(...)).
+ *   - Unfoldings Y_(n) use the Kolda column order (Eqs. 3-6): the
+ *     remaining modes in increasing order, lower modes varying fastest.
+ *   - All calls are blocking (stream-synchronised on return) and not
+ *     re-entrant per handle.  Different handles may be used from different
+ *     threads.
+ *   - Multi-GPU (world > 1): collective -- every rank makes the same call
+ *     sequence with the same arguments (round-1 builds accept world == 1 only
+ *     and return TUCKER_E_ARG otherwise).
+ *
+ * Return value: 0 (TUCKER_OK) or one of the TUCKER_E_* codes below; a
+ * human-readable message for the code is tucker_strerror(code) and the last
+ * detailed message of a handle is tucker_last_error(h).
+ *
+ * Ownership: tucker_init copies every input; the caller may free them on
+ * return.  The handle owns all device memory it allocates.  Output buffers are
+ * caller-owned host (or, with TUCKER_OUTPUT_ON_DEVICE, device) memory.
+ */
+#ifndef TUCKER_H
+#define TUCKER_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TUCKER_OK 0
+#define TUCKER_E_ARG 1     /* null pointer, order/dims/core/nnz/sweeps out of range          */
+#define TUCKER_E_INDEX 2   /* an index outside [0, I_n)                                        */
+#define TUCKER_E_DUP 3     /* duplicate coordinate                                */
+#define TUCKER_E_VALUE 4   /* non-finite value, or ||X|| = 0 (fit undefined, Eq. 9)            */
+#define TUCKER_E_FACTOR 5  /* initial factor not orthonormal (max|U^T U - I| > 1e-5)           */
+#define TUCKER_E_CUDA 6    /* CUDA runtime error (message in tucker_last_error)                */
+#define TUCKER_E_NCCL 7    /* NCCL error                                                       */
+#define TUCKER_E_OOM 8     /* device allocation failed                                         */
+#define TUCKER_E_STATE 9   /* call out of order (e.g. a debug query before it is available)    */
+#define TUCKER_E_CONVERGE 10 /* eigensolver hit its iteration cap above tolerance (result kept) */
+
+/* flags */
+#define TUCKER_INPUT_ON_DEVICE 0x1u   /* idx/vals/U0 pointers are device pointers                */
+#define TUCKER_OUTPUT_ON_DEVICE 0x2u  /* core_out/U_out/Y/S outputs are device pointers          */
+
+typedef struct tucker_handle tucker_handle;
+
+typedef struct {
+  int device;                 /* CUDA device ordinal for this rank                             */
+  int rank, world;            /* one rank per GPU; world == 1 in this build                     */
+  const void* nccl_unique_id; /* 128-byte ncclUniqueId (NULL when world == 1)                   */
+  void* stream;               /* cudaStream_t to run on (NULL = the handle's own stream)        */
+  int eig_oversample;         /* p in block size k = J + p (0 = default)         */
+  int eig_max_iter;           /* cap on Chebyshev-filter outer iterations (0 = default 40)      */
+  double eig_tol;             /* Ritz residual tolerance relative to theta_1 (0 = default)      */
+  unsigned flags;             /* TUCKER_* flags above                                           */
+} tucker_opts;
+
+/* Fill *opts with defaults (device 0, world 1, own stream). */
+void tucker_default_opts(tucker_opts* opts);
+
+/*
+ * tucker_init -- load an order-N sparse tensor and the initial factors.
+ *
+ *   order   N in {3, 4} (MP is defined for orders 3 and 4 only, Figs. 7-8
+ *           P:911-1114; SURVEY reading A18).
+ *   dims    I_1..I_N, each >= 1 and I_n < 2^31.
+ *   core    J_1..J_N, 1 <= J_n <= min(I_n, 128) (this build's eigensolver
+ *           block limit; TUCKER_E_ARG otherwise).
+ *   nnz     number of COO entries (>= 1).
+ *   idx     N pointers to int32[nnz], 0-based coordinates (any order).
+ *   vals    fp32[nnz].
+ *   U0      N pointers to fp32 I_n x J_n row-major, orthonormal columns (the
+ *           north star's seeded random orthonormal factors; SURVEY reading A5).
+ *           HOOI ignores U0[0] (Fig. 3 caption P:598-602); MP ignores U0[0]
+ *           too (Appendix P:1818-1830 forms M1 from B, C only).
+ *   opts    NULL for defaults.
+ * Work: copies inputs to the device, validates them, builds the sorted
+ * slice/fiber structures (CSF) for every ordering the sweeps need (the paper's
+ * "sort by mode n, one slice per index" step, done in HBM), and
+ * computes ||X||_F^2 in fp64.
+ * Errors: E_ARG, E_INDEX, E_DUP, E_VALUE, E_FACTOR, E_OOM, E_CUDA.
+ */
+int tucker_init(tucker_handle** out, int order, const int64_t* dims, const int64_t* core,
+                int64_t nnz, const int32_t* const* idx, const float* vals,
+                const float* const* U0, const tucker_opts* opts);
+
+/*
+ * hooi_sweep -- `sweeps` passes of HOOI's main loop (Fig. 4): for
+ * n = 1..N, Y_(n) = (X x_{m != n} U_m^T)_(n) (SpTTMc), S = Y Y^T or Y^T Y
+ * (whichever is smaller, fp64), U_n = J_n leading eigenvectors (descending,
+ * sign-canonical: largest |entry| positive).  Gauss-Seidel order.
+ *   fit_per_sweep  nullable, double[sweeps]: Eq. 9 fit after each sweep.
+ *   stage_ms       nullable, float[sweeps * 4]: per sweep {spttmc, gram, eig, corefit} ms.
+ * Errors: E_ARG (sweeps < 1), E_CUDA, E_CONVERGE (factors still returned).
+ */
+int hooi_sweep(tucker_handle* h, int sweeps, double* fit_per_sweep, float* stage_ms);
+
+/*
+ * mp_sweep -- `sweeps` passes of MP's main loop (Fig. 7, Fig. 8
+ * P:1040-1096, Appendix): for n = 1..N,
+ *   M_n = sum_{m != n} sum_{slices s fixing the modes not in {n,m}} (X_s U_m)(X_s U_m)^T
+ * (fp64, I_n x I_n), U_n = J_n leading eigenvectors of M_n (SURVEY reading A2:
+ * of M_n, not M_n M_n^T).  Same output arguments as hooi_sweep
+ * (stage_ms entries: {spmm, gram, eig, corefit}).
+ */
+int mp_sweep(tucker_handle* h, int sweeps, double* fit_per_sweep, float* stage_ms);
+
+/*
+ * core_and_fit -- G = [[X; U_1^T..U_N^T]] (Figs. 1-8 final step) and
+ * fit = 1 - sqrt(max(0, ||X||^2 - ||G||^2)) / ||X|| (Eq. 9 with the norm
+ * identity for orthonormal factors; SURVEY readings A7/A8).
+ *   core_out  nullable, fp32[prod J], mode-1 fastest.
+ *   U_out     nullable, N nullable pointers to fp32 I_n x J_n row-major.
+ *   fit_out   nullable.
+ */
+int core_and_fit(tucker_handle* h, float* core_out, float* const* U_out, double* fit_out);
+
+/* Overwrite the handle's current factors (same layout as U0); lets a caller
+ * restart HOOI/MP from the same U0 without rebuilding the CSF. */
+int tucker_set_factors(tucker_handle* h, const float* const* U);
+
+/* Release all device memory.  NULL is accepted. */
+int tucker_free(tucker_handle* h);
+
+const char* tucker_strerror(int code);
+const char* tucker_last_error(const tucker_handle* h);
+
+/* ------------------------------------------------------------------------
+ * Diagnostic entry points (used by the parity tests; same kernels as the
+ * sweeps, no side effect on the factors).
+ * ---------------------------------------------------------------------- */
+
+/* Y_(n) = (X x_{m != n} U_m^T)_(n) with the handle's CURRENT factors:
+ * fp32 I_n x prod_{m!=n} J_m row-major, Kolda column order.  mode is 0-based. */
+int tucker_debug_ttmc(tucker_handle* h, int mode, float* Y_out);
+
+/* The fp64 Gram that the next update of `mode` would diagonalise, with the
+ * current factors: algo 0 = HOOI (S = Y Y^T, I_n x I_n, always returned in this
+ * orientation), algo 1 = MP (M_n, I_n x I_n).  Row-major fp64. */
+int tucker_debug_gram(tucker_handle* h, int algo, int mode, double* S_out);
+
+/* Leading-J eigenvectors (descending, sign-canonical, fp32 row-major d x J) and
+ * eigenvalues (fp64[J]) of a caller-provided symmetric fp64 d x d matrix, with
+ * the library's eigensolver.  1 <= J <= min(d, 128). */
+int tucker_debug_eig(tucker_handle* h, int d, int J, const double* S, float* U_out,
+                     double* evals_out);
+
+/* Kernel statistics of the handle since the last reset (for bench/roofline):
+ * stats[0] = kernel launches issued by the library, [1] = eigensolver outer
+ * iterations, [2] = Chebyshev matvecs, [3] = small (k x k) Jacobi sweeps. */
+int tucker_stats(tucker_handle* h, int64_t* stats, int reset);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* TUCKER_H */

@@ -1,0 +1,247 @@
+"""Thin ctypes binding of libtucker.so (include/tucker.h).
+
+Argument marshalling only: every step of the path runs in the library's CUDA
+kernels.  The module fails loudly (ImportError) when libtucker.so is missing;
+there is no CPU fallback.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libtucker.so")
+
+TUCKER_INPUT_ON_DEVICE = 0x1
+TUCKER_OUTPUT_ON_DEVICE = 0x2
+E_CONVERGE = 10
+
+# every symbol declared in include/tucker.h
+EXPORTS = [
+    "tucker_default_opts", "tucker_init", "hooi_sweep", "mp_sweep", "core_and_fit",
+    "tucker_set_factors", "tucker_free", "tucker_strerror", "tucker_last_error",
+    "tucker_debug_ttmc", "tucker_debug_gram", "tucker_debug_eig", "tucker_stats",
+]
+
+
+class tucker_opts(C.Structure):
+    _fields_ = [
+        ("device", C.c_int), ("rank", C.c_int), ("world", C.c_int),
+        ("nccl_unique_id", C.c_void_p), ("stream", C.c_void_p),
+        ("eig_oversample", C.c_int), ("eig_max_iter", C.c_int), ("eig_tol", C.c_double),
+        ("flags", C.c_uint),
+    ]
+
+
+def load(path: str = LIB_PATH) -> C.CDLL:
+    if not os.path.exists(path):
+        raise ImportError(f"libtucker.so not built ({path}); run __graft_entry__.build()")
+    lib = C.CDLL(path)
+    P = C.c_void_p
+    i64p = C.POINTER(C.c_int64)
+    lib.tucker_default_opts.argtypes = [C.POINTER(tucker_opts)]
+    lib.tucker_default_opts.restype = None
+    lib.tucker_init.argtypes = [C.POINTER(P), C.c_int, i64p, i64p, C.c_int64, C.POINTER(P), P,
+                                C.POINTER(P), C.POINTER(tucker_opts)]
+    lib.hooi_sweep.argtypes = [P, C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_float)]
+    lib.mp_sweep.argtypes = [P, C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_float)]
+    lib.core_and_fit.argtypes = [P, P, C.POINTER(P), C.POINTER(C.c_double)]
+    lib.tucker_set_factors.argtypes = [P, C.POINTER(P)]
+    lib.tucker_free.argtypes = [P]
+    lib.tucker_strerror.argtypes = [C.c_int]
+    lib.tucker_strerror.restype = C.c_char_p
+    lib.tucker_last_error.argtypes = [P]
+    lib.tucker_last_error.restype = C.c_char_p
+    lib.tucker_debug_ttmc.argtypes = [P, C.c_int, P]
+    lib.tucker_debug_gram.argtypes = [P, C.c_int, C.c_int, P]
+    lib.tucker_debug_eig.argtypes = [P, C.c_int, C.c_int, P, P, P]
+    lib.tucker_stats.argtypes = [P, i64p, C.c_int]
+    for name in EXPORTS:
+        if name not in ("tucker_default_opts", "tucker_strerror", "tucker_last_error"):
+            getattr(lib, name).restype = C.c_int
+    return lib
+
+
+_lib = None
+
+
+def lib() -> C.CDLL:
+    global _lib
+    if _lib is None:
+        _lib = load()
+    return _lib
+
+
+class TuckerError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"[{code}] {msg}")
+        self.code = code
+
+
+def _check(rc: int, h=None, allow=()):
+    if rc != 0 and rc not in allow:
+        L = lib()
+        detail = L.tucker_last_error(h).decode() if h else ""
+        raise TuckerError(rc, L.tucker_strerror(rc).decode() + (": " + detail if detail else ""))
+    return rc
+
+
+def _ptr(a) -> int:
+    """Address of a numpy array or a torch tensor (host or device)."""
+    if hasattr(a, "data_ptr"):
+        return a.data_ptr()
+    return a.ctypes.data
+
+
+def tucker_init(dims, core, idx, vals, U0, *, device=0, stream=None, eig_oversample=0,
+                eig_max_iter=0, eig_tol=0.0, on_device=False):
+    """Returns an opaque handle (int).  idx: list of N int32 arrays (0-based),
+    vals: fp32, U0: list of N fp32 row-major I_n x J_n arrays.  Host numpy
+    arrays, or torch CUDA tensors with on_device=True."""
+    L = lib()
+    N = len(dims)
+    if not on_device:
+        idx = [np.ascontiguousarray(a, dtype=np.int32) for a in idx]
+        vals = np.ascontiguousarray(vals, dtype=np.float32)
+        U0 = [np.ascontiguousarray(u, dtype=np.float32) for u in U0]
+    o = tucker_opts()
+    L.tucker_default_opts(C.byref(o))
+    o.device = device
+    o.stream = stream
+    o.eig_oversample = eig_oversample
+    o.eig_max_iter = eig_max_iter
+    o.eig_tol = eig_tol
+    o.flags = TUCKER_INPUT_ON_DEVICE if on_device else 0
+    d = (C.c_int64 * N)(*[int(x) for x in dims])
+    j = (C.c_int64 * N)(*[int(x) for x in core])
+    ip = (C.c_void_p * N)(*[_ptr(a) for a in idx])
+    up = (C.c_void_p * N)(*[_ptr(u) for u in U0])
+    h = C.c_void_p()
+    nnz = int(vals.numel() if hasattr(vals, "numel") else vals.size)
+    rc = L.tucker_init(C.byref(h), N, d, j, nnz, ip, C.c_void_p(_ptr(vals)), up, C.byref(o))
+    _check(rc)
+    return h.value
+
+
+def hooi_sweep(h, sweeps, want_stage=False):
+    fits = np.zeros(sweeps, dtype=np.float64)
+    stage = np.zeros(sweeps * 4, dtype=np.float32)
+    rc = lib().hooi_sweep(h, sweeps, fits.ctypes.data_as(C.POINTER(C.c_double)),
+                          stage.ctypes.data_as(C.POINTER(C.c_float)) if want_stage else None)
+    _check(rc, h, allow=(E_CONVERGE,))
+    return (fits, stage.reshape(sweeps, 4), rc) if want_stage else fits
+
+
+def mp_sweep(h, sweeps, want_fit=True, want_stage=False):
+    fits = np.zeros(sweeps, dtype=np.float64)
+    stage = np.zeros(sweeps * 4, dtype=np.float32)
+    rc = lib().mp_sweep(h, sweeps, fits.ctypes.data_as(C.POINTER(C.c_double)) if want_fit else None,
+                        stage.ctypes.data_as(C.POINTER(C.c_float)) if want_stage else None)
+    _check(rc, h, allow=(E_CONVERGE,))
+    return (fits, stage.reshape(sweeps, 4), rc) if want_stage else fits
+
+
+def core_and_fit(h, dims, core, want_core=True, want_factors=True):
+    N = len(dims)
+    G = np.zeros(int(np.prod(core)), dtype=np.float32) if want_core else None
+    Us = [np.zeros((dims[n], core[n]), dtype=np.float32) for n in range(N)] if want_factors else None
+    up = (C.c_void_p * N)(*[u.ctypes.data for u in Us]) if want_factors else None
+    fit = C.c_double()
+    rc = lib().core_and_fit(h, C.c_void_p(G.ctypes.data) if want_core else None, up, C.byref(fit))
+    _check(rc, h)
+    if want_core:
+        G = G.reshape(tuple(core), order="F")  # mode-1 fastest
+    return G, Us, fit.value
+
+
+def tucker_set_factors(h, U):
+    U = [np.ascontiguousarray(u, dtype=np.float32) for u in U]
+    up = (C.c_void_p * len(U))(*[u.ctypes.data for u in U])
+    _check(lib().tucker_set_factors(h, up), h)
+
+
+def tucker_free(h):
+    if h:
+        lib().tucker_free(h)
+
+
+def tucker_debug_ttmc(h, mode, I, P):
+    Y = np.zeros((I, P), dtype=np.float32)
+    _check(lib().tucker_debug_ttmc(h, mode, C.c_void_p(Y.ctypes.data)), h)
+    return Y
+
+
+def tucker_debug_gram(h, algo, mode, I):
+    S = np.zeros((I, I), dtype=np.float64)
+    _check(lib().tucker_debug_gram(h, algo, mode, C.c_void_p(S.ctypes.data)), h)
+    return S
+
+
+def tucker_debug_eig(h, S, J):
+    S = np.ascontiguousarray(S, dtype=np.float64)
+    d = S.shape[0]
+    U = np.zeros((d, J), dtype=np.float32)
+    w = np.zeros(J, dtype=np.float64)
+    rc = lib().tucker_debug_eig(h, d, J, C.c_void_p(S.ctypes.data), C.c_void_p(U.ctypes.data),
+                                C.c_void_p(w.ctypes.data))
+    _check(rc, h, allow=(E_CONVERGE,))
+    return U, w, rc
+
+
+def tucker_stats(h, reset=False):
+    s = (C.c_int64 * 4)()
+    _check(lib().tucker_stats(h, s, 1 if reset else 0), h)
+    return dict(launches=s[0], eig_outer=s[1], eig_matvec=s[2], jacobi_sweeps=s[3])
+
+
+class Tucker:
+    """Convenience wrapper owning one handle."""
+
+    def __init__(self, dims, core, idx, vals, U0, **kw):
+        self.dims = tuple(int(x) for x in dims)
+        self.core = tuple(int(x) for x in core)
+        self.h = tucker_init(self.dims, self.core, idx, vals, U0, **kw)
+
+    def hooi_sweep(self, sweeps, want_stage=False):
+        return hooi_sweep(self.h, sweeps, want_stage)
+
+    def mp_sweep(self, sweeps, want_fit=True, want_stage=False):
+        return mp_sweep(self.h, sweeps, want_fit, want_stage)
+
+    def core_and_fit(self, **kw):
+        return core_and_fit(self.h, self.dims, self.core, **kw)
+
+    def set_factors(self, U):
+        tucker_set_factors(self.h, U)
+
+    def debug_ttmc(self, mode):
+        P = int(np.prod([J for m, J in enumerate(self.core) if m != mode]))
+        return tucker_debug_ttmc(self.h, mode, self.dims[mode], P)
+
+    def debug_gram(self, algo, mode):
+        return tucker_debug_gram(self.h, algo, mode, self.dims[mode])
+
+    def debug_eig(self, S, J):
+        return tucker_debug_eig(self.h, S, J)
+
+    def stats(self, reset=False):
+        return tucker_stats(self.h, reset)
+
+    def close(self):
+        if self.h:
+            tucker_free(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()

@@ -1,0 +1,77 @@
+// common.cuh -- shared host/device utilities of libtucker (no method arithmetic).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstdio>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/tucker.h"
+
+namespace tk {
+
+struct Error {
+  int code;
+  std::string msg;
+};
+
+[[noreturn]] inline void fail(int code, const std::string& msg) { throw Error{code, msg}; }
+
+#define TK_CUDA(x)                                                                           \
+  do {                                                                                       \
+    cudaError_t e_ = (x);                                                                    \
+    if (e_ != cudaSuccess) {                                                                 \
+      ::tk::fail(e_ == cudaErrorMemoryAllocation ? TUCKER_E_OOM : TUCKER_E_CUDA,             \
+                 std::string(#x) + ": " + cudaGetErrorString(e_) + " at " + __FILE__ + ":" + \
+                     std::to_string(__LINE__));                                              \
+    }                                                                                        \
+  } while (0)
+
+// Launch counter shared by all launches of one handle (reported by tucker_stats).
+extern thread_local int64_t* g_launch_counter;
+
+#define TK_LAUNCH(kernel, grid, block, smem, stream, ...)                 \
+  do {                                                                    \
+    kernel<<<(grid), (block), (smem), (stream)>>>(__VA_ARGS__);           \
+    TK_CUDA(cudaGetLastError());                                          \
+    if (::tk::g_launch_counter) ++(*::tk::g_launch_counter);              \
+  } while (0)
+
+inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+inline int64_t round_up(int64_t a, int64_t b) { return ceil_div(a, b) * b; }
+
+// RAII device buffer.
+template <typename T>
+struct DBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  DBuf() = default;
+  explicit DBuf(size_t count) { alloc(count); }
+  DBuf(const DBuf&) = delete;
+  DBuf& operator=(const DBuf&) = delete;
+  DBuf(DBuf&& o) noexcept : p(o.p), n(o.n) { o.p = nullptr; o.n = 0; }
+  DBuf& operator=(DBuf&& o) noexcept {
+    if (this != &o) { release(); p = o.p; n = o.n; o.p = nullptr; o.n = 0; }
+    return *this;
+  }
+  ~DBuf() { release(); }
+  void alloc(size_t count) {
+    release();
+    if (count == 0) return;
+    TK_CUDA(cudaMalloc(&p, count * sizeof(T)));
+    n = count;
+  }
+  // grow-only reallocation (contents are not preserved)
+  void ensure(size_t count) { if (count > n) alloc(count); }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+  size_t bytes() const { return n * sizeof(T); }
+};
+
+}  // namespace tk

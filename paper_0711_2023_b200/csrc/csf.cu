@@ -1,0 +1,306 @@
+// csf.cu -- COO validation and COO -> CSF (sorted slices/fibers) on the device.
+//
+// "To calculate the n-mode slices, we first sort the input
+// tensor file by mode n ... After sorting on mode n, we can read the sorted file
+// one slice at a time".  Here: one LSD radix sort of packed (root, mids, leaf)
+// keys per ordering (CUB, one-time preprocessing inside tucker_init), then
+// run-length boundaries give slice / node / fiber pointers.
+#include <cub/cub.cuh>
+
+#include "internal.cuh"
+
+namespace tk {
+
+thread_local int64_t* g_launch_counter = nullptr;
+
+namespace {
+
+__global__ void k_validate(int order, const int64_t* __restrict__ dims_unused, int64_t nnz,
+                           const int32_t* __restrict__ i0, const int32_t* __restrict__ i1,
+                           const int32_t* __restrict__ i2, const int32_t* __restrict__ i3,
+                           int64_t d0, int64_t d1, int64_t d2, int64_t d3,
+                           const float* __restrict__ v, int* flags, int32_t* keep) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < nnz;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    bool bad_idx = (i0[e] < 0 || i0[e] >= d0) || (i1[e] < 0 || i1[e] >= d1) ||
+                   (order > 2 && (i2[e] < 0 || i2[e] >= d2)) ||
+                   (order > 3 && (i3[e] < 0 || i3[e] >= d3));
+    float x = v[e];
+    bool bad_val = !isfinite(x);
+    if (bad_idx) atomicOr(flags, 1);
+    if (bad_val) atomicOr(flags, 2);
+    keep[e] = (x != 0.0f) ? 1 : 0;  // explicit zeros are dropped
+  }
+}
+
+__global__ void k_compact_i32(int64_t n, const int32_t* __restrict__ keep,
+                              const int32_t* __restrict__ pos, const int32_t* __restrict__ in,
+                              int32_t* __restrict__ out) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
+       e += (int64_t)gridDim.x * blockDim.x)
+    if (keep[e]) out[pos[e]] = in[e];
+}
+__global__ void k_compact_f32(int64_t n, const int32_t* __restrict__ keep,
+                              const int32_t* __restrict__ pos, const float* __restrict__ in,
+                              float* __restrict__ out) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
+       e += (int64_t)gridDim.x * blockDim.x)
+    if (keep[e]) out[pos[e]] = in[e];
+}
+
+// ||X||^2: per-block fp64 partials in a fixed grid, then one block sums them in order.
+constexpr int kNormBlocks = 592;
+__global__ void k_sumsq_partial(const float* __restrict__ v, int64_t n, double* part) {
+  double s = 0.0;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    double x = v[e];
+    s += x * x;
+  }
+  typedef cub::BlockReduce<double, 256> BR;
+  __shared__ typename BR::TempStorage tmp;
+  double t = BR(tmp).Sum(s);
+  if (threadIdx.x == 0) part[blockIdx.x] = t;
+}
+__global__ void k_sum_final(const double* part, int n, double* out) {
+  double s = 0.0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) s += part[i];
+  typedef cub::BlockReduce<double, 256> BR;
+  __shared__ typename BR::TempStorage tmp;
+  double t = BR(tmp).Sum(s);
+  if (threadIdx.x == 0) *out = t;
+}
+
+__global__ void k_pack_keys(int64_t nnz, const int32_t* __restrict__ r, const int32_t* __restrict__ m0,
+                            const int32_t* __restrict__ m1, const int32_t* __restrict__ lf,
+                            int64_t I_m0, int64_t I_m1, int64_t I_leaf, uint64_t* __restrict__ key) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < nnz;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    uint64_t k = (uint64_t)r[e];
+    k = k * (uint64_t)I_m0 + (uint64_t)m0[e];
+    if (m1) k = k * (uint64_t)I_m1 + (uint64_t)m1[e];
+    k = k * (uint64_t)I_leaf + (uint64_t)lf[e];
+    key[e] = k;
+  }
+}
+
+// fiber flags: 1 where (root, mids) changes; duplicate detection on full keys.
+__global__ void k_fiber_flags(int64_t nnz, const uint64_t* __restrict__ key, int64_t I_leaf,
+                              int32_t* __restrict__ flag, int32_t* __restrict__ leaf_id, int* dup) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < nnz;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    uint64_t k = key[e];
+    leaf_id[e] = (int32_t)(k % (uint64_t)I_leaf);
+    uint64_t fk = k / (uint64_t)I_leaf;
+    int f = 1;
+    if (e > 0) {
+      uint64_t kp = key[e - 1];
+      if (kp == k) atomicOr(dup, 1);
+      f = (kp / (uint64_t)I_leaf) != fk;
+    }
+    flag[e] = f;
+  }
+}
+
+__global__ void k_fiber_scatter(int64_t nnz, const uint64_t* __restrict__ key, int64_t I_leaf,
+                                int64_t I_m0, int64_t I_m1, bool has_m1,
+                                const int32_t* __restrict__ flag, const int32_t* __restrict__ pos,
+                                int32_t* __restrict__ fib_ptr, int32_t* __restrict__ fib_root,
+                                int32_t* __restrict__ fib_m0, int32_t* __restrict__ fib_m1) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < nnz;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    if (!flag[e]) continue;
+    int32_t f = pos[e];
+    uint64_t fk = key[e] / (uint64_t)I_leaf;
+    fib_ptr[f] = (int32_t)e;
+    if (has_m1) {
+      fib_m1[f] = (int32_t)(fk % (uint64_t)I_m1);
+      fk /= (uint64_t)I_m1;
+    }
+    fib_m0[f] = (int32_t)(fk % (uint64_t)I_m0);
+    fib_root[f] = (int32_t)(fk / (uint64_t)I_m0);
+  }
+}
+
+__global__ void k_node_flags(int64_t nfib, const int32_t* __restrict__ root,
+                             const int32_t* __restrict__ m0, int32_t* __restrict__ flag) {
+  for (int64_t f = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; f < nfib;
+       f += (int64_t)gridDim.x * blockDim.x)
+    flag[f] = (f == 0) || root[f] != root[f - 1] || m0[f] != m0[f - 1];
+}
+__global__ void k_node_scatter(int64_t nfib, const int32_t* __restrict__ flag,
+                               const int32_t* __restrict__ pos, const int32_t* __restrict__ root,
+                               const int32_t* __restrict__ m0, int32_t* __restrict__ node_ptr,
+                               int32_t* __restrict__ node_root, int32_t* __restrict__ node_m0) {
+  for (int64_t f = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; f < nfib;
+       f += (int64_t)gridDim.x * blockDim.x) {
+    if (!flag[f]) continue;
+    int32_t nd = pos[f];
+    node_ptr[nd] = (int32_t)f;
+    node_root[nd] = root[f];
+    node_m0[nd] = m0[f];
+  }
+}
+
+// slice_ptr[r] = first child whose root >= r (children sorted by root), r in [0, I_root]
+__global__ void k_slice_ptr(int64_t I_root, const int32_t* __restrict__ child_root, int64_t nchild,
+                            int32_t* __restrict__ slice_ptr) {
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r <= I_root;
+       r += (int64_t)gridDim.x * blockDim.x) {
+    int64_t lo = 0, hi = nchild;
+    while (lo < hi) {
+      int64_t mid = (lo + hi) >> 1;
+      if (child_root[mid] < r) lo = mid + 1; else hi = mid;
+    }
+    slice_ptr[r] = (int32_t)lo;
+  }
+}
+
+__global__ void k_set_last(int32_t* p, int64_t i, int32_t v) { p[i] = v; }
+
+inline int grid_for(int64_t n) {
+  int64_t g = ceil_div(n, 256);
+  if (g > 148 * 16) g = 148 * 16;
+  if (g < 1) g = 1;
+  return (int)g;
+}
+
+int bits_for(uint64_t total) {
+  int b = 0;
+  while (b < 64 && (total >> b) > 0) ++b;
+  return b;
+}
+
+// exclusive scan of int32 flags into pos; returns total (sum of flags)
+int64_t scan_flags(const int32_t* flag, int32_t* pos, int64_t n, DBuf<uint8_t>& tmp,
+                   cudaStream_t st) {
+  size_t bytes = 0;
+  TK_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, bytes, flag, pos, (int)n, st));
+  tmp.ensure(bytes);
+  TK_CUDA(cub::DeviceScan::ExclusiveSum(tmp.p, bytes, flag, pos, (int)n, st));
+  int32_t last_pos = 0, last_flag = 0;
+  TK_CUDA(cudaMemcpyAsync(&last_pos, pos + n - 1, 4, cudaMemcpyDeviceToHost, st));
+  TK_CUDA(cudaMemcpyAsync(&last_flag, flag + n - 1, 4, cudaMemcpyDeviceToHost, st));
+  TK_CUDA(cudaStreamSynchronize(st));
+  return (int64_t)last_pos + last_flag;
+}
+
+}  // namespace
+
+void coo_validate_compact(Coo& coo, cudaStream_t st) {
+  const int64_t n = coo.nnz;
+  DBuf<int> flags(1);
+  DBuf<int32_t> keep(n), pos(n);
+  TK_CUDA(cudaMemsetAsync(flags.p, 0, sizeof(int), st));
+  const int32_t* ix[4] = {coo.idx[0].p, coo.idx[1].p, coo.order > 2 ? coo.idx[2].p : coo.idx[0].p,
+                          coo.order > 3 ? coo.idx[3].p : coo.idx[0].p};
+  TK_LAUNCH(k_validate, grid_for(n), 256, 0, st, coo.order, (const int64_t*)nullptr, n, ix[0], ix[1],
+            ix[2], ix[3], coo.dims[0], coo.dims[1], coo.order > 2 ? coo.dims[2] : 1,
+            coo.order > 3 ? coo.dims[3] : 1, coo.val.p, flags.p, keep.p);
+  int h_flags = 0;
+  TK_CUDA(cudaMemcpyAsync(&h_flags, flags.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+  TK_CUDA(cudaStreamSynchronize(st));
+  if (h_flags & 1) fail(TUCKER_E_INDEX, "tucker_init: an index is outside [0, I_n)");
+  if (h_flags & 2) fail(TUCKER_E_VALUE, "tucker_init: non-finite value");
+  DBuf<uint8_t> tmp;
+  int64_t kept = scan_flags(keep.p, pos.p, n, tmp, st);
+  if (kept == n) return;
+  if (kept == 0) fail(TUCKER_E_VALUE, "tucker_init: all values are zero (||X|| = 0)");
+  for (int m = 0; m < coo.order; ++m) {
+    DBuf<int32_t> out(kept);
+    TK_LAUNCH(k_compact_i32, grid_for(n), 256, 0, st, n, keep.p, pos.p, coo.idx[m].p, out.p);
+    coo.idx[m] = std::move(out);
+  }
+  DBuf<float> vout(kept);
+  TK_LAUNCH(k_compact_f32, grid_for(n), 256, 0, st, n, keep.p, pos.p, coo.val.p, vout.p);
+  coo.val = std::move(vout);
+  coo.nnz = kept;
+  TK_CUDA(cudaStreamSynchronize(st));
+}
+
+double coo_norm2(const Coo& coo, cudaStream_t st) {
+  DBuf<double> part(kNormBlocks), out(1);
+  TK_LAUNCH(k_sumsq_partial, kNormBlocks, 256, 0, st, coo.val.p, coo.nnz, part.p);
+  TK_LAUNCH(k_sum_final, 1, 256, 0, st, part.p, kNormBlocks, out.p);
+  double h = 0;
+  TK_CUDA(cudaMemcpyAsync(&h, out.p, sizeof(double), cudaMemcpyDeviceToHost, st));
+  TK_CUDA(cudaStreamSynchronize(st));
+  return h;
+}
+
+void csf_build(const Coo& coo, Csf& c, int root, int mid0, int mid1, int leaf, cudaStream_t st) {
+  const int64_t nnz = coo.nnz;
+  c.order = coo.order;
+  c.root = root;
+  c.mid0 = mid0;
+  c.mid1 = mid1;
+  c.leaf = leaf;
+  c.I_root = coo.dims[root];
+  c.I_mid0 = coo.dims[mid0];
+  c.I_mid1 = mid1 >= 0 ? coo.dims[mid1] : 1;
+  c.I_leaf = coo.dims[leaf];
+  c.nnz = nnz;
+  const bool has_m1 = mid1 >= 0;
+
+  DBuf<uint64_t> keys(nnz), keys_sorted(nnz);
+  TK_LAUNCH(k_pack_keys, grid_for(nnz), 256, 0, st, nnz, coo.idx[root].p, coo.idx[mid0].p,
+            has_m1 ? coo.idx[mid1].p : nullptr, coo.idx[leaf].p, c.I_mid0, c.I_mid1, c.I_leaf,
+            keys.p);
+  const uint64_t total = (uint64_t)c.I_root * (uint64_t)c.I_mid0 * (uint64_t)c.I_mid1 *
+                         (uint64_t)c.I_leaf;
+  const int end_bit = bits_for(total - 1 > 0 ? total - 1 : 1);
+  c.val.alloc(nnz);
+  DBuf<uint8_t> tmp;
+  size_t bytes = 0;
+  TK_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, bytes, keys.p, keys_sorted.p, coo.val.p, c.val.p,
+                                          (int)nnz, 0, end_bit, st));
+  tmp.ensure(bytes);
+  TK_CUDA(cub::DeviceRadixSort::SortPairs(tmp.p, bytes, keys.p, keys_sorted.p, coo.val.p, c.val.p,
+                                          (int)nnz, 0, end_bit, st));
+  if (g_launch_counter) ++(*g_launch_counter);
+  keys.release();
+
+  DBuf<int32_t> flag(nnz), pos(nnz);
+  DBuf<int> dup(1);
+  TK_CUDA(cudaMemsetAsync(dup.p, 0, sizeof(int), st));
+  c.leaf_id.alloc(nnz);
+  TK_LAUNCH(k_fiber_flags, grid_for(nnz), 256, 0, st, nnz, keys_sorted.p, c.I_leaf, flag.p,
+            c.leaf_id.p, dup.p);
+  int h_dup = 0;
+  TK_CUDA(cudaMemcpyAsync(&h_dup, dup.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+  const int64_t nfib = scan_flags(flag.p, pos.p, nnz, tmp, st);  // synchronises
+  if (h_dup) fail(TUCKER_E_DUP, "tucker_init: duplicate coordinate");
+  c.nfib = nfib;
+  c.fib_ptr.alloc(nfib + 1);
+  c.fib_root.alloc(nfib);
+  c.fib_mid0.alloc(nfib);
+  if (has_m1) c.fib_mid1.alloc(nfib);
+  TK_LAUNCH(k_fiber_scatter, grid_for(nnz), 256, 0, st, nnz, keys_sorted.p, c.I_leaf, c.I_mid0,
+            c.I_mid1, has_m1, flag.p, pos.p, c.fib_ptr.p, c.fib_root.p, c.fib_mid0.p,
+            has_m1 ? c.fib_mid1.p : nullptr);
+  TK_LAUNCH(k_set_last, 1, 1, 0, st, c.fib_ptr.p, nfib, (int32_t)nnz);
+  keys_sorted.release();
+
+  c.slice_ptr.alloc(c.I_root + 1);
+  if (has_m1) {
+    DBuf<int32_t> nflag(nfib), npos(nfib), node_root;
+    TK_LAUNCH(k_node_flags, grid_for(nfib), 256, 0, st, nfib, c.fib_root.p, c.fib_mid0.p, nflag.p);
+    const int64_t nnode = scan_flags(nflag.p, npos.p, nfib, tmp, st);
+    c.nnode = nnode;
+    c.node_ptr.alloc(nnode + 1);
+    c.node_mid0.alloc(nnode);
+    node_root.alloc(nnode);
+    TK_LAUNCH(k_node_scatter, grid_for(nfib), 256, 0, st, nfib, nflag.p, npos.p, c.fib_root.p,
+              c.fib_mid0.p, c.node_ptr.p, node_root.p, c.node_mid0.p);
+    TK_LAUNCH(k_set_last, 1, 1, 0, st, c.node_ptr.p, nnode, (int32_t)nfib);
+    TK_LAUNCH(k_slice_ptr, grid_for(c.I_root + 1), 256, 0, st, c.I_root, node_root.p, nnode,
+              c.slice_ptr.p);
+    TK_CUDA(cudaStreamSynchronize(st));
+  } else {
+    TK_LAUNCH(k_slice_ptr, grid_for(c.I_root + 1), 256, 0, st, c.I_root, c.fib_root.p, nfib,
+              c.slice_ptr.p);
+    TK_CUDA(cudaStreamSynchronize(st));
+  }
+}
+
+}  // namespace tk

@@ -1,0 +1,122 @@
+// internal.cuh -- data structures and kernel entry points shared by the
+// libtucker translation units.  See DESIGN.md for the layouts.
+#pragma once
+
+#include "common.cuh"
+
+namespace tk {
+
+constexpr int kMaxOrder = 4;
+constexpr int kMaxJ = 128;       // per-mode core size limit of this build
+constexpr int kMaxBlock = 116;   // eigensolver block size k limit (Jacobi in shared memory)
+
+// ---------------------------------------------------------------------------
+// CSF: nonzeros sorted by (root, mid0[, mid1], leaf).
+// sorts the COO file by mode n and writes one slice per index;
+// here the sorted arrays stay in HBM and slice/fiber pointers replace files.
+//   slice_ptr[r]..slice_ptr[r+1]   children of root index r: fibers (order 3)
+//                                  or nodes (order 4)
+//   node_ptr / node_mid0           order 4: runs of equal (root, mid0) -> fibers
+//   fib_ptr[f]..fib_ptr[f+1]       nonzeros of fiber f (fixed root and mids)
+//   fib_root, fib_mid0, fib_mid1   coordinates of fiber f
+//   leaf_id, val                   per nonzero
+// ---------------------------------------------------------------------------
+struct Csf {
+  int order = 0;
+  int root = -1, mid0 = -1, mid1 = -1, leaf = -1;  // mode ids (0-based)
+  int64_t I_root = 0, I_mid0 = 0, I_mid1 = 1, I_leaf = 0;
+  int64_t nnz = 0, nfib = 0, nnode = 0;
+  DBuf<int32_t> slice_ptr, node_ptr, node_mid0, fib_ptr, fib_root, fib_mid0, fib_mid1, leaf_id;
+  DBuf<float> val;
+};
+
+struct Coo {  // validated, zero-free COO on the device
+  int order = 0;
+  int64_t dims[kMaxOrder] = {0, 0, 0, 0};
+  int64_t nnz = 0;
+  DBuf<int32_t> idx[kMaxOrder];
+  DBuf<float> val;
+};
+
+// csf.cu
+void coo_validate_compact(Coo& coo, cudaStream_t st);          // E_INDEX / E_VALUE, drops zeros
+double coo_norm2(const Coo& coo, cudaStream_t st);              // ||X||_F^2 (fp64, fixed order)
+void csf_build(const Coo& coo, Csf& out, int root, int mid0, int mid1, int leaf, cudaStream_t st);
+
+// ---------------------------------------------------------------------------
+// Split-fp32 matrix: a = hi + lo exactly, hi = tf32-rounded a (DESIGN.md
+// "3xTF32 operands").  Row-major rows x ld, zero padded.
+// ---------------------------------------------------------------------------
+struct Split {
+  float* hi = nullptr;
+  float* lo = nullptr;
+  int64_t rows = 0, cols = 0, ld = 0;  // logical rows/cols; ld = padded row length
+};
+
+// spttmc.cu
+// HOOI: Y_(n) (Kolda order) written as split fp32; transposed => out is Y_(n)^T.
+void spttmc_hooi(const Csf& c, const float* const* U, const int64_t* J, Split out, bool transposed,
+                 cudaStream_t st);
+// MP: W columns [col_off, col_off + prod(I_mids)*J_leaf) of the rows of out
+// (out pre-zeroed): W[i_root, col_off + mk*J_leaf + j] = sum_{x in fiber} x U_leaf[i_leaf, j].
+void spmm_mp(const Csf& c, const float* U_leaf, int64_t J_leaf, Split out, int64_t col_off,
+             cudaStream_t st);
+
+// gram.cu -- S (d x d fp64, row-major, ld = lds) = A A^T, A = d x K split fp32.
+struct GramWs {
+  DBuf<double> partial;
+  DBuf<uint8_t> scratch;
+};
+void gram_syrk(const Split& A, double* S, int64_t lds, GramWs& ws, cudaStream_t st);
+// reference SIMT fp64 path (debug/validation of the tensor-core kernel)
+void gram_syrk_simt(const Split& A, double* S, int64_t lds, cudaStream_t st);
+int gram_mode();  // 0 = tcgen05 (default), 1 = SIMT (env TUCKER_GRAM=simt)
+
+// dense.cu -- small fp64 dense kernels for the eigensolver and the core.
+enum class Elt { F64, F32, SPLIT };
+struct MatRef {
+  Elt t = Elt::F64;
+  const void* p = nullptr;     // F64: double*, F32: float*
+  const float* lo = nullptr;   // SPLIT: p = hi, lo = lo
+  int64_t ld = 0;
+  bool trans = false;          // op(A) = A^T
+};
+struct DenseWs {
+  DBuf<double> splitk;
+};
+// C (M x N fp64, ldc) = alpha op(A) op(B) + beta C + gamma D (D nullable, ldd)
+void dgemm(int64_t M, int64_t N, int64_t K, double alpha, MatRef A, MatRef B, double beta,
+           double* C, int64_t ldc, double gamma, const double* D, int64_t ldd, DenseWs& ws,
+           cudaStream_t st);
+double dnorm2_f32(const float* x, int64_t n, DenseWs& ws, cudaStream_t st);  // sum x^2, fp64
+
+// eig.cu
+struct EigSlot {              // warm-start state per (algorithm, mode)
+  DBuf<double> basis;         // d x k Ritz vectors of the last solve (row-major)
+  int64_t d = 0;
+  int k = 0;
+  bool valid = false;
+};
+struct EigWs {
+  DBuf<double> Q, SQ, X, Y, T, H, V, R;
+  DBuf<double> theta, resid;
+  DenseWs dense;
+  std::vector<double> h_theta, h_resid;
+  int64_t stat_outer = 0, stat_matvec = 0, stat_sweeps = 0;
+};
+struct EigOpts {
+  int oversample = 0;
+  int max_outer = 40;
+  double tol = 1e-11;
+};
+// Leading J eigenvectors of symmetric PSD S (d x d, lds): out_V (d x ldv fp64 row-major)
+// columns 0..J-1 descending, theta_out[0..J) host. Returns true if converged.
+bool eig_leading(const double* S, int64_t lds, int64_t d, int J, EigSlot& slot, EigWs& ws,
+                 const EigOpts& o, double* out_V, int64_t ldv, double* theta_out,
+                 cudaStream_t st);
+// Orthonormalise the columns of V (d x J fp64) in place (CholQR2).
+void cholqr2(double* V, int64_t ldv, int64_t d, int J, EigWs& ws, cudaStream_t st);
+// Order-preserving sign canonicalisation + fp32 conversion: U[i*J+j] = s_j V[i*ldv+j].
+void canon_to_f32(const double* V, int64_t ldv, int64_t d, int J, float* U, cudaStream_t st);
+
+}  // namespace tk

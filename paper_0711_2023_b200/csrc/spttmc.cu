@@ -1,0 +1,366 @@
+// spttmc.cu -- sparse tensor-times-matrix kernels.
+//
+// HOOI (Fig. 4): Y_(n) = (X x_{m != n} U_m^T)_(n).  Per slice i of
+// mode n (PAPER Appendix: row i of Y_(1) is B' * X1_slice * C):
+//   order 3:  Y_i[a, b] = sum_{fibers f of slice i} U_mid[mid(f), a] * t_f[b],
+//             t_f[b]    = sum_{x in f} x * U_leaf[leaf(x), b]           (Eq. 1)
+//   order 4:  Y_i[a0, a1, b] = sum_{nodes v of i} U_mid0[mid0(v), a0] * Z_v[a1, b],
+//             Z_v[a1, b] = sum_{fibers f of v} U_mid1[mid1(f), a1] * t_f[b]
+// One CTA per slice; the fiber (leaf) stage gathers U_leaf rows with
+// coalesced warp loads, the Kronecker stage is a register-tiled outer-product
+// accumulation; no global atomics.  The output row is written once, split
+// into (tf32 hi, tf32 lo) pairs for the 3xTF32 Gram.
+//
+// MP (Fig. 7/8, Appendix): W = (X x_m U_m^T)_(n), whose column
+// block for the slice s fixing the modes not in {n, m} is X_s U_m.
+#include "internal.cuh"
+
+namespace tk {
+
+__device__ __forceinline__ float tf32_rna(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return __uint_as_float(r);
+}
+__device__ __forceinline__ void split_store(float* hi, float* lo, int64_t off, float y) {
+  float h = tf32_rna(y);
+  hi[off] = h;
+  lo[off] = tf32_rna(y - h);
+}
+
+namespace {
+
+constexpr int kFC = 32;  // fibers per chunk
+
+// Leaf stage for the fibers [fc, fc+nf) of one chunk: T[fl][b] = t_f[b],
+// Mrow[fl][a] = U_mid[mid(f), a]; rows padded with zeros to JLP / JMP.
+template <int JLP, int JMP>
+__device__ __forceinline__ void leaf_stage(int fc, int nf, const int32_t* __restrict__ fib_ptr,
+                                           const int32_t* __restrict__ fib_mid,
+                                           const int32_t* __restrict__ leaf_id,
+                                           const float* __restrict__ val,
+                                           const float* __restrict__ Umid, int Jm,
+                                           const float* __restrict__ Uleaf, int Jl, float* T,
+                                           float* M) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nwarps = blockDim.x >> 5;
+  constexpr int QL = JLP / 32 > 0 ? (JLP + 31) / 32 : 1;
+  for (int fl = warp; fl < nf; fl += nwarps) {
+    const int f = fc + fl;
+    const int e0 = __ldg(fib_ptr + f), e1 = __ldg(fib_ptr + f + 1);
+    float t[QL];
+#pragma unroll
+    for (int q = 0; q < QL; ++q) t[q] = 0.f;
+    int e = e0;
+    for (; e + 1 < e1; e += 2) {  // two nonzeros in flight
+      const int l0 = __ldg(leaf_id + e), l1 = __ldg(leaf_id + e + 1);
+      const float x0 = __ldg(val + e), x1 = __ldg(val + e + 1);
+      const float* r0 = Uleaf + (int64_t)l0 * Jl;
+      const float* r1 = Uleaf + (int64_t)l1 * Jl;
+#pragma unroll
+      for (int q = 0; q < QL; ++q) {
+        const int j = lane + 32 * q;
+        if (j < Jl) t[q] += x0 * __ldg(r0 + j) + x1 * __ldg(r1 + j);
+      }
+    }
+    if (e < e1) {
+      const int l0 = __ldg(leaf_id + e);
+      const float x0 = __ldg(val + e);
+      const float* r0 = Uleaf + (int64_t)l0 * Jl;
+#pragma unroll
+      for (int q = 0; q < QL; ++q) {
+        const int j = lane + 32 * q;
+        if (j < Jl) t[q] += x0 * __ldg(r0 + j);
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < QL; ++q) {
+      const int j = lane + 32 * q;
+      if (j < JLP) T[fl * JLP + j] = (j < Jl) ? t[q] : 0.f;
+    }
+    const float* mr = Umid + (int64_t)__ldg(fib_mid + f) * Jm;
+    for (int j = lane; j < JMP; j += 32) M[fl * JMP + j] = (j < Jm) ? __ldg(mr + j) : 0.f;
+  }
+}
+
+// Kronecker stage over one chunk: acc[r][c] += M[fl][ty + 16 r] * T[fl][tx + 16 c]
+template <int RA, int RB>
+__device__ __forceinline__ void kron_stage(int nf, const float* T, const float* M,
+                                           float (&acc)[RA][RB]) {
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  constexpr int JLP = 16 * RB, JMP = 16 * RA;
+#pragma unroll 4
+  for (int fl = 0; fl < nf; ++fl) {
+    float a[RA], b[RB];
+#pragma unroll
+    for (int r = 0; r < RA; ++r) a[r] = M[fl * JMP + ty + 16 * r];
+#pragma unroll
+    for (int c = 0; c < RB; ++c) b[c] = T[fl * JLP + tx + 16 * c];
+#pragma unroll
+    for (int r = 0; r < RA; ++r)
+#pragma unroll
+      for (int c = 0; c < RB; ++c) acc[r][c] += a[r] * b[c];
+  }
+}
+
+struct Ttmc3Args {
+  const int32_t *slice_ptr, *fib_ptr, *fib_mid, *leaf_id;
+  const float* val;
+  const float *Umid, *Uleaf;
+  int Jm, Jl;
+  float *Yhi, *Ylo;
+  int64_t ldY;
+  int transposed;
+  int64_t sa, sb;  // Kolda strides of (mid index a, leaf index b) in the output column
+};
+
+template <int RA, int RB>
+__global__ void __launch_bounds__(256) k_spttmc3(Ttmc3Args p) {
+  constexpr int JLP = 16 * RB, JMP = 16 * RA;
+  __shared__ float T[kFC * JLP];
+  __shared__ float M[kFC * JMP];
+  const int i = blockIdx.x;
+  const int f0 = p.slice_ptr[i], f1 = p.slice_ptr[i + 1];
+  float acc[RA][RB];
+#pragma unroll
+  for (int r = 0; r < RA; ++r)
+#pragma unroll
+    for (int c = 0; c < RB; ++c) acc[r][c] = 0.f;
+  for (int fc = f0; fc < f1; fc += kFC) {
+    const int nf = min(kFC, f1 - fc);
+    leaf_stage<JLP, JMP>(fc, nf, p.fib_ptr, p.fib_mid, p.leaf_id, p.val, p.Umid, p.Jm, p.Uleaf,
+                         p.Jl, T, M);
+    __syncthreads();
+    kron_stage<RA, RB>(nf, T, M, acc);
+    __syncthreads();
+  }
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+#pragma unroll
+  for (int r = 0; r < RA; ++r)
+#pragma unroll
+    for (int c = 0; c < RB; ++c) {
+      const int a = ty + 16 * r, b = tx + 16 * c;
+      if (a < p.Jm && b < p.Jl) {
+        const int64_t col = a * p.sa + b * p.sb;
+        const int64_t off = p.transposed ? col * p.ldY + i : (int64_t)i * p.ldY + col;
+        split_store(p.Yhi, p.Ylo, off, acc[r][c]);
+      }
+    }
+}
+
+struct Ttmc4Args {
+  const int32_t *slice_ptr, *node_ptr, *node_mid0, *fib_ptr, *fib_mid1, *leaf_id;
+  const float* val;
+  const float *U0, *U1, *Uleaf;
+  int J0, J1, Jl;
+  float *Yhi, *Ylo;
+  int64_t ldY;
+  int transposed;
+  int64_t s0, s1, sb;  // Kolda strides of (mid0, mid1, leaf) indices
+};
+
+template <int RA, int RB, int RQ>
+__global__ void __launch_bounds__(256) k_spttmc4(Ttmc4Args p) {
+  constexpr int JLP = 16 * RB, JMP = 16 * RA;
+  __shared__ float T[kFC * JLP];
+  __shared__ float M[kFC * JMP];
+  __shared__ float Zs[JMP * JLP];
+  __shared__ float u0[128];
+  const int i = blockIdx.x;
+  const int n0 = p.slice_ptr[i], n1 = p.slice_ptr[i + 1];
+  const int P1 = p.J1 * p.Jl;
+  const int P = p.J0 * P1;
+  float y[RQ];
+#pragma unroll
+  for (int q = 0; q < RQ; ++q) y[q] = 0.f;
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  for (int nd = n0; nd < n1; ++nd) {
+    float acc[RA][RB];
+#pragma unroll
+    for (int r = 0; r < RA; ++r)
+#pragma unroll
+      for (int c = 0; c < RB; ++c) acc[r][c] = 0.f;
+    const int f0 = p.node_ptr[nd], f1 = p.node_ptr[nd + 1];
+    for (int fc = f0; fc < f1; fc += kFC) {
+      const int nf = min(kFC, f1 - fc);
+      leaf_stage<JLP, JMP>(fc, nf, p.fib_ptr, p.fib_mid1, p.leaf_id, p.val, p.U1, p.J1, p.Uleaf,
+                           p.Jl, T, M);
+      __syncthreads();
+      kron_stage<RA, RB>(nf, T, M, acc);
+      __syncthreads();
+    }
+#pragma unroll
+    for (int r = 0; r < RA; ++r)
+#pragma unroll
+      for (int c = 0; c < RB; ++c) {
+        const int a = ty + 16 * r, b = tx + 16 * c;
+        if (a < p.J1 && b < p.Jl) Zs[a * p.Jl + b] = acc[r][c];
+      }
+    const float* ur = p.U0 + (int64_t)p.node_mid0[nd] * p.J0;
+    for (int j = threadIdx.x; j < p.J0; j += blockDim.x) u0[j] = __ldg(ur + j);
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < RQ; ++q) {
+      const int c = threadIdx.x + 256 * q;
+      if (c < P) y[q] += u0[c / P1] * Zs[c % P1];
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int q = 0; q < RQ; ++q) {
+    const int c = threadIdx.x + 256 * q;
+    if (c < P) {
+      const int a0 = c / P1, rest = c % P1;
+      const int a1 = rest / p.Jl, b = rest % p.Jl;
+      const int64_t col = a0 * p.s0 + a1 * p.s1 + b * p.sb;
+      const int64_t off = p.transposed ? col * p.ldY + i : (int64_t)i * p.ldY + col;
+      split_store(p.Yhi, p.Ylo, off, y[q]);
+    }
+  }
+}
+
+struct SpmmArgs {
+  const int32_t *fib_ptr, *fib_root, *fib_mid0, *fib_mid1, *leaf_id;
+  const float* val;
+  const float* U;
+  int J;
+  int64_t nfib, I_mid1;
+  float *Whi, *Wlo;
+  int64_t ldW, col_off;
+};
+
+template <int QL>
+__global__ void __launch_bounds__(256) k_spmm_mp(SpmmArgs p) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t f = warp; f < p.nfib; f += nwarps) {
+    const int e0 = __ldg(p.fib_ptr + f), e1 = __ldg(p.fib_ptr + f + 1);
+    float t[QL];
+#pragma unroll
+    for (int q = 0; q < QL; ++q) t[q] = 0.f;
+    for (int e = e0; e < e1; ++e) {
+      const float x = __ldg(p.val + e);
+      const float* r = p.U + (int64_t)__ldg(p.leaf_id + e) * p.J;
+#pragma unroll
+      for (int q = 0; q < QL; ++q) {
+        const int j = lane + 32 * q;
+        if (j < p.J) t[q] += x * __ldg(r + j);
+      }
+    }
+    int64_t mk = __ldg(p.fib_mid0 + f);
+    if (p.fib_mid1) mk = mk * p.I_mid1 + __ldg(p.fib_mid1 + f);
+    const int64_t base = (int64_t)__ldg(p.fib_root + f) * p.ldW + p.col_off + mk * p.J;
+#pragma unroll
+    for (int q = 0; q < QL; ++q) {
+      const int j = lane + 32 * q;
+      if (j < p.J) split_store(p.Whi, p.Wlo, base + j, t[q]);
+    }
+  }
+}
+
+inline int rtile(int J) { return (J + 15) / 16; }  // 1..8
+
+}  // namespace
+
+// Kolda stride of mode `m` among the modes `others` (ascending lower-fastest).
+static int64_t kolda_stride(int m, const int* others, int nothers, const int64_t* J) {
+  int64_t s = 1;
+  for (int k = 0; k < nothers; ++k)
+    if (others[k] < m) s *= J[others[k]];
+  return s;
+}
+
+void spttmc_hooi(const Csf& c, const float* const* U, const int64_t* J, Split out, bool transposed,
+                 cudaStream_t st) {
+  int others[3], no = 0;
+  for (int m = 0; m < c.order; ++m)
+    if (m != c.root) others[no++] = m;
+  const int64_t ldY = out.ld;
+  if (c.order == 3) {
+    Ttmc3Args a;
+    a.slice_ptr = c.slice_ptr.p;
+    a.fib_ptr = c.fib_ptr.p;
+    a.fib_mid = c.fib_mid0.p;
+    a.leaf_id = c.leaf_id.p;
+    a.val = c.val.p;
+    a.Umid = U[c.mid0];
+    a.Uleaf = U[c.leaf];
+    a.Jm = (int)J[c.mid0];
+    a.Jl = (int)J[c.leaf];
+    a.Yhi = out.hi;
+    a.Ylo = out.lo;
+    a.ldY = ldY;
+    a.transposed = transposed;
+    a.sa = kolda_stride(c.mid0, others, no, J);
+    a.sb = kolda_stride(c.leaf, others, no, J);
+    const int RA = rtile(a.Jm), RB = rtile(a.Jl);
+    const dim3 g((unsigned)c.I_root);
+#define TK_S3(ra, rb) \
+  if (RA <= ra && RB <= rb) { TK_LAUNCH((k_spttmc3<ra, rb>), g, 256, 0, st, a); return; }
+    TK_S3(1, 1) TK_S3(2, 1) TK_S3(1, 2) TK_S3(2, 2) TK_S3(4, 1) TK_S3(1, 4) TK_S3(4, 2)
+    TK_S3(2, 4) TK_S3(4, 4) TK_S3(8, 2) TK_S3(2, 8) TK_S3(8, 4) TK_S3(4, 8) TK_S3(8, 8)
+#undef TK_S3
+    fail(TUCKER_E_ARG, "spttmc: unsupported core size");
+  }
+  Ttmc4Args a;
+  a.slice_ptr = c.slice_ptr.p;
+  a.node_ptr = c.node_ptr.p;
+  a.node_mid0 = c.node_mid0.p;
+  a.fib_ptr = c.fib_ptr.p;
+  a.fib_mid1 = c.fib_mid1.p;
+  a.leaf_id = c.leaf_id.p;
+  a.val = c.val.p;
+  a.U0 = U[c.mid0];
+  a.U1 = U[c.mid1];
+  a.Uleaf = U[c.leaf];
+  a.J0 = (int)J[c.mid0];
+  a.J1 = (int)J[c.mid1];
+  a.Jl = (int)J[c.leaf];
+  a.Yhi = out.hi;
+  a.Ylo = out.lo;
+  a.ldY = ldY;
+  a.transposed = transposed;
+  a.s0 = kolda_stride(c.mid0, others, no, J);
+  a.s1 = kolda_stride(c.mid1, others, no, J);
+  a.sb = kolda_stride(c.leaf, others, no, J);
+  const int64_t P = (int64_t)a.J0 * a.J1 * a.Jl;
+  const int RA = rtile(a.J1), RB = rtile(a.Jl);
+  const int64_t RQ = ceil_div(P, 256);
+  const dim3 g((unsigned)c.I_root);
+#define TK_S4(ra, rb, rq)                                                    \
+  if (RA <= ra && RB <= rb && RQ <= rq) {                                    \
+    TK_LAUNCH((k_spttmc4<ra, rb, rq>), g, 256, 0, st, a);                    \
+    return;                                                                  \
+  }
+  TK_S4(1, 1, 4) TK_S4(2, 2, 4) TK_S4(1, 1, 16) TK_S4(2, 2, 16) TK_S4(2, 2, 32) TK_S4(2, 2, 64)
+  TK_S4(4, 4, 32) TK_S4(4, 4, 64)
+#undef TK_S4
+  fail(TUCKER_E_ARG, "spttmc: unsupported order-4 core size (prod J <= 16384, J <= 64)");
+}
+
+void spmm_mp(const Csf& c, const float* U_leaf, int64_t J_leaf, Split out, int64_t col_off,
+             cudaStream_t st) {
+  SpmmArgs a;
+  a.fib_ptr = c.fib_ptr.p;
+  a.fib_root = c.fib_root.p;
+  a.fib_mid0 = c.fib_mid0.p;
+  a.fib_mid1 = c.mid1 >= 0 ? c.fib_mid1.p : nullptr;
+  a.leaf_id = c.leaf_id.p;
+  a.val = c.val.p;
+  a.U = U_leaf;
+  a.J = (int)J_leaf;
+  a.nfib = c.nfib;
+  a.I_mid1 = c.I_mid1;
+  a.Whi = out.hi;
+  a.Wlo = out.lo;
+  a.ldW = out.ld;
+  a.col_off = col_off;
+  const int64_t blocks = std::min<int64_t>(ceil_div(c.nfib, 8), 148 * 32);
+  const int QL = (int)ceil_div(J_leaf, 32);
+  if (QL <= 1) TK_LAUNCH((k_spmm_mp<1>), (unsigned)blocks, 256, 0, st, a);
+  else if (QL <= 2) TK_LAUNCH((k_spmm_mp<2>), (unsigned)blocks, 256, 0, st, a);
+  else TK_LAUNCH((k_spmm_mp<4>), (unsigned)blocks, 256, 0, st, a);
+}
+
+}  // namespace tk

@@ -1,0 +1,636 @@
+// tucker.cu -- the C-ABI (include/tucker.h): handle, validation, and the
+// per-sweep orchestration of the kernels in csf.cu / spttmc.cu / gram*.cu /
+// eig.cu / dense.cu.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "internal.cuh"
+
+using namespace tk;
+
+struct tucker_handle {
+  int order = 0;
+  int64_t dims[kMaxOrder] = {1, 1, 1, 1};
+  int64_t J[kMaxOrder] = {1, 1, 1, 1};
+  tucker_opts opts{};
+  cudaStream_t st = nullptr;
+  bool own_stream = false;
+  Coo coo;
+  std::vector<std::unique_ptr<Csf>> csfs;
+  int hooi_csf[kMaxOrder] = {-1, -1, -1, -1};
+  int mp_csf[kMaxOrder][kMaxOrder];
+  DBuf<float> U[kMaxOrder];
+  double normX2 = 0;
+  // workspaces
+  DBuf<float> Yhi, Ylo, Whi, Wlo;
+  Split Y;  // last HOOI projection (mode Y_mode)
+  int Y_mode = -1;
+  bool Y_transposed = false;
+  DBuf<double> S, V, Ufull, G64, scal;
+  DBuf<float> G32, Ytmp;
+  bool G_valid = false;
+  EigSlot slots[2][kMaxOrder];
+  EigSlot scratch_slot;
+  EigWs eig;
+  GramWs gram;
+  int64_t launches = 0;
+  int64_t stat_outer0 = 0, stat_matvec0 = 0, stat_sweeps0 = 0;
+  std::string last_error;
+  bool eig_unconverged = false;
+};
+
+namespace {
+
+struct LaunchScope {  // route TK_LAUNCH counting to this handle
+  int64_t* prev;
+  explicit LaunchScope(tucker_handle* h) : prev(g_launch_counter) { g_launch_counter = &h->launches; }
+  ~LaunchScope() { g_launch_counter = prev; }
+};
+
+template <typename F>
+int guarded(tucker_handle* h, F&& f) {
+  try {
+    if (h) {
+      LaunchScope ls(h);
+      TK_CUDA(cudaSetDevice(h->opts.device));
+      return f();
+    }
+    return f();
+  } catch (const Error& e) {
+    if (h) h->last_error = e.msg;
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    if (h) h->last_error = "host allocation failed";
+    return TUCKER_E_OOM;
+  } catch (const std::exception& e) {
+    if (h) h->last_error = e.what();
+    return TUCKER_E_CUDA;
+  }
+}
+
+__global__ void k_combine(const float* __restrict__ hi, const float* __restrict__ lo, int64_t rows,
+                          int64_t cols, int64_t ld, float* __restrict__ out) {
+  const int64_t n = rows * cols;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = e / cols, c = e % cols;
+    out[e] = hi[r * ld + c] + lo[r * ld + c];
+  }
+}
+__global__ void k_scale_cols(double* V, int64_t d, int J, const double* __restrict__ s) {
+  const int64_t n = d * J;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
+       e += (int64_t)gridDim.x * blockDim.x)
+    V[e] *= s[e % J];
+}
+__global__ void k_d2f(const double* __restrict__ x, int64_t n, float* __restrict__ y) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
+       e += (int64_t)gridDim.x * blockDim.x)
+    y[e] = (float)x[e];
+}
+// ||G||^2 in fp64 (single CTA, fixed order) and Eq. 9 fit via the norm identity
+__global__ void k_core_fit(const double* __restrict__ G, int64_t n, double normX2, double* out) {
+  __shared__ double red[512];
+  double s = 0.0;
+  for (int64_t e = threadIdx.x; e < n; e += blockDim.x) s += G[e] * G[e];
+  red[threadIdx.x] = s;
+  __syncthreads();
+  for (int w = 256; w > 0; w >>= 1) {
+    if (threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    const double g2 = red[0];
+    out[0] = g2;
+    out[1] = 1.0 - sqrt(fmax(0.0, normX2 - g2)) / sqrt(normX2);
+  }
+}
+
+inline int gridn(int64_t n) {
+  int64_t g = ceil_div(n, 256);
+  if (g > 148 * 8) g = 148 * 8;
+  return (int)(g < 1 ? 1 : g);
+}
+
+int64_t prod_J_except(const tucker_handle* h, int n) {
+  int64_t P = 1;
+  for (int m = 0; m < h->order; ++m)
+    if (m != n) P *= h->J[m];
+  return P;
+}
+
+const float* const* uptrs(tucker_handle* h) {
+  static thread_local const float* p[kMaxOrder];
+  for (int m = 0; m < h->order; ++m) p[m] = h->U[m].p;
+  return p;
+}
+
+EigOpts eig_opts(const tucker_handle* h) {
+  EigOpts o;
+  o.oversample = h->opts.eig_oversample;
+  if (h->opts.eig_max_iter > 0) o.max_outer = h->opts.eig_max_iter;
+  else o.max_outer = 60;
+  if (h->opts.eig_tol > 0) o.tol = h->opts.eig_tol;
+  return o;
+}
+
+// Y_(n) (or its transpose) with the current factors into h->Y (split, zero padded)
+void project_hooi(tucker_handle* h, int n, bool transposed) {
+  const int64_t P = prod_J_except(h, n);
+  const int64_t rows = transposed ? P : h->dims[n];
+  const int64_t cols = transposed ? h->dims[n] : P;
+  const int64_t rows_pad = round_up(rows, 128), ld = round_up(cols, 32);
+  const size_t need = (size_t)(rows_pad * ld);
+  h->Yhi.ensure(need);
+  h->Ylo.ensure(need);
+  TK_CUDA(cudaMemsetAsync(h->Yhi.p, 0, need * sizeof(float), h->st));
+  TK_CUDA(cudaMemsetAsync(h->Ylo.p, 0, need * sizeof(float), h->st));
+  h->Y.hi = h->Yhi.p;
+  h->Y.lo = h->Ylo.p;
+  h->Y.rows = rows;
+  h->Y.cols = cols;
+  h->Y.ld = ld;
+  spttmc_hooi(*h->csfs[h->hooi_csf[n]], uptrs(h), h->J, h->Y, transposed, h->st);
+  h->Y_mode = n;
+  h->Y_transposed = transposed;
+}
+
+// W_n = [ (X x_m U_m^T)_(n) ]_{m != n} into h->Whi/Wlo; returns the split view
+Split build_mp_w(tucker_handle* h, int n) {
+  int64_t K = 0;
+  for (int m = 0; m < h->order; ++m) {
+    if (m == n) continue;
+    const Csf& c = *h->csfs[h->mp_csf[n][m]];
+    K += h->J[m] * c.I_mid0 * c.I_mid1;
+  }
+  const int64_t rows = h->dims[n];
+  const int64_t rows_pad = round_up(rows, 128), ld = round_up(K, 32);
+  const size_t need = (size_t)(rows_pad * ld);
+  h->Whi.ensure(need);
+  h->Wlo.ensure(need);
+  TK_CUDA(cudaMemsetAsync(h->Whi.p, 0, need * sizeof(float), h->st));
+  TK_CUDA(cudaMemsetAsync(h->Wlo.p, 0, need * sizeof(float), h->st));
+  Split W;
+  W.hi = h->Whi.p;
+  W.lo = h->Wlo.p;
+  W.rows = rows;
+  W.cols = K;
+  W.ld = ld;
+  int64_t off = 0;
+  for (int m = 0; m < h->order; ++m) {
+    if (m == n) continue;
+    const Csf& c = *h->csfs[h->mp_csf[n][m]];
+    spmm_mp(c, h->U[m].p, h->J[m], W, off, h->st);
+    off += h->J[m] * c.I_mid0 * c.I_mid1;
+  }
+  return W;
+}
+
+// Leading eigenvectors of S (d x d) -> fp64 V (d x J) in h->V; returns eigenvalues
+std::vector<double> solve_eig(tucker_handle* h, int64_t d, int J, EigSlot& slot) {
+  h->V.ensure((size_t)(d * J));
+  std::vector<double> theta(J);
+  const bool ok = eig_leading(h->S.p, d, d, J, slot, h->eig, eig_opts(h), h->V.p, J, theta.data(),
+                              h->st);
+  if (!ok) h->eig_unconverged = true;
+  return theta;
+}
+
+// U_n from the eigenvectors of the Gram of the split matrix A (= Y, Y^T or W)
+void update_factor(tucker_handle* h, int n, const Split& A, bool transposed, EigSlot& slot,
+                   float* ms_gram, float* ms_eig) {
+  const int64_t d = A.rows;
+  const int J = (int)h->J[n];
+  h->S.ensure((size_t)(d * d));
+  cudaEvent_t e0, e1, e2;
+  TK_CUDA(cudaEventCreate(&e0));
+  TK_CUDA(cudaEventCreate(&e1));
+  TK_CUDA(cudaEventCreate(&e2));
+  TK_CUDA(cudaEventRecord(e0, h->st));
+  gram_syrk(A, h->S.p, d, h->gram, h->st);
+  TK_CUDA(cudaEventRecord(e1, h->st));
+  std::vector<double> theta = solve_eig(h, d, J, slot);
+  if (!transposed) {
+    canon_to_f32(h->V.p, J, d, J, h->U[n].p, h->st);
+  } else {
+    // Y^T Y route: U = Y_(n) V Theta^{-1/2} = (Y^T)^T V Theta^{-1/2}, then CholQR2
+    std::vector<double> sc(J);
+    for (int j = 0; j < J; ++j) sc[j] = theta[j] > 0 ? 1.0 / std::sqrt(theta[j]) : 0.0;
+    h->scal.ensure(J);
+    TK_CUDA(cudaMemcpyAsync(h->scal.p, sc.data(), J * sizeof(double), cudaMemcpyHostToDevice, h->st));
+    TK_LAUNCH(k_scale_cols, gridn(d * J), 256, 0, h->st, h->V.p, d, J, h->scal.p);
+    const int64_t I = h->dims[n];
+    h->Ufull.ensure((size_t)(I * J));
+    MatRef a;
+    a.t = Elt::SPLIT; a.p = A.hi; a.lo = A.lo; a.ld = A.ld; a.trans = true;
+    MatRef b;
+    b.t = Elt::F64; b.p = h->V.p; b.ld = J; b.trans = false;
+    dgemm(I, J, d, 1.0, a, b, 0.0, h->Ufull.p, J, 0.0, nullptr, 0, h->eig.dense, h->st);
+    cholqr2(h->Ufull.p, J, I, J, h->eig, h->st);
+    canon_to_f32(h->Ufull.p, J, I, J, h->U[n].p, h->st);
+  }
+  TK_CUDA(cudaEventRecord(e2, h->st));
+  TK_CUDA(cudaEventSynchronize(e2));
+  float a = 0, b = 0;
+  TK_CUDA(cudaEventElapsedTime(&a, e0, e1));
+  TK_CUDA(cudaEventElapsedTime(&b, e1, e2));
+  if (ms_gram) *ms_gram += a;
+  if (ms_eig) *ms_eig += b;
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaEventDestroy(e2);
+}
+
+// G_(N) = U_N^T Y_(N) from h->Y (must be the projection of the last mode with
+// the current factors), then ||G||^2 and the fit.
+double core_from_y(tucker_handle* h) {
+  const int n = h->order - 1;
+  const int64_t P = prod_J_except(h, n);
+  const int64_t JN = h->J[n];
+  const int64_t I = h->dims[n];
+  h->G64.ensure((size_t)(JN * P));
+  MatRef a;
+  a.t = Elt::F32; a.p = h->U[n].p; a.ld = JN; a.trans = true;
+  MatRef b;
+  b.t = Elt::SPLIT; b.p = h->Y.hi; b.lo = h->Y.lo; b.ld = h->Y.ld; b.trans = h->Y_transposed;
+  dgemm(JN, P, I, 1.0, a, b, 0.0, h->G64.p, P, 0.0, nullptr, 0, h->eig.dense, h->st);
+  h->scal.ensure(2);
+  TK_LAUNCH(k_core_fit, 1, 512, 0, h->st, h->G64.p, JN * P, h->normX2, h->scal.p);
+  double out[2];
+  TK_CUDA(cudaMemcpyAsync(out, h->scal.p, 2 * sizeof(double), cudaMemcpyDeviceToHost, h->st));
+  TK_CUDA(cudaStreamSynchronize(h->st));
+  h->G_valid = true;
+  return out[1];
+}
+
+double compute_core(tucker_handle* h) {
+  const int n = h->order - 1;
+  const bool tr = prod_J_except(h, n) < h->dims[n];
+  project_hooi(h, n, tr);
+  return core_from_y(h);
+}
+
+int validate_factor(const float* U, int64_t I, int64_t J) {
+  // max |U^T U - I| <= 1e-5 (host check on the caller's copy)
+  std::vector<double> G((size_t)(J * J), 0.0);
+  for (int64_t i = 0; i < I; ++i)
+    for (int64_t a = 0; a < J; ++a) {
+      const double ua = U[i * J + a];
+      if (!std::isfinite(ua)) return TUCKER_E_FACTOR;
+      for (int64_t b = a; b < J; ++b) G[a * J + b] += ua * (double)U[i * J + b];
+    }
+  for (int64_t a = 0; a < J; ++a)
+    for (int64_t b = a; b < J; ++b)
+      if (std::fabs(G[a * J + b] - (a == b ? 1.0 : 0.0)) > 1e-5) return TUCKER_E_FACTOR;
+  return TUCKER_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+void tucker_default_opts(tucker_opts* o) {
+  if (!o) return;
+  std::memset(o, 0, sizeof(*o));
+  o->device = 0;
+  o->rank = 0;
+  o->world = 1;
+}
+
+const char* tucker_strerror(int code) {
+  switch (code) {
+    case TUCKER_OK: return "ok";
+    case TUCKER_E_ARG: return "invalid argument";
+    case TUCKER_E_INDEX: return "index out of range";
+    case TUCKER_E_DUP: return "duplicate coordinate";
+    case TUCKER_E_VALUE: return "non-finite value or zero tensor";
+    case TUCKER_E_FACTOR: return "initial factor not orthonormal";
+    case TUCKER_E_CUDA: return "CUDA error";
+    case TUCKER_E_NCCL: return "NCCL error";
+    case TUCKER_E_OOM: return "out of device memory";
+    case TUCKER_E_STATE: return "call out of order";
+    case TUCKER_E_CONVERGE: return "eigensolver did not reach tolerance";
+    default: return "unknown error";
+  }
+}
+
+const char* tucker_last_error(const tucker_handle* h) { return h ? h->last_error.c_str() : ""; }
+
+int tucker_init(tucker_handle** out, int order, const int64_t* dims, const int64_t* core,
+                int64_t nnz, const int32_t* const* idx, const float* vals, const float* const* U0,
+                const tucker_opts* opts) {
+  if (!out || !dims || !core || !idx || !vals || !U0) return TUCKER_E_ARG;
+  *out = nullptr;
+  if (order < 3 || order > 4 || nnz <= 0 || nnz >= (int64_t)1 << 31) return TUCKER_E_ARG;
+  tucker_opts o;
+  tucker_default_opts(&o);
+  if (opts) o = *opts;
+  if (o.world != 1) return TUCKER_E_ARG;
+  for (int n = 0; n < order; ++n) {
+    if (dims[n] < 1 || dims[n] >= (int64_t)1 << 31) return TUCKER_E_ARG;
+    if (core[n] < 1 || core[n] > dims[n] || core[n] > kMaxJ) return TUCKER_E_ARG;
+    if (!idx[n] || !U0[n]) return TUCKER_E_ARG;
+  }
+  const bool on_dev = (o.flags & TUCKER_INPUT_ON_DEVICE) != 0;
+  if (!on_dev)
+    for (int n = 0; n < order; ++n) {
+      const int rc = validate_factor(U0[n], dims[n], core[n]);
+      if (rc) return rc;
+    }
+  auto h = std::make_unique<tucker_handle>();
+  h->order = order;
+  h->opts = o;
+  for (int n = 0; n < order; ++n) {
+    h->dims[n] = dims[n];
+    h->J[n] = core[n];
+  }
+  for (auto& r : h->mp_csf)
+    for (int& v : r) v = -1;
+  const int rc = guarded(h.get(), [&]() -> int {
+    if (o.stream) {
+      h->st = (cudaStream_t)o.stream;
+    } else {
+      TK_CUDA(cudaStreamCreateWithFlags(&h->st, cudaStreamNonBlocking));
+      h->own_stream = true;
+    }
+    const cudaMemcpyKind kind = on_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+    Coo& c = h->coo;
+    c.order = order;
+    c.nnz = nnz;
+    for (int n = 0; n < order; ++n) {
+      c.dims[n] = dims[n];
+      c.idx[n].alloc(nnz);
+      TK_CUDA(cudaMemcpyAsync(c.idx[n].p, idx[n], nnz * sizeof(int32_t), kind, h->st));
+      h->U[n].alloc((size_t)(dims[n] * core[n]));
+      TK_CUDA(cudaMemcpyAsync(h->U[n].p, U0[n], dims[n] * core[n] * sizeof(float), kind, h->st));
+    }
+    c.val.alloc(nnz);
+    TK_CUDA(cudaMemcpyAsync(c.val.p, vals, nnz * sizeof(float), kind, h->st));
+    coo_validate_compact(c, h->st);
+    h->normX2 = coo_norm2(c, h->st);
+    if (!(h->normX2 > 0) || !std::isfinite(h->normX2))
+      fail(TUCKER_E_VALUE, "tucker_init: ||X|| = 0 or not finite");
+    // orderings: root n, leaf m, mids = the other modes ascending
+    for (int n = 0; n < order; ++n) {
+      for (int m = 0; m < order; ++m) {
+        if (m == n) continue;
+        int mids[2] = {-1, -1}, nm = 0;
+        for (int q = 0; q < order; ++q)
+          if (q != n && q != m) mids[nm++] = q;
+        auto cs = std::make_unique<Csf>();
+        csf_build(c, *cs, n, mids[0], order == 4 ? mids[1] : -1, m, h->st);
+        h->mp_csf[n][m] = (int)h->csfs.size();
+        h->csfs.push_back(std::move(cs));
+      }
+      // HOOI: leaf = the other mode with the smallest J (ties: highest mode id)
+      int best = -1;
+      for (int m = 0; m < order; ++m)
+        if (m != n && (best < 0 || h->J[m] <= h->J[best])) best = m;
+      h->hooi_csf[n] = h->mp_csf[n][best];
+    }
+    // the COO copy is no longer needed
+    for (int n = 0; n < order; ++n) c.idx[n].release();
+    c.val.release();
+    TK_CUDA(cudaStreamSynchronize(h->st));
+    return TUCKER_OK;
+  });
+  if (rc != TUCKER_OK) {
+    // keep the message for the caller through stderr (no handle is returned)
+    std::fprintf(stderr, "tucker_init: %s\n", h->last_error.c_str());
+    if (h->own_stream && h->st) cudaStreamDestroy(h->st);
+    return rc;
+  }
+  *out = h.release();
+  return TUCKER_OK;
+}
+
+int tucker_set_factors(tucker_handle* h, const float* const* U) {
+  if (!h || !U) return TUCKER_E_ARG;
+  const bool on_dev = (h->opts.flags & TUCKER_INPUT_ON_DEVICE) != 0;
+  for (int n = 0; n < h->order; ++n) {
+    if (!U[n]) return TUCKER_E_ARG;
+    if (!on_dev) {
+      const int rc = validate_factor(U[n], h->dims[n], h->J[n]);
+      if (rc) return rc;
+    }
+  }
+  return guarded(h, [&]() -> int {
+    for (int n = 0; n < h->order; ++n)
+      TK_CUDA(cudaMemcpyAsync(h->U[n].p, U[n], h->dims[n] * h->J[n] * sizeof(float),
+                              on_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, h->st));
+    TK_CUDA(cudaStreamSynchronize(h->st));
+    h->G_valid = false;
+    for (auto& row : h->slots)
+      for (auto& s : row) s.valid = false;
+    return TUCKER_OK;
+  });
+}
+
+int hooi_sweep(tucker_handle* h, int sweeps, double* fit_per_sweep, float* stage_ms) {
+  if (!h || sweeps < 1) return TUCKER_E_ARG;
+  return guarded(h, [&]() -> int {
+    h->eig_unconverged = false;
+    for (int s = 0; s < sweeps; ++s) {
+      float ms[4] = {0, 0, 0, 0};
+      for (int n = 0; n < h->order; ++n) {
+        const bool tr = prod_J_except(h, n) < h->dims[n];  // Y^T Y is the smaller Gram
+        cudaEvent_t a, b;
+        TK_CUDA(cudaEventCreate(&a));
+        TK_CUDA(cudaEventCreate(&b));
+        TK_CUDA(cudaEventRecord(a, h->st));
+        project_hooi(h, n, tr);
+        TK_CUDA(cudaEventRecord(b, h->st));
+        TK_CUDA(cudaEventSynchronize(b));
+        float t = 0;
+        TK_CUDA(cudaEventElapsedTime(&t, a, b));
+        ms[0] += t;
+        cudaEventDestroy(a);
+        cudaEventDestroy(b);
+        update_factor(h, n, h->Y, tr, h->slots[0][n], &ms[1], &ms[2]);
+      }
+      // G_(N) = U_N^T Y_(N) is free after the last mode (Fig. 4)
+      cudaEvent_t a, b;
+      TK_CUDA(cudaEventCreate(&a));
+      TK_CUDA(cudaEventCreate(&b));
+      TK_CUDA(cudaEventRecord(a, h->st));
+      const double fit = core_from_y(h);
+      TK_CUDA(cudaEventRecord(b, h->st));
+      TK_CUDA(cudaEventSynchronize(b));
+      float t = 0;
+      TK_CUDA(cudaEventElapsedTime(&t, a, b));
+      ms[3] += t;
+      cudaEventDestroy(a);
+      cudaEventDestroy(b);
+      if (fit_per_sweep) fit_per_sweep[s] = fit;
+      if (stage_ms)
+        for (int q = 0; q < 4; ++q) stage_ms[4 * s + q] = ms[q];
+    }
+    return h->eig_unconverged ? TUCKER_E_CONVERGE : TUCKER_OK;
+  });
+}
+
+int mp_sweep(tucker_handle* h, int sweeps, double* fit_per_sweep, float* stage_ms) {
+  if (!h || sweeps < 1) return TUCKER_E_ARG;
+  return guarded(h, [&]() -> int {
+    h->eig_unconverged = false;
+    h->G_valid = false;
+    for (int s = 0; s < sweeps; ++s) {
+      float ms[4] = {0, 0, 0, 0};
+      for (int n = 0; n < h->order; ++n) {
+        cudaEvent_t a, b;
+        TK_CUDA(cudaEventCreate(&a));
+        TK_CUDA(cudaEventCreate(&b));
+        TK_CUDA(cudaEventRecord(a, h->st));
+        Split W = build_mp_w(h, n);
+        TK_CUDA(cudaEventRecord(b, h->st));
+        TK_CUDA(cudaEventSynchronize(b));
+        float t = 0;
+        TK_CUDA(cudaEventElapsedTime(&t, a, b));
+        ms[0] += t;
+        cudaEventDestroy(a);
+        cudaEventDestroy(b);
+        update_factor(h, n, W, false, h->slots[1][n], &ms[1], &ms[2]);
+      }
+      h->G_valid = false;
+      if (fit_per_sweep) {
+        cudaEvent_t a, b;
+        TK_CUDA(cudaEventCreate(&a));
+        TK_CUDA(cudaEventCreate(&b));
+        TK_CUDA(cudaEventRecord(a, h->st));
+        fit_per_sweep[s] = compute_core(h);
+        TK_CUDA(cudaEventRecord(b, h->st));
+        TK_CUDA(cudaEventSynchronize(b));
+        float t = 0;
+        TK_CUDA(cudaEventElapsedTime(&t, a, b));
+        ms[3] += t;
+        cudaEventDestroy(a);
+        cudaEventDestroy(b);
+      }
+      if (stage_ms)
+        for (int q = 0; q < 4; ++q) stage_ms[4 * s + q] = ms[q];
+    }
+    return h->eig_unconverged ? TUCKER_E_CONVERGE : TUCKER_OK;
+  });
+}
+
+int core_and_fit(tucker_handle* h, float* core_out, float* const* U_out, double* fit_out) {
+  if (!h) return TUCKER_E_ARG;
+  return guarded(h, [&]() -> int {
+    double fit;
+    if (h->G_valid && h->Y_mode == h->order - 1) {
+      fit = core_from_y(h);  // recompute from the cached Y_(N): cheap, same kernels
+    } else {
+      fit = compute_core(h);
+    }
+    const bool od = (h->opts.flags & TUCKER_OUTPUT_ON_DEVICE) != 0;
+    const cudaMemcpyKind kind = od ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
+    if (core_out) {
+      int64_t P = 1;
+      for (int n = 0; n < h->order; ++n) P *= h->J[n];
+      h->G32.ensure((size_t)P);
+      TK_LAUNCH(k_d2f, gridn(P), 256, 0, h->st, h->G64.p, P, h->G32.p);
+      TK_CUDA(cudaMemcpyAsync(core_out, h->G32.p, P * sizeof(float), kind, h->st));
+    }
+    if (U_out)
+      for (int n = 0; n < h->order; ++n)
+        if (U_out[n])
+          TK_CUDA(cudaMemcpyAsync(U_out[n], h->U[n].p, h->dims[n] * h->J[n] * sizeof(float), kind,
+                                  h->st));
+    TK_CUDA(cudaStreamSynchronize(h->st));
+    if (fit_out) *fit_out = fit;
+    return TUCKER_OK;
+  });
+}
+
+int tucker_free(tucker_handle* h) {
+  if (!h) return TUCKER_OK;
+  cudaSetDevice(h->opts.device);
+  if (h->st) cudaStreamSynchronize(h->st);
+  const bool own = h->own_stream;
+  cudaStream_t st = h->st;
+  delete h;
+  if (own && st) cudaStreamDestroy(st);
+  return TUCKER_OK;
+}
+
+int tucker_debug_ttmc(tucker_handle* h, int mode, float* Y_out) {
+  if (!h || !Y_out || mode < 0 || mode >= h->order) return TUCKER_E_ARG;
+  return guarded(h, [&]() -> int {
+    project_hooi(h, mode, false);
+    h->G_valid = false;
+    const int64_t rows = h->Y.rows, cols = h->Y.cols;
+    h->Ytmp.ensure((size_t)(rows * cols));
+    TK_LAUNCH(k_combine, gridn(rows * cols), 256, 0, h->st, h->Y.hi, h->Y.lo, rows, cols, h->Y.ld,
+              h->Ytmp.p);
+    const bool od = (h->opts.flags & TUCKER_OUTPUT_ON_DEVICE) != 0;
+    TK_CUDA(cudaMemcpyAsync(Y_out, h->Ytmp.p, rows * cols * sizeof(float),
+                            od ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, h->st));
+    TK_CUDA(cudaStreamSynchronize(h->st));
+    return TUCKER_OK;
+  });
+}
+
+int tucker_debug_gram(tucker_handle* h, int algo, int mode, double* S_out) {
+  if (!h || !S_out || mode < 0 || mode >= h->order || algo < 0 || algo > 1) return TUCKER_E_ARG;
+  return guarded(h, [&]() -> int {
+    Split A;
+    if (algo == 0) {
+      project_hooi(h, mode, false);
+      h->G_valid = false;
+      A = h->Y;
+    } else {
+      A = build_mp_w(h, mode);
+    }
+    const int64_t d = A.rows;
+    h->S.ensure((size_t)(d * d));
+    gram_syrk(A, h->S.p, d, h->gram, h->st);
+    const bool od = (h->opts.flags & TUCKER_OUTPUT_ON_DEVICE) != 0;
+    TK_CUDA(cudaMemcpyAsync(S_out, h->S.p, d * d * sizeof(double),
+                            od ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, h->st));
+    TK_CUDA(cudaStreamSynchronize(h->st));
+    return TUCKER_OK;
+  });
+}
+
+int tucker_debug_eig(tucker_handle* h, int d, int J, const double* S, float* U_out,
+                     double* evals_out) {
+  if (!h || !S || !U_out || d < 1 || J < 1 || J > d || J > kMaxJ) return TUCKER_E_ARG;
+  return guarded(h, [&]() -> int {
+    h->S.ensure((size_t)d * d);
+    const bool od = (h->opts.flags & TUCKER_OUTPUT_ON_DEVICE) != 0;
+    TK_CUDA(cudaMemcpyAsync(h->S.p, S, (size_t)d * d * sizeof(double),
+                            od ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, h->st));
+    h->scratch_slot.valid = false;
+    h->eig_unconverged = false;
+    std::vector<double> theta = solve_eig(h, d, J, h->scratch_slot);
+    h->Ytmp.ensure((size_t)d * J);
+    canon_to_f32(h->V.p, J, d, J, h->Ytmp.p, h->st);
+    TK_CUDA(cudaMemcpyAsync(U_out, h->Ytmp.p, (size_t)d * J * sizeof(float),
+                            od ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, h->st));
+    TK_CUDA(cudaStreamSynchronize(h->st));
+    if (evals_out)
+      for (int j = 0; j < J; ++j) evals_out[j] = theta[j];
+    return h->eig_unconverged ? TUCKER_E_CONVERGE : TUCKER_OK;
+  });
+}
+
+int tucker_stats(tucker_handle* h, int64_t* stats, int reset) {
+  if (!h || !stats) return TUCKER_E_ARG;
+  stats[0] = h->launches;
+  stats[1] = h->eig.stat_outer - h->stat_outer0;
+  stats[2] = h->eig.stat_matvec - h->stat_matvec0;
+  stats[3] = h->eig.stat_sweeps - h->stat_sweeps0;
+  if (reset) {
+    h->launches = 0;
+    h->stat_outer0 = h->eig.stat_outer;
+    h->stat_matvec0 = h->eig.stat_matvec;
+    h->stat_sweeps0 = h->eig.stat_sweeps;
+  }
+  return TUCKER_OK;
+}
+
+}  // extern "C"

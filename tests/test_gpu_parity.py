@@ -1,0 +1,195 @@
+"""GPU parity: the CUDA path (through the C-ABI) vs the fp64 oracle.
+
+Tolerances (BASELINE.json north star):
+  Y_(n)          <= 1e-4 relative Frobenius (expect ~1e-6, fp32 storage)
+  Gram / M_n     <= 1e-5 relative Frobenius (3xTF32 + fp64 accumulation)
+  factors        <= 1e-4 projector distance ||U U^T - U_o U_o^T||_F
+  fit            <= 1e-5 absolute
+  core G         <= 1e-4 relative after Procrustes alignment (reading A3)
+"""
+import numpy as np
+import pytest
+
+from oracle import tucker_oracle as O
+from synth import make_config, random_orthonormal, uniform_distinct_coo
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def capi():
+    import __graft_entry__
+    __graft_entry__.build()
+    from paper_0711_2023_b200 import capi as c
+    return c
+
+
+def case(dims, nnz, core, seed=7, fseed=8):
+    rng = np.random.default_rng(seed)
+    idx, vals = uniform_distinct_coo(dims, nnz, rng)
+    frng = np.random.default_rng(fseed)
+    U0 = [random_orthonormal(I, J, frng) for I, J in zip(dims, core)]
+    return idx, vals, U0
+
+
+def align_core(G, U, Go, Uo):
+    """Procrustes-align G to the oracle's bases: G x_n R_n^T with R_n = polar(U_n^T U_o,n)."""
+    Ga = np.asarray(G, dtype=np.float64)
+    for n in range(len(U)):
+        M = np.asarray(U[n], dtype=np.float64).T @ Uo[n]
+        a, _, bt = np.linalg.svd(M)
+        R = a @ bt
+        Ga = O.ttm(Ga, R.T, n)
+    return Ga
+
+
+SHAPES = [
+    ((100, 100, 100), 10_000, (10, 10, 10)),       # config 1
+    ((100, 110, 120), 13_200, (10, 11, 12)),       # non-cubic (Appendix `test`)
+    ((37, 300, 53), 9_000, (5, 16, 7)),            # ragged, one mode much longer (Y^T Y route)
+    ((20, 22, 18, 16), 12_000, (4, 5, 3, 6)),      # order 4
+]
+
+
+@pytest.mark.parametrize("dims,nnz,core", SHAPES)
+def test_ttmc_parity(capi, dims, nnz, core):
+    idx, vals, U0 = case(dims, nnz, core)
+    T = O.SparseTensor(dims, idx, vals)
+    with capi.Tucker(dims, core, idx, vals, U0) as t:
+        for n in range(len(dims)):
+            Y = t.debug_ttmc(n)
+            Yo = O.ttm_chain_unfold(T, U0, n)
+            assert O.rel_frobenius(Y, Yo) < 1e-4
+
+
+@pytest.mark.parametrize("dims,nnz,core", SHAPES)
+def test_gram_parity(capi, dims, nnz, core):
+    idx, vals, U0 = case(dims, nnz, core)
+    T = O.SparseTensor(dims, idx, vals)
+    with capi.Tucker(dims, core, idx, vals, U0) as t:
+        for n in range(len(dims)):
+            S = t.debug_gram(0, n)
+            Yo = O.ttm_chain_unfold(T, U0, n)
+            assert O.rel_frobenius(S, Yo @ Yo.T) < 1e-5
+            M = t.debug_gram(1, n)
+            assert O.rel_frobenius(M, O.mp_gram(T, U0, n)) < 1e-5
+
+
+@pytest.mark.parametrize("d,J,gap", [(100, 10, 1e-2), (300, 50, 1e-3), (1000, 50, 3e-4), (250, 100, 1e-2)])
+def test_eig_parity(capi, d, J, gap):
+    rng = np.random.default_rng(d + J)
+    Q = np.linalg.qr(rng.standard_normal((d, d)))[0]
+    # a dominant "mean" eigenvalue, a flat bulk and a small J/J+1 gap
+    w = np.sort(rng.uniform(0.1, 1.0, d))[::-1].copy()
+    w[0] = 60.0
+    w[J - 1] = w[J] * (1 + gap)
+    w[:J] = np.maximum(w[:J], w[J - 1])
+    S = (Q * w) @ Q.T
+    dims, core = (8, 8, 8), (2, 2, 2)
+    idx, vals, U0 = case(dims, 50, core)
+    with capi.Tucker(dims, core, idx, vals, U0) as t:
+        U, ev, rc = t.debug_eig(S, J)
+    Uo, wo = O.leading_eigenvectors(S, J)
+    assert rc == 0
+    assert O.projector_distance(U, Uo) < 1e-5
+    np.testing.assert_allclose(ev, wo[:J], rtol=1e-10)
+    # sign canonical and ordered
+    for j in range(J):
+        k = int(np.argmax(np.abs(U[:, j])))
+        assert U[k, j] > 0
+
+
+def run_both(capi, dims, idx, vals, U0, core, sweeps):
+    T = O.SparseTensor(dims, idx, vals)
+    out = {}
+    with capi.Tucker(dims, core, idx, vals, U0) as t:
+        fh = t.hooi_sweep(sweeps)
+        G, U, fit = t.core_and_fit()
+        out["hooi"] = (fh, G, U, fit)
+        t.set_factors(U0)
+        fm = t.mp_sweep(sweeps)
+        Gm, Um, fitm = t.core_and_fit()
+        out["mp"] = (fm, Gm, Um, fitm)
+    ref = {"hooi": O.run_hooi(T, U0, core, sweeps), "mp": O.run_mp(T, U0, core, sweeps)}
+    return out, ref
+
+
+@pytest.mark.parametrize("dims,nnz,core", SHAPES)
+def test_end_to_end_parity(capi, dims, nnz, core):
+    idx, vals, U0 = case(dims, nnz, core)
+    out, ref = run_both(capi, dims, idx, vals, U0, core, 3)
+    for algo in ("hooi", "mp"):
+        fits, G, U, fit = out[algo]
+        r = ref[algo]
+        for n in range(len(dims)):
+            assert O.projector_distance(U[n], r["U"][n]) < 1e-4, (algo, n)
+            assert np.abs(U[n].astype(np.float64).T @ U[n] - np.eye(core[n])).max() < 1e-5
+        assert abs(fit - r["fit"]) < 1e-5
+        np.testing.assert_allclose(fits, r["fits"], atol=1e-5)
+        Ga = align_core(G, U, r["G"], r["U"])
+        assert O.rel_frobenius(Ga, r["G"]) < 1e-4
+
+
+def test_config1_full(capi):
+    c = make_config(1)
+    out, ref = run_both(capi, c["dims"], c["idx"], c["vals"], c["U0"], c["core"], c["sweeps"])
+    for algo in ("hooi", "mp"):
+        _, _, U, fit = out[algo]
+        for n in range(3):
+            assert O.projector_distance(U[n], ref[algo]["U"][n]) < 1e-4
+        assert abs(fit - ref[algo]["fit"]) < 1e-5
+
+
+def test_edge_cases(capi):
+    dims, core = (30, 40, 25), (3, 4, 2)
+    idx, vals, U0 = case(dims, 600, core)
+    # duplicate coordinate
+    idx_d = [np.concatenate([a, a[:1]]) for a in idx]
+    with pytest.raises(capi.TuckerError) as e:
+        capi.Tucker(dims, core, idx_d, np.concatenate([vals, vals[:1]]), U0)
+    assert e.value.code == 3
+    # out of range
+    idx_o = [a.copy() for a in idx]
+    idx_o[2][5] = dims[2]
+    with pytest.raises(capi.TuckerError) as e:
+        capi.Tucker(dims, core, idx_o, vals, U0)
+    assert e.value.code == 2
+    # non-finite value
+    v = vals.copy()
+    v[3] = np.nan
+    with pytest.raises(capi.TuckerError) as e:
+        capi.Tucker(dims, core, idx, v, U0)
+    assert e.value.code == 4
+    # all-zero tensor
+    with pytest.raises(capi.TuckerError) as e:
+        capi.Tucker(dims, core, idx, np.zeros_like(vals), U0)
+    assert e.value.code == 4
+    # explicit zeros are dropped; empty slices (mode-1 indices >= 20 unused) are fine
+    v = vals.copy()
+    v[::7] = 0
+    idx_e = [a.copy() for a in idx]
+    idx_e[0] = idx_e[0] % 20
+    keep = np.unique(np.stack(idx_e), axis=1, return_index=True)[1]
+    idx_e = [a[np.sort(keep)] for a in idx_e]
+    v = v[np.sort(keep)]
+    out, ref = run_both(capi, dims, idx_e, v, U0, core, 2)
+    for algo in ("hooi", "mp"):
+        _, _, U, fit = out[algo]
+        assert abs(fit - ref[algo]["fit"]) < 1e-5
+        for n in range(3):
+            assert O.projector_distance(U[n], ref[algo]["U"][n]) < 1e-4
+
+
+def test_determinism(capi):
+    dims, core = (60, 50, 40), (6, 5, 4)
+    idx, vals, U0 = case(dims, 5000, core)
+    res = []
+    for _ in range(2):
+        with capi.Tucker(dims, core, idx, vals, U0) as t:
+            t.hooi_sweep(2)
+            G, U, fit = t.core_and_fit()
+            res.append((G, U, fit))
+    assert res[0][2] == res[1][2]
+    np.testing.assert_array_equal(res[0][0], res[1][0])
+    for a, b in zip(res[0][1], res[1][1]):
+        np.testing.assert_array_equal(a, b)
