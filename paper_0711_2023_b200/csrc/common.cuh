@@ -33,11 +33,19 @@ struct Error {
 // Launch counter shared by all launches of one handle (reported by tucker_stats).
 extern thread_local int64_t* g_launch_counter;
 
+bool sync_check_enabled();  // env TUCKER_SYNC_CHECK: synchronise + check after every launch
+
 #define TK_LAUNCH(kernel, grid, block, smem, stream, ...)                 \
   do {                                                                    \
     kernel<<<(grid), (block), (smem), (stream)>>>(__VA_ARGS__);           \
     TK_CUDA(cudaGetLastError());                                          \
     if (::tk::g_launch_counter) ++(*::tk::g_launch_counter);              \
+    if (::tk::sync_check_enabled()) {                                     \
+      cudaError_t se_ = cudaStreamSynchronize(stream);                    \
+      if (se_ != cudaSuccess)                                             \
+        ::tk::fail(TUCKER_E_CUDA, std::string("kernel ") + #kernel +      \
+                   " failed: " + cudaGetErrorString(se_));                \
+    }                                                                     \
   } while (0)
 
 inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }

@@ -7,11 +7,18 @@
 // run-length boundaries give slice / node / fiber pointers.
 #include <cub/cub.cuh>
 
+#include <cstdlib>
+
 #include "internal.cuh"
 
 namespace tk {
 
 thread_local int64_t* g_launch_counter = nullptr;
+
+bool sync_check_enabled() {
+  static const bool on = std::getenv("TUCKER_SYNC_CHECK") != nullptr;
+  return on;
+}
 
 namespace {
 

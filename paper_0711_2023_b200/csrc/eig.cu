@@ -7,7 +7,10 @@
 // Rayleigh-Ritz step whose k x k eigenproblem is solved by a one-CTA cyclic
 // Jacobi in shared memory (fp64).  Warm starts reuse the last Ritz basis of the
 // same (algorithm, mode) slot.
+#include <algorithm>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 
 #include "internal.cuh"
 
@@ -114,7 +117,13 @@ __global__ void __launch_bounds__(1024) k_jacobi(const double* __restrict__ Hin,
     if (!any_in_sweep) break;
   }
   // sort eigenvalues descending (stable by index): rank of each diagonal entry
-  if (tid < k) {
+  __shared__ int bad;
+  if (tid == 0) bad = 0;
+  if (tid < k) order[tid] = tid;
+  __syncthreads();
+  if (tid < k && !isfinite(H[tid * k + tid])) atomicOr(&bad, 1);
+  __syncthreads();
+  if (tid < k && !bad) {
     const double d = H[tid * k + tid];
     int rank = 0;
     for (int j = 0; j < k; ++j) {
@@ -129,29 +138,32 @@ __global__ void __launch_bounds__(1024) k_jacobi(const double* __restrict__ Hin,
     Vout[r * k + c] = V[r * k + order[c]];
   }
   if (tid < k) theta[tid] = H[order[tid] * k + order[tid]];
-  if (tid == 0 && sweeps_out) *sweeps_out = sweep;
+  if (tid == 0 && sweeps_out) *sweeps_out = bad ? -1 : sweep;
 }
 
 // ------------------------------------------------------- Cholesky / inverse --
 // One CTA.  G (k x k SPD) -> Rinv (k x k upper triangular) with G = R^T R.
 __global__ void __launch_bounds__(1024) k_chol_inv(const double* __restrict__ G, int k,
-                                                   double* __restrict__ Rinv) {
+                                                   double* __restrict__ Rinv, double shift) {
   extern __shared__ double sm[];
   double* A = sm;  // k*k
   const int tid = threadIdx.x, nt = blockDim.x;
   __shared__ double maxd;
-  for (int e = tid; e < k * k; e += nt) A[e] = G[e];
-  __syncthreads();
-  if (tid == 0) {
-    double m = 0.0;
-    for (int i = 0; i < k; ++i) m = fmax(m, A[i * k + i]);
-    maxd = m > 0 ? m : 1.0;
+  __shared__ double dsc[kMaxBlock];
+  for (int i = tid; i < k; i += nt) {
+    const double g = G[i * k + i];
+    dsc[i] = g > 0 ? 1.0 / sqrt(g) : 1.0;
   }
+  __syncthreads();
+  for (int e = tid; e < k * k; e += nt)
+    A[e] = G[e] * dsc[e / k] * dsc[e % k] + ((e / k == e % k) ? shift : 0.0);
+  __syncthreads();
+  if (tid == 0) maxd = 1.0;
   __syncthreads();
   for (int j = 0; j < k; ++j) {
     if (tid == 0) {
       double d = A[j * k + j];
-      const double floor = 1e-28 * maxd;
+      const double floor = 1e-12 * maxd;
       A[j * k + j] = sqrt(d > floor ? d : floor);
     }
     __syncthreads();
@@ -179,6 +191,16 @@ __global__ void __launch_bounds__(1024) k_chol_inv(const double* __restrict__ G,
       Rinv[i * k + c] = x;
     }
   }
+  __syncthreads();
+  for (int e = tid; e < k * k; e += nt) Rinv[e] *= dsc[e / k];
+}
+
+__global__ void k_count_nonfinite(const double* x, int64_t n, int* out) {
+  int c = 0;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
+       e += (int64_t)gridDim.x * blockDim.x)
+    c += !isfinite(x[e]);
+  if (c) atomicAdd(out, c);
 }
 
 // resid[i] = || SQ[:, i] - theta_i Q[:, i] ||_2, one CTA per column i < ncol
@@ -299,7 +321,7 @@ void cholqr2_impl(double* Q, int64_t d, int k, EigWs& ws, cudaStream_t st) {
   const size_t smem = (size_t)k * k * sizeof(double);
   for (int pass = 0; pass < 2; ++pass) {
     dgemm(k, k, d, 1.0, f64(Q, k, true), f64(Q, k), 0.0, ws.H.p, k, 0.0, nullptr, 0, ws.dense, st);
-    TK_LAUNCH(k_chol_inv, 1, 512, smem, st, ws.H.p, k, ws.R.p);
+    TK_LAUNCH(k_chol_inv, 1, 512, smem, st, ws.H.p, k, ws.R.p, 0.0);
     dgemm(d, k, k, 1.0, f64(Q, k), f64(ws.R.p, k), 0.0, ws.T.p, k, 0.0, nullptr, 0, ws.dense, st);
     TK_LAUNCH(k_copy_cols, grid_for(d * k), 256, 0, st, ws.T.p, (int64_t)k, Q, (int64_t)k, d, k);
   }
@@ -335,6 +357,7 @@ bool eig_leading(const double* S, int64_t lds, int64_t d, int J, EigSlot& slot, 
   if (lds != d) fail(TUCKER_E_ARG, "eig_leading: lds must equal d");
   const int k = choose_block(J, d, o.oversample);
   const size_t dk = (size_t)(d * k);
+  // A: active block (d x ka, contiguous, ld = ka) in ws.Q; L: locked vectors (d x J, ld = J)
   ws.Q.ensure(dk);
   ws.SQ.ensure(dk);
   ws.X.ensure(dk);
@@ -345,91 +368,201 @@ bool eig_leading(const double* S, int64_t lds, int64_t d, int J, EigSlot& slot, 
   ws.R.ensure((size_t)k * k);
   ws.theta.ensure(k);
   ws.resid.ensure(k);
-  ws.h_theta.resize(k);
-  ws.h_resid.resize(k);
-  DBuf<int> dsweeps(1);
+  ws.L.ensure((size_t)(d * J));
+  ws.LT.ensure((size_t)(d * J));
+  ws.Z.ensure((size_t)J * k);
+  ws.h_theta.assign(k, 0.0);
+  ws.h_resid.assign(k, 0.0);
+  ws.dsweeps.ensure(1);
+  std::vector<double> th_lock;  // Ritz values of the locked vectors
+  static const bool dbg = std::getenv("TUCKER_EIG_DEBUG") != nullptr;
 
+  int nlock = 0;
+  int ka = k;
   if (slot.valid && slot.d == d && slot.k == k) {
     TK_CUDA(cudaMemcpyAsync(ws.Q.p, slot.basis.p, dk * sizeof(double), cudaMemcpyDeviceToDevice, st));
   } else {
     TK_LAUNCH(k_fill_random, grid_for(d * k), 256, 0, st, ws.Q.p, d, k, 0,
               (uint64_t)0x5eed0000ull + (uint64_t)d * 131 + (uint64_t)J);
   }
-  cholqr2_impl(ws.Q.p, d, k, ws, st);
 
-  auto rayleigh_ritz = [&]() {
-    // SQ = S Q ; H = Q^T SQ ; eig(H) = V theta ; Q <- Q V ; SQ <- SQ V ; resid
-    dgemm(d, k, d, 1.0, f64(S, lds), f64(ws.Q.p, k), 0.0, ws.SQ.p, k, 0.0, nullptr, 0, ws.dense, st);
-    ++ws.stat_matvec;
-    dgemm(k, k, d, 1.0, f64(ws.Q.p, k, true), f64(ws.SQ.p, k), 0.0, ws.H.p, k, 0.0, nullptr, 0,
-          ws.dense, st);
-    TK_LAUNCH(k_jacobi, 1, 1024, (size_t)2 * k * k * sizeof(double), st, ws.H.p, k, ws.V.p,
-              ws.theta.p, 30, dsweeps.p);
-    dgemm(d, k, k, 1.0, f64(ws.Q.p, k), f64(ws.V.p, k), 0.0, ws.T.p, k, 0.0, nullptr, 0, ws.dense, st);
-    std::swap(ws.Q, ws.T);
-    dgemm(d, k, k, 1.0, f64(ws.SQ.p, k), f64(ws.V.p, k), 0.0, ws.T.p, k, 0.0, nullptr, 0, ws.dense, st);
-    std::swap(ws.SQ, ws.T);
-    TK_LAUNCH(k_resid, J, 256, 0, st, ws.SQ.p, ws.Q.p, d, k, ws.theta.p, ws.resid.p);
-    int hs = 0;
-    TK_CUDA(cudaMemcpyAsync(ws.h_theta.data(), ws.theta.p, k * sizeof(double), cudaMemcpyDeviceToHost, st));
-    TK_CUDA(cudaMemcpyAsync(ws.h_resid.data(), ws.resid.p, J * sizeof(double), cudaMemcpyDeviceToHost, st));
-    TK_CUDA(cudaMemcpyAsync(&hs, dsweeps.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+  auto nonfinite = [&](const double* x, int64_t n, const char* what) {
+    if (!dbg) return;
+    TK_CUDA(cudaMemsetAsync(ws.dsweeps.p, 0, sizeof(int), st));
+    TK_LAUNCH(k_count_nonfinite, grid_for(n), 256, 0, st, x, n, ws.dsweeps.p);
+    int h = 0;
+    TK_CUDA(cudaMemcpyAsync(&h, ws.dsweeps.p, sizeof(int), cudaMemcpyDeviceToHost, st));
     TK_CUDA(cudaStreamSynchronize(st));
+    std::fprintf(stderr, "[eig] nonfinite %s: %d of %lld\n", what, h, (long long)n);
+  };
+  // orthonormalise A (d x ka) against L (d x nlock) and itself (CholQR2, equilibrated)
+  auto orth_active = [&]() {
+    if (nlock > 0) {
+      for (int pass = 0; pass < 2; ++pass) {
+        dgemm(nlock, ka, d, 1.0, f64(ws.L.p, J, true), f64(ws.Q.p, ka), 0.0, ws.Z.p, ka, 0.0,
+              nullptr, 0, ws.dense, st);
+        dgemm(d, ka, nlock, -1.0, f64(ws.L.p, J), f64(ws.Z.p, ka), 1.0, ws.Q.p, ka, 0.0, nullptr, 0,
+              ws.dense, st);
+      }
+    }
+    const size_t smem = (size_t)ka * ka * sizeof(double);
+    // shifted CholQR3 (first pass shifted so the factorisation cannot break down)
+    const double shift = 11.0 * ((double)d * ka + (double)ka * (ka + 1)) * 1.1e-16 * ka;
+    for (int pass = 0; pass < 3; ++pass) {
+      dgemm(ka, ka, d, 1.0, f64(ws.Q.p, ka, true), f64(ws.Q.p, ka), 0.0, ws.H.p, ka, 0.0, nullptr,
+            0, ws.dense, st);
+      nonfinite(ws.H.p, (int64_t)ka * ka, "gram-in-orth");
+      TK_LAUNCH(k_chol_inv, 1, 512, smem, st, ws.H.p, ka, ws.R.p, pass == 0 ? shift : 0.0);
+      nonfinite(ws.R.p, (int64_t)ka * ka, "Rinv");
+      dgemm(d, ka, ka, 1.0, f64(ws.Q.p, ka), f64(ws.R.p, ka), 0.0, ws.T.p, ka, 0.0, nullptr, 0,
+            ws.dense, st);
+      std::swap(ws.Q, ws.T);
+    }
+  };
+  // out = alpha S_defl Y + gamma Dm, S_defl = S - L Theta_L L^T (LT holds S L = L Theta_L + R_L)
+  auto apply_op = [&](const double* Yp, double alpha, double* out, double gamma, const double* Dm) {
+    dgemm(d, ka, d, alpha, f64(S, lds), f64(Yp, ka), 0.0, out, ka, gamma, Dm, ka, ws.dense, st);
+    ++ws.stat_matvec;
+    if (nlock > 0) {
+      dgemm(nlock, ka, d, 1.0, f64(ws.LT.p, J, true), f64(Yp, ka), 0.0, ws.Z.p, ka, 0.0, nullptr,
+            0, ws.dense, st);
+      dgemm(d, ka, nlock, -alpha, f64(ws.L.p, J), f64(ws.Z.p, ka), 1.0, out, ka, 0.0, nullptr, 0,
+            ws.dense, st);
+    }
+  };
+  auto rayleigh_ritz = [&]() {
+    nonfinite(S, d * d, "S");
+    nonfinite(ws.Q.p, d * ka, "Q");
+    apply_op(ws.Q.p, 1.0, ws.SQ.p, 0.0, nullptr);
+    nonfinite(ws.SQ.p, d * ka, "SQ");
+    dgemm(ka, ka, d, 1.0, f64(ws.Q.p, ka, true), f64(ws.SQ.p, ka), 0.0, ws.H.p, ka, 0.0, nullptr,
+          0, ws.dense, st);
+    nonfinite(ws.H.p, (int64_t)ka * ka, "H");
+    TK_LAUNCH(k_jacobi, 1, 1024, (size_t)2 * ka * ka * sizeof(double), st, ws.H.p, ka, ws.V.p,
+              ws.theta.p, 40, ws.dsweeps.p);
+    dgemm(d, ka, ka, 1.0, f64(ws.Q.p, ka), f64(ws.V.p, ka), 0.0, ws.T.p, ka, 0.0, nullptr, 0,
+          ws.dense, st);
+    std::swap(ws.Q, ws.T);
+    dgemm(d, ka, ka, 1.0, f64(ws.SQ.p, ka), f64(ws.V.p, ka), 0.0, ws.T.p, ka, 0.0, nullptr, 0,
+          ws.dense, st);
+    std::swap(ws.SQ, ws.T);
+    TK_LAUNCH(k_resid, ka, 256, 0, st, ws.SQ.p, ws.Q.p, d, ka, ws.theta.p, ws.resid.p);
+    int hs = 0;
+    TK_CUDA(cudaMemcpyAsync(ws.h_theta.data() + nlock, ws.theta.p, ka * sizeof(double),
+                            cudaMemcpyDeviceToHost, st));
+    TK_CUDA(cudaMemcpyAsync(ws.h_resid.data() + nlock, ws.resid.p, ka * sizeof(double),
+                            cudaMemcpyDeviceToHost, st));
+    TK_CUDA(cudaMemcpyAsync(&hs, ws.dsweeps.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+    TK_CUDA(cudaStreamSynchronize(st));
+    if (hs < 0) fail(TUCKER_E_CUDA, "eigensolver breakdown (non-finite Rayleigh quotient)");
     ws.stat_sweeps += hs;
   };
-  auto max_rel_resid = [&]() {
-    double th1 = std::fabs(ws.h_theta[0]);
-    if (th1 == 0) th1 = 1;
-    double m = 0;
-    for (int i = 0; i < J; ++i) m = std::max(m, ws.h_resid[i] / th1);
-    return m;
+  auto theta1 = [&]() {
+    const double t = nlock > 0 ? th_lock[0] : ws.h_theta[0];
+    return t > 0 ? t : 1.0;
+  };
+  // move the converged leading active vectors into L (prefix, descending order)
+  auto lock = [&]() {
+    int nl = 0;
+    const double th1 = theta1();
+    while (nlock + nl < J && nl < ka && ws.h_resid[nlock + nl] <= o.tol * th1) ++nl;
+    if (nlock + nl < J) nl &= ~1;  // keep the active block even (Jacobi pairs all indices)
+    if (nl == 0) return;
+    TK_LAUNCH(k_copy_cols, grid_for(d * nl), 256, 0, st, ws.Q.p, (int64_t)ka, ws.L.p + nlock,
+              (int64_t)J, d, nl);
+    TK_LAUNCH(k_copy_cols, grid_for(d * nl), 256, 0, st, ws.SQ.p, (int64_t)ka, ws.LT.p + nlock,
+              (int64_t)J, d, nl);
+    for (int i = 0; i < nl; ++i) th_lock.push_back(ws.h_theta[nlock + i]);
+    const int kn = ka - nl;
+    if (kn > 0) {
+      TK_LAUNCH(k_copy_cols, grid_for(d * kn), 256, 0, st, ws.Q.p + nl, (int64_t)ka, ws.T.p,
+                (int64_t)kn, d, kn);
+      std::swap(ws.Q, ws.T);
+      TK_LAUNCH(k_copy_cols, grid_for(d * kn), 256, 0, st, ws.SQ.p + nl, (int64_t)ka, ws.T.p,
+                (int64_t)kn, d, kn);
+      std::swap(ws.SQ, ws.T);
+    }
+    nlock += nl;
+    ka = kn;
   };
 
+  orth_active();
   rayleigh_ritz();
-  bool converged = max_rel_resid() <= o.tol || k == d;
+  lock();
+  bool converged = nlock >= J || k == d;
   for (int outer = 0; outer < o.max_outer && !converged; ++outer) {
     ++ws.stat_outer;
-    const double th1 = ws.h_theta[0];
+    const double th1 = theta1();
     const double thJ = ws.h_theta[J - 1];
+    const double thtop = ws.h_theta[nlock];  // largest active Ritz value
     double b = ws.h_theta[k - 1];
     if (!(b > 0)) b = 1e-12 * th1;
+    if (thJ <= b * (1 + 1e-12)) b = thJ * (1 - 1e-3);
     const double a = 0.0;
-    if (thJ <= b * (1 + 1e-12)) b = thJ * (1 - 1e-3);  // degenerate estimate
-    // degree: reduce the current residual to tol, at most 8 between orthonormalisations
-    const double x = (2 * thJ - b - a) / (b - a);
-    const double rate = std::acosh(std::max(x, 1.0 + 1e-12));
-    const double need = std::log(std::max(max_rel_resid() / o.tol, 2.0)) / std::max(rate, 1e-6);
-    const int m = std::max(2, std::min(8, (int)std::ceil(need)));
-    // scaled Chebyshev recurrence (Zhou & Saad), damping [a, b], normalised at th1
     const double e = (b - a) / 2, c = (b + a) / 2;
-    double sigma = e / (th1 - c);
+    const double xJ = std::max((thJ - c) / e, 1.0 + 1e-12);
+    const double xt = std::max((thtop - c) / e, xJ);
+    const double rJ = std::acosh(xJ), rt = std::acosh(xt);
+    double rmax = 0;
+    for (int i = nlock; i < J; ++i) rmax = std::max(rmax, ws.h_resid[i] / th1);
+    // degree: enough to reach tol, while the top active direction outgrows the J-th by <= 1e8
+    int m = (int)std::ceil(std::log(std::max(rmax / o.tol, 4.0)) / std::max(rJ, 1e-6));
+    // the block's bottom Ritz directions (x ~ 1) must stay representable next to the top one:
+    // T_m(x_top) <= 1e7 keeps the filtered block inside CholQR's reach (kappa^2 <~ 1e14)
+    const int m_amp = (int)std::floor(std::log(2e7) / std::max(rt, 1e-6));
+    m = std::max(1, std::min(std::min(m, m_amp), 16));
+    // scaled Chebyshev recurrence (Zhou & Saad) damping [a, b], normalised at thtop
+    double sigma = e / (thtop - c);
     const double tau = 2.0 / sigma;
-    // Y1 = (S X - c X) * sigma / e with X = Q, S X = SQ (already computed)
-    TK_LAUNCH(k_axpby, grid_for(d * k), 256, 0, st, d * k, sigma / e, ws.SQ.p, -c * sigma / e,
+    // Y1 = (S_defl A - c A) sigma / e, where S_defl A = SQ (A is orthogonal to L)
+    TK_LAUNCH(k_axpby, grid_for(d * ka), 256, 0, st, d * ka, sigma / e, ws.SQ.p, -c * sigma / e,
               ws.Q.p, ws.Y.p);
-    TK_LAUNCH(k_axpby, grid_for(d * k), 256, 0, st, d * k, 1.0, ws.Q.p, 0.0, ws.Q.p, ws.X.p);
+    TK_LAUNCH(k_axpby, grid_for(d * ka), 256, 0, st, d * ka, 1.0, ws.Q.p, 0.0, ws.Q.p, ws.X.p);
     for (int i = 2; i <= m; ++i) {
       const double sigma2 = 1.0 / (tau - sigma);
-      // T = 2 sigma2 / e * (S Y - c Y) - sigma sigma2 X
-      dgemm(d, k, d, 2 * sigma2 / e, f64(S, lds), f64(ws.Y.p, k), 0.0, ws.T.p, k, -sigma * sigma2,
-            ws.X.p, k, ws.dense, st);
-      ++ws.stat_matvec;
-      TK_LAUNCH(k_axpby, grid_for(d * k), 256, 0, st, d * k, 1.0, ws.T.p, -2 * sigma2 * c / e,
+      // T = 2 sigma2 / e (S_defl Y - c Y) - sigma sigma2 X
+      apply_op(ws.Y.p, 2 * sigma2 / e, ws.T.p, -sigma * sigma2, ws.X.p);
+      TK_LAUNCH(k_axpby, grid_for(d * ka), 256, 0, st, d * ka, 1.0, ws.T.p, -2 * sigma2 * c / e,
                 ws.Y.p, ws.T.p);
-      std::swap(ws.X, ws.Y);  // X <- Y
-      std::swap(ws.Y, ws.T);  // Y <- T
+      std::swap(ws.X, ws.Y);
+      std::swap(ws.Y, ws.T);
       sigma = sigma2;
     }
-    TK_LAUNCH(k_copy_cols, grid_for(d * k), 256, 0, st, ws.Y.p, (int64_t)k, ws.Q.p, (int64_t)k, d, k);
-    cholqr2_impl(ws.Q.p, d, k, ws, st);
+    std::swap(ws.Q, ws.Y);
+    orth_active();
     rayleigh_ritz();
-    converged = max_rel_resid() <= o.tol;
+    if (dbg) {
+      std::fprintf(stderr, "[eig] d=%lld J=%d k=%d outer=%d m=%d(amp %d) nlock=%d ka=%d rmax=%.3e th1=%.6e thJ=%.6e thtop=%.6e b=%.6e\n",
+                   (long long)d, J, k, outer, m, m_amp, nlock, ka, rmax, th1, thJ, thtop, b);
+      for (int i = nlock; i < std::min(k, nlock + 4); ++i)
+        std::fprintf(stderr, "    th[%d]=%.6e res=%.3e\n", i, ws.h_theta[i], ws.h_resid[i]);
+    }
+    lock();
+    converged = nlock >= J;
   }
-  // outputs
-  TK_LAUNCH(k_copy_cols, grid_for(d * J), 256, 0, st, ws.Q.p, (int64_t)k, out_V, ldv, d, J);
-  for (int i = 0; i < J; ++i) theta_out[i] = ws.h_theta[i];
+  // outputs: the J leading columns of [L | A], sorted by Ritz value (descending)
+  std::vector<double> th_all(th_lock);
+  for (int i = 0; i < ka; ++i) th_all.push_back(ws.h_theta[nlock + i]);
+  std::vector<int> ord(k);
+  for (int i = 0; i < k; ++i) ord[i] = i;
+  std::stable_sort(ord.begin(), ord.end(), [&](int x, int y) { return th_all[x] > th_all[y]; });
+  for (int j = 0; j < J; ++j) {
+    const int src = ord[j];
+    if (src < nlock)
+      TK_LAUNCH(k_copy_cols, grid_for(d), 256, 0, st, ws.L.p + src, (int64_t)J, out_V + j, ldv, d, 1);
+    else
+      TK_LAUNCH(k_copy_cols, grid_for(d), 256, 0, st, ws.Q.p + (src - nlock), (int64_t)ka,
+                out_V + j, ldv, d, 1);
+    theta_out[j] = th_all[src];
+  }
+  // warm-start basis [L | A] for the next solve of this slot
   slot.basis.ensure(dk);
-  TK_CUDA(cudaMemcpyAsync(slot.basis.p, ws.Q.p, dk * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  if (nlock > 0)
+    TK_LAUNCH(k_copy_cols, grid_for(d * nlock), 256, 0, st, ws.L.p, (int64_t)J, slot.basis.p,
+              (int64_t)k, d, nlock);
+  if (ka > 0)
+    TK_LAUNCH(k_copy_cols, grid_for(d * ka), 256, 0, st, ws.Q.p, (int64_t)ka,
+              slot.basis.p + nlock, (int64_t)k, d, ka);
   slot.d = d;
   slot.k = k;
   slot.valid = true;

@@ -98,8 +98,9 @@ struct EigSlot {              // warm-start state per (algorithm, mode)
   bool valid = false;
 };
 struct EigWs {
-  DBuf<double> Q, SQ, X, Y, T, H, V, R;
+  DBuf<double> Q, SQ, X, Y, T, H, V, R, L, LT, Z;
   DBuf<double> theta, resid;
+  DBuf<int> dsweeps;
   DenseWs dense;
   std::vector<double> h_theta, h_resid;
   int64_t stat_outer = 0, stat_matvec = 0, stat_sweeps = 0;
