@@ -1,0 +1,347 @@
+"""bench.py -- HOOI / Multislice-Projection sweep throughput on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 2] [--impl ours|reference]
+
+One step = the whole hot path of SURVEY.md §8(a) over the config's tensor:
+5 HOOI sweeps + core/fit and 5 MP sweeps + core/fit (config 2 of BASELINE.json:
+1000^3, 1e6 uniform nonzeros, core 50^3), each from the same seeded U0, with
+the sparse tensor (CSF) already resident in HBM.  value = nonzero-mode updates
+per second = nnz * N_modes * (HOOI sweeps + MP sweeps) / step time, summed
+over ranks (ranks run replicas in this build).
+
+`e2e` is the same metric through the C-ABI from HOST buffers: tucker_init
+(H2D + CSF build) + sweeps + core_and_fit with the core and factors copied back.
+`--impl reference` times the fp64 oracle (oracle/) on the host cores on a
+bounded sample (1 HOOI sweep + 1 MP sweep) of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0,
+                "_fallback": True}
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.p = None
+        self.gpu = gpu_index
+        try:
+            self.p = subprocess.Popen(
+                ["nvidia-smi", f"--id={gpu_index}", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.p.terminate()
+        try:
+            out = self.p.communicate(timeout=5)[0]
+        except Exception:
+            self.p.kill()
+            out = ""
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in out.strip().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                smax.append(float(f[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        busy = [s for s in sm if s > 0.5 * max(sm)] if sm else []
+        return {"sm_mhz": statistics.median(busy) if busy else None,
+                "sm_max_mhz": max(smax) if smax else None, "samples": len(sm),
+                "reasons": sorted(reasons)}
+
+
+def workload(k):
+    from synth import make_config
+    c = make_config(k)
+    c["name"] = (f"config{k}: {'x'.join(map(str, c['dims']))}, {c['nnz']} nnz ({c['kind']}), "
+                 f"core {'x'.join(map(str, c['core']))}, {c['sweeps']} HOOI + {c['sweeps']} MP sweeps "
+                 f"+ core/fit per step")
+    return c
+
+
+def gram_flops(c):
+    """Algorithmic flops of the Gram (SYRK, upper triangle incl. diagonal) per
+    HOOI sweep and per MP sweep: d(d+1)K with d x K the Gram operand."""
+    dims, J, N = c["dims"], c["core"], len(c["dims"])
+    h = m = 0.0
+    for n in range(N):
+        P = int(np.prod([J[q] for q in range(N) if q != n]))
+        d, K = (dims[n], P) if P >= dims[n] else (P, dims[n])
+        h += d * (d + 1.0) * K
+        Kw = sum(J[q] * int(np.prod([dims[r] for r in range(N) if r not in (n, q)]))
+                 for q in range(N) if q != n)
+        m += dims[n] * (dims[n] + 1.0) * Kw
+    return h, m
+
+
+def cpu_oracle_sample(c):
+    """The fp64 oracle as it stands on a bounded sample: 1 HOOI sweep + 1 MP
+    sweep (+ their cores) of the same workload.  Returns (seconds, units)."""
+    from oracle import tucker_oracle as O
+    T = O.SparseTensor(c["dims"], c["idx"], c["vals"])
+    t0 = time.perf_counter()
+    O.run_hooi(T, c["U0"], c["core"], 1)
+    O.run_mp(T, c["U0"], c["core"], 1)
+    dt = time.perf_counter() - t0
+    return dt, c["nnz"] * len(c["dims"]) * 2
+
+
+def cores_used():
+    n = len(os.sched_getaffinity(0))
+    try:
+        from threadpoolctl import threadpool_info
+        th = [i.get("num_threads", 0) for i in threadpool_info() if i.get("user_api") == "blas"]
+        if th:
+            return int(max(th))
+    except Exception:
+        pass
+    return n
+
+
+def run_reference(args):
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return 0
+    c = workload(args.config)
+    for _ in range(args.warmup):
+        cpu_oracle_sample(c)
+    ts = []
+    units = 0
+    for _ in range(args.steps):
+        dt, units = cpu_oracle_sample(c)
+        ts.append(dt)
+    total = sum(ts)
+    val = units * args.steps / total / 1e9
+    line = {
+        "impl": "reference", "metric": "HOOI/MP sweep throughput (nnz x modes per second)",
+        "value": val, "unit": "Gnnz/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": c["name"] + " [reference step: 1 HOOI + 1 MP sweep sample]",
+                   "l2": "host oracle"},
+        "cpu_baseline": {"value": val, "unit": "Gnnz/s", "cores": cores_used(), "kind": "oracle",
+                         "sample": "1 HOOI sweep + 1 MP sweep (+ cores) of the workload per step"},
+        "e2e": {"value": val, "unit": "Gnnz/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def run_ours(args):
+    import torch
+    world, rank, local = dist_env()
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    import __graft_entry__
+    if rank == 0:
+        __graft_entry__.build()
+    if world > 1:
+        torch.distributed.barrier()
+    from paper_0711_2023_b200 import capi
+
+    c = workload(args.config)
+    dims, core, N, S = c["dims"], c["core"], len(c["dims"]), c["sweeps"]
+    stream = torch.cuda.current_stream(dev)
+    idx_d = [torch.from_numpy(a).to(dev) for a in c["idx"]]
+    vals_d = torch.from_numpy(c["vals"]).to(dev)
+    U0_d = [torch.from_numpy(u).to(dev) for u in c["U0"]]
+    G_d = torch.empty(int(np.prod(core)), dtype=torch.float32, device=dev)
+    U_d = [torch.empty_like(u) for u in U0_d]
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    h = capi.tucker_init(dims, core, idx_d, vals_d, U0_d, device=local, stream=stream.cuda_stream,
+                         on_device=True, output_on_device=True)
+    init_s = time.perf_counter() - t0
+    flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)  # 512 MB > L2
+
+    stage_acc = np.zeros(4)
+    stage_acc_mp = np.zeros(4)
+
+    def step(record=False):
+        nonlocal stage_acc, stage_acc_mp
+        capi.tucker_set_factors(h, U0_d)
+        fh, sh, _ = capi.hooi_sweep(h, S, want_stage=True)
+        capi.core_and_fit_into(h, G_d, U_d)
+        capi.tucker_set_factors(h, U0_d)
+        fm, sm, _ = capi.mp_sweep(h, S, want_fit=False, want_stage=True)
+        fit_m = capi.core_and_fit_into(h, G_d, U_d)
+        if record:
+            stage_acc += sh.sum(axis=0)
+            stage_acc_mp += sm.sum(axis=0)
+        return fh[-1], fit_m
+
+    for _ in range(args.warmup):
+        step()
+    capi.tucker_stats(h, reset=True)
+    clk = Clocks(local) if rank == 0 else None
+    times = []
+    fits = None
+    for _ in range(args.steps):
+        flush.zero_()
+        if world > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        fits = step(record=True)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        times.append(e0.elapsed_time(e1))
+    clocks = clk.stop() if clk else None
+    st = capi.tucker_stats(h)
+    total_ms = float(sum(times))
+    if world > 1:
+        t = torch.tensor([total_ms], device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        total_ms = float(t.item())
+    ms_step = total_ms / args.steps
+    units = c["nnz"] * N * 2 * S
+    value = units * world / (ms_step / 1e3) / 1e9
+
+    # ---- e2e through the C-ABI from pinned host buffers ----
+    idx_h = [torch.from_numpy(a).pin_memory() for a in c["idx"]]
+    vals_h = torch.from_numpy(c["vals"]).pin_memory()
+    U0_h = [torch.from_numpy(u).pin_memory() for u in c["U0"]]
+    G_h = torch.empty(int(np.prod(core)), dtype=torch.float32).pin_memory()
+    U_h = [torch.empty(u.shape, dtype=torch.float32).pin_memory() for u in U0_h]
+    h2d = sum(a.numel() * 4 for a in idx_h) + vals_h.numel() * 4 + sum(u.numel() * 4 for u in U0_h)
+    d2h = G_h.numel() * 4 + sum(u.numel() * 4 for u in U_h) + 2 * 8
+    e2e_steps = max(1, min(2, args.steps))
+    e2e_ms = []
+    for _ in range(e2e_steps):
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        h2 = capi.tucker_init(dims, core, [a.numpy() for a in idx_h], vals_h.numpy(),
+                              [u.numpy() for u in U0_h], device=local, stream=stream.cuda_stream)
+        capi.hooi_sweep(h2, S)
+        capi.core_and_fit_into(h2, G_h.numpy(), [u.numpy() for u in U_h])
+        capi.tucker_set_factors(h2, [u.numpy() for u in U0_h])
+        capi.mp_sweep(h2, S, want_fit=False)
+        capi.core_and_fit_into(h2, G_h.numpy(), [u.numpy() for u in U_h])
+        e1.record(stream)
+        torch.cuda.synchronize()
+        capi.tucker_free(h2)
+        e2e_ms.append(e0.elapsed_time(e1))
+    e2e_val = units / (statistics.median(e2e_ms) / 1e3) / 1e9 * world
+
+    # ---- roofline of the dominant kernel ----
+    pk = peaks()
+    hflops, mflops = gram_flops(c)
+    gram_ms = (stage_acc[1] + stage_acc_mp[1]) / args.steps
+    gram_path = "simt-fp64" if os.environ.get("TUCKER_GRAM") == "simt" else st.get("gram_path", "simt-fp64")
+    shares = {"spttmc+spmm": (stage_acc[0] + stage_acc_mp[0]) / args.steps,
+              "gram": gram_ms, "eig": (stage_acc[2] + stage_acc_mp[2]) / args.steps,
+              "core+fit": (stage_acc[3] + stage_acc_mp[3]) / args.steps}
+    gram_flops_step = S * (hflops + mflops)
+    achieved = gram_flops_step / (gram_ms / 1e3) / 1e12
+    if gram_path == "tcgen05-3xtf32":
+        peak = pk["bf16_tflops"] * (1.1 / 2.25) / 3.0
+        roof = {"kernel": "gram (tcgen05 3xTF32 SYRK, fp64 drain)", "bound": "tensor",
+                "peak_note": "measured bf16 burst x tf32/bf16 nominal (1.1/2.25) / 3 products"}
+    else:
+        peak = 148 * 64 * 2 * 1.965e9 / 1e12
+        roof = {"kernel": "gram (SIMT fp64 SYRK)", "bound": "alu",
+                "peak_note": "148 SMs x 64 DFMA/clk x 2 x 1.965 GHz (B200_PROFILING nominal clock)"}
+    roof.update({"achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
+                 "traffic": None, "stage_ms_per_step": shares,
+                 "dominant_stage": max(shares, key=shares.get)})
+
+    line = {
+        "metric": "HOOI/MP sweep throughput (nnz x modes per second)",
+        "value": value, "unit": "Gnnz/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32 storage, 3xTF32/f64 Gram, f64 eig",
+        "data": "synthetic",
+        "config": {"workload": c["name"], "l2": "flushed (512 MB write) before every timed step",
+                   "parallelism": f"replicas x{world}"},
+        "hooi_ms_per_sweep": float(stage_acc.sum() / args.steps / S),
+        "mp_ms_per_sweep": float(stage_acc_mp.sum() / args.steps / S),
+        "fit": {"hooi": fits[0], "mp": fits[1]},
+        "csf_build_s": init_s,
+        "gpu_launches": int(st["launches"]) // args.steps,
+        "gpu_launches_note": "library kernel launches per step (tucker_stats)",
+        "e2e": {"value": e2e_val, "unit": "Gnnz/s", "h2d_bytes_per_step": int(h2d),
+                "d2h_bytes_per_step": int(d2h)},
+        "roofline": roof,
+        "clocks": clocks,
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        dt, u = cpu_oracle_sample(c)
+        line["cpu_baseline"] = {"value": u / dt / 1e9, "unit": "Gnnz/s", "cores": cores_used(),
+                                "kind": "oracle",
+                                "sample": "1 HOOI sweep + 1 MP sweep (+ cores) of the same workload"}
+    capi.tucker_free(h)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+    return 0
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -159,7 +159,8 @@ int tucker_debug_eig(tucker_handle* h, int d, int J, const double* S, float* U_o
 
 /* Kernel statistics of the handle since the last reset (for bench/roofline):
  * stats[0] = kernel launches issued by the library, [1] = eigensolver outer
- * iterations, [2] = Chebyshev matvecs, [3] = small (k x k) Jacobi sweeps. */
+ * iterations, [2] = Chebyshev matvecs, [3] = small (k x k) Jacobi sweeps,
+ * [4] = Gram path (0 = tcgen05 3xTF32, 1 = SIMT fp64).  stats has 5 entries. */
 int tucker_stats(tucker_handle* h, int64_t* stats, int reset);
 
 #ifdef __cplusplus

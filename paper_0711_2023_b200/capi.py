@@ -96,7 +96,7 @@ def _ptr(a) -> int:
 
 
 def tucker_init(dims, core, idx, vals, U0, *, device=0, stream=None, eig_oversample=0,
-                eig_max_iter=0, eig_tol=0.0, on_device=False):
+                eig_max_iter=0, eig_tol=0.0, on_device=False, output_on_device=False):
     """Returns an opaque handle (int).  idx: list of N int32 arrays (0-based),
     vals: fp32, U0: list of N fp32 row-major I_n x J_n arrays.  Host numpy
     arrays, or torch CUDA tensors with on_device=True."""
@@ -113,7 +113,8 @@ def tucker_init(dims, core, idx, vals, U0, *, device=0, stream=None, eig_oversam
     o.eig_oversample = eig_oversample
     o.eig_max_iter = eig_max_iter
     o.eig_tol = eig_tol
-    o.flags = TUCKER_INPUT_ON_DEVICE if on_device else 0
+    o.flags = (TUCKER_INPUT_ON_DEVICE if on_device else 0) | (
+        TUCKER_OUTPUT_ON_DEVICE if output_on_device else 0)
     d = (C.c_int64 * N)(*[int(x) for x in dims])
     j = (C.c_int64 * N)(*[int(x) for x in core])
     ip = (C.c_void_p * N)(*[_ptr(a) for a in idx])
@@ -143,6 +144,18 @@ def mp_sweep(h, sweeps, want_fit=True, want_stage=False):
     return (fits, stage.reshape(sweeps, 4), rc) if want_stage else fits
 
 
+def core_and_fit_into(h, core_out, U_out):
+    """core_and_fit writing into caller buffers (numpy or torch, host or device
+    according to the handle's output flag); returns the fit."""
+    N = len(U_out) if U_out is not None else 0
+    up = (C.c_void_p * N)(*[_ptr(u) for u in U_out]) if U_out is not None else None
+    fit = C.c_double()
+    rc = lib().core_and_fit(h, C.c_void_p(_ptr(core_out)) if core_out is not None else None, up,
+                            C.byref(fit))
+    _check(rc, h)
+    return fit.value
+
+
 def core_and_fit(h, dims, core, want_core=True, want_factors=True):
     N = len(dims)
     G = np.zeros(int(np.prod(core)), dtype=np.float32) if want_core else None
@@ -157,8 +170,9 @@ def core_and_fit(h, dims, core, want_core=True, want_factors=True):
 
 
 def tucker_set_factors(h, U):
-    U = [np.ascontiguousarray(u, dtype=np.float32) for u in U]
-    up = (C.c_void_p * len(U))(*[u.ctypes.data for u in U])
+    if not all(hasattr(u, "data_ptr") for u in U):
+        U = [np.ascontiguousarray(u, dtype=np.float32) for u in U]
+    up = (C.c_void_p * len(U))(*[_ptr(u) for u in U])
     _check(lib().tucker_set_factors(h, up), h)
 
 
@@ -191,9 +205,10 @@ def tucker_debug_eig(h, S, J):
 
 
 def tucker_stats(h, reset=False):
-    s = (C.c_int64 * 4)()
+    s = (C.c_int64 * 5)()
     _check(lib().tucker_stats(h, s, 1 if reset else 0), h)
-    return dict(launches=s[0], eig_outer=s[1], eig_matvec=s[2], jacobi_sweeps=s[3])
+    return dict(launches=s[0], eig_outer=s[1], eig_matvec=s[2], jacobi_sweeps=s[3],
+                gram_path="tcgen05-3xtf32" if s[4] == 0 else "simt-fp64")
 
 
 class Tucker:

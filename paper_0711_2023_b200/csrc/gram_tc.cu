@@ -9,4 +9,6 @@ void gram_syrk(const Split& A, double* S, int64_t lds, GramWs& ws, cudaStream_t 
   gram_syrk_simt(A, S, lds, st);
 }
 
+int gram_path_id() { return 1; }
+
 }  // namespace tk

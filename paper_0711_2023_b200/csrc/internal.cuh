@@ -70,7 +70,8 @@ struct GramWs {
 void gram_syrk(const Split& A, double* S, int64_t lds, GramWs& ws, cudaStream_t st);
 // reference SIMT fp64 path (debug/validation of the tensor-core kernel)
 void gram_syrk_simt(const Split& A, double* S, int64_t lds, cudaStream_t st);
-int gram_mode();  // 0 = tcgen05 (default), 1 = SIMT (env TUCKER_GRAM=simt)
+int gram_mode();     // 0 = tcgen05 (default), 1 = SIMT (env TUCKER_GRAM=simt)
+int gram_path_id();  // path gram_syrk takes: 0 = tcgen05 3xTF32, 1 = SIMT fp64
 
 // dense.cu -- small fp64 dense kernels for the eigensolver and the core.
 enum class Elt { F64, F32, SPLIT };

@@ -624,6 +624,7 @@ int tucker_stats(tucker_handle* h, int64_t* stats, int reset) {
   stats[1] = h->eig.stat_outer - h->stat_outer0;
   stats[2] = h->eig.stat_matvec - h->stat_matvec0;
   stats[3] = h->eig.stat_sweeps - h->stat_sweeps0;
+  stats[4] = gram_path_id();
   if (reset) {
     h->launches = 0;
     h->stat_outer0 = h->eig.stat_outer;
