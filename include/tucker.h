@@ -76,7 +76,7 @@ void tucker_default_opts(tucker_opts* opts);
  *   order   N in {3, 4} (MP is defined for orders 3 and 4 only, Figs. 7-8
  *           P:911-1114; SURVEY reading A18).
  *   dims    I_1..I_N, each >= 1 and I_n < 2^31.
- *   core    J_1..J_N, 1 <= J_n <= min(I_n, 128) (this build's eigensolver
+ *   core    J_1..J_N, 1 <= J_n <= min(I_n, 112) (this build's eigensolver
  *           block limit; TUCKER_E_ARG otherwise).
  *   nnz     number of COO entries (>= 1).
  *   idx     N pointers to int32[nnz], 0-based coordinates (any order).
@@ -153,7 +153,7 @@ int tucker_debug_gram(tucker_handle* h, int algo, int mode, double* S_out);
 
 /* Leading-J eigenvectors (descending, sign-canonical, fp32 row-major d x J) and
  * eigenvalues (fp64[J]) of a caller-provided symmetric fp64 d x d matrix, with
- * the library's eigensolver.  1 <= J <= min(d, 128). */
+ * the library's eigensolver.  1 <= J <= min(d, 112). */
 int tucker_debug_eig(tucker_handle* h, int d, int J, const double* S, float* U_out,
                      double* evals_out);
 

@@ -18,26 +18,35 @@ namespace tk {
 namespace {
 
 // ---------------------------------------------------------------- Jacobi ----
-// One CTA.  H (k x k, row-major, ldh) -> V (k x k) eigenvectors in columns and
-// theta (k) eigenvalues, sorted descending.  k even, k <= kMaxBlock.
+// One CTA of 1024 threads.  H (k x k, row-major) -> V (k x k) eigenvectors in
+// columns and theta (k) eigenvalues, sorted descending.  k even, k <= kMaxBlock.
+// Parallel cyclic Jacobi (circle-method tournament: k/2 disjoint rotations per
+// round, k-1 rounds per sweep).  H and V live in shared memory with an odd row
+// stride (k+1) against bank conflicts.  Rotations with
+// |h_pq| <= tol * sqrt(h_pp h_qq) are skipped; the sweep loop stops when a sweep
+// makes no rotation or after max_sweeps (the caller's Ritz residuals decide
+// convergence, so a capped solve only costs another outer iteration).
 __global__ void __launch_bounds__(1024) k_jacobi(const double* __restrict__ Hin, int k,
                                                  double* __restrict__ Vout,
                                                  double* __restrict__ theta, int max_sweeps,
-                                                 int* sweeps_out) {
+                                                 double tol, int* sweeps_out) {
   extern __shared__ double sm[];
-  double* H = sm;          // k*k
-  double* V = sm + k * k;  // k*k
+  const int ld = k + 1;
+  double* H = sm;           // k x ld
+  double* V = sm + k * ld;  // k x ld
   __shared__ double cs_c[kMaxBlock / 2], cs_s[kMaxBlock / 2];
   __shared__ int top[kMaxBlock / 2], bot[kMaxBlock / 2], act[kMaxBlock / 2];
-  __shared__ int pos[kMaxBlock], npos[kMaxBlock];
+  __shared__ int pos[kMaxBlock];
   __shared__ int order[kMaxBlock];
+  __shared__ int bad;
   const int tid = threadIdx.x, nt = blockDim.x;
+  const int warp = tid >> 5, lane = tid & 31;
   const int np = k / 2;
-  for (int e = tid; e < k * k; e += nt) {
-    const int r = e / k, c = e % k;
-    H[e] = 0.5 * (Hin[r * k + c] + Hin[c * k + r]);
-    V[e] = (r == c) ? 1.0 : 0.0;
-  }
+  for (int r = warp; r < k; r += 32)
+    for (int c = lane; c < k; c += 32) {
+      H[r * ld + c] = 0.5 * (Hin[r * k + c] + Hin[c * k + r]);
+      V[r * ld + c] = (r == c) ? 1.0 : 0.0;
+    }
   for (int i = tid; i < k; i += nt) pos[i] = i;
   __syncthreads();
   int sweep = 0;
@@ -49,9 +58,9 @@ __global__ void __launch_bounds__(1024) k_jacobi(const double* __restrict__ Hin,
         const int p = pos[tid], q = pos[k - 1 - tid];
         top[tid] = p;
         bot[tid] = q;
-        const double app = H[p * k + p], aqq = H[q * k + q], apq = H[p * k + q];
+        const double app = H[p * ld + p], aqq = H[q * ld + q], apq = H[p * ld + q];
         double c = 1.0, s = 0.0;
-        if (apq != 0.0 && fabs(apq) > 1e-15 * sqrt(fabs(app * aqq))) {
+        if (fabs(apq) > tol * sqrt(fabs(app * aqq)) && apq != 0.0) {
           const double tau = (aqq - app) / (2.0 * apq);
           const double t = (tau >= 0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(1.0 + tau * tau));
           c = 1.0 / sqrt(1.0 + t * t);
@@ -63,136 +72,137 @@ __global__ void __launch_bounds__(1024) k_jacobi(const double* __restrict__ Hin,
         act[tid] = my_act;
       }
       const int any = __syncthreads_or(my_act);
+      int nextpos = 0;
+      if (tid < k) nextpos = (tid == 0) ? pos[0] : pos[tid == 1 ? k - 1 : tid - 1];
       if (any) {
         any_in_sweep = 1;
-        // two-sided update of every 2x2 block (P <= Q) touched by an active rotation
-        for (int b = tid; b < np * np; b += nt) {
-          const int P = b / np, Q = b % np;
-          if (P > Q || (!act[P] && !act[Q])) continue;
-          const int p1 = top[P], p2 = bot[P], q1 = top[Q], q2 = bot[Q];
-          const double cP = cs_c[P], sP = cs_s[P], cQ = cs_c[Q], sQ = cs_s[Q];
-          if (P == Q) {
-            const double app = H[p1 * k + p1], aqq = H[p2 * k + p2], apq = H[p1 * k + p2];
-            if (act[P]) {
-              const double t = sP / cP;
-              H[p1 * k + p1] = app - t * apq;
-              H[p2 * k + p2] = aqq + t * apq;
-              H[p1 * k + p2] = 0.0;
-              H[p2 * k + p1] = 0.0;
+        // two-sided update of the 2x2 blocks (P <= Q): warp -> P, lane -> Q
+        for (int P = warp; P < np; P += 32) {
+          const int p1 = top[P], p2 = bot[P];
+          const double cP = cs_c[P], sP = cs_s[P];
+          const int aP = act[P];
+          for (int Q = lane; Q < np; Q += 32) {
+            if (Q < P || (!aP && !act[Q])) continue;
+            if (Q == P) {
+              if (aP) {
+                const double apq = H[p1 * ld + p2];
+                const double t = sP / cP;
+                H[p1 * ld + p1] -= t * apq;
+                H[p2 * ld + p2] += t * apq;
+                H[p1 * ld + p2] = 0.0;
+                H[p2 * ld + p1] = 0.0;
+              }
+              continue;
             }
-            continue;
+            const int q1 = top[Q], q2 = bot[Q];
+            const double cQ = cs_c[Q], sQ = cs_s[Q];
+            const double b11 = H[p1 * ld + q1], b12 = H[p1 * ld + q2];
+            const double b21 = H[p2 * ld + q1], b22 = H[p2 * ld + q2];
+            const double r11 = cP * b11 - sP * b21, r12 = cP * b12 - sP * b22;
+            const double r21 = sP * b11 + cP * b21, r22 = sP * b12 + cP * b22;
+            const double n11 = r11 * cQ - r12 * sQ, n12 = r11 * sQ + r12 * cQ;
+            const double n21 = r21 * cQ - r22 * sQ, n22 = r21 * sQ + r22 * cQ;
+            H[p1 * ld + q1] = n11; H[q1 * ld + p1] = n11;
+            H[p1 * ld + q2] = n12; H[q2 * ld + p1] = n12;
+            H[p2 * ld + q1] = n21; H[q1 * ld + p2] = n21;
+            H[p2 * ld + q2] = n22; H[q2 * ld + p2] = n22;
           }
-          double b11 = H[p1 * k + q1], b12 = H[p1 * k + q2];
-          double b21 = H[p2 * k + q1], b22 = H[p2 * k + q2];
-          // rows: J_P^T
-          double r11 = cP * b11 - sP * b21, r12 = cP * b12 - sP * b22;
-          double r21 = sP * b11 + cP * b21, r22 = sP * b12 + cP * b22;
-          // cols: J_Q
-          b11 = r11 * cQ - r12 * sQ;
-          b12 = r11 * sQ + r12 * cQ;
-          b21 = r21 * cQ - r22 * sQ;
-          b22 = r21 * sQ + r22 * cQ;
-          H[p1 * k + q1] = b11; H[q1 * k + p1] = b11;
-          H[p1 * k + q2] = b12; H[q2 * k + p1] = b12;
-          H[p2 * k + q1] = b21; H[q1 * k + p2] = b21;
-          H[p2 * k + q2] = b22; H[q2 * k + p2] = b22;
         }
-        for (int e = tid; e < np * k; e += nt) {
-          const int P = e / k, r = e % k;
+        // V <- V J: warp -> pair P, lane -> rows
+        for (int P = warp; P < np; P += 32) {
           if (!act[P]) continue;
           const int p1 = top[P], p2 = bot[P];
           const double c = cs_c[P], s = cs_s[P];
-          const double x = V[r * k + p1], y = V[r * k + p2];
-          V[r * k + p1] = x * c - y * s;
-          V[r * k + p2] = x * s + y * c;
+          for (int r = lane; r < k; r += 32) {
+            const double x = V[r * ld + p1], y = V[r * ld + p2];
+            V[r * ld + p1] = x * c - y * s;
+            V[r * ld + p2] = x * s + y * c;
+          }
         }
       }
       __syncthreads();
-      // circle-method tournament: keep pos[0], rotate the rest
-      if (tid < k) npos[tid] = (tid == 0) ? pos[0] : pos[tid == 1 ? k - 1 : tid - 1];
-      __syncthreads();
-      if (tid < k) pos[tid] = npos[tid];
+      if (tid < k) pos[tid] = nextpos;  // circle-method tournament: keep pos[0], rotate the rest
       __syncthreads();
     }
     if (!any_in_sweep) break;
   }
-  // sort eigenvalues descending (stable by index): rank of each diagonal entry
-  __shared__ int bad;
+  // sort eigenvalues descending (stable by index)
   if (tid == 0) bad = 0;
   if (tid < k) order[tid] = tid;
   __syncthreads();
-  if (tid < k && !isfinite(H[tid * k + tid])) atomicOr(&bad, 1);
+  if (tid < k && !isfinite(H[tid * ld + tid])) atomicOr(&bad, 1);
   __syncthreads();
   if (tid < k && !bad) {
-    const double d = H[tid * k + tid];
+    const double d = H[tid * ld + tid];
     int rank = 0;
     for (int j = 0; j < k; ++j) {
-      const double e = H[j * k + j];
+      const double e = H[j * ld + j];
       rank += (e > d) || (e == d && j < tid);
     }
     order[rank] = tid;
   }
   __syncthreads();
-  for (int e = tid; e < k * k; e += nt) {
-    const int r = e / k, c = e % k;
-    Vout[r * k + c] = V[r * k + order[c]];
-  }
-  if (tid < k) theta[tid] = H[order[tid] * k + order[tid]];
+  for (int r = warp; r < k; r += 32)
+    for (int c = lane; c < k; c += 32) Vout[r * k + c] = V[r * ld + order[c]];
+  if (tid < k) theta[tid] = H[order[tid] * ld + order[tid]];
   if (tid == 0 && sweeps_out) *sweeps_out = bad ? -1 : sweep;
 }
 
 // ------------------------------------------------------- Cholesky / inverse --
-// One CTA.  G (k x k SPD) -> Rinv (k x k upper triangular) with G = R^T R.
-__global__ void __launch_bounds__(1024) k_chol_inv(const double* __restrict__ G, int k,
+// One CTA of 256 threads.  G (k x k SPD, equilibrated to unit diagonal first,
+// plus `shift` on the diagonal) -> Rinv (k x k upper) with D G D + shift I = R^T R
+// and Rinv = D R^{-1}, so Y Rinv has orthonormal columns when G = Y^T Y.
+__global__ void __launch_bounds__(256) k_chol_inv(const double* __restrict__ G, int k,
                                                    double* __restrict__ Rinv, double shift) {
   extern __shared__ double sm[];
-  double* A = sm;  // k*k
-  const int tid = threadIdx.x, nt = blockDim.x;
-  __shared__ double maxd;
+  const int ld = k + 1;
+  double* A = sm;           // k x ld : R (upper)
+  double* X = sm + k * ld;  // k x ld : R^{-1}
   __shared__ double dsc[kMaxBlock];
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const int warp = tid >> 5, lane = tid & 31;
   for (int i = tid; i < k; i += nt) {
     const double g = G[i * k + i];
     dsc[i] = g > 0 ? 1.0 / sqrt(g) : 1.0;
   }
   __syncthreads();
-  for (int e = tid; e < k * k; e += nt)
-    A[e] = G[e] * dsc[e / k] * dsc[e % k] + ((e / k == e % k) ? shift : 0.0);
-  __syncthreads();
-  if (tid == 0) maxd = 1.0;
-  __syncthreads();
-  for (int j = 0; j < k; ++j) {
-    if (tid == 0) {
-      double d = A[j * k + j];
-      const double floor = 1e-12 * maxd;
-      A[j * k + j] = sqrt(d > floor ? d : floor);
+  for (int r = warp; r < k; r += (nt >> 5))
+    for (int c = lane; c < k; c += 32) {
+      A[r * ld + c] = G[r * k + c] * dsc[r] * dsc[c] + (r == c ? shift : 0.0);
+      X[r * ld + c] = 0.0;
     }
+  __syncthreads();
+  // right-looking Cholesky, upper triangle: row j of R = row j / sqrt(pivot)
+  for (int j = 0; j < k; ++j) {
+    const double dj = A[j * ld + j];
+    const double piv = sqrt(dj > 1e-12 ? dj : 1e-12);
     __syncthreads();
-    const double piv = A[j * k + j];
-    for (int l = j + 1 + tid; l < k; l += nt) A[j * k + l] /= piv;
+    for (int l = j + tid; l < k; l += nt) A[j * ld + l] = (l == j) ? piv : A[j * ld + l] / piv;
     __syncthreads();
     const int w = k - j - 1;
-    for (int e = tid; e < w * w; e += nt) {
-      const int l = j + 1 + e / w, m = j + 1 + e % w;
-      if (m >= l) A[l * k + m] -= A[j * k + l] * A[j * k + m];
+    // trailing update of the upper triangle: warp -> rows, lane -> cols
+    for (int l = j + 1 + warp; l < k; l += (nt >> 5)) {
+      const double ajl = A[j * ld + l];
+      for (int m = l + lane; m < k; m += 32) A[l * ld + m] -= ajl * A[j * ld + m];
     }
+    (void)w;
     __syncthreads();
   }
-  // R = upper(A).  Solve R X = I column by column (thread c owns column c).
-  for (int c = tid; c < k; c += nt) {
-    for (int i = k - 1; i >= 0; --i) {
-      double x;
-      if (i > c) {
-        x = 0.0;
-      } else {
-        double s = (i == c) ? 1.0 : 0.0;
-        for (int l = i + 1; l <= c; ++l) s -= A[i * k + l] * Rinv[l * k + c];
-        x = s / A[i * k + i];
-      }
-      Rinv[i * k + c] = x;
-    }
+  // X = R^{-1}, rows from the bottom: X[i][j] = -(1/R_ii) sum_{l=i+1..j} R[i][l] X[l][j].
+  // 2 threads per column j (k <= 116 <= 128 columns), shuffle-reduced.
+  for (int i = k - 1; i >= 0; --i) {
+    const double rii = A[i * ld + i];
+    const int j = i + (tid >> 1);
+    const int sub = tid & 1;
+    double s = 0.0;
+    if (j < k && j > i)
+      for (int l = i + 1 + sub; l <= j; l += 2) s += A[i * ld + l] * X[l * ld + j];
+    s += __shfl_xor_sync(0xffffffffu, s, 1);
+    if (sub == 0 && j < k) X[i * ld + j] = (j == i) ? 1.0 / rii : -s / rii;
+    __syncthreads();
   }
-  __syncthreads();
-  for (int e = tid; e < k * k; e += nt) Rinv[e] *= dsc[e / k];
+  for (int r = warp; r < k; r += (nt >> 5))
+    for (int c = lane; c < k; c += 32) Rinv[r * k + c] = dsc[r] * X[r * ld + c];
 }
 
 __global__ void k_count_nonfinite(const double* x, int64_t n, int* out) {
@@ -318,10 +328,10 @@ int choose_block(int J, int64_t d, int oversample) {
 
 // Q (d x k) <- Q R^{-1} twice (CholQR2)
 void cholqr2_impl(double* Q, int64_t d, int k, EigWs& ws, cudaStream_t st) {
-  const size_t smem = (size_t)k * k * sizeof(double);
+  const size_t smem = (size_t)2 * k * (k + 1) * sizeof(double);
   for (int pass = 0; pass < 2; ++pass) {
     dgemm(k, k, d, 1.0, f64(Q, k, true), f64(Q, k), 0.0, ws.H.p, k, 0.0, nullptr, 0, ws.dense, st);
-    TK_LAUNCH(k_chol_inv, 1, 512, smem, st, ws.H.p, k, ws.R.p, 0.0);
+    TK_LAUNCH(k_chol_inv, 1, 256, smem, st, ws.H.p, k, ws.R.p, 0.0);
     dgemm(d, k, k, 1.0, f64(Q, k), f64(ws.R.p, k), 0.0, ws.T.p, k, 0.0, nullptr, 0, ws.dense, st);
     TK_LAUNCH(k_copy_cols, grid_for(d * k), 256, 0, st, ws.T.p, (int64_t)k, Q, (int64_t)k, d, k);
   }
@@ -349,9 +359,9 @@ bool eig_leading(const double* S, int64_t lds, int64_t d, int J, EigSlot& slot, 
   static bool attr_set = false;
   if (!attr_set) {
     TK_CUDA(cudaFuncSetAttribute(k_jacobi, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 2 * kMaxBlock * kMaxBlock * (int)sizeof(double)));
+                                 2 * kMaxBlock * (kMaxBlock + 1) * (int)sizeof(double)));
     TK_CUDA(cudaFuncSetAttribute(k_chol_inv, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 kMaxBlock * kMaxBlock * (int)sizeof(double) + 1024));
+                                 2 * kMaxBlock * (kMaxBlock + 1) * (int)sizeof(double)));
     attr_set = true;
   }
   if (lds != d) fail(TUCKER_E_ARG, "eig_leading: lds must equal d");
@@ -405,14 +415,14 @@ bool eig_leading(const double* S, int64_t lds, int64_t d, int J, EigSlot& slot, 
               ws.dense, st);
       }
     }
-    const size_t smem = (size_t)ka * ka * sizeof(double);
+    const size_t smem = (size_t)2 * ka * (ka + 1) * sizeof(double);
     // shifted CholQR3 (first pass shifted so the factorisation cannot break down)
     const double shift = 11.0 * ((double)d * ka + (double)ka * (ka + 1)) * 1.1e-16 * ka;
     for (int pass = 0; pass < 3; ++pass) {
       dgemm(ka, ka, d, 1.0, f64(ws.Q.p, ka, true), f64(ws.Q.p, ka), 0.0, ws.H.p, ka, 0.0, nullptr,
             0, ws.dense, st);
       nonfinite(ws.H.p, (int64_t)ka * ka, "gram-in-orth");
-      TK_LAUNCH(k_chol_inv, 1, 512, smem, st, ws.H.p, ka, ws.R.p, pass == 0 ? shift : 0.0);
+      TK_LAUNCH(k_chol_inv, 1, 256, smem, st, ws.H.p, ka, ws.R.p, pass == 0 ? shift : 0.0);
       nonfinite(ws.R.p, (int64_t)ka * ka, "Rinv");
       dgemm(d, ka, ka, 1.0, f64(ws.Q.p, ka), f64(ws.R.p, ka), 0.0, ws.T.p, ka, 0.0, nullptr, 0,
             ws.dense, st);
@@ -438,8 +448,9 @@ bool eig_leading(const double* S, int64_t lds, int64_t d, int J, EigSlot& slot, 
     dgemm(ka, ka, d, 1.0, f64(ws.Q.p, ka, true), f64(ws.SQ.p, ka), 0.0, ws.H.p, ka, 0.0, nullptr,
           0, ws.dense, st);
     nonfinite(ws.H.p, (int64_t)ka * ka, "H");
-    TK_LAUNCH(k_jacobi, 1, 1024, (size_t)2 * ka * ka * sizeof(double), st, ws.H.p, ka, ws.V.p,
-              ws.theta.p, 40, ws.dsweeps.p);
+    TK_LAUNCH(k_jacobi, 1, 1024, (size_t)2 * ka * (ka + 1) * sizeof(double), st, ws.H.p, ka,
+              ws.V.p, ws.theta.p, k == d ? 60 : o.jacobi_sweeps, k == d ? 1e-15 : 1e-13,
+              ws.dsweeps.p);
     dgemm(d, ka, ka, 1.0, f64(ws.Q.p, ka), f64(ws.V.p, ka), 0.0, ws.T.p, ka, 0.0, nullptr, 0,
           ws.dense, st);
     std::swap(ws.Q, ws.T);

@@ -1,14 +1,347 @@
-// gram_tc.cu -- S = A A^T dispatch.  The tcgen05 3xTF32 kernel lands here;
-// until it is validated the dispatcher uses the SIMT fp64 kernel.
+// gram_tc.cu -- S = A A^T on the 5th-generation tensor cores (tcgen05, sm_100a).
+//
+// Fig. 4 P:624-625 (S = Z_(n) Z_(n)^T) and Fig. 7/8 M_n = sum_s P_s P_s^T
+// (= W W^T): both are SYRKs of a split-fp32 operand A (d x K, K contiguous).
+//
+// 3xTF32: a = hi + lo with hi = tf32(a), lo = tf32(a - hi) (spttmc.cu writes
+// both), and a.b ~= hi.hi + hi.lo + lo.hi -- three kind::tf32 MMAs per K-step,
+// fp32 accumulation in TMEM.  Every K-tile (32 products) the fp32 partial is
+// drained from TMEM into fp64 registers (fp32 accumulation over the
+// full K fails MP parity), double-buffered so the tensor core keeps running.
+//
+// CTA = one 128x128 upper-triangle tile (bi <= bj) x one K-split; warp roles:
+//   warp 0      TMA producer (cp.async.bulk.tensor, 128B swizzle, 3-stage ring)
+//   warp 1      TMEM allocator + single-thread tcgen05.mma issuer
+//   warps 2..9  epilogue: tcgen05.ld -> fp64 accumulate -> fp64 partial tile
+// A second kernel sums the K-split partials in a fixed order (deterministic)
+// and mirrors the tile into both triangles of S.
+#include <cuda.h>
+
+#include <cstdlib>
+#include <cstring>
+#include <vector>
+
 #include "internal.cuh"
 
 namespace tk {
+namespace {
 
-void gram_syrk(const Split& A, double* S, int64_t lds, GramWs& ws, cudaStream_t st) {
-  (void)ws;
-  gram_syrk_simt(A, S, lds, st);
+constexpr int TM = 128;                 // tile rows (UMMA M)
+constexpr int TN = 128;                 // tile cols (UMMA N)
+constexpr int TKE = 32;                 // K elements per stage (128 B of fp32 -> one swizzle atom)
+constexpr int STAGES = 3;
+constexpr int OPB = TM * TKE * 4;       // bytes of one operand tile (16 KB)
+constexpr int STAGE_BYTES = 4 * OPB;    // A_hi, A_lo, B_hi, B_lo
+constexpr int NUM_THREADS = 320;        // 10 warps
+constexpr int TMEM_COLS = 256;          // two 128-column fp32 accumulators
+constexpr uint32_t IDESC =
+    (1u << 4) |               // D format: F32
+    (2u << 7) | (2u << 10) |  // A, B format: TF32
+    (0u << 15) | (0u << 16) | // A, B K-major
+    ((uint32_t)(TN >> 3) << 17) | ((uint32_t)(TM >> 4) << 24);
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t n) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(n));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(b)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0,
+                                            int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, "
+      "%3}], [%4];" ::"r"(smem_u32(dst)),
+      "l"((uint64_t)map), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      : "memory");
+}
+// K-major, 128B-swizzled smem matrix descriptor (rows of 128 B, 8-row atoms 1024 B apart)
+__device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
+  return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)1 << 16) | ((uint64_t)(1024 >> 4) << 32) |
+         ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
+}
+__device__ __forceinline__ void umma_tf32(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t acc) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(tmem_d),
+      "l"(a), "l"(b), "r"(IDESC), "r"(acc));
+}
+__device__ __forceinline__ void umma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                   smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
+  uint32_t r[32];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, "
+      "%12, %13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, "
+      "%30, %31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]),
+        "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]),
+        "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+
+struct SyrkArgs {
+  const int2* tiles;   // (bi, bj), bi <= bj
+  int ntiles;
+  int nkt;             // K-tiles in A
+  int kt_per_split;
+  double* partial;     // [split][tile][128][128]
+};
+
+__global__ void __launch_bounds__(NUM_THREADS, 1)
+    k_syrk_tc(const __grid_constant__ CUtensorMap map_hi, const __grid_constant__ CUtensorMap map_lo,
+              SyrkArgs p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  __shared__ __align__(8) uint64_t full_bar[STAGES], empty_bar[STAGES];
+  __shared__ __align__(8) uint64_t tfull_bar[2], tempty_bar[2];
+  __shared__ uint32_t tmem_base_slot;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int tile = blockIdx.x % p.ntiles;
+  const int split = blockIdx.x / p.ntiles;
+  const int2 bij = p.tiles[tile];
+  const bool diag = bij.x == bij.y;
+  const int kt0 = split * p.kt_per_split;
+  const int kt1 = min(p.nkt, kt0 + p.kt_per_split);
+  const int nk = max(0, kt1 - kt0);
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full_bar[s], 1);
+      mbar_init(&empty_bar[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&tfull_bar[b], 1);
+      mbar_init(&tempty_bar[b], 256);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(&tmem_base_slot)),
+                 "r"(TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = tmem_base_slot;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ producer
+    if (lane == 0) {
+      for (int i = 0; i < nk; ++i) {
+        const int s = i % STAGES;
+        const uint32_t ph = (uint32_t)((i / STAGES) & 1);
+        mbar_wait(&empty_bar[s], ph ^ 1);
+        uint8_t* st = smem + s * STAGE_BYTES;
+        const int kcol = (kt0 + i) * TKE;
+        mbar_expect_tx(&full_bar[s], diag ? 2 * OPB : 4 * OPB);
+        tma_load_2d(st, &map_hi, &full_bar[s], kcol, bij.x * TM);
+        tma_load_2d(st + OPB, &map_lo, &full_bar[s], kcol, bij.x * TM);
+        if (!diag) {
+          tma_load_2d(st + 2 * OPB, &map_hi, &full_bar[s], kcol, bij.y * TM);
+          tma_load_2d(st + 3 * OPB, &map_lo, &full_bar[s], kcol, bij.y * TM);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer
+    if (lane == 0) {
+      for (int i = 0; i < nk; ++i) {
+        const int s = i % STAGES;
+        const uint32_t ph = (uint32_t)((i / STAGES) & 1);
+        const int b = i & 1;
+        mbar_wait(&tempty_bar[b], (uint32_t)(((i >> 1) & 1) ^ 1));
+        mbar_wait(&full_bar[s], ph);
+        tc_fence_after();
+        const uint32_t base = smem_u32(smem + s * STAGE_BYTES);
+        const uint32_t ahi = base, alo = base + OPB;
+        const uint32_t bhi = diag ? ahi : base + 2 * OPB, blo = diag ? alo : base + 3 * OPB;
+        const uint32_t d = tmem_base + (uint32_t)(b * TN);
+#pragma unroll
+        for (int k = 0; k < TKE / 8; ++k) {
+          const uint32_t off = (uint32_t)(k * 32);  // 8 tf32 = 32 bytes along K inside the atom
+          umma_tf32(d, sw128_desc(ahi + off), sw128_desc(bhi + off), k > 0 ? 1u : 0u);
+          umma_tf32(d, sw128_desc(ahi + off), sw128_desc(blo + off), 1u);
+          umma_tf32(d, sw128_desc(alo + off), sw128_desc(bhi + off), 1u);
+        }
+        umma_commit(&empty_bar[s]);   // smem stage free once these MMAs complete
+        umma_commit(&tfull_bar[b]);   // fp32 partial of this K-tile ready in TMEM
+      }
+    }
+  } else {
+    // ------------------------------------------------------------ epilogue
+    const int g = warp & 3;              // TMEM lane group this warp may access
+    const int half = (warp - 2) >> 2;    // column half: 0 -> cols 0..63, 1 -> 64..127
+    double acc[64];
+#pragma unroll
+    for (int j = 0; j < 64; ++j) acc[j] = 0.0;
+    for (int i = 0; i < nk; ++i) {
+      const int b = i & 1;
+      mbar_wait(&tfull_bar[b], (uint32_t)((i >> 1) & 1));
+      tc_fence_after();
+      const uint32_t taddr = tmem_base + ((uint32_t)(32 * g) << 16) + (uint32_t)(b * TN + 64 * half);
+      float v0[32], v1[32];
+      tmem_ld32(taddr, v0);
+      tmem_ld32(taddr + 32, v1);
+      tmem_wait_ld();
+      tc_fence_before();
+      mbar_arrive(&tempty_bar[b]);
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        acc[j] += (double)v0[j];
+        acc[32 + j] += (double)v1[j];
+      }
+    }
+    // fp64 partial tile: row = 32 g + lane, cols 64 half + j
+    double* out = p.partial + ((int64_t)split * p.ntiles + tile) * (TM * TN) +
+                  (int64_t)(32 * g + lane) * TN + 64 * half;
+#pragma unroll
+    for (int j = 0; j < 64; j += 2) *reinterpret_cast<double2*>(out + j) = make_double2(acc[j], acc[j + 1]);
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 1)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                 "r"(TMEM_COLS));
 }
 
-int gram_path_id() { return 1; }
+// S[i][j] = S[j][i] = sum_z partial[z][t][r][c] (fixed order); diagonal tiles r <= c only
+__global__ void k_syrk_reduce(const double* __restrict__ partial, const int2* __restrict__ tiles,
+                              int ntiles, int splits, int64_t d, double* __restrict__ S,
+                              int64_t lds) {
+  const int t = blockIdx.y;
+  const int2 bij = tiles[t];
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < TM * TN; e += gridDim.x * blockDim.x) {
+    const int r = e / TN, c = e % TN;
+    if (bij.x == bij.y && r > c) continue;
+    const int64_t i = (int64_t)bij.x * TM + r, j = (int64_t)bij.y * TN + c;
+    if (i >= d || j >= d) continue;
+    double s = 0.0;
+    for (int z = 0; z < splits; ++z) s += partial[((int64_t)z * ntiles + t) * (TM * TN) + e];
+    S[i * lds + j] = s;
+    S[j * lds + i] = s;
+  }
+}
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                  const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                  const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    TK_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q));
+    if (!p || q != cudaDriverEntryPointSuccess)
+      fail(TUCKER_E_CUDA, "cuTensorMapEncodeTiled entry point unavailable");
+    fn = (EncodeTiledFn)p;
+  }
+  return fn;
+}
+
+CUtensorMap make_map(const float* base, int64_t rows_pad, int64_t ld) {
+  CUtensorMap m;
+  std::memset(&m, 0, sizeof(m));
+  const cuuint64_t gdim[2] = {(cuuint64_t)ld, (cuuint64_t)rows_pad};
+  const cuuint64_t gstride[1] = {(cuuint64_t)(ld * 4)};
+  const cuuint32_t box[2] = {(cuuint32_t)TKE, (cuuint32_t)TM};
+  const cuuint32_t estr[2] = {1, 1};
+  const CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, (void*)base, gdim, gstride,
+                                 box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                 CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) fail(TUCKER_E_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
+  return m;
+}
+
+}  // namespace
+
+void gram_syrk_tc(const Split& A, double* S, int64_t lds, GramWs& ws, cudaStream_t st) {
+  static bool attr = false;
+  const int smem_bytes = STAGES * STAGE_BYTES + 1024;
+  if (!attr) {
+    TK_CUDA(cudaFuncSetAttribute(k_syrk_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes));
+    attr = true;
+  }
+  const int64_t d = A.rows;
+  const int64_t rows_pad = round_up(d, TM);
+  if (A.ld % TKE != 0) fail(TUCKER_E_ARG, "gram_syrk_tc: ld must be a multiple of 32");
+  const int nb = (int)(rows_pad / TM);
+  const int ntiles = nb * (nb + 1) / 2;
+  const int nkt = (int)(A.ld / TKE);
+  std::vector<int2> tiles;
+  tiles.reserve(ntiles);
+  for (int i = 0; i < nb; ++i)
+    for (int j = i; j < nb; ++j) tiles.push_back(make_int2(i, j));
+  // K-splits so that tiles x splits fills the 148 SMs (>= 4 K-tiles per CTA)
+  int splits = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(148, ntiles), nkt / 4));
+  const int kt_per = (int)ceil_div(nkt, splits);
+  splits = (int)ceil_div(nkt, kt_per);
+  ws.scratch.ensure(sizeof(int2) * tiles.size());
+  TK_CUDA(cudaMemcpyAsync(ws.scratch.p, tiles.data(), sizeof(int2) * tiles.size(),
+                          cudaMemcpyHostToDevice, st));
+  ws.partial.ensure((size_t)splits * ntiles * TM * TN);
+  const CUtensorMap mhi = make_map(A.hi, rows_pad, A.ld);
+  const CUtensorMap mlo = make_map(A.lo, rows_pad, A.ld);
+  SyrkArgs a;
+  a.tiles = (const int2*)ws.scratch.p;
+  a.ntiles = ntiles;
+  a.nkt = nkt;
+  a.kt_per_split = kt_per;
+  a.partial = ws.partial.p;
+  TK_LAUNCH(k_syrk_tc, (unsigned)(ntiles * splits), NUM_THREADS, (size_t)smem_bytes, st, mhi, mlo, a);
+  TK_LAUNCH(k_syrk_reduce, dim3(16, (unsigned)ntiles), 256, 0, st, (const double*)ws.partial.p,
+            (const int2*)ws.scratch.p, ntiles, splits, d, S, lds);
+}
+
+void gram_syrk(const Split& A, double* S, int64_t lds, GramWs& ws, cudaStream_t st) {
+  if (gram_mode() == 1) {
+    gram_syrk_simt(A, S, lds, st);
+  } else {
+    gram_syrk_tc(A, S, lds, ws, st);
+  }
+}
+
+int gram_path_id() { return gram_mode(); }
 
 }  // namespace tk

@@ -7,7 +7,7 @@
 namespace tk {
 
 constexpr int kMaxOrder = 4;
-constexpr int kMaxJ = 128;       // per-mode core size limit of this build
+constexpr int kMaxJ = 112;       // per-mode core size limit of this build (eigensolver block <= 116)
 constexpr int kMaxBlock = 116;   // eigensolver block size k limit (Jacobi in shared memory)
 
 // ---------------------------------------------------------------------------
@@ -109,6 +109,7 @@ struct EigWs {
 struct EigOpts {
   int oversample = 0;
   int max_outer = 40;
+  int jacobi_sweeps = 2;  // cap per Rayleigh-Ritz step (residuals decide convergence)
   double tol = 1e-11;
 };
 // Leading J eigenvectors of symmetric PSD S (d x d, lds): out_V (d x ldv fp64 row-major)
