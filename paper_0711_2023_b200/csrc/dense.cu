@@ -40,6 +40,9 @@ struct GemmArgs {
   int64_t ldc;
   const double* D;
   int64_t ldd;
+  double delta;
+  const double* E;
+  int64_t lde;
   double* part;  // split-K partials [splits][M][N] or null
   int64_t kchunk;
 };
@@ -107,6 +110,7 @@ __global__ void __launch_bounds__(256) k_dgemm(GemmArgs g) {
         double c = g.alpha * acc[i][j];
         if (g.beta != 0.0) c += g.beta * g.C[m * g.ldc + n];
         if (g.gamma != 0.0) c += g.gamma * g.D[m * g.ldd + n];
+        if (g.delta != 0.0) c += g.delta * g.E[m * g.lde + n];
         g.C[m * g.ldc + n] = c;
       }
     }
@@ -114,7 +118,8 @@ __global__ void __launch_bounds__(256) k_dgemm(GemmArgs g) {
 
 __global__ void k_splitk_reduce(int64_t M, int64_t N, int splits, const double* __restrict__ part,
                                 double alpha, double beta, double* C, int64_t ldc, double gamma,
-                                const double* D, int64_t ldd) {
+                                const double* D, int64_t ldd, double delta, const double* E,
+                                int64_t lde) {
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < M * N;
        e += (int64_t)gridDim.x * blockDim.x) {
     const int64_t m = e / N, n = e % N;
@@ -123,8 +128,105 @@ __global__ void k_splitk_reduce(int64_t M, int64_t N, int splits, const double* 
     double c = alpha * s;
     if (beta != 0.0) c += beta * C[m * ldc + n];
     if (gamma != 0.0) c += gamma * D[m * ldd + n];
+    if (delta != 0.0) c += delta * E[m * lde + n];
     C[m * ldc + n] = c;
   }
+}
+
+
+// ---------------------------------------------------------------------------
+// NN fast path for the eigensolver's tall products C (M x N) = A (M x K) B (K x N),
+// fp64 row-major, N <= 128: CTA tile 64 x BN (BN = 32 * NC), BK = 16, 256 threads,
+// 8 rows x NC cols per thread, double-buffered cp.async staging.  Split-K over
+// blockIdx.z writes partials (reduced in a fixed order by k_splitk_reduce).
+// ---------------------------------------------------------------------------
+constexpr int NBM = 64, NBK = 16;
+
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem, bool pred) {
+  const uint32_t s = (uint32_t)__cvta_generic_to_shared(smem);
+  const int n = pred ? 8 : 0;
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(s), "l"(gmem), "r"(n));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;"); }
+__device__ __forceinline__ void cp_async_wait0() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+
+template <int NC>
+__global__ void __launch_bounds__(256) k_dgemm_nn(GemmArgs g) {
+  constexpr int BN = 32 * NC;
+  __shared__ __align__(16) double As[2][NBK][NBM];
+  __shared__ __align__(16) double Bs[2][NBK][BN];
+  const int tid = threadIdx.x, tx = tid & 31, ty = tid >> 5;
+  const int64_t m0 = (int64_t)blockIdx.y * NBM;
+  const int64_t kb = (int64_t)blockIdx.z * g.kchunk;
+  const int64_t ke = min(g.K, kb + g.kchunk);
+  const double* A = (const double*)g.A.p;
+  const double* B = (const double*)g.B.p;
+  auto load = [&](int buf, int64_t k0) {
+    // A tile 64 x 16 (row-major along K) -> As[k][m]
+#pragma unroll
+    for (int t = 0; t < (NBM * NBK) / 256; ++t) {
+      const int e = tid + 256 * t;
+      const int kk = e % NBK, mm = e / NBK;
+      const int64_t m = m0 + mm, k = k0 + kk;
+      const bool ok = m < g.M && k < ke;
+      cp_async8(&As[buf][kk][mm], ok ? A + m * g.A.ld + k : A, ok);
+    }
+#pragma unroll
+    for (int t = 0; t < (BN * NBK) / 256; ++t) {
+      const int e = tid + 256 * t;
+      const int nn = e % BN, kk = e / BN;
+      const int64_t k = k0 + kk;
+      const bool ok = nn < g.N && k < ke;
+      cp_async8(&Bs[buf][kk][nn], ok ? B + k * g.B.ld + nn : B, ok);
+    }
+    cp_async_commit();
+  };
+  double acc[8][NC];
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int j = 0; j < NC; ++j) acc[i][j] = 0.0;
+  int buf = 0;
+  if (kb < ke) load(0, kb);
+  for (int64_t k0 = kb; k0 < ke; k0 += NBK) {
+    cp_async_wait0();
+    __syncthreads();
+    if (k0 + NBK < ke) load(buf ^ 1, k0 + NBK);
+#pragma unroll
+    for (int kk = 0; kk < NBK; ++kk) {
+      double a[8], b[NC];
+      const double2* ap = reinterpret_cast<const double2*>(&As[buf][kk][ty * 8]);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const double2 v = ap[i];
+        a[2 * i] = v.x;
+        a[2 * i + 1] = v.y;
+      }
+#pragma unroll
+      for (int j = 0; j < NC; ++j) b[j] = Bs[buf][kk][tx + 32 * j];
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < NC; ++j) acc[i][j] = fma(a[i], b[j], acc[i][j]);
+    }
+    buf ^= 1;
+  }
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int j = 0; j < NC; ++j) {
+      const int64_t m = m0 + ty * 8 + i, n = tx + 32 * j;
+      if (m >= g.M || n >= g.N) continue;
+      if (g.part) {
+        g.part[((int64_t)blockIdx.z * g.M + m) * g.N + n] = acc[i][j];
+      } else {
+        double c = g.alpha * acc[i][j];
+        if (g.beta != 0.0) c += g.beta * g.C[m * g.ldc + n];
+        if (g.gamma != 0.0) c += g.gamma * g.D[m * g.ldd + n];
+        if (g.delta != 0.0) c += g.delta * g.E[m * g.lde + n];
+        g.C[m * g.ldc + n] = c;
+      }
+    }
 }
 
 template <Elt EA, Elt EB>
@@ -162,11 +264,46 @@ __global__ void k_sum_parts(const double* part, int n, double* out) {
 void dgemm(int64_t M, int64_t N, int64_t K, double alpha, MatRef A, MatRef B, double beta,
            double* C, int64_t ldc, double gamma, const double* D, int64_t ldd, DenseWs& ws,
            cudaStream_t st) {
+  dgemm4(M, N, K, alpha, A, B, beta, C, ldc, gamma, D, ldd, 0.0, nullptr, 0, ws, st);
+}
+
+void dgemm4(int64_t M, int64_t N, int64_t K, double alpha, MatRef A, MatRef B, double beta,
+            double* C, int64_t ldc, double gamma, const double* D, int64_t ldd, double delta,
+            const double* E, int64_t lde, DenseWs& ws, cudaStream_t st) {
   if (M <= 0 || N <= 0) return;
   GemmArgs g;
   g.M = M; g.N = N; g.K = K; g.A = A; g.B = B;
   g.alpha = alpha; g.beta = beta; g.gamma = gamma;
   g.C = C; g.ldc = ldc; g.D = D; g.ldd = ldd;
+  g.delta = delta; g.E = E; g.lde = lde;
+  const bool nn_fast = A.t == Elt::F64 && B.t == Elt::F64 && !A.trans && !B.trans && N <= 128 &&
+                       M >= 64 && K > 0;
+  if (nn_fast) {
+    const int NC = (int)ceil_div(N, 32);
+    const int64_t tiles_m = ceil_div(M, NBM);
+    int64_t splits = 1;
+    if (tiles_m < 148 && K > 4 * NBK)
+      splits = std::max<int64_t>(1, std::min<int64_t>(ceil_div(148, tiles_m), ceil_div(K, 64)));
+    g.kchunk = round_up(ceil_div(K, splits), NBK);
+    splits = ceil_div(K, g.kchunk);
+    if (splits > 1) {
+      ws.splitk.ensure((size_t)(splits * M * N));
+      g.part = ws.splitk.p;
+    } else {
+      g.part = nullptr;
+    }
+    const dim3 grid(1, (unsigned)tiles_m, (unsigned)splits);
+    if (NC == 1) TK_LAUNCH(k_dgemm_nn<1>, grid, 256, 0, st, g);
+    else if (NC == 2) TK_LAUNCH(k_dgemm_nn<2>, grid, 256, 0, st, g);
+    else if (NC == 3) TK_LAUNCH(k_dgemm_nn<3>, grid, 256, 0, st, g);
+    else TK_LAUNCH(k_dgemm_nn<4>, grid, 256, 0, st, g);
+    if (splits > 1) {
+      const int64_t blocks = std::min<int64_t>(ceil_div(M * N, 256), 148 * 8);
+      TK_LAUNCH(k_splitk_reduce, (unsigned)blocks, 256, 0, st, M, N, (int)splits, ws.splitk.p,
+                alpha, beta, C, ldc, gamma, D, ldd, delta, E, lde);
+    }
+    return;
+  }
   const int64_t tiles = ceil_div(M, BM) * ceil_div(N, BN);
   int64_t splits = 1;
   if (K <= 0) {
@@ -194,7 +331,7 @@ void dgemm(int64_t M, int64_t N, int64_t K, double alpha, MatRef A, MatRef B, do
   if (splits > 1) {
     const int64_t blocks = std::min<int64_t>(ceil_div(M * N, 256), 148 * 8);
     TK_LAUNCH(k_splitk_reduce, (unsigned)blocks, 256, 0, st, M, N, (int)splits, ws.splitk.p,
-              alpha, beta, C, ldc, gamma, D, ldd);
+              alpha, beta, C, ldc, gamma, D, ldd, delta, E, lde);
   }
 }
 

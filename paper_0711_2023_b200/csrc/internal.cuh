@@ -89,6 +89,10 @@ struct DenseWs {
 void dgemm(int64_t M, int64_t N, int64_t K, double alpha, MatRef A, MatRef B, double beta,
            double* C, int64_t ldc, double gamma, const double* D, int64_t ldd, DenseWs& ws,
            cudaStream_t st);
+// ... + delta E (E nullable, lde): the fused Chebyshev-recurrence epilogue
+void dgemm4(int64_t M, int64_t N, int64_t K, double alpha, MatRef A, MatRef B, double beta,
+            double* C, int64_t ldc, double gamma, const double* D, int64_t ldd, double delta,
+            const double* E, int64_t lde, DenseWs& ws, cudaStream_t st);
 double dnorm2_f32(const float* x, int64_t n, DenseWs& ws, cudaStream_t st);  // sum x^2, fp64
 
 // eig.cu
@@ -99,7 +103,7 @@ struct EigSlot {              // warm-start state per (algorithm, mode)
   bool valid = false;
 };
 struct EigWs {
-  DBuf<double> Q, SQ, X, Y, T, H, V, R, L, LT, Z;
+  DBuf<double> Q, SQ, X, Y, T, H, V, R, L, LT, Z, pq, py, pout;
   DBuf<double> theta, resid;
   DBuf<int> dsweeps;
   DenseWs dense;
@@ -110,11 +114,12 @@ struct EigOpts {
   int oversample = 0;
   int max_outer = 40;
   int jacobi_sweeps = 2;  // cap per Rayleigh-Ritz step (residuals decide convergence)
-  double tol = 1e-11;
+  double tol = 1e-10;
 };
-// Leading J eigenvectors of symmetric PSD S (d x d, lds): out_V (d x ldv fp64 row-major)
+// Leading J eigenvectors of symmetric PSD S (d x d, lds; S is used as workspace and
+// deflated in place): out_V (d x ldv fp64 row-major)
 // columns 0..J-1 descending, theta_out[0..J) host. Returns true if converged.
-bool eig_leading(const double* S, int64_t lds, int64_t d, int J, EigSlot& slot, EigWs& ws,
+bool eig_leading(double* S, int64_t lds, int64_t d, int J, EigSlot& slot, EigWs& ws,
                  const EigOpts& o, double* out_V, int64_t ldv, double* theta_out,
                  cudaStream_t st);
 // Orthonormalise the columns of V (d x J fp64) in place (CholQR2).

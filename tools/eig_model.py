@@ -14,14 +14,14 @@ def choose_block(J, d, p=0, kmax=116):
     return max(k, J)
 
 
-def chol_inv(G):
+def chol_inv(G, shift=0.0):
     dsc = 1 / np.sqrt(np.maximum(np.diag(G), 1e-300))
-    Gs = G * dsc[:, None] * dsc[None, :]
+    Gs = G * dsc[:, None] * dsc[None, :] + shift * np.eye(G.shape[0])
     R = np.linalg.cholesky(Gs).T
     return dsc[:, None] * np.linalg.inv(R)
 
 
-def eig_leading(S, J, tol=1e-11, max_outer=60, verbose=True, Q0=None):
+def eig_leading(S, J, tol=1e-10, max_outer=60, verbose=True, Q0=None):
     d = S.shape[0]
     k = choose_block(J, d)
     rng = np.random.default_rng(0)
@@ -34,8 +34,10 @@ def eig_leading(S, J, tol=1e-11, max_outer=60, verbose=True, Q0=None):
         if L.shape[1]:
             for _ in range(2):
                 A = A - L @ (L.T @ A)
-        for _ in range(2):
-            A = A @ chol_inv(A.T @ A)
+        ka = A.shape[1]
+        shift = 11.0 * (d * ka + ka * (ka + 1)) * 1.1e-16 * ka
+        for p in range(3):
+            A = A @ chol_inv(A.T @ A, shift if p == 0 else 0.0)
         return A
 
     def op(Y):
@@ -88,16 +90,25 @@ def eig_leading(S, J, tol=1e-11, max_outer=60, verbose=True, Q0=None):
         xJ = max((thJ - c) / e, 1 + 1e-12); xt = max((thtop - c) / e, xJ)
         rJ, rt = math.acosh(xJ), math.acosh(xt)
         rmax = max(res[i] / th1 for i in range(nlock, J))
-        m = math.ceil(math.log(max(rmax / tol, 4.0)) / max(rJ, 1e-6))
-        m_amp = math.floor(math.log(2e7) / max(rt, 1e-6))
-        m = max(1, min(m, m_amp, 16))
-        sigma = e / (thtop - c); tau = 2 / sigma
-        Y = (SA - c * A) * (sigma / e); X = A
-        for _ in range(2, m + 1):
-            s2 = 1 / (tau - sigma)
-            T = (2 * s2 / e) * op(Y) - sigma * s2 * X - (2 * s2 * c / e) * Y
-            X, Y = Y, T
-            sigma = s2
+        m_need = math.ceil(math.log(max(rmax / tol, 4.0)) / max(rJ, 1e-6))
+        m_amp = max(1, min(16, math.floor(math.log(2e7) / max(rt, 1e-6))))
+        m = m_need = max(1, min(m_need, 64, (2 if m_amp < 6 else 8) * m_amp))
+        done = 0
+        while done < m_need:
+            mseg = min(m_amp, m_need - done)
+            sigma = e / (thtop - c); tau = 2 / sigma
+            SA = op(A) if done > 0 else SA
+            Y = (SA - c * A) * (sigma / e); X = A
+            for _ in range(2, mseg + 1):
+                s2 = 1 / (tau - sigma)
+                T = (2 * s2 / e) * op(Y) - sigma * s2 * X - (2 * s2 * c / e) * Y
+                X, Y = Y, T
+                sigma = s2
+            done += mseg
+            A = Y
+            if done < m_need:
+                A = orth(A)
+        Y = A
         A = orth(Y)
         A, SA, w, r = rr(A)
         th[nlock:] = w; res[nlock:] = r
