@@ -157,10 +157,31 @@ int tucker_debug_gram(tucker_handle* h, int algo, int mode, double* S_out);
 int tucker_debug_eig(tucker_handle* h, int d, int J, const double* S, float* U_out,
                      double* evals_out);
 
+/* Unit test of the eigensolver's shared-memory k x k routines (1 <= k <= 116,
+ * one CTA on the current device; no handle).  mode 0: CholQR factor of the SPD
+ * matrix `in` (k x k row-major): out = M, upper triangular, with M^T in M = I
+ * (`shift` is added to the equilibrated matrix as in shifted CholQR).  mode 1:
+ * cyclic Jacobi with at most max_sweeps sweeps: out = V (eigenvectors in
+ * columns), theta = eigenvalues in descending order, *sweeps = sweeps used. */
+int tucker_debug_smalldense(int mode, int k, const double* in, double* out, double* theta,
+                            int* sweeps, int max_sweeps, double shift);
+
+/* Unit test of the eigensolver's fp64 tensor-core product (all SMs, no handle):
+ * out = alpha S Y + gamma D with S d x d, Y, D, out d x n row-major (1 <= n <= 116;
+ * D nullable). */
+int tucker_debug_product(int d, int n, const double* S, const double* Y, double alpha, double gamma,
+                         const double* D, double* out);
+
+/* Timing of the same product alone: *us = microseconds per launch (mean of reps). */
+int tucker_debug_product_time(int d, int n, int reps, double* us);
+
 /* Kernel statistics of the handle since the last reset (for bench/roofline):
  * stats[0] = kernel launches issued by the library, [1] = eigensolver outer
  * iterations, [2] = Chebyshev matvecs, [3] = small (k x k) Jacobi sweeps,
- * [4] = Gram path (0 = tcgen05 3xTF32, 1 = SIMT fp64).  stats has 5 entries. */
+ * [4] = Gram path (0 = tcgen05 3xTF32, 1 = SIMT fp64), [5..12] = time inside the
+ * fused eigensolver kernel by phase in ns as seen by its CTA 0 (matvec, k x k
+ * reductions, CholQR factor, Jacobi, row-block apply, deflation, power, other).
+ * stats has 13 entries. */
 int tucker_stats(tucker_handle* h, int64_t* stats, int reset);
 
 #ifdef __cplusplus

@@ -22,7 +22,8 @@ E_CONVERGE = 10
 EXPORTS = [
     "tucker_default_opts", "tucker_init", "hooi_sweep", "mp_sweep", "core_and_fit",
     "tucker_set_factors", "tucker_free", "tucker_strerror", "tucker_last_error",
-    "tucker_debug_ttmc", "tucker_debug_gram", "tucker_debug_eig", "tucker_stats",
+    "tucker_debug_ttmc", "tucker_debug_gram", "tucker_debug_eig", "tucker_debug_smalldense",
+    "tucker_debug_product", "tucker_debug_product_time", "tucker_stats",
 ]
 
 
@@ -58,6 +59,9 @@ def load(path: str = LIB_PATH) -> C.CDLL:
     lib.tucker_debug_gram.argtypes = [P, C.c_int, C.c_int, P]
     lib.tucker_debug_eig.argtypes = [P, C.c_int, C.c_int, P, P, P]
     lib.tucker_stats.argtypes = [P, i64p, C.c_int]
+    lib.tucker_debug_product.argtypes = [C.c_int, C.c_int, P, P, C.c_double, C.c_double, P, P]
+    lib.tucker_debug_product_time.argtypes = [C.c_int, C.c_int, C.c_int, C.POINTER(C.c_double)]
+    lib.tucker_debug_smalldense.argtypes = [C.c_int, C.c_int, P, P, P, P, C.c_int, C.c_double]
     for name in EXPORTS:
         if name not in ("tucker_default_opts", "tucker_strerror", "tucker_last_error"):
             getattr(lib, name).restype = C.c_int
@@ -204,11 +208,47 @@ def tucker_debug_eig(h, S, J):
     return U, w, rc
 
 
+def tucker_debug_smalldense(mode, A, max_sweeps=30, shift=0.0):
+    """mode 0: CholQR factor M of SPD A; mode 1: Jacobi -> (V, theta, sweeps)."""
+    A = np.ascontiguousarray(A, dtype=np.float64)
+    k = A.shape[0]
+    out = np.zeros((k, k))
+    th = np.zeros(k)
+    sw = C.c_int(0)
+    _check(lib().tucker_debug_smalldense(mode, k, C.c_void_p(A.ctypes.data), C.c_void_p(out.ctypes.data),
+                                         C.c_void_p(th.ctypes.data), C.c_void_p(C.addressof(sw)),
+                                         max_sweeps, shift))
+    return (out, th, sw.value) if mode == 1 else out
+
+
+def tucker_debug_product(S, Y, alpha=1.0, gamma=0.0, D=None):
+    """alpha S Y + gamma D on the eigensolver's fp64 tensor-core product."""
+    S = np.ascontiguousarray(S, dtype=np.float64)
+    Y = np.ascontiguousarray(Y, dtype=np.float64)
+    d, n = Y.shape
+    out = np.zeros((d, n))
+    Dp = None
+    if D is not None:
+        D = np.ascontiguousarray(D, dtype=np.float64)
+        Dp = C.c_void_p(D.ctypes.data)
+    _check(lib().tucker_debug_product(d, n, C.c_void_p(S.ctypes.data), C.c_void_p(Y.ctypes.data), alpha,
+                                      gamma, Dp, C.c_void_p(out.ctypes.data)))
+    return out
+
+
+def tucker_debug_product_time(d, n, reps=50):
+    us = C.c_double(0)
+    _check(lib().tucker_debug_product_time(d, n, reps, C.byref(us)))
+    return us.value
+
+
 def tucker_stats(h, reset=False):
-    s = (C.c_int64 * 5)()
+    s = (C.c_int64 * 13)()
     _check(lib().tucker_stats(h, s, 1 if reset else 0), h)
+    names = ("matvec", "reduce", "cholqr", "jacobi", "apply", "deflate", "power", "other")
     return dict(launches=s[0], eig_outer=s[1], eig_matvec=s[2], jacobi_sweeps=s[3],
-                gram_path="tcgen05-3xtf32" if s[4] == 0 else "simt-fp64")
+                gram_path="tcgen05-3xtf32" if s[4] == 0 else "simt-fp64",
+                eig_phase_ms={n: s[5 + i] / 1e6 for i, n in enumerate(names)})
 
 
 class Tucker:

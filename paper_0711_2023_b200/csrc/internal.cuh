@@ -105,6 +105,9 @@ struct EigSlot {              // warm-start state per (algorithm, mode)
 struct EigWs {
   DBuf<double> Q, SQ, X, Y, T, H, V, R, L, LT, Z, pq, py, pout;
   DBuf<double> theta, resid;
+  DBuf<double> fpart, fred;  // eig_fused reduction partials / results
+  DBuf<long long> fprof;      // eig_fused per-phase ns (accumulated over solves)
+  bool fprof_init = false;
   DBuf<int> dsweeps;
   DenseWs dense;
   std::vector<double> h_theta, h_resid;
@@ -122,6 +125,18 @@ struct EigOpts {
 bool eig_leading(double* S, int64_t lds, int64_t d, int J, EigSlot& slot, EigWs& ws,
                  const EigOpts& o, double* out_V, int64_t ldv, double* theta_out,
                  cudaStream_t st);
+// Same problem in one persistent cooperative kernel (eig_fused.cu): out_V (d x J,
+// ld = J) and theta_dev (J) on the device, info_dev[0..4] = {converged, outer
+// iterations, matvecs, Jacobi sweeps, breakdown}.  No host synchronisation.
+bool eig_fused(double* S, int64_t d, int J, EigSlot& slot, EigWs& ws, const EigOpts& o, double* out_V,
+               double* theta_dev, int* info_dev, cudaStream_t st);
+size_t eig_fused_smem(int k, int d, int G);
+// unit test of the fused solver's k x k routines (one CTA); see tucker_debug_smalldense
+void eig_unit_mv(const double* S, const double* Y, int d, int n, double alpha, double* Out, double gamma,
+                 const double* D, cudaStream_t st);
+double eig_unit_mv_time(int d, int n, int reps);  // us per product (zero data)
+void eig_unit(int mode, const double* in, int k, double* out, double* theta, int* iout, int sweeps,
+              double shift, cudaStream_t st);
 // Orthonormalise the columns of V (d x J fp64) in place (CholQR2).
 void cholqr2(double* V, int64_t ldv, int64_t d, int J, EigWs& ws, cudaStream_t st);
 // Order-preserving sign canonicalisation + fp32 conversion: U[i*J+j] = s_j V[i*ldv+j].

@@ -3,6 +3,7 @@
 // eig.cu / dense.cu.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -34,11 +35,14 @@ struct tucker_handle {
   DBuf<float> G32, Ytmp;
   bool G_valid = false;
   EigSlot slots[2][kMaxOrder];
+  DBuf<double> theta_d;
+  DBuf<int> info_d;
   EigSlot scratch_slot;
   EigWs eig;
   GramWs gram;
   int64_t launches = 0;
   int64_t stat_outer0 = 0, stat_matvec0 = 0, stat_sweeps0 = 0;
+  long long prof0[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   std::string last_error;
   bool eig_unconverged = false;
 };
@@ -86,6 +90,15 @@ __global__ void k_scale_cols(double* V, int64_t d, int J, const double* __restri
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
        e += (int64_t)gridDim.x * blockDim.x)
     V[e] *= s[e % J];
+}
+// V[:, j] *= theta_j^{-1/2} (0 if theta_j <= 0), theta on the device
+__global__ void k_scale_cols_rsqrt(double* V, int64_t d, int J, const double* __restrict__ theta) {
+  const int64_t n = d * J;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const double t = theta[e % J];
+    V[e] *= t > 0 ? 1.0 / sqrt(t) : 0.0;
+  }
 }
 __global__ void k_d2f(const double* __restrict__ x, int64_t n, float* __restrict__ y) {
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
@@ -190,14 +203,44 @@ Split build_mp_w(tucker_handle* h, int n) {
   return W;
 }
 
-// Leading eigenvectors of S (d x d) -> fp64 V (d x J) in h->V; returns eigenvalues
-std::vector<double> solve_eig(tucker_handle* h, int64_t d, int J, EigSlot& slot) {
+bool eig_multi() {
+  static const bool m = [] {
+    const char* e = std::getenv("TUCKER_EIG");
+    return e && std::strcmp(e, "multi") == 0;
+  }();
+  return m;
+}
+
+// Leading eigenvectors of S (d x d) -> fp64 V (d x J) in h->V, eigenvalues in
+// h->theta_d (device).  Default: the persistent fused solver (eig_fused.cu).
+void solve_eig(tucker_handle* h, int64_t d, int J, EigSlot& slot) {
   h->V.ensure((size_t)(d * J));
-  std::vector<double> theta(J);
-  const bool ok = eig_leading(h->S.p, d, d, J, slot, h->eig, eig_opts(h), h->V.p, J, theta.data(),
-                              h->st);
-  if (!ok) h->eig_unconverged = true;
-  return theta;
+  h->theta_d.ensure((size_t)J);
+  h->info_d.ensure(8);
+  if (eig_multi()) {
+    std::vector<double> theta(J);
+    const bool ok = eig_leading(h->S.p, d, d, J, slot, h->eig, eig_opts(h), h->V.p, J, theta.data(),
+                                h->st);
+    if (!ok) h->eig_unconverged = true;
+    TK_CUDA(cudaMemcpyAsync(h->theta_d.p, theta.data(), J * sizeof(double), cudaMemcpyHostToDevice, h->st));
+    TK_CUDA(cudaStreamSynchronize(h->st));
+    int info[8] = {ok ? 1 : 0, 0, 0, 0, 0, 0, 0, 0};
+    TK_CUDA(cudaMemcpy(h->info_d.p, info, sizeof(info), cudaMemcpyHostToDevice));
+    return;
+  }
+  eig_fused(h->S.p, d, J, slot, h->eig, eig_opts(h), h->V.p, h->theta_d.p, h->info_d.p, h->st);
+}
+
+// after the stream is synchronised: fold the solver's info into the handle
+void eig_check(tucker_handle* h) {
+  int info[8];
+  TK_CUDA(cudaMemcpy(info, h->info_d.p, 5 * sizeof(int), cudaMemcpyDeviceToHost));
+  if (eig_multi()) return;
+  if (info[4]) fail(TUCKER_E_CUDA, "eigensolver breakdown (non-finite Rayleigh quotient)");
+  if (!info[0]) h->eig_unconverged = true;
+  h->eig.stat_outer += info[1];
+  h->eig.stat_matvec += info[2];
+  h->eig.stat_sweeps += info[3];
 }
 
 // U_n from the eigenvectors of the Gram of the split matrix A (= Y, Y^T or W)
@@ -213,16 +256,12 @@ void update_factor(tucker_handle* h, int n, const Split& A, bool transposed, Eig
   TK_CUDA(cudaEventRecord(e0, h->st));
   gram_syrk(A, h->S.p, d, h->gram, h->st);
   TK_CUDA(cudaEventRecord(e1, h->st));
-  std::vector<double> theta = solve_eig(h, d, J, slot);
+  solve_eig(h, d, J, slot);
   if (!transposed) {
     canon_to_f32(h->V.p, J, d, J, h->U[n].p, h->st);
   } else {
     // Y^T Y route: U = Y_(n) V Theta^{-1/2} = (Y^T)^T V Theta^{-1/2}, then CholQR2
-    std::vector<double> sc(J);
-    for (int j = 0; j < J; ++j) sc[j] = theta[j] > 0 ? 1.0 / std::sqrt(theta[j]) : 0.0;
-    h->scal.ensure(J);
-    TK_CUDA(cudaMemcpyAsync(h->scal.p, sc.data(), J * sizeof(double), cudaMemcpyHostToDevice, h->st));
-    TK_LAUNCH(k_scale_cols, gridn(d * J), 256, 0, h->st, h->V.p, d, J, h->scal.p);
+    TK_LAUNCH(k_scale_cols_rsqrt, gridn(d * J), 256, 0, h->st, h->V.p, d, J, h->theta_d.p);
     const int64_t I = h->dims[n];
     h->Ufull.ensure((size_t)(I * J));
     MatRef a;
@@ -235,6 +274,7 @@ void update_factor(tucker_handle* h, int n, const Split& A, bool transposed, Eig
   }
   TK_CUDA(cudaEventRecord(e2, h->st));
   TK_CUDA(cudaEventSynchronize(e2));
+  eig_check(h);
   float a = 0, b = 0;
   TK_CUDA(cudaEventElapsedTime(&a, e0, e1));
   TK_CUDA(cudaEventElapsedTime(&b, e1, e2));
@@ -606,15 +646,56 @@ int tucker_debug_eig(tucker_handle* h, int d, int J, const double* S, float* U_o
                             od ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, h->st));
     h->scratch_slot.valid = false;
     h->eig_unconverged = false;
-    std::vector<double> theta = solve_eig(h, d, J, h->scratch_slot);
+    solve_eig(h, d, J, h->scratch_slot);
     h->Ytmp.ensure((size_t)d * J);
     canon_to_f32(h->V.p, J, d, J, h->Ytmp.p, h->st);
     TK_CUDA(cudaMemcpyAsync(U_out, h->Ytmp.p, (size_t)d * J * sizeof(float),
                             od ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, h->st));
     TK_CUDA(cudaStreamSynchronize(h->st));
+    eig_check(h);
     if (evals_out)
-      for (int j = 0; j < J; ++j) evals_out[j] = theta[j];
+      TK_CUDA(cudaMemcpy(evals_out, h->theta_d.p, J * sizeof(double), cudaMemcpyDeviceToHost));
     return h->eig_unconverged ? TUCKER_E_CONVERGE : TUCKER_OK;
+  });
+}
+
+int tucker_debug_smalldense(int mode, int k, const double* in, double* out, double* theta,
+                            int* sweeps, int max_sweeps, double shift) {
+  if (!in || !out || k < 1 || k > kMaxBlock || mode < 0 || mode > 1) return TUCKER_E_ARG;
+  return guarded(nullptr, [&]() -> int {
+    DBuf<double> din((size_t)k * k), dout((size_t)k * k), dth((size_t)k);
+    DBuf<int> di(1);
+    TK_CUDA(cudaMemcpy(din.p, in, (size_t)k * k * sizeof(double), cudaMemcpyHostToDevice));
+    eig_unit(mode, din.p, k, dout.p, dth.p, di.p, max_sweeps, shift, 0);
+    TK_CUDA(cudaDeviceSynchronize());
+    TK_CUDA(cudaMemcpy(out, dout.p, (size_t)k * k * sizeof(double), cudaMemcpyDeviceToHost));
+    if (theta) TK_CUDA(cudaMemcpy(theta, dth.p, (size_t)k * sizeof(double), cudaMemcpyDeviceToHost));
+    if (sweeps) TK_CUDA(cudaMemcpy(sweeps, di.p, sizeof(int), cudaMemcpyDeviceToHost));
+    return TUCKER_OK;
+  });
+}
+
+int tucker_debug_product(int d, int n, const double* S, const double* Y, double alpha, double gamma,
+                         const double* D, double* out) {
+  if (!S || !Y || !out || d < 1 || n < 1 || n > kMaxBlock) return TUCKER_E_ARG;
+  return guarded(nullptr, [&]() -> int {
+    DBuf<double> dS((size_t)d * d), dY((size_t)d * n), dD((size_t)d * n), dO((size_t)d * n);
+    TK_CUDA(cudaMemcpy(dS.p, S, (size_t)d * d * sizeof(double), cudaMemcpyHostToDevice));
+    TK_CUDA(cudaMemcpy(dY.p, Y, (size_t)d * n * sizeof(double), cudaMemcpyHostToDevice));
+    if (D) TK_CUDA(cudaMemcpy(dD.p, D, (size_t)d * n * sizeof(double), cudaMemcpyHostToDevice));
+    TK_CUDA(cudaMemset(dO.p, 0xff, (size_t)d * n * sizeof(double)));
+    eig_unit_mv(dS.p, dY.p, d, n, alpha, dO.p, D ? gamma : 0.0, dD.p, 0);
+    TK_CUDA(cudaDeviceSynchronize());
+    TK_CUDA(cudaMemcpy(out, dO.p, (size_t)d * n * sizeof(double), cudaMemcpyDeviceToHost));
+    return TUCKER_OK;
+  });
+}
+
+int tucker_debug_product_time(int d, int n, int reps, double* us) {
+  if (!us || d < 1 || n < 1 || n > kMaxBlock || reps < 1) return TUCKER_E_ARG;
+  return guarded(nullptr, [&]() -> int {
+    *us = eig_unit_mv_time(d, n, reps);
+    return TUCKER_OK;
   });
 }
 
@@ -625,6 +706,16 @@ int tucker_stats(tucker_handle* h, int64_t* stats, int reset) {
   stats[2] = h->eig.stat_matvec - h->stat_matvec0;
   stats[3] = h->eig.stat_sweeps - h->stat_sweeps0;
   stats[4] = gram_path_id();
+  {
+    long long pf[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    if (h->eig.fprof.p && h->eig.fprof_init) {
+      if (cudaMemcpy(pf, h->eig.fprof.p, sizeof(pf), cudaMemcpyDeviceToHost) != cudaSuccess)
+        return TUCKER_E_CUDA;
+    }
+    for (int i = 0; i < 8; ++i) stats[5 + i] = pf[i] - h->prof0[i];
+    if (reset)
+      for (int i = 0; i < 8; ++i) h->prof0[i] = pf[i];
+  }
   if (reset) {
     h->launches = 0;
     h->stat_outer0 = h->eig.stat_outer;
