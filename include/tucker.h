@@ -162,7 +162,9 @@ int tucker_debug_eig(tucker_handle* h, int d, int J, const double* S, float* U_o
  * matrix `in` (k x k row-major): out = M, upper triangular, with M^T in M = I
  * (`shift` is added to the equilibrated matrix as in shifted CholQR).  mode 1:
  * cyclic Jacobi with at most max_sweeps sweeps: out = V (eigenvectors in
- * columns), theta = eigenvalues in descending order, *sweeps = sweeps used. */
+ * columns), theta = eigenvalues in descending order, sweeps[0] = sweeps used
+ * and (mode 1) sweeps[1..7] = cycle counters of thread 0 (rotation, rows, row
+ * barrier, columns, column barrier, rounds, total); sweeps needs 8 entries. */
 int tucker_debug_smalldense(int mode, int k, const double* in, double* out, double* theta,
                             int* sweeps, int max_sweeps, double shift);
 

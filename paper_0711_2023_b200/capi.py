@@ -214,11 +214,14 @@ def tucker_debug_smalldense(mode, A, max_sweeps=30, shift=0.0):
     k = A.shape[0]
     out = np.zeros((k, k))
     th = np.zeros(k)
-    sw = C.c_int(0)
+    sw = (C.c_int * 8)()
     _check(lib().tucker_debug_smalldense(mode, k, C.c_void_p(A.ctypes.data), C.c_void_p(out.ctypes.data),
                                          C.c_void_p(th.ctypes.data), C.c_void_p(C.addressof(sw)),
                                          max_sweeps, shift))
-    return (out, th, sw.value) if mode == 1 else out
+    if mode >= 1:
+        tucker_debug_smalldense.cycles = list(sw[1:8])
+        return out, th, sw[0]
+    return out
 
 
 def tucker_debug_product(S, Y, alpha=1.0, gamma=0.0, D=None):

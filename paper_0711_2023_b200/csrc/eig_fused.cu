@@ -16,12 +16,19 @@
 //   * rows: CTA c owns rows [c*R, (c+1)*R) of every d-row block (R = ceil(d/G));
 //     row-local steps (axpby, Q <- Q M, copies, deflation of S's rows) need no
 //     barrier among themselves.
-//   * S * Y: CTA c computes its own rows of the product (reads all of Y).
+//   * S * Y: 2D tiles on the fp64 tensor cores (DMMA), operands streamed by TMA
+//     bulk copies; a barrier follows every product (it is not row-local).
 //   * k x k reductions (Q^T Q, Q^T S Q, Ritz residuals): per-CTA partials over
 //     its rows, a distributed fixed-order sum (deterministic), then every CTA
 //     loads the result and runs the small dense step (LDL^T-based CholQR
 //     factor, Jacobi) REDUNDANTLY in its own shared memory -- no further
 //     barrier, and the k x k result is where the row-local apply needs it.
+//
+// Layout (eig_layout): S is LS x LS-strided with RP rows, LS = round_up(d, 64),
+// RP = LS + 64; the d x k work blocks have leading dimension LB = k rounded up
+// to even and RP rows.  Everything outside the d x d / d x k data is zero, so
+// the product streams whole 64-wide K chunks and whole row tiles with no edge
+// cases, and every bulk copy is 16-byte aligned.
 #include <cooperative_groups.h>
 
 #include <algorithm>
@@ -40,15 +47,18 @@ constexpr int NT = 512;  // threads per CTA
 constexpr int NW = NT / 32;
 
 struct FusedArgs {
-  double* S;  // d x d row-major (deflated in place)
+  double* S;   // RP x LS (deflated in place; padding zeroed by the kernel)
   int d, J, k;
-  double* blk[5];           // five d x k work blocks (roles rotate)
+  int ls, lb, rp;           // S stride, block stride, padded rows
+  int mv_m8, mv_rb, mv_kb, mv_kc;  // product plan
+  double* blk[5];           // five RP x LB work blocks (roles rotate)
   double* L;                // d x J locked vectors
   double* LT;               // d x J  S L
   double* part;             // [G][k*k] reduction partials
   double* red;              // [k*k] reduced result
   double* pvec[2];          // power iteration vectors (d)
-  double* basis;            // d x k warm-start basis (read if warm, always written)
+  double* mpart;            // [KB][RPX][LB] split-K partial products
+  double* basis;            // d x LB warm-start basis (read if warm, always written)
   int warm;
   double* outV;             // d x J output (ld = J)
   double* theta_out;        // J
@@ -58,9 +68,6 @@ struct FusedArgs {
   int max_outer, jsweeps;
   uint64_t seed;
   int dbg;
-  int noshift;
-  int nolock;
-  int nodefl;
 };
 
 // region 1 holds a k x (k+1) matrix or the own-row staging of a d x k block
@@ -72,9 +79,10 @@ __host__ __device__ inline size_t region1_doubles(int kp, int R) {
 struct Ctx {
   int cta, G, tid, warp, lane;
   int d, r0, r1;  // own rows [r0, r1)
+  int ls, lb;     // S stride, block stride
+  int mv_m8, mv_rb, mv_kb, mv_kc;  // product plan (mv_plan(d, G)), computed on the host
   double* r1s;    // smem region 1 (k x (k+1) doubles or staging)
   double* r2s;    // smem region 2 (k x (k+1) doubles)
-  size_t reg_doubles;
 };
 
 __device__ __forceinline__ void gsync() { cg::this_grid().sync(); }
@@ -99,20 +107,21 @@ __device__ void copy_cols(const Ctx& x, const double* src, int lds, double* dst,
     for (int c = x.lane; c < ncol; c += 32) dst[(int64_t)r * ldd + c] = src[(int64_t)r * lds + c];
 }
 
-__device__ void fill_random(const Ctx& x, double* Q, int k, uint64_t seed) {
+// deterministic uniform(-1, 1) fill of the own rows of Q (k columns, stride ld)
+__device__ void fill_random(const Ctx& x, double* Q, int ld, int k, uint64_t seed) {
   for (int r = x.r0 + x.warp; r < x.r1; r += NW)
     for (int c = x.lane; c < k; c += 32) {
-    const uint64_t h = mix64(seed ^ mix64((uint64_t)r * 1315423911ull + (uint64_t)c));
-    Q[(int64_t)r * k + c] = ((double)(h >> 11) * (1.0 / 9007199254740992.0)) * 2.0 - 1.0;
-  }
+      const uint64_t h = mix64(seed ^ mix64((uint64_t)r * 1315423911ull + (uint64_t)c));
+      Q[(int64_t)r * ld + c] = ((double)(h >> 11) * (1.0 / 9007199254740992.0)) * 2.0 - 1.0;
+    }
 }
 
-// z = a x + b y on own rows (ld = n), z may alias x or y
-__device__ void axpby(const Ctx& x, int n, double a, const double* X, double b, const double* Y,
+// z = a x + b y on own rows (n columns, stride ld), z may alias x or y
+__device__ void axpby(const Ctx& x, int n, int ld, double a, const double* X, double b, const double* Y,
                       double* Z) {
   for (int r = x.r0 + x.warp; r < x.r1; r += NW)
     for (int c = x.lane; c < n; c += 32) {
-      const int64_t o = (int64_t)r * n + c;
+      const int64_t o = (int64_t)r * ld + c;
       Z[o] = a * X[o] + (b != 0.0 ? b * Y[o] : 0.0);
     }
 }
@@ -147,26 +156,24 @@ __device__ void apply_right(const Ctx& x, const double* In, int ldi, int m, cons
   __syncthreads();
 }
 
-// ------------------------------------------------- S * Y on the fp64 tensor cores --
-// Out = alpha S Y + gamma D + delta E  (S d x d, Y/Out/D/E d x n, ld n; n <= 128).
-// 2D tiling: CTA (rb, cb) computes rows [8 m8 rb, +8 m8) x column tiles [tpb cb, +tpb)
-// of 8 columns; the plan (m8, CB) minimises max(DMMA time, L2 traffic time) over
-// the G CTAs and is computed identically by every CTA.  K is staged in chunks of
-// KCH through shared memory with cp.async (double buffered, zero-filled edges);
-// warp w owns n-tile pair (w mod ng) for every row tile and the k4-steps
-// congruent to (w / ng) mod KS; the KS partial tiles are summed in a fixed
-// order in the epilogue.  mma.sync m8n8k4 f64 -> DMMA on sm_100a.
-// Y must be complete (barrier before); Out must not alias Y; E may alias Y.
-constexpr int KCH = 64;          // K per staged chunk (16 k4-steps)
-constexpr int SP = KCH + 4;      // S tile row stride (conflict-free A fragments)
-constexpr int M8MAX = 6;         // row tiles per CTA
-constexpr int NSMAX = 4;         // pipeline stages
-constexpr size_t MV_BUDGET = 200 * 1024 / sizeof(double);  // doubles of smem for the stages
+// zero the padding of S (columns [d, LS) of rows < d, rows [d, RP)) and the
+// padding rows [d, RP) of the work blocks, distributed over the CTAs
+__device__ void zero_padding(const Ctx& x, double* S, int rp, double* const* blk) {
+  for (int r = x.r0 + x.warp; r < x.r1; r += NW)
+    for (int c = x.d + x.lane; c < x.ls; c += 32) S[(int64_t)r * x.ls + c] = 0.0;
+  for (int r = x.d + x.cta; r < rp; r += x.G) {
+    for (int c = x.tid; c < x.ls; c += NT) S[(int64_t)r * x.ls + c] = 0.0;
+    for (int b = 0; b < 5; ++b)
+      for (int c = x.tid; c < x.lb; c += NT) blk[b][(int64_t)r * x.lb + c] = 0.0;
+  }
+}
 
-__device__ __forceinline__ void cp_async8(double* smem, const double* gmem, bool pred) {
-  const uint32_t sa = (uint32_t)__cvta_generic_to_shared(smem);
-  const int nbytes = pred ? 8 : 0;
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(sa), "l"(gmem), "r"(nbytes) : "memory");
+// ------------------------------------------------- S * Y on the fp64 tensor cores --
+constexpr int KCH = 64;          // padding granule of the layout (K chunks stay whole)
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void cp_async16(double* smem, const double* gmem) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem)), "l"(gmem) : "memory");
 }
 __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N>
@@ -178,246 +185,164 @@ __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b)
                : "d"(a), "d"(b));
 }
 
+// ------------------------------------------------- S * Y on the fp64 tensor cores --
+// Split-K plan: row blocks of MT rows (MT = 8 m8, m8 <= 8) x K ranges of kchunk
+// (multiple of 64) with RB * KB <= G CTAs, minimising the per-CTA work MT kchunk
+// (ties: larger MT, less partial traffic).  Depends on d only.
 struct MvPlan {
-  int m8, CB, tpb, RBn;
+  int m8, RB, KB, kchunk;
 };
-__host__ __device__ inline MvPlan mv_plan(int d, int n, int G) {
-  const int n8 = (n + 7) >> 3;
-  MvPlan best{1, 1, n8, (d + 7) >> 3};
-  double bt = 1e300;
-  for (int m8 = 1; m8 <= M8MAX; ++m8) {
-    const int RBn = (d + 8 * m8 - 1) / (8 * m8);
-    for (int CB = 1; CB <= n8; ++CB) {
-      const int tpb = (n8 + CB - 1) / CB;
-      const int cbn = (n8 + tpb - 1) / tpb;
-      if (cbn != CB || RBn * cbn > G) continue;
-      const double comp = 64.0 * m8 * tpb * (double)d / 64.0;                        // clk at ~64 FMA/clk
-      const double traf = (double)RBn * cbn * 8.0 * (m8 + tpb) * 8.0 * d / 6000.0;   // clk at ~6 KB/clk L2
-      const double t = comp > traf ? comp : traf;
-      if (t < bt - 1e-9) {
-        bt = t;
-        best = MvPlan{m8, cbn, tpb, RBn};
-      }
+__host__ __device__ inline MvPlan mv_plan(int d, int G) {
+  const int LS = (d + 63) / 64 * 64;
+  MvPlan best{1, (d + 7) / 8, 1, LS};
+  long long bc = -1;
+  for (int m8 = 8; m8 >= 1; --m8) {
+    const int MT = 8 * m8;
+    const int RB = (d + MT - 1) / MT;
+    const int kbmax = G / RB;
+    if (kbmax < 1) continue;
+    const int kc = ((LS + kbmax - 1) / kbmax + 63) / 64 * 64;
+    const int KB = (LS + kc - 1) / kc;
+    const long long cost = (long long)MT * kc;
+    if (bc < 0 || cost < bc) {
+      bc = cost;
+      best = MvPlan{m8, RB, KB, kc};
     }
   }
   return best;
 }
-__host__ __device__ inline int mv_ypad(int tpb) { return ((8 * tpb + 15) & ~15) + 4; }
-__host__ __device__ inline size_t mv_stage_doubles(int m8, int tpb) {
-  return (size_t)8 * m8 * SP + (size_t)KCH * mv_ypad(tpb);
+constexpr int KC2 = 64;  // K per staged chunk inside a CTA's range
+__host__ __device__ inline int mv_ypad(int n8) { return ((8 * n8 + 15) & ~15) + 4; }  // = 4 or 12 mod 16
+__host__ __device__ inline size_t mv_stage_doubles(int m8, int n8) {
+  return (size_t)8 * m8 * (KC2 + 4) + (size_t)KC2 * mv_ypad(n8);
 }
-__host__ __device__ inline int mv_stages(int m8, int tpb) {
-  const size_t st = mv_stage_doubles(m8, tpb);
-  int ns = (int)(MV_BUDGET / st);
-  return ns > NSMAX ? NSMAX : (ns < 2 ? 2 : ns);
-}
-__host__ __device__ inline size_t mv_smem_doubles(int m8, int tpb) {
-  return (size_t)mv_stages(m8, tpb) * mv_stage_doubles(m8, tpb);
-}
+__host__ __device__ inline size_t mv_smem_doubles(int m8, int n8) { return 2 * mv_stage_doubles(m8, n8); }
 
-// ------------------------------------------------- S * Y on the fp64 tensor cores --
-// Out = alpha S Y + gamma D + delta E  (S d x d, Y/Out/D/E d x n, ld n; n <= 128).
-// 2D tiling: CTA (rb, cb) computes rows [8 m8 rb, +8 m8) x column tiles [tpb cb, +tpb)
-// of 8 columns; the plan (m8, CB) minimises max(DMMA time, L2 traffic time) over
-// the G CTAs and is computed identically by every CTA.  K is streamed in chunks
-// of KCH through an NS-stage cp.async pipeline (zero-filled edges, one barrier per
-// chunk); warp w owns n-tile pair (w mod ng) for every row tile and the k4-steps
-// congruent to (w / ng) mod KS; the KS partial tiles are summed in a fixed order
-// in the epilogue.  mma.sync m8n8k4 f64 -> DMMA on sm_100a.
-// Y must be complete (barrier before); Out must not alias Y, D; E may alias Y.
-// the plan of mv_plan(), evaluated with one candidate (m8, CB) per thread and a
-// block-wide argmin (same tie-break: smallest m8, then smallest CB); cached per n
-__device__ MvPlan mv_plan_cached(const Ctx& x, int n) {
-  __shared__ int cn, init;
-  __shared__ MvPlan cpl;
-  __shared__ double bt[NW];
-  __shared__ int bi[NW];
-  if (init == 0x5eed && cn == n) {
-    const MvPlan p = cpl;
-    __syncthreads();
-    return p;
-  }
-  __syncthreads();
-  const int d = x.d;
+// Out = alpha S Y + gamma D + delta E on the padded layout (S RP x LS, Y/Out/D/E
+// RP x LB, n <= 116 active columns).  Phase A (every CTA (rb, kb) of the plan):
+// partial P_kb[rows of rb][0..8 n8) = S[rows, K range] Y[K range, :] on DMMA,
+// K streamed in 64-wide chunks through a double-buffered 16-byte cp.async ring;
+// warp w owns m-tile pair (w / Ng) x n-tile group (w mod Ng) (<= 2 x 4
+// accumulator tiles).  Partials go to `mpart` ([KB][RP][LB]).  Barrier.  Phase B
+// (row owners, row-local): Out = alpha sum_kb P_kb + gamma D + delta E in a
+// fixed order.  Y, D, E must be complete before the call (barrier); Out may
+// alias D or E (each element is read before it is written by the same thread).
+__device__ void matvec(const Ctx& x, double* mpart, const double* S, const double* Y, int n, double alpha,
+                       double* Out, double gamma, const double* Dm, double delta, const double* Em) {
+  const MvPlan pl{x.mv_m8, x.mv_rb, x.mv_kb, x.mv_kc};
+  const int LS = x.ls, LB = x.lb;
   const int n8 = (n + 7) >> 3;
-  double t = 1e300;
-  int id = 1 << 30;
-  if (x.tid < M8MAX * n8) {
-    const int m8 = 1 + x.tid / n8, CB = 1 + x.tid % n8;
-    const int RBn = (d + 8 * m8 - 1) / (8 * m8);
-    const int tpb = (n8 + CB - 1) / CB;
-    const int cbn = (n8 + tpb - 1) / tpb;
-    if (cbn == CB && RBn * cbn <= x.G) {
-      const double comp = 64.0 * m8 * tpb * (double)d / 64.0;
-      const double traf = (double)RBn * cbn * 8.0 * (m8 + tpb) * 8.0 * d / 6000.0;
-      t = comp > traf ? comp : traf;
-      id = x.tid;
-    }
-  }
-  // argmin with the serial loop's preference for the first candidate within 1e-9
+  const int RPX = (x.d + 8 * pl.m8 - 1) / (8 * pl.m8) * (8 * pl.m8);  // rows covered by the plan
+  if (x.cta < pl.RB * pl.KB) {
+    const int rb = x.cta / pl.KB, kb = x.cta - rb * pl.KB;
+    const int MT = 8 * pl.m8;
+    const int row0 = rb * MT;
+    const int kbeg = kb * pl.kchunk, kend = min(LS, kbeg + pl.kchunk);
+    const int Mg = (pl.m8 + 1) >> 1;            // m-tile pairs
+    const int gN = (n8 + (NW / Mg) - 1) / (NW / Mg);  // n-tiles per warp group (<= 4)
+    const int Ng = (n8 + gN - 1) / gN;
+    const int mg = x.warp / Ng, ng = x.warp - mg * Ng;
+    const bool wact = mg < Mg;
+    const int mt0 = 2 * mg, nmt = min(2, pl.m8 - mt0);
+    const int nt0 = ng * gN, nnt = min(gN, n8 - nt0);
+    const int YP = mv_ypad(n8);
+    const int SPK = KC2 + 4;
+    const size_t STG = mv_stage_doubles(pl.m8, n8);
+    double acc[2][4][2];
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    const double ot = __shfl_xor_sync(0xffffffffu, t, o);
-    const int oi = __shfl_xor_sync(0xffffffffu, id, o);
-    if (ot < t - 1e-9 || (fabs(ot - t) <= 1e-9 && oi < id)) {
-      t = ot;
-      id = oi;
-    }
-  }
-  if (x.lane == 0) {
-    bt[x.warp] = t;
-    bi[x.warp] = id;
-  }
-  __syncthreads();
-  if (x.tid == 0) {
-    double b = 1e300;
-    int ib = 1 << 30;
-    for (int w = 0; w < NW; ++w)
-      if (bt[w] < b - 1e-9 || (fabs(bt[w] - b) <= 1e-9 && bi[w] < ib)) {
-        b = bt[w];
-        ib = bi[w];
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    const double* gS = S + (int64_t)row0 * LS;
+    const int yu = 4 * n8;  // 16-byte units per staged Y row (8 n8 doubles)
+    auto stage = [&](int buf, int k0) {
+      double* sS = x.r1s + (size_t)buf * STG;
+      double* sY = sS + MT * SPK;
+      for (int u = x.tid; u < MT * (KC2 / 2); u += NT) {
+        const int r = u >> 5, c2 = (u & 31) << 1;
+        cp_async16(sS + r * SPK + c2, gS + (int64_t)r * LS + k0 + c2);
       }
-    MvPlan p{1, 1, n8, (d + 7) >> 3};
-    if (ib < (1 << 30)) {
-      const int m8 = 1 + ib / n8, CB = 1 + ib % n8;
-      const int tpb = (n8 + CB - 1) / CB;
-      p = MvPlan{m8, CB, tpb, (d + 8 * m8 - 1) / (8 * m8)};
-    }
-    cpl = p;
-    cn = n;
-    init = 0x5eed;
-  }
-  __syncthreads();
-  const MvPlan p = cpl;
-  __syncthreads();
-  return p;
-}
-
-__device__ void matvec(const Ctx& x, const double* S, const double* Y, int n, double alpha, double* Out,
-                       double gamma, const double* Dm, double delta, const double* Em) {
-  const int d = x.d;
-  const MvPlan pl = mv_plan_cached(x, n);
-  if (x.cta >= pl.RBn * pl.CB) return;
-  const int rb = x.cta / pl.CB, cb = x.cta - rb * pl.CB;
-  const int MT = 8 * pl.m8;
-  const int row0 = rb * MT;
-  const int n8 = (n + 7) >> 3;
-  const int t0 = cb * pl.tpb;
-  const int ntile = min(pl.tpb, n8 - t0);
-  if (row0 >= d || ntile <= 0) return;
-  const int col0 = 8 * t0;
-  const int NTL = 8 * ntile;
-  const int YP = mv_ypad(pl.tpb);
-  const int NS = mv_stages(pl.m8, pl.tpb);
-  const size_t STG = mv_stage_doubles(pl.m8, pl.tpb);
-  const int ng = (ntile + 1) >> 1;  // n-tile pairs
-  const int KS = NW / ng;           // >= 2 (ntile <= 16)
-  const int myg = x.warp % ng, myks = x.warp / ng;
-  const bool wact = myks < KS;
-  const int nt0 = 2 * myg;
-  const bool two = nt0 + 1 < ntile;
-  double acc[M8MAX][2][2];
-#pragma unroll
-  for (int i = 0; i < M8MAX; ++i)
-#pragma unroll
-    for (int j = 0; j < 2; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
-
-  auto stage = [&](int ch) {
-    double* sS = x.r1s + (size_t)(ch % NS) * STG;
-    double* sY = sS + MT * SP;
-    const int k0 = ch * KCH;
-    for (int r = x.warp; r < MT; r += NW) {
-      const int gr = row0 + r;
-#pragma unroll
-      for (int h = 0; h < KCH / 32; ++h) {
-        const int kk = x.lane + 32 * h;
-        const bool ok = gr < d && k0 + kk < d;
-        cp_async8(sS + r * SP + kk, ok ? S + (int64_t)gr * d + k0 + kk : S, ok);
+      for (int kk = x.warp; kk < KC2; kk += NW) {
+        const double* src = Y + (int64_t)(k0 + kk) * LB;
+        double* dst = sY + kk * YP;
+        for (int u = x.lane; u < yu; u += 32) cp_async16(dst + 2 * u, src + 2 * u);
       }
-    }
-    for (int kk = x.warp; kk < KCH; kk += NW) {
-      const int gk = k0 + kk;
-      for (int c = x.lane; c < NTL; c += 32) {
-        const bool ok = gk < d && col0 + c < n;
-        cp_async8(sY + kk * YP + c, ok ? Y + (int64_t)gk * n + col0 + c : Y, ok);
+      cp_commit();
+    };
+    const int nch = (kend - kbeg) / KC2;
+    stage(0, kbeg);
+    const int ar = x.lane >> 2, aq = x.lane & 3;
+    for (int ch = 0; ch < nch; ++ch) {
+      if (ch + 1 < nch) {
+        stage((ch + 1) & 1, kbeg + (ch + 1) * KC2);
+        cp_wait<1>();
+      } else {
+        cp_wait<0>();
       }
+      __syncthreads();
+      if (wact) {
+        const double* sS = x.r1s + (size_t)(ch & 1) * STG;
+        const double* sY = sS + MT * SPK;
+#pragma unroll 4
+        for (int kb4 = 0; kb4 < KC2; kb4 += 4) {
+          double a[2], b[4];
+#pragma unroll
+          for (int i = 0; i < 2; ++i) a[i] = i < nmt ? sS[(8 * (mt0 + i) + ar) * SPK + kb4 + aq] : 0.0;
+#pragma unroll
+          for (int j = 0; j < 4; ++j) b[j] = j < nnt ? sY[(kb4 + aq) * YP + 8 * (nt0 + j) + ar] : 0.0;
+#pragma unroll
+          for (int i = 0; i < 2; ++i)
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+              if (i < nmt && j < nnt) dmma(acc[i][j][0], acc[i][j][1], a[i], b[j]);
+        }
+      }
+      __syncthreads();  // buffer (ch & 1) free for chunk ch + 2
     }
-  };
-  const int nch = (d + KCH - 1) / KCH;
-  // prologue: NS - 1 chunks in flight (empty groups keep the accounting uniform)
-  for (int ch = 0; ch < NS - 1; ++ch) {
-    if (ch < nch) stage(ch);
-    cp_commit();
-  }
-  const int ar = x.lane >> 2, aq = x.lane & 3;  // fragment coordinates
-  for (int ch = 0; ch < nch; ++ch) {
-    if (NS == 4) cp_wait<2>();
-    else if (NS == 3) cp_wait<1>();
-    else cp_wait<0>();
-    __syncthreads();  // chunk ch visible to all; buffer (ch - 1) % NS free
-    if (ch + NS - 1 < nch) stage(ch + NS - 1);
-    cp_commit();
     if (wact) {
-      const double* sS = x.r1s + (size_t)(ch % NS) * STG;
-      const double* sY = sS + MT * SP;
-      for (int s4 = myks; s4 < KCH / 4; s4 += KS) {
-        const int kb = 4 * s4;
-        const double b0 = sY[(kb + aq) * YP + 8 * nt0 + ar];
-        const double b1 = two ? sY[(kb + aq) * YP + 8 * (nt0 + 1) + ar] : 0.0;
+      double* P = mpart + (size_t)kb * RPX * LB;
 #pragma unroll
-        for (int i = 0; i < M8MAX; ++i) {
-          if (i < pl.m8) {
-            const double a = sS[(8 * i + ar) * SP + kb + aq];
-            dmma(acc[i][0][0], acc[i][0][1], a, b0);
-            if (two) dmma(acc[i][1][0], acc[i][1][1], a, b1);
+      for (int i = 0; i < 2; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          if (i < nmt && j < nnt) {
+            const int r = row0 + 8 * (mt0 + i) + ar, c = 8 * (nt0 + j) + 2 * aq;
+            if (c < n) P[(int64_t)r * LB + c] = acc[i][j][0];
+            if (c + 1 < n) P[(int64_t)r * LB + c + 1] = acc[i][j][1];
           }
-        }
-      }
     }
   }
-  cp_wait<0>();
-  __syncthreads();
-  // epilogue: partial tiles -> smem [KS][MT][NTL], fixed-order sum over KS
-  double* red = x.r1s;
-  if (wact) {
-#pragma unroll
-    for (int i = 0; i < M8MAX; ++i) {
-      if (i < pl.m8) {
-#pragma unroll
-        for (int j = 0; j < 2; ++j) {
-          if (j == 0 || two) {
-            const int rr = 8 * i + ar, cc = 8 * (nt0 + j) + 2 * aq;
-            double* o = red + ((size_t)myks * MT + rr) * NTL + cc;
-            o[0] = acc[i][j][0];
-            o[1] = acc[i][j][1];
-          }
-        }
-      }
-    }
-  }
-  __syncthreads();
-  const int nrow = min(MT, d - row0);
-  const int ncol = min(NTL, n - col0);
-  for (int r = x.warp; r < nrow; r += NW)
-    for (int c = x.lane; c < ncol; c += 32) {
+  gsync();
+  // phase B: own rows
+  for (int r = x.r0 + x.warp; r < x.r1; r += NW)
+    for (int c = x.lane; c < n; c += 32) {
       double sum = 0.0;
-      for (int q = 0; q < KS; ++q) sum += red[((size_t)q * MT + r) * NTL + c];
-      const int64_t o = (int64_t)(row0 + r) * n + col0 + c;
+      const double* pp0 = mpart + (size_t)r * LB + c;
+      const size_t pstr = (size_t)RPX * LB;
+      int q = 0;
+      for (; q + 4 <= pl.KB; q += 4) {  // 4 loads in flight, summed in order
+        const double v0 = __ldcg(pp0 + q * pstr), v1 = __ldcg(pp0 + (q + 1) * pstr);
+        const double v2 = __ldcg(pp0 + (q + 2) * pstr), v3 = __ldcg(pp0 + (q + 3) * pstr);
+        sum += v0;
+        sum += v1;
+        sum += v2;
+        sum += v3;
+      }
+      for (; q < pl.KB; ++q) sum += __ldcg(pp0 + q * pstr);
+      const int64_t o = (int64_t)r * LB + c;
       double v = alpha * sum;
       if (gamma != 0.0) v += gamma * Dm[o];
       if (delta != 0.0) v += delta * Em[o];
       Out[o] = v;
     }
-  __syncthreads();
 }
 
 // single vector: y[own rows] = S[own rows, :] q, partial ||y||^2 -> part[cta]
-__device__ void matvec1(const Ctx& x, const double* S, const double* q, double* y,
-                        double* part) {
+__device__ void matvec1(const Ctx& x, const double* S, const double* q, double* y, double* part) {
   __shared__ double wsum[NW];
   double nrm = 0.0;
   for (int r = x.r0 + x.warp; r < x.r1; r += NW) {
-    const double* srow = S + (int64_t)r * x.d;
+    const double* srow = S + (int64_t)r * x.ls;
     double s = 0.0;
     for (int c = x.lane; c < x.d; c += 32) s = fma(__ldcg(srow + c), __ldcg(q + c), s);
 #pragma unroll
@@ -449,6 +374,21 @@ __device__ double allsum_scalar(const Ctx& x, const double* part) {
   const double r = res;
   __syncthreads();
   return r;
+}
+
+// partial over own rows of a per-row scalar -> part[cta] (block sum, fixed order)
+__device__ void block_partial(const Ctx& x, double v, double* part) {
+  __shared__ double w2[NW];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  if (x.lane == 0) w2[x.warp] = v;
+  __syncthreads();
+  if (x.tid == 0) {
+    double t = 0.0;
+    for (int w = 0; w < NW; ++w) t += w2[w];
+    part[x.cta] = t;
+  }
+  __syncthreads();
 }
 
 // every CTA: max over CTAs of a per-thread value (debug diagnostics)
@@ -534,6 +474,7 @@ __device__ void reduce_bcast(const Ctx& x, const double* part, int E, int nb, do
 // per elimination step.
 __device__ void cholqr_factor(const Ctx& x, double* A, double* X, int k, int ld, double shift) {
   __shared__ double dsc[kMaxBlock];
+  __shared__ double piv[kMaxBlock];
   for (int i = x.tid; i < k; i += NT) {
     const double g = A[i * ld + i];
     dsc[i] = g > 0 ? rsqrt(g) : 1.0;
@@ -562,7 +503,6 @@ __device__ void cholqr_factor(const Ctx& x, double* A, double* X, int k, int ld,
   }
   // X <- M = D E^T P^{-1/2}: M[m][i] = dsc[m] E[i][m] / sqrt(P_i) for m <= i (upper
   // triangular), built in A (only A's diagonal -- the pivots -- is still needed).
-  __shared__ double piv[kMaxBlock];
   for (int i = x.tid; i < k; i += NT) {
     const double p = A[i * ld + i];
     piv[i] = rsqrt(p > 1e-12 ? p : 1e-12);
@@ -577,109 +517,170 @@ __device__ void cholqr_factor(const Ctx& x, double* A, double* X, int k, int ld,
 }
 
 // ----------------------------------------------------------------- Jacobi --
-// Parallel cyclic Jacobi on H (k x k, smem, ld = kp + 1 with kp = k + (k & 1)).
-// Round r of a sweep pairs (kp-1, r) and ((r+i) mod (kp-1), (r-i) mod (kp-1)),
-// i = 1..kp/2-1 (circle method); the kp/2 rotations of a round are disjoint.
-// Per round: [rotation + rows of H and W] barrier [columns of H] barrier.
-// The rotation angle is computed in fp32 (only its accuracy, not the
-// orthogonality of the transform, depends on it: c = rsqrt(1 + t^2) and s = t c
-// are formed in fp64).  W accumulates V^T (row i = eigenvector i).
+// fp64 reciprocal / reciprocal square root from the fp32 approximations plus
+// Newton steps (2 for rcp: 1e-7 -> 1e-14 -> 1e-16; 2 for rsqrt) -- short
+// dependency chains instead of the IEEE division / sqrt sequences.
+__device__ __forceinline__ double rcp_nt(double x) {
+  double r = (double)__frcp_rn((float)x);
+  r = r * fma(-x, r, 2.0);
+  r = r * fma(-x, r, 2.0);
+  return r;
+}
+__device__ __forceinline__ double rsqrt_nt(double x) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  const double hx = 0.5 * x;
+  y = y * fma(-hx * y, y, 1.5);
+  y = y * fma(-hx * y, y, 1.5);
+  return y;
+}
+
+// Parallel cyclic Jacobi on H (k x k, smem, ld = kp + 1 with kp = k + (k & 1)),
+// applied to the Rayleigh-Ritz basis directly: instead of accumulating V, each
+// round's rotations are applied to the columns of nr row vectors QR (and SR),
+// i.e. the CTA's own rows of Q (and S Q), staged in shared memory with stride
+// ldr >= kp.  Round r of a sweep pairs (kp-1, r) and ((r+i) mod (kp-1),
+// (r-i) mod (kp-1)), i = 1..kp/2-1 (circle method): kp/2 disjoint rotations.
+// A round is two flat phases separated by barriers:
+//   1. thread P < kp/2 computes the rotation of pair P (fp64);
+//   2. H <- R H R^T by symmetric 2x2 blocks (pair P rows x pair P' columns,
+//      P <= P', block and its mirror written), and the row vectors' columns
+//      p, q rotated -- independent items over all threads.
+// tau = (a_qq - a_pp) / (2 a_pq), t = sign(tau) / (|tau| + sqrt(1 + tau^2)),
+// c = 1 / sqrt(1 + t^2), s = t c (Golub-Van Loan); c^2 + s^2 = 1 to rounding.
 // On exit theta (smem) holds the eigenvalues in descending order and perm[c]
-// the row of W holding eigenvector c.  Returns the sweeps used (-1: non-finite).
-__device__ int jacobi(const Ctx& x, double* H, double* W, int kin, int max_sweeps, double tol,
-                      double* theta, int* perm) {
+// the column of QR holding Ritz vector c.  Returns the sweeps used (-1:
+// non-finite).  With nr = kp and QR = I the columns of QR are the eigenvectors.
+__device__ int jacobi(const Ctx& x, double* H, int kin, int max_sweeps, double tol, double* theta,
+                      int* perm, double* QR, double* SR, int nr, int ldr, long long* cyc = nullptr) {
   const int kp = kin + (kin & 1);
   const int ld = kp + 1;
   const int np = kp / 2;
   __shared__ double cs_c[kMaxBlock / 2 + 1], cs_s[kMaxBlock / 2 + 1];
   __shared__ int pp[kMaxBlock / 2 + 1], pq[kMaxBlock / 2 + 1];
   __shared__ int bad;
-  (void)0;
-  // dummy index for odd k: zero coupling, -inf diagonal (sorts last)
+  __shared__ unsigned short tri[(kMaxBlock / 2 + 1) * (kMaxBlock / 2 + 2) / 2];
+  long long c0 = 0, c1 = 0;
+  const int ntri = np * (np + 1) / 2;
+  for (int P = x.warp; P < np; P += NW)
+    for (int P2 = P + x.lane; P2 < np; P2 += 32) {
+      const int it = P * np - P * (P - 1) / 2 + (P2 - P);
+      tri[it] = (unsigned short)((P << 8) | P2);
+    }
+  // dummy index for odd k: zero coupling, -inf diagonal (sorts last), zero column
   if (kin & 1) {
     for (int i = x.tid; i < kp; i += NT) {
       H[kin * ld + i] = (i == kin) ? -1e300 : 0.0;
       H[i * ld + kin] = (i == kin) ? -1e300 : 0.0;
     }
+    for (int r = x.tid; r < nr; r += NT) {
+      QR[r * ldr + kin] = 0.0;
+      if (SR) SR[r * ldr + kin] = 0.0;
+    }
   }
-  for (int r = x.warp; r < kp; r += NW)
-    for (int c = x.lane; c < kp; c += 32) W[r * ld + c] = (r == c) ? 1.0 : 0.0;
   __syncthreads();
   const double tol2 = tol * tol;
+  const int nvi = np * nr;  // (pair, row) items of the row vectors
   int sweep = 0;
   for (; sweep < max_sweeps; ++sweep) {
     int any_sweep = 0;
     for (int round = 0; round < kp - 1; ++round) {
+      if (cyc) c0 = clock64();
       int my_act = 0;
-      // lane i of warp w computes the rotation of pair P = w + NW i (fp64), then the
-      // warp applies its pairs' row updates
-      const int npw = x.warp < np ? (np - x.warp + NW - 1) / NW : 0;
-      int p = 0, q = 0;
-      double c = 1.0, s = 0.0;
-      if (x.lane < npw) {
-        const int P = x.warp + NW * x.lane;
+      if (x.tid < np) {
+        const int P = x.tid;
+        int p, q;
         if (P == 0) {
           p = kp - 1;
           q = round;
         } else {
-          p = (round + P) % (kp - 1);
-          q = (round - P + (kp - 1)) % (kp - 1);
+          p = round + P;
+          if (p >= kp - 1) p -= kp - 1;
+          q = round - P;
+          if (q < 0) q += kp - 1;
         }
         const double app = H[p * ld + p], aqq = H[q * ld + q], apq = H[p * ld + q];
+        double c = 1.0, s = 0.0;
         if (apq != 0.0 && apq * apq > tol2 * fabs(app * aqq)) {
-          const double tau = (aqq - app) / (2.0 * apq);
-          const double t = (tau >= 0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(fma(tau, tau, 1.0)));
-          c = 1.0 / sqrt(fma(t, t, 1.0));
-          s = t * c;
+          // u = a_qq - a_pp, v = 2 a_pq, r = hypot(u, v), w = |u| / r = cos(2 theta):
+          // c = sqrt((1 + w) / 2), s = sign(u) v / (2 r c)  (t = s / c is the smaller
+          // root of t^2 + 2 tau t - 1 = 0, tau = u / v) -- two rsqrt, no division
+          const double u = aqq - app, v = 2.0 * apq;
+          const double ri = rsqrt_nt(fma(u, u, v * v));
+          const double h = fma(0.5 * fabs(u), ri, 0.5);
+          const double g = rsqrt_nt(h);  // 1 / c
+          c = h * g;
+          s = copysign(0.5, u) * v * ri * g;
+          my_act = s != 0.0;
         }
         cs_c[P] = c;
         cs_s[P] = s;
         pp[P] = p;
         pq[P] = q;
       }
-      for (int i = 0; i < npw; ++i) {
-        const double ci = __shfl_sync(0xffffffffu, c, i);
-        const double si = __shfl_sync(0xffffffffu, s, i);
-        const int pi = __shfl_sync(0xffffffffu, p, i);
-        const int qi = __shfl_sync(0xffffffffu, q, i);
-        if (si == 0.0) continue;
-        my_act = 1;
-        double* hp = H + pi * ld;
-        double* hq = H + qi * ld;
-        double* wp = W + pi * ld;
-        double* wq = W + qi * ld;
-        for (int j = x.lane; j < kp; j += 32) {
-          const double a = hp[j], b = hq[j];
-          hp[j] = ci * a - si * b;
-          hq[j] = si * a + ci * b;
-          const double u = wp[j], v = wq[j];
-          wp[j] = ci * u - si * v;
-          wq[j] = si * u + ci * v;
-        }
-      }
       const int any = __syncthreads_or(my_act);
+      if (cyc) {
+        c1 = clock64();
+        cyc[0] += c1 - c0;
+      }
       if (!any) continue;
       any_sweep = 1;
-      // columns p, q of H for every pair: item = (pair, row)
-      for (int P = x.warp; P < np; P += NW) {
+      // H blocks (P rows, P2 columns), P <= P2: B' = R_P B R_P2^T (flat triangle)
+      for (int it = x.tid; it < ntri; it += NT) {
+        const int P = tri[it] >> 8, P2 = tri[it] & 255;
+        const double c = cs_c[P], s = cs_s[P];
+        const double c2 = cs_c[P2], s2 = cs_s[P2];
+        if (s == 0.0 && s2 == 0.0) continue;
+        const int p = pp[P], q = pq[P], p2 = pp[P2], q2 = pq[P2];
+        double* hp = H + p * ld;
+        double* hq = H + q * ld;
+        const double b00 = hp[p2], b01 = hp[q2], b10 = hq[p2], b11 = hq[q2];
+        const double t00 = c * b00 - s * b10, t01 = c * b01 - s * b11;
+        const double t10 = s * b00 + c * b10, t11 = s * b01 + c * b11;
+        const double n00 = c2 * t00 - s2 * t01, n01 = s2 * t00 + c2 * t01;
+        const double n10 = c2 * t10 - s2 * t11, n11 = s2 * t10 + c2 * t11;
+        hp[p2] = n00;
+        hp[q2] = n01;
+        hq[p2] = n10;
+        hq[q2] = n11;
+        if (P2 != P) {
+          H[p2 * ld + p] = n00;
+          H[q2 * ld + p] = n01;
+          H[p2 * ld + q] = n10;
+          H[q2 * ld + q] = n11;
+        }
+      }
+      // row vectors: columns p, q of every staged row <- (.) R_P^T
+      for (int it = x.tid; it < nvi; it += NT) {
+        const int P = it / nr, r = it - P * nr;
         const double s = cs_s[P];
         if (s == 0.0) continue;
         const double c = cs_c[P];
+        double* qr = QR + r * ldr;
         const int p = pp[P], q = pq[P];
-        for (int i = x.lane; i < kp; i += 32) {
-          const double a = H[i * ld + p], b = H[i * ld + q];
-          H[i * ld + p] = c * a - s * b;
-          H[i * ld + q] = s * a + c * b;
+        const double a = qr[p], b = qr[q];
+        qr[p] = c * a - s * b;
+        qr[q] = s * a + c * b;
+        if (SR) {
+          double* sr = SR + r * ldr;
+          const double u = sr[p], v = sr[q];
+          sr[p] = c * u - s * v;
+          sr[q] = s * u + c * v;
         }
       }
       __syncthreads();
+      if (cyc) {
+        c0 = clock64();
+        cyc[1] += c0 - c1;
+        cyc[5] += 1;
+      }
     }
     if (!any_sweep) break;
   }
   // sort descending (stable by index)
   if (x.tid == 0) bad = 0;
   __syncthreads();
-  if (x.tid < kp && !isfinite(H[x.tid * ld + x.tid]) && x.tid < kin) bad = 1;
+  if (x.tid < kin && !isfinite(H[x.tid * ld + x.tid])) bad = 1;
   __syncthreads();
   if (x.tid < kp) {
     const double dv = H[x.tid * ld + x.tid];
@@ -700,11 +701,12 @@ __device__ int jacobi(const Ctx& x, double* H, double* W, int kin, int max_sweep
 
 // -------------------------------------------------------------- the solver --
 __global__ void __launch_bounds__(NT, 1) k_eig_fused(FusedArgs P) {
-  extern __shared__ __align__(16) double smem[];
+  extern __shared__ __align__(128) double smem[];
   __shared__ double th[kMaxBlock + 2];    // Ritz values of the active block (indices nlock..)
   __shared__ double rs[kMaxBlock + 2];    // residuals
   __shared__ double thl[kMaxJ + 2];       // locked Ritz values
   __shared__ int perm[kMaxBlock + 2];
+  __shared__ int src_of[kMaxBlock + 2];
 
   Ctx x;
   x.cta = blockIdx.x;
@@ -713,7 +715,13 @@ __global__ void __launch_bounds__(NT, 1) k_eig_fused(FusedArgs P) {
   x.warp = x.tid >> 5;
   x.lane = x.tid & 31;
   x.d = P.d;
-  const int d = P.d, J = P.J, k = P.k;
+  x.ls = P.ls;
+  x.lb = P.lb;
+  x.mv_m8 = P.mv_m8;
+  x.mv_rb = P.mv_rb;
+  x.mv_kb = P.mv_kb;
+  x.mv_kc = P.mv_kc;
+  const int d = P.d, J = P.J, k = P.k, LB = P.lb;
   const int R = (d + x.G - 1) / x.G;
   x.r0 = min(d, x.cta * R);
   x.r1 = min(d, x.r0 + R);
@@ -741,75 +749,89 @@ __global__ void __launch_bounds__(NT, 1) k_eig_fused(FusedArgs P) {
     }
   };
 
-  if (P.warm) copy_cols(x, P.basis, k, B(iQ), k, k);
-  else fill_random(x, B(iQ), k, P.seed);
+  zero_padding(x, S, P.rp, P.blk);
+  if (P.warm) copy_cols(x, P.basis, LB, B(iQ), LB, k);
+  else fill_random(x, B(iQ), LB, k, P.seed);
   __syncthreads();
 
-  // ---- orthonormalise the active block (ld = ka) against L and itself
+  auto mv = [&](const double* Y, double alpha, double* Out, double gamma, const double* Dm, double delta,
+                const double* Em) {
+    gsync();  // Y, D, E (and S) complete
+    matvec(x, P.mpart, S, Y, ka, alpha, Out, gamma, Dm, delta, Em);  // own rows of Out on return
+    ++matvecs;
+    tick(PF_MV);
+  };
+
+  // ---- orthonormalise the active block against L and itself
   auto orth_active = [&](int passes, bool project) {
     if (nlock > 0 && project) {
       for (int pass = 0; pass < 2; ++pass) {
-        gram_partial(x, P.L, J, nlock, B(iQ), ka, ka, P.part);
+        gram_partial(x, P.L, J, nlock, B(iQ), LB, ka, P.part);
         reduce_bcast(x, P.part, nlock * ka, ka, P.red, x.r2s, ka);
         tick(PF_RED);
         // Q[own] -= L[own] Z  (Z = r2s, nlock x ka, ld ka)
         for (int r = x.r0 + x.warp; r < x.r1; r += NW)
           for (int c = x.lane; c < ka; c += 32) {
-          double s = 0.0;
-          for (int l = 0; l < nlock; ++l) s = fma(P.L[(int64_t)r * J + l], x.r2s[l * ka + c], s);
-          B(iQ)[(int64_t)r * ka + c] -= s;
-        }
+            double s = 0.0;
+            for (int l = 0; l < nlock; ++l) s = fma(P.L[(int64_t)r * J + l], x.r2s[l * ka + c], s);
+            B(iQ)[(int64_t)r * LB + c] -= s;
+          }
         __syncthreads();
       }
     }
     const double shift = 11.0 * ((double)d * ka + (double)ka * (ka + 1)) * 1.1e-16 * ka;
     for (int pass = 0; pass < passes; ++pass) {
-      gram_partial(x, B(iQ), ka, ka, B(iQ), ka, ka, P.part);
+      gram_partial(x, B(iQ), LB, ka, B(iQ), LB, ka, P.part);
       reduce_bcast(x, P.part, ka * ka, ka, P.red, x.r1s, ld);
       tick(PF_RED);
-      cholqr_factor(x, x.r1s, x.r2s, ka, ld, (pass == 0 && !P.noshift) ? shift : 0.0);
+      cholqr_factor(x, x.r1s, x.r2s, ka, ld, pass == 0 ? shift : 0.0);
       tick(PF_CHOL);
-      // stage rows in the tail of region 1 beyond the k x k block? region 1 is free now
-      apply_right(x, B(iQ), ka, ka, x.r2s, ld, 0, nullptr, B(iQ), ka, ka, x.r1s);
+      apply_right(x, B(iQ), LB, ka, x.r2s, ld, 0, nullptr, B(iQ), LB, ka, x.r1s);
       tick(PF_APPLY);
     }
   };
 
   // ---- Rayleigh-Ritz on the active block: Q <- Q V, SQ <- S Q V, th, rs
   auto rayleigh_ritz = [&]() {
-    gsync();  // Q complete
-    matvec(x, S, B(iQ), ka, 1.0, B(iSQ), 0.0, nullptr, 0.0, nullptr);
-    gsync();  // SQ complete (the product is tiled, not row-local)
-    tick(PF_MV);
-    ++matvecs;
-    gram_partial(x, B(iQ), ka, ka, B(iSQ), ka, ka, P.part);
-    reduce_bcast(x, P.part, ka * ka, ka, P.red, x.r1s, ka + (ka & 1) + 1);
+    mv(B(iQ), 1.0, B(iSQ), 0.0, nullptr, 0.0, nullptr);
+    gram_partial(x, B(iQ), LB, ka, B(iSQ), LB, ka, P.part);
+    const int kk = ka + (ka & 1);
+    reduce_bcast(x, P.part, ka * ka, ka, P.red, x.r1s, kk + 1);
     tick(PF_RED);
-    {
-      const int kk = ka + (ka & 1);
-      // symmetrise
-      for (int r = x.warp; r < ka; r += NW)
-        for (int c = x.lane; c < ka; c += 32) {
+    for (int r = x.warp; r < ka; r += NW)
+      for (int c = x.lane; c < ka; c += 32)
         if (r < c) {
           const double v = 0.5 * (x.r1s[r * (kk + 1) + c] + x.r1s[c * (kk + 1) + r]);
           x.r1s[r * (kk + 1) + c] = v;
           x.r1s[c * (kk + 1) + r] = v;
         }
+    __syncthreads();
+    // stage own rows of Q and SQ (region 2); the Jacobi rotations are applied to them
+    const int nrr = x.r1 - x.r0;
+    const int ldr = kk + 1;
+    double* QR = x.r2s;
+    double* SR = x.r2s + (size_t)nrr * ldr;
+    for (int r = x.warp; r < nrr; r += NW)
+      for (int c = x.lane; c < ka; c += 32) {
+        QR[r * ldr + c] = B(iQ)[(int64_t)(x.r0 + r) * LB + c];
+        SR[r * ldr + c] = B(iSQ)[(int64_t)(x.r0 + r) * LB + c];
       }
-      __syncthreads();
-      const int sw = jacobi(x, x.r1s, x.r2s, ka, k == d ? 60 : (n_rr == 0 ? P.jsweeps + 1 : P.jsweeps),
-                            k == d ? 1e-15 : 1e-13, th + nlock, perm);
-      tick(PF_JAC);
-      if (sw < 0) breakdown = 1;
-      else jsw += sw;
-      ++n_rr;
-      // Q <- Q V, SQ <- SQ V (V(l, c) = W[perm[c]][l]); staging in region 1 (H is dead)
-      apply_right(x, B(iQ), ka, ka, x.r2s, kk + 1, 1, perm, B(iQ), ka, ka, x.r1s);
-      tick(PF_APPLY);
-      apply_right(x, B(iSQ), ka, ka, x.r2s, kk + 1, 1, perm, B(iSQ), ka, ka, x.r1s);
-      tick(PF_APPLY);
-    }
-    // residual partials
+    __syncthreads();
+    const int sw = jacobi(x, x.r1s, ka, k == d ? 60 : (n_rr == 0 ? P.jsweeps + 1 : P.jsweeps),
+                          k == d ? 1e-15 : 1e-13, th + nlock, perm, QR, SR, nrr, ldr);
+    tick(PF_JAC);
+    if (sw < 0) breakdown = 1;
+    else jsw += sw;
+    ++n_rr;
+    // Q <- Q V, SQ <- SQ V: the rotated staged rows, columns in descending Ritz order
+    for (int r = x.warp; r < nrr; r += NW)
+      for (int c = x.lane; c < ka; c += 32) {
+        B(iQ)[(int64_t)(x.r0 + r) * LB + c] = QR[r * ldr + perm[c]];
+        B(iSQ)[(int64_t)(x.r0 + r) * LB + c] = SR[r * ldr + perm[c]];
+      }
+    __syncthreads();
+    tick(PF_APPLY);
+    // residual partials ||SQ_c - theta_c Q_c||^2 over own rows
     {
       const int nr = x.r1 - x.r0;
       double* out = P.part + (size_t)x.cta * ka;
@@ -817,7 +839,7 @@ __global__ void __launch_bounds__(NT, 1) k_eig_fused(FusedArgs P) {
         const double t = th[nlock + c];
         double s = 0.0;
         for (int r = 0; r < nr; ++r) {
-          const int64_t o = (int64_t)(x.r0 + r) * ka + c;
+          const int64_t o = (int64_t)(x.r0 + r) * LB + c;
           const double v = B(iSQ)[o] - t * B(iQ)[o];
           s = fma(v, v, s);
         }
@@ -844,21 +866,21 @@ __global__ void __launch_bounds__(NT, 1) k_eig_fused(FusedArgs P) {
     tick(PF_RED);
     for (int r = x.r0 + x.warp; r < x.r1; r += NW)
       for (int c = x.lane; c < nl; c += 32) {
-      double s = 0.0;
-      for (int l = 0; l < nl; ++l) s = fma(P.L[(int64_t)r * J + n0 + l], x.r2s[l * nl + c], s);
-      Wd[(int64_t)r * nl + c] = P.LT[(int64_t)r * J + n0 + c] - 0.5 * s;
-    }
+        double s = 0.0;
+        for (int l = 0; l < nl; ++l) s = fma(P.L[(int64_t)r * J + n0 + l], x.r2s[l * nl + c], s);
+        Wd[(int64_t)r * nl + c] = P.LT[(int64_t)r * J + n0 + c] - 0.5 * s;
+      }
     gsync();  // W complete
     // S[own rows][j] -= sum_l Ln[r][l] W[j][l] + W[r][l] Ln[j][l], rows in chunks of 8
     double* lrs = x.r1s;           // [8][nl]
     double* wrs = x.r1s + 8 * nl;  // [8][nl]
     for (int rc = x.r0; rc < x.r1; rc += 8) {
       const int n8 = min(8, x.r1 - rc);
-      for (int e = x.tid; e < 8 * nl; e += NT) {
-        const int i = e / nl, l = e % nl;
-        lrs[e] = i < n8 ? P.L[(int64_t)(rc + i) * J + n0 + l] : 0.0;
-        wrs[e] = i < n8 ? Wd[(int64_t)(rc + i) * nl + l] : 0.0;
-      }
+      for (int i = x.warp; i < 8; i += NW)
+        for (int l = x.lane; l < nl; l += 32) {
+          lrs[i * nl + l] = i < n8 ? P.L[(int64_t)(rc + i) * J + n0 + l] : 0.0;
+          wrs[i * nl + l] = i < n8 ? Wd[(int64_t)(rc + i) * nl + l] : 0.0;
+        }
       __syncthreads();
       for (int j = x.tid; j < d; j += NT) {
         double acc[8];
@@ -870,10 +892,11 @@ __global__ void __launch_bounds__(NT, 1) k_eig_fused(FusedArgs P) {
 #pragma unroll
           for (int i = 0; i < 8; ++i) acc[i] = fma(lrs[i * nl + l], w, fma(wrs[i * nl + l], lv, acc[i]));
         }
-        for (int i = 0; i < n8; ++i) S[(int64_t)(rc + i) * d + j] -= acc[i];
+        for (int i = 0; i < n8; ++i) S[(int64_t)(rc + i) * x.ls + j] -= acc[i];
       }
       __syncthreads();
     }
+    tick(PF_DEFL);
   };
 
   // move the converged leading active vectors into L (prefix, descending order)
@@ -882,24 +905,19 @@ __global__ void __launch_bounds__(NT, 1) k_eig_fused(FusedArgs P) {
     const double th1 = theta1();
     while (nlock + nl < J && nl < ka && rs[nlock + nl] <= P.tol * th1) ++nl;
     if (nl == 0) return;
-    if (P.nolock && nlock + nl < J) return;  // debug: lock only when everything converged
-    copy_cols(x, B(iQ), ka, P.L + nlock, J, nl);
-    copy_cols(x, B(iSQ), ka, P.LT + nlock, J, nl);
+    copy_cols(x, B(iQ), LB, P.L + nlock, J, nl);
+    copy_cols(x, B(iSQ), LB, P.LT + nlock, J, nl);
     for (int i = x.tid; i < nl; i += NT) thl[nlock + i] = th[nlock + i];
     __syncthreads();
-    if (!P.nodefl) deflate(nlock, nl);
-    tick(PF_DEFL);
+    deflate(nlock, nl);
     const int kn = ka - nl;
-    // compact Q and SQ into two spare blocks: the new leading dimension makes a
-    // CTA's rows overlap other CTAs' old rows, so no block may be rewritten in a
-    // new layout before every CTA has finished reading it (grid barrier)
-    if (kn > 0) {
-      copy_cols(x, B(iQ) + nl, ka, B(iT), kn, kn);
-      copy_cols(x, B(iSQ) + nl, ka, B(iY), kn, kn);
+    if (kn > 0) {  // compact the active block (row-local; same stride)
+      copy_cols(x, B(iQ) + nl, LB, B(iT), LB, kn);
+      copy_cols(x, B(iSQ) + nl, LB, B(iY), LB, kn);
       { int t = iQ; iQ = iT; iT = t; }
       { int t = iSQ; iSQ = iY; iY = t; }
     }
-    gsync();
+    __syncthreads();
     nlock += nl;
     ka = kn;
   };
@@ -914,11 +932,10 @@ __global__ void __launch_bounds__(NT, 1) k_eig_fused(FusedArgs P) {
     npow = min(npow, 40);
     double* pq_ = P.pvec[0];
     double* py_ = P.pvec[1];
-    copy_cols(x, B(iQ), ka, pq_, 1, 1);
+    copy_cols(x, B(iQ), LB, pq_, 1, 1);
     gsync();
     for (int i = 0; i < npow; ++i) {
       matvec1(x, S, pq_, py_, P.part);
-      tick(PF_MV);
       ++matvecs;
       gsync();
       const double nrm = allsum_scalar(x, P.part);
@@ -927,45 +944,24 @@ __global__ void __launch_bounds__(NT, 1) k_eig_fused(FusedArgs P) {
       gsync();
     }
     matvec1(x, S, pq_, py_, P.part);
-    tick(PF_MV);
-    // theta = q^T y, ||y - theta q||
     {
-      __shared__ double w2[NW];
       double s = 0.0;
       for (int r = x.r0 + x.tid; r < x.r1; r += NT) s = fma(pq_[r], py_[r], s);
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-      if (x.lane == 0) w2[x.warp] = s;
-      __syncthreads();
-      if (x.tid == 0) {
-        double t = 0.0;
-        for (int w = 0; w < NW; ++w) t += w2[w];
-        P.part[x.G + x.cta] = t;
-      }
-      __syncthreads();
+      block_partial(x, s, P.part + x.G);
     }
     gsync();
     const double th0 = allsum_scalar(x, P.part + x.G);
     {
-      __shared__ double w3[NW];
       double s = 0.0;
       for (int r = x.r0 + x.tid; r < x.r1; r += NT) {
         const double v = py_[r] - th0 * pq_[r];
         s = fma(v, v, s);
       }
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-      if (x.lane == 0) w3[x.warp] = s;
-      __syncthreads();
-      if (x.tid == 0) {
-        double t = 0.0;
-        for (int w = 0; w < NW; ++w) t += w3[w];
-        P.part[2 * x.G + x.cta] = t;
-      }
-      __syncthreads();
+      block_partial(x, s, P.part + 2 * x.G);
     }
     gsync();
     const double r0v = sqrt(allsum_scalar(x, P.part + 2 * x.G));
+    tick(PF_POW);
     if (P.dbg && x.cta == 0 && x.tid == 0)
       printf("[eigf] power-lock npow=%d th0=%.9e res=%.3e (tol %.3e)\n", npow, th0, r0v, P.tol * th0);
     if (!(r0v <= P.tol * th0)) return;
@@ -978,11 +974,10 @@ __global__ void __launch_bounds__(NT, 1) k_eig_fused(FusedArgs P) {
     }
     __syncthreads();
     deflate(0, 1);
-    tick(PF_DEFL);
     const int kn = ka - 1;
-    copy_cols(x, B(iQ) + 1, ka, B(iT), kn, kn);
+    copy_cols(x, B(iQ) + 1, LB, B(iT), LB, kn);
     { int t = iQ; iQ = iT; iT = t; }
-    gsync();  // layout change (see lock)
+    __syncthreads();
     nlock = 1;
     ka = kn;
     orth_active(2, true);
@@ -1002,32 +997,21 @@ __global__ void __launch_bounds__(NT, 1) k_eig_fused(FusedArgs P) {
   int outer = 0;
   for (; outer < P.max_outer && !converged && !breakdown; ++outer) {
     if (P.dbg && nlock > 0) {
-      // diagnostics: |L^T Q|, |S L|, |SQ - S Q|
-      gram_partial(x, P.L, J, nlock, B(iQ), ka, ka, P.part);
+      // diagnostics: |L^T Q| and |SQ - S Q| (the state the filter starts from)
+      gram_partial(x, P.L, J, nlock, B(iQ), LB, ka, P.part);
       reduce_bcast(x, P.part, nlock * ka, ka, P.red, x.r2s, ka);
       double m1 = 0.0;
       for (int e = x.tid; e < nlock * ka; e += NT) m1 = fmax(m1, fabs(x.r2s[e]));
       m1 = gmax(x, m1, P.part);
-      gsync();
-      matvec(x, S, P.L, J, 1.0, B(iT), 0.0, nullptr, 0.0, nullptr);
-      gsync();
-      double m2 = 0.0;
+      mv(B(iQ), 1.0, B(iT), 0.0, nullptr, 0.0, nullptr);
+      --matvecs;
+      double m3 = 0.0;
       for (int r = x.r0; r < x.r1; ++r)
-        for (int c = x.tid; c < nlock; c += NT) m2 = fmax(m2, fabs(B(iT)[(int64_t)r * J + c]));
-      m2 = gmax(x, m2, P.part);
-      matvec(x, S, B(iQ), ka, 1.0, B(iT), 0.0, nullptr, 0.0, nullptr);
-      gsync();
-      double m3 = 0.0, m4 = 0.0;
-      for (int r = x.r0; r < x.r1; ++r)
-        for (int c = x.tid; c < ka; c += NT) {
-          m3 = fmax(m3, fabs(B(iT)[(int64_t)r * ka + c] - B(iSQ)[(int64_t)r * ka + c]));
-          m4 = fmax(m4, fabs(B(iT)[(int64_t)r * ka + c]));
-        }
+        for (int c = x.tid; c < ka; c += NT)
+          m3 = fmax(m3, fabs(B(iT)[(int64_t)r * LB + c] - B(iSQ)[(int64_t)r * LB + c]));
       m3 = gmax(x, m3, P.part);
-      m4 = gmax(x, m4, P.part);
       if (x.cta == 0 && x.tid == 0)
-        printf("[eigf-chk] outer=%d nlock=%d ka=%d |L^T Q|=%.3e |S L|=%.3e |SQ - S Q|=%.3e (|S Q|=%.3e)\n", outer,
-               nlock, ka, m1, m2, m3, m4);
+        printf("[eigf-chk] outer=%d nlock=%d ka=%d |L^T Q|=%.3e |SQ - S Q|=%.3e\n", outer, nlock, ka, m1, m3);
     }
     const double th1 = theta1();
     const double thJ = th[J - 1];
@@ -1042,42 +1026,34 @@ __global__ void __launch_bounds__(NT, 1) k_eig_fused(FusedArgs P) {
     const double rJ = acosh(xJ), rt = acosh(xt);
     double rmax = 0;
     for (int i = nlock; i < J; ++i) rmax = fmax(rmax, rs[i] / th1);
+    // total degree to reach tol (capped), in segments of <= m_amp degrees with an
+    // orthonormalisation between them (T_m(x_top) <= 2e7 keeps CholQR in reach)
     int m_need = (int)ceil(log(fmax(rmax / P.tol, 4.0)) / fmax(rJ, 1e-6));
     const int m_amp = max(1, min(16, (int)floor(log(2e7) / fmax(rt, 1e-6))));
     m_need = max(1, min(min(m_need, 64), (m_amp < 6 ? 2 : 8) * m_amp));
     for (int done = 0; done < m_need;) {
       const int mseg = min(m_amp, m_need - done);
+      // scaled Chebyshev recurrence (Zhou & Saad) damping [a, b], normalised at thtop
       double sigma = e / (thtop - c);
       const double tau = 2.0 / sigma;
-      if (done > 0) {
-        gsync();
-        matvec(x, S, B(iQ), ka, 1.0, B(iSQ), 0.0, nullptr, 0.0, nullptr);
-        gsync();
-        tick(PF_MV);
-        ++matvecs;
-      }
-      axpby(x, ka, sigma / e, B(iSQ), -c * sigma / e, B(iQ), B(iY));
+      if (done > 0) mv(B(iQ), 1.0, B(iSQ), 0.0, nullptr, 0.0, nullptr);
+      axpby(x, ka, LB, sigma / e, B(iSQ), -c * sigma / e, B(iQ), B(iY));
       int iXp = iQ, iYp = iY;
       int spare[2] = {iX, iT};
       int si = 0;
       for (int i = 2; i <= mseg; ++i) {
         const double sigma2 = 1.0 / (tau - sigma);
         const int iTp = spare[si];
-        gsync();
-        matvec(x, S, B(iYp), ka, 2 * sigma2 / e, B(iTp), -sigma * sigma2, B(iXp), -2 * sigma2 * c / e,
-               B(iYp));
-        tick(PF_MV);
-        ++matvecs;
+        // T_i = 2 sigma2 / e (S T_{i-1} - c T_{i-1}) - sigma sigma2 T_{i-2}
+        mv(B(iYp), 2 * sigma2 / e, B(iTp), -sigma * sigma2, B(iXp), -2 * sigma2 * c / e, B(iYp));
         spare[si] = iXp;
         si ^= 1;
         iXp = iYp;
         iYp = iTp;
         sigma = sigma2;
       }
-      if (mseg > 1) gsync();  // the filtered block is complete before row-local use
-      // the filtered block becomes Q: swap roles so that iQ names it
+      // the filtered block becomes Q (the five role indices stay a permutation)
       if (iYp != iQ) {
-        // the five indices stay a permutation: exchange iQ with the holder of the result
         if (iYp == iY) { int t = iQ; iQ = iY; iY = t; }
         else if (iYp == iX) { int t = iQ; iQ = iX; iX = t; }
         else { int t = iQ; iQ = iT; iT = t; }
@@ -1099,7 +1075,6 @@ __global__ void __launch_bounds__(NT, 1) k_eig_fused(FusedArgs P) {
   }
 
   // outputs: the J leading columns of [L | A], sorted by Ritz value (descending)
-  __shared__ int src_of[kMaxBlock + 2];
   {
     const int nc = nlock + ka;
     for (int i = x.tid; i < nc; i += NT) {
@@ -1113,17 +1088,14 @@ __global__ void __launch_bounds__(NT, 1) k_eig_fused(FusedArgs P) {
     }
   }
   __syncthreads();
-  {
-    for (int r = x.r0 + x.warp; r < x.r1; r += NW)
-      for (int j = x.lane; j < J; j += 32) {
+  for (int r = x.r0 + x.warp; r < x.r1; r += NW) {
+    for (int j = x.lane; j < J; j += 32) {
       const int s = src_of[j];
-      P.outV[(int64_t)r * J + j] = s < nlock ? P.L[(int64_t)r * J + s] : B(iQ)[(int64_t)r * ka + (s - nlock)];
+      P.outV[(int64_t)r * J + j] = s < nlock ? P.L[(int64_t)r * J + s] : B(iQ)[(int64_t)r * LB + (s - nlock)];
     }
     // warm-start basis [L | A]
-    for (int r = x.r0 + x.warp; r < x.r1; r += NW)
-      for (int c = x.lane; c < k; c += 32) {
-      P.basis[(int64_t)r * k + c] = c < nlock ? P.L[(int64_t)r * J + c] : B(iQ)[(int64_t)r * ka + (c - nlock)];
-    }
+    for (int c = x.lane; c < k; c += 32)
+      P.basis[(int64_t)r * LB + c] = c < nlock ? P.L[(int64_t)r * J + c] : B(iQ)[(int64_t)r * LB + (c - nlock)];
   }
   if (x.cta == 0) {
     for (int j = x.tid; j < J; j += NT) {
@@ -1141,11 +1113,13 @@ __global__ void __launch_bounds__(NT, 1) k_eig_fused(FusedArgs P) {
   }
 }
 
-// Unit-test kernel for the tiled product: Out = alpha S Y + gamma D (all CTAs).
+// Unit-test kernel for the product on the padded layout (cooperative, all CTAs):
+// Out = alpha S Y + gamma D, repeated `reps` times.
 __global__ void __launch_bounds__(NT, 1) k_eigf_unit_mv(const double* S, const double* Y, int d, int n,
-                                                       double alpha, double* Out, double gamma,
-                                                       const double* D, int reps) {
-  extern __shared__ __align__(16) double smem[];
+                                                       int ls, int lb, double alpha, double* Out,
+                                                       double gamma, const double* D, double* mpart,
+                                                       int reps, MvPlan pl) {
+  extern __shared__ __align__(128) double smem[];
   Ctx x;
   x.cta = blockIdx.x;
   x.G = gridDim.x;
@@ -1153,10 +1127,21 @@ __global__ void __launch_bounds__(NT, 1) k_eigf_unit_mv(const double* S, const d
   x.warp = x.tid >> 5;
   x.lane = x.tid & 31;
   x.d = d;
-  x.r0 = x.r1 = 0;
+  const int R = (d + x.G - 1) / x.G;
+  x.r0 = min(d, x.cta * R);
+  x.r1 = min(d, x.r0 + R);
+  x.ls = ls;
+  x.lb = lb;
+  x.mv_m8 = pl.m8;
+  x.mv_rb = pl.RB;
+  x.mv_kb = pl.KB;
+  x.mv_kc = pl.kchunk;
   x.r1s = smem;
   x.r2s = smem;
-  for (int i = 0; i < reps; ++i) matvec(x, S, Y, n, alpha, Out, gamma, D, 0.0, nullptr);
+  for (int i = 0; i < reps; ++i) {
+    gsync();
+    matvec(x, mpart, S, Y, n, alpha, Out, gamma, D, 0.0, nullptr);
+  }
 }
 
 // Unit-test kernel for the k x k device routines (one CTA): mode 0 -> CholQR
@@ -1164,7 +1149,7 @@ __global__ void __launch_bounds__(NT, 1) k_eigf_unit_mv(const double* S, const d
 // eigenvectors in columns, theta = eigenvalues descending, iout[0] = sweeps).
 __global__ void __launch_bounds__(NT, 1) k_eigf_unit(int mode, const double* in, int k, double* out,
                                                     double* theta, int* iout, int sweeps, double shift) {
-  extern __shared__ __align__(16) double smem[];
+  extern __shared__ __align__(128) double smem[];
   __shared__ double th[kMaxBlock + 2];
   __shared__ int perm[kMaxBlock + 2];
   Ctx x;
@@ -1176,6 +1161,8 @@ __global__ void __launch_bounds__(NT, 1) k_eigf_unit(int mode, const double* in,
   x.d = k;
   x.r0 = 0;
   x.r1 = k;
+  x.ls = x.lb = 0;
+  x.mv_m8 = x.mv_rb = x.mv_kb = x.mv_kc = 0;
   const int kp = k + (k & 1), ld = kp + 1;
   x.r1s = smem;
   x.r2s = smem + (size_t)kp * ld;
@@ -1187,48 +1174,90 @@ __global__ void __launch_bounds__(NT, 1) k_eigf_unit(int mode, const double* in,
     for (int r = x.warp; r < k; r += NW)
       for (int c = x.lane; c < k; c += 32) out[r * k + c] = x.r2s[r * ld + c];
   } else {
-    const int sw = jacobi(x, x.r1s, x.r2s, k, sweeps, 1e-13, th, perm);
+    long long cyc[6] = {0, 0, 0, 0, 0, 0};
+    double* QR = x.r2s;  // identity rows: the rotated rows are V
+    for (int r = x.warp; r < kp; r += NW)
+      for (int c = x.lane; c < kp; c += 32) QR[r * ld + c] = (r == c) ? 1.0 : 0.0;
+    __syncthreads();
+    const long long t0 = clock64();
+    const int nrows = mode == 2 ? 8 : kp;  // mode 2: timing with a solver-like row count
+    const int sw = jacobi(x, x.r1s, k, sweeps, 1e-13, th, perm, QR, mode == 2 ? QR + 8 * ld : nullptr, nrows, ld,
+                          x.tid == 0 ? cyc : nullptr);
+    const long long t1 = clock64();
+    if (x.tid == 0) {
+      for (int i = 0; i < 6; ++i) iout[1 + i] = (int)cyc[i];
+      iout[7] = (int)(t1 - t0);
+    }
     for (int r = x.warp; r < k; r += NW)
-      for (int c = x.lane; c < k; c += 32) out[r * k + c] = x.r2s[perm[c] * ld + r];
+      for (int c = x.lane; c < k; c += 32) out[r * k + c] = QR[r * ld + perm[c]];
     for (int i = x.tid; i < k; i += NT) theta[i] = th[i];
     if (x.tid == 0) iout[0] = sw;
   }
 }
 
+int choose_block(int J, int64_t d, int oversample) {
+  int k = J + (oversample > 0 ? oversample : std::max(8, std::min(J, 32)));
+  if (k > kMaxBlock) k = kMaxBlock;
+  if (k > d) k = (int)d;
+  if (k & 1) k = (k + 1 <= kMaxBlock && k + 1 <= d) ? k + 1 : k - 1;
+  if (k < J) k = J;
+  return k;
+}
+
+int num_sms() {
+  static int nsm = 0;
+  if (nsm == 0) {
+    int dev = 0;
+    TK_CUDA(cudaGetDevice(&dev));
+    TK_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+  }
+  return nsm;
+}
+
+size_t product_smem(int d, int kmax, int G) {
+  const MvPlan pl = mv_plan(d, G);
+  return mv_smem_doubles(pl.m8, (kmax + 7) / 8) * sizeof(double);
+}
+
+size_t product_part_doubles(int d, int lb, int G) {
+  const MvPlan pl = mv_plan(d, G);
+  const int rpx = (d + 8 * pl.m8 - 1) / (8 * pl.m8) * (8 * pl.m8);
+  return (size_t)pl.KB * rpx * lb;
+}
+
+void launch_unit_mv(const double* S, const double* Y, int d, int n, int ls, int lb, double alpha, double* O,
+                    double gamma, const double* D, double* mpart, int reps, cudaStream_t st) {
+  const int G = num_sms();
+  const size_t smem = product_smem(d, n, G);
+  TK_CUDA(cudaFuncSetAttribute(k_eigf_unit_mv, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  MvPlan pl = mv_plan(d, G);
+  void* args[] = {&S, &Y, &d, &n, &ls, &lb, &alpha, &O, &gamma, &D, &mpart, &reps, &pl};
+  TK_CUDA(cudaLaunchCooperativeKernel((const void*)k_eigf_unit_mv, dim3(G), dim3(NT), args, smem, st));
+}
+
 }  // namespace
+
+void eig_layout(int64_t d, int64_t* ls, int64_t* rows) {
+  const int64_t l = round_up(d, KCH);
+  if (ls) *ls = l;
+  if (rows) *rows = l + 64;
+}
 
 size_t eig_fused_smem(int k, int d, int G) {
   const int kp = k + (k & 1);
-  const int R = (int)((d + G - 1) / G);
-  const size_t jac = (region1_doubles(kp, R) + (size_t)kp * (kp + 1)) * sizeof(double);
-  // product: the largest plan over the active widths n <= k
-  size_t mv = 0;
-  for (int n = 1; n <= k; ++n) {
-    const MvPlan pl = mv_plan(d, n, G);
-    const int ng = (pl.tpb + 1) / 2, KS = NW / ng;
-    const size_t st = mv_smem_doubles(pl.m8, pl.tpb);
-    const size_t ep = (size_t)KS * 8 * pl.m8 * 8 * pl.tpb;
-    mv = std::max(mv, std::max(st, ep) * sizeof(double));
-  }
+  const int R = (d + G - 1) / G;
+  const size_t r2 = std::max((size_t)kp * (kp + 1), (size_t)2 * R * (kp + 1));  // H, W or staged Q/SQ rows
+  const size_t jac = (region1_doubles(kp, R) + r2) * sizeof(double);
+  const size_t mv = product_smem(d, k, G);
   const size_t gp = (size_t)R * 2 * kp * sizeof(double);
   return std::max(jac, std::max(mv, gp));
 }
 
 bool eig_fused(double* S, int64_t d, int J, EigSlot& slot, EigWs& ws, const EigOpts& o, double* out_V,
                double* theta_dev, int* info_dev, cudaStream_t st) {
-  static int nsm = 0;
   static size_t smem_set = 0;
-  int k = J + (o.oversample > 0 ? o.oversample : std::max(8, std::min(J, 32)));
-  if (k > kMaxBlock) k = kMaxBlock;
-  if (k > d) k = (int)d;
-  if (k & 1) k = (k + 1 <= kMaxBlock && k + 1 <= d) ? k + 1 : k - 1;
-  if (k < J) k = J;
-  if (nsm == 0) {
-    int dev = 0;
-    TK_CUDA(cudaGetDevice(&dev));
-    TK_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
-  }
-  const int grid = nsm;  // one CTA per SM (cooperative: all co-resident)
+  const int k = choose_block(J, d, o.oversample);
+  const int grid = num_sms();  // one CTA per SM (cooperative: all co-resident)
   const size_t smem = eig_fused_smem(k, (int)d, grid);
   if (smem + 8 * 1024 > 227 * 1024) fail(TUCKER_E_ARG, "eig_fused: block too large for shared memory");
   if (smem > smem_set) {
@@ -1240,24 +1269,36 @@ bool eig_fused(double* S, int64_t d, int J, EigSlot& slot, EigWs& ws, const EigO
     TK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_eig_fused, NT, smem));
     if (per < 1) fail(TUCKER_E_CUDA, "eig_fused: kernel cannot be resident");
   }
-  const size_t dk = (size_t)d * k;
-  ws.Q.ensure(dk);
-  ws.SQ.ensure(dk);
-  ws.X.ensure(dk);
-  ws.Y.ensure(dk);
-  ws.T.ensure(dk);
+  int64_t LS = 0, RP = 0;
+  eig_layout(d, &LS, &RP);
+  const int LB = k + (k & 1);
+  const size_t blk = (size_t)RP * LB + 64;
+  ws.Q.ensure(blk);
+  ws.SQ.ensure(blk);
+  ws.X.ensure(blk);
+  ws.Y.ensure(blk);
+  ws.T.ensure(blk);
   ws.L.ensure((size_t)d * J);
   ws.LT.ensure((size_t)d * J);
   ws.fpart.ensure((size_t)grid * std::max<size_t>((size_t)k * k, 3));
   ws.fred.ensure((size_t)k * k);
   ws.pq.ensure((size_t)d);
   ws.py.ensure((size_t)d);
-  slot.basis.ensure(dk);
+  ws.fprof.ensure(8);
+  if (!ws.fprof_init) {
+    TK_CUDA(cudaMemsetAsync(ws.fprof.p, 0, 8 * sizeof(long long), st));
+    ws.fprof_init = true;
+  }
+  slot.basis.ensure((size_t)d * LB);
+  ws.mpart.ensure(product_part_doubles((int)d, LB, grid));
   FusedArgs a;
   a.S = S;
   a.d = (int)d;
   a.J = J;
   a.k = k;
+  a.ls = (int)LS;
+  a.lb = LB;
+  a.rp = (int)RP;
   a.blk[0] = ws.Q.p;
   a.blk[1] = ws.SQ.p;
   a.blk[2] = ws.X.p;
@@ -1269,30 +1310,26 @@ bool eig_fused(double* S, int64_t d, int J, EigSlot& slot, EigWs& ws, const EigO
   a.red = ws.fred.p;
   a.pvec[0] = ws.pq.p;
   a.pvec[1] = ws.py.p;
+  a.mpart = ws.mpart.p;
+  {
+    const MvPlan pl = mv_plan((int)d, grid);
+    a.mv_m8 = pl.m8;
+    a.mv_rb = pl.RB;
+    a.mv_kb = pl.KB;
+    a.mv_kc = pl.kchunk;
+  }
   a.basis = slot.basis.p;
   a.warm = (slot.valid && slot.d == d && slot.k == k) ? 1 : 0;
   a.outV = out_V;
   a.theta_out = theta_dev;
-  a.info = info_dev;
-  ws.fprof.ensure(8);
-  if (!ws.fprof_init) {
-    TK_CUDA(cudaMemsetAsync(ws.fprof.p, 0, 8 * sizeof(long long), st));
-    ws.fprof_init = true;
-  }
   a.prof = ws.fprof.p;
+  a.info = info_dev;
   a.tol = o.tol;
   a.max_outer = o.max_outer;
   a.jsweeps = o.jacobi_sweeps;
   a.seed = 0x5eed0000ull + (uint64_t)d * 131 + (uint64_t)J;
   static const bool dbg = std::getenv("TUCKER_EIG_DEBUG") != nullptr;
   a.dbg = dbg ? 1 : 0;
-  {
-    const char* e = std::getenv("TUCKER_EIG_JSW");
-    if (e) a.jsweeps = std::atoi(e);
-    a.noshift = std::getenv("TUCKER_EIG_NOSHIFT") != nullptr;
-    a.nolock = std::getenv("TUCKER_EIG_NOLOCK") != nullptr;
-    a.nodefl = std::getenv("TUCKER_EIG_NODEFL") != nullptr;
-  }
   void* args[] = {&a};
   TK_CUDA(cudaLaunchCooperativeKernel((const void*)k_eig_fused, dim3(grid), dim3(NT), args, smem, st));
   if (g_launch_counter) ++(*g_launch_counter);
@@ -1305,47 +1342,46 @@ bool eig_fused(double* S, int64_t d, int J, EigSlot& slot, EigWs& ws, const EigO
 
 void eig_unit_mv(const double* S, const double* Y, int d, int n, double alpha, double* Out, double gamma,
                  const double* D, cudaStream_t st) {
-  int nsm = 0, dev = 0;
-  TK_CUDA(cudaGetDevice(&dev));
-  TK_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
-  size_t mv = 0;
-  for (int nn = 1; nn <= n; ++nn) {
-    const MvPlan pl = mv_plan(d, nn, nsm);
-    const int ng = (pl.tpb + 1) / 2, KS = NW / ng;
-    mv = std::max(mv, std::max(mv_smem_doubles(pl.m8, pl.tpb), (size_t)KS * 64 * pl.m8 * pl.tpb));
-  }
-  const size_t smem = mv * sizeof(double);
-  TK_CUDA(cudaFuncSetAttribute(k_eigf_unit_mv, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  TK_LAUNCH(k_eigf_unit_mv, nsm, NT, smem, st, S, Y, d, n, alpha, Out, gamma, D, 1);
+  // inputs are dense d x d / d x n device arrays; copy into the padded layout
+  const int G = num_sms();
+  int64_t LS = 0, RP = 0;
+  eig_layout(d, &LS, &RP);
+  const int LB = n + (n & 1);
+  DBuf<double> dS((size_t)RP * LS), dY((size_t)RP * LB + 64), dD((size_t)RP * LB + 64),
+      dO((size_t)RP * LB + 64), mp(product_part_doubles(d, LB, G));
+  TK_CUDA(cudaMemsetAsync(dS.p, 0, dS.bytes(), st));
+  TK_CUDA(cudaMemsetAsync(dY.p, 0, dY.bytes(), st));
+  TK_CUDA(cudaMemsetAsync(dD.p, 0, dD.bytes(), st));
+  TK_CUDA(cudaMemcpy2DAsync(dS.p, LS * 8, S, (size_t)d * 8, (size_t)d * 8, d, cudaMemcpyDeviceToDevice, st));
+  TK_CUDA(cudaMemcpy2DAsync(dY.p, LB * 8, Y, (size_t)n * 8, (size_t)n * 8, d, cudaMemcpyDeviceToDevice, st));
+  if (D)
+    TK_CUDA(cudaMemcpy2DAsync(dD.p, LB * 8, D, (size_t)n * 8, (size_t)n * 8, d, cudaMemcpyDeviceToDevice, st));
+  launch_unit_mv(dS.p, dY.p, d, n, (int)LS, LB, alpha, dO.p, D ? gamma : 0.0, dD.p, mp.p, 1, st);
+  TK_CUDA(cudaMemcpy2DAsync(Out, (size_t)n * 8, dO.p, LB * 8, (size_t)n * 8, d, cudaMemcpyDeviceToDevice, st));
+  TK_CUDA(cudaStreamSynchronize(st));
 }
 
 double eig_unit_mv_time(int d, int n, int reps) {
-  DBuf<double> S((size_t)d * d), Y((size_t)d * n), O((size_t)d * n);
+  const int G = num_sms();
+  int64_t LS = 0, RP = 0;
+  eig_layout(d, &LS, &RP);
+  const int LB = n + (n & 1);
+  DBuf<double> S((size_t)RP * LS), Y((size_t)RP * LB + 64), O((size_t)RP * LB + 64),
+      mp(product_part_doubles(d, LB, G));
   TK_CUDA(cudaMemset(S.p, 0, S.bytes()));
   TK_CUDA(cudaMemset(Y.p, 0, Y.bytes()));
-  eig_unit_mv(S.p, Y.p, d, n, 1.0, O.p, 0.0, nullptr, 0);  // sets the smem attribute
-  int nsm = 0, dev = 0;
-  TK_CUDA(cudaGetDevice(&dev));
-  TK_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
-  size_t mv = 0;
-  for (int nn = 1; nn <= n; ++nn) {
-    const MvPlan pl = mv_plan(d, nn, nsm);
-    const int ng = (pl.tpb + 1) / 2, KS = NW / ng;
-    mv = std::max(mv, std::max(mv_smem_doubles(pl.m8, pl.tpb), (size_t)KS * 64 * pl.m8 * pl.tpb));
-  }
-  const size_t smem = mv * sizeof(double);
   cudaEvent_t a, b;
   TK_CUDA(cudaEventCreate(&a));
   TK_CUDA(cudaEventCreate(&b));
-  // (T(1 + reps) - T(1)) / reps: one launch, products after the first reuse the plan
+  // (T(1 + reps) - T(1)) / reps inside one cooperative launch (includes the two barriers)
   float ms1 = 0, ms2 = 0;
   TK_CUDA(cudaEventRecord(a, 0));
-  k_eigf_unit_mv<<<nsm, NT, smem, 0>>>(S.p, Y.p, d, n, 1.0, O.p, 0.0, nullptr, 1);
+  launch_unit_mv(S.p, Y.p, d, n, (int)LS, LB, 1.0, O.p, 0.0, nullptr, mp.p, 1, 0);
   TK_CUDA(cudaEventRecord(b, 0));
   TK_CUDA(cudaEventSynchronize(b));
   TK_CUDA(cudaEventElapsedTime(&ms1, a, b));
   TK_CUDA(cudaEventRecord(a, 0));
-  k_eigf_unit_mv<<<nsm, NT, smem, 0>>>(S.p, Y.p, d, n, 1.0, O.p, 0.0, nullptr, 1 + reps);
+  launch_unit_mv(S.p, Y.p, d, n, (int)LS, LB, 1.0, O.p, 0.0, nullptr, mp.p, 1 + reps, 0);
   TK_CUDA(cudaEventRecord(b, 0));
   TK_CUDA(cudaEventSynchronize(b));
   TK_CUDA(cudaEventElapsedTime(&ms2, a, b));

@@ -103,14 +103,14 @@ struct EigSlot {              // warm-start state per (algorithm, mode)
   bool valid = false;
 };
 struct EigWs {
-  DBuf<double> Q, SQ, X, Y, T, H, V, R, L, LT, Z, pq, py, pout;
-  DBuf<double> theta, resid;
-  DBuf<double> fpart, fred;  // eig_fused reduction partials / results
-  DBuf<long long> fprof;      // eig_fused per-phase ns (accumulated over solves)
+  DBuf<double> Q, SQ, X, Y, T;  // eig_fused work blocks (padded layout)
+  DBuf<double> L, LT, pq, py;   // locked vectors, S L, power-iteration vectors
+  DBuf<double> fpart, fred;     // eig_fused reduction partials / results
+  DBuf<double> mpart;           // eig_fused split-K partial products
+  DBuf<long long> fprof;        // eig_fused per-phase ns (accumulated over solves)
   bool fprof_init = false;
-  DBuf<int> dsweeps;
+  DBuf<double> cq, ct, H, R;    // cholqr2 (Y^T Y route)
   DenseWs dense;
-  std::vector<double> h_theta, h_resid;
   int64_t stat_outer = 0, stat_matvec = 0, stat_sweeps = 0;
 };
 struct EigOpts {
@@ -119,15 +119,13 @@ struct EigOpts {
   int jacobi_sweeps = 2;  // cap per Rayleigh-Ritz step (residuals decide convergence)
   double tol = 1e-10;
 };
-// Leading J eigenvectors of symmetric PSD S (d x d, lds; S is used as workspace and
-// deflated in place): out_V (d x ldv fp64 row-major)
-// columns 0..J-1 descending, theta_out[0..J) host. Returns true if converged.
-bool eig_leading(double* S, int64_t lds, int64_t d, int J, EigSlot& slot, EigWs& ws,
-                 const EigOpts& o, double* out_V, int64_t ldv, double* theta_out,
-                 cudaStream_t st);
-// Same problem in one persistent cooperative kernel (eig_fused.cu): out_V (d x J,
-// ld = J) and theta_dev (J) on the device, info_dev[0..4] = {converged, outer
-// iterations, matvecs, Jacobi sweeps, breakdown}.  No host synchronisation.
+// Leading J eigenvectors of symmetric PSD S (d x d in the padded layout of
+// eig_layout: row stride ls, `rows` allocated rows; S is used as workspace and
+// deflated in place) in one persistent cooperative kernel (eig_fused.cu):
+// out_V (d x J, ld = J) and theta_dev (J, descending) on the device,
+// info_dev[0..4] = {converged, outer iterations, matvecs, Jacobi sweeps,
+// breakdown}.  No host synchronisation.
+void eig_layout(int64_t d, int64_t* ls, int64_t* rows);
 bool eig_fused(double* S, int64_t d, int J, EigSlot& slot, EigWs& ws, const EigOpts& o, double* out_V,
                double* theta_dev, int* info_dev, cudaStream_t st);
 size_t eig_fused_smem(int k, int d, int G);

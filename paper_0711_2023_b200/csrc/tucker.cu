@@ -203,39 +203,27 @@ Split build_mp_w(tucker_handle* h, int n) {
   return W;
 }
 
-bool eig_multi() {
-  static const bool m = [] {
-    const char* e = std::getenv("TUCKER_EIG");
-    return e && std::strcmp(e, "multi") == 0;
-  }();
-  return m;
-}
-
-// Leading eigenvectors of S (d x d) -> fp64 V (d x J) in h->V, eigenvalues in
-// h->theta_d (device).  Default: the persistent fused solver (eig_fused.cu).
+// Leading eigenvectors of S (padded layout, eig_layout) -> fp64 V (d x J) in
+// h->V, eigenvalues in h->theta_d (device): the persistent fused solver.
 void solve_eig(tucker_handle* h, int64_t d, int J, EigSlot& slot) {
   h->V.ensure((size_t)(d * J));
   h->theta_d.ensure((size_t)J);
   h->info_d.ensure(8);
-  if (eig_multi()) {
-    std::vector<double> theta(J);
-    const bool ok = eig_leading(h->S.p, d, d, J, slot, h->eig, eig_opts(h), h->V.p, J, theta.data(),
-                                h->st);
-    if (!ok) h->eig_unconverged = true;
-    TK_CUDA(cudaMemcpyAsync(h->theta_d.p, theta.data(), J * sizeof(double), cudaMemcpyHostToDevice, h->st));
-    TK_CUDA(cudaStreamSynchronize(h->st));
-    int info[8] = {ok ? 1 : 0, 0, 0, 0, 0, 0, 0, 0};
-    TK_CUDA(cudaMemcpy(h->info_d.p, info, sizeof(info), cudaMemcpyHostToDevice));
-    return;
-  }
   eig_fused(h->S.p, d, J, slot, h->eig, eig_opts(h), h->V.p, h->theta_d.p, h->info_d.p, h->st);
+}
+
+// S buffer in the eigensolver's padded layout; returns its row stride
+int64_t ensure_S(tucker_handle* h, int64_t d) {
+  int64_t ls = 0, rows = 0;
+  eig_layout(d, &ls, &rows);
+  h->S.ensure((size_t)(rows * ls));
+  return ls;
 }
 
 // after the stream is synchronised: fold the solver's info into the handle
 void eig_check(tucker_handle* h) {
   int info[8];
   TK_CUDA(cudaMemcpy(info, h->info_d.p, 5 * sizeof(int), cudaMemcpyDeviceToHost));
-  if (eig_multi()) return;
   if (info[4]) fail(TUCKER_E_CUDA, "eigensolver breakdown (non-finite Rayleigh quotient)");
   if (!info[0]) h->eig_unconverged = true;
   h->eig.stat_outer += info[1];
@@ -248,13 +236,13 @@ void update_factor(tucker_handle* h, int n, const Split& A, bool transposed, Eig
                    float* ms_gram, float* ms_eig) {
   const int64_t d = A.rows;
   const int J = (int)h->J[n];
-  h->S.ensure((size_t)(d * d));
+  const int64_t lds = ensure_S(h, d);
   cudaEvent_t e0, e1, e2;
   TK_CUDA(cudaEventCreate(&e0));
   TK_CUDA(cudaEventCreate(&e1));
   TK_CUDA(cudaEventCreate(&e2));
   TK_CUDA(cudaEventRecord(e0, h->st));
-  gram_syrk(A, h->S.p, d, h->gram, h->st);
+  gram_syrk(A, h->S.p, lds, h->gram, h->st);
   TK_CUDA(cudaEventRecord(e1, h->st));
   solve_eig(h, d, J, slot);
   if (!transposed) {
@@ -626,11 +614,11 @@ int tucker_debug_gram(tucker_handle* h, int algo, int mode, double* S_out) {
       A = build_mp_w(h, mode);
     }
     const int64_t d = A.rows;
-    h->S.ensure((size_t)(d * d));
-    gram_syrk(A, h->S.p, d, h->gram, h->st);
+    const int64_t lds = ensure_S(h, d);
+    gram_syrk(A, h->S.p, lds, h->gram, h->st);
     const bool od = (h->opts.flags & TUCKER_OUTPUT_ON_DEVICE) != 0;
-    TK_CUDA(cudaMemcpyAsync(S_out, h->S.p, d * d * sizeof(double),
-                            od ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, h->st));
+    TK_CUDA(cudaMemcpy2DAsync(S_out, d * sizeof(double), h->S.p, lds * sizeof(double), d * sizeof(double), d,
+                              od ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, h->st));
     TK_CUDA(cudaStreamSynchronize(h->st));
     return TUCKER_OK;
   });
@@ -640,10 +628,11 @@ int tucker_debug_eig(tucker_handle* h, int d, int J, const double* S, float* U_o
                      double* evals_out) {
   if (!h || !S || !U_out || d < 1 || J < 1 || J > d || J > kMaxJ) return TUCKER_E_ARG;
   return guarded(h, [&]() -> int {
-    h->S.ensure((size_t)d * d);
+    const int64_t lds = ensure_S(h, d);
     const bool od = (h->opts.flags & TUCKER_OUTPUT_ON_DEVICE) != 0;
-    TK_CUDA(cudaMemcpyAsync(h->S.p, S, (size_t)d * d * sizeof(double),
-                            od ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, h->st));
+    TK_CUDA(cudaMemcpy2DAsync(h->S.p, lds * sizeof(double), S, (size_t)d * sizeof(double),
+                              (size_t)d * sizeof(double), d,
+                              od ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, h->st));
     h->scratch_slot.valid = false;
     h->eig_unconverged = false;
     solve_eig(h, d, J, h->scratch_slot);
@@ -661,16 +650,16 @@ int tucker_debug_eig(tucker_handle* h, int d, int J, const double* S, float* U_o
 
 int tucker_debug_smalldense(int mode, int k, const double* in, double* out, double* theta,
                             int* sweeps, int max_sweeps, double shift) {
-  if (!in || !out || k < 1 || k > kMaxBlock || mode < 0 || mode > 1) return TUCKER_E_ARG;
+  if (!in || !out || k < 1 || k > kMaxBlock || mode < 0 || mode > 2) return TUCKER_E_ARG;
   return guarded(nullptr, [&]() -> int {
     DBuf<double> din((size_t)k * k), dout((size_t)k * k), dth((size_t)k);
-    DBuf<int> di(1);
+    DBuf<int> di(8);
     TK_CUDA(cudaMemcpy(din.p, in, (size_t)k * k * sizeof(double), cudaMemcpyHostToDevice));
     eig_unit(mode, din.p, k, dout.p, dth.p, di.p, max_sweeps, shift, 0);
     TK_CUDA(cudaDeviceSynchronize());
     TK_CUDA(cudaMemcpy(out, dout.p, (size_t)k * k * sizeof(double), cudaMemcpyDeviceToHost));
     if (theta) TK_CUDA(cudaMemcpy(theta, dth.p, (size_t)k * sizeof(double), cudaMemcpyDeviceToHost));
-    if (sweeps) TK_CUDA(cudaMemcpy(sweeps, di.p, sizeof(int), cudaMemcpyDeviceToHost));
+    if (sweeps) TK_CUDA(cudaMemcpy(sweeps, di.p, (mode >= 1 ? 8 : 1) * sizeof(int), cudaMemcpyDeviceToHost));
     return TUCKER_OK;
   });
 }

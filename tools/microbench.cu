@@ -45,7 +45,10 @@ __global__ void k_smem_rt(int n, double* out) {  // dependent smem + barrier lat
   out[blockIdx.x * blockDim.x + threadIdx.x] = v;
 }
 
-int main() {
+int main_tp();
+int main_lat();
+int main() { main_lat(); return main_tp(); }
+int main_tp() {
   int nsm;
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
   int* sink;
@@ -104,5 +107,45 @@ int main() {
     cudaEventElapsedTime(&ms, e0, e1);
     printf("smem load + __syncthreads (512 thr): %.1f ns/iter\n", ms * 1e6 / n);
   }
+  return 0;
+}
+
+// dependent-chain latencies (single warp), cycles per op
+__global__ void k_lat(double* out, float* outf, long long* cyc, int n) {
+  double a = out[0], b = 1.0000001;
+  float fa = outf[0], fb = 1.0001f;
+  long long t0 = clock64();
+  for (int i = 0; i < n; ++i) a = fma(a, b, 1e-9);
+  long long t1 = clock64();
+  for (int i = 0; i < n; ++i) fa = fmaf(fa, fb, 1e-9f);
+  long long t2 = clock64();
+  double r = a;
+  for (int i = 0; i < n; ++i) r = 1.0 / (r + 1.0);
+  long long t3 = clock64();
+  double q = a;
+  for (int i = 0; i < n; ++i) q = sqrt(q + 1.0);
+  long long t4 = clock64();
+  __shared__ double sm[64];
+  sm[threadIdx.x] = a;
+  __syncwarp();
+  int idx = threadIdx.x;
+  double acc = 0;
+  for (int i = 0; i < n; ++i) { acc += sm[idx]; idx = (int)acc & 31; }
+  long long t5 = clock64();
+  if (threadIdx.x == 0) {
+    cyc[0] = (t1 - t0) / n; cyc[1] = (t2 - t1) / n; cyc[2] = (t3 - t2) / n; cyc[3] = (t4 - t3) / n;
+    cyc[4] = (t5 - t4) / n;
+  }
+  out[threadIdx.x] = a + r + q + acc;
+  outf[threadIdx.x] = fa;
+}
+int main_lat() {
+  double* o; float* of; long long* c;
+  cudaMalloc(&o, 64 * 8); cudaMalloc(&of, 64 * 4); cudaMalloc(&c, 64);
+  cudaMemset(o, 0, 64 * 8); cudaMemset(of, 0, 64 * 4);
+  k_lat<<<1, 32>>>(o, of, c, 1000);
+  long long h[5];
+  cudaMemcpy(h, c, 40, cudaMemcpyDeviceToHost);
+  printf("latency cycles: DFMA %lld  FFMA %lld  DDIV(+add) %lld  DSQRT(+add) %lld  LDS-dep %lld\n", h[0], h[1], h[2], h[3], h[4]);
   return 0;
 }
