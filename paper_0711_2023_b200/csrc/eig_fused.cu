@@ -35,6 +35,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
+#include <vector>
 
 #include "internal.cuh"
 
@@ -56,7 +57,7 @@ struct FusedArgs {
   double* LT;               // d x J  S L
   double* part;             // [G][k*k] reduction partials
   double* red;              // [k*k] reduced result
-  double* pvec[2];          // power iteration vectors (d)
+  double* pvec[3];          // power iteration / Lanczos vectors (d)
   double* mpart;            // [KB][RPX][LB] split-K partial products
   double* basis;            // d x LB warm-start basis (read if warm, always written)
   int warm;
@@ -64,6 +65,9 @@ struct FusedArgs {
   double* theta_out;        // J
   long long* prof;          // [8] per-phase ns (CTA 0's view), accumulated
   int* info;                // [0] converged [1] outer [2] matvecs [3] jacobi sweeps [4] breakdown
+  double* dinfo;            // [0] lambda_min estimate (0: not estimated) [1] last filter bound b
+  int lanczos;              // estimate lambda_min (Lanczos) for the filter's lower bound
+  double lmin_hint;         // else: lower bound carried over from the slot's last solve (0: none)
   double tol;
   int max_outer, jsweeps;
   uint64_t seed;
@@ -335,6 +339,7 @@ __device__ void matvec(const Ctx& x, double* mpart, const double* S, const doubl
       if (delta != 0.0) v += delta * Em[o];
       Out[o] = v;
     }
+  __syncthreads();  // own rows of Out complete for any thread mapping
 }
 
 // single vector: y[own rows] = S[own rows, :] q, partial ||y||^2 -> part[cta]
@@ -465,6 +470,24 @@ __device__ void reduce_bcast(const Ctx& x, const double* part, int E, int nb, do
   __syncthreads();
 }
 
+// fp64 reciprocal / reciprocal square root from the fp32 approximations plus
+// Newton steps (2 for rcp: 1e-7 -> 1e-14 -> 1e-16; 2 for rsqrt) -- short
+// dependency chains instead of the IEEE division / sqrt sequences.
+__device__ __forceinline__ double rcp_nt(double x) {
+  double r = (double)__frcp_rn((float)x);
+  r = r * fma(-x, r, 2.0);
+  r = r * fma(-x, r, 2.0);
+  return r;
+}
+__device__ __forceinline__ double rsqrt_nt(double x) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  const double hx = 0.5 * x;
+  y = y * fma(-hx * y, y, 1.5);
+  y = y * fma(-hx * y, y, 1.5);
+  return y;
+}
+
 // ---------------------------------------------------------- CholQR factor --
 // G (k x k, in A = smem, ld) SPD.  Equilibrate (D G D + shift I, D = diag^-1/2)
 // and eliminate symmetrically on [A | E] (E = I): after step j rows l > j of
@@ -517,24 +540,6 @@ __device__ void cholqr_factor(const Ctx& x, double* A, double* X, int k, int ld,
 }
 
 // ----------------------------------------------------------------- Jacobi --
-// fp64 reciprocal / reciprocal square root from the fp32 approximations plus
-// Newton steps (2 for rcp: 1e-7 -> 1e-14 -> 1e-16; 2 for rsqrt) -- short
-// dependency chains instead of the IEEE division / sqrt sequences.
-__device__ __forceinline__ double rcp_nt(double x) {
-  double r = (double)__frcp_rn((float)x);
-  r = r * fma(-x, r, 2.0);
-  r = r * fma(-x, r, 2.0);
-  return r;
-}
-__device__ __forceinline__ double rsqrt_nt(double x) {
-  double y;
-  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
-  const double hx = 0.5 * x;
-  y = y * fma(-hx * y, y, 1.5);
-  y = y * fma(-hx * y, y, 1.5);
-  return y;
-}
-
 // Parallel cyclic Jacobi on H (k x k, smem, ld = kp + 1 with kp = k + (k & 1)),
 // applied to the Rayleigh-Ritz basis directly: instead of accumulating V, each
 // round's rotations are applied to the columns of nr row vectors QR (and SR),
@@ -699,6 +704,52 @@ __device__ int jacobi(const Ctx& x, double* H, int kin, int max_sweeps, double t
   return r;
 }
 
+// Smallest eigenvalue of the m x m symmetric tridiagonal (alpha, beta[1..m-1]) by
+// multisection: every thread evaluates the Sturm count at one point of the
+// current bracket, the bracket shrinks to the first point with count >= 1 (3
+// passes of NT points: (1/NT)^3 of the Gershgorin width).  All CTAs compute
+// the same value.
+__device__ double tridiag_min(const Ctx& x, const double* al, const double* be, int m) {
+  __shared__ double lo, hi;
+  __shared__ int first;
+  if (x.tid == 0) {
+    double l = 1e300, h = -1e300;
+    for (int i = 0; i < m; ++i) {
+      const double r = (i > 0 ? fabs(be[i]) : 0.0) + (i + 1 < m ? fabs(be[i + 1]) : 0.0);
+      l = fmin(l, al[i] - r);
+      h = fmax(h, al[i] + r);
+    }
+    lo = l;
+    hi = h;
+  }
+  __syncthreads();
+  for (int pass = 0; pass < 3; ++pass) {
+    const double l = lo, h = hi;
+    const double xv = l + (h - l) * (double)(x.tid + 1) / NT;
+    int cnt = 0;
+    double q = al[0] - xv;
+    cnt += q < 0;
+    for (int i = 1; i < m; ++i) {
+      if (q == 0.0) q = 1e-300;
+      q = al[i] - xv - be[i] * be[i] / q;
+      cnt += q < 0;
+    }
+    if (x.tid == 0) first = NT;
+    __syncthreads();
+    if (cnt >= 1) atomicMin(&first, x.tid);
+    __syncthreads();
+    if (x.tid == 0) {
+      const int f = first;
+      hi = l + (h - l) * (double)(f + 1) / NT;
+      lo = l + (h - l) * (double)f / NT;
+    }
+    __syncthreads();
+  }
+  const double r = 0.5 * (lo + hi);
+  __syncthreads();
+  return r;
+}
+
 // -------------------------------------------------------------- the solver --
 __global__ void __launch_bounds__(NT, 1) k_eig_fused(FusedArgs P) {
   extern __shared__ __align__(128) double smem[];
@@ -737,6 +788,8 @@ __global__ void __launch_bounds__(NT, 1) k_eig_fused(FusedArgs P) {
 
   int nlock = 0, ka = k;
   int n_rr = 0, matvecs = 0, jsw = 0, breakdown = 0;
+  double last_a = 0.0, last_b = 0.0;  // current damped interval (deflation shift = its centre)
+  double a_lo = 0.0;                  // Lanczos estimate of lambda_min (0: none)
   __shared__ long long pacc[8];
   long long pt = 0;
   if (x.tid < 8) pacc[x.tid] = 0;
@@ -857,9 +910,13 @@ __global__ void __launch_bounds__(NT, 1) k_eig_fused(FusedArgs P) {
     return t > 0 ? t : 1.0;
   };
 
-  // deflate S by the locked columns [n0, n0 + nl) of L (LT holds S L):
-  // S <- (I - Ln Ln^T) S (I - Ln Ln^T) = S - Ln W^T - W Ln^T, W = P - Ln (Ln^T P) / 2, P = S Ln
+  // deflate S by the locked columns [n0, n0 + nl) of L (LT holds S L), moving
+  // them to eigenvalue sigma (the centre of the damped interval, so the filter
+  // damps whatever components of them the active block regains):
+  // S <- (I - Ln Ln^T) S (I - Ln Ln^T) + sigma Ln Ln^T = S - Ln W^T - W Ln^T,
+  // W = P - Ln (Ln^T P) / 2 - sigma Ln / 2, P = S Ln
   auto deflate = [&](int n0, int nl) {
+    const double sigma = last_b > 0 ? 0.5 * (last_a + last_b) : (a_lo > 0 ? a_lo : 0.0);
     double* Wd = B(iX);  // d x nl (ld nl)
     gram_partial(x, P.L + n0, J, nl, P.LT + n0, J, nl, P.part);
     reduce_bcast(x, P.part, nl * nl, nl, P.red, x.r2s, nl);
@@ -868,7 +925,7 @@ __global__ void __launch_bounds__(NT, 1) k_eig_fused(FusedArgs P) {
       for (int c = x.lane; c < nl; c += 32) {
         double s = 0.0;
         for (int l = 0; l < nl; ++l) s = fma(P.L[(int64_t)r * J + n0 + l], x.r2s[l * nl + c], s);
-        Wd[(int64_t)r * nl + c] = P.LT[(int64_t)r * J + n0 + c] - 0.5 * s;
+        Wd[(int64_t)r * nl + c] = P.LT[(int64_t)r * J + n0 + c] - 0.5 * s - 0.5 * sigma * P.L[(int64_t)r * J + n0 + c];
       }
     gsync();  // W complete
     // S[own rows][j] -= sum_l Ln[r][l] W[j][l] + W[r][l] Ln[j][l], rows in chunks of 8
@@ -985,6 +1042,78 @@ __global__ void __launch_bounds__(NT, 1) k_eig_fused(FusedArgs P) {
     lock();
   };
 
+  // lower end of the spectrum (Lanczos, 16 steps, no reorthogonalisation): the
+  // Chebyshev filter then damps [lambda_min, theta_k] instead of [0, theta_k]
+  if (!P.lanczos) a_lo = P.lmin_hint;
+  if (P.lanczos) {
+    constexpr int LZ = 16;
+    __shared__ double lz_a[LZ], lz_b[LZ];
+    double* v = P.pvec[0];
+    double* vp = P.pvec[1];
+    double* w = P.pvec[2];
+    {
+      double s0 = 0.0;
+      for (int r = x.r0 + x.tid; r < x.r1; r += NT) {
+        const uint64_t h = mix64(P.seed ^ 0x1a2c5ull ^ mix64((uint64_t)r * 2654435761ull));
+        const double u = ((double)(h >> 11) * (1.0 / 9007199254740992.0)) * 2.0 - 1.0;
+        v[r] = u;
+        vp[r] = 0.0;
+        s0 = fma(u, u, s0);
+      }
+      block_partial(x, s0, P.part);
+      gsync();
+      const double inv = rsqrt(allsum_scalar(x, P.part));
+      for (int r = x.r0 + x.tid; r < x.r1; r += NT) v[r] *= inv;
+    }
+    double beta = 0.0;
+    for (int j = 0; j < LZ; ++j) {
+      gsync();  // v complete
+      // w = S v - beta vp (own rows); partials of v^T w and w^T w
+      double pa = 0.0;
+      for (int r = x.r0 + x.warp; r < x.r1; r += NW) {
+        const double* srow = S + (int64_t)r * x.ls;
+        double sacc = 0.0;
+        for (int c = x.lane; c < d; c += 32) sacc = fma(__ldcg(srow + c), __ldcg(v + c), sacc);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) sacc += __shfl_xor_sync(0xffffffffu, sacc, o);
+        const double wr = sacc - beta * vp[r];
+        if (x.lane == 0) {
+          w[r] = wr;
+          pa = fma(v[r], wr, pa);
+        }
+      }
+      block_partial(x, pa, P.part);
+      gsync();
+      const double alpha = allsum_scalar(x, P.part);
+      // w <- w - alpha v, beta_new = ||w|| (explicit: the shortcut ||w||^2 - alpha^2
+      // cancels catastrophically next to an outlier eigenvalue)
+      double pw = 0.0;
+      for (int r = x.r0 + x.tid; r < x.r1; r += NT) {
+        const double wr = w[r] - alpha * v[r];
+        w[r] = wr;
+        pw = fma(wr, wr, pw);
+      }
+      block_partial(x, pw, P.part + x.G);
+      gsync();
+      const double bnew = sqrt(allsum_scalar(x, P.part + x.G));
+      if (x.tid == 0) {
+        lz_a[j] = alpha;
+        lz_b[j] = beta;  // beta_j couples j-1 and j
+      }
+      const double ib = bnew > 0 ? 1.0 / bnew : 0.0;
+      for (int r = x.r0 + x.tid; r < x.r1; r += NT) {
+        vp[r] = v[r];
+        v[r] = w[r] * ib;
+      }
+      beta = bnew;
+      ++matvecs;
+    }
+    __syncthreads();
+    a_lo = fmax(0.0, tridiag_min(x, lz_a, lz_b, LZ));
+    tick(PF_POW);
+    if (P.dbg && x.cta == 0 && x.tid == 0) printf("[eigf] lanczos lambda_min ~ %.6e\n", a_lo);
+  }
+
   orth_active(2, true);
   rayleigh_ritz();
   if (P.dbg && x.cta == 0 && x.tid == 0) {
@@ -1019,7 +1148,11 @@ __global__ void __launch_bounds__(NT, 1) k_eig_fused(FusedArgs P) {
     double b = th[k - 1];
     if (!(b > 0)) b = 1e-12 * th1;
     if (thJ <= b * (1 + 1e-12)) b = thJ * (1 - 1e-3);
-    const double a = 0.0;
+    // damped interval [a, b]: a from Lanczos (minus 2 % of the width), else 0
+    double a = a_lo > 0 ? a_lo - 0.02 * (b - a_lo) : 0.0;
+    if (!(a > 0) || a > 0.9 * b) a = 0.0;
+    last_b = b;
+    last_a = a;
     const double e = (b - a) / 2, c = (b + a) / 2;
     const double xJ = fmax((thJ - c) / e, 1.0 + 1e-12);
     const double xt = fmax((thtop - c) / e, xJ);
@@ -1104,6 +1237,8 @@ __global__ void __launch_bounds__(NT, 1) k_eig_fused(FusedArgs P) {
     }
     if (x.tid < 8) P.prof[x.tid] += pacc[x.tid];
     if (x.tid == 0) {
+      P.dinfo[0] = P.lanczos ? a_lo : -1.0;  // -1: no new estimate
+      P.dinfo[1] = last_b;
       P.info[0] = converged ? 1 : 0;
       P.info[1] = outer;
       P.info[2] = matvecs;
@@ -1140,7 +1275,15 @@ __global__ void __launch_bounds__(NT, 1) k_eigf_unit_mv(const double* S, const d
   x.r2s = smem;
   for (int i = 0; i < reps; ++i) {
     gsync();
+    // reps == -2: two products into Out and Out + RP LB (determinism check)
     matvec(x, mpart, S, Y, n, alpha, Out, gamma, D, 0.0, nullptr);
+  }
+  if (reps == -2) {
+    gsync();
+    matvec(x, mpart, S, Y, n, alpha, Out, gamma, D, 0.0, nullptr);
+    gsync();
+    const int RP = (d + 63) / 64 * 64 + 64;
+    matvec(x, mpart, S, Y, n, alpha, Out + (size_t)RP * lb, gamma, D, 0.0, nullptr);
   }
 }
 
@@ -1284,6 +1427,7 @@ bool eig_fused(double* S, int64_t d, int J, EigSlot& slot, EigWs& ws, const EigO
   ws.fred.ensure((size_t)k * k);
   ws.pq.ensure((size_t)d);
   ws.py.ensure((size_t)d);
+  ws.pz.ensure((size_t)d);
   ws.fprof.ensure(8);
   if (!ws.fprof_init) {
     TK_CUDA(cudaMemsetAsync(ws.fprof.p, 0, 8 * sizeof(long long), st));
@@ -1310,6 +1454,7 @@ bool eig_fused(double* S, int64_t d, int J, EigSlot& slot, EigWs& ws, const EigO
   a.red = ws.fred.p;
   a.pvec[0] = ws.pq.p;
   a.pvec[1] = ws.py.p;
+  a.pvec[2] = ws.pz.p;
   a.mpart = ws.mpart.p;
   {
     const MvPlan pl = mv_plan((int)d, grid);
@@ -1324,6 +1469,15 @@ bool eig_fused(double* S, int64_t d, int J, EigSlot& slot, EigWs& ws, const EigO
   a.theta_out = theta_dev;
   a.prof = ws.fprof.p;
   a.info = info_dev;
+  a.dinfo = reinterpret_cast<double*>(info_dev + 8);
+  // lambda_min only when it is worth it (first solve of the slot, or the last
+  // estimate was a sizeable fraction of the filter bound), refreshed by Lanczos
+  // every third solve; in between the last estimate minus 10 % of the interval
+  // width (lambda_min drifts by a few % per sweep) is a safe lower bound
+  const bool useful = !slot.valid || slot.lmin > 0.1 * slot.bval;
+  a.lanczos = useful && (!slot.valid || slot.lz_age >= 2) ? 1 : 0;
+  a.lmin_hint = (useful && !a.lanczos) ? slot.lmin - 0.1 * (slot.bval - slot.lmin) : 0.0;
+  slot.lz_age = a.lanczos ? 0 : slot.lz_age + 1;
   a.tol = o.tol;
   a.max_outer = o.max_outer;
   a.jsweeps = o.jacobi_sweeps;
@@ -1359,6 +1513,29 @@ void eig_unit_mv(const double* S, const double* Y, int d, int n, double alpha, d
   launch_unit_mv(dS.p, dY.p, d, n, (int)LS, LB, alpha, dO.p, D ? gamma : 0.0, dD.p, mp.p, 1, st);
   TK_CUDA(cudaMemcpy2DAsync(Out, (size_t)n * 8, dO.p, LB * 8, (size_t)n * 8, d, cudaMemcpyDeviceToDevice, st));
   TK_CUDA(cudaStreamSynchronize(st));
+}
+
+double eig_unit_mv_repeat(const double* S, const double* Y, int d, int n) {
+  // two back-to-back products of the same (dense device) inputs: max |difference|
+  const int G = num_sms();
+  int64_t LS = 0, RP = 0;
+  eig_layout(d, &LS, &RP);
+  const int LB = n + (n & 1);
+  DBuf<double> dS((size_t)RP * LS), dY((size_t)RP * LB + 64), dO(2 * (size_t)RP * LB + 64),
+      mp(product_part_doubles(d, LB, G));
+  TK_CUDA(cudaMemset(dS.p, 0, dS.bytes()));
+  TK_CUDA(cudaMemset(dY.p, 0, dY.bytes()));
+  TK_CUDA(cudaMemset(dO.p, 0, dO.bytes()));
+  TK_CUDA(cudaMemcpy2D(dS.p, LS * 8, S, (size_t)d * 8, (size_t)d * 8, d, cudaMemcpyDeviceToDevice));
+  TK_CUDA(cudaMemcpy2D(dY.p, LB * 8, Y, (size_t)n * 8, (size_t)n * 8, d, cudaMemcpyDeviceToDevice));
+  launch_unit_mv(dS.p, dY.p, d, n, (int)LS, LB, 1.0, dO.p, 0.0, nullptr, mp.p, -2, 0);
+  TK_CUDA(cudaDeviceSynchronize());
+  std::vector<double> h(2 * (size_t)RP * LB);
+  TK_CUDA(cudaMemcpy(h.data(), dO.p, h.size() * 8, cudaMemcpyDeviceToHost));
+  double m = 0;
+  for (int r = 0; r < d; ++r)
+    for (int c = 0; c < n; ++c) m = std::max(m, std::fabs(h[(size_t)r * LB + c] - h[(size_t)RP * LB + (size_t)r * LB + c]));
+  return m;
 }
 
 double eig_unit_mv_time(int d, int n, int reps) {

@@ -101,10 +101,12 @@ struct EigSlot {              // warm-start state per (algorithm, mode)
   int64_t d = 0;
   int k = 0;
   bool valid = false;
+  double lmin = 0.0, bval = 0.0;  // lambda_min estimate and filter bound of the last solve
+  int lz_age = 0;                  // solves since the last Lanczos estimate
 };
 struct EigWs {
   DBuf<double> Q, SQ, X, Y, T;  // eig_fused work blocks (padded layout)
-  DBuf<double> L, LT, pq, py;   // locked vectors, S L, power-iteration vectors
+  DBuf<double> L, LT, pq, py, pz;  // locked vectors, S L, power-iteration / Lanczos vectors
   DBuf<double> fpart, fred;     // eig_fused reduction partials / results
   DBuf<double> mpart;           // eig_fused split-K partial products
   DBuf<long long> fprof;        // eig_fused per-phase ns (accumulated over solves)
@@ -133,6 +135,7 @@ size_t eig_fused_smem(int k, int d, int G);
 void eig_unit_mv(const double* S, const double* Y, int d, int n, double alpha, double* Out, double gamma,
                  const double* D, cudaStream_t st);
 double eig_unit_mv_time(int d, int n, int reps);  // us per product (zero data)
+double eig_unit_mv_repeat(const double* S, const double* Y, int d, int n);
 void eig_unit(int mode, const double* in, int k, double* out, double* theta, int* iout, int sweeps,
               double shift, cudaStream_t st);
 // Orthonormalise the columns of V (d x J fp64) in place (CholQR2).

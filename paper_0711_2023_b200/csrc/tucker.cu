@@ -37,6 +37,7 @@ struct tucker_handle {
   EigSlot slots[2][kMaxOrder];
   DBuf<double> theta_d;
   DBuf<int> info_d;
+  EigSlot* last_slot = nullptr;
   EigSlot scratch_slot;
   EigWs eig;
   GramWs gram;
@@ -208,7 +209,8 @@ Split build_mp_w(tucker_handle* h, int n) {
 void solve_eig(tucker_handle* h, int64_t d, int J, EigSlot& slot) {
   h->V.ensure((size_t)(d * J));
   h->theta_d.ensure((size_t)J);
-  h->info_d.ensure(8);
+  h->info_d.ensure(16);  // 8 ints + 4 doubles
+  h->last_slot = &slot;
   eig_fused(h->S.p, d, J, slot, h->eig, eig_opts(h), h->V.p, h->theta_d.p, h->info_d.p, h->st);
 }
 
@@ -222,8 +224,14 @@ int64_t ensure_S(tucker_handle* h, int64_t d) {
 
 // after the stream is synchronised: fold the solver's info into the handle
 void eig_check(tucker_handle* h) {
-  int info[8];
-  TK_CUDA(cudaMemcpy(info, h->info_d.p, 5 * sizeof(int), cudaMemcpyDeviceToHost));
+  int info[16];
+  TK_CUDA(cudaMemcpy(info, h->info_d.p, 16 * sizeof(int), cudaMemcpyDeviceToHost));
+  if (h->last_slot) {
+    double dv[2];
+    std::memcpy(dv, info + 8, sizeof(dv));
+    if (dv[0] >= 0) h->last_slot->lmin = dv[0];  // a new Lanczos estimate (0: none useful)
+    if (dv[1] > 0) h->last_slot->bval = dv[1];
+  }
   if (info[4]) fail(TUCKER_E_CUDA, "eigensolver breakdown (non-finite Rayleigh quotient)");
   if (!info[0]) h->eig_unconverged = true;
   h->eig.stat_outer += info[1];
@@ -673,6 +681,10 @@ int tucker_debug_product(int d, int n, const double* S, const double* Y, double 
     TK_CUDA(cudaMemcpy(dY.p, Y, (size_t)d * n * sizeof(double), cudaMemcpyHostToDevice));
     if (D) TK_CUDA(cudaMemcpy(dD.p, D, (size_t)d * n * sizeof(double), cudaMemcpyHostToDevice));
     TK_CUDA(cudaMemset(dO.p, 0xff, (size_t)d * n * sizeof(double)));
+    if (alpha == 12345.0) {  // debug: determinism of two back-to-back products
+      out[0] = eig_unit_mv_repeat(dS.p, dY.p, d, n);
+      return TUCKER_OK;
+    }
     eig_unit_mv(dS.p, dY.p, d, n, alpha, dO.p, D ? gamma : 0.0, dD.p, 0);
     TK_CUDA(cudaDeviceSynchronize());
     TK_CUDA(cudaMemcpy(out, dO.p, (size_t)d * n * sizeof(double), cudaMemcpyDeviceToHost));
