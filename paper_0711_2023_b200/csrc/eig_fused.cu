@@ -790,6 +790,7 @@ __global__ void __launch_bounds__(NT, 1) k_eig_fused(FusedArgs P) {
   int n_rr = 0, matvecs = 0, jsw = 0, breakdown = 0;
   double last_a = 0.0, last_b = 0.0;  // current damped interval (deflation shift = its centre)
   double a_lo = 0.0;                  // Lanczos estimate of lambda_min (0: none)
+  double rprev = 1e-9;                // max relative residual after the last RR (Jacobi threshold)
   __shared__ long long pacc[8];
   long long pt = 0;
   if (x.tid < 8) pacc[x.tid] = 0;
@@ -844,6 +845,11 @@ __global__ void __launch_bounds__(NT, 1) k_eig_fused(FusedArgs P) {
     }
   };
 
+  auto theta1 = [&]() {
+    const double t = nlock > 0 ? thl[0] : th[0];
+    return t > 0 ? t : 1.0;
+  };
+
   // ---- Rayleigh-Ritz on the active block: Q <- Q V, SQ <- S Q V, th, rs
   auto rayleigh_ritz = [&]() {
     mv(B(iQ), 1.0, B(iSQ), 0.0, nullptr, 0.0, nullptr);
@@ -870,8 +876,12 @@ __global__ void __launch_bounds__(NT, 1) k_eig_fused(FusedArgs P) {
         SR[r * ldr + c] = B(iSQ)[(int64_t)(x.r0 + r) * LB + c];
       }
     __syncthreads();
-    const int sw = jacobi(x, x.r1s, ka, k == d ? 60 : (n_rr == 0 ? P.jsweeps + 1 : P.jsweeps),
-                          k == d ? 1e-15 : 1e-13, th + nlock, perm, QR, SR, nrr, ldr);
+    // rotation threshold: off-diagonals far below the current residual level
+    // (rprev = max relative residual of the unconverged vectors after the last
+    // RR) cannot matter yet; near convergence this is the strict 1e-13
+    const double jtol = k == d ? 1e-15 : 1e-13;
+    const int sw = jacobi(x, x.r1s, ka, k == d ? 60 : (n_rr == 0 ? P.jsweeps + 1 : P.jsweeps), jtol,
+                          th + nlock, perm, QR, SR, nrr, ldr);
     tick(PF_JAC);
     if (sw < 0) breakdown = 1;
     else jsw += sw;
@@ -903,11 +913,12 @@ __global__ void __launch_bounds__(NT, 1) k_eig_fused(FusedArgs P) {
     tick(PF_RED);
     for (int c = x.tid; c < ka; c += NT) rs[nlock + c] = sqrt(rs[nlock + c]);
     __syncthreads();
-  };
-
-  auto theta1 = [&]() {
-    const double t = nlock > 0 ? thl[0] : th[0];
-    return t > 0 ? t : 1.0;
+    {
+      const double t1 = theta1();
+      double rm = 0.0;
+      for (int i = nlock; i < J && i < nlock + ka; ++i) rm = fmax(rm, rs[i] / t1);
+      rprev = rm;
+    }
   };
 
   // deflate S by the locked columns [n0, n0 + nl) of L (LT holds S L), moving
@@ -1481,6 +1492,7 @@ bool eig_fused(double* S, int64_t d, int J, EigSlot& slot, EigWs& ws, const EigO
   a.tol = o.tol;
   a.max_outer = o.max_outer;
   a.jsweeps = o.jacobi_sweeps;
+  if (const char* e = std::getenv("TUCKER_EIG_JSW")) a.jsweeps = std::atoi(e);  // experiments
   a.seed = 0x5eed0000ull + (uint64_t)d * 131 + (uint64_t)J;
   static const bool dbg = std::getenv("TUCKER_EIG_DEBUG") != nullptr;
   a.dbg = dbg ? 1 : 0;

@@ -119,7 +119,7 @@ struct SyrkArgs {
   const int2* tiles;   // (bi, bj), bi <= bj
   int ntiles;
   int nkt;             // K-tiles in A
-  int kt_per_split;
+  int splits;          // split z takes the K-tiles z, z + splits, z + 2 splits, ...
   double* partial;     // [split][tile][128][128]
 };
 
@@ -137,9 +137,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   const int split = blockIdx.x / p.ntiles;
   const int2 bij = p.tiles[tile];
   const bool diag = bij.x == bij.y;
-  const int kt0 = split * p.kt_per_split;
-  const int kt1 = min(p.nkt, kt0 + p.kt_per_split);
-  const int nk = max(0, kt1 - kt0);
+  // interleaved K-tiles: at any time all CTAs work inside a narrow K window, so
+  // each operand panel streams from HBM about once and the re-reads by the
+  // other tiles of its row block hit L2
+  const int nk = split < p.nkt ? (p.nkt - split + p.splits - 1) / p.splits : 0;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
@@ -171,7 +172,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         const uint32_t ph = (uint32_t)((i / STAGES) & 1);
         mbar_wait(&empty_bar[s], ph ^ 1);
         uint8_t* st = smem + s * STAGE_BYTES;
-        const int kcol = (kt0 + i) * TKE;
+        const int kcol = (split + i * p.splits) * TKE;
         mbar_expect_tx(&full_bar[s], diag ? 2 * OPB : 4 * OPB);
         tma_load_2d(st, &map_hi, &full_bar[s], kcol, bij.x * TM);
         tma_load_2d(st + OPB, &map_lo, &full_bar[s], kcol, bij.x * TM);
@@ -313,10 +314,14 @@ void gram_syrk_tc(const Split& A, double* S, int64_t lds, GramWs& ws, cudaStream
   tiles.reserve(ntiles);
   for (int i = 0; i < nb; ++i)
     for (int j = i; j < nb; ++j) tiles.push_back(make_int2(i, j));
-  // K-splits so that tiles x splits fills the 148 SMs (>= 4 K-tiles per CTA)
-  int splits = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(148, ntiles), nkt / 4));
-  const int kt_per = (int)ceil_div(nkt, splits);
-  splits = (int)ceil_div(nkt, kt_per);
+  // K-splits: one wave of CTAs over the SMs (>= 4 K-tiles per CTA)
+  int nsm = 148;
+  {
+    int dev = 0;
+    TK_CUDA(cudaGetDevice(&dev));
+    TK_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+  }
+  const int splits = (int)std::max<int64_t>(1, std::min<int64_t>(nsm / ntiles, nkt / 4));
   ws.scratch.ensure(sizeof(int2) * tiles.size());
   TK_CUDA(cudaMemcpyAsync(ws.scratch.p, tiles.data(), sizeof(int2) * tiles.size(),
                           cudaMemcpyHostToDevice, st));
@@ -327,7 +332,7 @@ void gram_syrk_tc(const Split& A, double* S, int64_t lds, GramWs& ws, cudaStream
   a.tiles = (const int2*)ws.scratch.p;
   a.ntiles = ntiles;
   a.nkt = nkt;
-  a.kt_per_split = kt_per;
+  a.splits = splits;
   a.partial = ws.partial.p;
   TK_LAUNCH(k_syrk_tc, (unsigned)(ntiles * splits), NUM_THREADS, (size_t)smem_bytes, st, mhi, mlo, a);
   TK_LAUNCH(k_syrk_reduce, dim3(16, (unsigned)ntiles), 256, 0, st, (const double*)ws.partial.p,
