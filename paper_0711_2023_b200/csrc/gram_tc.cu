@@ -30,6 +30,11 @@ constexpr int TM = 128;                 // tile rows (UMMA M)
 constexpr int TN = 128;                 // tile cols (UMMA N)
 constexpr int TKE = 32;                 // K elements per stage (128 B of fp32 -> one swizzle atom)
 constexpr int STAGES = 3;
+// K-tiles accumulated in fp32 in TMEM before each fp64 drain: 1 for short K
+// (the drain is cheap there), DRAIN_LONG (128 products per fp32 partial) when a
+// CTA streams many K-tiles and the drain would otherwise starve the tensor core
+// (SURVEY F4 is about fp32 accumulation over the FULL K)
+constexpr int DRAIN_LONG = 4;
 constexpr int OPB = TM * TKE * 4;       // bytes of one operand tile (16 KB)
 constexpr int STAGE_BYTES = 4 * OPB;    // A_hi, A_lo, B_hi, B_lo
 constexpr int NUM_THREADS = 320;        // 10 warps
@@ -141,6 +146,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   // each operand panel streams from HBM about once and the re-reads by the
   // other tiles of its row block hit L2
   const int nk = split < p.nkt ? (p.nkt - split + p.splits - 1) / p.splits : 0;
+  const int DRAIN = nk >= 64 ? DRAIN_LONG : 1;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
@@ -188,8 +194,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       for (int i = 0; i < nk; ++i) {
         const int s = i % STAGES;
         const uint32_t ph = (uint32_t)((i / STAGES) & 1);
-        const int b = i & 1;
-        mbar_wait(&tempty_bar[b], (uint32_t)(((i >> 1) & 1) ^ 1));
+        const int grp = i / DRAIN, b = grp & 1;
+        const bool first = (i % DRAIN) == 0, last = (i % DRAIN) == DRAIN - 1 || i == nk - 1;
+        if (first) mbar_wait(&tempty_bar[b], (uint32_t)(((grp >> 1) & 1) ^ 1));
         mbar_wait(&full_bar[s], ph);
         tc_fence_after();
         const uint32_t base = smem_u32(smem + s * STAGE_BYTES);
@@ -199,12 +206,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 #pragma unroll
         for (int k = 0; k < TKE / 8; ++k) {
           const uint32_t off = (uint32_t)(k * 32);  // 8 tf32 = 32 bytes along K inside the atom
-          umma_tf32(d, sw128_desc(ahi + off), sw128_desc(bhi + off), k > 0 ? 1u : 0u);
+          umma_tf32(d, sw128_desc(ahi + off), sw128_desc(bhi + off), (k > 0 || !first) ? 1u : 0u);
           umma_tf32(d, sw128_desc(ahi + off), sw128_desc(blo + off), 1u);
           umma_tf32(d, sw128_desc(alo + off), sw128_desc(bhi + off), 1u);
         }
-        umma_commit(&empty_bar[s]);   // smem stage free once these MMAs complete
-        umma_commit(&tfull_bar[b]);   // fp32 partial of this K-tile ready in TMEM
+        umma_commit(&empty_bar[s]);         // smem stage free once these MMAs complete
+        if (last) umma_commit(&tfull_bar[b]);  // fp32 partial of this K-tile group ready in TMEM
       }
     }
   } else {
@@ -214,9 +221,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     double acc[64];
 #pragma unroll
     for (int j = 0; j < 64; ++j) acc[j] = 0.0;
-    for (int i = 0; i < nk; ++i) {
-      const int b = i & 1;
-      mbar_wait(&tfull_bar[b], (uint32_t)((i >> 1) & 1));
+    const int ngrp = (nk + DRAIN - 1) / DRAIN;
+    for (int grp = 0; grp < ngrp; ++grp) {
+      const int b = grp & 1;
+      mbar_wait(&tfull_bar[b], (uint32_t)((grp >> 1) & 1));
       tc_fence_after();
       const uint32_t taddr = tmem_base + ((uint32_t)(32 * g) << 16) + (uint32_t)(b * TN + 64 * half);
       float v0[32], v1[32];

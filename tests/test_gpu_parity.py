@@ -140,6 +140,24 @@ def test_config1_full(capi):
         assert abs(fit - ref[algo]["fit"]) < 1e-5
 
 
+@pytest.mark.parametrize("k", [2])
+def test_config_full(capi, k):
+    """BASELINE.json configs[k-1] at full size, 5 HOOI + 5 MP sweeps from the same
+    U0 (the bench's workload): factors, fits per sweep and core vs the fp64 oracle."""
+    c = make_config(k)
+    out, ref = run_both(capi, c["dims"], c["idx"], c["vals"], c["U0"], c["core"], c["sweeps"])
+    for algo in ("hooi", "mp"):
+        fits, G, U, fit = out[algo]
+        r = ref[algo]
+        for n in range(3):
+            d = O.projector_distance(U[n], r["U"][n])
+            assert d < 1e-4, (algo, n, d)
+        assert abs(fit - r["fit"]) < 1e-5
+        np.testing.assert_allclose(fits, r["fits"], atol=1e-5)
+        Ga = align_core(G, U, r["G"], r["U"])
+        assert O.rel_frobenius(Ga, r["G"]) < 1e-4
+
+
 def test_edge_cases(capi):
     dims, core = (30, 40, 25), (3, 4, 2)
     idx, vals, U0 = case(dims, 600, core)
