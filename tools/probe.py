@@ -11,7 +11,7 @@ k = int(sys.argv[1]) if len(sys.argv) > 1 else 2
 sweeps = int(sys.argv[2]) if len(sys.argv) > 2 else 2
 t0 = time.time(); c = make_config(k); print("gen %.1fs" % (time.time() - t0), flush=True)
 t0 = time.time()
-t = capi.Tucker(c["dims"], c["core"], c["idx"], c["vals"], c["U0"])
+t = capi.Tucker(c["dims"], c["core"], c["idx"], c["vals"], c["U0"], eig_oversample=int(os.environ.get("OVS", "0")))
 print("init %.2fs" % (time.time() - t0), flush=True)
 for algo in ("hooi", "mp"):
     t.set_factors(c["U0"]); t.stats(reset=True)
