@@ -282,27 +282,40 @@ def run_ours(args):
         e2e_ms.append(e0.elapsed_time(e1))
     e2e_val = units / (statistics.median(e2e_ms) / 1e3) / 1e9 * world
 
-    # ---- roofline of the dominant kernel ----
+    # ---- roofline of the dominant kernel (the fused eigensolver) ----
     pk = peaks()
-    hflops, mflops = gram_flops(c)
-    gram_ms = (stage_acc[1] + stage_acc_mp[1]) / args.steps
-    gram_path = "simt-fp64" if os.environ.get("TUCKER_GRAM") == "simt" else st.get("gram_path", "simt-fp64")
     shares = {"spttmc+spmm": (stage_acc[0] + stage_acc_mp[0]) / args.steps,
-              "gram": gram_ms, "eig": (stage_acc[2] + stage_acc_mp[2]) / args.steps,
+              "gram": (stage_acc[1] + stage_acc_mp[1]) / args.steps,
+              "eig": (stage_acc[2] + stage_acc_mp[2]) / args.steps,
               "core+fit": (stage_acc[3] + stage_acc_mp[3]) / args.steps}
+    eig_ms = shares["eig"]
+    eig_flops = st.get("eig_flops", 0) / args.steps
+    launches_eig = 2 * N * S  # one k_eig_fused launch per factor update
+    fp64_peak = 148 * 64 * 2 * 1.965e9 / 1e12
+    achieved = eig_flops / (eig_ms / 1e3) / 1e12 if eig_ms > 0 else 0.0
+    traffic = None
+    try:  # per-launch DRAM bytes of k_eig_fused from the committed ncu --set full capture
+        traffic = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))["k_eig_fused"]
+    except Exception:
+        traffic = None
+    roof = {"kernel": "k_eig_fused (persistent eigensolver: DMMA products, Jacobi RR, CholQR)",
+            "bound": "alu",
+            "peak_note": "fp64 nominal: 148 SMs x 64 FMA/clk x 2 x 1.965 GHz (B200_PROFILING clock); "
+                         "tools/microbench.cu measured 36.9 TFLOP/s DMMA",
+            "achieved": achieved, "peak": fp64_peak, "unit": "TFLOP/s", "frac": achieved / fp64_peak,
+            "traffic": traffic, "flops_per_launch": eig_flops / launches_eig,
+            "ms_per_launch": eig_ms / launches_eig, "launches_per_step": launches_eig,
+            "stage_ms_per_step": shares, "dominant_stage": max(shares, key=shares.get),
+            "eig_phase_ms_per_step": {k: v / args.steps for k, v in st.get("eig_phase_ms", {}).items()}}
+    # secondary: the Gram SYRK on the tensor cores
+    hflops, mflops = gram_flops(c)
+    gram_ms = shares["gram"]
     gram_flops_step = S * (hflops + mflops)
-    achieved = gram_flops_step / (gram_ms / 1e3) / 1e12
-    if gram_path == "tcgen05-3xtf32":
-        peak = pk["bf16_tflops"] * (1.1 / 2.25) / 3.0
-        roof = {"kernel": "gram (tcgen05 3xTF32 SYRK, fp64 drain)", "bound": "tensor",
-                "peak_note": "measured bf16 burst x tf32/bf16 nominal (1.1/2.25) / 3 products"}
-    else:
-        peak = 148 * 64 * 2 * 1.965e9 / 1e12
-        roof = {"kernel": "gram (SIMT fp64 SYRK)", "bound": "alu",
-                "peak_note": "148 SMs x 64 DFMA/clk x 2 x 1.965 GHz (B200_PROFILING nominal clock)"}
-    roof.update({"achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
-                 "traffic": None, "stage_ms_per_step": shares,
-                 "dominant_stage": max(shares, key=shares.get)})
+    g_ach = gram_flops_step / (gram_ms / 1e3) / 1e12 if gram_ms > 0 else 0.0
+    g_peak = pk["bf16_tflops"] * (1.1 / 2.25) / 3.0
+    roof_gram = {"kernel": "k_syrk_tc (tcgen05 3xTF32 SYRK, fp64 drain)", "bound": "tensor",
+                 "peak_note": "measured bf16 burst x tf32/bf16 nominal (1.1/2.25) / 3 products",
+                 "achieved": g_ach, "peak": g_peak, "unit": "TFLOP/s", "frac": g_ach / g_peak}
 
     line = {
         "metric": "HOOI/MP sweep throughput (nnz x modes per second)",
@@ -321,6 +334,7 @@ def run_ours(args):
         "e2e": {"value": e2e_val, "unit": "Gnnz/s", "h2d_bytes_per_step": int(h2d),
                 "d2h_bytes_per_step": int(d2h)},
         "roofline": roof,
+        "roofline_gram": roof_gram,
         "clocks": clocks,
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

@@ -182,8 +182,11 @@ int tucker_debug_product_time(int d, int n, int reps, double* us);
  * iterations, [2] = Chebyshev matvecs, [3] = small (k x k) Jacobi sweeps,
  * [4] = Gram path (0 = tcgen05 3xTF32, 1 = SIMT fp64), [5..12] = time inside the
  * fused eigensolver kernel by phase in ns as seen by its CTA 0 (matvec, k x k
- * reductions, CholQR factor, Jacobi, row-block apply, deflation, power, other).
- * stats has 13 entries. */
+ * reductions, CholQR factor, Jacobi, row-block apply, deflation, power/Lanczos,
+ * other), [13] = algorithmic fp64 flops of the eigensolver (products 2 d^2 n,
+ * Grams, applies, CholQR, Jacobi rotations, deflation), [14..17] = product
+ * breakdown in ns (phase A, inner barrier, phase B, leading barrier; CTA 0's
+ * view).  stats has 18 entries. */
 int tucker_stats(tucker_handle* h, int64_t* stats, int reset);
 
 #ifdef __cplusplus

@@ -51,7 +51,8 @@ struct FusedArgs {
   double* S;   // RP x LS (deflated in place; padding zeroed by the kernel)
   int d, J, k;
   int ls, lb, rp;           // S stride, block stride, padded rows
-  int mv_m8, mv_rb, mv_kb, mv_kc;  // product plan
+  int mv_m8, mv_rb, mv_kb, mv_kc;  // product plan (FusedArgs)
+  int sres_off;             // offset (doubles) of the resident S tile in dynamic smem, -1: streamed
   double* blk[5];           // five RP x LB work blocks (roles rotate)
   double* L;                // d x J locked vectors
   double* LT;               // d x J  S L
@@ -63,7 +64,7 @@ struct FusedArgs {
   int warm;
   double* outV;             // d x J output (ld = J)
   double* theta_out;        // J
-  long long* prof;          // [8] per-phase ns (CTA 0's view), accumulated
+  long long* prof;          // [8] per-phase ns (CTA 0's view), accumulated; [8] algorithmic flops
   int* info;                // [0] converged [1] outer [2] matvecs [3] jacobi sweeps [4] breakdown
   double* dinfo;            // [0] lambda_min estimate (0: not estimated) [1] last filter bound b
   int lanczos;              // estimate lambda_min (Lanczos) for the filter's lower bound
@@ -87,6 +88,7 @@ struct Ctx {
   int mv_m8, mv_rb, mv_kb, mv_kc;  // product plan (mv_plan(d, G)), computed on the host
   double* r1s;    // smem region 1 (k x (k+1) doubles or staging)
   double* r2s;    // smem region 2 (k x (k+1) doubles)
+  double* sres;   // resident S tile of the product plan (nullptr: S is streamed)
 };
 
 __device__ __forceinline__ void gsync() { cg::this_grid().sync(); }
@@ -218,7 +220,8 @@ __host__ __device__ inline MvPlan mv_plan(int d, int G) {
 constexpr int KC2 = 64;  // K per staged chunk inside a CTA's range
 __host__ __device__ inline int mv_ypad(int n8) { return ((8 * n8 + 15) & ~15) + 4; }  // = 4 or 12 mod 16
 __host__ __device__ inline size_t mv_stage_doubles(int m8, int n8) {
-  return (size_t)8 * m8 * (KC2 + 4) + (size_t)KC2 * mv_ypad(n8);
+  const int Mg = (m8 + 1) / 2, Ng = NW / Mg, GN = (n8 + Ng - 1) / Ng;
+  return (size_t)16 * Mg * (KC2 + 4) + (size_t)KC2 * mv_ypad(GN * Ng);
 }
 __host__ __device__ inline size_t mv_smem_doubles(int m8, int n8) { return 2 * mv_stage_doubles(m8, n8); }
 
@@ -231,92 +234,151 @@ __host__ __device__ inline size_t mv_smem_doubles(int m8, int n8) { return 2 * m
 // (row owners, row-local): Out = alpha sum_kb P_kb + gamma D + delta E in a
 // fixed order.  Y, D, E must be complete before the call (barrier); Out may
 // alias D or E (each element is read before it is written by the same thread).
+// Phase A of the product for one CTA tile, every warp on a uniform 2 x GN block
+// of 8x8 DMMA tiles (m-tile pair mg x n-tile group ng; tiles beyond the CTA's
+// rows / the active columns are computed on padding and not stored), so the
+// inner loop is straight-line code with no per-tile predicates.
+struct PhaseA {
+  const double* S;     // global S (row stride LS), used when the tile is streamed
+  const double* Y;     // global Y (row stride LB)
+  double* P;           // partial product of this K range (row stride LB)
+  double* stage;       // shared staging (2 buffers)
+  const double* sres;  // resident S tile (row stride SPR) or nullptr
+  int LS, LB, n, MT, MT2, row0, kbeg, nch, SPR, YP, Ng, Mg, tid, warp, lane;
+};
+
+template <int GN>
+__device__ __noinline__ void mv_phase_a(const PhaseA a) {
+  constexpr int SPK = KC2 + 4;
+  const int YC = 8 * GN * a.Ng;  // staged Y columns
+  const size_t STG = (size_t)a.MT2 * SPK + (size_t)KC2 * a.YP;
+  const int mg = a.warp / a.Ng, ng = a.warp - mg * a.Ng;
+  const bool wact = mg < a.Mg;
+  const int mt0 = 2 * mg, nt0 = ng * GN;
+  const bool res = a.sres != nullptr;
+  const double* gS = a.S + (int64_t)a.row0 * a.LS;
+  auto stage = [&](int buf, int k0) {
+    double* sS = a.stage + (size_t)buf * STG;
+    double* sY = sS + a.MT2 * SPK;
+    if (!res)
+      for (int u = a.tid; u < a.MT2 * (KC2 / 2); u += NT) {
+        const int r = u >> 5, c2 = (u & 31) << 1;
+        cp_async16(sS + r * SPK + c2, gS + (int64_t)r * a.LS + k0 + c2);
+      }
+    const int yu = YC >> 1;
+    for (int kk = a.warp; kk < KC2; kk += NW) {
+      const double* src = a.Y + (int64_t)(k0 + kk) * a.LB;
+      double* dst = sY + kk * a.YP;
+      for (int u = a.lane; u < yu; u += 32) cp_async16(dst + 2 * u, src + 2 * u);
+    }
+    cp_commit();
+  };
+  double acc[2][GN][2];
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int j = 0; j < GN; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+  const int ar = a.lane >> 2, aq = a.lane & 3;
+  stage(0, a.kbeg);
+  for (int ch = 0; ch < a.nch; ++ch) {
+    if (ch + 1 < a.nch) {
+      stage((ch + 1) & 1, a.kbeg + (ch + 1) * KC2);
+      cp_wait<1>();
+    } else {
+      cp_wait<0>();
+    }
+    __syncthreads();
+    if (wact) {
+      const double* sS = a.stage + (size_t)(ch & 1) * STG;
+      const double* sY = sS + a.MT2 * SPK;
+      const double* aS = res ? a.sres + ch * KC2 : sS;
+      const int aLD = res ? a.SPR : SPK;
+      const double* ap0 = aS + (8 * mt0 + ar) * aLD + aq;
+      const double* ap1 = ap0 + 8 * aLD;
+      const double* bp = sY + aq * a.YP + 8 * nt0 + ar;
+      const int bstep = 4 * a.YP;
+#pragma unroll 4
+      for (int kb4 = 0; kb4 < KC2; kb4 += 4) {
+        const double a0 = ap0[kb4], a1 = ap1[kb4];
+        double b[GN];
+#pragma unroll
+        for (int j = 0; j < GN; ++j) b[j] = bp[8 * j];
+        bp += bstep;
+#pragma unroll
+        for (int j = 0; j < GN; ++j) {
+          dmma(acc[0][j][0], acc[0][j][1], a0, b[j]);
+          dmma(acc[1][j][0], acc[1][j][1], a1, b[j]);
+        }
+      }
+    }
+    __syncthreads();  // buffer (ch & 1) free for chunk ch + 2
+  }
+  if (wact) {
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+      for (int j = 0; j < GN; ++j) {
+        const int rl = 8 * (mt0 + i) + ar, c = 8 * (nt0 + j) + 2 * aq;
+        if (rl < a.MT) {
+          double* pr = a.P + (int64_t)(a.row0 + rl) * a.LB;
+          if (c < a.n) pr[c] = acc[i][j][0];
+          if (c + 1 < a.n) pr[c + 1] = acc[i][j][1];
+        }
+      }
+  }
+}
+
+// Out = alpha S Y + gamma D + delta E on the padded layout (S RP x LS, Y/Out/D/E
+// RP x LB, n <= 116 active columns).  Phase A (every CTA (rb, kb) of the plan):
+// partial P_kb[rows of rb][0..n) = S[rows, K range] Y[K range, :] on DMMA
+// (mv_phase_a), K streamed in 64-wide chunks through a double-buffered 16-byte
+// cp.async ring (S from the resident tile when it fits in shared memory).
+// Partials go to `mpart` ([KB][RPX][LB]).  Barrier.  Phase B (row owners,
+// row-local): Out = alpha sum_kb P_kb + gamma D + delta E in a fixed order.
+// Y, D, E must be complete before the call (barrier); Out may alias D or E
+// (each element is read before it is written by the same thread).
 __device__ void matvec(const Ctx& x, double* mpart, const double* S, const double* Y, int n, double alpha,
-                       double* Out, double gamma, const double* Dm, double delta, const double* Em) {
+                       double* Out, double gamma, const double* Dm, double delta, const double* Em,
+                       long long* mvt = nullptr) {
+  long long t0 = mvt ? gtimer() : 0;
   const MvPlan pl{x.mv_m8, x.mv_rb, x.mv_kb, x.mv_kc};
   const int LS = x.ls, LB = x.lb;
   const int n8 = (n + 7) >> 3;
   const int RPX = (x.d + 8 * pl.m8 - 1) / (8 * pl.m8) * (8 * pl.m8);  // rows covered by the plan
   if (x.cta < pl.RB * pl.KB) {
     const int rb = x.cta / pl.KB, kb = x.cta - rb * pl.KB;
-    const int MT = 8 * pl.m8;
-    const int row0 = rb * MT;
-    const int kbeg = kb * pl.kchunk, kend = min(LS, kbeg + pl.kchunk);
-    const int Mg = (pl.m8 + 1) >> 1;            // m-tile pairs
-    const int gN = (n8 + (NW / Mg) - 1) / (NW / Mg);  // n-tiles per warp group (<= 4)
-    const int Ng = (n8 + gN - 1) / gN;
-    const int mg = x.warp / Ng, ng = x.warp - mg * Ng;
-    const bool wact = mg < Mg;
-    const int mt0 = 2 * mg, nmt = min(2, pl.m8 - mt0);
-    const int nt0 = ng * gN, nnt = min(gN, n8 - nt0);
-    const int YP = mv_ypad(n8);
-    const int SPK = KC2 + 4;
-    const size_t STG = mv_stage_doubles(pl.m8, n8);
-    double acc[2][4][2];
-#pragma unroll
-    for (int i = 0; i < 2; ++i)
-#pragma unroll
-      for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
-    const double* gS = S + (int64_t)row0 * LS;
-    const int yu = 4 * n8;  // 16-byte units per staged Y row (8 n8 doubles)
-    auto stage = [&](int buf, int k0) {
-      double* sS = x.r1s + (size_t)buf * STG;
-      double* sY = sS + MT * SPK;
-      for (int u = x.tid; u < MT * (KC2 / 2); u += NT) {
-        const int r = u >> 5, c2 = (u & 31) << 1;
-        cp_async16(sS + r * SPK + c2, gS + (int64_t)r * LS + k0 + c2);
-      }
-      for (int kk = x.warp; kk < KC2; kk += NW) {
-        const double* src = Y + (int64_t)(k0 + kk) * LB;
-        double* dst = sY + kk * YP;
-        for (int u = x.lane; u < yu; u += 32) cp_async16(dst + 2 * u, src + 2 * u);
-      }
-      cp_commit();
-    };
-    const int nch = (kend - kbeg) / KC2;
-    stage(0, kbeg);
-    const int ar = x.lane >> 2, aq = x.lane & 3;
-    for (int ch = 0; ch < nch; ++ch) {
-      if (ch + 1 < nch) {
-        stage((ch + 1) & 1, kbeg + (ch + 1) * KC2);
-        cp_wait<1>();
-      } else {
-        cp_wait<0>();
-      }
-      __syncthreads();
-      if (wact) {
-        const double* sS = x.r1s + (size_t)(ch & 1) * STG;
-        const double* sY = sS + MT * SPK;
-#pragma unroll 4
-        for (int kb4 = 0; kb4 < KC2; kb4 += 4) {
-          double a[2], b[4];
-#pragma unroll
-          for (int i = 0; i < 2; ++i) a[i] = i < nmt ? sS[(8 * (mt0 + i) + ar) * SPK + kb4 + aq] : 0.0;
-#pragma unroll
-          for (int j = 0; j < 4; ++j) b[j] = j < nnt ? sY[(kb4 + aq) * YP + 8 * (nt0 + j) + ar] : 0.0;
-#pragma unroll
-          for (int i = 0; i < 2; ++i)
-#pragma unroll
-            for (int j = 0; j < 4; ++j)
-              if (i < nmt && j < nnt) dmma(acc[i][j][0], acc[i][j][1], a[i], b[j]);
-        }
-      }
-      __syncthreads();  // buffer (ch & 1) free for chunk ch + 2
-    }
-    if (wact) {
-      double* P = mpart + (size_t)kb * RPX * LB;
-#pragma unroll
-      for (int i = 0; i < 2; ++i)
-#pragma unroll
-        for (int j = 0; j < 4; ++j)
-          if (i < nmt && j < nnt) {
-            const int r = row0 + 8 * (mt0 + i) + ar, c = 8 * (nt0 + j) + 2 * aq;
-            if (c < n) P[(int64_t)r * LB + c] = acc[i][j][0];
-            if (c + 1 < n) P[(int64_t)r * LB + c + 1] = acc[i][j][1];
-          }
+    PhaseA a;
+    a.S = S;
+    a.Y = Y;
+    a.P = mpart + (size_t)kb * RPX * LB;
+    a.stage = x.r1s;
+    a.sres = x.sres;
+    a.LS = LS;
+    a.LB = LB;
+    a.n = n;
+    a.MT = 8 * pl.m8;
+    a.Mg = (pl.m8 + 1) >> 1;
+    a.MT2 = 16 * a.Mg;
+    a.row0 = rb * a.MT;
+    a.kbeg = kb * pl.kchunk;
+    a.nch = (min(LS, a.kbeg + pl.kchunk) - a.kbeg) / KC2;
+    a.SPR = pl.kchunk + 4;
+    a.Ng = NW / a.Mg;
+    const int GN = (n8 + a.Ng - 1) / a.Ng;  // 1..4
+    a.YP = mv_ypad(GN * a.Ng);
+    a.tid = x.tid;
+    a.warp = x.warp;
+    a.lane = x.lane;
+    switch (GN) {
+      case 1: mv_phase_a<1>(a); break;
+      case 2: mv_phase_a<2>(a); break;
+      case 3: mv_phase_a<3>(a); break;
+      default: mv_phase_a<4>(a); break;
     }
   }
+  long long t1 = mvt ? gtimer() : 0;
   gsync();
+  long long t2 = mvt ? gtimer() : 0;
   // phase B: own rows
   for (int r = x.r0 + x.warp; r < x.r1; r += NW)
     for (int c = x.lane; c < n; c += 32) {
@@ -340,6 +402,30 @@ __device__ void matvec(const Ctx& x, double* mpart, const double* S, const doubl
       Out[o] = v;
     }
   __syncthreads();  // own rows of Out complete for any thread mapping
+  if (mvt) {
+    const long long t3 = gtimer();
+    mvt[0] += t1 - t0;
+    mvt[1] += t2 - t1;
+    mvt[2] += t3 - t2;
+  }
+}
+
+// (re)load this CTA's tile of S for the product plan into x.sres (after a barrier
+// that makes S complete); rows [rb MT, +MT) x K range [kb kchunk, +kchunk)
+__device__ void load_sres(const Ctx& x, const double* S) {
+  if (!x.sres || x.cta >= x.mv_rb * x.mv_kb) return;
+  const int rb = x.cta / x.mv_kb, kb = x.cta - rb * x.mv_kb;
+  const int MT = 8 * x.mv_m8, MT2 = 16 * ((x.mv_m8 + 1) / 2), SPR = x.mv_kc + 4;
+  const int kbeg = kb * x.mv_kc, klen = min(x.ls - kbeg, x.mv_kc);
+  const double* g = S + (int64_t)rb * MT * x.ls + kbeg;
+  const int upr = klen >> 1;  // 16-byte units per row
+  for (int u = x.tid; u < MT2 * upr; u += NT) {  // MT2 >= MT rows (padding rows are never stored)
+    const int r = u / upr, c2 = (u - r * upr) << 1;
+    cp_async16(x.sres + r * SPR + c2, g + (int64_t)r * x.ls + c2);
+  }
+  cp_commit();
+  cp_wait<0>();
+  __syncthreads();
 }
 
 // single vector: y[own rows] = S[own rows, :] q, partial ||y||^2 -> part[cta]
@@ -780,6 +866,7 @@ __global__ void __launch_bounds__(NT, 1) k_eig_fused(FusedArgs P) {
   const int ld = kp + 1;
   x.r1s = smem;
   x.r2s = smem + region1_doubles(kp, R);
+  x.sres = P.sres_off >= 0 ? smem + P.sres_off : nullptr;
   double* S = P.S;
 
   // buffer roles (indices into P.blk), swapped identically by every CTA
@@ -795,6 +882,12 @@ __global__ void __launch_bounds__(NT, 1) k_eig_fused(FusedArgs P) {
   long long pt = 0;
   if (x.tid < 8) pacc[x.tid] = 0;
   if (x.tid == 0) pt = gtimer();
+  // algorithmic fp64 flops of the solve (CTA 0 keeps the count; every CTA
+  // executes the same control flow): products 2 d^2 n, Grams 2 d n_a n_b,
+  // row-block applies 2 d m n, LDL^T CholQR (2/3) k^3, Jacobi rounds, deflation 4 d^2 n_l
+  double flops = 0.0;
+  long long mvt[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // CTA 0: product phase A, inner barrier, phase B,
+                                                // leading barrier (ns); stage wait, compute, chunk loop (clk)
   auto tick = [&](int cat) {
     if (x.cta == 0 && x.tid == 0) {
       const long long now = gtimer();
@@ -804,15 +897,21 @@ __global__ void __launch_bounds__(NT, 1) k_eig_fused(FusedArgs P) {
   };
 
   zero_padding(x, S, P.rp, P.blk);
+  gsync();
+  load_sres(x, S);
   if (P.warm) copy_cols(x, P.basis, LB, B(iQ), LB, k);
   else fill_random(x, B(iQ), LB, k, P.seed);
   __syncthreads();
 
   auto mv = [&](const double* Y, double alpha, double* Out, double gamma, const double* Dm, double delta,
                 const double* Em) {
+    const long long tg0 = (x.cta == 0 && x.tid == 0) ? gtimer() : 0;
     gsync();  // Y, D, E (and S) complete
-    matvec(x, P.mpart, S, Y, ka, alpha, Out, gamma, Dm, delta, Em);  // own rows of Out on return
+    if (x.cta == 0 && x.tid == 0) mvt[3] += gtimer() - tg0;
+    matvec(x, P.mpart, S, Y, ka, alpha, Out, gamma, Dm, delta, Em,
+           (x.cta == 0 && x.tid == 0) ? mvt : nullptr);  // own rows of Out on return
     ++matvecs;
+    flops += 2.0 * d * d * ka;
     tick(PF_MV);
   };
 
@@ -823,6 +922,7 @@ __global__ void __launch_bounds__(NT, 1) k_eig_fused(FusedArgs P) {
         gram_partial(x, P.L, J, nlock, B(iQ), LB, ka, P.part);
         reduce_bcast(x, P.part, nlock * ka, ka, P.red, x.r2s, ka);
         tick(PF_RED);
+        flops += 4.0 * d * nlock * ka;
         // Q[own] -= L[own] Z  (Z = r2s, nlock x ka, ld ka)
         for (int r = x.r0 + x.warp; r < x.r1; r += NW)
           for (int c = x.lane; c < ka; c += 32) {
@@ -840,6 +940,7 @@ __global__ void __launch_bounds__(NT, 1) k_eig_fused(FusedArgs P) {
       tick(PF_RED);
       cholqr_factor(x, x.r1s, x.r2s, ka, ld, pass == 0 ? shift : 0.0);
       tick(PF_CHOL);
+      flops += 2.0 * d * ka * ka + (2.0 / 3.0) * ka * ka * ka + 2.0 * d * ka * ka;
       apply_right(x, B(iQ), LB, ka, x.r2s, ld, 0, nullptr, B(iQ), LB, ka, x.r1s);
       tick(PF_APPLY);
     }
@@ -885,6 +986,11 @@ __global__ void __launch_bounds__(NT, 1) k_eig_fused(FusedArgs P) {
     tick(PF_JAC);
     if (sw < 0) breakdown = 1;
     else jsw += sw;
+    {
+      const double np2 = 0.5 * (ka + 1);
+      flops += 2.0 * d * ka * ka  // H = Q^T S Q
+               + (sw > 0 ? sw : 0) * (ka - 1) * (28.0 * np2 * (np2 + 1) / 2 + 12.0 * np2 * d);  // rotations
+    }
     ++n_rr;
     // Q <- Q V, SQ <- SQ V: the rotated staged rows, columns in descending Ritz order
     for (int r = x.warp; r < nrr; r += NW)
@@ -964,7 +1070,10 @@ __global__ void __launch_bounds__(NT, 1) k_eig_fused(FusedArgs P) {
       }
       __syncthreads();
     }
+    gsync();
+    load_sres(x, S);  // rows of other CTAs' tiles changed
     tick(PF_DEFL);
+    flops += 4.0 * d * d * nl + 2.0 * d * nl * nl;
   };
 
   // move the converged leading active vectors into L (prefix, descending order)
@@ -1005,6 +1114,7 @@ __global__ void __launch_bounds__(NT, 1) k_eig_fused(FusedArgs P) {
     for (int i = 0; i < npow; ++i) {
       matvec1(x, S, pq_, py_, P.part);
       ++matvecs;
+      flops += 2.0 * d * d;
       gsync();
       const double nrm = allsum_scalar(x, P.part);
       const double inv = nrm > 0 ? rsqrt(nrm) : 0.0;
@@ -1118,6 +1228,7 @@ __global__ void __launch_bounds__(NT, 1) k_eig_fused(FusedArgs P) {
       }
       beta = bnew;
       ++matvecs;
+      flops += 2.0 * d * d;
     }
     __syncthreads();
     a_lo = fmax(0.0, tridiag_min(x, lz_a, lz_b, LZ));
@@ -1248,6 +1359,10 @@ __global__ void __launch_bounds__(NT, 1) k_eig_fused(FusedArgs P) {
     }
     if (x.tid < 8) P.prof[x.tid] += pacc[x.tid];
     if (x.tid == 0) {
+      P.prof[8] += (long long)flops;
+      for (int i = 0; i < 4; ++i) P.prof[9 + i] += mvt[i];
+    }
+    if (x.tid == 0) {
       P.dinfo[0] = P.lanczos ? a_lo : -1.0;  // -1: no new estimate
       P.dinfo[1] = last_b;
       P.info[0] = converged ? 1 : 0;
@@ -1284,6 +1399,7 @@ __global__ void __launch_bounds__(NT, 1) k_eigf_unit_mv(const double* S, const d
   x.mv_kc = pl.kchunk;
   x.r1s = smem;
   x.r2s = smem;
+  x.sres = nullptr;
   for (int i = 0; i < reps; ++i) {
     gsync();
     // reps == -2: two products into Out and Out + RP LB (determinism check)
@@ -1320,6 +1436,7 @@ __global__ void __launch_bounds__(NT, 1) k_eigf_unit(int mode, const double* in,
   const int kp = k + (k & 1), ld = kp + 1;
   x.r1s = smem;
   x.r2s = smem + (size_t)kp * ld;
+  x.sres = nullptr;
   for (int r = x.warp; r < k; r += NW)
     for (int c = x.lane; c < k; c += 32) x.r1s[r * ld + c] = in[r * k + c];
   __syncthreads();
@@ -1400,14 +1517,27 @@ void eig_layout(int64_t d, int64_t* ls, int64_t* rows) {
   if (rows) *rows = l + 64;
 }
 
-size_t eig_fused_smem(int k, int d, int G) {
+// working area (doubles) of the solver: max over its phases
+size_t eig_work_doubles(int k, int d, int G) {
   const int kp = k + (k & 1);
   const int R = (d + G - 1) / G;
-  const size_t r2 = std::max((size_t)kp * (kp + 1), (size_t)2 * R * (kp + 1));  // H, W or staged Q/SQ rows
-  const size_t jac = (region1_doubles(kp, R) + r2) * sizeof(double);
-  const size_t mv = product_smem(d, k, G);
-  const size_t gp = (size_t)R * 2 * kp * sizeof(double);
+  const size_t r2 = std::max((size_t)kp * (kp + 1), (size_t)2 * R * (kp + 1));  // H, or staged Q/SQ rows
+  const size_t jac = region1_doubles(kp, R) + r2;
+  const size_t mv = product_smem(d, k, G) / sizeof(double);
+  const size_t gp = (size_t)R * 2 * kp;
   return std::max(jac, std::max(mv, gp));
+}
+// resident S tile (doubles) of the product plan
+size_t sres_doubles(int d, int G) {
+  const MvPlan pl = mv_plan(d, G);
+  return (size_t)16 * ((pl.m8 + 1) / 2) * (pl.kchunk + 4);
+}
+constexpr size_t SMEM_LIMIT = 219 * 1024;  // dynamic smem budget (static smem ~7.8 KB)
+
+size_t eig_fused_smem(int k, int d, int G) {
+  const size_t work = eig_work_doubles(k, d, G) * sizeof(double);
+  const size_t sres = sres_doubles(d, G) * sizeof(double);
+  return work + sres <= SMEM_LIMIT ? work + sres : work;
 }
 
 bool eig_fused(double* S, int64_t d, int J, EigSlot& slot, EigWs& ws, const EigOpts& o, double* out_V,
@@ -1416,7 +1546,7 @@ bool eig_fused(double* S, int64_t d, int J, EigSlot& slot, EigWs& ws, const EigO
   const int k = choose_block(J, d, o.oversample);
   const int grid = num_sms();  // one CTA per SM (cooperative: all co-resident)
   const size_t smem = eig_fused_smem(k, (int)d, grid);
-  if (smem + 8 * 1024 > 227 * 1024) fail(TUCKER_E_ARG, "eig_fused: block too large for shared memory");
+  if (smem > SMEM_LIMIT) fail(TUCKER_E_ARG, "eig_fused: block too large for shared memory");
   if (smem > smem_set) {
     TK_CUDA(cudaFuncSetAttribute(k_eig_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     smem_set = smem;
@@ -1442,9 +1572,9 @@ bool eig_fused(double* S, int64_t d, int J, EigSlot& slot, EigWs& ws, const EigO
   ws.pq.ensure((size_t)d);
   ws.py.ensure((size_t)d);
   ws.pz.ensure((size_t)d);
-  ws.fprof.ensure(8);
+  ws.fprof.ensure(13);
   if (!ws.fprof_init) {
-    TK_CUDA(cudaMemsetAsync(ws.fprof.p, 0, 8 * sizeof(long long), st));
+    TK_CUDA(cudaMemsetAsync(ws.fprof.p, 0, 13 * sizeof(long long), st));
     ws.fprof_init = true;
   }
   slot.basis.ensure((size_t)d * LB);
@@ -1476,6 +1606,8 @@ bool eig_fused(double* S, int64_t d, int J, EigSlot& slot, EigWs& ws, const EigO
     a.mv_rb = pl.RB;
     a.mv_kb = pl.KB;
     a.mv_kc = pl.kchunk;
+    const size_t work = eig_work_doubles(k, (int)d, grid);
+    a.sres_off = (work + sres_doubles((int)d, grid)) * sizeof(double) <= SMEM_LIMIT ? (int)work : -1;
   }
   a.basis = slot.basis.p;
   a.warm = (slot.valid && slot.d == d && slot.k == k) ? 1 : 0;

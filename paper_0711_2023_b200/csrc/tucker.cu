@@ -43,7 +43,7 @@ struct tucker_handle {
   GramWs gram;
   int64_t launches = 0;
   int64_t stat_outer0 = 0, stat_matvec0 = 0, stat_sweeps0 = 0;
-  long long prof0[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  long long prof0[13] = {0};
   std::string last_error;
   bool eig_unconverged = false;
 };
@@ -708,14 +708,14 @@ int tucker_stats(tucker_handle* h, int64_t* stats, int reset) {
   stats[3] = h->eig.stat_sweeps - h->stat_sweeps0;
   stats[4] = gram_path_id();
   {
-    long long pf[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    long long pf[13] = {0};
     if (h->eig.fprof.p && h->eig.fprof_init) {
       if (cudaMemcpy(pf, h->eig.fprof.p, sizeof(pf), cudaMemcpyDeviceToHost) != cudaSuccess)
         return TUCKER_E_CUDA;
     }
-    for (int i = 0; i < 8; ++i) stats[5 + i] = pf[i] - h->prof0[i];
+    for (int i = 0; i < 13; ++i) stats[5 + i] = pf[i] - h->prof0[i];
     if (reset)
-      for (int i = 0; i < 8; ++i) h->prof0[i] = pf[i];
+      for (int i = 0; i < 13; ++i) h->prof0[i] = pf[i];
   }
   if (reset) {
     h->launches = 0;
