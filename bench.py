@@ -313,6 +313,20 @@ def run_ours(args):
     gram_flops_step = S * (hflops + mflops)
     g_ach = gram_flops_step / (gram_ms / 1e3) / 1e12 if gram_ms > 0 else 0.0
     g_peak = pk["bf16_tflops"] * (1.1 / 2.25) / 3.0
+    # SpTTMc (HOOI projections): nonzeros per second and HBM fraction of its algorithmic bytes
+    # (CSF read 8 B/nnz + 12 B/fiber, split Y written 8 B/entry, factors read once)
+    hooi_proj_ms = stage_acc[0] / args.steps / S  # per HOOI sweep (N projections)
+    nfib = capi.tucker_csf_fibers(h, N)
+    ybytes = 0.0
+    for n in range(N):
+        P = int(np.prod([core[q] for q in range(N) if q != n]))
+        ybytes += 8.0 * dims[n] * P
+    alg_bytes = N * 8.0 * c["nnz"] + (12.0 * nfib if nfib else 0.0) + ybytes
+    spttmc = {"gnnz_s_per_mode": c["nnz"] * N / (hooi_proj_ms / 1e3) / 1e9 if hooi_proj_ms > 0 else None,
+              "alg_bytes_per_sweep": alg_bytes,
+              "hbm_frac": (alg_bytes / (hooi_proj_ms / 1e3)) / (pk["hbm_gbs"] * 1e9) if hooi_proj_ms > 0 else None,
+              "note": "HOOI SpTTMc (k_spttmc3/4) per sweep; bound is FP32 ALU + L2 gathers at config 2 "
+                      "(139 flop/B), so the HBM fraction is small by construction (SURVEY §8d)"}
     roof_gram = {"kernel": "k_syrk_tc (tcgen05 3xTF32 SYRK, fp64 drain)", "bound": "tensor",
                  "peak_note": "measured bf16 burst x tf32/bf16 nominal (1.1/2.25) / 3 products",
                  "achieved": g_ach, "peak": g_peak, "unit": "TFLOP/s", "frac": g_ach / g_peak}
@@ -335,6 +349,7 @@ def run_ours(args):
                 "d2h_bytes_per_step": int(d2h)},
         "roofline": roof,
         "roofline_gram": roof_gram,
+        "spttmc": spttmc,
         "clocks": clocks,
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

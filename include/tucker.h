@@ -177,6 +177,10 @@ int tucker_debug_product(int d, int n, const double* S, const double* Y, double 
 /* Timing of the same product alone: *us = microseconds per launch (mean of reps). */
 int tucker_debug_product_time(int d, int n, int reps, double* us);
 
+/* Sparse layout of the handle: out[2n] = fibers and out[2n + 1] = nonzeros of
+ * the CSF ordering mode n's HOOI projection uses (out has 2 N entries). */
+int tucker_csf_stats(tucker_handle* h, int64_t* out);
+
 /* Kernel statistics of the handle since the last reset (for bench/roofline):
  * stats[0] = kernel launches issued by the library, [1] = eigensolver outer
  * iterations, [2] = Chebyshev matvecs, [3] = small (k x k) Jacobi sweeps,

@@ -23,7 +23,7 @@ EXPORTS = [
     "tucker_default_opts", "tucker_init", "hooi_sweep", "mp_sweep", "core_and_fit",
     "tucker_set_factors", "tucker_free", "tucker_strerror", "tucker_last_error",
     "tucker_debug_ttmc", "tucker_debug_gram", "tucker_debug_eig", "tucker_debug_smalldense",
-    "tucker_debug_product", "tucker_debug_product_time", "tucker_stats",
+    "tucker_debug_product", "tucker_debug_product_time", "tucker_csf_stats", "tucker_stats",
 ]
 
 
@@ -61,6 +61,7 @@ def load(path: str = LIB_PATH) -> C.CDLL:
     lib.tucker_stats.argtypes = [P, i64p, C.c_int]
     lib.tucker_debug_product.argtypes = [C.c_int, C.c_int, P, P, C.c_double, C.c_double, P, P]
     lib.tucker_debug_product_time.argtypes = [C.c_int, C.c_int, C.c_int, C.POINTER(C.c_double)]
+    lib.tucker_csf_stats.argtypes = [P, i64p]
     lib.tucker_debug_smalldense.argtypes = [C.c_int, C.c_int, P, P, P, P, C.c_int, C.c_double]
     for name in EXPORTS:
         if name not in ("tucker_default_opts", "tucker_strerror", "tucker_last_error"):
@@ -243,6 +244,13 @@ def tucker_debug_product_time(d, n, reps=50):
     us = C.c_double(0)
     _check(lib().tucker_debug_product_time(d, n, reps, C.byref(us)))
     return us.value
+
+
+def tucker_csf_fibers(h, order=3):
+    """Total fibers of the HOOI CSF orderings (all modes)."""
+    s = (C.c_int64 * 8)()
+    _check(lib().tucker_csf_stats(h, s), h)
+    return int(sum(s[2 * n] for n in range(order)))
 
 
 def tucker_stats(h, reset=False):

@@ -91,7 +91,18 @@ struct Ctx {
   double* sres;   // resident S tile of the product plan (nullptr: S is streamed)
 };
 
-__device__ __forceinline__ void gsync() { cg::this_grid().sync(); }
+__device__ unsigned long long g_gsync_stat[2];  // [0] barriers, [1] ns (CTA 0's view; debug)
+__device__ __forceinline__ void gsync() {
+  long long t0 = 0;
+  if (blockIdx.x == 0 && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  cg::this_grid().sync();
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    long long t1;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+    g_gsync_stat[0] += 1;
+    g_gsync_stat[1] += (unsigned long long)(t1 - t0);
+  }
+}
 
 __device__ __forceinline__ long long gtimer() {
   long long t;
@@ -533,17 +544,30 @@ __device__ void gram_partial(const Ctx& x, const double* A, int lda, int na, con
 
 // red[e] = sum_z part[z][e] (fixed order), entries distributed over CTAs; then
 // barrier and every CTA copies red into dst (smem, row stride ldd, nb columns).
+// Loads are issued in batches (independent registers) so each phase costs about
+// one L2 round trip instead of one per element.
 __device__ void reduce_bcast(const Ctx& x, const double* part, int E, int nb, double* red, double* dst,
                              int ldd) {
   gsync();
   const int per = (E + x.G - 1) / x.G;
   const int e0 = x.cta * per, e1 = min(E, e0 + per);
-  // 8 threads per entry, each a strided subset of the partials, combined by shuffles
+  // 8 threads per entry, each a strided subset of the partials (4 loads in flight),
+  // combined by shuffles in a fixed pattern
   for (int base = e0; base < e1; base += NT / 8) {
     const int e = base + x.tid / 8, sub = x.tid % 8;
     double s = 0.0;
-    if (e < e1)
-      for (int z = sub; z < x.G; z += 8) s += __ldcg(part + (size_t)z * E + e);
+    if (e < e1) {
+      int z = sub;
+      for (; z + 24 < x.G; z += 32) {
+        const double v0 = __ldcg(part + (size_t)z * E + e), v1 = __ldcg(part + (size_t)(z + 8) * E + e);
+        const double v2 = __ldcg(part + (size_t)(z + 16) * E + e), v3 = __ldcg(part + (size_t)(z + 24) * E + e);
+        s += v0;
+        s += v1;
+        s += v2;
+        s += v3;
+      }
+      for (; z < x.G; z += 8) s += __ldcg(part + (size_t)z * E + e);
+    }
     s += __shfl_xor_sync(0xffffffffu, s, 1);
     s += __shfl_xor_sync(0xffffffffu, s, 2);
     s += __shfl_xor_sync(0xffffffffu, s, 4);
@@ -551,14 +575,30 @@ __device__ void reduce_bcast(const Ctx& x, const double* part, int E, int nb, do
   }
   gsync();
   const int nrow = E / nb;
-  for (int i = x.warp; i < nrow; i += NW)
-    for (int j = x.lane; j < nb; j += 32) dst[i * ldd + j] = __ldcg(red + i * nb + j);
+  constexpr int B8 = 8;
+  for (int e0b = 0; e0b < E; e0b += NT * B8) {
+    double v[B8];
+#pragma unroll
+    for (int t = 0; t < B8; ++t) {
+      const int e = e0b + x.tid + NT * t;
+      v[t] = e < E ? __ldcg(red + e) : 0.0;
+    }
+#pragma unroll
+    for (int t = 0; t < B8; ++t) {
+      const int e = e0b + x.tid + NT * t;
+      if (e < E) {
+        const int i = e / nb;
+        dst[i * ldd + (e - i * nb)] = v[t];
+      }
+    }
+  }
+  (void)nrow;
   __syncthreads();
 }
 
-// fp64 reciprocal / reciprocal square root from the fp32 approximations plus
-// Newton steps (2 for rcp: 1e-7 -> 1e-14 -> 1e-16; 2 for rsqrt) -- short
-// dependency chains instead of the IEEE division / sqrt sequences.
+// fp64 reciprocal / reciprocal square root from the hardware approximations plus
+// Newton steps -- short dependency chains instead of the IEEE division / sqrt
+// sequences.
 __device__ __forceinline__ double rcp_nt(double x) {
   double r = (double)__frcp_rn((float)x);
   r = r * fma(-x, r, 2.0);
@@ -1359,6 +1399,7 @@ __global__ void __launch_bounds__(NT, 1) k_eig_fused(FusedArgs P) {
     }
     if (x.tid < 8) P.prof[x.tid] += pacc[x.tid];
     if (x.tid == 0) {
+      if (P.dbg) printf("[eigf-sync] grid barriers so far %llu, %.3f ms\n", g_gsync_stat[0], g_gsync_stat[1] * 1e-6);
       P.prof[8] += (long long)flops;
       for (int i = 0; i < 4; ++i) P.prof[9 + i] += mvt[i];
     }

@@ -347,12 +347,17 @@ void gram_syrk_tc(const Split& A, double* S, int64_t lds, GramWs& ws, cudaStream
             (const int2*)ws.scratch.p, ntiles, splits, d, S, lds);
 }
 
+// Path selection: fp64 DMMA when the SYRK is small enough to afford fp64
+// (<= 2e10 FMA, ~1 ms at the measured 37 TFLOP/s; all HOOI Grams of configs 1-4),
+// 3xTF32 tcgen05 with fp64 drains for the large MP Grams.
 void gram_syrk(const Split& A, double* S, int64_t lds, GramWs& ws, cudaStream_t st) {
   if (gram_mode() == 1) {
     gram_syrk_simt(A, S, lds, st);
-  } else {
-    gram_syrk_tc(A, S, lds, ws, st);
+    return;
   }
+  const double fma = 0.5 * (double)A.rows * (double)(A.rows + 1) * (double)A.ld;
+  if (fma <= 2e10) gram_syrk_dmma(A, S, lds, ws, st);
+  else gram_syrk_tc(A, S, lds, ws, st);
 }
 
 int gram_path_id() { return gram_mode(); }

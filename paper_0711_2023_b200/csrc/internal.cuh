@@ -68,6 +68,8 @@ struct GramWs {
   DBuf<uint8_t> scratch;
 };
 void gram_syrk(const Split& A, double* S, int64_t lds, GramWs& ws, cudaStream_t st);
+// fp64 tensor-core (DMMA) path for Grams small enough to afford fp64
+void gram_syrk_dmma(const Split& A, double* S, int64_t lds, GramWs& ws, cudaStream_t st);
 // reference SIMT fp64 path (debug/validation of the tensor-core kernel)
 void gram_syrk_simt(const Split& A, double* S, int64_t lds, cudaStream_t st);
 int gram_mode();     // 0 = tcgen05 (default), 1 = SIMT (env TUCKER_GRAM=simt)

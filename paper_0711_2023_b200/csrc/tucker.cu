@@ -700,6 +700,16 @@ int tucker_debug_product_time(int d, int n, int reps, double* us) {
   });
 }
 
+int tucker_csf_stats(tucker_handle* h, int64_t* out) {
+  if (!h || !out) return TUCKER_E_ARG;
+  for (int n = 0; n < h->order; ++n) {
+    const Csf& c = *h->csfs[h->hooi_csf[n]];
+    out[2 * n] = c.nfib;
+    out[2 * n + 1] = c.nnz;
+  }
+  return TUCKER_OK;
+}
+
 int tucker_stats(tucker_handle* h, int64_t* stats, int reset) {
   if (!h || !stats) return TUCKER_E_ARG;
   stats[0] = h->launches;

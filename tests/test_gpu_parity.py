@@ -140,16 +140,20 @@ def test_config1_full(capi):
         assert abs(fit - ref[algo]["fit"]) < 1e-5
 
 
-@pytest.mark.parametrize("k", [2])
-def test_config_full(capi, k):
-    """BASELINE.json configs[k-1] at full size, 5 HOOI + 5 MP sweeps from the same
-    U0 (the bench's workload): factors, fits per sweep and core vs the fp64 oracle."""
+@pytest.mark.parametrize("k,sweeps", [(2, None), (3, 2), (4, 2)])
+def test_config_full(capi, k, sweeps):
+    """BASELINE.json configs[k-1] at full size from the seeded U0: config 2 with its
+    5 HOOI + 5 MP sweeps (the bench's workload), configs 3 (2000^3, 8e6 nnz, core
+    100x25x10) and 4 (order 4, 200^4, 1.6e7 nnz) with 2 sweeps each to bound the fp64
+    oracle's host time.  Factors (projector distance), fits per sweep and the core
+    (after Procrustes alignment) vs the oracle."""
     c = make_config(k)
-    out, ref = run_both(capi, c["dims"], c["idx"], c["vals"], c["U0"], c["core"], c["sweeps"])
+    sw = c["sweeps"] if sweeps is None else sweeps
+    out, ref = run_both(capi, c["dims"], c["idx"], c["vals"], c["U0"], c["core"], sw)
     for algo in ("hooi", "mp"):
         fits, G, U, fit = out[algo]
         r = ref[algo]
-        for n in range(3):
+        for n in range(len(c["dims"])):
             d = O.projector_distance(U[n], r["U"][n])
             assert d < 1e-4, (algo, n, d)
         assert abs(fit - r["fit"]) < 1e-5
