@@ -177,8 +177,10 @@ int tucker_debug_product(int d, int n, const double* S, const double* Y, double 
 /* Timing of the same product alone: *us = microseconds per launch (mean of reps). */
 int tucker_debug_product_time(int d, int n, int reps, double* us);
 
-/* Sparse layout of the handle: out[2n] = fibers and out[2n + 1] = nonzeros of
- * the CSF ordering mode n's HOOI projection uses (out has 2 N entries). */
+/* Sparse layout of the handle, for the CSF ordering mode n's HOOI projection
+ * uses (out has 4 N entries): out[4n] = fibers, out[4n + 1] = nonzeros,
+ * out[4n + 2] = virtual fibers of the SpTTMc work plan and out[4n + 3] = its
+ * work units (both 0 when the tensor needs no plan: one CTA per slice). */
 int tucker_csf_stats(tucker_handle* h, int64_t* out);
 
 /* Kernel statistics of the handle since the last reset (for bench/roofline):

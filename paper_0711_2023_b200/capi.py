@@ -246,11 +246,17 @@ def tucker_debug_product_time(d, n, reps=50):
     return us.value
 
 
+def tucker_csf_stats(h, order=3):
+    """Per mode (fibers, nonzeros, virtual fibers, work units) of the HOOI CSF
+    orderings; the last two are 0 without a SpTTMc work plan."""
+    s = (C.c_int64 * 16)()
+    _check(lib().tucker_csf_stats(h, s), h)
+    return [tuple(int(s[4 * n + q]) for q in range(4)) for n in range(order)]
+
+
 def tucker_csf_fibers(h, order=3):
     """Total fibers of the HOOI CSF orderings (all modes)."""
-    s = (C.c_int64 * 8)()
-    _check(lib().tucker_csf_stats(h, s), h)
-    return int(sum(s[2 * n] for n in range(order)))
+    return sum(st[0] for st in tucker_csf_stats(h, order))
 
 
 def tucker_stats(h, reset=False):
@@ -287,6 +293,9 @@ class Tucker:
     def debug_ttmc(self, mode):
         P = int(np.prod([J for m, J in enumerate(self.core) if m != mode]))
         return tucker_debug_ttmc(self.h, mode, self.dims[mode], P)
+
+    def csf_stats(self):
+        return tucker_csf_stats(self.h, len(self.dims))
 
     def debug_gram(self, algo, mode):
         return tucker_debug_gram(self.h, algo, mode, self.dims[mode])

@@ -28,6 +28,19 @@ struct Csf {
   int64_t nnz = 0, nfib = 0, nnode = 0;
   DBuf<int32_t> slice_ptr, node_ptr, node_mid0, fib_ptr, fib_root, fib_mid0, fib_mid1, leaf_id;
   DBuf<float> val;
+  // HOOI SpTTMc work plan (order 3, spttmc_plan), built only for skewed
+  // tensors: fibers longer than lmax nonzeros are cut into virtual fibers
+  // (same mid index; Eq. 1 is linear in t_f), and slices whose work
+  // J_l*nnz + J_m*J_l*fibers exceeds cmax are cut into units over virtual-
+  // fiber ranges that write fp32 partial tiles, summed per slice in fixed
+  // order (deterministic).  Units are ordered heaviest first so the block
+  // scheduler packs them greedily.
+  int64_t nunits = 0, nred = 0, nslots = 0, nvfib = 0, lmax = 0;
+  double cmax = 0;
+  DBuf<int32_t> vfib_ptr, vfib_mid;  // virtual fibers (nvfib + 1 / nvfib)
+  DBuf<int32_t> unit;  // 4 ints per unit: slice, vf0, vf1, slot (-1: write Y directly)
+  DBuf<int32_t> red;   // 3 ints per split slice: slice, first slot, #slots
+  DBuf<float> part;    // nslots x (J_mid * J_leaf) partial tiles
 };
 
 struct Coo {  // validated, zero-free COO on the device
@@ -42,6 +55,8 @@ struct Coo {  // validated, zero-free COO on the device
 void coo_validate_compact(Coo& coo, cudaStream_t st);          // E_INDEX / E_VALUE, drops zeros
 double coo_norm2(const Coo& coo, cudaStream_t st);              // ||X||_F^2 (fp64, fixed order)
 void csf_build(const Coo& coo, Csf& out, int root, int mid0, int mid1, int leaf, cudaStream_t st);
+// spttmc.cu: HOOI work units for an order-3 CSF whose output tile is Jm x Jl
+void spttmc_plan(Csf& c, int64_t Jm, int64_t Jl, int num_sms, cudaStream_t st);
 
 // ---------------------------------------------------------------------------
 // Split-fp32 matrix: a = hi + lo exactly, hi = tf32-rounded a (DESIGN.md

@@ -13,6 +13,11 @@
 //
 // MP (Fig. 7/8, Appendix): W = (X x_m U_m^T)_(n), whose column
 // block for the slice s fixing the modes not in {n, m} is X_s U_m.
+#include <algorithm>
+#include <cstdlib>
+#include <array>
+#include <vector>
+
 #include "internal.cuh"
 
 namespace tk {
@@ -105,6 +110,8 @@ __device__ __forceinline__ void kron_stage(int nf, const float* T, const float* 
 
 struct Ttmc3Args {
   const int32_t *slice_ptr, *fib_ptr, *fib_mid, *leaf_id;
+  const int32_t* unit;  // work units (slice, f0, f1, slot) or null: one CTA per slice
+  float* part;          // partial tiles of split slices (Jm * Jl floats per slot)
   const float* val;
   const float *Umid, *Uleaf;
   int Jm, Jl;
@@ -119,8 +126,18 @@ __global__ void __launch_bounds__(256) k_spttmc3(Ttmc3Args p) {
   constexpr int JLP = 16 * RB, JMP = 16 * RA;
   __shared__ float T[kFC * JLP];
   __shared__ float M[kFC * JMP];
-  const int i = blockIdx.x;
-  const int f0 = p.slice_ptr[i], f1 = p.slice_ptr[i + 1];
+  int i, f0, f1, slot = -1;
+  if (p.unit) {
+    const int4 u = reinterpret_cast<const int4*>(p.unit)[blockIdx.x];
+    i = u.x;
+    f0 = u.y;
+    f1 = u.z;
+    slot = u.w;
+  } else {
+    i = blockIdx.x;
+    f0 = p.slice_ptr[i];
+    f1 = p.slice_ptr[i + 1];
+  }
   float acc[RA][RB];
 #pragma unroll
   for (int r = 0; r < RA; ++r)
@@ -140,12 +157,32 @@ __global__ void __launch_bounds__(256) k_spttmc3(Ttmc3Args p) {
 #pragma unroll
     for (int c = 0; c < RB; ++c) {
       const int a = ty + 16 * r, b = tx + 16 * c;
-      if (a < p.Jm && b < p.Jl) {
+      if (slot >= 0) {
+        if (a < p.Jm && b < p.Jl) p.part[(int64_t)slot * p.Jm * p.Jl + a * p.Jl + b] = acc[r][c];
+      } else if (a < p.Jm && b < p.Jl) {
         const int64_t col = a * p.sa + b * p.sb;
         const int64_t off = p.transposed ? col * p.ldY + i : (int64_t)i * p.ldY + col;
         split_store(p.Yhi, p.Ylo, off, acc[r][c]);
       }
     }
+}
+
+// Y row of a split slice = sum of its units' partial tiles, in slot order
+__global__ void __launch_bounds__(256) k_spttmc3_reduce(const int32_t* __restrict__ red,
+                                                        const float* __restrict__ part, int Jm, int Jl,
+                                                        int64_t sa, int64_t sb, float* Yhi, float* Ylo,
+                                                        int64_t ldY, int transposed) {
+  const int r = blockIdx.y;
+  const int i = red[3 * r], s0 = red[3 * r + 1], ns = red[3 * r + 2];
+  const int P = Jm * Jl;
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= P) return;
+  float y = 0.f;
+  for (int s = 0; s < ns; ++s) y += __ldcs(part + (int64_t)(s0 + s) * P + c);
+  const int a = c / Jl, b = c - a * Jl;
+  const int64_t col = a * sa + b * sb;
+  const int64_t off = transposed ? col * ldY + i : (int64_t)i * ldY + col;
+  split_store(Yhi, Ylo, off, y);
 }
 
 struct Ttmc4Args {
@@ -294,14 +331,30 @@ void spttmc_hooi(const Csf& c, const float* const* U, const int64_t* J, Split ou
     a.transposed = transposed;
     a.sa = kolda_stride(c.mid0, others, no, J);
     a.sb = kolda_stride(c.leaf, others, no, J);
+    a.unit = c.nunits > 0 ? c.unit.p : nullptr;
+    if (c.nunits > 0) {  // virtual fibers
+      a.fib_ptr = c.vfib_ptr.p;
+      a.fib_mid = c.vfib_mid.p;
+    }
+    a.part = c.part.p;
     const int RA = rtile(a.Jm), RB = rtile(a.Jl);
-    const dim3 g((unsigned)c.I_root);
-#define TK_S3(ra, rb) \
-  if (RA <= ra && RB <= rb) { TK_LAUNCH((k_spttmc3<ra, rb>), g, 256, 0, st, a); return; }
+    const dim3 g((unsigned)(c.nunits > 0 ? c.nunits : c.I_root));
+    bool launched = false;
+#define TK_S3(ra, rb)                                            \
+  if (!launched && RA <= ra && RB <= rb) {                        \
+    TK_LAUNCH((k_spttmc3<ra, rb>), g, 256, 0, st, a);             \
+    launched = true;                                              \
+  }
     TK_S3(1, 1) TK_S3(2, 1) TK_S3(1, 2) TK_S3(2, 2) TK_S3(4, 1) TK_S3(1, 4) TK_S3(4, 2)
     TK_S3(2, 4) TK_S3(4, 4) TK_S3(8, 2) TK_S3(2, 8) TK_S3(8, 4) TK_S3(4, 8) TK_S3(8, 8)
 #undef TK_S3
-    fail(TUCKER_E_ARG, "spttmc: unsupported core size");
+    if (!launched) fail(TUCKER_E_ARG, "spttmc: unsupported core size");
+    if (c.nred > 0) {
+      const dim3 gr((unsigned)ceil_div((int64_t)a.Jm * a.Jl, 256), (unsigned)c.nred);
+      TK_LAUNCH(k_spttmc3_reduce, gr, 256, 0, st, c.red.p, c.part.p, a.Jm, a.Jl, a.sa, a.sb, a.Yhi,
+                a.Ylo, ldY, (int)transposed);
+    }
+    return;
   }
   Ttmc4Args a;
   a.slice_ptr = c.slice_ptr.p;
@@ -337,6 +390,114 @@ void spttmc_hooi(const Csf& c, const float* const* U, const int64_t* J, Split ou
   TK_S4(4, 4, 32) TK_S4(4, 4, 64)
 #undef TK_S4
   fail(TUCKER_E_ARG, "spttmc: unsupported order-4 core size (prod J <= 16384, J <= 64)");
+}
+
+// Work plan for the order-3 HOOI kernel (see Csf).  lmax = 1024 nonzeros
+// per virtual fiber (the extra Kronecker updates cost <= J_m/1024 of the
+// fiber stage); cmax = max(2^22, total work / (16 * #SMs)).  Uniform configs
+// 1-4 have short fibers and light slices: no plan, one CTA per slice.
+// Config 5's Zipf head (a slice with 7e6 nonzeros in <= 5000 fibers) is what
+// this is for.
+void spttmc_plan(Csf& c, int64_t Jm, int64_t Jl, int num_sms, cudaStream_t st) {
+  if (c.order != 3) return;
+  const int64_t I = c.I_root, F = c.nfib;
+  std::vector<int32_t> sp((size_t)I + 1), fp((size_t)F + 1);
+  TK_CUDA(cudaMemcpyAsync(sp.data(), c.slice_ptr.p, sp.size() * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+  TK_CUDA(cudaMemcpyAsync(fp.data(), c.fib_ptr.p, fp.size() * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+  TK_CUDA(cudaStreamSynchronize(st));
+  c.lmax = 1024;
+  // test hooks: force the plan on small inputs (TUCKER_TTMC_LMAX / _CMAX)
+  const char* el = std::getenv("TUCKER_TTMC_LMAX");
+  const char* ec = std::getenv("TUCKER_TTMC_CMAX");
+  if (el && std::atoll(el) > 0) c.lmax = std::atoll(el);
+  const double wf = (double)Jm * Jl, wn = (double)Jl;  // work per fiber / per nonzero
+  double total = 0;
+  int64_t longest = 0;
+  for (int64_t f = 0; f < F; ++f) {
+    const int64_t L = fp[f + 1] - fp[f];
+    longest = std::max(longest, L);
+    total += wf * (double)ceil_div(L, c.lmax) + wn * (double)L;
+  }
+  c.cmax = std::max(4194304.0, total / (16.0 * num_sms));
+  if (ec && std::atof(ec) > 0) c.cmax = std::atof(ec);
+  double heaviest = 0;
+  for (int64_t i = 0; i < I; ++i) {
+    const double w = wf * (double)(sp[i + 1] - sp[i]) + wn * (double)(fp[sp[i + 1]] - fp[sp[i]]);
+    heaviest = std::max(heaviest, w);
+  }
+  c.nunits = c.nred = c.nslots = c.nvfib = 0;
+  if (longest <= c.lmax && heaviest <= c.cmax) return;  // one CTA per slice
+  std::vector<int32_t> fm((size_t)F);
+  TK_CUDA(cudaMemcpyAsync(fm.data(), c.fib_mid0.p, fm.size() * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+  TK_CUDA(cudaStreamSynchronize(st));
+  // virtual fibers, and per slice the virtual-fiber range
+  std::vector<int32_t> vptr, vmid, vsp((size_t)I + 1);
+  vptr.reserve((size_t)F + 1);
+  vmid.reserve((size_t)F);
+  for (int64_t i = 0; i < I; ++i) {
+    vsp[i] = (int32_t)vmid.size();
+    for (int64_t f = sp[i]; f < sp[i + 1]; ++f) {
+      const int64_t L = fp[f + 1] - fp[f], nv = std::max<int64_t>(1, ceil_div(L, c.lmax));
+      for (int64_t v = 0; v < nv; ++v) {
+        vptr.push_back((int32_t)(fp[f] + v * L / nv));
+        vmid.push_back(fm[f]);
+      }
+    }
+  }
+  vsp[I] = (int32_t)vmid.size();
+  vptr.push_back(fp[F]);
+  c.nvfib = (int64_t)vmid.size();
+  // units: greedy cut of each slice's virtual fibers at ~equal work
+  std::vector<std::array<int32_t, 4>> units;
+  std::vector<double> uw;
+  std::vector<int32_t> red;
+  int32_t slot = 0;
+  for (int64_t i = 0; i < I; ++i) {
+    const int64_t v0 = vsp[i], v1 = vsp[i + 1];
+    if (v1 == v0) continue;  // Y is zeroed before the launch
+    const double w = wf * (double)(v1 - v0) + wn * (double)(vptr[v1] - vptr[v0]);
+    if (w <= c.cmax) {
+      units.push_back({(int32_t)i, (int32_t)v0, (int32_t)v1, -1});
+      uw.push_back(w);
+      continue;
+    }
+    const int64_t nu = (int64_t)std::ceil(w / c.cmax);
+    const double target = w / (double)nu;
+    const int32_t first = slot;
+    int64_t a = v0;
+    double acc = 0;
+    for (int64_t v = v0; v < v1; ++v) {
+      acc += wf + wn * (double)(vptr[v + 1] - vptr[v]);
+      if (acc >= target || v + 1 == v1) {
+        units.push_back({(int32_t)i, (int32_t)a, (int32_t)(v + 1), slot++});
+        uw.push_back(acc);
+        a = v + 1;
+        acc = 0;
+      }
+    }
+    red.insert(red.end(), {(int32_t)i, first, slot - first});
+  }
+  std::vector<int64_t> order(units.size());
+  for (size_t u = 0; u < order.size(); ++u) order[u] = (int64_t)u;
+  std::stable_sort(order.begin(), order.end(), [&](int64_t x, int64_t y) { return uw[x] > uw[y]; });
+  std::vector<int32_t> flat;
+  flat.reserve(units.size() * 4);
+  for (int64_t u : order) flat.insert(flat.end(), units[u].begin(), units[u].end());
+  c.nunits = (int64_t)units.size();
+  c.nred = (int64_t)red.size() / 3;
+  c.nslots = slot;
+  c.vfib_ptr.alloc(vptr.size());
+  c.vfib_mid.alloc(vmid.size());
+  c.unit.alloc(flat.size());
+  TK_CUDA(cudaMemcpyAsync(c.vfib_ptr.p, vptr.data(), vptr.size() * sizeof(int32_t), cudaMemcpyHostToDevice, st));
+  TK_CUDA(cudaMemcpyAsync(c.vfib_mid.p, vmid.data(), vmid.size() * sizeof(int32_t), cudaMemcpyHostToDevice, st));
+  TK_CUDA(cudaMemcpyAsync(c.unit.p, flat.data(), flat.size() * sizeof(int32_t), cudaMemcpyHostToDevice, st));
+  if (!red.empty()) {
+    c.red.alloc(red.size());
+    TK_CUDA(cudaMemcpyAsync(c.red.p, red.data(), red.size() * sizeof(int32_t), cudaMemcpyHostToDevice, st));
+    c.part.alloc((size_t)(c.nslots * Jm * Jl));
+  }
+  TK_CUDA(cudaStreamSynchronize(st));  // the host vectors go out of scope
 }
 
 void spmm_mp(const Csf& c, const float* U_leaf, int64_t J_leaf, Split out, int64_t col_off,

@@ -356,6 +356,12 @@ const char* tucker_strerror(int code) {
 
 const char* tucker_last_error(const tucker_handle* h) { return h ? h->last_error.c_str() : ""; }
 
+static int sm_count(int dev) {
+  int n = 0;
+  TK_CUDA(cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev));
+  return n;
+}
+
 int tucker_init(tucker_handle** out, int order, const int64_t* dims, const int64_t* core,
                 int64_t nnz, const int32_t* const* idx, const float* vals, const float* const* U0,
                 const tucker_opts* opts) {
@@ -422,11 +428,28 @@ int tucker_init(tucker_handle** out, int order, const int64_t* dims, const int64
         h->mp_csf[n][m] = (int)h->csfs.size();
         h->csfs.push_back(std::move(cs));
       }
-      // HOOI: leaf = the other mode with the smallest J (ties: highest mode id)
+      // HOOI leaf: minimise the SpTTMc flop model
+      // J_leaf * nnz (fiber stage) + (prod_{q != n} J_q) * nfib (Kronecker
+      // stage) over the built orderings (ties: highest mode id)
       int best = -1;
-      for (int m = 0; m < order; ++m)
-        if (m != n && (best < 0 || h->J[m] <= h->J[best])) best = m;
+      double best_cost = 0;
+      double Pn = 1;
+      for (int q = 0; q < order; ++q)
+        if (q != n) Pn *= (double)h->J[q];
+      for (int m = 0; m < order; ++m) {
+        if (m == n) continue;
+        const Csf& cm = *h->csfs[h->mp_csf[n][m]];
+        const double cost = (double)h->J[m] * (double)cm.nnz + Pn * (double)(order == 4 ? cm.nnode : cm.nfib);
+        if (best < 0 || cost <= best_cost) {
+          best = m;
+          best_cost = cost;
+        }
+      }
       h->hooi_csf[n] = h->mp_csf[n][best];
+      if (order == 3) {
+        Csf& ch = *h->csfs[h->hooi_csf[n]];
+        spttmc_plan(ch, h->J[ch.mid0], h->J[ch.leaf], sm_count(h->opts.device), h->st);
+      }
     }
     // the COO copy is no longer needed
     for (int n = 0; n < order; ++n) c.idx[n].release();
@@ -704,8 +727,10 @@ int tucker_csf_stats(tucker_handle* h, int64_t* out) {
   if (!h || !out) return TUCKER_E_ARG;
   for (int n = 0; n < h->order; ++n) {
     const Csf& c = *h->csfs[h->hooi_csf[n]];
-    out[2 * n] = c.nfib;
-    out[2 * n + 1] = c.nnz;
+    out[4 * n] = c.nfib;
+    out[4 * n + 1] = c.nnz;
+    out[4 * n + 2] = c.nvfib;   // 0: no work plan (one CTA per slice)
+    out[4 * n + 3] = c.nunits;
   }
   return TUCKER_OK;
 }

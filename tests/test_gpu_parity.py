@@ -62,6 +62,35 @@ def test_ttmc_parity(capi, dims, nnz, core):
             assert O.rel_frobenius(Y, Yo) < 1e-4
 
 
+@pytest.mark.parametrize("lmax,cmax", [(None, None), ("7", "3000"), ("64", "20000")])
+def test_ttmc_parity_skewed(capi, monkeypatch, lmax, cmax):
+    """Zipf-skewed tensor (config 5's index law at oracle size): long fibers and
+    heavy head slices.  With the env hooks the SpTTMc work plan cuts fibers
+    into virtual fibers of <= lmax nonzeros and slices into units of <= cmax
+    work; Y must not depend on the cut (Eq. 1 is linear in t_f)."""
+    from synth.generators import zipf_coo
+    dims, nnz, core = (60, 70, 900), 30_000, (6, 5, 4)
+    idx, vals = zipf_coo(dims, nnz, np.random.default_rng(11), batch=1 << 14)
+    frng = np.random.default_rng(12)
+    U0 = [random_orthonormal(I, J, frng) for I, J in zip(dims, core)]
+    if lmax:
+        monkeypatch.setenv("TUCKER_TTMC_LMAX", lmax)
+        monkeypatch.setenv("TUCKER_TTMC_CMAX", cmax)
+    T = O.SparseTensor(dims, idx, vals)
+    with capi.Tucker(dims, core, idx, vals, U0) as t:
+        st = t.csf_stats()
+        if lmax:
+            assert all(vf > f and u > 0 for f, _, vf, u in st), st
+        for n in range(len(dims)):
+            Y = t.debug_ttmc(n)
+            Yo = O.ttm_chain_unfold(T, U0, n)
+            assert O.rel_frobenius(Y, Yo) < 1e-4
+        fits = t.hooi_sweep(2)
+    # the whole sweep on the split path agrees with the oracle
+    ref = O.run_hooi(T, U0, core, 2)
+    assert np.max(np.abs(np.asarray(fits) - np.asarray(ref["fits"]))) < 1e-5
+
+
 @pytest.mark.parametrize("dims,nnz,core", SHAPES)
 def test_gram_parity(capi, dims, nnz, core):
     idx, vals, U0 = case(dims, nnz, core)
