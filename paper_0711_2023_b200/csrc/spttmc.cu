@@ -88,19 +88,173 @@ __device__ __forceinline__ void leaf_stage(int fc, int nf, const int32_t* __rest
   }
 }
 
-// Kronecker stage over one chunk: acc[r][c] += M[fl][ty + 16 r] * T[fl][tx + 16 c]
+// Leaf stage with the chunk's fiber metadata (fptr: nf + 1 nonzero offsets,
+// fmid: mid indices) already in shared memory and, when the chunk's
+// nonzeros fit (sl != nullptr), their leaf ids / values staged too: per
+// fiber the only global hop left is the U row gathers.  Lane l gathers the
+// VW-float vector at columns VW*l (+ 32 VW per pass) of each U_leaf row (one
+// 64/128-bit load per nonzero and pass), UN nonzeros in flight at a time.
+constexpr int kNS = 512;  // staged nonzeros per chunk
+template <int VW>
+struct FVec;
+template <>
+struct FVec<1> {
+  using T = float;
+  static __device__ __forceinline__ void fma(float x, T g, float* t) { t[0] = fmaf(x, g, t[0]); }
+};
+template <>
+struct FVec<2> {
+  using T = float2;
+  static __device__ __forceinline__ void fma(float x, T g, float* t) {
+    t[0] = fmaf(x, g.x, t[0]);
+    t[1] = fmaf(x, g.y, t[1]);
+  }
+};
+template <>
+struct FVec<4> {
+  using T = float4;
+  static __device__ __forceinline__ void fma(float x, T g, float* t) {
+    t[0] = fmaf(x, g.x, t[0]);
+    t[1] = fmaf(x, g.y, t[1]);
+    t[2] = fmaf(x, g.z, t[2]);
+    t[3] = fmaf(x, g.w, t[3]);
+  }
+};
+
+template <int VW, int QV, int UN>
+__device__ __forceinline__ void gather_rows(const int* l, const float* x, int n,
+                                            const float* __restrict__ Uleaf, int Jl, int lane,
+                                            float (&t)[QV][VW]) {
+  using V = typename FVec<VW>::T;
+  V g[UN][QV];
+#pragma unroll
+  for (int u = 0; u < UN; ++u) {
+    const V* r = reinterpret_cast<const V*>(Uleaf + (int64_t)l[u] * Jl);
+#pragma unroll
+    for (int q = 0; q < QV; ++q) {
+      const int v = lane + 32 * q;
+      if (u < n && v * VW < Jl) g[u][q] = __ldg(r + v);
+      else g[u][q] = V{};
+    }
+  }
+#pragma unroll
+  for (int u = 0; u < UN; ++u)
+#pragma unroll
+    for (int q = 0; q < QV; ++q) FVec<VW>::fma(x[u], g[u][q], t[q]);
+}
+
+template <int JLP, int JMP, int VW>
+__device__ __forceinline__ void leaf_stage_s(int nf, const int* fptr, const int* fmid, const int* sl,
+                                             const float* sv, const int32_t* __restrict__ leaf_id,
+                                             const float* __restrict__ val,
+                                             const float* __restrict__ Umid, int Jm,
+                                             const float* __restrict__ Uleaf, int Jl, float* T,
+                                             float* M) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nwarps = blockDim.x >> 5;
+  constexpr int QV = (JLP + 32 * VW - 1) / (32 * VW);
+  constexpr int QM = (JMP + 31) / 32;
+  constexpr int UN = 4;
+  const int E0 = fptr[0];
+  for (int fl = warp; fl < nf; fl += nwarps) {
+    const int e0 = fptr[fl], e1 = fptr[fl + 1];
+    const float* mr = Umid + (int64_t)fmid[fl] * Jm;
+    float mv[QM];
+#pragma unroll
+    for (int q = 0; q < QM; ++q) {
+      const int j = lane + 32 * q;
+      mv[q] = (j < Jm) ? __ldg(mr + j) : 0.f;
+    }
+    float t[QV][VW];
+#pragma unroll
+    for (int q = 0; q < QV; ++q)
+#pragma unroll
+      for (int k = 0; k < VW; ++k) t[q][k] = 0.f;
+    int l[UN];
+    float x[UN];
+    if (sl) {
+      for (int e = e0; e < e1; e += UN) {
+        const int n = min(UN, e1 - e);
+#pragma unroll
+        for (int u = 0; u < UN; ++u) {
+          l[u] = u < n ? sl[e + u - E0] : 0;
+          x[u] = u < n ? sv[e + u - E0] : 0.f;
+        }
+        gather_rows<VW, QV, UN>(l, x, n, Uleaf, Jl, lane, t);
+      }
+    } else {
+      for (int e = e0; e < e1; e += UN) {
+        const int n = min(UN, e1 - e);
+#pragma unroll
+        for (int u = 0; u < UN; ++u) {
+          l[u] = u < n ? __ldg(leaf_id + e + u) : 0;
+          x[u] = u < n ? __ldg(val + e + u) : 0.f;
+        }
+        gather_rows<VW, QV, UN>(l, x, n, Uleaf, Jl, lane, t);
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < QV; ++q)
+#pragma unroll
+      for (int k = 0; k < VW; ++k) {
+        const int j = (lane + 32 * q) * VW + k;
+        if (j < JLP) T[fl * JLP + j] = t[q][k];
+      }
+#pragma unroll
+    for (int q = 0; q < QM; ++q) {
+      const int j = lane + 32 * q;
+      if (j < JMP) M[fl * JMP + j] = mv[q];
+    }
+  }
+}
+
+// Kronecker stage over one chunk: acc[r][c] += M[fl][a(r)] * T[fl][b(c)].
+// Thread (tx, ty) owns rows a(r) = ty*RA + r (contiguous: RA/4 broadcast
+// 128-bit loads) and columns b(c) = (c/V)*16V + tx*V + c%V with V = min(RB, 4)
+// (each vector load of a half-warp is one contiguous 16V-float run: no bank
+// conflicts).  Per fiber a warp issues RA/4 + RB/V loads for RA*RB FFMAs.
+template <int RB>
+struct KronV {
+  static constexpr int V = RB < 4 ? RB : 4;
+};
+template <int RA, int RB>
+__device__ __forceinline__ int kron_col(int tx, int c) {
+  constexpr int V = KronV<RB>::V;
+  return (c / V) * 16 * V + tx * V + (c % V);
+}
 template <int RA, int RB>
 __device__ __forceinline__ void kron_stage(int nf, const float* T, const float* M,
                                            float (&acc)[RA][RB]) {
   const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
   constexpr int JLP = 16 * RB, JMP = 16 * RA;
-#pragma unroll 4
+  constexpr int V = KronV<RB>::V;
+#pragma unroll 2
   for (int fl = 0; fl < nf; ++fl) {
     float a[RA], b[RB];
+    const float* mr = M + fl * JMP + ty * RA;
+    if constexpr (RA % 4 == 0) {
 #pragma unroll
-    for (int r = 0; r < RA; ++r) a[r] = M[fl * JMP + ty + 16 * r];
+      for (int r = 0; r < RA; r += 4) {
+        const float4 v = *reinterpret_cast<const float4*>(mr + r);
+        a[r] = v.x; a[r + 1] = v.y; a[r + 2] = v.z; a[r + 3] = v.w;
+      }
+    } else {
 #pragma unroll
-    for (int c = 0; c < RB; ++c) b[c] = T[fl * JLP + tx + 16 * c];
+      for (int r = 0; r < RA; ++r) a[r] = mr[r];
+    }
+    const float* tr = T + fl * JLP + tx * V;
+#pragma unroll
+    for (int q = 0; q < RB / V; ++q) {
+      if constexpr (V == 4) {
+        const float4 v = *reinterpret_cast<const float4*>(tr + q * 16 * V);
+        b[4 * q] = v.x; b[4 * q + 1] = v.y; b[4 * q + 2] = v.z; b[4 * q + 3] = v.w;
+      } else if constexpr (V == 2) {
+        const float2 v = *reinterpret_cast<const float2*>(tr + q * 16 * V);
+        b[2 * q] = v.x; b[2 * q + 1] = v.y;
+      } else {
+        b[q] = tr[q * 16];
+      }
+    }
 #pragma unroll
     for (int r = 0; r < RA; ++r)
 #pragma unroll
@@ -121,11 +275,11 @@ struct Ttmc3Args {
   int64_t sa, sb;  // Kolda strides of (mid index a, leaf index b) in the output column
 };
 
-template <int RA, int RB>
+template <int RA, int RB, int VW>
 __global__ void __launch_bounds__(256) k_spttmc3(Ttmc3Args p) {
   constexpr int JLP = 16 * RB, JMP = 16 * RA;
-  __shared__ float T[kFC * JLP];
-  __shared__ float M[kFC * JMP];
+  __shared__ __align__(16) float T[kFC * JLP];
+  __shared__ __align__(16) float M[kFC * JMP];
   int i, f0, f1, slot = -1;
   if (p.unit) {
     const int4 u = reinterpret_cast<const int4*>(p.unit)[blockIdx.x];
@@ -143,10 +297,37 @@ __global__ void __launch_bounds__(256) k_spttmc3(Ttmc3Args p) {
   for (int r = 0; r < RA; ++r)
 #pragma unroll
     for (int c = 0; c < RB; ++c) acc[r][c] = 0.f;
+  __shared__ int fptr[kFC + 1], fmid[kFC];
+  __shared__ int sl[kNS];
+  __shared__ float sv[kNS];
+  // chunk metadata prefetched into registers one chunk ahead
+  int nx_ptr = 0, nx_mid = 0;
+  if (f0 < f1 && threadIdx.x <= min(kFC, f1 - f0)) {
+    nx_ptr = __ldg(p.fib_ptr + f0 + threadIdx.x);
+    if (threadIdx.x < min(kFC, f1 - f0)) nx_mid = __ldg(p.fib_mid + f0 + threadIdx.x);
+  }
   for (int fc = f0; fc < f1; fc += kFC) {
     const int nf = min(kFC, f1 - fc);
-    leaf_stage<JLP, JMP>(fc, nf, p.fib_ptr, p.fib_mid, p.leaf_id, p.val, p.Umid, p.Jm, p.Uleaf,
-                         p.Jl, T, M);
+    if (threadIdx.x <= nf) fptr[threadIdx.x] = nx_ptr;
+    if (threadIdx.x < nf) fmid[threadIdx.x] = nx_mid;
+    __syncthreads();
+    const int E0 = fptr[0], E1 = fptr[nf];
+    const bool staged = E1 - E0 <= kNS;
+    if (staged)
+      for (int e = E0 + (int)threadIdx.x; e < E1; e += blockDim.x) {
+        sl[e - E0] = __ldg(p.leaf_id + e);
+        sv[e - E0] = __ldg(p.val + e);
+      }
+    // next chunk's metadata: in flight during this chunk's stages
+    const int fn = fc + kFC;
+    if (fn < f1) {
+      const int nfn = min(kFC, f1 - fn);
+      if (threadIdx.x <= nfn) nx_ptr = __ldg(p.fib_ptr + fn + threadIdx.x);
+      if (threadIdx.x < nfn) nx_mid = __ldg(p.fib_mid + fn + threadIdx.x);
+    }
+    __syncthreads();
+    leaf_stage_s<JLP, JMP, VW>(nf, fptr, fmid, staged ? sl : nullptr, sv, p.leaf_id, p.val, p.Umid, p.Jm,
+                           p.Uleaf, p.Jl, T, M);
     __syncthreads();
     kron_stage<RA, RB>(nf, T, M, acc);
     __syncthreads();
@@ -156,7 +337,7 @@ __global__ void __launch_bounds__(256) k_spttmc3(Ttmc3Args p) {
   for (int r = 0; r < RA; ++r)
 #pragma unroll
     for (int c = 0; c < RB; ++c) {
-      const int a = ty + 16 * r, b = tx + 16 * c;
+      const int a = ty * RA + r, b = kron_col<RA, RB>(tx, c);
       if (slot >= 0) {
         if (a < p.Jm && b < p.Jl) p.part[(int64_t)slot * p.Jm * p.Jl + a * p.Jl + b] = acc[r][c];
       } else if (a < p.Jm && b < p.Jl) {
@@ -199,8 +380,8 @@ struct Ttmc4Args {
 template <int RA, int RB, int RQ>
 __global__ void __launch_bounds__(256) k_spttmc4(Ttmc4Args p) {
   constexpr int JLP = 16 * RB, JMP = 16 * RA;
-  __shared__ float T[kFC * JLP];
-  __shared__ float M[kFC * JMP];
+  __shared__ __align__(16) float T[kFC * JLP];
+  __shared__ __align__(16) float M[kFC * JMP];
   __shared__ float Zs[JMP * JLP];
   __shared__ float u0[128];
   const int i = blockIdx.x;
@@ -230,7 +411,7 @@ __global__ void __launch_bounds__(256) k_spttmc4(Ttmc4Args p) {
     for (int r = 0; r < RA; ++r)
 #pragma unroll
       for (int c = 0; c < RB; ++c) {
-        const int a = ty + 16 * r, b = tx + 16 * c;
+        const int a = ty * RA + r, b = kron_col<RA, RB>(tx, c);
         if (a < p.J1 && b < p.Jl) Zs[a * p.Jl + b] = acc[r][c];
       }
     const float* ur = p.U0 + (int64_t)p.node_mid0[nd] * p.J0;
@@ -340,14 +521,19 @@ void spttmc_hooi(const Csf& c, const float* const* U, const int64_t* J, Split ou
     const int RA = rtile(a.Jm), RB = rtile(a.Jl);
     const dim3 g((unsigned)(c.nunits > 0 ? c.nunits : c.I_root));
     bool launched = false;
-#define TK_S3(ra, rb)                                            \
-  if (!launched && RA <= ra && RB <= rb) {                        \
-    TK_LAUNCH((k_spttmc3<ra, rb>), g, 256, 0, st, a);             \
-    launched = true;                                              \
+    // U_leaf row vector width: rows of Jl floats are 16-byte aligned iff 4 | Jl
+    const int VW = a.Jl % 4 == 0 ? 4 : (a.Jl % 2 == 0 ? 2 : 1);
+#define TK_S3V(ra, rb, vw) \
+  if (VW == vw) TK_LAUNCH((k_spttmc3<ra, rb, vw>), g, 256, 0, st, a);
+#define TK_S3(ra, rb)                                                         \
+  if (!launched && RA <= ra && RB <= rb) {                                     \
+    TK_S3V(ra, rb, 1) TK_S3V(ra, rb, 2) TK_S3V(ra, rb, 4)                      \
+    launched = true;                                                           \
   }
     TK_S3(1, 1) TK_S3(2, 1) TK_S3(1, 2) TK_S3(2, 2) TK_S3(4, 1) TK_S3(1, 4) TK_S3(4, 2)
     TK_S3(2, 4) TK_S3(4, 4) TK_S3(8, 2) TK_S3(2, 8) TK_S3(8, 4) TK_S3(4, 8) TK_S3(8, 8)
 #undef TK_S3
+#undef TK_S3V
     if (!launched) fail(TUCKER_E_ARG, "spttmc: unsupported core size");
     if (c.nred > 0) {
       const dim3 gr((unsigned)ceil_div((int64_t)a.Jm * a.Jl, 256), (unsigned)c.nred);
