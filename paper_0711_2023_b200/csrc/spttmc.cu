@@ -15,10 +15,12 @@
 // block for the slice s fixing the modes not in {n, m} is X_s U_m.
 #include <algorithm>
 #include <cstdlib>
+#include <cstring>
 #include <array>
 #include <vector>
 
 #include "internal.cuh"
+#include "tc_ptx.cuh"
 
 namespace tk {
 
@@ -348,6 +350,237 @@ __global__ void __launch_bounds__(256) k_spttmc3(Ttmc3Args p) {
     }
 }
 
+// ---------------------------------------------------------------------------
+// Tensor-core Kronecker stage (order 3, J_mid, J_leaf <= 128).  Per chunk of
+// KC = 32 fibers the Kronecker update Y_i += M_c^T T_c (M_c: KC x J_mid rows
+// of U_mid, T_c: KC x J_leaf fiber sums t_f, Eq. 1) is a K = 32 contraction,
+// run as 3xTF32 tcgen05 MMAs (hi.hi + hi.lo + lo.hi, fp32 accumulation in
+// TMEM, D = 128 x N with row a = mid index, column b = leaf index).  Both
+// operands are K-major with the 128-byte swizzle (the layout the Gram kernel
+// uses): one operand row = one mid/leaf index, its 32 fibers = one 128-byte
+// swizzle row, so the leaf stage stores fiber k's values into column k.  One
+// operand buffer (so 3-4 CTAs fit per SM and the latency-bound gathers have
+// warps to hide behind): the chunk's metadata staging overlaps the previous
+// chunk's MMAs, and the operand stores wait for their commit.
+// (MN-major tf32 operands would avoid the transposed stores, but produced
+// zeros in tools/umma_mn_test.cu; K-major is the verified layout.)
+// ---------------------------------------------------------------------------
+constexpr int KC = 32;                // fibers (K) per chunk = one 128-byte swizzle row
+constexpr int TC_A_BYTES = 128 * 128; // A: 128 rows (M) x 128 B
+
+template <int NA>  // B: 32 NA rows (N = 32 NA)
+struct TcTile {
+  static constexpr int B_BYTES = 32 * NA * 128;
+  static constexpr int BUF = 2 * TC_A_BYTES + 2 * B_BYTES;  // A_hi, A_lo, B_hi, B_lo
+  static constexpr int SMEM = BUF + KC * 32 * NA * 4 + 1024;  // operands + plain t rows + alignment slack
+  static constexpr uint32_t IDESC = (1u << 4) | (2u << 7) | (2u << 10) |  // F32 <- TF32 x TF32, K-major
+                                    ((uint32_t)(32 * NA) >> 3 << 17) | ((uint32_t)(128 >> 4) << 24);
+  static constexpr int TMEM_COLS = NA <= 1 ? 32 : (NA <= 2 ? 64 : 128);
+};
+
+// byte offset of element (row, k) in a K-major SW128 tile (K = 32 per row)
+__device__ __forceinline__ uint32_t k_sw128(int row, int k) {
+  return (uint32_t)((row >> 3) * 1024 + (row & 7) * 128 + ((((k >> 2) ^ (row & 7)) << 4) | ((k & 3) << 2)));
+}
+
+__device__ __forceinline__ void st_split1(uint8_t* hi, uint8_t* lo, uint32_t off, float v) {
+  const float h = tf32_rna(v);
+  *reinterpret_cast<float*>(hi + off) = h;
+  *reinterpret_cast<float*>(lo + off) = tf32_rna(v - h);
+}
+
+template <int NA, int VW>
+__global__ void __launch_bounds__(256) k_spttmc3_tc(Ttmc3Args p) {
+  using Tile = TcTile<NA>;
+  constexpr int QV = (32 * NA + 32 * VW - 1) / (32 * VW);
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  float* Tp = reinterpret_cast<float*>(smem + Tile::BUF);  // KC x 32 NA plain t rows
+  __shared__ __align__(8) uint64_t mma_done;
+  __shared__ uint32_t tmem_slot;
+  __shared__ int fptr[KC + 1], fmid[KC];
+  __shared__ int sl[kNS];
+  __shared__ float sv[kNS];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  int i, f0, f1, slot = -1;
+  if (p.unit) {
+    const int4 u = reinterpret_cast<const int4*>(p.unit)[blockIdx.x];
+    i = u.x;
+    f0 = u.y;
+    f1 = u.z;
+    slot = u.w;
+  } else {
+    i = blockIdx.x;
+    f0 = p.slice_ptr[i];
+    f1 = p.slice_ptr[i + 1];
+  }
+  if (f0 >= f1) return;  // empty slice: Y was zeroed before the launch
+
+  // zero both buffers once: padding rows/columns (a >= J_mid, b >= J_leaf) are never written again
+  for (int o = threadIdx.x * 16; o < Tile::BUF; o += 256 * 16)
+    *reinterpret_cast<float4*>(smem + o) = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (threadIdx.x == 0) {
+    tc::mbar_init(&mma_done, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     tc::smem_u32(&tmem_slot)),
+                 "r"(Tile::TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  int nx_ptr = 0, nx_mid = 0;
+  if (threadIdx.x <= min(KC, f1 - f0)) {
+    nx_ptr = __ldg(p.fib_ptr + f0 + threadIdx.x);
+    if (threadIdx.x < min(KC, f1 - f0)) nx_mid = __ldg(p.fib_mid + f0 + threadIdx.x);
+  }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
+  const uint32_t tmem = tmem_slot;
+  const uint32_t sbase = tc::smem_u32(smem);
+
+  int c = 0;
+  for (int fc = f0; fc < f1; fc += KC, ++c) {
+    const int nf = min(KC, f1 - fc);
+    uint8_t* buf = smem;
+    uint8_t *Ahi = buf, *Alo = buf + TC_A_BYTES, *Bhi = buf + 2 * TC_A_BYTES,
+            *Blo = buf + 2 * TC_A_BYTES + Tile::B_BYTES;
+    if (threadIdx.x <= nf) fptr[threadIdx.x] = nx_ptr;
+    if (threadIdx.x < nf) fmid[threadIdx.x] = nx_mid;
+    __syncthreads();
+    const int E0 = fptr[0], E1 = fptr[nf];
+    const bool staged = E1 - E0 <= kNS;
+    if (staged)
+      for (int e = E0 + (int)threadIdx.x; e < E1; e += 256) {
+        sl[e - E0] = __ldg(p.leaf_id + e);
+        sv[e - E0] = __ldg(p.val + e);
+      }
+    const int fn = fc + KC;
+    if (fn < f1) {
+      const int nfn = min(KC, f1 - fn);
+      if (threadIdx.x <= nfn) nx_ptr = __ldg(p.fib_ptr + fn + threadIdx.x);
+      if (threadIdx.x < nfn) nx_mid = __ldg(p.fib_mid + fn + threadIdx.x);
+    }
+    __syncthreads();
+    // leaf stage: warp per fiber -> row fl of the plain t buffer Tp (16-byte
+    // chunks XOR-swizzled by fl & 7: conflict-free row stores and column reads)
+    for (int fl = warp; fl < KC; fl += 8) {
+      float t[QV][VW];
+#pragma unroll
+      for (int q = 0; q < QV; ++q)
+#pragma unroll
+        for (int k = 0; k < VW; ++k) t[q][k] = 0.f;
+      if (fl < nf) {
+        const int e0 = fptr[fl], e1 = fptr[fl + 1];
+        int l[4];
+        float x[4];
+        if (staged) {
+          for (int e = e0; e < e1; e += 4) {
+            const int n = min(4, e1 - e);
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              l[u] = u < n ? sl[e + u - E0] : 0;
+              x[u] = u < n ? sv[e + u - E0] : 0.f;
+            }
+            gather_rows<VW, QV, 4>(l, x, n, p.Uleaf, p.Jl, lane, t);
+          }
+        } else {
+          for (int e = e0; e < e1; e += 4) {
+            const int n = min(4, e1 - e);
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              l[u] = u < n ? __ldg(p.leaf_id + e + u) : 0;
+              x[u] = u < n ? __ldg(p.val + e + u) : 0.f;
+            }
+            gather_rows<VW, QV, 4>(l, x, n, p.Uleaf, p.Jl, lane, t);
+          }
+        }
+      }
+      float* row = Tp + fl * (32 * NA);
+#pragma unroll
+      for (int q = 0; q < QV; ++q) {
+        const int col = (lane + 32 * q) * VW;  // VW consecutive columns inside one 16-byte chunk
+        if (col < 32 * NA) {
+          const int pc = ((col >> 2) ^ (fl & 7)) * 4 + (col & 3);
+          if constexpr (VW == 4) *reinterpret_cast<float4*>(row + pc) = make_float4(t[q][0], t[q][1], t[q][2], t[q][3]);
+          else if constexpr (VW == 2) *reinterpret_cast<float2*>(row + pc) = make_float2(t[q][0], t[q][1]);
+          else row[pc] = t[q][0];
+        }
+      }
+    }
+    // the operand buffer was last read by the MMAs of chunk c - 1
+    if (c >= 1) tc::mbar_wait(&mma_done, (uint32_t)((c - 1) & 1));
+    __syncthreads();
+    // transpose into the K-major operands: lanes run over the 32 fibers, so a
+    // warp's store fills one 128-byte swizzle row (conflict-free)
+    {
+      const int k = lane;
+      // B: rows n (leaf index), 4 per item, read as one 16-byte chunk of Tp row k
+      for (int q = warp; q < 8 * NA; q += 8) {
+        const float4 v = *reinterpret_cast<const float4*>(Tp + k * (32 * NA) + ((q ^ (k & 7)) << 2));
+        st_split1(Bhi, Blo, k_sw128(4 * q, k), v.x);
+        st_split1(Bhi, Blo, k_sw128(4 * q + 1, k), v.y);
+        st_split1(Bhi, Blo, k_sw128(4 * q + 2, k), v.z);
+        st_split1(Bhi, Blo, k_sw128(4 * q + 3, k), v.w);
+      }
+      // A: rows a (mid index) straight from the U_mid rows of the chunk's fibers
+      if (k < nf) {
+        const float* mr = p.Umid + (int64_t)fmid[k] * p.Jm;
+        for (int a = warp; a < p.Jm; a += 8) st_split1(Ahi, Alo, k_sw128(a, k), __ldg(mr + a));
+      }
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      tc::tc_fence_after();
+      const uint32_t ah = sbase, al = ah + TC_A_BYTES;
+      const uint32_t bh = ah + 2 * TC_A_BYTES, bl = bh + Tile::B_BYTES;
+#pragma unroll
+      for (int g = 0; g < KC / 8; ++g) {
+        const uint32_t o = (uint32_t)(g * 32);  // 8 tf32 = 32 bytes along K inside the swizzle row
+        tc::umma_tf32(tmem, tc::sw128_desc(ah + o), tc::sw128_desc(bh + o), Tile::IDESC, (c > 0 || g > 0) ? 1u : 0u);
+        tc::umma_tf32(tmem, tc::sw128_desc(ah + o), tc::sw128_desc(bl + o), Tile::IDESC, 1u);
+        tc::umma_tf32(tmem, tc::sw128_desc(al + o), tc::sw128_desc(bh + o), Tile::IDESC, 1u);
+      }
+      tc::umma_commit(&mma_done);
+    }
+  }
+  // all MMAs done once the last chunk's commit arrives
+  tc::mbar_wait(&mma_done, (uint32_t)((c - 1) & 1));
+  tc::tc_fence_after();
+  if (warp < 4) {
+    const int a = 32 * warp + lane;  // D row = mid index
+#pragma unroll
+    for (int nb = 0; nb < NA; ++nb) {
+      float v[32];
+      tc::tmem_ld32(tmem + ((uint32_t)(32 * warp) << 16) + (uint32_t)(32 * nb), v);
+      tc::tmem_wait_ld();
+      if (a < p.Jm) {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          const int bcol = 32 * nb + j;
+          if (bcol < p.Jl) {
+            if (slot >= 0) {
+              p.part[(int64_t)slot * p.Jm * p.Jl + a * p.Jl + bcol] = v[j];
+            } else {
+              const int64_t col = a * p.sa + bcol * p.sb;
+              const int64_t off = p.transposed ? col * p.ldY + i : (int64_t)i * p.ldY + col;
+              split_store(p.Yhi, p.Ylo, off, v[j]);
+            }
+          }
+        }
+      }
+    }
+  }
+  tc::tc_fence_before();
+  __syncthreads();
+  if (warp == 0)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(Tile::TMEM_COLS));
+}
+
 // Y row of a split slice = sum of its units' partial tiles, in slot order
 __global__ void __launch_bounds__(256) k_spttmc3_reduce(const int32_t* __restrict__ red,
                                                         const float* __restrict__ part, int Jm, int Jl,
@@ -523,6 +756,31 @@ void spttmc_hooi(const Csf& c, const float* const* U, const int64_t* J, Split ou
     bool launched = false;
     // U_leaf row vector width: rows of Jl floats are 16-byte aligned iff 4 | Jl
     const int VW = a.Jl % 4 == 0 ? 4 : (a.Jl % 2 == 0 ? 2 : 1);
+    // tcgen05 Kronecker stage where the Kronecker work dominates (measured on
+    // B200: J_mid J_leaf = 10^4 -> 35 vs 41 ms at config 5 mode 3; at 5000 and
+    // 2500 the SIMT kernel's higher occupancy hides the gathers better: 35 vs
+    // 42 ms, 0.28 vs 0.31 ms).  TUCKER_TTMC=tc|simt forces one (tests).
+    const char* fe = std::getenv("TUCKER_TTMC");
+    const int force = !fe ? 0 : (std::strcmp(fe, "tc") == 0 ? 1 : (std::strcmp(fe, "simt") == 0 ? -1 : 0));
+    const bool use_tc = a.Jm <= 128 && a.Jl <= 128 &&
+                        (force == 1 || (force == 0 && (int64_t)a.Jm * a.Jl >= 8192));
+    if (use_tc) {
+      const int NA = (a.Jl + 31) / 32;
+#define TK_TC(na, vw)                                                                          \
+  if (!launched && NA == na && VW == vw) {                                                     \
+    static bool attr = false;                                                                  \
+    if (!attr) {                                                                               \
+      TK_CUDA(cudaFuncSetAttribute(k_spttmc3_tc<na, vw>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                                   TcTile<na>::SMEM));                                         \
+      attr = true;                                                                             \
+    }                                                                                          \
+    TK_LAUNCH((k_spttmc3_tc<na, vw>), g, 256, TcTile<na>::SMEM, st, a);                        \
+    launched = true;                                                                           \
+  }
+      TK_TC(1, 1) TK_TC(1, 2) TK_TC(1, 4) TK_TC(2, 1) TK_TC(2, 2) TK_TC(2, 4)
+      TK_TC(3, 1) TK_TC(3, 2) TK_TC(3, 4) TK_TC(4, 1) TK_TC(4, 2) TK_TC(4, 4)
+#undef TK_TC
+    }
 #define TK_S3V(ra, rb, vw) \
   if (VW == vw) TK_LAUNCH((k_spttmc3<ra, rb, vw>), g, 256, 0, st, a);
 #define TK_S3(ra, rb)                                                         \

@@ -51,8 +51,15 @@ SHAPES = [
 ]
 
 
+@pytest.mark.parametrize("kernel", ["auto", "tc", "simt"])
 @pytest.mark.parametrize("dims,nnz,core", SHAPES)
-def test_ttmc_parity(capi, dims, nnz, core):
+def test_ttmc_parity(capi, monkeypatch, dims, nnz, core, kernel):
+    """Both order-3 Kronecker kernels (tcgen05 3xTF32 and SIMT fp32) and the
+    default dispatch agree with the oracle's Y_(n)."""
+    if kernel != "auto":
+        if len(dims) != 3:
+            pytest.skip("order 4 has one kernel")
+        monkeypatch.setenv("TUCKER_TTMC", kernel)
     idx, vals, U0 = case(dims, nnz, core)
     T = O.SparseTensor(dims, idx, vals)
     with capi.Tucker(dims, core, idx, vals, U0) as t:
@@ -62,8 +69,9 @@ def test_ttmc_parity(capi, dims, nnz, core):
             assert O.rel_frobenius(Y, Yo) < 1e-4
 
 
+@pytest.mark.parametrize("kernel", ["tc", "simt"])
 @pytest.mark.parametrize("lmax,cmax", [(None, None), ("7", "3000"), ("64", "20000")])
-def test_ttmc_parity_skewed(capi, monkeypatch, lmax, cmax):
+def test_ttmc_parity_skewed(capi, monkeypatch, lmax, cmax, kernel):
     """Zipf-skewed tensor (config 5's index law at oracle size): long fibers and
     heavy head slices.  With the env hooks the SpTTMc work plan cuts fibers
     into virtual fibers of <= lmax nonzeros and slices into units of <= cmax
@@ -73,6 +81,7 @@ def test_ttmc_parity_skewed(capi, monkeypatch, lmax, cmax):
     idx, vals = zipf_coo(dims, nnz, np.random.default_rng(11), batch=1 << 14)
     frng = np.random.default_rng(12)
     U0 = [random_orthonormal(I, J, frng) for I, J in zip(dims, core)]
+    monkeypatch.setenv("TUCKER_TTMC", kernel)
     if lmax:
         monkeypatch.setenv("TUCKER_TTMC_LMAX", lmax)
         monkeypatch.setenv("TUCKER_TTMC_CMAX", cmax)
