@@ -16,6 +16,7 @@ LIB_PATH = os.path.join(_HERE, "libtucker.so")
 
 TUCKER_INPUT_ON_DEVICE = 0x1
 TUCKER_OUTPUT_ON_DEVICE = 0x2
+E_OOM = 8
 E_CONVERGE = 10
 
 # every symbol declared in include/tucker.h

@@ -184,6 +184,19 @@ Split build_mp_w(tucker_handle* h, int n) {
   const int64_t rows = h->dims[n];
   const int64_t rows_pad = round_up(rows, 128), ld = round_up(K, 32);
   const size_t need = (size_t)(rows_pad * ld);
+  if (need > h->Whi.n) {
+    size_t free_b = 0, total_b = 0;
+    TK_CUDA(cudaMemGetInfo(&free_b, &total_b));
+    const double gb = 2.0 * (double)need * sizeof(float) / 1e9;
+    if (2.0 * (double)need * sizeof(float) > (double)free_b + 4.0 * (double)h->Whi.n) {
+      char msg[200];
+      std::snprintf(msg, sizeof msg,
+                    "mp_sweep: W_%d needs %.1f GB (split fp32 %lld x %lld); the fused per-slice multislice "
+                    "Gram for tensors this size is not implemented",
+                    n + 1, gb, (long long)rows, (long long)K);
+      fail(TUCKER_E_OOM, msg);
+    }
+  }
   h->Whi.ensure(need);
   h->Wlo.ensure(need);
   TK_CUDA(cudaMemsetAsync(h->Whi.p, 0, need * sizeof(float), h->st));

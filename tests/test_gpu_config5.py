@@ -78,3 +78,14 @@ def test_config5_hooi_sweep_properties(c5):
     S = t.debug_gram(0, 2)
     V, w = O.leading_eigenvectors(S, core[2])
     assert O.projector_distance(U[2].astype(np.float64), V) < 1e-4
+
+
+def test_config5_mp_reports_unsupported(c5):
+    """MP at config 5 needs the fused multislice Gram (W_1 would be 0.6 TB):
+    the library must refuse with E_OOM and a message, not crash."""
+    from paper_0711_2023_b200 import capi
+    c, t = c5
+    with pytest.raises(capi.TuckerError) as e:
+        t.mp_sweep(1)
+    assert e.value.code == capi.E_OOM
+    assert "multislice" in str(e.value)
