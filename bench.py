@@ -6,8 +6,10 @@ One step = the whole hot path of SURVEY.md §8(a) over the config's tensor:
 5 HOOI sweeps + core/fit and 5 MP sweeps + core/fit (config 2 of BASELINE.json:
 1000^3, 1e6 uniform nonzeros, core 50^3), each from the same seeded U0, with
 the sparse tensor (CSF) already resident in HBM.  value = nonzero-mode updates
-per second = nnz * N_modes * (HOOI sweeps + MP sweeps) / step time, summed
-over ranks (ranks run replicas in this build).
+per second = nnz * N_modes * (HOOI sweeps + MP sweeps) / step time.  With N>1
+(torchrun) the ranks shard the one workload (HOOI by mode-n slice ranges, MP by
+slice-index ranges, NCCL allreduces inside the library):
+strong scaling, time = max over ranks.
 
 `e2e` is the same metric through the C-ABI from HOST buffers: tucker_init
 (H2D + CSF build) + sweeps + core_and_fit with the core and factors copied back.
@@ -38,6 +40,8 @@ def parse():
     ap.add_argument("--config", type=int, default=2)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--sharded", action="store_true",
+                    help="run the sharded (NCCL) sweep even at N=1 (a 1-rank communicator; N>1 always shards)")
     return ap.parse_args()
 
 
@@ -197,6 +201,19 @@ def run_ours(args):
     c = workload(args.config)
     dims, core, N, S = c["dims"], c["core"], len(c["dims"]), c["sweeps"]
     stream = torch.cuda.current_stream(dev)
+    sharded = world > 1 or args.sharded
+
+    def nccl_id():
+        """A fresh ncclUniqueId from rank 0, broadcast over torch.distributed
+        (each sharded handle owns its own communicator)."""
+        if not sharded:
+            return {}
+        buf = torch.zeros(128, dtype=torch.uint8, device=dev)
+        if rank == 0:
+            buf.copy_(torch.frombuffer(bytearray(capi.nccl_unique_id()), dtype=torch.uint8))
+        if world > 1:
+            torch.distributed.broadcast(buf, src=0)
+        return {"rank": rank, "world": world, "nccl_id": bytes(buf.cpu().numpy().tobytes())}
     idx_d = [torch.from_numpy(a).to(dev) for a in c["idx"]]
     vals_d = torch.from_numpy(c["vals"]).to(dev)
     U0_d = [torch.from_numpy(u).to(dev) for u in c["U0"]]
@@ -205,7 +222,7 @@ def run_ours(args):
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     h = capi.tucker_init(dims, core, idx_d, vals_d, U0_d, device=local, stream=stream.cuda_stream,
-                         on_device=True, output_on_device=True)
+                         on_device=True, output_on_device=True, **nccl_id())
     init_s = time.perf_counter() - t0
     flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)  # 512 MB > L2
 
@@ -252,7 +269,8 @@ def run_ours(args):
         total_ms = float(t.item())
     ms_step = total_ms / args.steps
     units = c["nnz"] * N * 2 * S
-    value = units * world / (ms_step / 1e3) / 1e9
+    # sharded: the N ranks process the one workload together (strong scaling)
+    value = units * (1 if sharded else world) / (ms_step / 1e3) / 1e9
 
     # ---- e2e through the C-ABI from pinned host buffers ----
     idx_h = [torch.from_numpy(a).pin_memory() for a in c["idx"]]
@@ -265,12 +283,15 @@ def run_ours(args):
     e2e_steps = max(1, min(2, args.steps))
     e2e_ms = []
     for _ in range(e2e_steps):
+        kw2 = nccl_id()
+        if world > 1:
+            torch.distributed.barrier()
         torch.cuda.synchronize()
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record(stream)
         h2 = capi.tucker_init(dims, core, [a.numpy() for a in idx_h], vals_h.numpy(),
-                              [u.numpy() for u in U0_h], device=local, stream=stream.cuda_stream)
+                              [u.numpy() for u in U0_h], device=local, stream=stream.cuda_stream, **kw2)
         capi.hooi_sweep(h2, S)
         capi.core_and_fit_into(h2, G_h.numpy(), [u.numpy() for u in U_h])
         capi.tucker_set_factors(h2, [u.numpy() for u in U0_h])
@@ -280,7 +301,12 @@ def run_ours(args):
         torch.cuda.synchronize()
         capi.tucker_free(h2)
         e2e_ms.append(e0.elapsed_time(e1))
-    e2e_val = units / (statistics.median(e2e_ms) / 1e3) / 1e9 * world
+    e2e_med = statistics.median(e2e_ms)
+    if world > 1:
+        t = torch.tensor([e2e_med], device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        e2e_med = float(t.item())
+    e2e_val = units / (e2e_med / 1e3) / 1e9 * (1 if sharded else world)
 
     # ---- roofline of the dominant kernel (the fused eigensolver) ----
     pk = peaks()
@@ -335,10 +361,13 @@ def run_ours(args):
         "metric": "HOOI/MP sweep throughput (nnz x modes per second)",
         "value": value, "unit": "Gnnz/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f32 storage, 3xTF32/f64 Gram, f64 eig",
+        "scaling": "strong" if sharded else "weak", "vs_baseline": None,
+        "dtype": "f32 storage, 3xTF32/f64 Gram, f64 eig",
         "data": "synthetic",
         "config": {"workload": c["name"], "l2": "flushed (512 MB write) before every timed step",
-                   "parallelism": f"replicas x{world}"},
+                   "parallelism": (f"sharded x{world}: HOOI by mode-n slice ranges, MP by slice-index ranges; "
+                                   "NCCL allreduce of Y / partial Gram / U / G / M_n (DESIGN.md Multi-GPU)")
+                   if sharded else "single GPU"},
         "hooi_ms_per_sweep": float(stage_acc.sum() / args.steps / S),
         "mp_ms_per_sweep": float(stage_acc_mp.sum() / args.steps / S),
         "fit": {"hooi": fits[0], "mp": fits[1]},

@@ -17,9 +17,16 @@
  *   - All calls are blocking (stream-synchronised on return) and not
  *     re-entrant per handle.  Different handles may be used from different
  *     threads.
- *   - Multi-GPU (world > 1): collective -- every rank makes the same call
- *     sequence with the same arguments (round-1 builds accept world == 1 only
- *     and return TUCKER_E_ARG otherwise).
+ *   - Multi-GPU: one process per GPU;
+ *     every rank passes the FULL tensor and the same arguments, plus its rank,
+ *     the world size and the same 128-byte ncclUniqueId (tucker_nccl_unique_id
+ *     on one rank, broadcast by the caller).  hooi_sweep, mp_sweep,
+ *     core_and_fit and the debug Gram/TTMc calls are then collective: every
+ *     rank makes the same call sequence (the debug Gram returns this rank's
+ *     partial Gram).  The library picks its own shard
+ *     (HOOI: a contiguous range of mode-n slices, MP: of each term's slice
+ *     index) and sums partial results with NCCL allreduces on its stream;
+ *     factors, core and fit come back replicated on every rank.
  *
  * Return value: 0 (TUCKER_OK) or one of the TUCKER_E_* codes below; a
  * human-readable message for the code is tucker_strerror(code) and the last
@@ -58,8 +65,9 @@ typedef struct tucker_handle tucker_handle;
 
 typedef struct {
   int device;                 /* CUDA device ordinal for this rank                             */
-  int rank, world;            /* one rank per GPU; world == 1 in this build                     */
-  const void* nccl_unique_id; /* 128-byte ncclUniqueId (NULL when world == 1)                   */
+  int rank, world;            /* one rank per GPU, 0 <= rank < world                           */
+  const void* nccl_unique_id; /* 128-byte ncclUniqueId, required when world > 1; with world == 1
+                                 it runs the sharded code path over a 1-rank communicator       */
   void* stream;               /* cudaStream_t to run on (NULL = the handle's own stream)        */
   int eig_oversample;         /* p in block size k = J + p (0 = default)         */
   int eig_max_iter;           /* cap on Chebyshev-filter outer iterations (0 = default 40)      */
@@ -194,6 +202,23 @@ int tucker_csf_stats(tucker_handle* h, int64_t* out);
  * breakdown in ns (phase A, inner barrier, phase B, leading barrier; CTA 0's
  * view).  stats has 18 entries. */
 int tucker_stats(tucker_handle* h, int64_t* stats, int reset);
+
+/* A fresh 128-byte ncclUniqueId in id_out (caller-owned) for tucker_opts;
+ * loads NCCL (libnccl.so.2) on demand.  TUCKER_E_NCCL if it cannot. */
+int tucker_nccl_unique_id(void* id_out);
+
+/* The library's shard rule, host only (no device work): contiguous bounds
+ * over n items with nonnegative work[i], bounds[0] = 0, bounds[world] = n,
+ * bounds[r] = the first index whose work prefix (counting half of the item
+ * itself) reaches r/world of the total; shards may be empty.  bounds has
+ * world + 1 entries.  TUCKER_E_ARG on null pointers, n < 0 or world < 1. */
+int tucker_shard_bounds(const double* work, int64_t n, int world, int64_t* bounds);
+
+/* This rank's shards (out has 2 N + 2 N N entries): out[2n], out[2n + 1] =
+ * [lo, hi) of the root slices of mode n's HOOI projection; out[2N + 2(nN + m)],
+ * [.. + 1] = [lo, hi) of the slice index of MP term (n, m) (0, 0 for n == m).
+ * Unsharded handles report the full ranges. */
+int tucker_shard_info(tucker_handle* h, int64_t* out);
 
 #ifdef __cplusplus
 }

@@ -12,7 +12,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libtucker.so")
-SOURCES = ["tucker.cu", "csf.cu", "spttmc.cu", "gram_tc.cu", "gram_simt.cu", "dense.cu", "eig.cu", "eig_fused.cu"]
+SOURCES = ["tucker.cu", "csf.cu", "spttmc.cu", "gram_tc.cu", "gram_simt.cu", "dense.cu", "eig.cu", "eig_fused.cu", "dist.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
@@ -54,7 +54,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         raise RuntimeError("nvcc failed:\n" + "\n".join(failed))
     tmp = LIB + ".tmp"
     cmd = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", tmp, *objs,
-           "-Xcompiler", "-fPIC"]
+           "-Xcompiler", "-fPIC", "-ldl"]
     subprocess.run(cmd, check=True)
     os.replace(tmp, LIB)
     return LIB

@@ -25,6 +25,7 @@ EXPORTS = [
     "tucker_set_factors", "tucker_free", "tucker_strerror", "tucker_last_error",
     "tucker_debug_ttmc", "tucker_debug_gram", "tucker_debug_eig", "tucker_debug_smalldense",
     "tucker_debug_product", "tucker_debug_product_time", "tucker_csf_stats", "tucker_stats",
+    "tucker_nccl_unique_id", "tucker_shard_bounds", "tucker_shard_info",
 ]
 
 
@@ -63,6 +64,9 @@ def load(path: str = LIB_PATH) -> C.CDLL:
     lib.tucker_debug_product.argtypes = [C.c_int, C.c_int, P, P, C.c_double, C.c_double, P, P]
     lib.tucker_debug_product_time.argtypes = [C.c_int, C.c_int, C.c_int, C.POINTER(C.c_double)]
     lib.tucker_csf_stats.argtypes = [P, i64p]
+    lib.tucker_nccl_unique_id.argtypes = [P]
+    lib.tucker_shard_bounds.argtypes = [C.POINTER(C.c_double), C.c_int64, C.c_int, i64p]
+    lib.tucker_shard_info.argtypes = [P, i64p]
     lib.tucker_debug_smalldense.argtypes = [C.c_int, C.c_int, P, P, P, P, C.c_int, C.c_double]
     for name in EXPORTS:
         if name not in ("tucker_default_opts", "tucker_strerror", "tucker_last_error"):
@@ -102,10 +106,13 @@ def _ptr(a) -> int:
 
 
 def tucker_init(dims, core, idx, vals, U0, *, device=0, stream=None, eig_oversample=0,
-                eig_max_iter=0, eig_tol=0.0, on_device=False, output_on_device=False):
+                eig_max_iter=0, eig_tol=0.0, on_device=False, output_on_device=False,
+                rank=0, world=1, nccl_id=None):
     """Returns an opaque handle (int).  idx: list of N int32 arrays (0-based),
     vals: fp32, U0: list of N fp32 row-major I_n x J_n arrays.  Host numpy
-    arrays, or torch CUDA tensors with on_device=True."""
+    arrays, or torch CUDA tensors with on_device=True.  Multi-GPU: every rank
+    passes the full tensor, its rank, the world size and the same 128-byte
+    nccl_id (nccl_unique_id() on one rank, broadcast by the caller)."""
     L = lib()
     N = len(dims)
     if not on_device:
@@ -121,6 +128,12 @@ def tucker_init(dims, core, idx, vals, U0, *, device=0, stream=None, eig_oversam
     o.eig_tol = eig_tol
     o.flags = (TUCKER_INPUT_ON_DEVICE if on_device else 0) | (
         TUCKER_OUTPUT_ON_DEVICE if output_on_device else 0)
+    o.rank = rank
+    o.world = world
+    idbuf = None
+    if nccl_id is not None:
+        idbuf = C.create_string_buffer(bytes(nccl_id), 128)
+        o.nccl_unique_id = C.cast(idbuf, C.c_void_p)
     d = (C.c_int64 * N)(*[int(x) for x in dims])
     j = (C.c_int64 * N)(*[int(x) for x in core])
     ip = (C.c_void_p * N)(*[_ptr(a) for a in idx])
@@ -260,6 +273,36 @@ def tucker_csf_fibers(h, order=3):
     return sum(st[0] for st in tucker_csf_stats(h, order))
 
 
+def nccl_unique_id():
+    """A fresh 128-byte ncclUniqueId (bytes) for tucker_init(..., nccl_id=)."""
+    buf = C.create_string_buffer(128)
+    _check(lib().tucker_nccl_unique_id(buf))
+    return buf.raw
+
+
+def shard_bounds(work, world):
+    """The library's contiguous shard bounds (host only) -> int64 array world+1."""
+    w = np.ascontiguousarray(work, dtype=np.float64)
+    b = np.zeros(world + 1, dtype=np.int64)
+    _check(lib().tucker_shard_bounds(w.ctypes.data_as(C.POINTER(C.c_double)), C.c_int64(w.size),
+                                     world, b.ctypes.data_as(C.POINTER(C.c_int64))))
+    return b
+
+
+def tucker_shard_info(h, order):
+    """This rank's shards: (hooi [(lo, hi)] per mode, mp {(n, m): (lo, hi)})."""
+    out = np.zeros(2 * order + 2 * order * order, dtype=np.int64)
+    _check(lib().tucker_shard_info(h, out.ctypes.data_as(C.POINTER(C.c_int64))), h)
+    hooi = [(int(out[2 * n]), int(out[2 * n + 1])) for n in range(order)]
+    mp = {}
+    for n in range(order):
+        for m in range(order):
+            if m != n:
+                k = 2 * order + 2 * (n * order + m)
+                mp[(n, m)] = (int(out[k]), int(out[k + 1]))
+    return hooi, mp
+
+
 def tucker_stats(h, reset=False):
     s = (C.c_int64 * 18)()
     _check(lib().tucker_stats(h, s, 1 if reset else 0), h)
@@ -294,6 +337,9 @@ class Tucker:
     def debug_ttmc(self, mode):
         P = int(np.prod([J for m, J in enumerate(self.core) if m != mode]))
         return tucker_debug_ttmc(self.h, mode, self.dims[mode], P)
+
+    def shard_info(self):
+        return tucker_shard_info(self.h, len(self.dims))
 
     def csf_stats(self):
         return tucker_csf_stats(self.h, len(self.dims))

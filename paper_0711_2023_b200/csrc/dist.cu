@@ -1,0 +1,104 @@
+// dist.cu -- multi-GPU plumbing for the sharded sweep:
+// NCCL loaded on demand (dlopen of libnccl.so.2: the one torch already loaded
+// when the caller imported it; a single-GPU process never needs it), the
+// collectives the sweep uses, and the contiguous work-balanced shard bounds.
+//
+// Exchange steps (one per mode, all sums of disjoint or partial terms):
+//   HOOI, Y Y^T route: rows of Y_(n) are disjoint across ranks -> allreduce Y
+//   HOOI, Y^T Y route: partial Gram over the rank's K range -> allreduce S (fp64);
+//                      rows of U = Y V Theta^{-1/2} disjoint -> allreduce U
+//   HOOI core:         G = U_N^T Y_(N) partial when Y was not gathered -> allreduce G
+//   MP:                partial M_n over the rank's slices -> allreduce M_n (fp64)
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <cstring>
+#include <string>
+
+#include "internal.cuh"
+
+namespace tk {
+namespace {
+
+struct NcclApi {
+  void* lib = nullptr;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+
+NcclApi& api() {
+  static NcclApi a;
+  if (!a.lib) {
+    void* l = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!l) fail(TUCKER_E_NCCL, std::string("cannot load libnccl.so.2: ") + dlerror());
+    auto sym = [&](const char* n) {
+      void* p = dlsym(l, n);
+      if (!p) fail(TUCKER_E_NCCL, std::string("libnccl.so.2 lacks ") + n);
+      return p;
+    };
+    a.GetUniqueId = (decltype(a.GetUniqueId))sym("ncclGetUniqueId");
+    a.CommInitRank = (decltype(a.CommInitRank))sym("ncclCommInitRank");
+    a.AllReduce = (decltype(a.AllReduce))sym("ncclAllReduce");
+    a.CommDestroy = (decltype(a.CommDestroy))sym("ncclCommDestroy");
+    a.GetErrorString = (decltype(a.GetErrorString))sym("ncclGetErrorString");
+    a.lib = l;
+  }
+  return a;
+}
+
+void check(ncclResult_t r, const char* what) {
+  if (r != ncclSuccess) fail(TUCKER_E_NCCL, std::string(what) + ": " + api().GetErrorString(r));
+}
+
+}  // namespace
+
+void* dist_comm_init(const void* unique_id, int world, int rank) {
+  static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId is 128 bytes");
+  ncclUniqueId id;
+  std::memcpy(&id, unique_id, sizeof(id));
+  ncclComm_t c = nullptr;
+  check(api().CommInitRank(&c, world, id, rank), "ncclCommInitRank");
+  return c;
+}
+
+void dist_comm_destroy(void* comm) {
+  if (comm) api().CommDestroy((ncclComm_t)comm);
+}
+
+void dist_allreduce_f32(void* comm, float* p, int64_t n, cudaStream_t st) {
+  if (n > 0) check(api().AllReduce(p, p, (size_t)n, ncclFloat32, ncclSum, (ncclComm_t)comm, st), "ncclAllReduce");
+}
+
+void dist_allreduce_f64(void* comm, double* p, int64_t n, cudaStream_t st) {
+  if (n > 0) check(api().AllReduce(p, p, (size_t)n, ncclFloat64, ncclSum, (ncclComm_t)comm, st), "ncclAllReduce");
+}
+
+void dist_unique_id(void* out) {
+  ncclUniqueId id;
+  check(api().GetUniqueId(&id), "ncclGetUniqueId");
+  std::memcpy(out, &id, sizeof(id));
+}
+
+// Contiguous shard bounds over n items with nonnegative work w: bounds[0] = 0,
+// bounds[world] = n, bounds[r] = the first index whose work prefix reaches
+// r / world of the total (ties and zero work go to the lower rank); empty
+// shards are allowed (more ranks than items, or one item heavier than a share).
+void shard_bounds(const double* w, int64_t n, int world, int64_t* bounds) {
+  double total = 0;
+  for (int64_t i = 0; i < n; ++i) total += w[i];
+  bounds[0] = 0;
+  int64_t i = 0;
+  double prefix = 0;
+  for (int r = 1; r < world; ++r) {
+    const double target = total * (double)r / (double)world;
+    while (i < n && prefix + 0.5 * w[i] < target) prefix += w[i++];
+    bounds[r] = i;
+  }
+  bounds[world] = n;
+}
+
+}  // namespace tk

@@ -145,8 +145,8 @@ void gram_syrk_dmma(const Split& A, double* S, int64_t lds, GramWs& ws, cudaStre
   const int64_t d = A.rows;
   const int nb = (int)ceil_div(d, DT);
   const int ntiles = nb * (nb + 1) / 2;
-  if (A.ld % DKC != 0) fail(TUCKER_E_ARG, "gram_syrk_dmma: ld must be a multiple of 32");
-  const int nchunks = (int)(A.ld / DKC);
+  if (A.ld % DKC != 0 || A.K() % DKC != 0) fail(TUCKER_E_ARG, "gram_syrk_dmma: ld and K must be multiples of 32");
+  const int nchunks = (int)(A.K() / DKC);
   int nsm = 148;
   {
     int dev = 0;
@@ -170,8 +170,8 @@ void gram_syrk_dmma(const Split& A, double* S, int64_t lds, GramWs& ws, cudaStre
 
 void gram_syrk_simt(const Split& A, double* S, int64_t lds, cudaStream_t st) {
   const int64_t nb = ceil_div(A.rows, TB);
-  TK_LAUNCH(k_syrk_simt, (unsigned)(nb * (nb + 1) / 2), 256, 0, st, A.hi, A.lo, A.rows, A.cols,
-            A.ld, S, lds);
+  TK_LAUNCH(k_syrk_simt, (unsigned)(nb * (nb + 1) / 2), 256, 0, st, A.hi, A.lo, A.rows,
+            A.kext > 0 ? A.kext : A.cols, A.ld, S, lds);
 }
 
 int gram_mode() {

@@ -220,10 +220,10 @@ EncodeTiledFn encode_fn() {
   return fn;
 }
 
-CUtensorMap make_map(const float* base, int64_t rows_pad, int64_t ld) {
+CUtensorMap make_map(const float* base, int64_t rows_pad, int64_t ld, int64_t kext) {
   CUtensorMap m;
   std::memset(&m, 0, sizeof(m));
-  const cuuint64_t gdim[2] = {(cuuint64_t)ld, (cuuint64_t)rows_pad};
+  const cuuint64_t gdim[2] = {(cuuint64_t)kext, (cuuint64_t)rows_pad};
   const cuuint64_t gstride[1] = {(cuuint64_t)(ld * 4)};
   const cuuint32_t box[2] = {(cuuint32_t)TKE, (cuuint32_t)TM};
   const cuuint32_t estr[2] = {1, 1};
@@ -245,10 +245,10 @@ void gram_syrk_tc(const Split& A, double* S, int64_t lds, GramWs& ws, cudaStream
   }
   const int64_t d = A.rows;
   const int64_t rows_pad = round_up(d, TM);
-  if (A.ld % TKE != 0) fail(TUCKER_E_ARG, "gram_syrk_tc: ld must be a multiple of 32");
+  if (A.ld % TKE != 0 || A.K() % TKE != 0) fail(TUCKER_E_ARG, "gram_syrk_tc: ld and K must be multiples of 32");
   const int nb = (int)(rows_pad / TM);
   const int ntiles = nb * (nb + 1) / 2;
-  const int nkt = (int)(A.ld / TKE);
+  const int nkt = (int)(A.K() / TKE);
   std::vector<int2> tiles;
   tiles.reserve(ntiles);
   for (int i = 0; i < nb; ++i)
@@ -265,8 +265,8 @@ void gram_syrk_tc(const Split& A, double* S, int64_t lds, GramWs& ws, cudaStream
   TK_CUDA(cudaMemcpyAsync(ws.scratch.p, tiles.data(), sizeof(int2) * tiles.size(),
                           cudaMemcpyHostToDevice, st));
   ws.partial.ensure((size_t)splits * ntiles * TM * TN);
-  const CUtensorMap mhi = make_map(A.hi, rows_pad, A.ld);
-  const CUtensorMap mlo = make_map(A.lo, rows_pad, A.ld);
+  const CUtensorMap mhi = make_map(A.hi, rows_pad, A.ld, A.K());
+  const CUtensorMap mlo = make_map(A.lo, rows_pad, A.ld, A.K());
   SyrkArgs a;
   a.tiles = (const int2*)ws.scratch.p;
   a.ntiles = ntiles;
@@ -286,7 +286,12 @@ void gram_syrk(const Split& A, double* S, int64_t lds, GramWs& ws, cudaStream_t 
     gram_syrk_simt(A, S, lds, st);
     return;
   }
-  const double fma = 0.5 * (double)A.rows * (double)(A.rows + 1) * (double)A.ld;
+  if (A.K() == 0) {  // empty K shard: S = 0
+    for (int64_t i = 0; i < A.rows; ++i)
+      TK_CUDA(cudaMemsetAsync(S + i * lds, 0, A.rows * sizeof(double), st));
+    return;
+  }
+  const double fma = 0.5 * (double)A.rows * (double)(A.rows + 1) * (double)A.K();
   if (fma <= 2e10) gram_syrk_dmma(A, S, lds, ws, st);
   else gram_syrk_tc(A, S, lds, ws, st);
 }

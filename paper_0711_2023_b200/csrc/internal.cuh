@@ -56,7 +56,8 @@ void coo_validate_compact(Coo& coo, cudaStream_t st);          // E_INDEX / E_VA
 double coo_norm2(const Coo& coo, cudaStream_t st);              // ||X||_F^2 (fp64, fixed order)
 void csf_build(const Coo& coo, Csf& out, int root, int mid0, int mid1, int leaf, cudaStream_t st);
 // spttmc.cu: HOOI work units for an order-3 CSF whose output tile is Jm x Jl
-void spttmc_plan(Csf& c, int64_t Jm, int64_t Jl, int num_sms, cudaStream_t st);
+// (lo, hi): the rank's root-slice range (hi < 0: all)
+void spttmc_plan(Csf& c, int64_t Jm, int64_t Jl, int num_sms, cudaStream_t st, int64_t lo = 0, int64_t hi = -1);
 
 // ---------------------------------------------------------------------------
 // Split-fp32 matrix: a = hi + lo exactly, hi = tf32-rounded a (DESIGN.md
@@ -66,16 +67,31 @@ struct Split {
   float* hi = nullptr;
   float* lo = nullptr;
   int64_t rows = 0, cols = 0, ld = 0;  // logical rows/cols; ld = padded row length
+  // Gram K extent when the view covers part of each row (a K-range shard of
+  // Y^T whose pointers are offset by a multiple of 32 columns); 0 = ld
+  int64_t kext = 0;
+  int64_t K() const { return kext > 0 ? kext : ld; }
 };
 
 // spttmc.cu
 // HOOI: Y_(n) (Kolda order) written as split fp32; transposed => out is Y_(n)^T.
+// Only the root slices [lo, hi) are computed (a rank's shard; hi < 0: all); the
+// other rows of out stay as they are (zero).
 void spttmc_hooi(const Csf& c, const float* const* U, const int64_t* J, Split out, bool transposed,
-                 cudaStream_t st);
-// MP: W columns [col_off, col_off + prod(I_mids)*J_leaf) of the rows of out
-// (out pre-zeroed): W[i_root, col_off + mk*J_leaf + j] = sum_{x in fiber} x U_leaf[i_leaf, j].
+                 cudaStream_t st, int64_t lo = 0, int64_t hi = -1);
+// MP: W columns [col_off, col_off + (s_hi - s_lo)*J_leaf) of the rows of out
+// (out pre-zeroed): W[i_root, col_off + (mk - s_lo)*J_leaf + j] = sum_{x in fiber} x U_leaf[i_leaf, j]
+// for the slices mk (the mid index) in [s_lo, s_hi) (a rank's shard; s_hi < 0: all).
 void spmm_mp(const Csf& c, const float* U_leaf, int64_t J_leaf, Split out, int64_t col_off,
-             cudaStream_t st);
+             cudaStream_t st, int64_t s_lo = 0, int64_t s_hi = -1);
+
+// dist.cu -- NCCL (loaded on demand) and shard bounds for the sharded sweep
+void* dist_comm_init(const void* unique_id, int world, int rank);
+void dist_comm_destroy(void* comm);
+void dist_allreduce_f32(void* comm, float* p, int64_t n, cudaStream_t st);
+void dist_allreduce_f64(void* comm, double* p, int64_t n, cudaStream_t st);
+void dist_unique_id(void* out128);
+void shard_bounds(const double* w, int64_t n, int world, int64_t* bounds);
 
 // gram.cu -- S (d x d fp64, row-major, ld = lds) = A A^T, A = d x K split fp32.
 struct GramWs {

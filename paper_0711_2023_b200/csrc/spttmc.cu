@@ -267,6 +267,7 @@ __device__ __forceinline__ void kron_stage(int nf, const float* T, const float* 
 struct Ttmc3Args {
   const int32_t *slice_ptr, *fib_ptr, *fib_mid, *leaf_id;
   const int32_t* unit;  // work units (slice, f0, f1, slot) or null: one CTA per slice
+  int slice0;           // first slice of this launch (rank shard) when unit == null
   float* part;          // partial tiles of split slices (Jm * Jl floats per slot)
   const float* val;
   const float *Umid, *Uleaf;
@@ -290,7 +291,7 @@ __global__ void __launch_bounds__(256) k_spttmc3(Ttmc3Args p) {
     f1 = u.z;
     slot = u.w;
   } else {
-    i = blockIdx.x;
+    i = p.slice0 + blockIdx.x;
     f0 = p.slice_ptr[i];
     f1 = p.slice_ptr[i + 1];
   }
@@ -411,7 +412,7 @@ __global__ void __launch_bounds__(256) k_spttmc3_tc(Ttmc3Args p) {
     f1 = u.z;
     slot = u.w;
   } else {
-    i = blockIdx.x;
+    i = p.slice0 + blockIdx.x;
     f0 = p.slice_ptr[i];
     f1 = p.slice_ptr[i + 1];
   }
@@ -608,6 +609,7 @@ struct Ttmc4Args {
   int64_t ldY;
   int transposed;
   int64_t s0, s1, sb;  // Kolda strides of (mid0, mid1, leaf) indices
+  int slice0;          // first slice of this launch (rank shard)
 };
 
 template <int RA, int RB, int RQ>
@@ -617,7 +619,7 @@ __global__ void __launch_bounds__(256) k_spttmc4(Ttmc4Args p) {
   __shared__ __align__(16) float M[kFC * JMP];
   __shared__ float Zs[JMP * JLP];
   __shared__ float u0[128];
-  const int i = blockIdx.x;
+  const int i = p.slice0 + blockIdx.x;
   const int n0 = p.slice_ptr[i], n1 = p.slice_ptr[i + 1];
   const int P1 = p.J1 * p.Jl;
   const int P = p.J0 * P1;
@@ -678,6 +680,7 @@ struct SpmmArgs {
   int64_t nfib, I_mid1;
   float *Whi, *Wlo;
   int64_t ldW, col_off;
+  int64_t s_lo, s_hi, s_all;  // slices (mid index) of this rank of s_all; W columns start at col_off for s_lo
 };
 
 template <int QL>
@@ -686,6 +689,11 @@ __global__ void __launch_bounds__(256) k_spmm_mp(SpmmArgs p) {
   const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   for (int64_t f = warp; f < p.nfib; f += nwarps) {
+    if (p.s_lo > 0 || p.s_hi < p.s_all) {  // sharded: skip other ranks' slices before any leaf work
+      int64_t mk = __ldg(p.fib_mid0 + f);
+      if (p.fib_mid1) mk = mk * p.I_mid1 + __ldg(p.fib_mid1 + f);
+      if (mk < p.s_lo || mk >= p.s_hi) continue;
+    }
     const int e0 = __ldg(p.fib_ptr + f), e1 = __ldg(p.fib_ptr + f + 1);
     float t[QL];
 #pragma unroll
@@ -701,7 +709,8 @@ __global__ void __launch_bounds__(256) k_spmm_mp(SpmmArgs p) {
     }
     int64_t mk = __ldg(p.fib_mid0 + f);
     if (p.fib_mid1) mk = mk * p.I_mid1 + __ldg(p.fib_mid1 + f);
-    const int64_t base = (int64_t)__ldg(p.fib_root + f) * p.ldW + p.col_off + mk * p.J;
+    if (mk < p.s_lo || mk >= p.s_hi) continue;  // another rank's slice
+    const int64_t base = (int64_t)__ldg(p.fib_root + f) * p.ldW + p.col_off + (mk - p.s_lo) * p.J;
 #pragma unroll
     for (int q = 0; q < QL; ++q) {
       const int j = lane + 32 * q;
@@ -723,7 +732,9 @@ static int64_t kolda_stride(int m, const int* others, int nothers, const int64_t
 }
 
 void spttmc_hooi(const Csf& c, const float* const* U, const int64_t* J, Split out, bool transposed,
-                 cudaStream_t st) {
+                 cudaStream_t st, int64_t lo, int64_t hi) {
+  if (hi < 0) hi = c.I_root;
+  if (hi <= lo) return;  // empty shard: Y stays zero
   int others[3], no = 0;
   for (int m = 0; m < c.order; ++m)
     if (m != c.root) others[no++] = m;
@@ -746,13 +757,14 @@ void spttmc_hooi(const Csf& c, const float* const* U, const int64_t* J, Split ou
     a.sa = kolda_stride(c.mid0, others, no, J);
     a.sb = kolda_stride(c.leaf, others, no, J);
     a.unit = c.nunits > 0 ? c.unit.p : nullptr;
+    a.slice0 = (int)lo;  // the work plan (if any) was built for [lo, hi) already
     if (c.nunits > 0) {  // virtual fibers
       a.fib_ptr = c.vfib_ptr.p;
       a.fib_mid = c.vfib_mid.p;
     }
     a.part = c.part.p;
     const int RA = rtile(a.Jm), RB = rtile(a.Jl);
-    const dim3 g((unsigned)(c.nunits > 0 ? c.nunits : c.I_root));
+    const dim3 g((unsigned)(c.nunits > 0 ? c.nunits : hi - lo));
     bool launched = false;
     // U_leaf row vector width: rows of Jl floats are 16-byte aligned iff 4 | Jl
     const int VW = a.Jl % 4 == 0 ? 4 : (a.Jl % 2 == 0 ? 2 : 1);
@@ -824,7 +836,8 @@ void spttmc_hooi(const Csf& c, const float* const* U, const int64_t* J, Split ou
   const int64_t P = (int64_t)a.J0 * a.J1 * a.Jl;
   const int RA = rtile(a.J1), RB = rtile(a.Jl);
   const int64_t RQ = ceil_div(P, 256);
-  const dim3 g((unsigned)c.I_root);
+  a.slice0 = (int)lo;
+  const dim3 g((unsigned)(hi - lo));
 #define TK_S4(ra, rb, rq)                                                    \
   if (RA <= ra && RB <= rb && RQ <= rq) {                                    \
     TK_LAUNCH((k_spttmc4<ra, rb, rq>), g, 256, 0, st, a);                    \
@@ -842,8 +855,9 @@ void spttmc_hooi(const Csf& c, const float* const* U, const int64_t* J, Split ou
 // 1-4 have short fibers and light slices: no plan, one CTA per slice.
 // Config 5's Zipf head (a slice with 7e6 nonzeros in <= 5000 fibers) is what
 // this is for.
-void spttmc_plan(Csf& c, int64_t Jm, int64_t Jl, int num_sms, cudaStream_t st) {
+void spttmc_plan(Csf& c, int64_t Jm, int64_t Jl, int num_sms, cudaStream_t st, int64_t lo, int64_t hi) {
   if (c.order != 3) return;
+  if (hi < 0) hi = c.I_root;
   const int64_t I = c.I_root, F = c.nfib;
   std::vector<int32_t> sp((size_t)I + 1), fp((size_t)F + 1);
   TK_CUDA(cudaMemcpyAsync(sp.data(), c.slice_ptr.p, sp.size() * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
@@ -857,7 +871,7 @@ void spttmc_plan(Csf& c, int64_t Jm, int64_t Jl, int num_sms, cudaStream_t st) {
   const double wf = (double)Jm * Jl, wn = (double)Jl;  // work per fiber / per nonzero
   double total = 0;
   int64_t longest = 0;
-  for (int64_t f = 0; f < F; ++f) {
+  for (int64_t f = sp[lo]; f < sp[hi]; ++f) {  // this rank's slices only
     const int64_t L = fp[f + 1] - fp[f];
     longest = std::max(longest, L);
     total += wf * (double)ceil_div(L, c.lmax) + wn * (double)L;
@@ -865,7 +879,7 @@ void spttmc_plan(Csf& c, int64_t Jm, int64_t Jl, int num_sms, cudaStream_t st) {
   c.cmax = std::max(4194304.0, total / (16.0 * num_sms));
   if (ec && std::atof(ec) > 0) c.cmax = std::atof(ec);
   double heaviest = 0;
-  for (int64_t i = 0; i < I; ++i) {
+  for (int64_t i = lo; i < hi; ++i) {
     const double w = wf * (double)(sp[i + 1] - sp[i]) + wn * (double)(fp[sp[i + 1]] - fp[sp[i]]);
     heaviest = std::max(heaviest, w);
   }
@@ -878,7 +892,7 @@ void spttmc_plan(Csf& c, int64_t Jm, int64_t Jl, int num_sms, cudaStream_t st) {
   std::vector<int32_t> vptr, vmid, vsp((size_t)I + 1);
   vptr.reserve((size_t)F + 1);
   vmid.reserve((size_t)F);
-  for (int64_t i = 0; i < I; ++i) {
+  for (int64_t i = lo; i < hi; ++i) {
     vsp[i] = (int32_t)vmid.size();
     for (int64_t f = sp[i]; f < sp[i + 1]; ++f) {
       const int64_t L = fp[f + 1] - fp[f], nv = std::max<int64_t>(1, ceil_div(L, c.lmax));
@@ -888,15 +902,15 @@ void spttmc_plan(Csf& c, int64_t Jm, int64_t Jl, int num_sms, cudaStream_t st) {
       }
     }
   }
-  vsp[I] = (int32_t)vmid.size();
-  vptr.push_back(fp[F]);
+  vsp[hi] = (int32_t)vmid.size();
+  vptr.push_back(fp[sp[hi]]);
   c.nvfib = (int64_t)vmid.size();
   // units: greedy cut of each slice's virtual fibers at ~equal work
   std::vector<std::array<int32_t, 4>> units;
   std::vector<double> uw;
   std::vector<int32_t> red;
   int32_t slot = 0;
-  for (int64_t i = 0; i < I; ++i) {
+  for (int64_t i = lo; i < hi; ++i) {
     const int64_t v0 = vsp[i], v1 = vsp[i + 1];
     if (v1 == v0) continue;  // Y is zeroed before the launch
     const double w = wf * (double)(v1 - v0) + wn * (double)(vptr[v1] - vptr[v0]);
@@ -945,8 +959,12 @@ void spttmc_plan(Csf& c, int64_t Jm, int64_t Jl, int num_sms, cudaStream_t st) {
 }
 
 void spmm_mp(const Csf& c, const float* U_leaf, int64_t J_leaf, Split out, int64_t col_off,
-             cudaStream_t st) {
+             cudaStream_t st, int64_t s_lo, int64_t s_hi) {
   SpmmArgs a;
+  a.s_all = c.I_mid0 * c.I_mid1;
+  a.s_lo = s_lo;
+  a.s_hi = s_hi < 0 ? a.s_all : s_hi;
+  if (a.s_hi <= a.s_lo) return;
   a.fib_ptr = c.fib_ptr.p;
   a.fib_root = c.fib_root.p;
   a.fib_mid0 = c.fib_mid0.p;

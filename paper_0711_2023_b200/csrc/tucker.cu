@@ -46,6 +46,12 @@ struct tucker_handle {
   long long prof0[13] = {0};
   std::string last_error;
   bool eig_unconverged = false;
+  // multi-GPU: a sharded sweep when opts.nccl_unique_id is set
+  void* comm = nullptr;
+  bool sharded = false;
+  int64_t hooi_lo[kMaxOrder] = {0, 0, 0, 0}, hooi_hi[kMaxOrder] = {-1, -1, -1, -1};  // root slices of mode n
+  int64_t mp_lo[kMaxOrder][kMaxOrder] = {}, mp_hi[kMaxOrder][kMaxOrder] = {};       // slices of MP term (n, m)
+  bool Y_partial = false;  // h->Y holds only this rank's rows (Y^T Y route, not gathered)
 };
 
 namespace {
@@ -168,18 +174,35 @@ void project_hooi(tucker_handle* h, int n, bool transposed) {
   h->Y.rows = rows;
   h->Y.cols = cols;
   h->Y.ld = ld;
-  spttmc_hooi(*h->csfs[h->hooi_csf[n]], uptrs(h), h->J, h->Y, transposed, h->st);
+  spttmc_hooi(*h->csfs[h->hooi_csf[n]], uptrs(h), h->J, h->Y, transposed, h->st, h->hooi_lo[n], h->hooi_hi[n]);
   h->Y_mode = n;
   h->Y_transposed = transposed;
+  h->Y_partial = false;
+  if (h->sharded) {
+    if (!transposed) {
+      // Y Y^T route: the ranks' rows of Y_(n) are disjoint -> the sum gathers Y
+      dist_allreduce_f32(h->comm, h->Yhi.p, (int64_t)need, h->st);
+      dist_allreduce_f32(h->comm, h->Ylo.p, (int64_t)need, h->st);
+    } else {
+      h->Y_partial = true;  // Y^T Y route: partial Gram over this rank's K range instead
+    }
+  }
 }
 
 // W_n = [ (X x_m U_m^T)_(n) ]_{m != n} into h->Whi/Wlo; returns the split view
 Split build_mp_w(tucker_handle* h, int n) {
+  // sharded: this rank's slices [mp_lo, mp_hi) of every term, columns compacted
+  auto slices = [&](int m, const Csf& c, int64_t& lo, int64_t& hi) {
+    lo = h->sharded ? h->mp_lo[n][m] : 0;
+    hi = h->sharded ? h->mp_hi[n][m] : c.I_mid0 * c.I_mid1;
+  };
   int64_t K = 0;
   for (int m = 0; m < h->order; ++m) {
     if (m == n) continue;
     const Csf& c = *h->csfs[h->mp_csf[n][m]];
-    K += h->J[m] * c.I_mid0 * c.I_mid1;
+    int64_t lo, hi;
+    slices(m, c, lo, hi);
+    K += h->J[m] * (hi - lo);
   }
   const int64_t rows = h->dims[n];
   const int64_t rows_pad = round_up(rows, 128), ld = round_up(K, 32);
@@ -211,8 +234,10 @@ Split build_mp_w(tucker_handle* h, int n) {
   for (int m = 0; m < h->order; ++m) {
     if (m == n) continue;
     const Csf& c = *h->csfs[h->mp_csf[n][m]];
-    spmm_mp(c, h->U[m].p, h->J[m], W, off, h->st);
-    off += h->J[m] * c.I_mid0 * c.I_mid1;
+    int64_t lo, hi;
+    slices(m, c, lo, hi);
+    spmm_mp(c, h->U[m].p, h->J[m], W, off, h->st, lo, hi);
+    off += h->J[m] * (hi - lo);
   }
   return W;
 }
@@ -253,8 +278,11 @@ void eig_check(tucker_handle* h) {
 }
 
 // U_n from the eigenvectors of the Gram of the split matrix A (= Y, Y^T or W)
+// Sharded: a partial Gram (MP: this rank's W columns; HOOI Y^T Y route: this
+// rank's K range of Y^T, rounded out to 32 columns -- the other ranks' columns
+// in the rounding are zero here) summed by an fp64 allreduce.
 void update_factor(tucker_handle* h, int n, const Split& A, bool transposed, EigSlot& slot,
-                   float* ms_gram, float* ms_eig) {
+                   float* ms_gram, float* ms_eig, bool partial_gram) {
   const int64_t d = A.rows;
   const int J = (int)h->J[n];
   const int64_t lds = ensure_S(h, d);
@@ -263,7 +291,19 @@ void update_factor(tucker_handle* h, int n, const Split& A, bool transposed, Eig
   TK_CUDA(cudaEventCreate(&e1));
   TK_CUDA(cudaEventCreate(&e2));
   TK_CUDA(cudaEventRecord(e0, h->st));
-  gram_syrk(A, h->S.p, lds, h->gram, h->st);
+  if (partial_gram && transposed) {
+    const int64_t lo = h->hooi_lo[n], hi = h->hooi_hi[n];
+    const int64_t k0 = std::min(A.ld, lo / 32 * 32), k1 = std::min(A.ld, round_up(std::max(hi, lo), 32));
+    Split Ar = A;
+    Ar.hi = A.hi + k0;
+    Ar.lo = A.lo + k0;
+    Ar.kext = k1 - k0;
+    if (Ar.kext == 0) Ar.ld = 0;  // empty shard: gram_syrk writes S = 0
+    gram_syrk(Ar, h->S.p, lds, h->gram, h->st);
+  } else {
+    gram_syrk(A, h->S.p, lds, h->gram, h->st);
+  }
+  if (partial_gram) dist_allreduce_f64(h->comm, h->S.p, d * lds, h->st);
   TK_CUDA(cudaEventRecord(e1, h->st));
   solve_eig(h, d, J, slot);
   if (!transposed) {
@@ -278,6 +318,8 @@ void update_factor(tucker_handle* h, int n, const Split& A, bool transposed, Eig
     MatRef b;
     b.t = Elt::F64; b.p = h->V.p; b.ld = J; b.trans = false;
     dgemm(I, J, d, 1.0, a, b, 0.0, h->Ufull.p, J, 0.0, nullptr, 0, h->eig.dense, h->st);
+    // sharded: rows of U outside this rank's shard are zero (Y was) -> the sum gathers U
+    if (partial_gram) dist_allreduce_f64(h->comm, h->Ufull.p, I * J, h->st);
     cholqr2(h->Ufull.p, J, I, J, h->eig, h->st);
     canon_to_f32(h->Ufull.p, J, I, J, h->U[n].p, h->st);
   }
@@ -307,6 +349,7 @@ double core_from_y(tucker_handle* h) {
   MatRef b;
   b.t = Elt::SPLIT; b.p = h->Y.hi; b.lo = h->Y.lo; b.ld = h->Y.ld; b.trans = h->Y_transposed;
   dgemm(JN, P, I, 1.0, a, b, 0.0, h->G64.p, P, 0.0, nullptr, 0, h->eig.dense, h->st);
+  if (h->Y_partial) dist_allreduce_f64(h->comm, h->G64.p, JN * P, h->st);  // partial sums over the row shards
   h->scal.ensure(2);
   TK_LAUNCH(k_core_fit, 1, 512, 0, h->st, h->G64.p, JN * P, h->normX2, h->scal.p);
   double out[2];
@@ -321,6 +364,59 @@ double compute_core(tucker_handle* h) {
   const bool tr = prod_J_except(h, n) < h->dims[n];
   project_hooi(h, n, tr);
   return core_from_y(h);
+}
+
+template <typename T>
+std::vector<T> to_host(const DBuf<T>& b, int64_t n, cudaStream_t st) {
+  std::vector<T> v((size_t)n);
+  if (n > 0) TK_CUDA(cudaMemcpyAsync(v.data(), b.p, n * sizeof(T), cudaMemcpyDeviceToHost, st));
+  TK_CUDA(cudaStreamSynchronize(st));
+  return v;
+}
+
+// Work-balanced contiguous shards: HOOI mode n by root slice of
+// its CSF (work J_leaf nnz + prod_{q != n} J_q fibers per slice, the SpTTMc flop
+// model; order 4: J_leaf nnz), MP term (n, m) by slice = mid index (work J_m
+// (nnz + fibers) per slice: the leaf SpMM and its W writes).
+void make_shards(tucker_handle* h) {
+  const int W = h->opts.world, r = h->opts.rank;
+  std::vector<int64_t> b((size_t)W + 1);
+  for (int n = 0; n < h->order; ++n) {
+    const Csf& c = *h->csfs[h->hooi_csf[n]];
+    const auto sp = to_host(c.slice_ptr, c.I_root + 1, h->st);
+    const auto fp = to_host(c.fib_ptr, c.nfib + 1, h->st);
+    std::vector<int32_t> np;
+    if (c.order == 4) np = to_host(c.node_ptr, c.nnode + 1, h->st);
+    const double P = (double)prod_J_except(h, n), Jl = (double)h->J[c.leaf];
+    std::vector<double> w((size_t)c.I_root);
+    for (int64_t i = 0; i < c.I_root; ++i) {
+      if (c.order == 3) {
+        w[i] = Jl * (double)(fp[sp[i + 1]] - fp[sp[i]]) + P * (double)(sp[i + 1] - sp[i]);
+      } else {
+        w[i] = Jl * (double)(fp[np[sp[i + 1]]] - fp[np[sp[i]]]);
+      }
+    }
+    shard_bounds(w.data(), c.I_root, W, b.data());
+    h->hooi_lo[n] = b[r];
+    h->hooi_hi[n] = b[r + 1];
+    for (int m = 0; m < h->order; ++m) {
+      if (m == n) continue;
+      const Csf& t = *h->csfs[h->mp_csf[n][m]];
+      const int64_t ns = t.I_mid0 * t.I_mid1;
+      const auto tf = to_host(t.fib_ptr, t.nfib + 1, h->st);
+      const auto m0 = to_host(t.fib_mid0, t.nfib, h->st);
+      std::vector<int32_t> m1;
+      if (t.mid1 >= 0) m1 = to_host(t.fib_mid1, t.nfib, h->st);
+      std::vector<double> ws((size_t)ns, 0.0);
+      for (int64_t f = 0; f < t.nfib; ++f) {
+        const int64_t mk = t.mid1 >= 0 ? (int64_t)m0[f] * t.I_mid1 + m1[f] : m0[f];
+        ws[mk] += (double)h->J[m] * (double)(tf[f + 1] - tf[f] + 1);
+      }
+      shard_bounds(ws.data(), ns, W, b.data());
+      h->mp_lo[n][m] = b[r];
+      h->mp_hi[n][m] = b[r + 1];
+    }
+  }
 }
 
 int validate_factor(const float* U, int64_t I, int64_t J) {
@@ -384,7 +480,8 @@ int tucker_init(tucker_handle** out, int order, const int64_t* dims, const int64
   tucker_opts o;
   tucker_default_opts(&o);
   if (opts) o = *opts;
-  if (o.world != 1) return TUCKER_E_ARG;
+  if (o.world < 1 || o.rank < 0 || o.rank >= o.world) return TUCKER_E_ARG;
+  if (o.world > 1 && !o.nccl_unique_id) return TUCKER_E_ARG;
   for (int n = 0; n < order; ++n) {
     if (dims[n] < 1 || dims[n] >= (int64_t)1 << 31) return TUCKER_E_ARG;
     if (core[n] < 1 || core[n] > dims[n] || core[n] > kMaxJ) return TUCKER_E_ARG;
@@ -459,11 +556,18 @@ int tucker_init(tucker_handle** out, int order, const int64_t* dims, const int64
         }
       }
       h->hooi_csf[n] = h->mp_csf[n][best];
-      if (order == 3) {
-        Csf& ch = *h->csfs[h->hooi_csf[n]];
-        spttmc_plan(ch, h->J[ch.mid0], h->J[ch.leaf], sm_count(h->opts.device), h->st);
-      }
     }
+    if (o.nccl_unique_id) {
+      h->comm = dist_comm_init(o.nccl_unique_id, o.world, o.rank);
+      h->sharded = true;
+      make_shards(h.get());
+    }
+    if (order == 3)
+      for (int n = 0; n < order; ++n) {
+        Csf& ch = *h->csfs[h->hooi_csf[n]];
+        spttmc_plan(ch, h->J[ch.mid0], h->J[ch.leaf], sm_count(h->opts.device), h->st, h->hooi_lo[n],
+                    h->hooi_hi[n]);
+      }
     // the COO copy is no longer needed
     for (int n = 0; n < order; ++n) c.idx[n].release();
     c.val.release();
@@ -522,7 +626,7 @@ int hooi_sweep(tucker_handle* h, int sweeps, double* fit_per_sweep, float* stage
         ms[0] += t;
         cudaEventDestroy(a);
         cudaEventDestroy(b);
-        update_factor(h, n, h->Y, tr, h->slots[0][n], &ms[1], &ms[2]);
+        update_factor(h, n, h->Y, tr, h->slots[0][n], &ms[1], &ms[2], h->sharded && tr);
       }
       // G_(N) = U_N^T Y_(N) is free after the last mode (Fig. 4)
       cudaEvent_t a, b;
@@ -565,7 +669,7 @@ int mp_sweep(tucker_handle* h, int sweeps, double* fit_per_sweep, float* stage_m
         ms[0] += t;
         cudaEventDestroy(a);
         cudaEventDestroy(b);
-        update_factor(h, n, W, false, h->slots[1][n], &ms[1], &ms[2]);
+        update_factor(h, n, W, false, h->slots[1][n], &ms[1], &ms[2], h->sharded);
       }
       h->G_valid = false;
       if (fit_per_sweep) {
@@ -624,6 +728,7 @@ int tucker_free(tucker_handle* h) {
   if (h->st) cudaStreamSynchronize(h->st);
   const bool own = h->own_stream;
   cudaStream_t st = h->st;
+  if (h->comm) dist_comm_destroy(h->comm);
   delete h;
   if (own && st) cudaStreamDestroy(st);
   return TUCKER_OK;
@@ -744,6 +849,43 @@ int tucker_csf_stats(tucker_handle* h, int64_t* out) {
     out[4 * n + 1] = c.nnz;
     out[4 * n + 2] = c.nvfib;   // 0: no work plan (one CTA per slice)
     out[4 * n + 3] = c.nunits;
+  }
+  return TUCKER_OK;
+}
+
+int tucker_nccl_unique_id(void* id_out) {
+  if (!id_out) return TUCKER_E_ARG;
+  return guarded(nullptr, [&]() -> int {
+    dist_unique_id(id_out);
+    return TUCKER_OK;
+  });
+}
+
+int tucker_shard_bounds(const double* work, int64_t n, int world, int64_t* bounds) {
+  if (!bounds || world < 1 || n < 0 || (n > 0 && !work)) return TUCKER_E_ARG;
+  for (int64_t i = 0; i < n; ++i)
+    if (!(work[i] >= 0)) return TUCKER_E_ARG;
+  shard_bounds(work, n, world, bounds);
+  return TUCKER_OK;
+}
+
+int tucker_shard_info(tucker_handle* h, int64_t* out) {
+  if (!h || !out) return TUCKER_E_ARG;
+  const int N = h->order;
+  for (int n = 0; n < N; ++n) {
+    const Csf& c = *h->csfs[h->hooi_csf[n]];
+    out[2 * n] = h->sharded ? h->hooi_lo[n] : 0;
+    out[2 * n + 1] = h->sharded ? h->hooi_hi[n] : c.I_root;
+    for (int m = 0; m < N; ++m) {
+      int64_t* o = out + 2 * N + 2 * (n * N + m);
+      if (m == n) {
+        o[0] = o[1] = 0;
+        continue;
+      }
+      const Csf& t = *h->csfs[h->mp_csf[n][m]];
+      o[0] = h->sharded ? h->mp_lo[n][m] : 0;
+      o[1] = h->sharded ? h->mp_hi[n][m] : t.I_mid0 * t.I_mid1;
+    }
   }
   return TUCKER_OK;
 }
