@@ -203,6 +203,16 @@ int tucker_csf_stats(tucker_handle* h, int64_t* out);
  * view).  stats has 18 entries. */
 int tucker_stats(tucker_handle* h, int64_t* stats, int reset);
 
+/* The paper's stop rule (Eq. 10; MP: Appendix, NEXT 2 of
+ * SURVEY.md §8(f)): sweep from the factors in the handle until
+ * Delta_fit(t) = fit(t) - fit(t-1) < tol (fit(0) = 0; the paper uses 1e-4) or
+ * max_sweeps sweeps (the paper: 50).  fits: per-sweep fit (length max_sweeps,
+ * nullable); *sweeps_done (nullable) = sweeps run.  TUCKER_E_ARG on a null
+ * handle, max_sweeps < 1 or tol < 0; TUCKER_E_CONVERGE if some eigensolve did
+ * not reach its tolerance (the loop still completes).  Collective when sharded. */
+int hooi_run(tucker_handle* h, int max_sweeps, double tol, double* fits, int* sweeps_done);
+int mp_run(tucker_handle* h, int max_sweeps, double tol, double* fits, int* sweeps_done);
+
 /* A fresh 128-byte ncclUniqueId in id_out (caller-owned) for tucker_opts;
  * loads NCCL (libnccl.so.2) on demand.  TUCKER_E_NCCL if it cannot. */
 int tucker_nccl_unique_id(void* id_out);

@@ -25,7 +25,7 @@ EXPORTS = [
     "tucker_set_factors", "tucker_free", "tucker_strerror", "tucker_last_error",
     "tucker_debug_ttmc", "tucker_debug_gram", "tucker_debug_eig", "tucker_debug_smalldense",
     "tucker_debug_product", "tucker_debug_product_time", "tucker_csf_stats", "tucker_stats",
-    "tucker_nccl_unique_id", "tucker_shard_bounds", "tucker_shard_info",
+    "tucker_nccl_unique_id", "tucker_shard_bounds", "tucker_shard_info", "hooi_run", "mp_run",
 ]
 
 
@@ -65,6 +65,8 @@ def load(path: str = LIB_PATH) -> C.CDLL:
     lib.tucker_debug_product_time.argtypes = [C.c_int, C.c_int, C.c_int, C.POINTER(C.c_double)]
     lib.tucker_csf_stats.argtypes = [P, i64p]
     lib.tucker_nccl_unique_id.argtypes = [P]
+    lib.hooi_run.argtypes = [P, C.c_int, C.c_double, C.POINTER(C.c_double), C.POINTER(C.c_int)]
+    lib.mp_run.argtypes = [P, C.c_int, C.c_double, C.POINTER(C.c_double), C.POINTER(C.c_int)]
     lib.tucker_shard_bounds.argtypes = [C.POINTER(C.c_double), C.c_int64, C.c_int, i64p]
     lib.tucker_shard_info.argtypes = [P, i64p]
     lib.tucker_debug_smalldense.argtypes = [C.c_int, C.c_int, P, P, P, P, C.c_int, C.c_double]
@@ -273,6 +275,23 @@ def tucker_csf_fibers(h, order=3):
     return sum(st[0] for st in tucker_csf_stats(h, order))
 
 
+def _run(fn, h, max_sweeps, tol):
+    fits = np.zeros(max_sweeps, dtype=np.float64)
+    done = C.c_int(0)
+    rc = fn(h, max_sweeps, tol, fits.ctypes.data_as(C.POINTER(C.c_double)), C.byref(done))
+    _check(rc, h, allow=(E_CONVERGE,))
+    return fits[: done.value], rc
+
+
+def hooi_run(h, max_sweeps=50, tol=1e-4):
+    """Sweeps until Delta_fit < tol or max_sweeps (Eq. 10); returns (fits, rc)."""
+    return _run(lib().hooi_run, h, max_sweeps, tol)
+
+
+def mp_run(h, max_sweeps=50, tol=1e-4):
+    return _run(lib().mp_run, h, max_sweeps, tol)
+
+
 def nccl_unique_id():
     """A fresh 128-byte ncclUniqueId (bytes) for tucker_init(..., nccl_id=)."""
     buf = C.create_string_buffer(128)
@@ -337,6 +356,12 @@ class Tucker:
     def debug_ttmc(self, mode):
         P = int(np.prod([J for m, J in enumerate(self.core) if m != mode]))
         return tucker_debug_ttmc(self.h, mode, self.dims[mode], P)
+
+    def hooi_run(self, max_sweeps=50, tol=1e-4):
+        return hooi_run(self.h, max_sweeps, tol)[0]
+
+    def mp_run(self, max_sweeps=50, tol=1e-4):
+        return mp_run(self.h, max_sweeps, tol)[0]
 
     def shard_info(self):
         return tucker_shard_info(self.h, len(self.dims))

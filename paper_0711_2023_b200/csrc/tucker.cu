@@ -419,6 +419,30 @@ void make_shards(tucker_handle* h) {
   }
 }
 
+// The paper's stop rule (Eq. 10; MP: Appendix): sweep until
+// Delta_fit(t) = fit(t) - fit(t-1) < tol (fit(0) = 0) or max_sweeps sweeps,
+// from the factors currently in the handle.  fits[t] per sweep (length
+// max_sweeps, nullable); *sweeps_done = t.  An unconverged eigensolve is not
+// fatal here (reported as TUCKER_E_CONVERGE after the loop, like the sweeps).
+template <typename SweepFn>
+int run_until(tucker_handle* h, int max_sweeps, double tol, double* fits, int* sweeps_done, SweepFn sweep) {
+  if (!h || max_sweeps < 1 || !(tol >= 0)) return TUCKER_E_ARG;
+  double old = 0.0;
+  int t = 0, rc_all = TUCKER_OK;
+  while (t < max_sweeps) {
+    double fit = 0.0;
+    const int rc = sweep(h, &fit);
+    if (rc == TUCKER_E_CONVERGE) rc_all = rc;
+    else if (rc != TUCKER_OK) return rc;
+    if (fits) fits[t] = fit;
+    ++t;
+    if (fit - old < tol) break;
+    old = fit;
+  }
+  if (sweeps_done) *sweeps_done = t;
+  return rc_all;
+}
+
 int validate_factor(const float* U, int64_t I, int64_t J) {
   // max |U^T U - I| <= 1e-5 (host check on the caller's copy)
   std::vector<double> G((size_t)(J * J), 0.0);
@@ -691,6 +715,16 @@ int mp_sweep(tucker_handle* h, int sweeps, double* fit_per_sweep, float* stage_m
     }
     return h->eig_unconverged ? TUCKER_E_CONVERGE : TUCKER_OK;
   });
+}
+
+int hooi_run(tucker_handle* h, int max_sweeps, double tol, double* fits, int* sweeps_done) {
+  return run_until(h, max_sweeps, tol, fits, sweeps_done,
+                   [](tucker_handle* hh, double* f) { return hooi_sweep(hh, 1, f, nullptr); });
+}
+
+int mp_run(tucker_handle* h, int max_sweeps, double tol, double* fits, int* sweeps_done) {
+  return run_until(h, max_sweeps, tol, fits, sweeps_done,
+                   [](tucker_handle* hh, double* f) { return mp_sweep(hh, 1, f, nullptr); });
 }
 
 int core_and_fit(tucker_handle* h, float* core_out, float* const* U_out, double* fit_out) {

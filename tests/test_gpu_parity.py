@@ -253,3 +253,22 @@ def test_determinism(capi):
     np.testing.assert_array_equal(res[0][0], res[1][0])
     for a, b in zip(res[0][1], res[1][1]):
         np.testing.assert_array_equal(a, b)
+
+
+@pytest.mark.parametrize("algo", ["hooi", "mp"])
+def test_convergence_driver(capi, algo):
+    """hooi_run / mp_run (Eq. 10 stop rule, NEXT 2): the per-sweep fits match the
+    oracle's sweeps from the same U0, and the loop stops at the first sweep
+    whose Delta_fit < tol (tol chosen away from the measured increments)."""
+    dims, nnz, core = (100, 100, 100), 10_000, (10, 10, 10)
+    idx, vals, U0 = case(dims, nnz, core)
+    T = O.SparseTensor(dims, idx, vals)
+    ref = (O.run_hooi if algo == "hooi" else O.run_mp)(T, U0, core, 12)["fits"]
+    inc = np.diff(np.concatenate([[0.0], ref]))
+    # a tolerance below every earlier increment and above the stopping one
+    k = next(i for i in range(2, len(inc)) if inc[i] < 0.5 * inc[:i].min())
+    tol = float(np.sqrt(inc[k] * inc[:k].min()))
+    with capi.Tucker(dims, core, idx, vals, U0) as t:
+        fits = getattr(t, algo + "_run")(max_sweeps=50, tol=tol)
+    assert len(fits) == k + 1
+    assert np.max(np.abs(fits - ref[: k + 1])) < 1e-5
