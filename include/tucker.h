@@ -203,6 +203,17 @@ int tucker_csf_stats(tucker_handle* h, int64_t* out);
  * view).  stats has 18 entries. */
 int tucker_stats(tucker_handle* h, int64_t* stats, int reset);
 
+/* HO-SVD initialisation (NEXT 1 of SURVEY.md §8(f)): for every mode n with bit
+ * n of mode_mask set, U_n <- the J_n leading eigenvectors of X_(n) X_(n)^T
+ * (Fig. 2; HOOI's init of modes 2..N, Fig. 4; MP's pseudo
+ * HO-SVD (N-1) X_(n) X_(n)^T has the same eigenvectors, Fig. 7), sign-
+ * canonicalised, written into the handle's factors.  The sparse Gram is formed
+ * from the fibers of an ordering with leaf n (pairs sorted and reduced in a
+ * fixed order: deterministic).  TUCKER_E_ARG for bits >= order; TUCKER_E_OOM
+ * when a mode has more than 2^31 fiber pairs; TUCKER_E_CONVERGE as the sweeps.
+ * Collective when sharded (each rank a fiber range, S allreduced). */
+int tucker_hosvd(tucker_handle* h, unsigned mode_mask);
+
 /* The paper's stop rule (Eq. 10; MP: Appendix, NEXT 2 of
  * SURVEY.md §8(f)): sweep from the factors in the handle until
  * Delta_fit(t) = fit(t) - fit(t-1) < tol (fit(0) = 0; the paper uses 1e-4) or

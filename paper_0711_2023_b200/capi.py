@@ -26,6 +26,7 @@ EXPORTS = [
     "tucker_debug_ttmc", "tucker_debug_gram", "tucker_debug_eig", "tucker_debug_smalldense",
     "tucker_debug_product", "tucker_debug_product_time", "tucker_csf_stats", "tucker_stats",
     "tucker_nccl_unique_id", "tucker_shard_bounds", "tucker_shard_info", "hooi_run", "mp_run",
+    "tucker_hosvd",
 ]
 
 
@@ -65,6 +66,7 @@ def load(path: str = LIB_PATH) -> C.CDLL:
     lib.tucker_debug_product_time.argtypes = [C.c_int, C.c_int, C.c_int, C.POINTER(C.c_double)]
     lib.tucker_csf_stats.argtypes = [P, i64p]
     lib.tucker_nccl_unique_id.argtypes = [P]
+    lib.tucker_hosvd.argtypes = [P, C.c_uint]
     lib.hooi_run.argtypes = [P, C.c_int, C.c_double, C.POINTER(C.c_double), C.POINTER(C.c_int)]
     lib.mp_run.argtypes = [P, C.c_int, C.c_double, C.POINTER(C.c_double), C.POINTER(C.c_int)]
     lib.tucker_shard_bounds.argtypes = [C.POINTER(C.c_double), C.c_int64, C.c_int, i64p]
@@ -292,6 +294,11 @@ def mp_run(h, max_sweeps=50, tol=1e-4):
     return _run(lib().mp_run, h, max_sweeps, tol)
 
 
+def tucker_hosvd(h, mode_mask):
+    """U_n <- leading eigenvectors of X_(n) X_(n)^T for the modes in mode_mask."""
+    return _check(lib().tucker_hosvd(h, mode_mask), h, allow=(E_CONVERGE,))
+
+
 def nccl_unique_id():
     """A fresh 128-byte ncclUniqueId (bytes) for tucker_init(..., nccl_id=)."""
     buf = C.create_string_buffer(128)
@@ -356,6 +363,11 @@ class Tucker:
     def debug_ttmc(self, mode):
         P = int(np.prod([J for m, J in enumerate(self.core) if m != mode]))
         return tucker_debug_ttmc(self.h, mode, self.dims[mode], P)
+
+    def hosvd(self, modes=None):
+        """HO-SVD factors for `modes` (default all) into the handle."""
+        modes = range(len(self.dims)) if modes is None else modes
+        return tucker_hosvd(self.h, sum(1 << m for m in modes))
 
     def hooi_run(self, max_sweeps=50, tol=1e-4):
         return hooi_run(self.h, max_sweeps, tol)[0]

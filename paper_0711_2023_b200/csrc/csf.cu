@@ -311,3 +311,100 @@ void csf_build(const Coo& coo, Csf& c, int root, int mid0, int mid1, int leaf, c
 }
 
 }  // namespace tk
+
+namespace tk {
+
+// ---------------------------------------------------------------------------
+// Sparse Gram S = X_(n) X_(n)^T for HO-SVD (Fig. 2, Fig. 4)
+// and MP's pseudo HO-SVD (Fig. 7/8 P:921-937: (N-1) X_(n) X_(n)^T, the same
+// eigenvectors).  c is an ordering whose LEAF is mode n, so one fiber = one
+// column of X_(n) (all other indices fixed) with its leaf ids sorted.  Every
+// fiber emits its pairs (i_a <= i_b, x_a x_b); a stable radix sort by the key
+// i_a I + i_b and a reduce-by-key sum them in a fixed order (deterministic, no
+// atomics); both triangles of S are then written.  Fibers [f0, f1) only (a
+// rank's shard); S (fp64, row stride lds) must be zero beforehand.
+// ---------------------------------------------------------------------------
+namespace {
+
+__global__ void k_pair_count(const int32_t* __restrict__ fib_ptr, int64_t f0, int64_t nf,
+                             int64_t* __restrict__ cnt) {
+  for (int64_t f = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; f < nf; f += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t L = fib_ptr[f0 + f + 1] - fib_ptr[f0 + f];
+    cnt[f] = L * (L + 1) / 2;
+  }
+}
+
+// warp per fiber: pairs (a, b >= a) in row-major triangle order
+__global__ void k_pair_emit(const int32_t* __restrict__ fib_ptr, const int32_t* __restrict__ leaf,
+                            const float* __restrict__ val, int64_t f0, int64_t nf,
+                            const int64_t* __restrict__ off, int64_t I, int64_t* __restrict__ key,
+                            double* __restrict__ pv) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t f = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; f < nf; f += nw) {
+    const int64_t e0 = fib_ptr[f0 + f], L = fib_ptr[f0 + f + 1] - e0;
+    int64_t o = off[f];
+    for (int64_t a = 0; a < L; ++a) {
+      const int64_t ia = leaf[e0 + a];
+      const double xa = (double)val[e0 + a];
+      for (int64_t b = a + lane; b < L; b += 32) {
+        key[o + (b - a)] = ia * I + leaf[e0 + b];
+        pv[o + (b - a)] = xa * (double)val[e0 + b];
+      }
+      o += L - a;
+    }
+  }
+}
+
+__global__ void k_pair_scatter(const int64_t* __restrict__ ukey, const double* __restrict__ sum,
+                               const int* __restrict__ nruns, int64_t I, double* __restrict__ S,
+                               int64_t lds) {
+  const int64_t n = *nruns;
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n; r += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = ukey[r] / I, j = ukey[r] - i * I;
+    S[i * lds + j] = sum[r];
+    S[j * lds + i] = sum[r];
+  }
+}
+
+}  // namespace
+
+void sparse_gram(const Csf& c, int64_t f0, int64_t f1, double* S, int64_t lds, cudaStream_t st) {
+  const int64_t nf = f1 - f0, I = c.I_leaf;
+  if (nf <= 0) return;
+  DBuf<int64_t> cnt((size_t)nf + 1), off((size_t)nf + 1);
+  TK_CUDA(cudaMemsetAsync(cnt.p + nf, 0, sizeof(int64_t), st));
+  TK_LAUNCH(k_pair_count, grid_for(nf), 256, 0, st, c.fib_ptr.p, f0, nf, cnt.p);
+  DBuf<uint8_t> tmp;
+  size_t bytes = 0;
+  TK_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, bytes, cnt.p, off.p, nf + 1, st));
+  tmp.ensure(bytes);
+  TK_CUDA(cub::DeviceScan::ExclusiveSum(tmp.p, bytes, cnt.p, off.p, nf + 1, st));
+  int64_t P = 0;
+  TK_CUDA(cudaMemcpyAsync(&P, off.p + nf, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  TK_CUDA(cudaStreamSynchronize(st));
+  if (P > ((int64_t)1 << 31) - 1)
+    fail(TUCKER_E_OOM, "tucker_hosvd: X_(n) X_(n)^T has " + std::to_string(P) +
+                           " fiber pairs (> 2^31); dense-block sparse Gram not implemented");
+  DBuf<int64_t> key((size_t)P), key2((size_t)P), ukey((size_t)P);
+  DBuf<double> pv((size_t)P), pv2((size_t)P), sum((size_t)P);
+  DBuf<int> nruns(1);
+  TK_LAUNCH(k_pair_emit, grid_for(nf * 32), 256, 0, st, c.fib_ptr.p, c.leaf_id.p, c.val.p, f0, nf, off.p, I,
+            key.p, pv.p);
+  int bits = 1;
+  while (((int64_t)1 << bits) < I * I) ++bits;
+  bytes = 0;
+  TK_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, bytes, key.p, key2.p, pv.p, pv2.p, P, 0, bits, st));
+  tmp.ensure(bytes);
+  TK_CUDA(cub::DeviceRadixSort::SortPairs(tmp.p, bytes, key.p, key2.p, pv.p, pv2.p, P, 0, bits, st));
+  bytes = 0;
+  TK_CUDA(cub::DeviceReduce::ReduceByKey(nullptr, bytes, key2.p, ukey.p, pv2.p, sum.p, nruns.p,
+                                         cub::Sum(), P, st));
+  tmp.ensure(bytes);
+  TK_CUDA(cub::DeviceReduce::ReduceByKey(tmp.p, bytes, key2.p, ukey.p, pv2.p, sum.p, nruns.p, cub::Sum(),
+                                         P, st));
+  TK_LAUNCH(k_pair_scatter, grid_for(P), 256, 0, st, ukey.p, sum.p, nruns.p, I, S, lds);
+  TK_CUDA(cudaStreamSynchronize(st));  // the scratch buffers go out of scope
+}
+
+}  // namespace tk

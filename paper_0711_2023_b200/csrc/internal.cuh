@@ -55,6 +55,9 @@ struct Coo {  // validated, zero-free COO on the device
 void coo_validate_compact(Coo& coo, cudaStream_t st);          // E_INDEX / E_VALUE, drops zeros
 double coo_norm2(const Coo& coo, cudaStream_t st);              // ||X||_F^2 (fp64, fixed order)
 void csf_build(const Coo& coo, Csf& out, int root, int mid0, int mid1, int leaf, cudaStream_t st);
+// S += X_(n) X_(n)^T over the fibers [f0, f1) of an ordering whose leaf is n
+// (S fp64, row stride lds, zeroed by the caller; both triangles written)
+void sparse_gram(const Csf& c, int64_t f0, int64_t f1, double* S, int64_t lds, cudaStream_t st);
 // spttmc.cu: HOOI work units for an order-3 CSF whose output tile is Jm x Jl
 // (lo, hi): the rank's root-slice range (hi < 0: all)
 void spttmc_plan(Csf& c, int64_t Jm, int64_t Jl, int num_sms, cudaStream_t st, int64_t lo = 0, int64_t hi = -1);

@@ -887,6 +887,37 @@ int tucker_csf_stats(tucker_handle* h, int64_t* out) {
   return TUCKER_OK;
 }
 
+int tucker_hosvd(tucker_handle* h, unsigned mode_mask) {
+  if (!h || (mode_mask >> h->order) != 0) return TUCKER_E_ARG;
+  return guarded(h, [&]() -> int {
+    h->eig_unconverged = false;
+    for (int n = 0; n < h->order; ++n) {
+      if (!((mode_mask >> n) & 1u)) continue;
+      // an ordering with leaf n: each fiber is one column of X_(n)
+      const int r = (n + 1) % h->order;
+      const Csf& c = *h->csfs[h->mp_csf[r][n]];
+      const int64_t d = h->dims[n];
+      const int J = (int)h->J[n];
+      const int64_t lds = ensure_S(h, d);
+      TK_CUDA(cudaMemsetAsync(h->S.p, 0, (size_t)(d * lds) * sizeof(double), h->st));
+      int64_t f0 = 0, f1 = c.nfib;
+      if (h->sharded) {  // equal fiber ranges (work ~ pairs per fiber, uniform enough for a one-off)
+        f0 = c.nfib * h->opts.rank / h->opts.world;
+        f1 = c.nfib * (h->opts.rank + 1) / h->opts.world;
+      }
+      sparse_gram(c, f0, f1, h->S.p, lds, h->st);
+      if (h->sharded) dist_allreduce_f64(h->comm, h->S.p, d * lds, h->st);
+      h->scratch_slot.valid = false;
+      solve_eig(h, d, J, h->scratch_slot);
+      canon_to_f32(h->V.p, J, d, J, h->U[n].p, h->st);
+      TK_CUDA(cudaStreamSynchronize(h->st));
+      eig_check(h);
+    }
+    h->G_valid = false;
+    return h->eig_unconverged ? TUCKER_E_CONVERGE : TUCKER_OK;
+  });
+}
+
 int tucker_nccl_unique_id(void* id_out) {
   if (!id_out) return TUCKER_E_ARG;
   return guarded(nullptr, [&]() -> int {

@@ -1,0 +1,69 @@
+"""HO-SVD initialisation on the GPU (NEXT 1 of SURVEY.md §8(f); tucker_hosvd)
+and the paper's printed fits reproduced end to end through the C-ABI.
+
+* factors vs the oracle's hosvd_factor (X_(n) X_(n)^T by scipy.sparse, eigh):
+  projector distance <= 1e-4; the HO-SVD fit within 1e-5;
+* Tables 2 and 6 of the paper (250^3 and 100^4 at density 0.1, J = 25 and 20^4;
+  PAPER.md P:1244-1277; the golden file tests/golden/paper_fits.json): HO-SVD fit, HOOI from HO-SVD init
+  and MP from pseudo-HO-SVD init with the Delta_fit < 1e-4 rule (hooi_run /
+  mp_run) within the golden 0.02 percentage points of the printed numbers
+  (the CPU pin P12 holds the oracle to the same bar on the same tensor).
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+
+from oracle import tucker_oracle as O
+from synth import bernoulli_dense, random_orthonormal, uniform_distinct_coo
+
+pytestmark = pytest.mark.gpu
+HERE = os.path.dirname(os.path.abspath(__file__))
+
+
+@pytest.fixture(scope="module")
+def capi():
+    import __graft_entry__
+    __graft_entry__.build()
+    from paper_0711_2023_b200 import capi as c
+    return c
+
+
+@pytest.mark.parametrize("dims,nnz,core", [((100, 110, 120), 13_200, (10, 11, 12)),
+                                           ((20, 22, 18, 16), 12_000, (4, 5, 3, 6))])
+def test_hosvd_factors_and_fit(capi, dims, nnz, core):
+    idx, vals = uniform_distinct_coo(dims, nnz, np.random.default_rng(51))
+    U0 = [random_orthonormal(I, J, np.random.default_rng(52 + k)) for k, (I, J) in enumerate(zip(dims, core))]
+    T = O.SparseTensor(dims, idx, vals)
+    ref = O.run_hosvd(T, core)
+    with capi.Tucker(dims, core, idx, vals, U0) as t:
+        t.hosvd()
+        G, U, fit = t.core_and_fit()
+    for n in range(len(dims)):
+        assert O.projector_distance(U[n].astype(np.float64), ref["U"][n]) < 1e-4, n
+    assert abs(fit - ref["fit"]) < 1e-5
+
+
+@pytest.mark.parametrize("key", ["table2_250cube_J25", "table6_100pow4_J20"])
+def test_paper_fits_on_gpu(capi, key):
+    g = json.load(open(os.path.join(HERE, "golden", "paper_fits.json")))
+    case, tol = g[key], g["tolerance_pp"]
+    dims, core = tuple(case["dims"]), tuple(case["core"])
+    X = bernoulli_dense(dims, case["density"], np.random.default_rng(1))  # the P12 pin's tensor
+    nz = np.nonzero(X)
+    idx = [np.asarray(i, dtype=np.int32) for i in nz]
+    vals = X[nz].astype(np.float32)
+    U0 = [random_orthonormal(I, J, np.random.default_rng(60 + k)) for k, (I, J) in enumerate(zip(dims, core))]
+    with capi.Tucker(dims, core, idx, vals, U0) as t:
+        t.hosvd()
+        _, _, fit_hosvd = t.core_and_fit()
+        t.set_factors(U0)
+        t.hosvd(range(1, len(dims)))  # HOOI: HO-SVD of modes 2..N (U_1 is not used, Fig. 4)
+        fit_hooi = t.hooi_run(50, 1e-4)[-1]
+        t.set_factors(U0)
+        t.hosvd(range(1, len(dims)))  # MP: pseudo HO-SVD of modes 2..N (same eigenvectors)
+        fit_mp = t.mp_run(50, 1e-4)[-1]
+    assert abs(100 * fit_hosvd - case["hosvd"]) < tol, fit_hosvd
+    assert abs(100 * fit_hooi - case["hooi"]) < tol, fit_hooi
+    assert abs(100 * fit_mp - case["mp"]) < tol, fit_mp
