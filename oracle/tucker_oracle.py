@@ -261,6 +261,74 @@ def mp_sweep(T: SparseTensor, U, core, diag=None):
 
 
 # ---------------------------------------------------------------------------
+# Slice Projection (Figs. 5-6; Wang & Ahuja).  Mode n is updated from
+# ONE other factor, the previous mode's (cyclically: mode 1 from the last):
+#   order 3: M13 = sum_{i in mode 2} X_{:i:} C C^T X_{:i:}^T  -> A   (n=1, m=3)
+#            M21 = sum_{i in mode 3} X_{::i}^T A A^T X_{::i}  -> B   (n=2, m=1)
+#            M32 = sum_{i in mode 1} X_{i::}^T B B^T X_{i::}  -> C   (n=3, m=2)
+#   order 4: the same with slices fixing the two modes not in {n, m} (Fig. 6).
+# Each M is one term of MP's M_n (the slices fix every mode not in {n, m}).
+# ---------------------------------------------------------------------------
+
+
+def sp_gram(T: SparseTensor, U, n: int) -> np.ndarray:
+    """SP's M for mode n: sum over slices s fixing the modes not in {n, m},
+    m = n - 1 (cyclic), of (X_s U_m)(X_s U_m)^T (Figs. 5-6)."""
+    m = (n - 1) % T.N
+    W = mp_term_unfold(T, np.asarray(U[m], dtype=np.float64), n, m)
+    return W @ W.T
+
+
+def sp_sweep(T: SparseTensor, U, core, diag=None):
+    """One pass of Fig. 5/6's main loop: A(n) <- J_n leading eigenvectors of
+    M (reading A2: of M itself, not M M^T), freshest factors."""
+    U = [np.asarray(u, dtype=np.float64) for u in U]
+    for n in range(T.N):
+        U[n], w = leading_eigenvectors(sp_gram(T, U, n), core[n])
+        if diag is not None:
+            diag.append(dict(mode=n, **eig_diag(w, core[n])))
+    return U
+
+
+def sp_random_init(I: int, J: int, rng: np.random.Generator) -> np.ndarray:
+    """SP's initial last factor: uniform [0, 1] entries, columns
+    normalised to unit length (not orthonormalised)."""
+    C = rng.random((I, J))
+    return C / np.linalg.norm(C, axis=0, keepdims=True)
+
+
+def run_sp(T: SparseTensor, U0, core_dims, sweeps: int):
+    """Fixed-sweep SP from given factors (only the last one is used first)."""
+    U = [np.asarray(u, dtype=np.float64) for u in U0]
+    nx2 = T.norm2()
+    fits, gn = [], []
+    for _ in range(sweeps):
+        U = sp_sweep(T, U, core_dims)
+        G = core(T, U)
+        fits.append(fit_from_core(nx2, G))
+        gn.append(float(np.linalg.norm(G)))
+    return dict(U=U, fits=fits, gnorms=gn)
+
+
+def run_sp_converged(T: SparseTensor, core_dims, C0, tol=1e-4, maxit=50):
+    """The paper's SP: random-uniform last factor C0, main loop until
+    Delta_G(t) = 1 - ||G^(t-1)||_F / ||G^(t)||_F < tol or maxit (Eq. 11,
+    P:874-886); ||G^(0)|| = 0, so the first sweep never stops."""
+    U = [np.zeros((d, J)) for d, J in zip(T.dims, core_dims)]
+    U[-1] = np.asarray(C0, dtype=np.float64)
+    nx2 = T.norm2()
+    gprev, it, G = 0.0, 0, None
+    for it in range(1, maxit + 1):
+        U = sp_sweep(T, U, core_dims)
+        G = core(T, U)
+        g = float(np.linalg.norm(G))
+        if 1.0 - gprev / g < tol:
+            break
+        gprev = g
+    return dict(U=U, fit=fit_from_core(nx2, G), iters=it)
+
+
+# ---------------------------------------------------------------------------
 # Core and fit (Fig. 4 last step P:629-631, Appendix P:1861-1884, Eq. 9)
 # ---------------------------------------------------------------------------
 

@@ -346,3 +346,65 @@ def test_p12_table6_statistical_pin(golden_dir):
     core = tuple(case["core"])
     assert abs(100 * O.run_hooi_converged(T, core)["fit"] - case["hooi"]) < tol
     assert abs(100 * O.run_mp_converged(T, core)["fit"] - case["mp"]) < tol
+
+
+# ------------------------------------------------------ Slice Projection ----
+# Figs. 5-6 written out literally with dense slices, against the
+# oracle's sp_gram (which reuses MP's single-term unfolding): pins the mode
+# mapping (mode n from the previous mode's factor, slices on the remaining
+# modes) against the figures themselves.
+
+def test_sp_gram_matches_figure5_slice_loops():
+    rng = np.random.default_rng(71)
+    I1, I2, I3 = 5, 6, 7
+    X = rng.random((I1, I2, I3)) * (rng.random((I1, I2, I3)) < 0.5)
+    T = O.SparseTensor.from_dense(X)
+    A, B, C = rng.random((I1, 2)), rng.random((I2, 3)), rng.random((I3, 2))
+    U = [A, B, C]
+    M13 = sum(X[:, i, :] @ C @ C.T @ X[:, i, :].T for i in range(I2))       # slices on mode 2
+    M21 = sum(X[:, :, i].T @ A @ A.T @ X[:, :, i] for i in range(I3))       # slices on mode 3
+    M32 = sum(X[i, :, :].T @ B @ B.T @ X[i, :, :] for i in range(I1))       # slices on mode 1
+    for n, M in enumerate((M13, M21, M32)):
+        np.testing.assert_allclose(O.sp_gram(T, U, n), M, rtol=1e-12, atol=1e-12)
+
+
+def test_sp_gram_matches_figure6_slice_loops():
+    rng = np.random.default_rng(72)
+    d = (3, 4, 5, 3)
+    X = rng.random(d) * (rng.random(d) < 0.6)
+    T = O.SparseTensor.from_dense(X)
+    A, B, C, D = (rng.random((n, 2)) for n in d)
+    U = [A, B, C, D]
+    M14 = sum(X[:, i, j, :] @ D @ D.T @ X[:, i, j, :].T for i in range(d[1]) for j in range(d[2]))
+    M21 = sum(X[:, :, i, j].T @ A @ A.T @ X[:, :, i, j] for i in range(d[2]) for j in range(d[3]))
+    M32 = sum(X[i, :, :, j].T @ B @ B.T @ X[i, :, :, j] for i in range(d[0]) for j in range(d[3]))
+    M43 = sum(X[i, j, :, :].T @ C @ C.T @ X[i, j, :, :] for i in range(d[0]) for j in range(d[1]))
+    for n, M in enumerate((M14, M21, M32, M43)):
+        np.testing.assert_allclose(O.sp_gram(T, U, n), M, rtol=1e-12, atol=1e-12)
+
+
+def test_sp_exact_multilinear_rank_fit_one():
+    rng = np.random.default_rng(73)
+    dims, core = (12, 10, 9), (3, 2, 2)
+    G = rng.standard_normal(core)
+    Us = [np.linalg.qr(rng.standard_normal((I, J)))[0] for I, J in zip(dims, core)]
+    X = O.tucker_operator(G, Us)
+    T = O.SparseTensor.from_dense(X)
+    r = O.run_sp(T, [np.zeros((I, J)) for I, J in zip(dims[:-1], core[:-1])] +
+                 [O.sp_random_init(dims[-1], core[-1], rng)], core, 3)
+    # exact rank: the core keeps all of X (||G|| = ||X||); the fit's sqrt turns
+    # 1e-16 rounding of ||X||^2 - ||G||^2 into ~1e-8
+    assert abs(r["gnorms"][-1] / np.sqrt(T.norm2()) - 1.0) < 1e-12
+    assert abs(r["fits"][-1] - 1.0) < 1e-6
+    # Delta_G proxy (Eq. 11) is consistent: the core norm never decreases here
+    assert np.all(np.diff(r["gnorms"]) > -1e-12)
+
+
+@pytest.mark.slow
+def test_p12_table2_sp_statistical_pin(golden_dir):
+    """The paper's SP fit at 250^3 (Table 2: 3.934 %) from a random
+    uniform, column-normalised last factor, Delta_G < 1e-4 (Eq. 11)."""
+    T, case, tol = _paper_fit_case(golden_dir, "table2_250cube_J25", 1)
+    core = tuple(case["core"])
+    C0 = O.sp_random_init(T.dims[-1], core[-1], np.random.default_rng(7))
+    assert abs(100 * O.run_sp_converged(T, core, C0)["fit"] - case["sp"]) < tol
