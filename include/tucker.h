@@ -214,6 +214,22 @@ int tucker_stats(tucker_handle* h, int64_t* stats, int reset);
  * Collective when sharded (each rank a fiber range, S allreduced). */
 int tucker_hosvd(tucker_handle* h, unsigned mode_mask);
 
+/* Slice Projection (NEXT 3 of SURVEY.md §8(f); Figs. 5-6): one sweep
+ * updates U_n, n = 1..N, from the single multislice term of the previous
+ * mode's factor (m = n - 1, cyclic: U_1 from U_N), i.e. the J_n leading
+ * eigenvectors of sum_s (X_s U_m)(X_s U_m)^T over the slices s fixing the
+ * modes not in {n, m}; then the core.  fits / gnorms (nullable, length
+ * sweeps): fit and ||G||_F after each sweep.  Collective when sharded. */
+int sp_sweep(tucker_handle* h, int sweeps, double* fits, double* gnorms, float* stage_ms);
+/* SP until Delta_G(t) = 1 - ||G^(t-1)||_F / ||G^(t)||_F < tol (Eq. 11; the
+ * paper: 1e-4) or max_sweeps (50); as hooi_run otherwise. */
+int sp_run(tucker_handle* h, int max_sweeps, double tol, double* fits, int* sweeps_done);
+/* Replace factor n (I_n x J_n fp32 row-major, host or -- with
+ * TUCKER_INPUT_ON_DEVICE -- device).  check = 1: must be orthonormal
+ * (TUCKER_E_FACTOR); check = 0: any finite matrix, for SP's random-uniform
+ * column-normalised initial factor. */
+int tucker_set_factor(tucker_handle* h, int n, const float* U, int check);
+
 /* The paper's stop rule (Eq. 10; MP: Appendix, NEXT 2 of
  * SURVEY.md §8(f)): sweep from the factors in the handle until
  * Delta_fit(t) = fit(t) - fit(t-1) < tol (fit(0) = 0; the paper uses 1e-4) or

@@ -290,13 +290,6 @@ def sp_sweep(T: SparseTensor, U, core, diag=None):
     return U
 
 
-def sp_random_init(I: int, J: int, rng: np.random.Generator) -> np.ndarray:
-    """SP's initial last factor: uniform [0, 1] entries, columns
-    normalised to unit length (not orthonormalised)."""
-    C = rng.random((I, J))
-    return C / np.linalg.norm(C, axis=0, keepdims=True)
-
-
 def run_sp(T: SparseTensor, U0, core_dims, sweeps: int):
     """Fixed-sweep SP from given factors (only the last one is used first)."""
     U = [np.asarray(u, dtype=np.float64) for u in U0]

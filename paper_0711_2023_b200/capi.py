@@ -26,7 +26,7 @@ EXPORTS = [
     "tucker_debug_ttmc", "tucker_debug_gram", "tucker_debug_eig", "tucker_debug_smalldense",
     "tucker_debug_product", "tucker_debug_product_time", "tucker_csf_stats", "tucker_stats",
     "tucker_nccl_unique_id", "tucker_shard_bounds", "tucker_shard_info", "hooi_run", "mp_run",
-    "tucker_hosvd",
+    "tucker_hosvd", "sp_sweep", "sp_run", "tucker_set_factor",
 ]
 
 
@@ -67,6 +67,9 @@ def load(path: str = LIB_PATH) -> C.CDLL:
     lib.tucker_csf_stats.argtypes = [P, i64p]
     lib.tucker_nccl_unique_id.argtypes = [P]
     lib.tucker_hosvd.argtypes = [P, C.c_uint]
+    lib.sp_sweep.argtypes = [P, C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_double), C.POINTER(C.c_float)]
+    lib.sp_run.argtypes = [P, C.c_int, C.c_double, C.POINTER(C.c_double), C.POINTER(C.c_int)]
+    lib.tucker_set_factor.argtypes = [P, C.c_int, P, C.c_int]
     lib.hooi_run.argtypes = [P, C.c_int, C.c_double, C.POINTER(C.c_double), C.POINTER(C.c_int)]
     lib.mp_run.argtypes = [P, C.c_int, C.c_double, C.POINTER(C.c_double), C.POINTER(C.c_int)]
     lib.tucker_shard_bounds.argtypes = [C.POINTER(C.c_double), C.c_int64, C.c_int, i64p]
@@ -299,6 +302,26 @@ def tucker_hosvd(h, mode_mask):
     return _check(lib().tucker_hosvd(h, mode_mask), h, allow=(E_CONVERGE,))
 
 
+def sp_sweep(h, sweeps):
+    """Slice Projection sweeps -> (fits, core norms, rc)."""
+    fits = np.zeros(sweeps, dtype=np.float64)
+    gn = np.zeros(sweeps, dtype=np.float64)
+    rc = lib().sp_sweep(h, sweeps, fits.ctypes.data_as(C.POINTER(C.c_double)),
+                        gn.ctypes.data_as(C.POINTER(C.c_double)), None)
+    _check(rc, h, allow=(E_CONVERGE,))
+    return fits, gn, rc
+
+
+def sp_run(h, max_sweeps=50, tol=1e-4):
+    return _run(lib().sp_run, h, max_sweeps, tol)
+
+
+def tucker_set_factor(h, n, U, check=True):
+    if not hasattr(U, "data_ptr"):
+        U = np.ascontiguousarray(U, dtype=np.float32)
+    _check(lib().tucker_set_factor(h, n, C.c_void_p(_ptr(U)), 1 if check else 0), h)
+
+
 def nccl_unique_id():
     """A fresh 128-byte ncclUniqueId (bytes) for tucker_init(..., nccl_id=)."""
     buf = C.create_string_buffer(128)
@@ -363,6 +386,15 @@ class Tucker:
     def debug_ttmc(self, mode):
         P = int(np.prod([J for m, J in enumerate(self.core) if m != mode]))
         return tucker_debug_ttmc(self.h, mode, self.dims[mode], P)
+
+    def sp_sweep(self, sweeps):
+        return sp_sweep(self.h, sweeps)
+
+    def sp_run(self, max_sweeps=50, tol=1e-4):
+        return sp_run(self.h, max_sweeps, tol)[0]
+
+    def set_factor(self, n, U, check=True):
+        tucker_set_factor(self.h, n, U, check)
 
     def hosvd(self, modes=None):
         """HO-SVD factors for `modes` (default all) into the handle."""

@@ -34,7 +34,8 @@ struct tucker_handle {
   DBuf<double> S, V, Ufull, G64, scal;
   DBuf<float> G32, Ytmp;
   bool G_valid = false;
-  EigSlot slots[2][kMaxOrder];
+  EigSlot slots[3][kMaxOrder];  // warm starts: [0] HOOI, [1] MP, [2] SP
+  double last_g2 = 0;           // ||G||_F^2 of the last core (SP's Delta_G rule)
   DBuf<double> theta_d;
   DBuf<int> info_d;
   EigSlot* last_slot = nullptr;
@@ -190,7 +191,8 @@ void project_hooi(tucker_handle* h, int n, bool transposed) {
 }
 
 // W_n = [ (X x_m U_m^T)_(n) ]_{m != n} into h->Whi/Wlo; returns the split view
-Split build_mp_w(tucker_handle* h, int n) {
+// only_m >= 0: the single term m (Slice Projection, Figs. 5-6)
+Split build_mp_w(tucker_handle* h, int n, int only_m = -1) {
   // sharded: this rank's slices [mp_lo, mp_hi) of every term, columns compacted
   auto slices = [&](int m, const Csf& c, int64_t& lo, int64_t& hi) {
     lo = h->sharded ? h->mp_lo[n][m] : 0;
@@ -198,7 +200,7 @@ Split build_mp_w(tucker_handle* h, int n) {
   };
   int64_t K = 0;
   for (int m = 0; m < h->order; ++m) {
-    if (m == n) continue;
+    if (m == n || (only_m >= 0 && m != only_m)) continue;
     const Csf& c = *h->csfs[h->mp_csf[n][m]];
     int64_t lo, hi;
     slices(m, c, lo, hi);
@@ -232,7 +234,7 @@ Split build_mp_w(tucker_handle* h, int n) {
   W.ld = ld;
   int64_t off = 0;
   for (int m = 0; m < h->order; ++m) {
-    if (m == n) continue;
+    if (m == n || (only_m >= 0 && m != only_m)) continue;
     const Csf& c = *h->csfs[h->mp_csf[n][m]];
     int64_t lo, hi;
     slices(m, c, lo, hi);
@@ -356,6 +358,7 @@ double core_from_y(tucker_handle* h) {
   TK_CUDA(cudaMemcpyAsync(out, h->scal.p, 2 * sizeof(double), cudaMemcpyDeviceToHost, h->st));
   TK_CUDA(cudaStreamSynchronize(h->st));
   h->G_valid = true;
+  h->last_g2 = out[0];
   return out[1];
 }
 
@@ -725,6 +728,92 @@ int hooi_run(tucker_handle* h, int max_sweeps, double tol, double* fits, int* sw
 int mp_run(tucker_handle* h, int max_sweeps, double tol, double* fits, int* sweeps_done) {
   return run_until(h, max_sweeps, tol, fits, sweeps_done,
                    [](tucker_handle* hh, double* f) { return mp_sweep(hh, 1, f, nullptr); });
+}
+
+// Slice Projection (Figs. 5-6): mode n from the single MP term
+// m = n - 1 (cyclic); after every sweep the core and fit (fits[s]) and the core
+// norm (gnorms[s], for Delta_G, Eq. 11) -- both nullable.
+int sp_sweep(tucker_handle* h, int sweeps, double* fits, double* gnorms, float* stage_ms) {
+  if (!h || sweeps < 1) return TUCKER_E_ARG;
+  return guarded(h, [&]() -> int {
+    h->eig_unconverged = false;
+    for (int s = 0; s < sweeps; ++s) {
+      float ms[4] = {0, 0, 0, 0};
+      for (int n = 0; n < h->order; ++n) {
+        cudaEvent_t a, b;
+        TK_CUDA(cudaEventCreate(&a));
+        TK_CUDA(cudaEventCreate(&b));
+        TK_CUDA(cudaEventRecord(a, h->st));
+        Split W = build_mp_w(h, n, (n + h->order - 1) % h->order);
+        TK_CUDA(cudaEventRecord(b, h->st));
+        TK_CUDA(cudaEventSynchronize(b));
+        float t = 0;
+        TK_CUDA(cudaEventElapsedTime(&t, a, b));
+        ms[0] += t;
+        cudaEventDestroy(a);
+        cudaEventDestroy(b);
+        update_factor(h, n, W, false, h->slots[2][n], &ms[1], &ms[2], h->sharded);
+      }
+      cudaEvent_t a, b;
+      TK_CUDA(cudaEventCreate(&a));
+      TK_CUDA(cudaEventCreate(&b));
+      TK_CUDA(cudaEventRecord(a, h->st));
+      const double fit = compute_core(h);
+      TK_CUDA(cudaEventRecord(b, h->st));
+      TK_CUDA(cudaEventSynchronize(b));
+      float t = 0;
+      TK_CUDA(cudaEventElapsedTime(&t, a, b));
+      ms[3] += t;
+      cudaEventDestroy(a);
+      cudaEventDestroy(b);
+      if (fits) fits[s] = fit;
+      if (gnorms) gnorms[s] = std::sqrt(h->last_g2);
+      if (stage_ms)
+        for (int q = 0; q < 4; ++q) stage_ms[4 * s + q] = ms[q];
+    }
+    return h->eig_unconverged ? TUCKER_E_CONVERGE : TUCKER_OK;
+  });
+}
+
+// SP's stop rule (Eq. 11): Delta_G(t) = 1 - ||G^(t-1)|| / ||G^(t)|| < tol
+// (||G^(0)|| = 0) or max_sweeps; fits[t] per sweep.
+int sp_run(tucker_handle* h, int max_sweeps, double tol, double* fits, int* sweeps_done) {
+  if (!h || max_sweeps < 1 || !(tol >= 0)) return TUCKER_E_ARG;
+  double gprev = 0.0;
+  int t = 0, rc_all = TUCKER_OK;
+  while (t < max_sweeps) {
+    double fit = 0.0, g = 0.0;
+    const int rc = sp_sweep(h, 1, &fit, &g, nullptr);
+    if (rc == TUCKER_E_CONVERGE) rc_all = rc;
+    else if (rc != TUCKER_OK) return rc;
+    if (fits) fits[t] = fit;
+    ++t;
+    if (g > 0 && 1.0 - gprev / g < tol) break;
+    gprev = g;
+  }
+  if (sweeps_done) *sweeps_done = t;
+  return rc_all;
+}
+
+int tucker_set_factor(tucker_handle* h, int n, const float* U, int check) {
+  if (!h || !U || n < 0 || n >= h->order) return TUCKER_E_ARG;
+  const bool on_dev = (h->opts.flags & TUCKER_INPUT_ON_DEVICE) != 0;
+  if (!on_dev) {
+    if (check) {
+      const int rc = validate_factor(U, h->dims[n], h->J[n]);
+      if (rc) return rc;
+    } else {
+      for (int64_t i = 0; i < h->dims[n] * h->J[n]; ++i)
+        if (!std::isfinite(U[i])) return TUCKER_E_FACTOR;
+    }
+  }
+  return guarded(h, [&]() -> int {
+    TK_CUDA(cudaMemcpyAsync(h->U[n].p, U, h->dims[n] * h->J[n] * sizeof(float),
+                            on_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, h->st));
+    TK_CUDA(cudaStreamSynchronize(h->st));
+    h->G_valid = false;
+    return TUCKER_OK;
+  });
 }
 
 int core_and_fit(tucker_handle* h, float* core_out, float* const* U_out, double* fit_out) {

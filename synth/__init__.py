@@ -17,6 +17,7 @@ from .generators import (  # noqa: F401
     bernoulli_coo,
     make_config,
     random_orthonormal,
+    sp_random_init,
     uniform_distinct_coo,
     zipf_coo,
 )

@@ -185,6 +185,14 @@ def random_orthonormal(I: int, J: int, rng: np.random.Generator) -> np.ndarray:
     return np.ascontiguousarray(Q.astype(np.float32))
 
 
+def sp_random_init(I: int, J: int, rng: np.random.Generator) -> np.ndarray:
+    """Slice Projection's initial last factor: uniform [0, 1]
+    entries, columns normalised to unit length (not orthonormalised).  An input
+    draw shared by the oracle and the CUDA path (fp64; cast for the GPU)."""
+    C = rng.random((I, J))
+    return C / np.linalg.norm(C, axis=0, keepdims=True)
+
+
 def make_config(k: int, *, nnz: int | None = None, dims=None, core=None, device=None):
     """Materialise BASELINE.json config `k` (optionally resized for tests).
 

@@ -12,7 +12,7 @@ import numpy as np
 import pytest
 
 from oracle import tucker_oracle as O
-from synth import bernoulli_dense
+from synth import bernoulli_dense, sp_random_init
 
 
 def rng(s=0):
@@ -391,7 +391,7 @@ def test_sp_exact_multilinear_rank_fit_one():
     X = O.tucker_operator(G, Us)
     T = O.SparseTensor.from_dense(X)
     r = O.run_sp(T, [np.zeros((I, J)) for I, J in zip(dims[:-1], core[:-1])] +
-                 [O.sp_random_init(dims[-1], core[-1], rng)], core, 3)
+                 [sp_random_init(dims[-1], core[-1], rng)], core, 3)
     # exact rank: the core keeps all of X (||G|| = ||X||); the fit's sqrt turns
     # 1e-16 rounding of ||X||^2 - ||G||^2 into ~1e-8
     assert abs(r["gnorms"][-1] / np.sqrt(T.norm2()) - 1.0) < 1e-12
@@ -406,5 +406,5 @@ def test_p12_table2_sp_statistical_pin(golden_dir):
     uniform, column-normalised last factor, Delta_G < 1e-4 (Eq. 11)."""
     T, case, tol = _paper_fit_case(golden_dir, "table2_250cube_J25", 1)
     core = tuple(case["core"])
-    C0 = O.sp_random_init(T.dims[-1], core[-1], np.random.default_rng(7))
+    C0 = sp_random_init(T.dims[-1], core[-1], np.random.default_rng(7))
     assert abs(100 * O.run_sp_converged(T, core, C0)["fit"] - case["sp"]) < tol
