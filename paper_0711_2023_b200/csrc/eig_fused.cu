@@ -390,28 +390,31 @@ __device__ void matvec(const Ctx& x, double* mpart, const double* S, const doubl
   long long t1 = mvt ? gtimer() : 0;
   gsync();
   long long t2 = mvt ? gtimer() : 0;
-  // phase B: own rows
-  for (int r = x.r0 + x.warp; r < x.r1; r += NW)
-    for (int c = x.lane; c < n; c += 32) {
-      double sum = 0.0;
-      const double* pp0 = mpart + (size_t)r * LB + c;
-      const size_t pstr = (size_t)RPX * LB;
-      int q = 0;
-      for (; q + 4 <= pl.KB; q += 4) {  // 4 loads in flight, summed in order
-        const double v0 = __ldcg(pp0 + q * pstr), v1 = __ldcg(pp0 + (q + 1) * pstr);
-        const double v2 = __ldcg(pp0 + (q + 2) * pstr), v3 = __ldcg(pp0 + (q + 3) * pstr);
-        sum += v0;
-        sum += v1;
-        sum += v2;
-        sum += v3;
-      }
-      for (; q < pl.KB; ++q) sum += __ldcg(pp0 + q * pstr);
-      const int64_t o = (int64_t)r * LB + c;
-      double v = alpha * sum;
-      if (gamma != 0.0) v += gamma * Dm[o];
-      if (delta != 0.0) v += delta * Em[o];
-      Out[o] = v;
+  // phase B: own rows; the (row, column) items are spread over all threads
+  // (a CTA owns ~d/G rows, fewer than its warps) with 8 partial loads in flight
+  const int nrow = x.r1 - x.r0;
+  const size_t pstr = (size_t)RPX * LB;
+  for (int it = x.tid; it < nrow * n; it += NT) {
+    const int rr = it / n, c = it - rr * n;
+    const int r = x.r0 + rr;
+    const double* pp0 = mpart + (size_t)r * LB + c;
+    const int64_t o = (int64_t)r * LB + c;
+    const double dv = gamma != 0.0 ? Dm[o] : 0.0, ev = delta != 0.0 ? Em[o] : 0.0;
+    double sum = 0.0;
+    int q = 0;
+    for (; q + 8 <= pl.KB; q += 8) {  // summed in order
+      double v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = __ldcg(pp0 + (q + u) * pstr);
+#pragma unroll
+      for (int u = 0; u < 8; ++u) sum += v[u];
     }
+    for (; q < pl.KB; ++q) sum += __ldcg(pp0 + q * pstr);
+    double val = alpha * sum;
+    if (gamma != 0.0) val += gamma * dv;
+    if (delta != 0.0) val += delta * ev;
+    Out[o] = val;
+  }
   __syncthreads();  // own rows of Out complete for any thread mapping
   if (mvt) {
     const long long t3 = gtimer();
@@ -551,26 +554,28 @@ __device__ void reduce_bcast(const Ctx& x, const double* part, int E, int nb, do
   gsync();
   const int per = (E + x.G - 1) / x.G;
   const int e0 = x.cta * per, e1 = min(E, e0 + per);
-  // 8 threads per entry, each a strided subset of the partials (4 loads in flight),
-  // combined by shuffles in a fixed pattern
-  for (int base = e0; base < e1; base += NT / 8) {
-    const int e = base + x.tid / 8, sub = x.tid % 8;
+  // tpe threads per entry (the largest power of two <= 32 that keeps the CTA's
+  // entries in one pass), each a strided subset of the partials with 8 loads in
+  // flight, combined by shuffles in a fixed pattern (depends on E and G only:
+  // deterministic)
+  int tpe = 32;
+  while (tpe > 1 && tpe * per > NT) tpe >>= 1;
+  for (int base = e0; base < e1; base += NT / tpe) {
+    const int e = base + x.tid / tpe, sub = x.tid % tpe;
     double s = 0.0;
     if (e < e1) {
-      int z = sub;
-      for (; z + 24 < x.G; z += 32) {
-        const double v0 = __ldcg(part + (size_t)z * E + e), v1 = __ldcg(part + (size_t)(z + 8) * E + e);
-        const double v2 = __ldcg(part + (size_t)(z + 16) * E + e), v3 = __ldcg(part + (size_t)(z + 24) * E + e);
-        s += v0;
-        s += v1;
-        s += v2;
-        s += v3;
+      for (int z0 = sub; z0 < x.G; z0 += 8 * tpe) {
+        double v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int z = z0 + u * tpe;
+          v[u] = z < x.G ? __ldcg(part + (size_t)z * E + e) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) s += v[u];
       }
-      for (; z < x.G; z += 8) s += __ldcg(part + (size_t)z * E + e);
     }
-    s += __shfl_xor_sync(0xffffffffu, s, 1);
-    s += __shfl_xor_sync(0xffffffffu, s, 2);
-    s += __shfl_xor_sync(0xffffffffu, s, 4);
+    for (int o = 1; o < tpe; o <<= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
     if (e < e1 && sub == 0) red[e] = s;
   }
   gsync();
