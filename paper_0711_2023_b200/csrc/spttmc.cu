@@ -683,37 +683,40 @@ struct SpmmArgs {
   int64_t s_lo, s_hi, s_all;  // slices (mid index) of this rank of s_all; W columns start at col_off for s_lo
 };
 
-template <int QL>
+// GL lanes per fiber (GL = 8/16/32 by J: several fibers per warp, so the
+// dependent fib_ptr -> leaf -> U-row chains of short fibers overlap), QL row
+// elements per lane, two nonzeros in flight.
+template <int GL, int QL>
 __global__ void __launch_bounds__(256) k_spmm_mp(SpmmArgs p) {
-  const int lane = threadIdx.x & 31;
-  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t f = warp; f < p.nfib; f += nwarps) {
-    if (p.s_lo > 0 || p.s_hi < p.s_all) {  // sharded: skip other ranks' slices before any leaf work
-      int64_t mk = __ldg(p.fib_mid0 + f);
-      if (p.fib_mid1) mk = mk * p.I_mid1 + __ldg(p.fib_mid1 + f);
-      if (mk < p.s_lo || mk >= p.s_hi) continue;
-    }
+  const int gl = threadIdx.x & (GL - 1);
+  const int64_t grp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / GL;
+  const int64_t ngrp = ((int64_t)gridDim.x * blockDim.x) / GL;
+  const bool sharded = p.s_lo > 0 || p.s_hi < p.s_all;
+  for (int64_t f = grp; f < p.nfib; f += ngrp) {
+    int64_t mk = __ldg(p.fib_mid0 + f);
+    if (p.fib_mid1) mk = mk * p.I_mid1 + __ldg(p.fib_mid1 + f);
+    const int64_t root = __ldg(p.fib_root + f);
     const int e0 = __ldg(p.fib_ptr + f), e1 = __ldg(p.fib_ptr + f + 1);
+    if (sharded && (mk < p.s_lo || mk >= p.s_hi)) continue;  // another rank's slice
     float t[QL];
 #pragma unroll
     for (int q = 0; q < QL; ++q) t[q] = 0.f;
-    for (int e = e0; e < e1; ++e) {
-      const float x = __ldg(p.val + e);
-      const float* r = p.U + (int64_t)__ldg(p.leaf_id + e) * p.J;
+    for (int e = e0; e < e1; e += 2) {
+      const bool two = e + 1 < e1;
+      const float x0 = __ldg(p.val + e), x1 = two ? __ldg(p.val + e + 1) : 0.f;
+      const int l0 = __ldg(p.leaf_id + e), l1 = two ? __ldg(p.leaf_id + e + 1) : l0;
+      const float* r0 = p.U + (int64_t)l0 * p.J;
+      const float* r1 = p.U + (int64_t)l1 * p.J;
 #pragma unroll
       for (int q = 0; q < QL; ++q) {
-        const int j = lane + 32 * q;
-        if (j < p.J) t[q] += x * __ldg(r + j);
+        const int j = gl + GL * q;
+        if (j < p.J) t[q] += x0 * __ldg(r0 + j) + x1 * __ldg(r1 + j);
       }
     }
-    int64_t mk = __ldg(p.fib_mid0 + f);
-    if (p.fib_mid1) mk = mk * p.I_mid1 + __ldg(p.fib_mid1 + f);
-    if (mk < p.s_lo || mk >= p.s_hi) continue;  // another rank's slice
-    const int64_t base = (int64_t)__ldg(p.fib_root + f) * p.ldW + p.col_off + (mk - p.s_lo) * p.J;
+    const int64_t base = root * p.ldW + p.col_off + (mk - p.s_lo) * p.J;
 #pragma unroll
     for (int q = 0; q < QL; ++q) {
-      const int j = lane + 32 * q;
+      const int j = gl + GL * q;
       if (j < p.J) split_store(p.Whi, p.Wlo, base + j, t[q]);
     }
   }
@@ -980,10 +983,10 @@ void spmm_mp(const Csf& c, const float* U_leaf, int64_t J_leaf, Split out, int64
   a.ldW = out.ld;
   a.col_off = col_off;
   const int64_t blocks = std::min<int64_t>(ceil_div(c.nfib, 8), 148 * 32);
-  const int QL = (int)ceil_div(J_leaf, 32);
-  if (QL <= 1) TK_LAUNCH((k_spmm_mp<1>), (unsigned)blocks, 256, 0, st, a);
-  else if (QL <= 2) TK_LAUNCH((k_spmm_mp<2>), (unsigned)blocks, 256, 0, st, a);
-  else TK_LAUNCH((k_spmm_mp<4>), (unsigned)blocks, 256, 0, st, a);
+  if (J_leaf <= 8) TK_LAUNCH((k_spmm_mp<8, 1>), (unsigned)blocks, 256, 0, st, a);
+  else if (J_leaf <= 32) TK_LAUNCH((k_spmm_mp<16, 2>), (unsigned)blocks, 256, 0, st, a);
+  else if (J_leaf <= 64) TK_LAUNCH((k_spmm_mp<16, 4>), (unsigned)blocks, 256, 0, st, a);
+  else TK_LAUNCH((k_spmm_mp<32, 4>), (unsigned)blocks, 256, 0, st, a);
 }
 
 }  // namespace tk
