@@ -94,17 +94,38 @@ __global__ void __launch_bounds__(256) k_syrk_dmma(const float* __restrict__ hi,
   const float* lA = lo + (int64_t)bij.x * DT * lda;
   const float* hB = hi + (int64_t)bij.y * DT * lda;
   const float* lB = lo + (int64_t)bij.y * DT * lda;
-  for (int ch = z; ch < nchunks; ch += splits) {
+  // the next chunk's operands are prefetched into registers while the
+  // current chunk's DMMAs run (one smem buffer); diagonal tiles load A only
+  const bool diag = bij.x == bij.y;
+  constexpr int PER = DT * DKC / 256;  // elements per thread per operand (8)
+  float pah[PER], pal[PER], pbh[PER], pbl[PER];
+  auto gload = [&](int ch) {
     const int k0 = ch * DKC;
-    for (int e = threadIdx.x; e < DT * DKC; e += 256) {
-      const int r = e >> 5, kk = e & 31;
+#pragma unroll
+    for (int u = 0; u < PER; ++u) {
+      const int e = threadIdx.x + 256 * u, r = e >> 5, kk = e & 31;
       const int64_t o = (int64_t)r * lda + k0 + kk;
-      As[r * DSP + kk] = (double)__ldg(hA + o) + (double)__ldg(lA + o);
-      Bs[r * DSP + kk] = (double)__ldg(hB + o) + (double)__ldg(lB + o);
+      pah[u] = __ldg(hA + o);
+      pal[u] = __ldg(lA + o);
+      if (!diag) {
+        pbh[u] = __ldg(hB + o);
+        pbl[u] = __ldg(lB + o);
+      }
+    }
+  };
+  if (z < nchunks) gload(z);
+  const double* Bsrc = diag ? As : Bs;
+  for (int ch = z; ch < nchunks; ch += splits) {
+#pragma unroll
+    for (int u = 0; u < PER; ++u) {
+      const int e = threadIdx.x + 256 * u, r = e >> 5, kk = e & 31;
+      As[r * DSP + kk] = (double)pah[u] + (double)pal[u];
+      if (!diag) Bs[r * DSP + kk] = (double)pbh[u] + (double)pbl[u];
     }
     __syncthreads();
+    if (ch + splits < nchunks) gload(ch + splits);
     const double* ap = As + (8 * warp + ar) * DSP + aq;
-    const double* bp = Bs + ar * DSP + aq;
+    const double* bp = Bsrc + ar * DSP + aq;
 #pragma unroll
     for (int kb = 0; kb < DKC; kb += 4) {
       const double a = ap[kb];
