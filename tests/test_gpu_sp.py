@@ -73,3 +73,27 @@ def test_paper_sp_fit_on_gpu(capi, key):
         t.set_factor(len(dims) - 1, C0, check=False)
         fits = t.sp_run(50, 1e-4)
     assert abs(100 * fits[-1] - case["sp"]) < tol, (fits[-1], len(fits))
+
+
+def test_hosvd_and_sp_bitwise_deterministic(capi):
+    """Same inputs -> bit-identical factors, core and fits: the
+    sparse Gram's pair sort + reduce-by-key and SP's single-term Gram have no
+    atomics."""
+    dims, core = (60, 70, 80), (6, 7, 8)
+    idx, vals = uniform_distinct_coo(dims, 20_000, np.random.default_rng(91))
+    U0 = [random_orthonormal(I, J, np.random.default_rng(92 + k)) for k, (I, J) in enumerate(zip(dims, core))]
+    C0 = sp_random_init(dims[-1], core[-1], np.random.default_rng(93)).astype(np.float32)
+    outs = []
+    for _ in range(2):
+        with capi.Tucker(dims, core, idx, vals, U0) as t:
+            t.hosvd()
+            Gh, Uh, fh = t.core_and_fit()
+            t.set_factor(len(dims) - 1, C0, check=False)
+            fits, gn, _ = t.sp_sweep(2)
+            Gs, Us, fs = t.core_and_fit()
+        outs.append((Gh, Uh, fh, fits, gn, Gs, Us, fs))
+    for x, y in zip(*outs):
+        if isinstance(x, list):
+            assert all(np.array_equal(u, v) for u, v in zip(x, y))
+        else:
+            assert np.array_equal(np.asarray(x), np.asarray(y))
