@@ -609,7 +609,9 @@ struct Ttmc4Args {
   int64_t ldY;
   int transposed;
   int64_t s0, s1, sb;  // Kolda strides of (mid0, mid1, leaf) indices
-  int slice0;          // first slice of this launch (rank shard)
+  int slice0;          // first slice of this launch (rank shard) when unit == null
+  const int32_t* unit; // work units (slice, node0, node1, slot) or null: one CTA per slice
+  float* part;         // partial rows of split slices (J0 J1 Jl floats per slot)
 };
 
 template <int RA, int RB, int RQ>
@@ -619,8 +621,18 @@ __global__ void __launch_bounds__(256) k_spttmc4(Ttmc4Args p) {
   __shared__ __align__(16) float M[kFC * JMP];
   __shared__ float Zs[JMP * JLP];
   __shared__ float u0[128];
-  const int i = p.slice0 + blockIdx.x;
-  const int n0 = p.slice_ptr[i], n1 = p.slice_ptr[i + 1];
+  int i, n0, n1, slot = -1;
+  if (p.unit) {
+    const int4 u = reinterpret_cast<const int4*>(p.unit)[blockIdx.x];
+    i = u.x;
+    n0 = u.y;
+    n1 = u.z;
+    slot = u.w;
+  } else {
+    i = p.slice0 + blockIdx.x;
+    n0 = p.slice_ptr[i];
+    n1 = p.slice_ptr[i + 1];
+  }
   const int P1 = p.J1 * p.Jl;
   const int P = p.J0 * P1;
   float y[RQ];
@@ -663,6 +675,10 @@ __global__ void __launch_bounds__(256) k_spttmc4(Ttmc4Args p) {
   for (int q = 0; q < RQ; ++q) {
     const int c = threadIdx.x + 256 * q;
     if (c < P) {
+      if (slot >= 0) {
+        p.part[(int64_t)slot * P + c] = y[q];
+        continue;
+      }
       const int a0 = c / P1, rest = c % P1;
       const int a1 = rest / p.Jl, b = rest % p.Jl;
       const int64_t col = a0 * p.s0 + a1 * p.s1 + b * p.sb;
@@ -670,6 +686,25 @@ __global__ void __launch_bounds__(256) k_spttmc4(Ttmc4Args p) {
       split_store(p.Yhi, p.Ylo, off, y[q]);
     }
   }
+}
+
+// order 4: Y row of a split slice = sum of its units' partial rows, in slot order
+__global__ void __launch_bounds__(256) k_spttmc4_reduce(const int32_t* __restrict__ red,
+                                                        const float* __restrict__ part, int J0, int J1, int Jl,
+                                                        int64_t s0, int64_t s1, int64_t sb, float* Yhi,
+                                                        float* Ylo, int64_t ldY, int transposed) {
+  const int r = blockIdx.y;
+  const int i = red[3 * r], q0 = red[3 * r + 1], nq = red[3 * r + 2];
+  const int P1 = J1 * Jl, P = J0 * P1;
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= P) return;
+  float y = 0.f;
+  for (int q = 0; q < nq; ++q) y += __ldcs(part + (int64_t)(q0 + q) * P + c);
+  const int a0 = c / P1, rest = c - a0 * P1;
+  const int a1 = rest / Jl, b = rest - a1 * Jl;
+  const int64_t col = a0 * s0 + a1 * s1 + b * sb;
+  const int64_t off = transposed ? col * ldY + i : (int64_t)i * ldY + col;
+  split_store(Yhi, Ylo, off, y);
 }
 
 struct SpmmArgs {
@@ -840,16 +875,24 @@ void spttmc_hooi(const Csf& c, const float* const* U, const int64_t* J, Split ou
   const int RA = rtile(a.J1), RB = rtile(a.Jl);
   const int64_t RQ = ceil_div(P, 256);
   a.slice0 = (int)lo;
-  const dim3 g((unsigned)(hi - lo));
+  a.unit = c.nunits > 0 ? c.unit.p : nullptr;  // the plan (if any) was built for [lo, hi)
+  a.part = c.part.p;
+  const dim3 g((unsigned)(c.nunits > 0 ? c.nunits : hi - lo));
+  bool launched = false;
 #define TK_S4(ra, rb, rq)                                                    \
-  if (RA <= ra && RB <= rb && RQ <= rq) {                                    \
+  if (!launched && RA <= ra && RB <= rb && RQ <= rq) {                       \
     TK_LAUNCH((k_spttmc4<ra, rb, rq>), g, 256, 0, st, a);                    \
-    return;                                                                  \
+    launched = true;                                                         \
   }
   TK_S4(1, 1, 4) TK_S4(2, 2, 4) TK_S4(1, 1, 16) TK_S4(2, 2, 16) TK_S4(2, 2, 32) TK_S4(2, 2, 64)
   TK_S4(4, 4, 32) TK_S4(4, 4, 64)
 #undef TK_S4
-  fail(TUCKER_E_ARG, "spttmc: unsupported order-4 core size (prod J <= 16384, J <= 64)");
+  if (!launched) fail(TUCKER_E_ARG, "spttmc: unsupported order-4 core size (prod J <= 16384, J <= 64)");
+  if (c.nred > 0) {
+    const dim3 gr((unsigned)ceil_div(P, 256), (unsigned)c.nred);
+    TK_LAUNCH(k_spttmc4_reduce, gr, 256, 0, st, c.red.p, c.part.p, a.J0, a.J1, a.Jl, a.s0, a.s1, a.sb, a.Yhi,
+              a.Ylo, ldY, (int)transposed);
+  }
 }
 
 // Work plan for the order-3 HOOI kernel (see Csf).  lmax = 1024 nonzeros
@@ -858,9 +901,61 @@ void spttmc_hooi(const Csf& c, const float* const* U, const int64_t* J, Split ou
 // 1-4 have short fibers and light slices: no plan, one CTA per slice.
 // Config 5's Zipf head (a slice with 7e6 nonzeros in <= 5000 fibers) is what
 // this is for.
+// Order 4: slices are cut into units of at most nmax = max(8, nodes / (16 #SMs))
+// nodes (mid0 indices), each writing a partial row of Jm = J0 J1 times Jl
+// floats (one CTA per slice starves the GPU when there are few slices:
+// config 4 has 200).
+static void spttmc_plan4(Csf& c, int64_t P, int num_sms, cudaStream_t st, int64_t lo, int64_t hi) {
+  std::vector<int32_t> sp((size_t)c.I_root + 1);
+  TK_CUDA(cudaMemcpyAsync(sp.data(), c.slice_ptr.p, sp.size() * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+  TK_CUDA(cudaStreamSynchronize(st));
+  int64_t nmax = std::max<int64_t>(8, ceil_div((int64_t)(sp[hi] - sp[lo]), (int64_t)16 * num_sms));
+  const char* en = std::getenv("TUCKER_TTMC_NMAX");  // test hook
+  if (en && std::atoll(en) > 0) nmax = std::atoll(en);
+  int64_t widest = 0;
+  for (int64_t i = lo; i < hi; ++i) widest = std::max<int64_t>(widest, sp[i + 1] - sp[i]);
+  c.nunits = c.nred = c.nslots = 0;
+  if (widest <= nmax) return;
+  std::vector<std::array<int32_t, 4>> units;
+  std::vector<int32_t> red;
+  int32_t slot = 0;
+  for (int64_t i = lo; i < hi; ++i) {
+    const int64_t n0 = sp[i], n1 = sp[i + 1];
+    if (n1 == n0) continue;
+    if (n1 - n0 <= nmax) {
+      units.push_back({(int32_t)i, (int32_t)n0, (int32_t)n1, -1});
+      continue;
+    }
+    const int64_t nu = ceil_div(n1 - n0, nmax);
+    red.insert(red.end(), {(int32_t)i, slot, (int32_t)nu});
+    for (int64_t u = 0; u < nu; ++u)
+      units.push_back({(int32_t)i, (int32_t)(n0 + u * (n1 - n0) / nu), (int32_t)(n0 + (u + 1) * (n1 - n0) / nu), slot++});
+  }
+  std::stable_sort(units.begin(), units.end(), [](const std::array<int32_t, 4>& x, const std::array<int32_t, 4>& y) {
+    return x[2] - x[1] > y[2] - y[1];
+  });
+  std::vector<int32_t> flat;
+  for (const auto& u : units) flat.insert(flat.end(), u.begin(), u.end());
+  c.nunits = (int64_t)units.size();
+  c.nred = (int64_t)red.size() / 3;
+  c.nslots = slot;
+  c.unit.alloc(flat.size());
+  TK_CUDA(cudaMemcpyAsync(c.unit.p, flat.data(), flat.size() * sizeof(int32_t), cudaMemcpyHostToDevice, st));
+  if (!red.empty()) {
+    c.red.alloc(red.size());
+    TK_CUDA(cudaMemcpyAsync(c.red.p, red.data(), red.size() * sizeof(int32_t), cudaMemcpyHostToDevice, st));
+    c.part.alloc((size_t)(c.nslots * P));
+  }
+  TK_CUDA(cudaStreamSynchronize(st));
+}
+
 void spttmc_plan(Csf& c, int64_t Jm, int64_t Jl, int num_sms, cudaStream_t st, int64_t lo, int64_t hi) {
-  if (c.order != 3) return;
   if (hi < 0) hi = c.I_root;
+  if (c.order == 4) {
+    spttmc_plan4(c, Jm * Jl, num_sms, st, lo, hi);
+    return;
+  }
+  if (c.order != 3) return;
   const int64_t I = c.I_root, F = c.nfib;
   std::vector<int32_t> sp((size_t)I + 1), fp((size_t)F + 1);
   TK_CUDA(cudaMemcpyAsync(sp.data(), c.slice_ptr.p, sp.size() * sizeof(int32_t), cudaMemcpyDeviceToHost, st));

@@ -589,12 +589,11 @@ int tucker_init(tucker_handle** out, int order, const int64_t* dims, const int64
       h->sharded = true;
       make_shards(h.get());
     }
-    if (order == 3)
-      for (int n = 0; n < order; ++n) {
-        Csf& ch = *h->csfs[h->hooi_csf[n]];
-        spttmc_plan(ch, h->J[ch.mid0], h->J[ch.leaf], sm_count(h->opts.device), h->st, h->hooi_lo[n],
-                    h->hooi_hi[n]);
-      }
+    for (int n = 0; n < order; ++n) {  // order 4: Jm = J_mid0 J_mid1 (the partial row is prod_{q != n} J_q)
+      Csf& ch = *h->csfs[h->hooi_csf[n]];
+      const int64_t Jm = h->J[ch.mid0] * (order == 4 ? h->J[ch.mid1] : 1);
+      spttmc_plan(ch, Jm, h->J[ch.leaf], sm_count(h->opts.device), h->st, h->hooi_lo[n], h->hooi_hi[n]);
+    }
     // the COO copy is no longer needed
     for (int n = 0; n < order; ++n) c.idx[n].release();
     c.val.release();

@@ -100,6 +100,27 @@ def test_ttmc_parity_skewed(capi, monkeypatch, lmax, cmax, kernel):
     assert np.max(np.abs(np.asarray(fits) - np.asarray(ref["fits"]))) < 1e-5
 
 
+@pytest.mark.parametrize("nmax", [None, "3"])
+def test_ttmc_parity_order4_plan(capi, monkeypatch, nmax):
+    """Order 4 with the work plan forced (slices cut into node ranges of <= nmax
+    mid0 indices, fp32 partial rows summed in slot order): Y and a HOOI sweep
+    agree with the oracle."""
+    dims, nnz, core = (20, 22, 18, 16), 12_000, (4, 5, 3, 6)
+    idx, vals, U0 = case(dims, nnz, core)
+    if nmax:
+        monkeypatch.setenv("TUCKER_TTMC_NMAX", nmax)
+    T = O.SparseTensor(dims, idx, vals)
+    with capi.Tucker(dims, core, idx, vals, U0) as t:
+        st = t.csf_stats()
+        if nmax:
+            assert all(u > 0 for _, _, _, u in st), st
+        for n in range(4):
+            assert O.rel_frobenius(t.debug_ttmc(n), O.ttm_chain_unfold(T, U0, n)) < 1e-4
+        fits = t.hooi_sweep(2)
+    ref = O.run_hooi(T, U0, core, 2)
+    assert np.max(np.abs(np.asarray(fits) - np.asarray(ref["fits"]))) < 1e-5
+
+
 @pytest.mark.parametrize("dims,nnz,core", SHAPES)
 def test_gram_parity(capi, dims, nnz, core):
     idx, vals, U0 = case(dims, nnz, core)
