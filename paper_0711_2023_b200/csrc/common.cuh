@@ -32,6 +32,12 @@ struct Error {
 
 // Launch counter shared by all launches of one handle (reported by tucker_stats).
 extern thread_local int64_t* g_launch_counter;
+// Stream of the handle call in progress: DBuf allocations are stream-ordered on
+// it (cudaMallocAsync from the device's default pool, which keeps freed memory
+// for reuse), so per-call temporaries cost no synchronous cudaMalloc/cudaFree.
+// nullptr (no handle call, e.g. unit-test entry points): plain cudaMalloc.
+extern thread_local cudaStream_t g_alloc_stream;
+void mempool_retain(int device);  // default pool keeps freed memory (once per device)
 
 bool sync_check_enabled();  // env TUCKER_SYNC_CHECK: synchronise + check after every launch
 
@@ -56,28 +62,38 @@ template <typename T>
 struct DBuf {
   T* p = nullptr;
   size_t n = 0;
+  cudaStream_t s = nullptr;  // stream of a stream-ordered allocation (freed on it)
   DBuf() = default;
   explicit DBuf(size_t count) { alloc(count); }
   DBuf(const DBuf&) = delete;
   DBuf& operator=(const DBuf&) = delete;
-  DBuf(DBuf&& o) noexcept : p(o.p), n(o.n) { o.p = nullptr; o.n = 0; }
+  DBuf(DBuf&& o) noexcept : p(o.p), n(o.n), s(o.s) { o.p = nullptr; o.n = 0; o.s = nullptr; }
   DBuf& operator=(DBuf&& o) noexcept {
-    if (this != &o) { release(); p = o.p; n = o.n; o.p = nullptr; o.n = 0; }
+    if (this != &o) { release(); p = o.p; n = o.n; s = o.s; o.p = nullptr; o.n = 0; o.s = nullptr; }
     return *this;
   }
   ~DBuf() { release(); }
   void alloc(size_t count) {
     release();
     if (count == 0) return;
-    TK_CUDA(cudaMalloc(&p, count * sizeof(T)));
+    if (g_alloc_stream) {
+      TK_CUDA(cudaMallocAsync(&p, count * sizeof(T), g_alloc_stream));
+      s = g_alloc_stream;
+    } else {
+      TK_CUDA(cudaMalloc(&p, count * sizeof(T)));
+    }
     n = count;
   }
   // grow-only reallocation (contents are not preserved)
   void ensure(size_t count) { if (count > n) alloc(count); }
   void release() {
-    if (p) cudaFree(p);
+    if (p) {
+      if (s) cudaFreeAsync(p, s);  // ordered after every use on the handle's stream
+      else cudaFree(p);
+    }
     p = nullptr;
     n = 0;
+    s = nullptr;
   }
   size_t bytes() const { return n * sizeof(T); }
 };

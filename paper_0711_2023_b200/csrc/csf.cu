@@ -14,6 +14,16 @@
 namespace tk {
 
 thread_local int64_t* g_launch_counter = nullptr;
+thread_local cudaStream_t g_alloc_stream = nullptr;
+void mempool_retain(int device) {
+  static bool done[64] = {};
+  if (device < 0 || device >= 64 || done[device]) return;
+  cudaMemPool_t pool;
+  TK_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
+  uint64_t thr = ~0ull;
+  TK_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+  done[device] = true;
+}
 
 bool sync_check_enabled() {
   static const bool on = std::getenv("TUCKER_SYNC_CHECK") != nullptr;

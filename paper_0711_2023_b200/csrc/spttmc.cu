@@ -949,6 +949,28 @@ static void spttmc_plan4(Csf& c, int64_t P, int num_sms, cudaStream_t st, int64_
   TK_CUDA(cudaStreamSynchronize(st));
 }
 
+// Exact (int64) plan statistics on the device, so the common no-plan case costs
+// three numbers of D2H instead of the fiber pointers: out[0] = longest fiber,
+// out[1] = total work sum_f (wf ceil(L/lmax) + wn L), out[2] = heaviest slice
+// wf F_i + wn nnz_i, over the slices [lo, hi).
+__global__ void k_plan_stats(const int32_t* __restrict__ sp, const int32_t* __restrict__ fp, int64_t lo,
+                             int64_t hi, int64_t lmax, int64_t wf, int64_t wn,
+                             unsigned long long* __restrict__ out) {
+  const int64_t f0 = sp[lo], f1 = sp[hi];
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  unsigned long long lmx = 0, tot = 0, smx = 0;
+  for (int64_t f = f0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; f < f1; f += stride) {
+    const int64_t L = fp[f + 1] - fp[f];
+    lmx = max(lmx, (unsigned long long)L);
+    tot += (unsigned long long)(wf * ((L + lmax - 1) / lmax) + wn * L);
+  }
+  for (int64_t i = lo + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < hi; i += stride)
+    smx = max(smx, (unsigned long long)(wf * (sp[i + 1] - sp[i]) + wn * (fp[sp[i + 1]] - fp[sp[i]])));
+  atomicMax(out, lmx);
+  atomicAdd(out + 1, tot);  // integer sum: order independent
+  atomicMax(out + 2, smx);
+}
+
 void spttmc_plan(Csf& c, int64_t Jm, int64_t Jl, int num_sms, cudaStream_t st, int64_t lo, int64_t hi) {
   if (hi < 0) hi = c.I_root;
   if (c.order == 4) {
@@ -957,32 +979,30 @@ void spttmc_plan(Csf& c, int64_t Jm, int64_t Jl, int num_sms, cudaStream_t st, i
   }
   if (c.order != 3) return;
   const int64_t I = c.I_root, F = c.nfib;
-  std::vector<int32_t> sp((size_t)I + 1), fp((size_t)F + 1);
-  TK_CUDA(cudaMemcpyAsync(sp.data(), c.slice_ptr.p, sp.size() * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
-  TK_CUDA(cudaMemcpyAsync(fp.data(), c.fib_ptr.p, fp.size() * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
-  TK_CUDA(cudaStreamSynchronize(st));
   c.lmax = 1024;
   // test hooks: force the plan on small inputs (TUCKER_TTMC_LMAX / _CMAX)
   const char* el = std::getenv("TUCKER_TTMC_LMAX");
   const char* ec = std::getenv("TUCKER_TTMC_CMAX");
   if (el && std::atoll(el) > 0) c.lmax = std::atoll(el);
   const double wf = (double)Jm * Jl, wn = (double)Jl;  // work per fiber / per nonzero
-  double total = 0;
-  int64_t longest = 0;
-  for (int64_t f = sp[lo]; f < sp[hi]; ++f) {  // this rank's slices only
-    const int64_t L = fp[f + 1] - fp[f];
-    longest = std::max(longest, L);
-    total += wf * (double)ceil_div(L, c.lmax) + wn * (double)L;
-  }
-  c.cmax = std::max(4194304.0, total / (16.0 * num_sms));
-  if (ec && std::atof(ec) > 0) c.cmax = std::atof(ec);
-  double heaviest = 0;
-  for (int64_t i = lo; i < hi; ++i) {
-    const double w = wf * (double)(sp[i + 1] - sp[i]) + wn * (double)(fp[sp[i + 1]] - fp[sp[i]]);
-    heaviest = std::max(heaviest, w);
-  }
   c.nunits = c.nred = c.nslots = c.nvfib = 0;
-  if (longest <= c.lmax && heaviest <= c.cmax) return;  // one CTA per slice
+  if (hi <= lo) return;
+  {
+    DBuf<unsigned long long> stats(3);
+    TK_CUDA(cudaMemsetAsync(stats.p, 0, 3 * sizeof(unsigned long long), st));
+    TK_LAUNCH(k_plan_stats, 2 * num_sms, 256, 0, st, c.slice_ptr.p, c.fib_ptr.p, lo, hi, c.lmax, Jm * Jl, Jl,
+              stats.p);
+    unsigned long long h[3];
+    TK_CUDA(cudaMemcpyAsync(h, stats.p, sizeof(h), cudaMemcpyDeviceToHost, st));
+    TK_CUDA(cudaStreamSynchronize(st));
+    c.cmax = std::max(4194304.0, (double)h[1] / (16.0 * num_sms));
+    if (ec && std::atof(ec) > 0) c.cmax = std::atof(ec);
+    if ((int64_t)h[0] <= c.lmax && (double)h[2] <= c.cmax) return;  // one CTA per slice
+  }
+  std::vector<int32_t> sp((size_t)I + 1), fp((size_t)F + 1);
+  TK_CUDA(cudaMemcpyAsync(sp.data(), c.slice_ptr.p, sp.size() * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+  TK_CUDA(cudaMemcpyAsync(fp.data(), c.fib_ptr.p, fp.size() * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+  TK_CUDA(cudaStreamSynchronize(st));
   std::vector<int32_t> fm((size_t)F);
   TK_CUDA(cudaMemcpyAsync(fm.data(), c.fib_mid0.p, fm.size() * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
   TK_CUDA(cudaStreamSynchronize(st));

@@ -2,6 +2,7 @@
 // per-sweep orchestration of the kernels in csf.cu / spttmc.cu / gram*.cu /
 // eig.cu / dense.cu.
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -57,10 +58,17 @@ struct tucker_handle {
 
 namespace {
 
-struct LaunchScope {  // route TK_LAUNCH counting to this handle
+struct LaunchScope {  // route TK_LAUNCH counting and stream-ordered allocations to this handle
   int64_t* prev;
-  explicit LaunchScope(tucker_handle* h) : prev(g_launch_counter) { g_launch_counter = &h->launches; }
-  ~LaunchScope() { g_launch_counter = prev; }
+  cudaStream_t prev_st;
+  explicit LaunchScope(tucker_handle* h) : prev(g_launch_counter), prev_st(g_alloc_stream) {
+    g_launch_counter = &h->launches;
+    g_alloc_stream = h->st;
+  }
+  ~LaunchScope() {
+    g_launch_counter = prev;
+    g_alloc_stream = prev_st;
+  }
 };
 
 template <typename F>
@@ -536,6 +544,19 @@ int tucker_init(tucker_handle** out, int order, const int64_t* dims, const int64
       TK_CUDA(cudaStreamCreateWithFlags(&h->st, cudaStreamNonBlocking));
       h->own_stream = true;
     }
+    mempool_retain(o.device);
+    g_alloc_stream = h->st;  // the scope (guarded) restores the previous value
+    // TUCKER_PROFILE_INIT=1: phase times on stderr (host clock, stream synchronised)
+    const bool prof = std::getenv("TUCKER_PROFILE_INIT") != nullptr;
+    auto tp = std::chrono::steady_clock::now();
+    auto mark = [&](const char* what) {
+      if (!prof) return;
+      TK_CUDA(cudaStreamSynchronize(h->st));
+      const auto now = std::chrono::steady_clock::now();
+      std::fprintf(stderr, "[init] %-28s %8.3f ms\n", what,
+                   std::chrono::duration<double, std::milli>(now - tp).count());
+      tp = now;
+    };
     const cudaMemcpyKind kind = on_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
     Coo& c = h->coo;
     c.order = order;
@@ -549,8 +570,11 @@ int tucker_init(tucker_handle** out, int order, const int64_t* dims, const int64
     }
     c.val.alloc(nnz);
     TK_CUDA(cudaMemcpyAsync(c.val.p, vals, nnz * sizeof(float), kind, h->st));
+    mark("H2D copies + allocs");
     coo_validate_compact(c, h->st);
+    mark("validate");
     h->normX2 = coo_norm2(c, h->st);
+    mark("norm");
     if (!(h->normX2 > 0) || !std::isfinite(h->normX2))
       fail(TUCKER_E_VALUE, "tucker_init: ||X|| = 0 or not finite");
     // orderings: root n, leaf m, mids = the other modes ascending
@@ -562,6 +586,7 @@ int tucker_init(tucker_handle** out, int order, const int64_t* dims, const int64
           if (q != n && q != m) mids[nm++] = q;
         auto cs = std::make_unique<Csf>();
         csf_build(c, *cs, n, mids[0], order == 4 ? mids[1] : -1, m, h->st);
+        mark("csf_build");
         h->mp_csf[n][m] = (int)h->csfs.size();
         h->csfs.push_back(std::move(cs));
       }
@@ -594,6 +619,7 @@ int tucker_init(tucker_handle** out, int order, const int64_t* dims, const int64
       const int64_t Jm = h->J[ch.mid0] * (order == 4 ? h->J[ch.mid1] : 1);
       spttmc_plan(ch, Jm, h->J[ch.leaf], sm_count(h->opts.device), h->st, h->hooi_lo[n], h->hooi_hi[n]);
     }
+    mark("spttmc plans");
     // the COO copy is no longer needed
     for (int n = 0; n < order; ++n) c.idx[n].release();
     c.val.release();
@@ -603,7 +629,12 @@ int tucker_init(tucker_handle** out, int order, const int64_t* dims, const int64
   if (rc != TUCKER_OK) {
     // keep the message for the caller through stderr (no handle is returned)
     std::fprintf(stderr, "tucker_init: %s\n", h->last_error.c_str());
-    if (h->own_stream && h->st) cudaStreamDestroy(h->st);
+    // free the handle's buffers (stream-ordered on h->st) before the stream goes
+    const bool own = h->own_stream;
+    cudaStream_t st = h->st;
+    if (h->comm) dist_comm_destroy(h->comm);
+    h.reset();
+    if (own && st) cudaStreamDestroy(st);
     return rc;
   }
   *out = h.release();
