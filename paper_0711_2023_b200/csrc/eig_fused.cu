@@ -1586,8 +1586,28 @@ size_t eig_fused_smem(int k, int d, int G) {
   return work + sres <= SMEM_LIMIT ? work + sres : work;
 }
 
+// Cold slot with a hint (the current factor, fp32 d x J row-major): the first J
+// basis columns start from it, the k - J oversampling columns are a fixed
+// pseudo-random fill (deterministic).
+__global__ void k_seed_basis(double* __restrict__ basis, int64_t d, int LB, int k, const float* __restrict__ hint,
+                             int J, uint64_t seed) {
+  const int64_t n = d * LB;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = e / LB;
+    const int c = (int)(e - r * LB);
+    double v = 0.0;
+    if (c < J) {
+      v = (double)hint[r * J + c];
+    } else if (c < k) {
+      const uint64_t z = mix64(seed ^ ((uint64_t)r * 0x9E3779B97F4A7C15ull + (uint64_t)c));
+      v = (double)(z >> 11) * (2.0 / 9007199254740992.0) - 1.0;
+    }
+    basis[e] = v;
+  }
+}
+
 bool eig_fused(double* S, int64_t d, int J, EigSlot& slot, EigWs& ws, const EigOpts& o, double* out_V,
-               double* theta_dev, int* info_dev, cudaStream_t st) {
+               double* theta_dev, int* info_dev, cudaStream_t st, const float* hint) {
   static size_t smem_set = 0;
   const int k = choose_block(J, d, o.oversample);
   const int grid = num_sms();  // one CTA per SM (cooperative: all co-resident)
@@ -1657,6 +1677,11 @@ bool eig_fused(double* S, int64_t d, int J, EigSlot& slot, EigWs& ws, const EigO
   }
   a.basis = slot.basis.p;
   a.warm = (slot.valid && slot.d == d && slot.k == k) ? 1 : 0;
+  if (!a.warm && hint) {  // cold slot: start from the caller's current factor
+    TK_LAUNCH(k_seed_basis, 2 * grid, 256, 0, st, slot.basis.p, d, LB, k, hint, J,
+              0x5eedb0000ull + (uint64_t)d * 131 + (uint64_t)J);
+    a.warm = 1;
+  }
   a.outV = out_V;
   a.theta_out = theta_dev;
   a.prof = ws.fprof.p;

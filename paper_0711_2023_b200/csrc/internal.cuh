@@ -165,7 +165,7 @@ struct EigOpts {
 // breakdown}.  No host synchronisation.
 void eig_layout(int64_t d, int64_t* ls, int64_t* rows);
 bool eig_fused(double* S, int64_t d, int J, EigSlot& slot, EigWs& ws, const EigOpts& o, double* out_V,
-               double* theta_dev, int* info_dev, cudaStream_t st);
+               double* theta_dev, int* info_dev, cudaStream_t st, const float* hint = nullptr);
 size_t eig_fused_smem(int k, int d, int G);
 // unit test of the fused solver's k x k routines (one CTA); see tucker_debug_smalldense
 void eig_unit_mv(const double* S, const double* Y, int d, int n, double alpha, double* Out, double gamma,

@@ -254,12 +254,13 @@ Split build_mp_w(tucker_handle* h, int n, int only_m = -1) {
 
 // Leading eigenvectors of S (padded layout, eig_layout) -> fp64 V (d x J) in
 // h->V, eigenvalues in h->theta_d (device): the persistent fused solver.
-void solve_eig(tucker_handle* h, int64_t d, int J, EigSlot& slot) {
+// hint: the current factor (fp32 d x J) seeds a cold slot's basis (S is I_n x I_n)
+void solve_eig(tucker_handle* h, int64_t d, int J, EigSlot& slot, const float* hint = nullptr) {
   h->V.ensure((size_t)(d * J));
   h->theta_d.ensure((size_t)J);
   h->info_d.ensure(16);  // 8 ints + 4 doubles
   h->last_slot = &slot;
-  eig_fused(h->S.p, d, J, slot, h->eig, eig_opts(h), h->V.p, h->theta_d.p, h->info_d.p, h->st);
+  eig_fused(h->S.p, d, J, slot, h->eig, eig_opts(h), h->V.p, h->theta_d.p, h->info_d.p, h->st, hint);
 }
 
 // S buffer in the eigensolver's padded layout; returns its row stride
@@ -315,7 +316,7 @@ void update_factor(tucker_handle* h, int n, const Split& A, bool transposed, Eig
   }
   if (partial_gram) dist_allreduce_f64(h->comm, h->S.p, d * lds, h->st);
   TK_CUDA(cudaEventRecord(e1, h->st));
-  solve_eig(h, d, J, slot);
+  solve_eig(h, d, J, slot, transposed ? nullptr : h->U[n].p);
   if (!transposed) {
     canon_to_f32(h->V.p, J, d, J, h->U[n].p, h->st);
   } else {
@@ -1027,7 +1028,7 @@ int tucker_hosvd(tucker_handle* h, unsigned mode_mask) {
       sparse_gram(c, f0, f1, h->S.p, lds, h->st);
       if (h->sharded) dist_allreduce_f64(h->comm, h->S.p, d * lds, h->st);
       h->scratch_slot.valid = false;
-      solve_eig(h, d, J, h->scratch_slot);
+      solve_eig(h, d, J, h->scratch_slot, h->U[n].p);
       canon_to_f32(h->V.p, J, d, J, h->U[n].p, h->st);
       TK_CUDA(cudaStreamSynchronize(h->st));
       eig_check(h);
