@@ -56,3 +56,37 @@ def test_strerror_and_arg_errors_without_device(lib):
     with pytest.raises(capi.TuckerError) as e:
         capi.tucker_init(dims, core, idx, vals, Ubad)
     assert e.value.code == 5
+
+
+def test_new_entry_points_reject_bad_arguments_without_device(lib):
+    """The drivers, HO-SVD, Slice Projection, factor setter and multi-GPU
+    helpers validate their arguments before any device work (E_ARG = 1)."""
+    import ctypes as C
+    from paper_0711_2023_b200 import capi
+    d = C.c_double(0)
+    i = C.c_int(0)
+    nul = None
+    assert lib.hooi_run(nul, 5, 1e-4, C.byref(d), C.byref(i)) == 1
+    assert lib.mp_run(nul, 5, 1e-4, C.byref(d), C.byref(i)) == 1
+    assert lib.sp_run(nul, 5, 1e-4, C.byref(d), C.byref(i)) == 1
+    assert lib.sp_sweep(nul, 1, None, None, None) == 1
+    assert lib.tucker_hosvd(nul, 1) == 1
+    assert lib.tucker_set_factor(nul, 0, nul, 1) == 1
+    assert lib.tucker_shard_info(nul, nul) == 1
+    assert lib.tucker_nccl_unique_id(nul) == 1
+    b = np.zeros(3, np.int64)
+    w = np.ones(4)
+    bp = b.ctypes.data_as(C.POINTER(C.c_int64))
+    wp = w.ctypes.data_as(C.POINTER(C.c_double))
+    assert lib.tucker_shard_bounds(wp, 4, 0, bp) == 1   # world < 1
+    assert lib.tucker_shard_bounds(wp, -1, 2, bp) == 1  # n < 0
+    assert lib.tucker_shard_bounds(None, 4, 2, bp) == 1
+    # world > 1 without an NCCL id, and rank outside [0, world): E_ARG before any CUDA call
+    dims, core = (4, 5, 6), (2, 2, 2)
+    idx = [np.zeros(3, np.int32)] * 3
+    vals = np.ones(3, np.float32)
+    U = [np.eye(n, c, dtype=np.float32) for n, c in zip(dims, core)]
+    for kw in ({"world": 2}, {"rank": 2, "world": 2, "nccl_id": b"\0" * 128}, {"rank": -1}):
+        with pytest.raises(capi.TuckerError) as e:
+            capi.tucker_init(dims, core, idx, vals, U, **kw)
+        assert e.value.code == 1, kw
