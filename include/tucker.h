@@ -60,6 +60,8 @@ extern "C" {
 /* flags */
 #define TUCKER_INPUT_ON_DEVICE 0x1u   /* idx/vals/U0 pointers are device pointers                */
 #define TUCKER_OUTPUT_ON_DEVICE 0x2u  /* core_out/U_out/Y/S outputs are device pointers          */
+#define TUCKER_HOST_COLLECTIVES 0x4u  /* world > 1 without NCCL: the sharded sweep's sums go through
+                                         the callback of tucker_set_allreduce (tests; other layers)  */
 
 typedef struct tucker_handle tucker_handle;
 
@@ -250,6 +252,14 @@ int tucker_nccl_unique_id(void* id_out);
  * itself) reaches r/world of the total; shards may be empty.  bounds has
  * world + 1 entries.  TUCKER_E_ARG on null pointers, n < 0 or world < 1. */
 int tucker_shard_bounds(const double* work, int64_t n, int world, int64_t* bounds);
+
+/* TUCKER_HOST_COLLECTIVES handles: fn is an
+ *   int fn(void* dev_buf, int64_t count, int dtype, void* stream, void* user)
+ * that replaces dev_buf (count elements, dtype 0 = fp32, 1 = fp64, device
+ * memory of this rank) by its sum over the ranks and returns 0; the library
+ * synchronises its stream before the call.  Set it before the first sweep.
+ * TUCKER_E_ARG for a handle without host collectives. */
+int tucker_set_allreduce(tucker_handle* h, void* fn, void* user);
 
 /* This rank's shards (out has 2 N + 2 N N entries): out[2n], out[2n + 1] =
  * [lo, hi) of the root slices of mode n's HOOI projection; out[2N + 2(nN + m)],

@@ -16,6 +16,9 @@ LIB_PATH = os.path.join(_HERE, "libtucker.so")
 
 TUCKER_INPUT_ON_DEVICE = 0x1
 TUCKER_OUTPUT_ON_DEVICE = 0x2
+TUCKER_HOST_COLLECTIVES = 0x4
+# int fn(void* dev_buf, int64_t count, int dtype, void* stream, void* user)
+ALLREDUCE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_int64, C.c_int, C.c_void_p, C.c_void_p)
 E_OOM = 8
 E_CONVERGE = 10
 
@@ -26,7 +29,7 @@ EXPORTS = [
     "tucker_debug_ttmc", "tucker_debug_gram", "tucker_debug_eig", "tucker_debug_smalldense",
     "tucker_debug_product", "tucker_debug_product_time", "tucker_csf_stats", "tucker_stats",
     "tucker_nccl_unique_id", "tucker_shard_bounds", "tucker_shard_info", "hooi_run", "mp_run",
-    "tucker_hosvd", "sp_sweep", "sp_run", "tucker_set_factor",
+    "tucker_hosvd", "sp_sweep", "sp_run", "tucker_set_factor", "tucker_set_allreduce",
 ]
 
 
@@ -67,6 +70,7 @@ def load(path: str = LIB_PATH) -> C.CDLL:
     lib.tucker_csf_stats.argtypes = [P, i64p]
     lib.tucker_nccl_unique_id.argtypes = [P]
     lib.tucker_hosvd.argtypes = [P, C.c_uint]
+    lib.tucker_set_allreduce.argtypes = [P, P, P]
     lib.sp_sweep.argtypes = [P, C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_double), C.POINTER(C.c_float)]
     lib.sp_run.argtypes = [P, C.c_int, C.c_double, C.POINTER(C.c_double), C.POINTER(C.c_int)]
     lib.tucker_set_factor.argtypes = [P, C.c_int, P, C.c_int]
@@ -114,7 +118,7 @@ def _ptr(a) -> int:
 
 def tucker_init(dims, core, idx, vals, U0, *, device=0, stream=None, eig_oversample=0,
                 eig_max_iter=0, eig_tol=0.0, on_device=False, output_on_device=False,
-                rank=0, world=1, nccl_id=None):
+                rank=0, world=1, nccl_id=None, host_collectives=False):
     """Returns an opaque handle (int).  idx: list of N int32 arrays (0-based),
     vals: fp32, U0: list of N fp32 row-major I_n x J_n arrays.  Host numpy
     arrays, or torch CUDA tensors with on_device=True.  Multi-GPU: every rank
@@ -137,8 +141,11 @@ def tucker_init(dims, core, idx, vals, U0, *, device=0, stream=None, eig_oversam
         TUCKER_OUTPUT_ON_DEVICE if output_on_device else 0)
     o.rank = rank
     o.world = world
+    if host_collectives:
+        o.flags |= TUCKER_HOST_COLLECTIVES
     idbuf = None
     if nccl_id is not None:
+        _load_torch_nccl()
         idbuf = C.create_string_buffer(bytes(nccl_id), 128)
         o.nccl_unique_id = C.cast(idbuf, C.c_void_p)
     d = (C.c_int64 * N)(*[int(x) for x in dims])
@@ -322,8 +329,16 @@ def tucker_set_factor(h, n, U, check=True):
     _check(lib().tucker_set_factor(h, n, C.c_void_p(_ptr(U)), 1 if check else 0), h)
 
 
+def _load_torch_nccl():
+    """The library dlopens libnccl.so.2 on first use; import torch first so that
+    soname resolves to torch's bundled NCCL (a system NCCL loaded first would
+    break a later `import torch`, whose libraries need the bundled version)."""
+    import torch  # noqa: F401
+
+
 def nccl_unique_id():
     """A fresh 128-byte ncclUniqueId (bytes) for tucker_init(..., nccl_id=)."""
+    _load_torch_nccl()
     buf = C.create_string_buffer(128)
     _check(lib().tucker_nccl_unique_id(buf))
     return buf.raw
@@ -336,6 +351,15 @@ def shard_bounds(work, world):
     _check(lib().tucker_shard_bounds(w.ctypes.data_as(C.POINTER(C.c_double)), C.c_int64(w.size),
                                      world, b.ctypes.data_as(C.POINTER(C.c_int64))))
     return b
+
+
+def tucker_set_allreduce(h, fn):
+    """Host collectives: fn(dev_ptr, count, dtype, stream) sums the device buffer
+    over the ranks in place (dtype 0 fp32, 1 fp64) and returns 0.  The ctypes
+    callback object is returned; keep it alive as long as the handle."""
+    cb = ALLREDUCE_FN(lambda p, n, dt, st, user: fn(p, n, dt, st))
+    _check(lib().tucker_set_allreduce(h, C.cast(cb, C.c_void_p), None), h)
+    return cb
 
 
 def tucker_shard_info(h, order):

@@ -12,6 +12,7 @@
 #include <dlfcn.h>
 #include <nccl.h>
 
+#include <cstdlib>
 #include <cstring>
 #include <string>
 
@@ -33,8 +34,11 @@ struct NcclApi {
 NcclApi& api() {
   static NcclApi a;
   if (!a.lib) {
-    void* l = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
-    if (!l) fail(TUCKER_E_NCCL, std::string("cannot load libnccl.so.2: ") + dlerror());
+    // an NCCL already in the process (e.g. torch's) is reused through its soname;
+    // TUCKER_NCCL_LIB names a specific library otherwise
+    const char* path = std::getenv("TUCKER_NCCL_LIB");
+    void* l = dlopen(path && *path ? path : "libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!l) fail(TUCKER_E_NCCL, std::string("cannot load NCCL: ") + dlerror());
     auto sym = [&](const char* n) {
       void* p = dlsym(l, n);
       if (!p) fail(TUCKER_E_NCCL, std::string("libnccl.so.2 lacks ") + n);
@@ -56,26 +60,60 @@ void check(ncclResult_t r, const char* what) {
 
 }  // namespace
 
+// A handle's communicator: NCCL, or (TUCKER_HOST_COLLECTIVES) a host callback
+// int fn(void* dev_buf, int64_t count, int dtype, void* stream, void* user)
+// that sums dev_buf over the ranks in place (dtype 0 = fp32, 1 = fp64), called
+// after the library's stream is synchronised.
+struct DistComm {
+  ncclComm_t nccl = nullptr;
+  int (*cb)(void*, int64_t, int, void*, void*) = nullptr;
+  void* user = nullptr;
+};
+
 void* dist_comm_init(const void* unique_id, int world, int rank) {
   static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId is 128 bytes");
   ncclUniqueId id;
   std::memcpy(&id, unique_id, sizeof(id));
-  ncclComm_t c = nullptr;
-  check(api().CommInitRank(&c, world, id, rank), "ncclCommInitRank");
+  auto* c = new DistComm;
+  try {
+    check(api().CommInitRank(&c->nccl, world, id, rank), "ncclCommInitRank");
+  } catch (...) {
+    delete c;
+    throw;
+  }
   return c;
 }
 
+void* dist_comm_host() { return new DistComm; }
+
+void dist_comm_set_callback(void* comm, void* fn, void* user) {
+  auto* c = static_cast<DistComm*>(comm);
+  c->cb = reinterpret_cast<int (*)(void*, int64_t, int, void*, void*)>(fn);
+  c->user = user;
+}
+
 void dist_comm_destroy(void* comm) {
-  if (comm) api().CommDestroy((ncclComm_t)comm);
+  auto* c = static_cast<DistComm*>(comm);
+  if (!c) return;
+  if (c->nccl) api().CommDestroy(c->nccl);
+  delete c;
 }
 
-void dist_allreduce_f32(void* comm, float* p, int64_t n, cudaStream_t st) {
-  if (n > 0) check(api().AllReduce(p, p, (size_t)n, ncclFloat32, ncclSum, (ncclComm_t)comm, st), "ncclAllReduce");
+static void allreduce(void* comm, void* p, int64_t n, int dtype, cudaStream_t st) {
+  auto* c = static_cast<DistComm*>(comm);
+  if (n <= 0) return;
+  if (c->nccl) {
+    check(api().AllReduce(p, p, (size_t)n, dtype ? ncclFloat64 : ncclFloat32, ncclSum, c->nccl, st),
+          "ncclAllReduce");
+    return;
+  }
+  if (!c->cb) fail(TUCKER_E_STATE, "host collectives: no allreduce callback (tucker_set_allreduce)");
+  TK_CUDA(cudaStreamSynchronize(st));
+  if (c->cb(p, n, dtype, (void*)st, c->user) != 0) fail(TUCKER_E_NCCL, "host allreduce callback failed");
 }
 
-void dist_allreduce_f64(void* comm, double* p, int64_t n, cudaStream_t st) {
-  if (n > 0) check(api().AllReduce(p, p, (size_t)n, ncclFloat64, ncclSum, (ncclComm_t)comm, st), "ncclAllReduce");
-}
+void dist_allreduce_f32(void* comm, float* p, int64_t n, cudaStream_t st) { allreduce(comm, p, n, 0, st); }
+void dist_allreduce_f64(void* comm, double* p, int64_t n, cudaStream_t st) { allreduce(comm, p, n, 1, st); }
 
 void dist_unique_id(void* out) {
   ncclUniqueId id;

@@ -91,6 +91,8 @@ void spmm_mp(const Csf& c, const float* U_leaf, int64_t J_leaf, Split out, int64
 // dist.cu -- NCCL (loaded on demand) and shard bounds for the sharded sweep
 void* dist_comm_init(const void* unique_id, int world, int rank);
 void dist_comm_destroy(void* comm);
+void* dist_comm_host();  // TUCKER_HOST_COLLECTIVES: sums through a host callback
+void dist_comm_set_callback(void* comm, void* fn, void* user);
 void dist_allreduce_f32(void* comm, float* p, int64_t n, cudaStream_t st);
 void dist_allreduce_f64(void* comm, double* p, int64_t n, cudaStream_t st);
 void dist_unique_id(void* out128);

@@ -517,7 +517,8 @@ int tucker_init(tucker_handle** out, int order, const int64_t* dims, const int64
   tucker_default_opts(&o);
   if (opts) o = *opts;
   if (o.world < 1 || o.rank < 0 || o.rank >= o.world) return TUCKER_E_ARG;
-  if (o.world > 1 && !o.nccl_unique_id) return TUCKER_E_ARG;
+  const bool host_coll = (o.flags & TUCKER_HOST_COLLECTIVES) != 0;
+  if (o.world > 1 && !o.nccl_unique_id && !host_coll) return TUCKER_E_ARG;
   for (int n = 0; n < order; ++n) {
     if (dims[n] < 1 || dims[n] >= (int64_t)1 << 31) return TUCKER_E_ARG;
     if (core[n] < 1 || core[n] > dims[n] || core[n] > kMaxJ) return TUCKER_E_ARG;
@@ -610,8 +611,8 @@ int tucker_init(tucker_handle** out, int order, const int64_t* dims, const int64
       }
       h->hooi_csf[n] = h->mp_csf[n][best];
     }
-    if (o.nccl_unique_id) {
-      h->comm = dist_comm_init(o.nccl_unique_id, o.world, o.rank);
+    if (o.nccl_unique_id || host_coll) {
+      h->comm = o.nccl_unique_id ? dist_comm_init(o.nccl_unique_id, o.world, o.rank) : dist_comm_host();
       h->sharded = true;
       make_shards(h.get());
     }
@@ -1051,6 +1052,12 @@ int tucker_shard_bounds(const double* work, int64_t n, int world, int64_t* bound
   for (int64_t i = 0; i < n; ++i)
     if (!(work[i] >= 0)) return TUCKER_E_ARG;
   shard_bounds(work, n, world, bounds);
+  return TUCKER_OK;
+}
+
+int tucker_set_allreduce(tucker_handle* h, void* fn, void* user) {
+  if (!h || !fn || !h->comm || !(h->opts.flags & TUCKER_HOST_COLLECTIVES)) return TUCKER_E_ARG;
+  dist_comm_set_callback(h->comm, fn, user);
   return TUCKER_OK;
 }
 
