@@ -91,17 +91,26 @@ struct Ctx {
   double* sres;   // resident S tile of the product plan (nullptr: S is streamed)
 };
 
+// TK_GSYNC_STATS=1 (debug builds): count grid barriers and their time as seen
+// by CTA 0 (the timer reads delay CTA 0's arrival, so it is off by default)
+#ifndef TK_GSYNC_STATS
+#define TK_GSYNC_STATS 0
+#endif
 __device__ unsigned long long g_gsync_stat[2];  // [0] barriers, [1] ns (CTA 0's view; debug)
 __device__ __forceinline__ void gsync() {
+#if TK_GSYNC_STATS
   long long t0 = 0;
   if (blockIdx.x == 0 && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+#endif
   cg::this_grid().sync();
+#if TK_GSYNC_STATS
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     long long t1;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
     g_gsync_stat[0] += 1;
     g_gsync_stat[1] += (unsigned long long)(t1 - t0);
   }
+#endif
 }
 
 __device__ __forceinline__ long long gtimer() {
