@@ -260,10 +260,12 @@ def run_ours(args):
     flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)  # 512 MB > L2
 
     stage_acc = np.zeros(4)
+    sweep_acc = np.zeros(S)      # HOOI per-sweep time (all stages), summed over timed steps
+    sweep_acc_mp = np.zeros(S)
     stage_acc_mp = np.zeros(4)
 
     def step(record=False):
-        nonlocal stage_acc, stage_acc_mp
+        nonlocal stage_acc, stage_acc_mp, sweep_acc, sweep_acc_mp
         capi.tucker_set_factors(h, U0_d)
         fh, sh, _ = capi.hooi_sweep(h, S, want_stage=True)
         capi.core_and_fit_into(h, G_d, U_d)
@@ -273,6 +275,8 @@ def run_ours(args):
         if record:
             stage_acc += sh.sum(axis=0)
             stage_acc_mp += sm.sum(axis=0)
+            sweep_acc += sh.sum(axis=1)
+            sweep_acc_mp += sm.sum(axis=1)
         return fh[-1], fit_m
 
     for _ in range(args.warmup):
@@ -415,6 +419,11 @@ def run_ours(args):
                                    "NCCL allreduce of Y / partial Gram / U / G / M_n (DESIGN.md Multi-GPU)")
                    if sharded else "single GPU"},
         "hooi_ms_per_sweep": float(stage_acc.sum() / args.steps / S),
+        # sweep 0 (cold eigensolves from U0) apart from the warm sweeps >= 1
+        "sweep_ms": {"hooi_sweep0": float(sweep_acc[0] / args.steps),
+                     "hooi_sweeps_ge1": float(sweep_acc[1:].mean() / args.steps) if S > 1 else None,
+                     "mp_sweep0": float(sweep_acc_mp[0] / args.steps),
+                     "mp_sweeps_ge1": float(sweep_acc_mp[1:].mean() / args.steps) if S > 1 else None},
         "mp_ms_per_sweep": float(stage_acc_mp.sum() / args.steps / S),
         "fit": {"hooi": fits[0], "mp": fits[1]},
         "csf_build_s": init_s,
