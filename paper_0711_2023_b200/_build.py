@@ -18,7 +18,7 @@ FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "-std=c++17", "--expt-relaxed-constexpr",
     "-Xcompiler", "-fPIC,-O2", "-Xptxas", "-O3",
-]
+] + os.environ.get("TUCKER_NVCC_EXTRA", "").split()  # debug variants, e.g. -DTK_GSYNC_STATS=1
 
 
 def _stale() -> bool:

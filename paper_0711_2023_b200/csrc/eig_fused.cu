@@ -1587,7 +1587,21 @@ size_t sres_doubles(int d, int G) {
   const MvPlan pl = mv_plan(d, G);
   return (size_t)16 * ((pl.m8 + 1) / 2) * (pl.kchunk + 4);
 }
-constexpr size_t SMEM_LIMIT = 219 * 1024;  // dynamic smem budget (static smem ~7.8 KB)
+// dynamic smem budget: the device's per-block opt-in limit minus the solver's
+// static shared memory (Jacobi tables, Ritz values: ~13.5 KB)
+size_t smem_limit() {
+  static size_t lim = 0;
+  if (!lim) {
+    int dev = 0, optin = 0;
+    TK_CUDA(cudaGetDevice(&dev));
+    TK_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+    cudaFuncAttributes fa;
+    TK_CUDA(cudaFuncGetAttributes(&fa, (const void*)k_eig_fused));
+    lim = (size_t)optin - fa.sharedSizeBytes;
+  }
+  return lim;
+}
+#define SMEM_LIMIT smem_limit()
 
 size_t eig_fused_smem(int k, int d, int G) {
   const size_t work = eig_work_doubles(k, d, G) * sizeof(double);
@@ -1705,6 +1719,7 @@ bool eig_fused(double* S, int64_t d, int J, EigSlot& slot, EigWs& ws, const EigO
   a.lmin_hint = (useful && !a.lanczos) ? slot.lmin - 0.1 * (slot.bval - slot.lmin) : 0.0;
   slot.lz_age = a.lanczos ? 0 : slot.lz_age + 1;
   a.tol = o.tol;
+  if (const char* e = std::getenv("TUCKER_EIG_TOL")) a.tol = std::atof(e);  // experiments
   a.max_outer = o.max_outer;
   a.jsweeps = o.jacobi_sweeps;
   if (const char* e = std::getenv("TUCKER_EIG_JSW")) a.jsweeps = std::atoi(e);  // experiments

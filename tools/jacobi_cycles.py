@@ -5,7 +5,7 @@ import __graft_entry__
 __graft_entry__.build()
 from paper_0711_2023_b200 import capi
 rng = np.random.default_rng(0)
-for k in (40, 82, 116):
+for k in (40, 60, 82, 116):
     Q = np.linalg.qr(rng.standard_normal((k, k)))[0]
     H = (Q * np.sort(rng.uniform(1, 2, k))[::-1]) @ Q.T
     for mode in (1, 2):
