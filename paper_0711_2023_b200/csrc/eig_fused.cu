@@ -1088,7 +1088,10 @@ __global__ void __launch_bounds__(NT, 1) k_eig_fused(FusedArgs P) {
   // W = P - Ln (Ln^T P) / 2 - sigma Ln / 2, P = S Ln
   auto deflate = [&](int n0, int nl) {
     const double sigma = last_b > 0 ? 0.5 * (last_a + last_b) : (a_lo > 0 ? a_lo : 0.0);
-    double* Wd = B(iX);  // d x nl (ld nl)
+    // W and Ln stored transposed (nl x d; B(iX), B(iT) are scratch here: both
+    // callers overwrite iT next), so the update's loads are coalesced over j
+    double* WT = B(iX);
+    double* LnT = B(iT);
     gram_partial(x, P.L + n0, J, nl, P.LT + n0, J, nl, P.part);
     reduce_bcast(x, P.part, nl * nl, nl, P.red, x.r2s, nl);
     tick(PF_RED);
@@ -1096,7 +1099,9 @@ __global__ void __launch_bounds__(NT, 1) k_eig_fused(FusedArgs P) {
       for (int c = x.lane; c < nl; c += 32) {
         double s = 0.0;
         for (int l = 0; l < nl; ++l) s = fma(P.L[(int64_t)r * J + n0 + l], x.r2s[l * nl + c], s);
-        Wd[(int64_t)r * nl + c] = P.LT[(int64_t)r * J + n0 + c] - 0.5 * s - 0.5 * sigma * P.L[(int64_t)r * J + n0 + c];
+        const double lv = P.L[(int64_t)r * J + n0 + c];
+        WT[(int64_t)c * d + r] = P.LT[(int64_t)r * J + n0 + c] - 0.5 * s - 0.5 * sigma * lv;
+        LnT[(int64_t)c * d + r] = lv;
       }
     gsync();  // W complete
     // S[own rows][j] -= sum_l Ln[r][l] W[j][l] + W[r][l] Ln[j][l], rows in chunks of 8
@@ -1107,7 +1112,7 @@ __global__ void __launch_bounds__(NT, 1) k_eig_fused(FusedArgs P) {
       for (int i = x.warp; i < 8; i += NW)
         for (int l = x.lane; l < nl; l += 32) {
           lrs[i * nl + l] = i < n8 ? P.L[(int64_t)(rc + i) * J + n0 + l] : 0.0;
-          wrs[i * nl + l] = i < n8 ? Wd[(int64_t)(rc + i) * nl + l] : 0.0;
+          wrs[i * nl + l] = i < n8 ? __ldcg(WT + (int64_t)l * d + rc + i) : 0.0;
         }
       __syncthreads();
       for (int j = x.tid; j < d; j += NT) {
@@ -1115,8 +1120,8 @@ __global__ void __launch_bounds__(NT, 1) k_eig_fused(FusedArgs P) {
 #pragma unroll
         for (int i = 0; i < 8; ++i) acc[i] = 0.0;
         for (int l = 0; l < nl; ++l) {
-          const double w = __ldcg(Wd + (int64_t)j * nl + l);
-          const double lv = __ldcg(P.L + (int64_t)j * J + n0 + l);
+          const double w = __ldcg(WT + (int64_t)l * d + j);
+          const double lv = __ldcg(LnT + (int64_t)l * d + j);
 #pragma unroll
           for (int i = 0; i < 8; ++i) acc[i] = fma(lrs[i * nl + l], w, fma(wrs[i * nl + l], lv, acc[i]));
         }
