@@ -649,10 +649,57 @@ __device__ void cholqr_factor(const Ctx& x, double* A, double* X, int k, int ld,
       X[r * ld + c] = (r == c) ? 1.0 : 0.0;
     }
   __syncthreads();
-  for (int j = 0; j < k - 1; ++j) {
+  // Two elimination steps (pivots j, j+1) per barrier: row l > j+1 applies step
+  // j and, with row j+1's step-j values formed on the fly, step j+1.  Row j+1
+  // itself (its E part and its pivot) is brought up to date in the NEXT period,
+  // when no row reads it any more.
+  int jd = -1;  // row whose update is deferred (-1: none): E[jd] -= fd E[jd-1], A[jd][jd] = pd
+  double fd = 0.0, pd = 0.0;
+  int j = 0;
+  for (; j + 2 < k; j += 2) {
+    const double a00 = A[j * ld + j], a01 = A[j * ld + j + 1], a11 = A[(j + 1) * ld + j + 1];
+    const double ip0 = 1.0 / (a00 > 1e-12 ? a00 : 1e-12);
+    const double f1 = a01 * ip0;
+    const double p1 = fma(-f1, a01, a11);
+    const double ip1 = 1.0 / (p1 > 1e-12 ? p1 : 1e-12);
+    if (jd >= 0 && x.warp == NW - 1) {  // deferred: row jd (= previous j + 1)
+      double* el = X + jd * ld;
+      const double* ej = X + (jd - 1) * ld;
+      for (int m = x.lane; m < jd; m += 32) el[m] = fma(-fd, ej[m], el[m]);
+      if (x.lane == 0) A[jd * ld + jd] = pd;
+    }
+    const double* aj = A + j * ld;
+    const double* aj1 = A + (j + 1) * ld;
+    const double* ej = X + j * ld;
+    const double* ej1 = X + (j + 1) * ld;
+    for (int l = j + 2 + x.warp; l < k; l += NW) {
+      const double f = aj[l] * ip0;
+      const double g = fma(-f1, aj[l], aj1[l]) * ip1;  // A'[j+1][l] / p1
+      double* al = A + l * ld;
+      for (int m = l + x.lane; m < k; m += 32) {
+        const double u = aj[m];
+        al[m] = fma(-g, fma(-f1, u, aj1[m]), fma(-f, u, al[m]));
+      }
+      double* el = X + l * ld;
+      for (int m = x.lane; m <= j + 1; m += 32) {
+        const double u = ej[m];
+        el[m] = fma(-g, fma(-f1, u, ej1[m]), fma(-f, u, el[m]));
+      }
+    }
+    jd = j + 1;
+    fd = f1;
+    pd = p1;
+    __syncthreads();
+  }
+  if (jd >= 0 && x.warp == NW - 1) {
+    double* el = X + jd * ld;
+    const double* ej = X + (jd - 1) * ld;
+    for (int m = x.lane; m < jd; m += 32) el[m] = fma(-fd, ej[m], el[m]);
+    if (x.lane == 0) A[jd * ld + jd] = pd;
+  }
+  for (; j < k - 1; ++j) {  // a last single step (k - 1 odd)
     const double pj = A[j * ld + j];
     const double ip = 1.0 / (pj > 1e-12 ? pj : 1e-12);
-    // rows l > j, one warp per row: upper part (m >= l) and E part (m <= j)
     for (int l = j + 1 + x.warp; l < k; l += NW) {
       const double f = A[j * ld + l] * ip;
       double* al = A + l * ld;
@@ -662,8 +709,8 @@ __device__ void cholqr_factor(const Ctx& x, double* A, double* X, int k, int ld,
       const double* ej = X + j * ld;
       for (int m = x.lane; m <= j; m += 32) el[m] = fma(-f, ej[m], el[m]);
     }
-    __syncthreads();
   }
+  __syncthreads();
   // X <- M = D E^T P^{-1/2}: M[m][i] = dsc[m] E[i][m] / sqrt(P_i) for m <= i (upper
   // triangular), built in A (only A's diagonal -- the pivots -- is still needed).
   for (int i = x.tid; i < k; i += NT) {
