@@ -142,10 +142,14 @@ def test_world2_sharded_sweep_matches_unsharded(capi):
         for algo in ("hooi", "mp", "hosvd", "sp"):
             fits, G, U, fit = got[algo]
             rfits, rG, rU, rfit = ref[algo]
-            # summation order of the partial Grams differs (1e-16 relative); the first
-            # MP sweep's small eigengaps (~1e-4) amplify it to ~1e-8 in the fit
-            assert abs(fit - rfit) < 1e-7, (dims, algo, fit, rfit)
-            assert np.max(np.abs(np.asarray(fits) - np.asarray(rfits))) < 1e-7, (dims, algo)
+            # the partial Grams' summation order differs, so the two eigensolves stop at
+            # different points inside the acceptance tolerance (residual <= 1e-10 theta_1,
+            # DESIGN.md §2): with the first MP sweep's relative gaps down to ~1e-4
+            # the factors agree to ~1e-6 and MP's fit (not stationary in U)
+            # moves linearly with them; a sharding error (a lost or doubled term) moves
+            # it by orders of magnitude more
+            assert abs(fit - rfit) < 1e-6, (dims, algo, fit, rfit)
+            assert np.max(np.abs(np.asarray(fits) - np.asarray(rfits))) < 1e-6, (dims, algo)
             for n in range(len(dims)):
                 d = O.projector_distance(np.asarray(U[n], np.float64), np.asarray(rU[n], np.float64))
                 assert d < 1e-5, (dims, algo, n, d)
