@@ -532,7 +532,7 @@ __device__ double gmax(const Ctx& x, double v, double* part) {
 }
 
 // ------------------------------------------------------- k x k reductions --
-// part[cta][i*nb + j] = sum_{own rows r} A[r][i] B[r][j]
+// part[i*nb + j][cta] = sum_{own rows r} A[r][i] B[r][j]
 __device__ void gram_partial(const Ctx& x, const double* A, int lda, int na, const double* B, int ldb,
                              int nb, double* part) {
   const int nr = x.r1 - x.r0;
@@ -544,17 +544,18 @@ __device__ void gram_partial(const Ctx& x, const double* A, int lda, int na, con
     for (int c = x.lane; c < nb; c += 32) sB[r * nb + c] = B[(int64_t)(x.r0 + r) * ldb + c];
   }
   __syncthreads();
-  double* out = part + (size_t)x.cta * E;
+  // entry-major partials: part[e * G + cta] (reduce_bcast reads each entry's G
+  // partials as one contiguous run)
   for (int i = x.warp; i < na; i += NW)
     for (int j = x.lane; j < nb; j += 32) {
       double s = 0.0;
       for (int r = 0; r < nr; ++r) s = fma(sA[r * na + i], sB[r * nb + j], s);
-      out[i * nb + j] = s;
+      part[(size_t)(i * nb + j) * x.G + x.cta] = s;
     }
   __syncthreads();
 }
 
-// red[e] = sum_z part[z][e] (fixed order), entries distributed over CTAs; then
+// red[e] = sum_z part[e][z] (entry-major partials, fixed order), entries distributed over CTAs; then
 // barrier and every CTA copies red into dst (smem, row stride ldd, nb columns).
 // Loads are issued in batches (independent registers) so each phase costs about
 // one L2 round trip instead of one per element.
@@ -578,7 +579,7 @@ __device__ void reduce_bcast(const Ctx& x, const double* part, int E, int nb, do
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
           const int z = z0 + u * tpe;
-          v[u] = z < x.G ? __ldcg(part + (size_t)z * E + e) : 0.0;
+          v[u] = z < x.G ? __ldcg(part + (size_t)e * x.G + z) : 0.0;
         }
 #pragma unroll
         for (int u = 0; u < 8; ++u) s += v[u];
@@ -1104,7 +1105,6 @@ __global__ void __launch_bounds__(NT, 1) k_eig_fused(FusedArgs P) {
     // residual partials ||SQ_c - theta_c Q_c||^2 over own rows
     {
       const int nr = x.r1 - x.r0;
-      double* out = P.part + (size_t)x.cta * ka;
       for (int c = x.tid; c < ka; c += NT) {
         const double t = th[nlock + c];
         double s = 0.0;
@@ -1113,7 +1113,7 @@ __global__ void __launch_bounds__(NT, 1) k_eig_fused(FusedArgs P) {
           const double v = B(iSQ)[o] - t * B(iQ)[o];
           s = fma(v, v, s);
         }
-        out[c] = s;
+        P.part[(size_t)c * x.G + x.cta] = s;  // entry-major
       }
     }
     reduce_bcast(x, P.part, ka, ka, P.red, rs + nlock, ka);
