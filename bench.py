@@ -369,7 +369,10 @@ def run_ours(args):
             "traffic": traffic, "flops_per_launch": eig_flops / launches_eig,
             "ms_per_launch": eig_ms / launches_eig, "launches_per_step": launches_eig,
             "stage_ms_per_step": shares, "dominant_stage": max(shares, key=shares.get),
-            "eig_phase_ms_per_step": {k: v / args.steps for k, v in st.get("eig_phase_ms", {}).items()}}
+            }
+    phases = {k: v / args.steps for k, v in st.get("eig_phase_ms", {}).items()}
+    if any(v > 0 for v in phases.values()):  # only in TK_EIG_PROFILE builds (tools/eig_profile.sh)
+        roof["eig_phase_ms_per_step"] = phases
     # secondary: the Gram SYRK on the tensor cores
     hflops, mflops = gram_flops(c)
     gram_ms = shares["gram"]

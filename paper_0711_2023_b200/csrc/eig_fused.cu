@@ -96,6 +96,13 @@ struct Ctx {
 #ifndef TK_GSYNC_STATS
 #define TK_GSYNC_STATS 0
 #endif
+// TK_EIG_PROFILE=1 (profiling builds, TUCKER_NVCC_EXTRA): per-phase and
+// per-product globaltimer accounting by CTA 0 (tucker_stats eig_phase_ms /
+// product_ms).  Off by default: the timer reads sit on CTA 0's path into the
+// next grid barrier, which every CTA waits for.
+#ifndef TK_EIG_PROFILE
+#define TK_EIG_PROFILE 0
+#endif
 __device__ unsigned long long g_gsync_stat[2];  // [0] barriers, [1] ns (CTA 0's view; debug)
 __device__ __forceinline__ void gsync() {
 #if TK_GSYNC_STATS
@@ -983,7 +990,7 @@ __global__ void __launch_bounds__(NT, 1) k_eig_fused(FusedArgs P) {
   __shared__ long long pacc[8];
   long long pt = 0;
   if (x.tid < 8) pacc[x.tid] = 0;
-  if (x.tid == 0) pt = gtimer();
+  if (TK_EIG_PROFILE && x.tid == 0) pt = gtimer();
   // algorithmic fp64 flops of the solve (CTA 0 keeps the count; every CTA
   // executes the same control flow): products 2 d^2 n, Grams 2 d n_a n_b,
   // row-block applies 2 d m n, LDL^T CholQR (2/3) k^3, Jacobi rounds, deflation 4 d^2 n_l
@@ -991,7 +998,7 @@ __global__ void __launch_bounds__(NT, 1) k_eig_fused(FusedArgs P) {
   long long mvt[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // CTA 0: product phase A, inner barrier, phase B,
                                                 // leading barrier (ns); stage wait, compute, chunk loop (clk)
   auto tick = [&](int cat) {
-    if (x.cta == 0 && x.tid == 0) {
+    if (TK_EIG_PROFILE && x.cta == 0 && x.tid == 0) {
       const long long now = gtimer();
       pacc[cat] += now - pt;
       pt = now;
@@ -1007,11 +1014,12 @@ __global__ void __launch_bounds__(NT, 1) k_eig_fused(FusedArgs P) {
 
   auto mv = [&](const double* Y, double alpha, double* Out, double gamma, const double* Dm, double delta,
                 const double* Em) {
-    const long long tg0 = (x.cta == 0 && x.tid == 0) ? gtimer() : 0;
+    const bool prof = TK_EIG_PROFILE && x.cta == 0 && x.tid == 0;
+    const long long tg0 = prof ? gtimer() : 0;
     gsync();  // Y, D, E (and S) complete
-    if (x.cta == 0 && x.tid == 0) mvt[3] += gtimer() - tg0;
+    if (prof) mvt[3] += gtimer() - tg0;
     matvec(x, P.mpart, S, Y, ka, alpha, Out, gamma, Dm, delta, Em,
-           (x.cta == 0 && x.tid == 0) ? mvt : nullptr);  // own rows of Out on return
+           prof ? mvt : nullptr);  // own rows of Out on return
     ++matvecs;
     flops += 2.0 * d * d * ka;
     tick(PF_MV);
