@@ -29,6 +29,15 @@ struct tucker_handle {
   double normX2 = 0;
   // workspaces
   DBuf<float> Yhi, Ylo, Whi, Wlo;
+  // W_n per (mode, term set): W's zero blocks depend only on the tensor, and the
+  // SpMM rewrites every present block in full, so a kept buffer needs no memset
+  // on later builds (kept while the buffers fit a quarter of the device memory)
+  struct WKeep {
+    DBuf<float> hi, lo;
+    size_t need = 0;
+  };
+  WKeep wkeep[kMaxOrder][kMaxOrder + 1];
+  size_t wkeep_bytes = 0;
   Split Y;  // last HOOI projection (mode Y_mode)
   int Y_mode = -1;
   bool Y_transposed = false;
@@ -198,7 +207,8 @@ void project_hooi(tucker_handle* h, int n, bool transposed) {
   }
 }
 
-// W_n = [ (X x_m U_m^T)_(n) ]_{m != n} into h->Whi/Wlo; returns the split view
+// W_n = [ (X x_m U_m^T)_(n) ]_{m != n} into a kept per-(n, term set) buffer or
+// h->Whi/Wlo; returns the split view
 // only_m >= 0: the single term m (Slice Projection, Figs. 5-6)
 Split build_mp_w(tucker_handle* h, int n, int only_m = -1) {
   // sharded: this rank's slices [mp_lo, mp_hi) of every term, columns compacted
@@ -217,7 +227,9 @@ Split build_mp_w(tucker_handle* h, int n, int only_m = -1) {
   const int64_t rows = h->dims[n];
   const int64_t rows_pad = round_up(rows, 128), ld = round_up(K, 32);
   const size_t need = (size_t)(rows_pad * ld);
-  if (need > h->Whi.n) {
+  auto& wk = h->wkeep[n][only_m + 1];
+  const bool reuse = wk.need == need && wk.hi.p;
+  if (!reuse && need > h->Whi.n) {
     size_t free_b = 0, total_b = 0;
     TK_CUDA(cudaMemGetInfo(&free_b, &total_b));
     const double gb = 2.0 * (double)need * sizeof(float) / 1e9;
@@ -230,13 +242,34 @@ Split build_mp_w(tucker_handle* h, int n, int only_m = -1) {
       fail(TUCKER_E_OOM, msg);
     }
   }
-  h->Whi.ensure(need);
-  h->Wlo.ensure(need);
-  TK_CUDA(cudaMemsetAsync(h->Whi.p, 0, need * sizeof(float), h->st));
-  TK_CUDA(cudaMemsetAsync(h->Wlo.p, 0, need * sizeof(float), h->st));
+  float* whi = nullptr;
+  float* wlo = nullptr;
+  if (reuse) {
+    whi = wk.hi.p;  // same pattern: zeros still in place
+    wlo = wk.lo.p;
+  } else {
+    size_t free_b = 0, total_b = 0;
+    TK_CUDA(cudaMemGetInfo(&free_b, &total_b));
+    const size_t bytes = 2 * need * sizeof(float);
+    if (!wk.hi.p && h->wkeep_bytes + bytes <= total_b / 4 && bytes + total_b / 8 <= free_b) {
+      wk.hi.alloc(need);
+      wk.lo.alloc(need);
+      wk.need = need;
+      h->wkeep_bytes += bytes;
+      whi = wk.hi.p;
+      wlo = wk.lo.p;
+    } else {
+      h->Whi.ensure(need);
+      h->Wlo.ensure(need);
+      whi = h->Whi.p;
+      wlo = h->Wlo.p;
+    }
+    TK_CUDA(cudaMemsetAsync(whi, 0, need * sizeof(float), h->st));
+    TK_CUDA(cudaMemsetAsync(wlo, 0, need * sizeof(float), h->st));
+  }
   Split W;
-  W.hi = h->Whi.p;
-  W.lo = h->Wlo.p;
+  W.hi = whi;
+  W.lo = wlo;
   W.rows = rows;
   W.cols = K;
   W.ld = ld;
