@@ -257,7 +257,8 @@ int tucker_shard_bounds(const double* work, int64_t n, int world, int64_t* bound
  *   int fn(void* dev_buf, int64_t count, int dtype, void* stream, void* user)
  * that replaces dev_buf (count elements, dtype 0 = fp32, 1 = fp64, device
  * memory of this rank) by its sum over the ranks and returns 0; the library
- * synchronises its stream before the call.  Set it before the first sweep.
+ * synchronises its stream before the call and the whole device after it (the
+ * callback may write the result back on any stream).  Set it before the first sweep.
  * TUCKER_E_ARG for a handle without host collectives. */
 int tucker_set_allreduce(tucker_handle* h, void* fn, void* user);
 

@@ -110,6 +110,10 @@ static void allreduce(void* comm, void* p, int64_t n, int dtype, cudaStream_t st
   if (!c->cb) fail(TUCKER_E_STATE, "host collectives: no allreduce callback (tucker_set_allreduce)");
   TK_CUDA(cudaStreamSynchronize(st));
   if (c->cb(p, n, dtype, (void*)st, c->user) != 0) fail(TUCKER_E_NCCL, "host allreduce callback failed");
+  // the callback may write the result back on any stream (e.g. a pageable
+  // cudaMemcpy, whose DMA can still be in flight when it returns): wait for the
+  // whole device before the handle's stream reads the buffer
+  TK_CUDA(cudaDeviceSynchronize());
 }
 
 void dist_allreduce_f32(void* comm, float* p, int64_t n, cudaStream_t st) { allreduce(comm, p, n, 0, st); }

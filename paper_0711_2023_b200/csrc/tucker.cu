@@ -47,8 +47,8 @@ struct tucker_handle {
   EigSlot slots[3][kMaxOrder];  // warm starts: [0] HOOI, [1] MP, [2] SP
   double last_g2 = 0;           // ||G||_F^2 of the last core (SP's Delta_G rule)
   DBuf<double> theta_d;
-  DBuf<int> info_d;
-  EigSlot* last_slot = nullptr;
+  DBuf<int> info_d;                        // eigensolver info records (16 ints each)
+  EigSlot* rec_slot[kMaxOrder + 1] = {};   // slot of each record: [n] sweep mode n, [kMaxOrder] one-off
   EigSlot scratch_slot;
   EigWs eig;
   GramWs gram;
@@ -288,12 +288,14 @@ Split build_mp_w(tucker_handle* h, int n, int only_m = -1) {
 // Leading eigenvectors of S (padded layout, eig_layout) -> fp64 V (d x J) in
 // h->V, eigenvalues in h->theta_d (device): the persistent fused solver.
 // hint: the current factor (fp32 d x J) seeds a cold slot's basis (S is I_n x I_n)
-void solve_eig(tucker_handle* h, int64_t d, int J, EigSlot& slot, const float* hint = nullptr) {
+// rec: info record (sweeps: the mode, so one host sync per sweep reads them all)
+void solve_eig(tucker_handle* h, int64_t d, int J, EigSlot& slot, const float* hint = nullptr,
+               int rec = kMaxOrder) {
   h->V.ensure((size_t)(d * J));
   h->theta_d.ensure((size_t)J);
-  h->info_d.ensure(16);  // 8 ints + 4 doubles
-  h->last_slot = &slot;
-  eig_fused(h->S.p, d, J, slot, h->eig, eig_opts(h), h->V.p, h->theta_d.p, h->info_d.p, h->st, hint);
+  h->info_d.ensure(16 * (kMaxOrder + 1));  // per record: 8 ints + 4 doubles
+  h->rec_slot[rec] = &slot;
+  eig_fused(h->S.p, d, J, slot, h->eig, eig_opts(h), h->V.p, h->theta_d.p, h->info_d.p + 16 * rec, h->st, hint);
 }
 
 // S buffer in the eigensolver's padded layout; returns its row stride
@@ -304,37 +306,58 @@ int64_t ensure_S(tucker_handle* h, int64_t d) {
   return ls;
 }
 
-// after the stream is synchronised: fold the solver's info into the handle
-void eig_check(tucker_handle* h) {
-  int info[16];
-  TK_CUDA(cudaMemcpy(info, h->info_d.p, 16 * sizeof(int), cudaMemcpyDeviceToHost));
-  if (h->last_slot) {
-    double dv[2];
-    std::memcpy(dv, info + 8, sizeof(dv));
-    if (dv[0] >= 0) h->last_slot->lmin = dv[0];  // a new Lanczos estimate (0: none useful)
-    if (dv[1] > 0) h->last_slot->bval = dv[1];
+// after the stream is synchronised: fold the solver's info records [r0, r1) into
+// the handle (the Lanczos / filter-bound estimates go back to each record's slot)
+void eig_check(tucker_handle* h, int r0 = kMaxOrder, int r1 = kMaxOrder + 1) {
+  int info[16 * (kMaxOrder + 1)];
+  TK_CUDA(cudaMemcpy(info + 16 * r0, h->info_d.p + 16 * r0, 16 * (r1 - r0) * sizeof(int),
+                     cudaMemcpyDeviceToHost));
+  for (int r = r0; r < r1; ++r) {
+    const int* in = info + 16 * r;
+    if (EigSlot* sl = h->rec_slot[r]) {
+      double dv[2];
+      std::memcpy(dv, in + 8, sizeof(dv));
+      if (dv[0] >= 0) sl->lmin = dv[0];  // a new Lanczos estimate (0: none useful)
+      if (dv[1] > 0) sl->bval = dv[1];
+    }
+    if (in[4]) fail(TUCKER_E_CUDA, "eigensolver breakdown (non-finite Rayleigh quotient)");
+    if (!in[0]) h->eig_unconverged = true;
+    h->eig.stat_outer += in[1];
+    h->eig.stat_matvec += in[2];
+    h->eig.stat_sweeps += in[3];
   }
-  if (info[4]) fail(TUCKER_E_CUDA, "eigensolver breakdown (non-finite Rayleigh quotient)");
-  if (!info[0]) h->eig_unconverged = true;
-  h->eig.stat_outer += info[1];
-  h->eig.stat_matvec += info[2];
-  h->eig.stat_sweeps += info[3];
 }
+
+// timing events of one sweep (recorded on the handle stream, read after its one sync)
+struct SweepEvents {
+  std::vector<cudaEvent_t> e;
+  explicit SweepEvents(int n) : e((size_t)n, nullptr) {
+    for (auto& x : e) TK_CUDA(cudaEventCreate(&x));
+  }
+  ~SweepEvents() {
+    for (auto x : e)
+      if (x) cudaEventDestroy(x);
+  }
+  SweepEvents(const SweepEvents&) = delete;
+  SweepEvents& operator=(const SweepEvents&) = delete;
+  float ms(int i, int j) const {
+    float t = 0;
+    TK_CUDA(cudaEventElapsedTime(&t, e[i], e[j]));
+    return t;
+  }
+};
 
 // U_n from the eigenvectors of the Gram of the split matrix A (= Y, Y^T or W)
 // Sharded: a partial Gram (MP: this rank's W columns; HOOI Y^T Y route: this
 // rank's K range of Y^T, rounded out to 32 columns -- the other ranks' columns
 // in the rounding are zero here) summed by an fp64 allreduce.
-void update_factor(tucker_handle* h, int n, const Split& A, bool transposed, EigSlot& slot,
-                   float* ms_gram, float* ms_eig, bool partial_gram) {
+// ev_gram (nullable) is recorded after the Gram; the solver writes info record n
+// (no host synchronisation here: the sweep reads its records once, at its end)
+void update_factor(tucker_handle* h, int n, const Split& A, bool transposed, EigSlot& slot, cudaEvent_t ev_gram,
+                   bool partial_gram) {
   const int64_t d = A.rows;
   const int J = (int)h->J[n];
   const int64_t lds = ensure_S(h, d);
-  cudaEvent_t e0, e1, e2;
-  TK_CUDA(cudaEventCreate(&e0));
-  TK_CUDA(cudaEventCreate(&e1));
-  TK_CUDA(cudaEventCreate(&e2));
-  TK_CUDA(cudaEventRecord(e0, h->st));
   if (partial_gram && transposed) {
     const int64_t lo = h->hooi_lo[n], hi = h->hooi_hi[n];
     const int64_t k0 = std::min(A.ld, lo / 32 * 32), k1 = std::min(A.ld, round_up(std::max(hi, lo), 32));
@@ -348,8 +371,8 @@ void update_factor(tucker_handle* h, int n, const Split& A, bool transposed, Eig
     gram_syrk(A, h->S.p, lds, h->gram, h->st);
   }
   if (partial_gram) dist_allreduce_f64(h->comm, h->S.p, d * lds, h->st);
-  TK_CUDA(cudaEventRecord(e1, h->st));
-  solve_eig(h, d, J, slot, transposed ? nullptr : h->U[n].p);
+  if (ev_gram) TK_CUDA(cudaEventRecord(ev_gram, h->st));
+  solve_eig(h, d, J, slot, transposed ? nullptr : h->U[n].p, n);
   if (!transposed) {
     canon_to_f32(h->V.p, J, d, J, h->U[n].p, h->st);
   } else {
@@ -367,17 +390,6 @@ void update_factor(tucker_handle* h, int n, const Split& A, bool transposed, Eig
     cholqr2(h->Ufull.p, J, I, J, h->eig, h->st);
     canon_to_f32(h->Ufull.p, J, I, J, h->U[n].p, h->st);
   }
-  TK_CUDA(cudaEventRecord(e2, h->st));
-  TK_CUDA(cudaEventSynchronize(e2));
-  eig_check(h);
-  float a = 0, b = 0;
-  TK_CUDA(cudaEventElapsedTime(&a, e0, e1));
-  TK_CUDA(cudaEventElapsedTime(&b, e1, e2));
-  if (ms_gram) *ms_gram += a;
-  if (ms_eig) *ms_eig += b;
-  cudaEventDestroy(e0);
-  cudaEventDestroy(e1);
-  cudaEventDestroy(e2);
 }
 
 // G_(N) = U_N^T Y_(N) from h->Y (must be the projection of the last mode with
@@ -702,37 +714,31 @@ int hooi_sweep(tucker_handle* h, int sweeps, double* fit_per_sweep, float* stage
   if (!h || sweeps < 1) return TUCKER_E_ARG;
   return guarded(h, [&]() -> int {
     h->eig_unconverged = false;
+    const int N = h->order;
+    // events per mode: [4n] start, [4n+1] projected, [4n+2] Gram, [4n+3] factor; [4N], [4N+1] core
+    SweepEvents ev(4 * N + 2);
     for (int s = 0; s < sweeps; ++s) {
-      float ms[4] = {0, 0, 0, 0};
-      for (int n = 0; n < h->order; ++n) {
+      for (int n = 0; n < N; ++n) {
         const bool tr = prod_J_except(h, n) < h->dims[n];  // Y^T Y is the smaller Gram
-        cudaEvent_t a, b;
-        TK_CUDA(cudaEventCreate(&a));
-        TK_CUDA(cudaEventCreate(&b));
-        TK_CUDA(cudaEventRecord(a, h->st));
+        TK_CUDA(cudaEventRecord(ev.e[4 * n], h->st));
         project_hooi(h, n, tr);
-        TK_CUDA(cudaEventRecord(b, h->st));
-        TK_CUDA(cudaEventSynchronize(b));
-        float t = 0;
-        TK_CUDA(cudaEventElapsedTime(&t, a, b));
-        ms[0] += t;
-        cudaEventDestroy(a);
-        cudaEventDestroy(b);
-        update_factor(h, n, h->Y, tr, h->slots[0][n], &ms[1], &ms[2], h->sharded && tr);
+        TK_CUDA(cudaEventRecord(ev.e[4 * n + 1], h->st));
+        update_factor(h, n, h->Y, tr, h->slots[0][n], ev.e[4 * n + 2], h->sharded && tr);
+        TK_CUDA(cudaEventRecord(ev.e[4 * n + 3], h->st));
       }
-      // G_(N) = U_N^T Y_(N) is free after the last mode (Fig. 4)
-      cudaEvent_t a, b;
-      TK_CUDA(cudaEventCreate(&a));
-      TK_CUDA(cudaEventCreate(&b));
-      TK_CUDA(cudaEventRecord(a, h->st));
+      // G_(N) = U_N^T Y_(N) is free after the last mode (Fig. 4); reading
+      // the fit is the sweep's one host synchronisation
+      TK_CUDA(cudaEventRecord(ev.e[4 * N], h->st));
       const double fit = core_from_y(h);
-      TK_CUDA(cudaEventRecord(b, h->st));
-      TK_CUDA(cudaEventSynchronize(b));
-      float t = 0;
-      TK_CUDA(cudaEventElapsedTime(&t, a, b));
-      ms[3] += t;
-      cudaEventDestroy(a);
-      cudaEventDestroy(b);
+      TK_CUDA(cudaEventRecord(ev.e[4 * N + 1], h->st));
+      TK_CUDA(cudaEventSynchronize(ev.e[4 * N + 1]));
+      eig_check(h, 0, N);
+      float ms[4] = {0, 0, 0, ev.ms(4 * N, 4 * N + 1)};
+      for (int n = 0; n < N; ++n) {
+        ms[0] += ev.ms(4 * n, 4 * n + 1);
+        ms[1] += ev.ms(4 * n + 1, 4 * n + 2);
+        ms[2] += ev.ms(4 * n + 2, 4 * n + 3);
+      }
       if (fit_per_sweep) fit_per_sweep[s] = fit;
       if (stage_ms)
         for (int q = 0; q < 4; ++q) stage_ms[4 * s + q] = ms[q];
@@ -746,37 +752,27 @@ int mp_sweep(tucker_handle* h, int sweeps, double* fit_per_sweep, float* stage_m
   return guarded(h, [&]() -> int {
     h->eig_unconverged = false;
     h->G_valid = false;
+    const int N = h->order;
+    SweepEvents ev(4 * N + 2);
     for (int s = 0; s < sweeps; ++s) {
-      float ms[4] = {0, 0, 0, 0};
-      for (int n = 0; n < h->order; ++n) {
-        cudaEvent_t a, b;
-        TK_CUDA(cudaEventCreate(&a));
-        TK_CUDA(cudaEventCreate(&b));
-        TK_CUDA(cudaEventRecord(a, h->st));
+      for (int n = 0; n < N; ++n) {
+        TK_CUDA(cudaEventRecord(ev.e[4 * n], h->st));
         Split W = build_mp_w(h, n);
-        TK_CUDA(cudaEventRecord(b, h->st));
-        TK_CUDA(cudaEventSynchronize(b));
-        float t = 0;
-        TK_CUDA(cudaEventElapsedTime(&t, a, b));
-        ms[0] += t;
-        cudaEventDestroy(a);
-        cudaEventDestroy(b);
-        update_factor(h, n, W, false, h->slots[1][n], &ms[1], &ms[2], h->sharded);
+        TK_CUDA(cudaEventRecord(ev.e[4 * n + 1], h->st));
+        update_factor(h, n, W, false, h->slots[1][n], ev.e[4 * n + 2], h->sharded);
+        TK_CUDA(cudaEventRecord(ev.e[4 * n + 3], h->st));
       }
       h->G_valid = false;
-      if (fit_per_sweep) {
-        cudaEvent_t a, b;
-        TK_CUDA(cudaEventCreate(&a));
-        TK_CUDA(cudaEventCreate(&b));
-        TK_CUDA(cudaEventRecord(a, h->st));
-        fit_per_sweep[s] = compute_core(h);
-        TK_CUDA(cudaEventRecord(b, h->st));
-        TK_CUDA(cudaEventSynchronize(b));
-        float t = 0;
-        TK_CUDA(cudaEventElapsedTime(&t, a, b));
-        ms[3] += t;
-        cudaEventDestroy(a);
-        cudaEventDestroy(b);
+      TK_CUDA(cudaEventRecord(ev.e[4 * N], h->st));
+      if (fit_per_sweep) fit_per_sweep[s] = compute_core(h);
+      TK_CUDA(cudaEventRecord(ev.e[4 * N + 1], h->st));
+      TK_CUDA(cudaEventSynchronize(ev.e[4 * N + 1]));  // the sweep's one host synchronisation
+      eig_check(h, 0, N);
+      float ms[4] = {0, 0, 0, ev.ms(4 * N, 4 * N + 1)};
+      for (int n = 0; n < N; ++n) {
+        ms[0] += ev.ms(4 * n, 4 * n + 1);
+        ms[1] += ev.ms(4 * n + 1, 4 * n + 2);
+        ms[2] += ev.ms(4 * n + 2, 4 * n + 3);
       }
       if (stage_ms)
         for (int q = 0; q < 4; ++q) stage_ms[4 * s + q] = ms[q];
@@ -802,35 +798,27 @@ int sp_sweep(tucker_handle* h, int sweeps, double* fits, double* gnorms, float* 
   if (!h || sweeps < 1) return TUCKER_E_ARG;
   return guarded(h, [&]() -> int {
     h->eig_unconverged = false;
+    const int N = h->order;
+    SweepEvents ev(4 * N + 2);
     for (int s = 0; s < sweeps; ++s) {
-      float ms[4] = {0, 0, 0, 0};
-      for (int n = 0; n < h->order; ++n) {
-        cudaEvent_t a, b;
-        TK_CUDA(cudaEventCreate(&a));
-        TK_CUDA(cudaEventCreate(&b));
-        TK_CUDA(cudaEventRecord(a, h->st));
-        Split W = build_mp_w(h, n, (n + h->order - 1) % h->order);
-        TK_CUDA(cudaEventRecord(b, h->st));
-        TK_CUDA(cudaEventSynchronize(b));
-        float t = 0;
-        TK_CUDA(cudaEventElapsedTime(&t, a, b));
-        ms[0] += t;
-        cudaEventDestroy(a);
-        cudaEventDestroy(b);
-        update_factor(h, n, W, false, h->slots[2][n], &ms[1], &ms[2], h->sharded);
+      for (int n = 0; n < N; ++n) {
+        TK_CUDA(cudaEventRecord(ev.e[4 * n], h->st));
+        Split W = build_mp_w(h, n, (n + N - 1) % N);
+        TK_CUDA(cudaEventRecord(ev.e[4 * n + 1], h->st));
+        update_factor(h, n, W, false, h->slots[2][n], ev.e[4 * n + 2], h->sharded);
+        TK_CUDA(cudaEventRecord(ev.e[4 * n + 3], h->st));
       }
-      cudaEvent_t a, b;
-      TK_CUDA(cudaEventCreate(&a));
-      TK_CUDA(cudaEventCreate(&b));
-      TK_CUDA(cudaEventRecord(a, h->st));
-      const double fit = compute_core(h);
-      TK_CUDA(cudaEventRecord(b, h->st));
-      TK_CUDA(cudaEventSynchronize(b));
-      float t = 0;
-      TK_CUDA(cudaEventElapsedTime(&t, a, b));
-      ms[3] += t;
-      cudaEventDestroy(a);
-      cudaEventDestroy(b);
+      TK_CUDA(cudaEventRecord(ev.e[4 * N], h->st));
+      const double fit = compute_core(h);  // synchronises (the fit is read on the host)
+      TK_CUDA(cudaEventRecord(ev.e[4 * N + 1], h->st));
+      TK_CUDA(cudaEventSynchronize(ev.e[4 * N + 1]));
+      eig_check(h, 0, N);
+      float ms[4] = {0, 0, 0, ev.ms(4 * N, 4 * N + 1)};
+      for (int n = 0; n < N; ++n) {
+        ms[0] += ev.ms(4 * n, 4 * n + 1);
+        ms[1] += ev.ms(4 * n + 1, 4 * n + 2);
+        ms[2] += ev.ms(4 * n + 2, 4 * n + 3);
+      }
       if (fits) fits[s] = fit;
       if (gnorms) gnorms[s] = std::sqrt(h->last_g2);
       if (stage_ms)
