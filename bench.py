@@ -415,7 +415,9 @@ def run_ours(args):
         "value": value, "unit": "Gnnz/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
         "scaling": "strong" if sharded else "weak", "vs_baseline": None,
-        "dtype": "f32 storage, 3xTF32/f64 Gram, f64 eig",
+        "dtype": "f64",  # the eigensolver (~3/4 of the step), Gram accumulation and fit compute in fp64
+        "dtype_detail": "fp32 storage and SpTTMc/SpMM, 3xTF32 or fp64-DMMA Gram products with fp64 accumulation, "
+                        "fp64 eigensolver",
         "data": "synthetic",
         "config": {"workload": c["name"], "l2": "flushed (512 MB write) before every timed step",
                    "parallelism": (f"sharded x{world}: HOOI by mode-n slice ranges, MP by slice-index ranges; "
