@@ -643,6 +643,15 @@ __device__ __forceinline__ double rsqrt_nt(double x) {
 // pivots).  Then M = D E^T P^{-1/2} (upper triangular) satisfies M^T G M = I,
 // written to X (smem, ld): Q M has orthonormal columns (CholQR).  One barrier
 // per elimination step.
+// 1/x from the fp64 reciprocal approximation plus two Newton steps (x > 0
+// normal): a short dependency chain on the elimination's critical path
+__device__ __forceinline__ double rcp_nt64(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  r = r * fma(-x, r, 2.0);
+  r = r * fma(-x, r, 2.0);
+  return r;
+}
 __device__ void cholqr_factor(const Ctx& x, double* A, double* X, int k, int ld, double shift) {
   __shared__ double dsc[kMaxBlock];
   __shared__ double piv[kMaxBlock];
@@ -666,10 +675,10 @@ __device__ void cholqr_factor(const Ctx& x, double* A, double* X, int k, int ld,
   int j = 0;
   for (; j + 2 < k; j += 2) {
     const double a00 = A[j * ld + j], a01 = A[j * ld + j + 1], a11 = A[(j + 1) * ld + j + 1];
-    const double ip0 = 1.0 / (a00 > 1e-12 ? a00 : 1e-12);
+    const double ip0 = rcp_nt64(a00 > 1e-12 ? a00 : 1e-12);
     const double f1 = a01 * ip0;
     const double p1 = fma(-f1, a01, a11);
-    const double ip1 = 1.0 / (p1 > 1e-12 ? p1 : 1e-12);
+    const double ip1 = rcp_nt64(p1 > 1e-12 ? p1 : 1e-12);
     if (jd >= 0 && x.warp == NW - 1) {  // deferred: row jd (= previous j + 1)
       double* el = X + jd * ld;
       const double* ej = X + (jd - 1) * ld;
@@ -707,7 +716,7 @@ __device__ void cholqr_factor(const Ctx& x, double* A, double* X, int k, int ld,
   }
   for (; j < k - 1; ++j) {  // a last single step (k - 1 odd)
     const double pj = A[j * ld + j];
-    const double ip = 1.0 / (pj > 1e-12 ? pj : 1e-12);
+    const double ip = rcp_nt64(pj > 1e-12 ? pj : 1e-12);
     for (int l = j + 1 + x.warp; l < k; l += NW) {
       const double f = A[j * ld + l] * ip;
       double* al = A + l * ld;
