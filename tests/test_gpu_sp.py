@@ -97,3 +97,47 @@ def test_hosvd_and_sp_bitwise_deterministic(capi):
             assert all(np.array_equal(u, v) for u, v in zip(x, y))
         else:
             assert np.array_equal(np.asarray(x), np.asarray(y))
+
+
+@pytest.mark.parametrize("dims,nnz,core", [((100, 100, 100), 10_000, (10, 10, 10)),
+                                           ((20, 22, 18, 16), 12_000, (4, 5, 3, 6))])
+def test_kept_w_buffers_across_algorithms(capi, dims, nnz, core):
+    """W_n buffers are kept per (mode, term set) and not re-zeroed (their zero
+    blocks depend only on the tensor): interleaving MP and SP on one handle
+    must give bit-identical results to fresh handles (set_factors resets the
+    warm-start slots, so every run starts cold)."""
+    idx, vals = uniform_distinct_coo(dims, nnz, np.random.default_rng(91))
+    U0 = [random_orthonormal(I, J, np.random.default_rng(92 + k)) for k, (I, J) in enumerate(zip(dims, core))]
+    C0 = sp_random_init(dims[-1], core[-1], np.random.default_rng(93)).astype(np.float32)
+
+    def mp(t):
+        t.set_factors(U0)
+        fits = t.mp_sweep(2)
+        G, U, fit = t.core_and_fit()
+        return fits, G, U
+
+    def sp(t):
+        t.set_factors(U0)
+        t.set_factor(len(dims) - 1, C0, check=False)
+        fits, gn, _ = t.sp_sweep(2)
+        G, U, fit = t.core_and_fit()
+        return fits, G, U
+
+    def same(a, b):
+        fa, Ga, Ua = a
+        fb, Gb, Ub = b
+        assert np.array_equal(fa, fb)
+        assert np.array_equal(Ga, Gb)
+        assert all(np.array_equal(x, y) for x, y in zip(Ua, Ub))
+
+    with capi.Tucker(dims, core, idx, vals, U0) as t:
+        mp1 = mp(t)
+        sp1 = sp(t)
+        mp2 = mp(t)
+    with capi.Tucker(dims, core, idx, vals, U0) as t:
+        mp_fresh = mp(t)
+    with capi.Tucker(dims, core, idx, vals, U0) as t:
+        sp_fresh = sp(t)
+    same(mp1, mp2)
+    same(mp1, mp_fresh)
+    same(sp1, sp_fresh)
