@@ -141,3 +141,30 @@ def test_kept_w_buffers_across_algorithms(capi, dims, nnz, core):
     same(mp1, mp2)
     same(mp1, mp_fresh)
     same(sp1, sp_fresh)
+
+
+def test_unconverged_solve_is_reported(capi):
+    """The sweeps read every mode's solver info once, at the end of the sweep:
+    a solve that cannot converge (one outer iteration, tol 1e-15) must still
+    surface as TUCKER_E_CONVERGE (with finite results); default options as 0."""
+    dims, core = (100, 100, 100), (10, 10, 10)
+    idx, vals = uniform_distinct_coo(dims, 10_000, np.random.default_rng(95))
+    U0 = [random_orthonormal(I, J, np.random.default_rng(96 + k)) for k, (I, J) in enumerate(zip(dims, core))]
+    h = capi.tucker_init(dims, core, idx, vals, U0, eig_max_iter=1, eig_tol=1e-15)
+    try:
+        fits, _, rc = capi.hooi_sweep(h, 2, want_stage=True)
+        assert rc == capi.E_CONVERGE and np.all(np.isfinite(fits))
+        capi.tucker_set_factors(h, U0)
+        fits, _, rc = capi.mp_sweep(h, 2, want_stage=True)
+        assert rc == capi.E_CONVERGE and np.all(np.isfinite(fits))
+    finally:
+        capi.tucker_free(h)
+    h = capi.tucker_init(dims, core, idx, vals, U0)
+    try:
+        _, _, rc = capi.hooi_sweep(h, 2, want_stage=True)
+        assert rc == 0
+        capi.tucker_set_factors(h, U0)
+        _, _, rc = capi.mp_sweep(h, 2, want_stage=True)
+        assert rc == 0
+    finally:
+        capi.tucker_free(h)
