@@ -2,6 +2,7 @@
 // per-sweep orchestration of the kernels in csf.cu / spttmc.cu / gram*.cu /
 // eig.cu / dense.cu.
 #include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <cmath>
 #include <cstdlib>
@@ -31,13 +32,15 @@ struct tucker_handle {
   DBuf<float> Yhi, Ylo, Whi, Wlo;
   // W_n per (mode, term set): W's zero blocks depend only on the tensor, and the
   // SpMM rewrites every present block in full, so a kept buffer needs no memset
-  // on later builds (kept while the buffers fit a quarter of the device memory)
+  // on later builds (kept while all handles' kept buffers fit a quarter of the
+  // device memory)
   struct WKeep {
     DBuf<float> hi, lo;
     size_t need = 0;
   };
   WKeep wkeep[kMaxOrder][kMaxOrder + 1];
-  size_t wkeep_bytes = 0;
+  size_t wkeep_bytes = 0;  // this handle's share of g_wkeep_bytes (returned when it is freed)
+  ~tucker_handle();
   Split Y;  // last HOOI projection (mode Y_mode)
   int Y_mode = -1;
   bool Y_transposed = false;
@@ -64,6 +67,10 @@ struct tucker_handle {
   int64_t mp_lo[kMaxOrder][kMaxOrder] = {}, mp_hi[kMaxOrder][kMaxOrder] = {};       // slices of MP term (n, m)
   bool Y_partial = false;  // h->Y holds only this rank's rows (Y^T Y route, not gathered)
 };
+// kept W buffers of all live handles in this process (budget: a quarter of the device)
+static std::atomic<size_t> g_wkeep_bytes{0};
+tucker_handle::~tucker_handle() { g_wkeep_bytes -= wkeep_bytes; }
+
 
 namespace {
 
@@ -251,11 +258,12 @@ Split build_mp_w(tucker_handle* h, int n, int only_m = -1) {
     size_t free_b = 0, total_b = 0;
     TK_CUDA(cudaMemGetInfo(&free_b, &total_b));
     const size_t bytes = 2 * need * sizeof(float);
-    if (!wk.hi.p && h->wkeep_bytes + bytes <= total_b / 4 && bytes + total_b / 8 <= free_b) {
+    if (!wk.hi.p && g_wkeep_bytes.load() + bytes <= total_b / 4 && bytes + total_b / 8 <= free_b) {
       wk.hi.alloc(need);
       wk.lo.alloc(need);
       wk.need = need;
       h->wkeep_bytes += bytes;
+      g_wkeep_bytes += bytes;
       whi = wk.hi.p;
       wlo = wk.lo.p;
     } else {
