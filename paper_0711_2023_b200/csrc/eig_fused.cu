@@ -70,7 +70,7 @@ struct FusedArgs {
   int lanczos;              // estimate lambda_min (Lanczos) for the filter's lower bound
   double lmin_hint;         // else: lower bound carried over from the slot's last solve (0: none)
   double tol;
-  int max_outer, jsweeps;
+  int max_outer, jsweeps, jsweeps0;
   uint64_t seed;
   int dbg;
 };
@@ -1100,7 +1100,7 @@ __global__ void __launch_bounds__(NT, 1) k_eig_fused(FusedArgs P) {
     // (rprev = max relative residual of the unconverged vectors after the last
     // RR) cannot matter yet; near convergence this is the strict 1e-13
     const double jtol = k == d ? 1e-15 : 1e-13;
-    const int sw = jacobi(x, x.r1s, ka, k == d ? 60 : (n_rr == 0 ? P.jsweeps + 1 : P.jsweeps), jtol,
+    const int sw = jacobi(x, x.r1s, ka, k == d ? 60 : (n_rr == 0 ? P.jsweeps0 : P.jsweeps), jtol,
                           th + nlock, perm, QR, SR, nrr, ldr);
     tick(PF_JAC);
     if (sw < 0) breakdown = 1;
@@ -1791,6 +1791,8 @@ bool eig_fused(double* S, int64_t d, int J, EigSlot& slot, EigWs& ws, const EigO
   if (const char* e = std::getenv("TUCKER_EIG_TOL")) a.tol = std::atof(e);  // experiments
   a.max_outer = o.max_outer;
   a.jsweeps = o.jacobi_sweeps;
+  a.jsweeps0 = o.jacobi_sweeps_first;
+  if (const char* e = std::getenv("TUCKER_EIG_JSW0")) a.jsweeps0 = std::atoi(e);  // experiments
   if (const char* e = std::getenv("TUCKER_EIG_JSW")) a.jsweeps = std::atoi(e);  // experiments
   a.seed = 0x5eed0000ull + (uint64_t)d * 131 + (uint64_t)J;
   static const bool dbg = std::getenv("TUCKER_EIG_DEBUG") != nullptr;

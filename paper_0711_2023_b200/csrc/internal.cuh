@@ -156,7 +156,8 @@ struct EigWs {
 struct EigOpts {
   int oversample = 0;
   int max_outer = 40;
-  int jacobi_sweeps = 2;  // cap per Rayleigh-Ritz step (residuals decide convergence)
+  int jacobi_sweeps = 2;        // cap per Rayleigh-Ritz step (residuals decide convergence)
+  int jacobi_sweeps_first = 1;  // cap for a solve's first Rayleigh-Ritz step (measured best at config 2)
   double tol = 1e-10;
 };
 // Leading J eigenvectors of symmetric PSD S (d x d in the padded layout of
