@@ -62,6 +62,7 @@ struct FusedArgs {
   double* mpart;            // [KB][RPX][LB] split-K partial products
   double* basis;            // d x LB warm-start basis (read if warm, always written)
   int warm;
+  int warm_exact;           // basis = the slot's previous [L | Q] (orthonormal): no initial CholQR
   double* outV;             // d x J output (ld = J)
   double* theta_out;        // J
   long long* prof;          // [8] per-phase ns (CTA 0's view), accumulated; [8] algorithmic flops
@@ -1359,7 +1360,9 @@ __global__ void __launch_bounds__(NT, 1) k_eig_fused(FusedArgs P) {
     if (P.dbg && x.cta == 0 && x.tid == 0) printf("[eigf] lanczos lambda_min ~ %.6e\n", a_lo);
   }
 
-  orth_active(2, true);
+  // an exact warm basis is the previous solve's orthonormal [L | Q]; a seeded
+  // (fp32 hint + pseudo-random) or random block is orthonormalised first
+  orth_active(P.warm_exact ? 0 : 2, true);
   rayleigh_ritz();
   if (P.dbg && x.cta == 0 && x.tid == 0) {
     printf("[eigf] first RR warm=%d\n", P.warm);
@@ -1769,6 +1772,7 @@ bool eig_fused(double* S, int64_t d, int J, EigSlot& slot, EigWs& ws, const EigO
   }
   a.basis = slot.basis.p;
   a.warm = (slot.valid && slot.d == d && slot.k == k) ? 1 : 0;
+  a.warm_exact = a.warm;
   if (!a.warm && hint) {  // cold slot: start from the caller's current factor
     TK_LAUNCH(k_seed_basis, 2 * grid, 256, 0, st, slot.basis.p, d, LB, k, hint, J,
               0x5eedb0000ull + (uint64_t)d * 131 + (uint64_t)J);
