@@ -37,7 +37,10 @@ def parse():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--config", type=int, default=4,
+                    help="BASELINE.json config of the timed step (default 4: the largest single-GPU config)")
+    ap.add_argument("--spttmc-configs", default="1,2,3,4,5",
+                    help="configs of the per-mode SpTTMc roofline table ('' to skip)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--sharded", action="store_true",
@@ -115,6 +118,75 @@ def workload(k):
     return c
 
 
+def compute_peaks():
+    """Measured compute peaks (tools/peaks.py on a B200 of this pool, committed under
+    profiles/); None where unmeasured."""
+    try:
+        return json.load(open(os.path.join(ROOT, "profiles", "measured_compute_peaks.json")))
+    except Exception:
+        return {}
+
+
+def spttmc_model(dims, core, layout):
+    """SURVEY §8(d) algorithmic work of the HOOI SpTTMc of each mode, on the CSF
+    ordering the library uses for it (tucker_csf_layout): bytes = CSF read (leaf id +
+    value 8 B per nonzero, fiber id + pointer 8 B per fiber, 8 B per order-4 node) +
+    Y_(n) written once in fp32 + one read of every other factor; flops = 2 J_leaf nnz
+    + 2 J_mid J_leaf fibers (order 4: 2 J_mid1 J_leaf fibers + 2 J_mid0 J_mid1 J_leaf
+    nodes).  Gathers served from L2 are not algorithmic bytes."""
+    out = []
+    for n, L in enumerate(layout):
+        oth = [q for q in range(len(dims)) if q != n]
+        P = int(np.prod([core[q] for q in oth]))
+        b = (8.0 * L["nnz"] + 8.0 * L["fibers"] + 8.0 * L["nodes"] + 4.0 * dims[n] * P
+             + sum(4.0 * dims[q] * core[q] for q in oth))
+        jl = core[L["leaf"]]
+        if L["mid1"] < 0:
+            fl = 2.0 * jl * L["nnz"] + 2.0 * core[L["mid0"]] * jl * L["fibers"]
+        else:
+            fl = (2.0 * jl * L["nnz"] + 2.0 * core[L["mid1"]] * jl * L["fibers"]
+                  + 2.0 * P * L["nodes"])
+        out.append((b, fl))
+    return out
+
+
+def spttmc_table(capi, configs, local, stream, pk, cpk):
+    """Per-config, per-mode HOOI SpTTMc time (tucker_time_ttmc: CUDA events on the
+    library stream, 5 back-to-back projections after an untimed one, random U0), with
+    Gnnz/s and the fractions of the HBM (measured copy bandwidth), FP32 (measured
+    FFMA) and 3xTF32 (measured tcgen05 kind::tf32 issue peak / 3) rooflines."""
+    import torch
+    from synth import make_config
+    rows = []
+    hbm = pk["hbm_gbs"] * 1e9
+    f32 = (cpk.get("ffma_tflops") or 148 * 128 * 2 * 1.965e9 / 1e12) * 1e12
+    tf3 = ((cpk.get("tcgen05_tf32_tflops") or pk["bf16_tflops"] * 1.1 / 2.25) / 3.0) * 1e12
+    for k in configs:
+        c = make_config(k, device="cuda" if k == 5 else None)
+        dims, core, nnz = c["dims"], c["core"], c["nnz"]
+        dev = torch.device("cuda", local)
+        idx = [torch.from_numpy(a).to(dev) for a in c["idx"]]
+        vals = torch.from_numpy(c["vals"]).to(dev)
+        U0 = [torch.from_numpy(u).to(dev) for u in c["U0"]]
+        del c
+        h = capi.tucker_init(dims, core, idx, vals, U0, device=local, stream=stream.cuda_stream, on_device=True)
+        del idx, vals
+        model = spttmc_model(dims, core, capi.tucker_csf_layout(h, len(dims)))
+        for n in range(len(dims)):
+            ms = capi.tucker_time_ttmc(h, n, 5)
+            b, fl = model[n]
+            t = ms / 1e3
+            rows.append({"config": k, "mode": n + 1, "ms": round(ms, 4), "gnnz_s": nnz / t / 1e9,
+                         "alg_bytes": b, "flops": fl, "hbm_frac": b / t / hbm, "fp32_frac": fl / t / f32,
+                         "tf32x3_frac": fl / t / tf3,
+                         "t_hbm_us": 1e6 * b / hbm, "t_fp32_us": 1e6 * fl / f32, "t_3xtf32_us": 1e6 * fl / tf3,
+                         "binding": "hbm" if b / hbm >= fl / tf3 else "tensor(3xTF32)",
+                         "binding_frac": max(b / hbm, fl / tf3) / t})
+        capi.tucker_free(h)
+        torch.cuda.empty_cache()
+    return rows
+
+
 def gram_flops(c):
     """Algorithmic flops of the Gram (SYRK, upper triangle incl. diagonal) per
     HOOI sweep and per MP sweep: d(d+1)K with d x K the Gram operand."""
@@ -140,6 +212,27 @@ def cpu_oracle_sample(c):
     O.run_mp(T, c["U0"], c["core"], 1)
     dt = time.perf_counter() - t0
     return dt, c["nnz"] * len(c["dims"]) * 2
+
+
+def host_info():
+    """CPU model and BLAS library of the host the oracle runs on."""
+    model = "unknown"
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                model = ln.split(":", 1)[1].strip()
+                break
+    except Exception:
+        pass
+    blas = "unknown"
+    try:
+        from threadpoolctl import threadpool_info
+        b = [i for i in threadpool_info() if i.get("user_api") == "blas"]
+        if b:
+            blas = f"{b[0].get('internal_api')} {b[0].get('version')} ({b[0].get('num_threads')} threads)"
+    except Exception:
+        pass
+    return {"cpu_model": model, "blas": blas, "host_cores": len(os.sched_getaffinity(0))}
 
 
 def cores_used():
@@ -348,8 +441,9 @@ def run_ours(args):
         e2e_med = float(t.item())
     e2e_val = units / (e2e_med / 1e3) / 1e9 * (1 if sharded else world)
 
-    # ---- roofline of the dominant kernel (the fused eigensolver) ----
+    # ---- roofline of the dominant kernel ----
     pk = peaks()
+    cpk = compute_peaks()
     shares = {"spttmc+spmm": (stage_acc[0] + stage_acc_mp[0]) / args.steps,
               "gram": (stage_acc[1] + stage_acc_mp[1]) / args.steps,
               "eig": (stage_acc[2] + stage_acc_mp[2]) / args.steps,
@@ -357,70 +451,64 @@ def run_ours(args):
     eig_ms = shares["eig"]
     eig_flops = st.get("eig_flops", 0) / args.steps
     launches_eig = 2 * N * S  # one k_eig_fused launch per factor update
-    fp64_peak = 148 * 64 * 2 * 1.965e9 / 1e12
+    fp64_peak = cpk.get("dmma_tflops") or 148 * 64 * 2 * 1.965e9 / 1e12
     achieved = eig_flops / (eig_ms / 1e3) / 1e12 if eig_ms > 0 else 0.0
-    traffic = None
-    try:  # per-launch DRAM bytes of k_eig_fused from the committed ncu --set full capture
-        traffic = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))["k_eig_fused"]
+    try:  # per-launch DRAM bytes from the committed ncu --set full captures
+        traffic_all = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
     except Exception:
-        traffic = None
-    roof = {"kernel": "k_eig_fused (persistent eigensolver: DMMA products, Jacobi RR, CholQR)",
-            "bound": "alu",
-            "peak_note": "fp64 nominal: 148 SMs x 64 FMA/clk x 2 x 1.965 GHz (B200_PROFILING clock); "
-                         "tools/microbench.cu measured 36.9 TFLOP/s DMMA",
-            "achieved": achieved, "peak": fp64_peak, "unit": "TFLOP/s", "frac": achieved / fp64_peak,
-            "traffic": traffic, "flops_per_launch": eig_flops / launches_eig,
-            "ms_per_launch": eig_ms / launches_eig, "launches_per_step": launches_eig,
-            "stage_ms_per_step": shares, "dominant_stage": max(shares, key=shares.get),
-            }
+        traffic_all = {}
+    roof_eig = {"kernel": "k_eig_fused (persistent eigensolver: DMMA products, Jacobi RR, CholQR)",
+                "bound": "alu",
+                "peak_note": ("fp64 DMMA measured (tools/peaks.cu, profiles/measured_compute_peaks.json)"
+                              if cpk.get("dmma_tflops") else
+                              "fp64 nominal: 148 SMs x 64 FMA/clk x 2 x 1.965 GHz (B200_PROFILING clock)"),
+                "achieved": achieved, "peak": fp64_peak, "unit": "TFLOP/s", "frac": achieved / fp64_peak,
+                "traffic": traffic_all.get("k_eig_fused"), "flops_per_launch": eig_flops / launches_eig,
+                "ms_per_launch": eig_ms / launches_eig, "launches_per_step": launches_eig,
+                "products_per_solve": st.get("eig_matvec", 0) / args.steps / launches_eig}
     phases = {k: v / args.steps for k, v in st.get("eig_phase_ms", {}).items()}
     if any(v > 0 for v in phases.values()):  # only in TK_EIG_PROFILE builds (tools/eig_profile.sh)
-        roof["eig_phase_ms_per_step"] = phases
-    # secondary: the Gram SYRK on the tensor cores
+        roof_eig["eig_phase_ms_per_step"] = phases
+    # the Gram SYRK: 3xTF32 on tcgen05 (MP) / fp64 DMMA (HOOI <= 2e10 FMA)
     hflops, mflops = gram_flops(c)
     gram_ms = shares["gram"]
     gram_flops_step = S * (hflops + mflops)
     g_ach = gram_flops_step / (gram_ms / 1e3) / 1e12 if gram_ms > 0 else 0.0
-    g_peak = pk["bf16_tflops"] * (1.1 / 2.25) / 3.0
-    # SpTTMc (HOOI projections): nonzeros per second and HBM fraction of its algorithmic bytes
-    # (CSF read 8 B/nnz + 12 B/fiber, split Y written 8 B/entry, factors read once)
-    hooi_proj_ms = stage_acc[0] / args.steps / S  # per HOOI sweep (N projections)
-    nfib = capi.tucker_csf_fibers(h, N)
-    ybytes = 0.0
-    for n in range(N):
-        P = int(np.prod([core[q] for q in range(N) if q != n]))
-        ybytes += 8.0 * dims[n] * P
-    alg_bytes = N * 8.0 * c["nnz"] + (12.0 * nfib if nfib else 0.0) + ybytes
-    # SpTTMc flop model: per mode 2 J_leaf nnz + 2 (prod_{q != n} J_q) F_n, with F_n the
-    # fibers of the ordering mode n uses and J_leaf the smaller J of the other modes (the leaf the flop model
-    # picks when the J are equal, as in config 2)
-    fibers = [st[0] for st in capi.tucker_csf_stats(h, N)]
-    sp_flops = 0.0
-    for n in range(N):
-        oth = [core[q] for q in range(N) if q != n]
-        sp_flops += 2.0 * min(oth) * c["nnz"] + 2.0 * float(np.prod(oth)) * fibers[n]
-    fp32_peak = 148 * 128 * 2 * 1.965e9 / 1e12  # FP32 FMA nominal (B200_PROFILING clock)
-    sp_tf = sp_flops / (hooi_proj_ms / 1e3) / 1e12 if hooi_proj_ms > 0 else None
-    spttmc = {"gnnz_s_per_mode": c["nnz"] * N / (hooi_proj_ms / 1e3) / 1e9 if hooi_proj_ms > 0 else None,
-              "alg_bytes_per_sweep": alg_bytes,
-              "hbm_frac": (alg_bytes / (hooi_proj_ms / 1e3)) / (pk["hbm_gbs"] * 1e9) if hooi_proj_ms > 0 else None,
-              "binding": "fp32 ALU + L2 gathers (139 flop/B at config 2)",
-              "fp32_tflops": sp_tf, "fp32_peak_tflops": fp32_peak,
-              "binding_frac": sp_tf / fp32_peak if sp_tf else None,
-              "note": "HOOI SpTTMc (k_spttmc3/4) per sweep; bound is FP32 ALU + L2 gathers at config 2 "
-                      "(139 flop/B), so the HBM fraction is small by construction (SURVEY §8d)"}
-    roof_gram = {"kernel": "k_syrk_tc (tcgen05 3xTF32 SYRK, fp64 drain)", "bound": "tensor",
-                 "peak_note": "measured bf16 burst x tf32/bf16 nominal (1.1/2.25) / 3 products",
+    tf32_peak = cpk.get("tcgen05_tf32_tflops") or pk["bf16_tflops"] * (1.1 / 2.25)
+    g_peak = tf32_peak / 3.0
+    roof_gram = {"kernel": "k_syrk_tc (tcgen05 3xTF32 SYRK, fp64 drain) + k_syrk_dmma", "bound": "tensor",
+                 "peak_note": ("measured tcgen05 kind::tf32 issue peak / 3 products (profiles/measured_compute_peaks.json)"
+                               if cpk.get("tcgen05_tf32_tflops") else
+                               "measured bf16 burst x tf32/bf16 nominal (1.1/2.25) / 3 products"),
                  "achieved": g_ach, "peak": g_peak, "unit": "TFLOP/s", "frac": g_ach / g_peak}
+    # HOOI SpTTMc of the timed workload (per sweep, all modes): §8(d) bytes / flops
+    layout = capi.tucker_csf_layout(h, N)
+    model = spttmc_model(dims, core, layout)
+    hooi_proj_ms = stage_acc[0] / args.steps / S
+    sp_bytes = sum(b for b, _ in model)
+    sp_flops = sum(f for _, f in model)
+    roof_sp = {"kernel": "k_spttmc3/k_spttmc4 (HOOI SpTTMc, all modes of one sweep)",
+               "bound": "hbm", "unit": "GB/s",
+               "achieved": sp_bytes / (hooi_proj_ms / 1e3) / 1e9 if hooi_proj_ms > 0 else None,
+               "peak": pk["hbm_gbs"], "alg_bytes": sp_bytes, "flops": sp_flops,
+               "ms_per_sweep": hooi_proj_ms,
+               "gnnz_s_per_mode": c["nnz"] * N / (hooi_proj_ms / 1e3) / 1e9 if hooi_proj_ms > 0 else None,
+               "traffic": traffic_all.get("k_spttmc4" if N == 4 else "k_spttmc3")}
+    roof_sp["frac"] = roof_sp["achieved"] / roof_sp["peak"] if roof_sp["achieved"] else None
+    dom = max(shares, key=shares.get)
+    roof = dict({"spttmc+spmm": roof_sp, "gram": roof_gram, "eig": roof_eig}.get(dom, roof_eig))
+    roof["dominant_stage"] = dom
+    roof["stage_ms_per_step"] = shares
 
     line = {
         "metric": "HOOI/MP sweep throughput (nnz x modes per second)",
         "value": value, "unit": "Gnnz/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
         "scaling": "strong" if sharded else "weak", "vs_baseline": None,
-        "dtype": "f64",  # the eigensolver (~3/4 of the step), Gram accumulation and fit compute in fp64
-        "dtype_detail": "fp32 storage and SpTTMc/SpMM, 3xTF32 or fp64-DMMA Gram products with fp64 accumulation, "
-                        "fp64 eigensolver",
+        "dtype": "f32+3xtf32+f64",
+        "dtype_detail": "mixed: fp32 storage and SpTTMc/SpMM arithmetic; Gram products 3xTF32 on tcgen05 (MP) or "
+                        "fp64 DMMA (HOOI Grams <= 2e10 FMA), both accumulated in fp64; fp64 eigensolver, core "
+                        "accumulation and fit",
         "data": "synthetic",
         "config": {"workload": c["name"], "l2": "flushed (512 MB write) before every timed step",
                    "parallelism": (f"sharded x{world}: HOOI by mode-n slice ranges, MP by slice-index ranges; "
@@ -441,16 +529,22 @@ def run_ours(args):
                 "h2d_bytes_per_step": int(h2d),
                 "d2h_bytes_per_step": int(d2h)},
         "roofline": roof,
+        "roofline_eig": roof_eig,
         "roofline_gram": roof_gram,
-        "spttmc": spttmc,
+        "roofline_spttmc": roof_sp,
         "clocks": clocks,
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         dt, u = cpu_oracle_sample(c)
         line["cpu_baseline"] = {"value": u / dt / 1e9, "unit": "Gnnz/s", "cores": cores_used(),
-                                "kind": "oracle",
+                                "kind": "oracle", "seconds": dt, **host_info(),
                                 "sample": "1 HOOI sweep + 1 MP sweep (+ cores) of the same workload"}
     capi.tucker_free(h)
+    if rank == 0 and world == 1 and args.spttmc_configs:
+        del idx_d, vals_d
+        torch.cuda.empty_cache()
+        line["spttmc_table"] = spttmc_table(capi, [int(x) for x in args.spttmc_configs.split(",")], local,
+                                            stream, pk, cpk)
     if rank == 0 and world == 1:
         line["paper_context"] = paper_context(capi, local, stream)
     if rank == 0:

@@ -72,7 +72,7 @@ typedef struct {
                                  it runs the sharded code path over a 1-rank communicator       */
   void* stream;               /* cudaStream_t to run on (NULL = the handle's own stream)        */
   int eig_oversample;         /* p in block size k = J + p (0 = default)         */
-  int eig_max_iter;           /* cap on Chebyshev-filter outer iterations (0 = default 40)      */
+  int eig_max_iter;           /* cap on Chebyshev-filter outer iterations (0 = default 60)      */
   double eig_tol;             /* Ritz residual tolerance relative to theta_1 (0 = default)      */
   unsigned flags;             /* TUCKER_* flags above                                           */
 } tucker_opts;
@@ -85,9 +85,12 @@ void tucker_default_opts(tucker_opts* opts);
  *
  *   order   N in {3, 4} (MP is defined for orders 3 and 4 only, Figs. 7-8
  *           P:911-1114; SURVEY reading A18).
- *   dims    I_1..I_N, each >= 1 and I_n < 2^31.
+ *   dims    I_1..I_N, each >= 1 and I_n < 2^31, with prod_n I_n < 2^64 (the
+ *           sort keys pack every coordinate into 64 bits; TUCKER_E_ARG otherwise).
  *   core    J_1..J_N, 1 <= J_n <= min(I_n, 112) (this build's eigensolver
- *           block limit; TUCKER_E_ARG otherwise).
+ *           block limit) and J_n <= prod_{q != n} J_q (Y_(n) has at most that
+ *           rank, so no J_n-dimensional dominant subspace exists beyond it);
+ *           TUCKER_E_ARG otherwise.
  *   nnz     number of COO entries (>= 1).
  *   idx     N pointers to int32[nnz], 0-based coordinates (any order).
  *   vals    fp32[nnz].
@@ -187,11 +190,25 @@ int tucker_debug_product(int d, int n, const double* S, const double* Y, double 
 /* Timing of the same product alone: *us = microseconds per launch (mean of reps). */
 int tucker_debug_product_time(int d, int n, int reps, double* us);
 
+/* Measurement entry point: the HOOI projection of `mode` (0-based) with the
+ * handle's current factors, run `reps` >= 1 times back to back on the handle's
+ * stream after one untimed run; *ms_out = mean milliseconds per projection
+ * (CUDA events around the repetitions: the SpTTMc kernels and the zero fill of
+ * the Y buffer).  Leaves the handle's cached core invalid.  E_ARG on bad
+ * arguments. */
+int tucker_time_ttmc(tucker_handle* h, int mode, int reps, float* ms_out);
+
 /* Sparse layout of the handle, for the CSF ordering mode n's HOOI projection
  * uses (out has 4 N entries): out[4n] = fibers, out[4n + 1] = nonzeros,
  * out[4n + 2] = virtual fibers of the SpTTMc work plan and out[4n + 3] = its
  * work units (both 0 when the tensor needs no plan: one CTA per slice). */
 int tucker_csf_stats(tucker_handle* h, int64_t* out);
+
+/* The CSF ordering each mode's HOOI projection uses (out has 8 N entries):
+ * out[8n .. 8n+7] = root mode, mid0 mode, mid1 mode (-1 at order 3), leaf mode
+ * (0-based), fibers (distinct root/mid coordinates), nodes (order 4: distinct
+ * (root, mid0); order 3: 0), nonzeros, root slices. */
+int tucker_csf_layout(tucker_handle* h, int64_t* out);
 
 /* Kernel statistics of the handle since the last reset (for bench/roofline):
  * stats[0] = kernel launches issued by the library, [1] = eigensolver outer

@@ -19,6 +19,12 @@ Parity status per function:
   mp_gram / mp_gram_slices / run_mp          pinned (P1, P4, P6, P9, P12)
   core / fit_from_core                       pinned (P2, P7)
   hosvd, pseudo_hosvd                        pinned (P5, P6, P12)
+  ttm_chain_unfold_slices                    pinned (Eq. 1 brute force, = ttm_chain_unfold)
+  leading_left_vectors_gram_t                pinned (SVD of Y, = the Y Y^T route, ragged shapes)
+  hooi_sweep_large / run_hooi_large          pinned (= hooi_sweep / run_hooi on small tensors,
+                                             P1 exact multilinear rank)
+  projector_distance                         pinned (explicit ||U U^T - V V^T||_F, sqrt 2 for
+                                             one swapped column, rotation/sign invariance)
 """
 from __future__ import annotations
 
@@ -147,6 +153,58 @@ def ttm_chain_unfold(T: SparseTensor, U, n: int) -> np.ndarray:
     return unfold(ttm_chain(T, U, n), n)
 
 
+def ttm_chain_unfold_slices(T: SparseTensor, U, n: int) -> np.ndarray:
+    """Y_(n) = (X x_{m != n} U_m^T)_(n) for ORDER-3 tensors, one mode-n slice at a
+    time, as the paper's own code forms it: row i of Y_(1) is B' * X1_slice * C
+    (Appendix) with X1_slice the I_a x I_b slice of index i (a < b the two
+    other modes).  That is Eq. 1 applied to the slice twice; only the rows of the
+    slice that hold nonzeros (its fibers) take part, so no dense I_a x J_b
+    intermediate is formed.  The row is the J_a x J_b matrix U_a^T X_i U_b
+    flattened with the lower mode fastest (Kolda order, Eqs. 3-6).  Memory and
+    time grow with the nonzeros and fibers only (config 5 of BASELINE.json)."""
+    if T.N != 3:
+        raise ValueError("ttm_chain_unfold_slices: order 3 only")
+    a, b = [m for m in range(3) if m != n]
+    Ua = np.asarray(U[a], dtype=np.float64)
+    Ub = np.asarray(U[b], dtype=np.float64)
+    Ja, Jb = Ua.shape[1], Ub.shape[1]
+    Y = np.zeros((T.dims[n], Ja * Jb))
+    # the slice / fiber grouping depends on the tensor only: kept on T for later sweeps
+    plans = T.__dict__.setdefault("_slice_plans", {})
+    if n not in plans:
+        i_n, i_a, i_b = T.idx[n], T.idx[a], T.idx[b]
+        order = np.lexsort((i_b, i_a, i_n))
+        i_n, i_a, i_b, x = i_n[order], i_a[order], i_b[order], T.vals[order]
+        # fibers = distinct (i_n, i_a): the nonzero rows of each slice X_i
+        fkey = i_n * T.dims[a] + i_a
+        fstart = np.flatnonzero(np.r_[True, fkey[1:] != fkey[:-1]])
+        del fkey
+        f_n, f_a = i_n[fstart], i_a[fstart]
+        del i_n, i_a
+        sstart = np.flatnonzero(np.r_[True, f_n[1:] != f_n[:-1]])
+        plans[n] = (i_b, x, fstart, f_n, f_a, sstart)
+    i_b, x, fstart, f_n, f_a, sstart = plans[n]
+    send = np.r_[sstart[1:], f_n.size]
+    fend_nz = np.r_[fstart[1:], x.size]
+    # process slices in chunks of <= ~2e6 fibers: t_f = X_i[row f, :] U_b (Eq. 1)
+    s0 = 0
+    while s0 < sstart.size:
+        s1 = s0 + 1
+        while s1 < sstart.size and send[s1] - sstart[s0] <= 2_000_000:
+            s1 += 1
+        f0, f1 = sstart[s0], send[s1 - 1]
+        e0, e1 = fstart[f0], fend_nz[f1 - 1]
+        rows = np.repeat(np.arange(f1 - f0), np.diff(np.r_[fstart[f0:f1], e1]))
+        Xf = sp.csr_matrix((x[e0:e1], (rows, i_b[e0:e1])), shape=(f1 - f0, T.dims[b]))
+        Tf = Xf @ Ub                                    # fibers x J_b
+        for s in range(s0, s1):
+            g0, g1 = sstart[s] - f0, send[s] - f0
+            M = Ua[f_a[sstart[s] : send[s]]].T @ Tf[g0:g1]  # U_a^T X_i U_b (J_a x J_b)
+            Y[f_n[sstart[s]]] = M.ravel(order="F")  # j_a + J_a j_b (a < b)
+        s0 = s1
+    return Y
+
+
 def leading_eigenvectors(S: np.ndarray, J: int):
     """J leading eigenvectors of symmetric S (Fig. 4 `A(n) <- J_n leading
     eigenvectors of Z_(n) Z_(n)^T`), descending eigenvalue order, each column
@@ -163,6 +221,31 @@ def leading_eigenvectors(S: np.ndarray, J: int):
         if V[k, j] < 0:
             V[:, j] = -V[:, j]
     return V, w
+
+
+def leading_left_vectors_gram_t(Y: np.ndarray, J: int):
+    """The J leading eigenvectors of Y Y^T computed from the smaller Gram Y^T Y
+    (reading A10, used when I_n > prod_{m != n} J_m): with Y^T Y = V Theta V^T,
+    the left singular vectors are U = Y V Theta^{-1/2} (Y = U Sigma V^T, Theta =
+    Sigma^2), orthonormal in exact arithmetic.  Descending order, columns
+    sign-canonicalised as in :func:`leading_eigenvectors` (S:136).  Returns
+    (U, w) with w the eigenvalues of Y^T Y, descending (the nonzero spectrum of
+    Y Y^T)."""
+    Y = np.asarray(Y, dtype=np.float64)
+    if J > Y.shape[1]:
+        raise ValueError("Y^T Y route: J exceeds the columns of Y")
+    w, V = np.linalg.eigh(Y.T @ Y)
+    order = np.argsort(-w, kind="stable")
+    w = w[order]
+    V = V[:, order[:J]]
+    if not w[J - 1] > 1e-12 * w[0]:  # reading A10: theta_J <= 1e-12 theta_1 is rank deficient
+        raise ValueError("Y^T Y route: rank(Y) < J (use the S:136 completion)")
+    U = (Y @ V) / np.sqrt(w[:J])
+    for j in range(J):
+        k = int(np.argmax(np.abs(U[:, j])))
+        if U[k, j] < 0:
+            U[:, j] = -U[:, j]
+    return U, w
 
 
 def eig_diag(w: np.ndarray, J: int) -> dict:
@@ -189,6 +272,50 @@ def hooi_sweep(T: SparseTensor, U, core, diag=None):
         if diag is not None:
             diag.append(dict(mode=n, **eig_diag(w, core[n])))
     return U, Y
+
+
+def hooi_sweep_large(T: SparseTensor, U, core, diag=None):
+    """:func:`hooi_sweep` for tensors whose dense intermediates do not fit: the
+    projection is :func:`ttm_chain_unfold_slices` (order 3) and the factor comes
+    from the smaller Gram (Y Y^T when I_n <= prod_{m != n} J_m, else Y^T Y via
+    :func:`leading_left_vectors_gram_t`; reading A10: the same U_n).  Returns
+    (U_new, Y_last) like hooi_sweep."""
+    U = [np.asarray(u, dtype=np.float64) for u in U]
+    Y = None
+    for n in range(T.N):
+        Y = ttm_chain_unfold_slices(T, U, n)
+        if Y.shape[0] <= Y.shape[1]:
+            U[n], w = leading_eigenvectors(Y @ Y.T, core[n])
+        else:
+            U[n], w = leading_left_vectors_gram_t(Y, core[n])
+        if diag is not None:
+            diag.append(dict(mode=n, **eig_diag(w, core[n])))
+    return U, Y
+
+
+def core_from_last_projection(U, Y_last) -> np.ndarray:
+    """G from Y_(N) = (X x_{m < N} U_m^T)_(N): G_(N) = U_N^T Y_(N) (Eq. 1 for the
+    last mode, Fig. 4 last step), folded to J_1 x ... x J_N (mode-1 fastest)."""
+    N = len(U)
+    GN = np.asarray(U[N - 1], dtype=np.float64).T @ Y_last
+    dims = [u.shape[1] for u in U]
+    return fold(GN, N - 1, dims)
+
+
+def run_hooi_large(T: SparseTensor, U0, core_dims, sweeps: int, diag=None, log=None):
+    """Fixed-sweep HOOI (Fig. 4) with :func:`hooi_sweep_large`; the core of each
+    sweep comes from that sweep's last projection.  `log(msg)` (optional)
+    reports progress.  Returns dict(U, G, fits, fit)."""
+    U = [np.asarray(u, dtype=np.float64) for u in U0]
+    nx2 = T.norm2()
+    fits, G = [], None
+    for t in range(sweeps):
+        U, Y = hooi_sweep_large(T, U, core_dims, diag)
+        G = core_from_last_projection(U, Y)
+        fits.append(fit_from_core(nx2, G))
+        if log:
+            log(f"sweep {t + 1}: fit {fits[-1]:.10f}")
+    return dict(U=U, G=G, fits=fits, fit=fits[-1])
 
 
 # ---------------------------------------------------------------------------

@@ -30,6 +30,7 @@ EXPORTS = [
     "tucker_debug_product", "tucker_debug_product_time", "tucker_csf_stats", "tucker_stats",
     "tucker_nccl_unique_id", "tucker_shard_bounds", "tucker_shard_info", "hooi_run", "mp_run",
     "tucker_hosvd", "sp_sweep", "sp_run", "tucker_set_factor", "tucker_set_allreduce",
+    "tucker_time_ttmc", "tucker_csf_layout",
 ]
 
 
@@ -68,6 +69,8 @@ def load(path: str = LIB_PATH) -> C.CDLL:
     lib.tucker_debug_product.argtypes = [C.c_int, C.c_int, P, P, C.c_double, C.c_double, P, P]
     lib.tucker_debug_product_time.argtypes = [C.c_int, C.c_int, C.c_int, C.POINTER(C.c_double)]
     lib.tucker_csf_stats.argtypes = [P, i64p]
+    lib.tucker_csf_layout.argtypes = [P, i64p]
+    lib.tucker_time_ttmc.argtypes = [P, C.c_int, C.c_int, C.POINTER(C.c_float)]
     lib.tucker_nccl_unique_id.argtypes = [P]
     lib.tucker_hosvd.argtypes = [P, C.c_uint]
     lib.tucker_set_allreduce.argtypes = [P, P, P]
@@ -116,6 +119,44 @@ def _ptr(a) -> int:
     return a.ctypes.data
 
 
+# shapes of every live handle (dims, core), so calls that take factors can check them
+_shapes: dict = {}
+
+
+def _numel(a) -> int:
+    return int(a.numel() if hasattr(a, "numel") else np.asarray(a).size)
+
+
+def _check_array(a, what, dtype, shape=None, size=None, device=False):
+    """The C side reads exactly the declared number of elements from these pointers:
+    reject a wrong dtype, size or shape here instead of reading out of bounds."""
+    if hasattr(a, "data_ptr"):  # torch tensor
+        import torch
+        tdt = {np.int32: torch.int32, np.float32: torch.float32}[dtype]
+        if a.dtype != tdt:
+            raise TypeError(f"{what}: dtype {a.dtype}, expected {tdt}")
+        if not a.is_contiguous():
+            raise ValueError(f"{what}: tensor must be contiguous")
+        if device != a.is_cuda:
+            raise ValueError(f"{what}: expected a {'device' if device else 'host'} tensor")
+        got = tuple(a.shape)
+    else:
+        if device:
+            raise ValueError(f"{what}: on_device=True needs torch CUDA tensors")
+        got = np.shape(a)
+    if shape is not None and tuple(got) != tuple(shape):
+        raise ValueError(f"{what}: shape {tuple(got)}, expected {tuple(shape)}")
+    if size is not None and _numel(a) != size:
+        raise ValueError(f"{what}: {_numel(a)} elements, expected {size}")
+
+
+def _check_factors(dims, core, U, device, what="U"):
+    if len(U) != len(dims):
+        raise ValueError(f"{what}: {len(U)} factors for an order-{len(dims)} tensor")
+    for n, u in enumerate(U):
+        _check_array(u, f"{what}[{n}]", np.float32, shape=(dims[n], core[n]), device=device)
+
+
 def tucker_init(dims, core, idx, vals, U0, *, device=0, stream=None, eig_oversample=0,
                 eig_max_iter=0, eig_tol=0.0, on_device=False, output_on_device=False,
                 rank=0, world=1, nccl_id=None, host_collectives=False):
@@ -126,10 +167,24 @@ def tucker_init(dims, core, idx, vals, U0, *, device=0, stream=None, eig_oversam
     nccl_id (nccl_unique_id() on one rank, broadcast by the caller)."""
     L = lib()
     N = len(dims)
+    dims = tuple(int(x) for x in dims)
+    core = tuple(int(x) for x in core)
+    if len(core) != N or len(idx) != N or len(U0) != N:
+        raise ValueError(f"order {N}: need {N} core sizes, index arrays and factors "
+                         f"(got {len(core)}, {len(idx)}, {len(U0)})")
     if not on_device:
         idx = [np.ascontiguousarray(a, dtype=np.int32) for a in idx]
         vals = np.ascontiguousarray(vals, dtype=np.float32)
         U0 = [np.ascontiguousarray(u, dtype=np.float32) for u in U0]
+    nnz = _numel(vals)
+    _check_array(vals, "vals", np.float32, device=on_device)
+    if not hasattr(vals, "data_ptr") and np.ndim(vals) != 1:
+        raise ValueError("vals must be 1-D")
+    for n, a in enumerate(idx):
+        _check_array(a, f"idx[{n}]", np.int32, size=nnz, device=on_device)
+        if np.ndim(a) != 1 and not hasattr(a, "data_ptr"):
+            raise ValueError(f"idx[{n}] must be 1-D")
+    _check_factors(dims, core, U0, on_device, "U0")
     o = tucker_opts()
     L.tucker_default_opts(C.byref(o))
     o.device = device
@@ -153,9 +208,9 @@ def tucker_init(dims, core, idx, vals, U0, *, device=0, stream=None, eig_oversam
     ip = (C.c_void_p * N)(*[_ptr(a) for a in idx])
     up = (C.c_void_p * N)(*[_ptr(u) for u in U0])
     h = C.c_void_p()
-    nnz = int(vals.numel() if hasattr(vals, "numel") else vals.size)
     rc = L.tucker_init(C.byref(h), N, d, j, nnz, ip, C.c_void_p(_ptr(vals)), up, C.byref(o))
     _check(rc)
+    _shapes[h.value] = (dims, core, bool(on_device))
     return h.value
 
 
@@ -181,7 +236,17 @@ def core_and_fit_into(h, core_out, U_out):
     """core_and_fit writing into caller buffers (numpy or torch, host or device
     according to the handle's output flag); returns the fit."""
     N = len(U_out) if U_out is not None else 0
-    up = (C.c_void_p * N)(*[_ptr(u) for u in U_out]) if U_out is not None else None
+    if h in _shapes:  # the library writes prod J and I_n x J_n elements into these
+        dims, core, _ = _shapes[h]
+        if core_out is not None and _numel(core_out) != int(np.prod(core)):
+            raise ValueError(f"core_out: {_numel(core_out)} elements, expected {int(np.prod(core))}")
+        if U_out is not None:
+            if N != len(dims):
+                raise ValueError(f"U_out: {N} buffers for an order-{len(dims)} tensor")
+            for n, u in enumerate(U_out):
+                if u is not None and _numel(u) != dims[n] * core[n]:
+                    raise ValueError(f"U_out[{n}]: {_numel(u)} elements, expected {dims[n] * core[n]}")
+    up = (C.c_void_p * N)(*[_ptr(u) if u is not None else None for u in U_out]) if U_out is not None else None
     fit = C.c_double()
     rc = lib().core_and_fit(h, C.c_void_p(_ptr(core_out)) if core_out is not None else None, up,
                             C.byref(fit))
@@ -205,12 +270,16 @@ def core_and_fit(h, dims, core, want_core=True, want_factors=True):
 def tucker_set_factors(h, U):
     if not all(hasattr(u, "data_ptr") for u in U):
         U = [np.ascontiguousarray(u, dtype=np.float32) for u in U]
+    if h in _shapes:
+        dims, core, dev = _shapes[h]
+        _check_factors(dims, core, U, dev)
     up = (C.c_void_p * len(U))(*[_ptr(u) for u in U])
     _check(lib().tucker_set_factors(h, up), h)
 
 
 def tucker_free(h):
     if h:
+        _shapes.pop(h, None)
         lib().tucker_free(h)
 
 
@@ -282,6 +351,22 @@ def tucker_csf_stats(h, order=3):
     return [tuple(int(s[4 * n + q]) for q in range(4)) for n in range(order)]
 
 
+def tucker_csf_layout(h, order):
+    """Per mode: dict(root, mid0, mid1, leaf, fibers, nodes, nnz, slices) of the CSF
+    ordering its HOOI projection uses (mode ids 0-based; mid1 = -1 at order 3)."""
+    s = (C.c_int64 * (8 * order))()
+    _check(lib().tucker_csf_layout(h, s), h)
+    keys = ("root", "mid0", "mid1", "leaf", "fibers", "nodes", "nnz", "slices")
+    return [{k: int(s[8 * n + i]) for i, k in enumerate(keys)} for n in range(order)]
+
+
+def tucker_time_ttmc(h, mode, reps=5):
+    """Mean ms of the HOOI projection of `mode` (measurement entry point)."""
+    ms = C.c_float(0)
+    _check(lib().tucker_time_ttmc(h, mode, reps, C.byref(ms)), h)
+    return ms.value
+
+
 def tucker_csf_fibers(h, order=3):
     """Total fibers of the HOOI CSF orderings (all modes)."""
     return sum(st[0] for st in tucker_csf_stats(h, order))
@@ -326,6 +411,11 @@ def sp_run(h, max_sweeps=50, tol=1e-4):
 def tucker_set_factor(h, n, U, check=True):
     if not hasattr(U, "data_ptr"):
         U = np.ascontiguousarray(U, dtype=np.float32)
+    if h in _shapes:
+        dims, core, dev = _shapes[h]
+        if not 0 <= n < len(dims):
+            raise ValueError(f"mode {n} out of range for order {len(dims)}")
+        _check_array(U, f"U[{n}]", np.float32, shape=(dims[n], core[n]), device=dev)
     _check(lib().tucker_set_factor(h, n, C.c_void_p(_ptr(U)), 1 if check else 0), h)
 
 

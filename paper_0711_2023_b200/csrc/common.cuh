@@ -41,6 +41,11 @@ void mempool_retain(int device);  // default pool keeps freed memory (once per d
 
 bool sync_check_enabled();  // env TUCKER_SYNC_CHECK: synchronise + check after every launch
 
+// Dynamic shared-memory opt-in (cudaFuncAttributeMaxDynamicSharedMemorySize) is
+// a per-device setting: raise it for `fn` on the CURRENT device whenever `bytes`
+// exceeds what was set there before (cached per (kernel, device), thread safe).
+void smem_optin(const void* fn, size_t bytes);
+
 #define TK_LAUNCH(kernel, grid, block, smem, stream, ...)                 \
   do {                                                                    \
     kernel<<<(grid), (block), (smem), (stream)>>>(__VA_ARGS__);           \

@@ -8,6 +8,8 @@
 #include <cub/cub.cuh>
 
 #include <cstdlib>
+#include <map>
+#include <mutex>
 
 #include "internal.cuh"
 
@@ -28,6 +30,18 @@ void mempool_retain(int device) {
 bool sync_check_enabled() {
   static const bool on = std::getenv("TUCKER_SYNC_CHECK") != nullptr;
   return on;
+}
+
+void smem_optin(const void* fn, size_t bytes) {
+  static std::mutex mu;
+  static std::map<std::pair<const void*, int>, size_t> set;
+  int dev = 0;
+  TK_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lk(mu);
+  size_t& cur = set[{fn, dev}];
+  if (bytes <= cur) return;
+  TK_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+  cur = bytes;
 }
 
 namespace {

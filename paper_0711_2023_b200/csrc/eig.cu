@@ -185,14 +185,11 @@ MatRef f64(const double* p, int64_t ld, bool trans = false) {
 
 // dynamic smem opt-in for the Cholesky kernel (2 k (k + 1) doubles)
 void chol_attr() {
-  static bool done = false;
-  if (done) return;
-  const int bytes = 2 * kMaxBlock * (kMaxBlock + 1) * (int)sizeof(double);
-  TK_CUDA(cudaFuncSetAttribute(k_chol_inv<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
-  TK_CUDA(cudaFuncSetAttribute(k_chol_inv<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
-  TK_CUDA(cudaFuncSetAttribute(k_chol_inv<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
-  TK_CUDA(cudaFuncSetAttribute(k_chol_inv<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
-  done = true;
+  const size_t bytes = 2 * kMaxBlock * (kMaxBlock + 1) * sizeof(double);
+  smem_optin((const void*)k_chol_inv<1>, bytes);
+  smem_optin((const void*)k_chol_inv<2>, bytes);
+  smem_optin((const void*)k_chol_inv<3>, bytes);
+  smem_optin((const void*)k_chol_inv<4>, bytes);
 }
 
 // Q (d x k) <- Q R^{-1} twice (CholQR2)

@@ -1630,7 +1630,7 @@ void launch_unit_mv(const double* S, const double* Y, int d, int n, int ls, int 
                     double gamma, const double* D, double* mpart, int reps, cudaStream_t st) {
   const int G = num_sms();
   const size_t smem = product_smem(d, n, G);
-  TK_CUDA(cudaFuncSetAttribute(k_eigf_unit_mv, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  smem_optin((const void*)k_eigf_unit_mv, smem);
   MvPlan pl = mv_plan(d, G);
   void* args[] = {&S, &Y, &d, &n, &ls, &lb, &alpha, &O, &gamma, &D, &mpart, &reps, &pl};
   TK_CUDA(cudaLaunchCooperativeKernel((const void*)k_eigf_unit_mv, dim3(G), dim3(NT), args, smem, st));
@@ -1703,15 +1703,11 @@ __global__ void k_seed_basis(double* __restrict__ basis, int64_t d, int LB, int 
 
 bool eig_fused(double* S, int64_t d, int J, EigSlot& slot, EigWs& ws, const EigOpts& o, double* out_V,
                double* theta_dev, int* info_dev, cudaStream_t st, const float* hint) {
-  static size_t smem_set = 0;
   const int k = choose_block(J, d, o.oversample);
   const int grid = num_sms();  // one CTA per SM (cooperative: all co-resident)
   const size_t smem = eig_fused_smem(k, (int)d, grid);
   if (smem > SMEM_LIMIT) fail(TUCKER_E_ARG, "eig_fused: block too large for shared memory");
-  if (smem > smem_set) {
-    TK_CUDA(cudaFuncSetAttribute(k_eig_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    smem_set = smem;
-  }
+  smem_optin((const void*)k_eig_fused, smem);
   {
     int per = 0;
     TK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_eig_fused, NT, smem));
@@ -1772,7 +1768,11 @@ bool eig_fused(double* S, int64_t d, int J, EigSlot& slot, EigWs& ws, const EigO
   }
   a.basis = slot.basis.p;
   a.warm = (slot.valid && slot.d == d && slot.k == k) ? 1 : 0;
-  a.warm_exact = a.warm;
+  // an exact warm start reuses the last solve's orthonormal [L | Q] without the
+  // initial CholQR; every 4th one re-orthonormalises so rounding drift cannot
+  // accumulate over many sweeps
+  a.warm_exact = a.warm && slot.exact_age < 4;
+  slot.exact_age = a.warm_exact ? slot.exact_age + 1 : 0;
   if (!a.warm && hint) {  // cold slot: start from the caller's current factor
     TK_LAUNCH(k_seed_basis, 2 * grid, 256, 0, st, slot.basis.p, d, LB, k, hint, J,
               0x5eedb0000ull + (uint64_t)d * 131 + (uint64_t)J);
@@ -1888,7 +1888,7 @@ void eig_unit(int mode, const double* in, int k, double* out, double* theta, int
               double shift, cudaStream_t st) {
   const int kp = k + (k & 1);
   const size_t smem = (size_t)2 * kp * (kp + 1) * sizeof(double);
-  TK_CUDA(cudaFuncSetAttribute(k_eigf_unit, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  smem_optin((const void*)k_eigf_unit, smem);
   TK_LAUNCH(k_eigf_unit, 1, NT, smem, st, mode, in, k, out, theta, iout, sweeps, shift);
 }
 

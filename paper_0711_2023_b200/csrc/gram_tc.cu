@@ -237,12 +237,8 @@ CUtensorMap make_map(const float* base, int64_t rows_pad, int64_t ld, int64_t ke
 }  // namespace
 
 void gram_syrk_tc(const Split& A, double* S, int64_t lds, GramWs& ws, cudaStream_t st) {
-  static bool attr = false;
   const int smem_bytes = STAGES * STAGE_BYTES + 1024;
-  if (!attr) {
-    TK_CUDA(cudaFuncSetAttribute(k_syrk_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes));
-    attr = true;
-  }
+  smem_optin((const void*)k_syrk_tc, smem_bytes);
   const int64_t d = A.rows;
   const int64_t rows_pad = round_up(d, TM);
   if (A.ld % TKE != 0 || A.K() % TKE != 0) fail(TUCKER_E_ARG, "gram_syrk_tc: ld and K must be multiples of 32");

@@ -141,6 +141,7 @@ struct EigSlot {              // warm-start state per (algorithm, mode)
   bool valid = false;
   double lmin = 0.0, bval = 0.0;  // lambda_min estimate and filter bound of the last solve
   int lz_age = 0;                  // solves since the last Lanczos estimate
+  int exact_age = 0;               // consecutive exact warm starts (no re-orthonormalisation)
 };
 struct EigWs {
   DBuf<double> Q, SQ, X, Y, T;  // eig_fused work blocks (padded layout)
@@ -155,7 +156,7 @@ struct EigWs {
 };
 struct EigOpts {
   int oversample = 0;
-  int max_outer = 40;
+  int max_outer = 60;             // tucker_opts.eig_max_iter default (include/tucker.h)
   int jacobi_sweeps = 2;        // cap per Rayleigh-Ritz step (residuals decide convergence)
   int jacobi_sweeps_first = 1;  // cap for a solve's first Rayleigh-Ritz step (measured best at config 2)
   double tol = 1e-10;

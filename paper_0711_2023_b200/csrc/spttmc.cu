@@ -19,8 +19,12 @@
 #include <array>
 #include <vector>
 
+#include <cooperative_groups.h>
+
 #include "internal.cuh"
 #include "tc_ptx.cuh"
+
+namespace cg = cooperative_groups;
 
 namespace tk {
 
@@ -38,57 +42,6 @@ __device__ __forceinline__ void split_store(float* hi, float* lo, int64_t off, f
 namespace {
 
 constexpr int kFC = 32;  // fibers per chunk
-
-// Leaf stage for the fibers [fc, fc+nf) of one chunk: T[fl][b] = t_f[b],
-// Mrow[fl][a] = U_mid[mid(f), a]; rows padded with zeros to JLP / JMP.
-template <int JLP, int JMP>
-__device__ __forceinline__ void leaf_stage(int fc, int nf, const int32_t* __restrict__ fib_ptr,
-                                           const int32_t* __restrict__ fib_mid,
-                                           const int32_t* __restrict__ leaf_id,
-                                           const float* __restrict__ val,
-                                           const float* __restrict__ Umid, int Jm,
-                                           const float* __restrict__ Uleaf, int Jl, float* T,
-                                           float* M) {
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int nwarps = blockDim.x >> 5;
-  constexpr int QL = JLP / 32 > 0 ? (JLP + 31) / 32 : 1;
-  for (int fl = warp; fl < nf; fl += nwarps) {
-    const int f = fc + fl;
-    const int e0 = __ldg(fib_ptr + f), e1 = __ldg(fib_ptr + f + 1);
-    float t[QL];
-#pragma unroll
-    for (int q = 0; q < QL; ++q) t[q] = 0.f;
-    int e = e0;
-    for (; e + 1 < e1; e += 2) {  // two nonzeros in flight
-      const int l0 = __ldg(leaf_id + e), l1 = __ldg(leaf_id + e + 1);
-      const float x0 = __ldg(val + e), x1 = __ldg(val + e + 1);
-      const float* r0 = Uleaf + (int64_t)l0 * Jl;
-      const float* r1 = Uleaf + (int64_t)l1 * Jl;
-#pragma unroll
-      for (int q = 0; q < QL; ++q) {
-        const int j = lane + 32 * q;
-        if (j < Jl) t[q] += x0 * __ldg(r0 + j) + x1 * __ldg(r1 + j);
-      }
-    }
-    if (e < e1) {
-      const int l0 = __ldg(leaf_id + e);
-      const float x0 = __ldg(val + e);
-      const float* r0 = Uleaf + (int64_t)l0 * Jl;
-#pragma unroll
-      for (int q = 0; q < QL; ++q) {
-        const int j = lane + 32 * q;
-        if (j < Jl) t[q] += x0 * __ldg(r0 + j);
-      }
-    }
-#pragma unroll
-    for (int q = 0; q < QL; ++q) {
-      const int j = lane + 32 * q;
-      if (j < JLP) T[fl * JLP + j] = (j < Jl) ? t[q] : 0.f;
-    }
-    const float* mr = Umid + (int64_t)__ldg(fib_mid + f) * Jm;
-    for (int j = lane; j < JMP; j += 32) M[fl * JMP + j] = (j < Jm) ? __ldg(mr + j) : 0.f;
-  }
-}
 
 // Leaf stage with the chunk's fiber metadata (fptr: nf + 1 nonzero offsets,
 // fmid: mid indices) already in shared memory and, when the chunk's
@@ -612,99 +565,248 @@ struct Ttmc4Args {
   int slice0;          // first slice of this launch (rank shard) when unit == null
   const int32_t* unit; // work units (slice, node0, node1, slot) or null: one CTA per slice
   float* part;         // partial rows of split slices (J0 J1 Jl floats per slot)
+  // k_spttmc4w: factor table sizes, padded strides and the cluster split of a slice
+  int I_leaf, I_mid1;
+  int J1P, J0P;        // J1, J0 rounded up to 4 (smem row strides)
+  int csize;           // CTAs (cluster ranks) per slice
 };
 
-template <int RA, int RB, int RQ>
-__global__ void __launch_bounds__(256) k_spttmc4(Ttmc4Args p) {
-  constexpr int JLP = 16 * RB, JMP = 16 * RA;
-  __shared__ __align__(16) float T[kFC * JLP];
-  __shared__ __align__(16) float M[kFC * JMP];
-  __shared__ float Zs[JMP * JLP];
-  __shared__ float u0[128];
-  int i, n0, n1, slot = -1;
-  if (p.unit) {
-    const int4 u = reinterpret_cast<const int4*>(p.unit)[blockIdx.x];
-    i = u.x;
-    n0 = u.y;
-    n1 = u.z;
-    slot = u.w;
-  } else {
-    i = p.slice0 + blockIdx.x;
-    n0 = p.slice_ptr[i];
-    n1 = p.slice_ptr[i + 1];
-  }
-  const int P1 = p.J1 * p.Jl;
-  const int P = p.J0 * P1;
-  float y[RQ];
-#pragma unroll
-  for (int q = 0; q < RQ; ++q) y[q] = 0.f;
-  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
-  for (int nd = n0; nd < n1; ++nd) {
-    float acc[RA][RB];
-#pragma unroll
-    for (int r = 0; r < RA; ++r)
-#pragma unroll
-      for (int c = 0; c < RB; ++c) acc[r][c] = 0.f;
-    const int f0 = p.node_ptr[nd], f1 = p.node_ptr[nd + 1];
-    for (int fc = f0; fc < f1; fc += kFC) {
-      const int nf = min(kFC, f1 - fc);
-      leaf_stage<JLP, JMP>(fc, nf, p.fib_ptr, p.fib_mid1, p.leaf_id, p.val, p.U1, p.J1, p.Uleaf,
-                           p.Jl, T, M);
-      __syncthreads();
-      kron_stage<RA, RB>(nf, T, M, acc);
-      __syncthreads();
-    }
-#pragma unroll
-    for (int r = 0; r < RA; ++r)
-#pragma unroll
-      for (int c = 0; c < RB; ++c) {
-        const int a = ty * RA + r, b = kron_col<RA, RB>(tx, c);
-        if (a < p.J1 && b < p.Jl) Zs[a * p.Jl + b] = acc[r][c];
-      }
-    const float* ur = p.U0 + (int64_t)p.node_mid0[nd] * p.J0;
-    for (int j = threadIdx.x; j < p.J0; j += blockDim.x) u0[j] = __ldg(ur + j);
-    __syncthreads();
-#pragma unroll
-    for (int q = 0; q < RQ; ++q) {
-      const int c = threadIdx.x + 256 * q;
-      if (c < P) y[q] += u0[c / P1] * Zs[c % P1];
-    }
-    __syncthreads();
-  }
-#pragma unroll
-  for (int q = 0; q < RQ; ++q) {
-    const int c = threadIdx.x + 256 * q;
-    if (c < P) {
-      if (slot >= 0) {
-        p.part[(int64_t)slot * P + c] = y[q];
-        continue;
-      }
-      const int a0 = c / P1, rest = c % P1;
-      const int a1 = rest / p.Jl, b = rest % p.Jl;
-      const int64_t col = a0 * p.s0 + a1 * p.s1 + b * p.sb;
-      const int64_t off = p.transposed ? col * p.ldY + i : (int64_t)i * p.ldY + col;
-      split_store(p.Yhi, p.Ylo, off, y[q]);
-    }
-  }
-}
+// ---------------------------------------------------------------------------
+// Order-4 HOOI SpTTMc, node per warp (k_spttmc4w).  Per slice i (root) and
+// node v = (i, mid0 index a):
+//   leaf     t_f   = sum_{x in f} x U_leaf[leaf(x), :]          (Eq. 1; lanes = fibers)
+//   level 2  Z_v   = sum_{f in v} U_mid1[mid1(f), :] (x) t_f     (J1 x Jl, lanes own 4x4 blocks)
+//   level 3  Y_i  += U_mid0[a, :] (x) Z_v                        (all threads, per batch of 8 nodes)
+// Each warp works on its own node (no block barrier inside a node); the CTA
+// syncs twice per batch of 8 nodes for level 3.  U_leaf and U_mid1 are staged
+// in shared memory when they fit (config 4: 16 KB each), zero padded to 4-float
+// rows so every gather is a 128-bit load.  A slice is split over the `csize`
+// CTAs of one thread-block cluster (contiguous node ranges); their partial Y
+// rows are summed through distributed shared memory in fixed rank order
+// (deterministic, no atomics, no partial rows in HBM) and written once.
+// ---------------------------------------------------------------------------
+constexpr int kW4 = 8;        // warps = nodes in flight per CTA
+constexpr int kStage4 = 128;  // staged nonzeros per warp and fiber chunk (longer chunks read global memory)
 
-// order 4: Y row of a split slice = sum of its units' partial rows, in slot order
-__global__ void __launch_bounds__(256) k_spttmc4_reduce(const int32_t* __restrict__ red,
-                                                        const float* __restrict__ part, int J0, int J1, int Jl,
-                                                        int64_t s0, int64_t s1, int64_t sb, float* Yhi,
-                                                        float* Ylo, int64_t ldY, int transposed) {
-  const int r = blockIdx.y;
-  const int i = red[3 * r], q0 = red[3 * r + 1], nq = red[3 * r + 2];
+// per-warp region (floats): T 32 x JLP | Z J1 x Jl (<= J1P JLP) | bix 32 | staged leaf ids / values
+__host__ __device__ inline int w4_floats(int JLP, int J1P) { return 32 * JLP + J1P * JLP + 32 + 2 * kStage4; }
+
+template <int JLP, int NBL, bool SM>
+__global__ void __launch_bounds__(256, 2) k_spttmc4w(Ttmc4Args p) {
+  extern __shared__ __align__(16) float sm4[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int J0 = p.J0, J1 = p.J1, Jl = p.Jl, J1P = p.J1P, J0P = p.J0P;
   const int P1 = J1 * Jl, P = J0 * P1;
-  const int c = blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= P) return;
-  float y = 0.f;
-  for (int q = 0; q < nq; ++q) y += __ldcs(part + (int64_t)(q0 + q) * P + c);
-  const int a0 = c / P1, rest = c - a0 * P1;
-  const int a1 = rest / Jl, b = rest - a1 * Jl;
-  const int64_t col = a0 * s0 + a1 * s1 + b * sb;
-  const int64_t off = transposed ? col * ldY + i : (int64_t)i * ldY + col;
-  split_store(Yhi, Ylo, off, y);
+  // layout: [U_leaf | U_mid1] (SM) | y (P, the slice's partial row) | u0t (J0P x kW4) | warp regions
+  float* Uls = sm4;
+  float* U1s = Uls + (SM ? p.I_leaf * JLP : 0);
+  float* ys = U1s + (SM ? p.I_mid1 * J1P : 0);
+  float* u0t = ys + ((P + 3) & ~3);
+  float* wreg = u0t + J0P * kW4;
+  const int WF = w4_floats(JLP, J1P);
+  float* T = wreg + warp * WF;        // 32 x JLP fiber sums t_f
+  float* Z = T + 32 * JLP;            // J1 x Jl (compact, row j1) node result
+  int* bix = reinterpret_cast<int*>(Z + J1P * JLP);
+  int* stl = bix + 32;                // staged leaf ids
+  float* stv = reinterpret_cast<float*>(stl + kStage4);
+  const unsigned full = 0xffffffffu;
+
+  const int csize = p.csize;
+  const int slice = p.slice0 + (int)(blockIdx.x / csize);
+  const int rank = (int)(blockIdx.x % csize);
+  const int sn0 = p.slice_ptr[slice], sn1 = p.slice_ptr[slice + 1];
+  const int n0 = sn0 + (int)((int64_t)(sn1 - sn0) * rank / csize);
+  const int n1 = sn0 + (int)((int64_t)(sn1 - sn0) * (rank + 1) / csize);
+
+  if (SM) {  // factor tables, rows zero padded to JLP / J1P floats
+    for (int e = threadIdx.x; e < p.I_leaf * JLP; e += blockDim.x) {
+      const int r = e / JLP, j = e - r * JLP;
+      Uls[e] = j < Jl ? __ldg(p.Uleaf + (int64_t)r * Jl + j) : 0.f;
+    }
+    for (int e = threadIdx.x; e < p.I_mid1 * J1P; e += blockDim.x) {
+      const int r = e / J1P, j = e - r * J1P;
+      U1s[e] = j < J1 ? __ldg(p.U1 + (int64_t)r * J1 + j) : 0.f;
+    }
+  }
+  for (int e = threadIdx.x; e < P; e += blockDim.x) ys[e] = 0.f;
+  const int NB = (J1P / 4) * (JLP / 4);  // 4x4 blocks of Z
+  // lane's Z blocks
+  int bro[NBL], bco[NBL];
+#pragma unroll
+  for (int r = 0; r < NBL; ++r) {
+    const int blk = lane + 32 * r;
+    bro[r] = blk < NB ? 4 * (blk / (JLP / 4)) : -1;
+    bco[r] = blk < NB ? 4 * (blk % (JLP / 4)) : 0;
+  }
+  __syncthreads();
+
+  for (int base = n0; base < n1; base += kW4) {
+    const int nd = base + warp;
+    if (nd < n1) {
+      float acc[NBL][4][4];
+#pragma unroll
+      for (int r = 0; r < NBL; ++r)
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) acc[r][i][j] = 0.f;
+      const int f0 = __ldg(p.node_ptr + nd), f1 = __ldg(p.node_ptr + nd + 1);
+      // chunk metadata one chunk ahead
+      int eb = 0, ee = 0, b = 0;
+      if (lane < min(32, f1 - f0)) {
+        eb = __ldg(p.fib_ptr + f0 + lane);
+        ee = __ldg(p.fib_ptr + f0 + lane + 1);
+        b = __ldg(p.fib_mid1 + f0 + lane);
+      }
+      for (int fc = f0; fc < f1; fc += 32) {
+        const int nf = min(32, f1 - fc);
+        const int E0 = __shfl_sync(full, eb, 0), E1 = __shfl_sync(full, ee, nf - 1);
+        const bool staged = E1 - E0 <= kStage4;
+        if (staged) {
+          for (int e = E0 + lane; e < E1; e += 32) {
+            stl[e - E0] = __ldg(p.leaf_id + e);
+            stv[e - E0] = __ldg(p.val + e);
+          }
+        }
+        const int ceb = eb, cee = ee;
+        bix[lane] = SM ? b * J1P : b;
+        const int fn = fc + 32;
+        eb = ee = b = 0;  // lanes past the next chunk's fibers: empty
+        if (fn < f1 && lane < min(32, f1 - fn)) {
+          eb = __ldg(p.fib_ptr + fn + lane);
+          ee = __ldg(p.fib_ptr + fn + lane + 1);
+          b = __ldg(p.fib_mid1 + fn + lane);
+        }
+        __syncwarp();
+        float t[JLP];
+#pragma unroll
+        for (int j = 0; j < JLP; ++j) t[j] = 0.f;
+        for (int e = ceb; e < cee; ++e) {  // lanes >= nf have ceb == cee
+          int cl;
+          float x;
+          if (staged) {
+            cl = stl[e - E0];
+            x = stv[e - E0];
+          } else {
+            cl = __ldg(p.leaf_id + e);
+            x = __ldg(p.val + e);
+          }
+          if (SM) {
+            const float4* r4 = reinterpret_cast<const float4*>(Uls + cl * JLP);
+#pragma unroll
+            for (int q = 0; q < JLP / 4; ++q) {
+              const float4 g = r4[q];
+              t[4 * q] = fmaf(x, g.x, t[4 * q]);
+              t[4 * q + 1] = fmaf(x, g.y, t[4 * q + 1]);
+              t[4 * q + 2] = fmaf(x, g.z, t[4 * q + 2]);
+              t[4 * q + 3] = fmaf(x, g.w, t[4 * q + 3]);
+            }
+          } else {
+            const float* rg = p.Uleaf + (int64_t)cl * Jl;
+#pragma unroll
+            for (int j = 0; j < JLP; ++j)
+              if (j < Jl) t[j] = fmaf(x, __ldg(rg + j), t[j]);
+          }
+        }
+        float4* Tw = reinterpret_cast<float4*>(T + lane * JLP);
+#pragma unroll
+        for (int q = 0; q < JLP / 4; ++q) Tw[q] = make_float4(t[4 * q], t[4 * q + 1], t[4 * q + 2], t[4 * q + 3]);
+        __syncwarp();
+        // level 2: lane owns 4x4 blocks (rows j1 = bro.., cols jl = bco..) of Z; two fibers per step
+        auto kron = [&](int k) {
+          const int bk = bix[k];
+#pragma unroll
+          for (int r = 0; r < NBL; ++r) {
+            if (bro[r] >= 0) {
+              float4 u;
+              if (SM) {
+                u = *reinterpret_cast<const float4*>(U1s + bk + bro[r]);
+              } else {
+                const float* ug = p.U1 + (int64_t)bk * J1;
+                const int j = bro[r];
+                u.x = j < J1 ? __ldg(ug + j) : 0.f;
+                u.y = j + 1 < J1 ? __ldg(ug + j + 1) : 0.f;
+                u.z = j + 2 < J1 ? __ldg(ug + j + 2) : 0.f;
+                u.w = j + 3 < J1 ? __ldg(ug + j + 3) : 0.f;
+              }
+              const float4 tt = *reinterpret_cast<const float4*>(T + k * JLP + bco[r]);
+              const float ua[4] = {u.x, u.y, u.z, u.w}, ta[4] = {tt.x, tt.y, tt.z, tt.w};
+#pragma unroll
+              for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) acc[r][i][j] = fmaf(ua[i], ta[j], acc[r][i][j]);
+            }
+          }
+        };
+        int k = 0;
+        for (; k + 1 < nf; k += 2) {
+          kron(k);
+          kron(k + 1);
+        }
+        if (k < nf) kron(k);
+        __syncwarp();  // T / bix / stage are rewritten by the next chunk
+      }
+      // node result Z (compact J1 x Jl) and its U_mid0 row (transposed: u0t[j0][warp])
+#pragma unroll
+      for (int r = 0; r < NBL; ++r) {
+        if (bro[r] >= 0) {
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              const int j1 = bro[r] + i, jl = bco[r] + j;
+              if (j1 < J1 && jl < Jl) Z[j1 * Jl + jl] = acc[r][i][j];
+            }
+        }
+      }
+      const float* ur = p.U0 + (int64_t)__ldg(p.node_mid0 + nd) * J0;
+      for (int j = lane; j < J0P; j += 32) u0t[j * kW4 + warp] = j < J0 ? __ldg(ur + j) : 0.f;
+    } else {
+      for (int j = lane; j < J0P; j += 32) u0t[j * kW4 + warp] = 0.f;  // idle warp: zero weight
+    }
+    __syncthreads();
+    // level 3: y[j0, rem] += sum_w U_mid0[a_w, j0] Z_w[rem] over the batch's nodes; the thread's
+    // positions rem keep their 8 Z values in registers, the 8 weights come as two broadcast loads
+    const int nw = min(kW4, n1 - base);
+    for (int rem = threadIdx.x; rem < P1; rem += blockDim.x) {
+      float z[kW4];
+#pragma unroll
+      for (int w = 0; w < kW4; ++w) z[w] = w < nw ? wreg[w * WF + 32 * JLP + rem] : 0.f;
+      for (int j0 = 0; j0 < J0; ++j0) {
+        const float4 a = *reinterpret_cast<const float4*>(u0t + j0 * kW4);
+        const float4 c = *reinterpret_cast<const float4*>(u0t + j0 * kW4 + 4);
+        float sacc = ys[j0 * P1 + rem];
+        sacc = fmaf(a.x, z[0], sacc);
+        sacc = fmaf(a.y, z[1], sacc);
+        sacc = fmaf(a.z, z[2], sacc);
+        sacc = fmaf(a.w, z[3], sacc);
+        sacc = fmaf(c.x, z[4], sacc);
+        sacc = fmaf(c.y, z[5], sacc);
+        sacc = fmaf(c.z, z[6], sacc);
+        sacc = fmaf(c.w, z[7], sacc);
+        ys[j0 * P1 + rem] = sacc;
+      }
+    }
+    __syncthreads();
+  }
+
+  // cluster reduction of the slice's partial rows through distributed shared memory
+  cg::cluster_group cl = cg::this_cluster();
+  if (csize > 1) cl.sync();
+  const int c0 = (int)((int64_t)P * rank / csize), c1 = (int)((int64_t)P * (rank + 1) / csize);
+  for (int c = c0 + (int)threadIdx.x; c < c1; c += blockDim.x) {
+    float v = 0.f;
+    for (int r = 0; r < csize; ++r) {
+      const float* peer = csize > 1 ? cl.map_shared_rank(ys, r) : ys;
+      v += peer[c];
+    }
+    const int j0 = c / P1, rem = c - j0 * P1;
+    const int j1 = rem / Jl, jl = rem - j1 * Jl;
+    const int64_t col = j0 * p.s0 + j1 * p.s1 + jl * p.sb;
+    const int64_t off = p.transposed ? col * p.ldY + slice : (int64_t)slice * p.ldY + col;
+    split_store(p.Yhi, p.Ylo, off, v);
+  }
+  if (csize > 1) cl.sync();  // peers' shared memory stays alive until every rank has read it
 }
 
 struct SpmmArgs {
@@ -818,12 +920,7 @@ void spttmc_hooi(const Csf& c, const float* const* U, const int64_t* J, Split ou
       const int NA = (a.Jl + 31) / 32;
 #define TK_TC(na, vw)                                                                          \
   if (!launched && NA == na && VW == vw) {                                                     \
-    static bool attr = false;                                                                  \
-    if (!attr) {                                                                               \
-      TK_CUDA(cudaFuncSetAttribute(k_spttmc3_tc<na, vw>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
-                                   TcTile<na>::SMEM));                                         \
-      attr = true;                                                                             \
-    }                                                                                          \
+    smem_optin((const void*)k_spttmc3_tc<na, vw>, TcTile<na>::SMEM);                          \
     TK_LAUNCH((k_spttmc3_tc<na, vw>), g, 256, TcTile<na>::SMEM, st, a);                        \
     launched = true;                                                                           \
   }
@@ -872,27 +969,61 @@ void spttmc_hooi(const Csf& c, const float* const* U, const int64_t* J, Split ou
   a.s1 = kolda_stride(c.mid1, others, no, J);
   a.sb = kolda_stride(c.leaf, others, no, J);
   const int64_t P = (int64_t)a.J0 * a.J1 * a.Jl;
-  const int RA = rtile(a.J1), RB = rtile(a.Jl);
-  const int64_t RQ = ceil_div(P, 256);
   a.slice0 = (int)lo;
-  a.unit = c.nunits > 0 ? c.unit.p : nullptr;  // the plan (if any) was built for [lo, hi)
-  a.part = c.part.p;
-  const dim3 g((unsigned)(c.nunits > 0 ? c.nunits : hi - lo));
+  a.I_leaf = (int)c.I_leaf;
+  a.I_mid1 = (int)c.I_mid1;
+  a.J1P = (int)round_up(a.J1, 4);
+  a.J0P = (int)round_up(a.J0, 4);
+  const int JLP = (int)round_up(a.Jl, 4);
+  const int NB = (a.J1P / 4) * (JLP / 4);
+  const int64_t nsl = hi - lo;
+  // cluster split: enough CTAs for ~4 per SM, at most 8 (portable cluster size)
+  int num_sms = 0, dev = 0;
+  TK_CUDA(cudaGetDevice(&dev));
+  TK_CUDA(cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev));
+  int cs = 1;
+  while (cs < 8 && nsl * cs < 4 * num_sms) cs *= 2;
+  if (const char* e = std::getenv("TUCKER_TTMC4_CS")) cs = std::max(1, std::min(8, std::atoi(e)));  // tests
+  a.csize = cs;
+  const size_t fac_bytes = ((size_t)a.I_leaf * JLP + (size_t)a.I_mid1 * a.J1P) * sizeof(float);
+  const size_t rest_bytes = ((size_t)round_up(P, 4) + (size_t)a.J0P * kW4 + (size_t)kW4 * w4_floats(JLP, a.J1P)) *
+                            sizeof(float);
+  bool fac_smem = fac_bytes + rest_bytes <= 110 * 1024;
+  if (std::getenv("TUCKER_TTMC4_GMEM")) fac_smem = false;  // tests: factors read from global memory
+  const size_t smem = (fac_smem ? fac_bytes : 0) + rest_bytes;
+  if (smem > 220 * 1024) fail(TUCKER_E_ARG, "spttmc: order-4 core too large for shared memory");
   bool launched = false;
-#define TK_S4(ra, rb, rq)                                                    \
-  if (!launched && RA <= ra && RB <= rb && RQ <= rq) {                       \
-    TK_LAUNCH((k_spttmc4<ra, rb, rq>), g, 256, 0, st, a);                    \
-    launched = true;                                                         \
+  auto launch = [&](const void* fn) {
+    smem_optin(fn, smem);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)(nsl * cs));
+    cfg.blockDim = dim3(256);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = (unsigned)cs;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    void* args[] = {&a};
+    TK_CUDA(cudaLaunchKernelExC(&cfg, fn, args));
+    if (g_launch_counter) ++(*g_launch_counter);
+    if (sync_check_enabled()) TK_CUDA(cudaStreamSynchronize(st));
+    launched = true;
+  };
+#define TK_S4W(jlp, nbl)                                                      \
+  if (!launched && JLP == jlp && NB <= 32 * nbl) {                             \
+    if (fac_smem) launch((const void*)k_spttmc4w<jlp, nbl, true>);             \
+    else launch((const void*)k_spttmc4w<jlp, nbl, false>);                     \
   }
-  TK_S4(1, 1, 4) TK_S4(2, 2, 4) TK_S4(1, 1, 16) TK_S4(2, 2, 16) TK_S4(2, 2, 32) TK_S4(2, 2, 64)
-  TK_S4(4, 4, 32) TK_S4(4, 4, 64)
-#undef TK_S4
-  if (!launched) fail(TUCKER_E_ARG, "spttmc: unsupported order-4 core size (prod J <= 16384, J <= 64)");
-  if (c.nred > 0) {
-    const dim3 gr((unsigned)ceil_div(P, 256), (unsigned)c.nred);
-    TK_LAUNCH(k_spttmc4_reduce, gr, 256, 0, st, c.red.p, c.part.p, a.J0, a.J1, a.Jl, a.s0, a.s1, a.sb, a.Yhi,
-              a.Ylo, ldY, (int)transposed);
-  }
+#define TK_S4WJ(jlp) TK_S4W(jlp, 1) TK_S4W(jlp, 2) TK_S4W(jlp, 4)
+  TK_S4WJ(4) TK_S4WJ(8) TK_S4WJ(12) TK_S4WJ(16) TK_S4WJ(20) TK_S4WJ(24) TK_S4WJ(28) TK_S4WJ(32)
+#undef TK_S4WJ
+#undef TK_S4W
+  if (!launched)
+    fail(TUCKER_E_ARG, "spttmc: unsupported order-4 core size (leaf J <= 32, J_mid1 J_leaf <= 2048)");
 }
 
 // Work plan for the order-3 HOOI kernel (see Csf).  lmax = 1024 nonzeros
@@ -901,54 +1032,6 @@ void spttmc_hooi(const Csf& c, const float* const* U, const int64_t* J, Split ou
 // 1-4 have short fibers and light slices: no plan, one CTA per slice.
 // Config 5's Zipf head (a slice with 7e6 nonzeros in <= 5000 fibers) is what
 // this is for.
-// Order 4: slices are cut into units of at most nmax = max(8, nodes / (16 #SMs))
-// nodes (mid0 indices), each writing a partial row of Jm = J0 J1 times Jl
-// floats (one CTA per slice starves the GPU when there are few slices:
-// config 4 has 200).
-static void spttmc_plan4(Csf& c, int64_t P, int num_sms, cudaStream_t st, int64_t lo, int64_t hi) {
-  std::vector<int32_t> sp((size_t)c.I_root + 1);
-  TK_CUDA(cudaMemcpyAsync(sp.data(), c.slice_ptr.p, sp.size() * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
-  TK_CUDA(cudaStreamSynchronize(st));
-  int64_t nmax = std::max<int64_t>(8, ceil_div((int64_t)(sp[hi] - sp[lo]), (int64_t)16 * num_sms));
-  const char* en = std::getenv("TUCKER_TTMC_NMAX");  // test hook
-  if (en && std::atoll(en) > 0) nmax = std::atoll(en);
-  int64_t widest = 0;
-  for (int64_t i = lo; i < hi; ++i) widest = std::max<int64_t>(widest, sp[i + 1] - sp[i]);
-  c.nunits = c.nred = c.nslots = 0;
-  if (widest <= nmax) return;
-  std::vector<std::array<int32_t, 4>> units;
-  std::vector<int32_t> red;
-  int32_t slot = 0;
-  for (int64_t i = lo; i < hi; ++i) {
-    const int64_t n0 = sp[i], n1 = sp[i + 1];
-    if (n1 == n0) continue;
-    if (n1 - n0 <= nmax) {
-      units.push_back({(int32_t)i, (int32_t)n0, (int32_t)n1, -1});
-      continue;
-    }
-    const int64_t nu = ceil_div(n1 - n0, nmax);
-    red.insert(red.end(), {(int32_t)i, slot, (int32_t)nu});
-    for (int64_t u = 0; u < nu; ++u)
-      units.push_back({(int32_t)i, (int32_t)(n0 + u * (n1 - n0) / nu), (int32_t)(n0 + (u + 1) * (n1 - n0) / nu), slot++});
-  }
-  std::stable_sort(units.begin(), units.end(), [](const std::array<int32_t, 4>& x, const std::array<int32_t, 4>& y) {
-    return x[2] - x[1] > y[2] - y[1];
-  });
-  std::vector<int32_t> flat;
-  for (const auto& u : units) flat.insert(flat.end(), u.begin(), u.end());
-  c.nunits = (int64_t)units.size();
-  c.nred = (int64_t)red.size() / 3;
-  c.nslots = slot;
-  c.unit.alloc(flat.size());
-  TK_CUDA(cudaMemcpyAsync(c.unit.p, flat.data(), flat.size() * sizeof(int32_t), cudaMemcpyHostToDevice, st));
-  if (!red.empty()) {
-    c.red.alloc(red.size());
-    TK_CUDA(cudaMemcpyAsync(c.red.p, red.data(), red.size() * sizeof(int32_t), cudaMemcpyHostToDevice, st));
-    c.part.alloc((size_t)(c.nslots * P));
-  }
-  TK_CUDA(cudaStreamSynchronize(st));
-}
-
 // Exact (int64) plan statistics on the device, so the common no-plan case costs
 // three numbers of D2H instead of the fiber pointers: out[0] = longest fiber,
 // out[1] = total work sum_f (wf ceil(L/lmax) + wn L), out[2] = heaviest slice
@@ -973,10 +1056,7 @@ __global__ void k_plan_stats(const int32_t* __restrict__ sp, const int32_t* __re
 
 void spttmc_plan(Csf& c, int64_t Jm, int64_t Jl, int num_sms, cudaStream_t st, int64_t lo, int64_t hi) {
   if (hi < 0) hi = c.I_root;
-  if (c.order == 4) {
-    spttmc_plan4(c, Jm * Jl, num_sms, st, lo, hi);
-    return;
-  }
+  if (c.order == 4) return;  // k_spttmc4w splits slices over thread-block clusters instead
   if (c.order != 3) return;
   const int64_t I = c.I_root, F = c.nfib;
   c.lmax = 1024;

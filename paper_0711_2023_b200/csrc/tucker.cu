@@ -328,6 +328,8 @@ void eig_check(tucker_handle* h, int r0 = kMaxOrder, int r1 = kMaxOrder + 1) {
       if (dv[0] >= 0) sl->lmin = dv[0];  // a new Lanczos estimate (0: none useful)
       if (dv[1] > 0) sl->bval = dv[1];
     }
+    // a broken-down or unconverged solve leaves no trustworthy basis to warm-start from
+    if ((in[4] || !in[0]) && h->rec_slot[r]) h->rec_slot[r]->valid = false;
     if (in[4]) fail(TUCKER_E_CUDA, "eigensolver breakdown (non-finite Rayleigh quotient)");
     if (!in[0]) h->eig_unconverged = true;
     h->eig.stat_outer += in[1];
@@ -572,10 +574,20 @@ int tucker_init(tucker_handle** out, int order, const int64_t* dims, const int64
   if (o.world < 1 || o.rank < 0 || o.rank >= o.world) return TUCKER_E_ARG;
   const bool host_coll = (o.flags & TUCKER_HOST_COLLECTIVES) != 0;
   if (o.world > 1 && !o.nccl_unique_id && !host_coll) return TUCKER_E_ARG;
+  uint64_t cells = 1;  // the CSF sort keys pack every coordinate into one 64-bit key
   for (int n = 0; n < order; ++n) {
     if (dims[n] < 1 || dims[n] >= (int64_t)1 << 31) return TUCKER_E_ARG;
     if (core[n] < 1 || core[n] > dims[n] || core[n] > kMaxJ) return TUCKER_E_ARG;
     if (!idx[n] || !U0[n]) return TUCKER_E_ARG;
+    if (__builtin_mul_overflow(cells, (uint64_t)dims[n], &cells)) return TUCKER_E_ARG;
+  }
+  // J_n <= prod_{q != n} J_q: Y_(n) has rank <= prod_{q != n} J_q, so a larger J_n
+  // has no J_n-dimensional dominant subspace to return (S:136 rank deficiency)
+  for (int n = 0; n < order; ++n) {
+    int64_t P = 1;
+    for (int q = 0; q < order; ++q)
+      if (q != n) P *= core[q];
+    if (core[n] > P) return TUCKER_E_ARG;
   }
   const bool on_dev = (o.flags & TUCKER_INPUT_ON_DEVICE) != 0;
   if (!on_dev)
@@ -873,6 +885,7 @@ int tucker_set_factor(tucker_handle* h, int n, const float* U, int check) {
                             on_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, h->st));
     TK_CUDA(cudaStreamSynchronize(h->st));
     h->G_valid = false;
+    for (auto& row : h->slots) row[n].valid = false;  // the next solve of mode n starts from U
     return TUCKER_OK;
   });
 }
@@ -1023,6 +1036,39 @@ int tucker_debug_product_time(int d, int n, int reps, double* us) {
     *us = eig_unit_mv_time(d, n, reps);
     return TUCKER_OK;
   });
+}
+
+int tucker_time_ttmc(tucker_handle* h, int mode, int reps, float* ms_out) {
+  if (!h || !ms_out || mode < 0 || mode >= h->order || reps < 1) return TUCKER_E_ARG;
+  return guarded(h, [&]() -> int {
+    const bool tr = prod_J_except(h, mode) < h->dims[mode];
+    project_hooi(h, mode, tr);  // untimed: buffers, first-touch
+    SweepEvents ev(2);
+    TK_CUDA(cudaEventRecord(ev.e[0], h->st));
+    for (int r = 0; r < reps; ++r) project_hooi(h, mode, tr);
+    TK_CUDA(cudaEventRecord(ev.e[1], h->st));
+    TK_CUDA(cudaEventSynchronize(ev.e[1]));
+    *ms_out = ev.ms(0, 1) / (float)reps;
+    h->G_valid = false;
+    return TUCKER_OK;
+  });
+}
+
+int tucker_csf_layout(tucker_handle* h, int64_t* out) {
+  if (!h || !out) return TUCKER_E_ARG;
+  for (int n = 0; n < h->order; ++n) {
+    const Csf& c = *h->csfs[h->hooi_csf[n]];
+    int64_t* o = out + 8 * n;
+    o[0] = c.root;
+    o[1] = c.mid0;
+    o[2] = c.order == 4 ? c.mid1 : -1;
+    o[3] = c.leaf;
+    o[4] = c.nfib;
+    o[5] = c.order == 4 ? c.nnode : 0;
+    o[6] = c.nnz;
+    o[7] = c.I_root;
+  }
+  return TUCKER_OK;
 }
 
 int tucker_csf_stats(tucker_handle* h, int64_t* out) {

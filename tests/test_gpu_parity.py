@@ -100,25 +100,41 @@ def test_ttmc_parity_skewed(capi, monkeypatch, lmax, cmax, kernel):
     assert np.max(np.abs(np.asarray(fits) - np.asarray(ref["fits"]))) < 1e-5
 
 
-@pytest.mark.parametrize("nmax", [None, "3"])
-def test_ttmc_parity_order4_plan(capi, monkeypatch, nmax):
-    """Order 4 with the work plan forced (slices cut into node ranges of <= nmax
-    mid0 indices, fp32 partial rows summed in slot order): Y and a HOOI sweep
-    agree with the oracle."""
+@pytest.mark.parametrize("cs,gmem", [(None, None), ("1", None), ("2", "1"), ("8", None), ("4", "1")])
+def test_ttmc_parity_order4_clusters(capi, monkeypatch, cs, gmem):
+    """Order 4 (k_spttmc4w): every slice split over a thread-block cluster of
+    1/2/4/8 CTAs whose partial rows are summed through distributed shared memory,
+    with the factor tables in shared memory or read from global memory; Y and a
+    HOOI sweep agree with the oracle, and the result is bit-identical across
+    cluster sizes' repeated runs."""
     dims, nnz, core = (20, 22, 18, 16), 12_000, (4, 5, 3, 6)
     idx, vals, U0 = case(dims, nnz, core)
-    if nmax:
-        monkeypatch.setenv("TUCKER_TTMC_NMAX", nmax)
+    if cs:
+        monkeypatch.setenv("TUCKER_TTMC4_CS", cs)
+    if gmem:
+        monkeypatch.setenv("TUCKER_TTMC4_GMEM", gmem)
     T = O.SparseTensor(dims, idx, vals)
     with capi.Tucker(dims, core, idx, vals, U0) as t:
-        st = t.csf_stats()
-        if nmax:
-            assert all(u > 0 for _, _, _, u in st), st
         for n in range(4):
-            assert O.rel_frobenius(t.debug_ttmc(n), O.ttm_chain_unfold(T, U0, n)) < 1e-4
+            Y = t.debug_ttmc(n)
+            assert O.rel_frobenius(Y, O.ttm_chain_unfold(T, U0, n)) < 1e-4
+            np.testing.assert_array_equal(Y, t.debug_ttmc(n))
         fits = t.hooi_sweep(2)
     ref = O.run_hooi(T, U0, core, 2)
     assert np.max(np.abs(np.asarray(fits) - np.asarray(ref["fits"]))) < 1e-5
+
+
+@pytest.mark.parametrize("dims,nnz,core", [((9, 40, 33, 7), 6_000, (3, 8, 12, 2)),
+                                            ((30, 6, 5, 50), 4_000, (7, 2, 5, 9)),
+                                            ((12, 13, 14, 15), 20_000, (2, 3, 5, 7))])
+def test_ttmc_parity_order4_shapes(capi, dims, nnz, core):
+    """Ragged order-4 shapes: core sizes that are not multiples of 4 (padded
+    factor rows), empty slices and nodes, and different leaf / mid choices."""
+    idx, vals, U0 = case(dims, nnz, core)
+    T = O.SparseTensor(dims, idx, vals)
+    with capi.Tucker(dims, core, idx, vals, U0) as t:
+        for n in range(4):
+            assert O.rel_frobenius(t.debug_ttmc(n), O.ttm_chain_unfold(T, U0, n)) < 1e-4
 
 
 @pytest.mark.parametrize("dims,nnz,core", SHAPES)
@@ -169,7 +185,16 @@ def run_both(capi, dims, idx, vals, U0, core, sweeps):
         fm = t.mp_sweep(sweeps)
         Gm, Um, fitm = t.core_and_fit()
         out["mp"] = (fm, Gm, Um, fitm)
-    ref = {"hooi": O.run_hooi(T, U0, core, sweeps), "mp": O.run_mp(T, U0, core, sweeps)}
+    dh, dm = [], []
+    ref = {"hooi": O.run_hooi(T, U0, core, sweeps, diag=dh), "mp": O.run_mp(T, U0, core, sweeps, diag=dm)}
+    # the conditioning of every factor update the parity rests on
+    N = len(dims)
+    for algo, dg in (("hooi", dh), ("mp", dm)):
+        for i, d in enumerate(dg):
+            print(f"kappa {algo} sweep {i // N} mode {d['mode'] + 1}: lambda_1 {d['l1']:.6g} "
+                  f"lambda_J {d['lJ']:.6g} lambda_J+1 {d['lJ1']:.6g} rel_gap {d['rel_gap']:.3g} "
+                  f"kappa {d['kappa']:.4g}")
+    ref["hooi"]["diag"], ref["mp"]["diag"] = dh, dm
     return out, ref
 
 
@@ -199,16 +224,18 @@ def test_config1_full(capi):
         assert abs(fit - ref[algo]["fit"]) < 1e-5
 
 
-@pytest.mark.parametrize("k,sweeps", [(2, None), (3, 2), (4, 2)])
-def test_config_full(capi, k, sweeps):
-    """BASELINE.json configs[k-1] at full size from the seeded U0: config 2 with its
-    5 HOOI + 5 MP sweeps (the bench's workload), configs 3 (2000^3, 8e6 nnz, core
-    100x25x10) and 4 (order 4, 200^4, 1.6e7 nnz) with 2 sweeps each to bound the fp64
-    oracle's host time.  Factors (projector distance), fits per sweep and the core
-    (after Procrustes alignment) vs the oracle."""
+@pytest.mark.parametrize("k", [2, 3, 4])
+def test_config_full(capi, k, record_property):
+    """BASELINE.json configs[k-1] at full size from the seeded U0 with their full
+    5 HOOI + 5 MP sweeps: config 2 (1000^3, 1e6 nnz, core 50^3), config 3 (2000^3,
+    8e6 nnz, unbalanced core 100x25x10) and config 4 (order 4, 200^4, 1.6e7 nnz, the
+    bench's workload).  Factors (projector distance), fits per sweep and the core
+    (after Procrustes alignment) vs the oracle; kappa of every update is printed and
+    recorded."""
     c = make_config(k)
-    sw = c["sweeps"] if sweeps is None else sweeps
+    sw = c["sweeps"]
     out, ref = run_both(capi, c["dims"], c["idx"], c["vals"], c["U0"], c["core"], sw)
+    record_property("kappa", {a: [round(d["kappa"], 3) for d in ref[a]["diag"]] for a in ("hooi", "mp")})
     for algo in ("hooi", "mp"):
         fits, G, U, fit = out[algo]
         r = ref[algo]

@@ -408,3 +408,102 @@ def test_p12_table2_sp_statistical_pin(golden_dir):
     core = tuple(case["core"])
     C0 = sp_random_init(T.dims[-1], core[-1], np.random.default_rng(7))
     assert abs(100 * O.run_sp_converged(T, core, C0)["fit"] - case["sp"]) < tol
+
+
+# ------------------------------------- the parity metric and the large-tensor routes ----
+
+def test_projector_distance_pins():
+    """The metric behind every factor-parity assertion, pinned to its definition
+    ||U U^T - V V^T||_F written out with explicit I x I projectors, and to closed
+    forms: a subspace that differs in one orthogonal direction is sqrt(2) away,
+    orthogonal J-dimensional subspaces are sqrt(2 J) apart, and rotating or
+    sign-flipping the basis changes nothing."""
+    r = rng(40)
+    for I, J in [(7, 1), (12, 3), (30, 5), (9, 9)]:
+        U = np.linalg.qr(r.standard_normal((I, J)))[0]
+        V = np.linalg.qr(r.standard_normal((I, J)))[0]
+        explicit = np.linalg.norm(U @ U.T - V @ V.T)
+        assert abs(O.projector_distance(U, V) - explicit) < 1e-12
+        Q = np.linalg.qr(r.standard_normal((J, J)))[0]
+        assert O.projector_distance(U, U @ Q) < 1e-12
+        assert O.projector_distance(U, U * np.where(np.arange(J) % 2, -1.0, 1.0)) < 1e-12
+    # one column swapped for a direction orthogonal to the whole subspace
+    B = np.linalg.qr(r.standard_normal((10, 4)))[0]
+    U, V = B[:, :3], np.c_[B[:, :2], B[:, 3]]
+    assert abs(O.projector_distance(U, V) - np.sqrt(2.0)) < 1e-12
+    # mutually orthogonal subspaces
+    assert abs(O.projector_distance(B[:, :2], B[:, 2:]) - 2.0) < 1e-12
+    # small rotation by angle eps out of the subspace: distance = sqrt(2) sin(eps)
+    eps = 1e-5
+    W = B[:, :3].copy()
+    W[:, 0] = np.cos(eps) * B[:, 0] + np.sin(eps) * B[:, 3]
+    assert abs(O.projector_distance(B[:, :3], W) - np.sqrt(2.0) * np.sin(eps)) < 1e-15
+
+
+@pytest.mark.parametrize("dims,core,density", [((7, 9, 5), (2, 3, 2), 0.3), ((11, 4, 6), (3, 2, 4), 0.15),
+                                                ((5, 13, 8), (4, 5, 3), 0.05)])
+def test_slice_chain_matches_eq1_loops(dims, core, density):
+    """ttm_chain_unfold_slices (the Appendix's B' X_slice C per slice) against
+    pure Eq. 1 loops over the nonzeros (no shared code), ragged dims and sparse
+    enough that some slices and fibers are empty."""
+    X, T = rand_sparse(dims, density, 41)
+    U = rand_factors(dims, core, 42)
+    for n in range(3):
+        Y = O.ttm_chain_unfold_slices(T, U, n)
+        others = [m for m in range(3) if m != n]
+        Yb = np.zeros((dims[n], core[others[0]] * core[others[1]]))
+        for e in range(T.vals.size):
+            ii = [T.idx[m][e] for m in range(3)]
+            for ja in range(core[others[0]]):
+                for jb in range(core[others[1]]):
+                    Yb[ii[n], ja + core[others[0]] * jb] += (T.vals[e] * U[others[0]][ii[others[0]], ja]
+                                                             * U[others[1]][ii[others[1]], jb])
+        np.testing.assert_allclose(Y, Yb, rtol=1e-12, atol=1e-13)
+        np.testing.assert_allclose(Y, O.ttm_chain_unfold(T, U, n), rtol=1e-12, atol=1e-13)
+
+
+@pytest.mark.parametrize("shape,J", [((40, 12), 3), ((57, 9), 9), ((25, 24), 5)])
+def test_gram_t_route_is_left_singular_subspace(shape, J):
+    """Reading A10: U from Y^T Y equals the J leading left singular vectors of Y
+    (numpy's SVD, a library routine) and the Y Y^T route, including the sign
+    convention; it is orthonormal and its eigenvalues are sigma^2."""
+    r = rng(43)
+    Y = r.standard_normal(shape) @ np.diag(np.linspace(3.0, 1.0, shape[1]))
+    U, w = O.leading_left_vectors_gram_t(Y, J)
+    Us, sv, _ = np.linalg.svd(Y, full_matrices=False)
+    assert O.projector_distance(U, Us[:, :J]) < 1e-10
+    np.testing.assert_allclose(w[:J], sv[:J] ** 2, rtol=1e-12)
+    assert np.abs(U.T @ U - np.eye(J)).max() < 1e-12
+    V, _ = O.leading_eigenvectors(Y @ Y.T, J)
+    np.testing.assert_allclose(U, V, atol=1e-10)  # same columns, same signs (S:136)
+    with pytest.raises(ValueError):
+        O.leading_left_vectors_gram_t(np.c_[Y[:, :2], Y[:, :2]], 4)  # rank 2 < J
+
+
+@pytest.mark.parametrize("dims,core", [((30, 8, 9), (4, 3, 3)), ((10, 12, 40), (3, 4, 5))])
+def test_hooi_large_matches_hooi(dims, core):
+    """The large-tensor driver (slice-wise chain, Y^T Y route where I_n > prod J,
+    core from the last projection) reproduces run_hooi sweep by sweep; both Gram
+    routes occur in these shapes."""
+    X, T = rand_sparse(dims, 0.2, 44)
+    U0 = rand_factors(dims, core, 45)
+    assert any(dims[n] > np.prod([core[m] for m in range(3) if m != n]) for n in range(3))
+    a = O.run_hooi(T, U0, core, 3)
+    b = O.run_hooi_large(T, U0, core, 3)
+    np.testing.assert_allclose(b["fits"], a["fits"], atol=1e-12)
+    for n in range(3):
+        assert O.projector_distance(a["U"][n], b["U"][n]) < 1e-9
+    np.testing.assert_allclose(b["G"], O.core(T, b["U"]), atol=1e-12)
+
+
+def test_hooi_large_exact_multilinear_rank():
+    """P1 through the large-tensor driver: exact multilinear rank gives fit 1."""
+    dims, core = (40, 9, 10), (3, 2, 4)
+    r = rng(46)
+    C = r.standard_normal(core)
+    A = [np.linalg.qr(r.standard_normal((I, J)))[0] for I, J in zip(dims, core)]
+    T = O.SparseTensor.from_dense(O.tucker_operator(C, A))
+    out = O.run_hooi_large(T, rand_factors(dims, core, 47), core, 1)
+    assert out["fit"] > 1 - 1e-6
+    for n in range(3):
+        assert O.projector_distance(out["U"][n], A[n]) < 1e-8
