@@ -213,7 +213,7 @@ int tucker_csf_layout(tucker_handle* h, int64_t* out);
 /* Kernel statistics of the handle since the last reset (for bench/roofline):
  * stats[0] = kernel launches issued by the library, [1] = eigensolver outer
  * iterations, [2] = Chebyshev matvecs, [3] = small (k x k) Jacobi sweeps,
- * [4] = Gram path (0 = tcgen05 3xTF32, 1 = SIMT fp64), [5..12] = time inside the
+ * [4] = Gram path (0 = by size: fp64 DMMA up to 2e10 FMA, tcgen05 3xTF32 above; 1 = fp64 DMMA for every Gram, env TUCKER_GRAM_FP64=1), [5..12] = time inside the
  * fused eigensolver kernel by phase in ns as seen by its CTA 0 (matvec, k x k
  * reductions, CholQR factor, Jacobi, row-block apply, deflation, power/Lanczos,
  * other), [13] = algorithmic fp64 flops of the eigensolver (products 2 d^2 n,

@@ -471,7 +471,7 @@ def tucker_stats(h, reset=False):
     _check(lib().tucker_stats(h, s, 1 if reset else 0), h)
     names = ("matvec", "reduce", "cholqr", "jacobi", "apply", "deflate", "power", "other")
     return dict(launches=s[0], eig_outer=s[1], eig_matvec=s[2], jacobi_sweeps=s[3],
-                gram_path="tcgen05-3xtf32" if s[4] == 0 else "simt-fp64",
+                gram_path="by-size (dmma <= 2e10 FMA, else tcgen05 3xTF32)" if s[4] == 0 else "all-dmma-fp64",
                 eig_phase_ms={n: s[5 + i] / 1e6 for i, n in enumerate(names)},
                 eig_flops=s[13],
                 product_ms={n: s[14 + i] / 1e6 for i, n in enumerate(("phaseA", "inner_bar", "phaseB", "lead_bar"))})

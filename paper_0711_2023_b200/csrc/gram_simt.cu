@@ -7,7 +7,8 @@
 //     bulk eigenvectors next to an outlier theta_1 >> theta_J are sensitive to
 //     relative errors of S at the 1e-7 level that 3xTF32 leaves (config 4 HOOI,
 //     theta_1 / gap ~ 1e4).
-//   * k_syrk_simt: reference SIMT fp64 kernel (TUCKER_GRAM=simt), validation.
+// (TUCKER_GRAM_FP64=1 sends every Gram through DMMA: a precision experiment switch,
+// used to separate Gram rounding from projection rounding at config 5.)
 #include <algorithm>
 #include <cstdlib>
 #include <cstring>
@@ -17,55 +18,6 @@
 
 namespace tk {
 namespace {
-
-constexpr int TB = 64, TK = 16;
-
-__global__ void __launch_bounds__(256) k_syrk_simt(const float* __restrict__ hi,
-                                                   const float* __restrict__ lo, int64_t d,
-                                                   int64_t K, int64_t lda, double* __restrict__ S,
-                                                   int64_t lds) {
-  // upper-triangle tile (bi <= bj) from a linear block index
-  int64_t t = blockIdx.x, bi = 0;
-  const int64_t nb = (d + TB - 1) / TB;
-  while (t >= nb - bi) { t -= nb - bi; ++bi; }
-  const int64_t bj = bi + t;
-  __shared__ double As[TK][TB + 1], Bs[TK][TB + 1];
-  const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
-  double acc[4][4] = {};
-  for (int64_t k0 = 0; k0 < K; k0 += TK) {
-    for (int e = tid; e < TB * TK; e += 256) {
-      const int kk = e % TK, rr = e / TK;
-      const int64_t k = k0 + kk;
-      const int64_t ra = bi * TB + rr, rb = bj * TB + rr;
-      As[kk][rr] = (ra < d && k < K) ? (double)hi[ra * lda + k] + (double)lo[ra * lda + k] : 0.0;
-      Bs[kk][rr] = (rb < d && k < K) ? (double)hi[rb * lda + k] + (double)lo[rb * lda + k] : 0.0;
-    }
-    __syncthreads();
-#pragma unroll
-    for (int kk = 0; kk < TK; ++kk) {
-      double a[4], b[4];
-#pragma unroll
-      for (int i = 0; i < 4; ++i) a[i] = As[kk][ty + 16 * i];
-#pragma unroll
-      for (int j = 0; j < 4; ++j) b[j] = Bs[kk][tx + 16 * j];
-#pragma unroll
-      for (int i = 0; i < 4; ++i)
-#pragma unroll
-        for (int j = 0; j < 4; ++j) acc[i][j] = fma(a[i], b[j], acc[i][j]);
-    }
-    __syncthreads();
-  }
-#pragma unroll
-  for (int i = 0; i < 4; ++i)
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int64_t r = bi * TB + ty + 16 * i, c = bj * TB + tx + 16 * j;
-      if (r < d && c < d) {
-        S[r * lds + c] = acc[i][j];
-        S[c * lds + r] = acc[i][j];
-      }
-    }
-}
 
 // ---------------------------------------------------------------- DMMA path --
 constexpr int DT = 64, DKC = 32, DSP = DKC + 4;  // tile, K chunk, smem row stride (conflict-free)
@@ -189,17 +141,11 @@ void gram_syrk_dmma(const Split& A, double* S, int64_t lds, GramWs& ws, cudaStre
             (const int2*)ws.scratch.p, ntiles, splits, d, S, lds);
 }
 
-void gram_syrk_simt(const Split& A, double* S, int64_t lds, cudaStream_t st) {
-  const int64_t nb = ceil_div(A.rows, TB);
-  TK_LAUNCH(k_syrk_simt, (unsigned)(nb * (nb + 1) / 2), 256, 0, st, A.hi, A.lo, A.rows,
-            A.kext > 0 ? A.kext : A.cols, A.ld, S, lds);
-}
-
 int gram_mode() {
   static int mode = -1;
   if (mode < 0) {
-    const char* e = std::getenv("TUCKER_GRAM");
-    mode = (e && std::strcmp(e, "simt") == 0) ? 1 : 0;
+    const char* e = std::getenv("TUCKER_GRAM_FP64");  // precision experiments: every Gram in fp64
+    mode = (e && std::strcmp(e, "1") == 0) ? 1 : 0;
   }
   return mode;
 }

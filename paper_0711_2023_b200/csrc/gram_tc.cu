@@ -278,17 +278,13 @@ void gram_syrk_tc(const Split& A, double* S, int64_t lds, GramWs& ws, cudaStream
 // (<= 2e10 FMA, ~1 ms at the measured 37 TFLOP/s; all HOOI Grams of configs 1-4),
 // 3xTF32 tcgen05 with fp64 drains for the large MP Grams.
 void gram_syrk(const Split& A, double* S, int64_t lds, GramWs& ws, cudaStream_t st) {
-  if (gram_mode() == 1) {
-    gram_syrk_simt(A, S, lds, st);
-    return;
-  }
   if (A.K() == 0) {  // empty K shard: S = 0
     for (int64_t i = 0; i < A.rows; ++i)
       TK_CUDA(cudaMemsetAsync(S + i * lds, 0, A.rows * sizeof(double), st));
     return;
   }
   const double fma = 0.5 * (double)A.rows * (double)(A.rows + 1) * (double)A.K();
-  if (fma <= 2e10) gram_syrk_dmma(A, S, lds, ws, st);
+  if (fma <= 2e10 || gram_mode() == 1) gram_syrk_dmma(A, S, lds, ws, st);
   else gram_syrk_tc(A, S, lds, ws, st);
 }
 

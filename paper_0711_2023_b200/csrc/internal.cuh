@@ -106,10 +106,8 @@ struct GramWs {
 void gram_syrk(const Split& A, double* S, int64_t lds, GramWs& ws, cudaStream_t st);
 // fp64 tensor-core (DMMA) path for Grams small enough to afford fp64
 void gram_syrk_dmma(const Split& A, double* S, int64_t lds, GramWs& ws, cudaStream_t st);
-// reference SIMT fp64 path (debug/validation of the tensor-core kernel)
-void gram_syrk_simt(const Split& A, double* S, int64_t lds, cudaStream_t st);
-int gram_mode();     // 0 = tcgen05 (default), 1 = SIMT (env TUCKER_GRAM=simt)
-int gram_path_id();  // path gram_syrk takes: 0 = tcgen05 3xTF32, 1 = SIMT fp64
+int gram_mode();     // 0 = by size (default), 1 = every Gram on fp64 DMMA (env TUCKER_GRAM_FP64=1)
+int gram_path_id();  // 0 = by size (DMMA <= 2e10 FMA, else tcgen05 3xTF32), 1 = all DMMA
 
 // dense.cu -- small fp64 dense kernels for the eigensolver and the core.
 enum class Elt { F64, F32, SPLIT };

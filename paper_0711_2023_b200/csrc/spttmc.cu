@@ -312,7 +312,11 @@ __global__ void __launch_bounds__(256) k_spttmc3(Ttmc3Args p) {
 // TMEM, D = 128 x N with row a = mid index, column b = leaf index).  Both
 // operands are K-major with the 128-byte swizzle (the layout the Gram kernel
 // uses): one operand row = one mid/leaf index, its 32 fibers = one 128-byte
-// swizzle row, so the leaf stage stores fiber k's values into column k.  One
+// swizzle row, so the leaf stage stores fiber k's values into column k.  The
+// TMEM accumulator is drained into fp32 registers every kTcGroup chunks and
+// restarted (measured: accumulating a whole heavy slice in TMEM left Y with
+// 3-5e-5 relative error at config 5 mode 3, against ~5e-7 for the SIMT kernel --
+// the tensor core's accumulation is not an IEEE fp32 sum).  One
 // operand buffer (so 3-4 CTAs fit per SM and the latency-bound gathers have
 // warps to hide behind): the chunk's metadata staging overlaps the previous
 // chunk's MMAs, and the operand stores wait for their commit.
@@ -320,6 +324,7 @@ __global__ void __launch_bounds__(256) k_spttmc3(Ttmc3Args p) {
 // zeros in tools/umma_mn_test.cu; K-major is the verified layout.)
 // ---------------------------------------------------------------------------
 constexpr int KC = 32;                // fibers (K) per chunk = one 128-byte swizzle row
+constexpr int kTcGroup = 4;           // chunks accumulated in TMEM between drains into registers
 constexpr int TC_A_BYTES = 128 * 128; // A: 128 rows (M) x 128 B
 
 template <int NA>  // B: 32 NA rows (N = 32 NA)
@@ -396,6 +401,22 @@ __global__ void __launch_bounds__(256) k_spttmc3_tc(Ttmc3Args p) {
   const uint32_t tmem = tmem_slot;
   const uint32_t sbase = tc::smem_u32(smem);
 
+  // register accumulators: warp w drains TMEM lanes 32 (w % 4).. (D rows = mid index), columns
+  // [16 NA (w / 4), 16 NA (w / 4 + 1)) (the warp's lane quarter is fixed by its rank in the warpgroup)
+  float racc[16 * NA];
+#pragma unroll
+  for (int j = 0; j < 16 * NA; ++j) racc[j] = 0.f;
+  const uint32_t tq = tmem + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)(16 * NA * (warp >> 2));
+  auto drain = [&]() {
+#pragma unroll
+    for (int q = 0; q < NA; ++q) {
+      float v[16];
+      tc::tmem_ld16(tq + (uint32_t)(16 * q), v);
+      tc::tmem_wait_ld();
+#pragma unroll
+      for (int j = 0; j < 16; ++j) racc[16 * q + j] += v[j];
+    }
+  };
   int c = 0;
   for (int fc = f0; fc < f1; fc += KC, ++c) {
     const int nf = min(KC, f1 - fc);
@@ -465,8 +486,14 @@ __global__ void __launch_bounds__(256) k_spttmc3_tc(Ttmc3Args p) {
         }
       }
     }
-    // the operand buffer was last read by the MMAs of chunk c - 1
+    // the operand buffer was last read by the MMAs of chunk c - 1; when c - 1 closed a TMEM
+    // group, its sum moves into the registers before chunk c restarts the accumulator
     if (c >= 1) tc::mbar_wait(&mma_done, (uint32_t)((c - 1) & 1));
+    if (c >= 1 && c % kTcGroup == 0) {
+      tc::tc_fence_after();
+      drain();
+      tc::tc_fence_before();
+    }
     __syncthreads();
     // transpose into the K-major operands: lanes run over the 32 fibers, so a
     // warp's store fills one 128-byte swizzle row (conflict-free)
@@ -495,35 +522,31 @@ __global__ void __launch_bounds__(256) k_spttmc3_tc(Ttmc3Args p) {
 #pragma unroll
       for (int g = 0; g < KC / 8; ++g) {
         const uint32_t o = (uint32_t)(g * 32);  // 8 tf32 = 32 bytes along K inside the swizzle row
-        tc::umma_tf32(tmem, tc::sw128_desc(ah + o), tc::sw128_desc(bh + o), Tile::IDESC, (c > 0 || g > 0) ? 1u : 0u);
+        tc::umma_tf32(tmem, tc::sw128_desc(ah + o), tc::sw128_desc(bh + o), Tile::IDESC,
+                      (c % kTcGroup > 0 || g > 0) ? 1u : 0u);
         tc::umma_tf32(tmem, tc::sw128_desc(ah + o), tc::sw128_desc(bl + o), Tile::IDESC, 1u);
         tc::umma_tf32(tmem, tc::sw128_desc(al + o), tc::sw128_desc(bh + o), Tile::IDESC, 1u);
       }
       tc::umma_commit(&mma_done);
     }
   }
-  // all MMAs done once the last chunk's commit arrives
+  // all MMAs done once the last chunk's commit arrives; the last (partial) group joins the registers
   tc::mbar_wait(&mma_done, (uint32_t)((c - 1) & 1));
   tc::tc_fence_after();
-  if (warp < 4) {
-    const int a = 32 * warp + lane;  // D row = mid index
+  drain();
+  {
+    const int a = 32 * (warp & 3) + lane;  // D row = mid index
+    if (a < p.Jm) {
 #pragma unroll
-    for (int nb = 0; nb < NA; ++nb) {
-      float v[32];
-      tc::tmem_ld32(tmem + ((uint32_t)(32 * warp) << 16) + (uint32_t)(32 * nb), v);
-      tc::tmem_wait_ld();
-      if (a < p.Jm) {
-#pragma unroll
-        for (int j = 0; j < 32; ++j) {
-          const int bcol = 32 * nb + j;
-          if (bcol < p.Jl) {
-            if (slot >= 0) {
-              p.part[(int64_t)slot * p.Jm * p.Jl + a * p.Jl + bcol] = v[j];
-            } else {
-              const int64_t col = a * p.sa + bcol * p.sb;
-              const int64_t off = p.transposed ? col * p.ldY + i : (int64_t)i * p.ldY + col;
-              split_store(p.Yhi, p.Ylo, off, v[j]);
-            }
+      for (int j = 0; j < 16 * NA; ++j) {
+        const int bcol = 16 * NA * (warp >> 2) + j;
+        if (bcol < p.Jl) {
+          if (slot >= 0) {
+            p.part[(int64_t)slot * p.Jm * p.Jl + a * p.Jl + bcol] = racc[j];
+          } else {
+            const int64_t col = a * p.sa + bcol * p.sb;
+            const int64_t off = p.transposed ? col * p.ldY + i : (int64_t)i * p.ldY + col;
+            split_store(p.Yhi, p.Ylo, off, racc[j]);
           }
         }
       }
@@ -586,10 +609,12 @@ struct Ttmc4Args {
 // (deterministic, no atomics, no partial rows in HBM) and written once.
 // ---------------------------------------------------------------------------
 constexpr int kW4 = 8;        // warps = nodes in flight per CTA
+constexpr int kNPW = 1;       // nodes per warp between the CTA's level-3 barriers (2: one CTA per SM, slower)
+constexpr int kB4 = kW4 * kNPW;  // nodes per batch
 constexpr int kStage4 = 128;  // staged nonzeros per warp and fiber chunk (longer chunks read global memory)
 
-// per-warp region (floats): T 32 x JLP | Z J1 x Jl (<= J1P JLP) | bix 32 | staged leaf ids / values
-__host__ __device__ inline int w4_floats(int JLP, int J1P) { return 32 * JLP + J1P * JLP + 32 + 2 * kStage4; }
+// per-warp region (floats): T 32 x JLP | Z kNPW x (J1 x Jl <= J1P JLP) | bix 32 | staged leaf ids / values
+__host__ __device__ inline int w4_floats(int JLP, int J1P) { return 32 * JLP + kNPW * J1P * JLP + 32 + 2 * kStage4; }
 
 template <int JLP, int NBL, bool SM>
 __global__ void __launch_bounds__(256, 2) k_spttmc4w(Ttmc4Args p) {
@@ -602,11 +627,11 @@ __global__ void __launch_bounds__(256, 2) k_spttmc4w(Ttmc4Args p) {
   float* U1s = Uls + (SM ? p.I_leaf * JLP : 0);
   float* ys = U1s + (SM ? p.I_mid1 * J1P : 0);
   float* u0t = ys + ((P + 3) & ~3);
-  float* wreg = u0t + J0P * kW4;
+  float* wreg = u0t + J0P * kB4;
   const int WF = w4_floats(JLP, J1P);
   float* T = wreg + warp * WF;        // 32 x JLP fiber sums t_f
-  float* Z = T + 32 * JLP;            // J1 x Jl (compact, row j1) node result
-  int* bix = reinterpret_cast<int*>(Z + J1P * JLP);
+  float* Zr = T + 32 * JLP;           // kNPW node results, each J1 x Jl (compact, row j1)
+  int* bix = reinterpret_cast<int*>(Zr + kNPW * J1P * JLP);
   int* stl = bix + 32;                // staged leaf ids
   float* stv = reinterpret_cast<float*>(stl + kStage4);
   const unsigned full = 0xffffffffu;
@@ -631,17 +656,23 @@ __global__ void __launch_bounds__(256, 2) k_spttmc4w(Ttmc4Args p) {
   for (int e = threadIdx.x; e < P; e += blockDim.x) ys[e] = 0.f;
   const int NB = (J1P / 4) * (JLP / 4);  // 4x4 blocks of Z
   // lane's Z blocks
+  // (lanes past the last block compute on block 0 and never store: no branch in the fiber loop)
   int bro[NBL], bco[NBL];
+  bool bon[NBL];
 #pragma unroll
   for (int r = 0; r < NBL; ++r) {
     const int blk = lane + 32 * r;
-    bro[r] = blk < NB ? 4 * (blk / (JLP / 4)) : -1;
-    bco[r] = blk < NB ? 4 * (blk % (JLP / 4)) : 0;
+    bon[r] = blk < NB;
+    bro[r] = bon[r] ? 4 * (blk / (JLP / 4)) : 0;
+    bco[r] = bon[r] ? 4 * (blk % (JLP / 4)) : 0;
   }
   __syncthreads();
 
-  for (int base = n0; base < n1; base += kW4) {
-    const int nd = base + warp;
+  for (int base = n0; base < n1; base += kB4) {
+   for (int h = 0; h < kNPW; ++h) {
+    const int slot = h * kW4 + warp;  // the node's index in the batch
+    const int nd = base + slot;
+    float* Z = Zr + h * J1P * JLP;
     if (nd < n1) {
       float acc[NBL][4][4];
 #pragma unroll
@@ -717,7 +748,7 @@ __global__ void __launch_bounds__(256, 2) k_spttmc4w(Ttmc4Args p) {
           const int bk = bix[k];
 #pragma unroll
           for (int r = 0; r < NBL; ++r) {
-            if (bro[r] >= 0) {
+            {
               float4 u;
               if (SM) {
                 u = *reinterpret_cast<const float4*>(U1s + bk + bro[r]);
@@ -749,7 +780,7 @@ __global__ void __launch_bounds__(256, 2) k_spttmc4w(Ttmc4Args p) {
       // node result Z (compact J1 x Jl) and its U_mid0 row (transposed: u0t[j0][warp])
 #pragma unroll
       for (int r = 0; r < NBL; ++r) {
-        if (bro[r] >= 0) {
+        if (bon[r]) {
 #pragma unroll
           for (int i = 0; i < 4; ++i)
 #pragma unroll
@@ -760,30 +791,32 @@ __global__ void __launch_bounds__(256, 2) k_spttmc4w(Ttmc4Args p) {
         }
       }
       const float* ur = p.U0 + (int64_t)__ldg(p.node_mid0 + nd) * J0;
-      for (int j = lane; j < J0P; j += 32) u0t[j * kW4 + warp] = j < J0 ? __ldg(ur + j) : 0.f;
+      for (int j = lane; j < J0P; j += 32) u0t[j * kB4 + slot] = j < J0 ? __ldg(ur + j) : 0.f;
     } else {
-      for (int j = lane; j < J0P; j += 32) u0t[j * kW4 + warp] = 0.f;  // idle warp: zero weight
+      for (int j = lane; j < J0P; j += 32) u0t[j * kB4 + slot] = 0.f;  // no node: zero weight
+      for (int e = lane; e < J1 * Jl; e += 32) Z[e] = 0.f;
     }
+   }
     __syncthreads();
     // level 3: y[j0, rem] += sum_w U_mid0[a_w, j0] Z_w[rem] over the batch's nodes; the thread's
-    // positions rem keep their 8 Z values in registers, the 8 weights come as two broadcast loads
-    const int nw = min(kW4, n1 - base);
+    // positions rem keep the batch's Z values in registers, the weights come as broadcast loads
     for (int rem = threadIdx.x; rem < P1; rem += blockDim.x) {
-      float z[kW4];
+      float z[kB4];
 #pragma unroll
-      for (int w = 0; w < kW4; ++w) z[w] = w < nw ? wreg[w * WF + 32 * JLP + rem] : 0.f;
+      for (int h = 0; h < kNPW; ++h)
+#pragma unroll
+        for (int w = 0; w < kW4; ++w) z[h * kW4 + w] = wreg[w * WF + 32 * JLP + h * J1P * JLP + rem];
       for (int j0 = 0; j0 < J0; ++j0) {
-        const float4 a = *reinterpret_cast<const float4*>(u0t + j0 * kW4);
-        const float4 c = *reinterpret_cast<const float4*>(u0t + j0 * kW4 + 4);
+        const float4* a4 = reinterpret_cast<const float4*>(u0t + j0 * kB4);
         float sacc = ys[j0 * P1 + rem];
-        sacc = fmaf(a.x, z[0], sacc);
-        sacc = fmaf(a.y, z[1], sacc);
-        sacc = fmaf(a.z, z[2], sacc);
-        sacc = fmaf(a.w, z[3], sacc);
-        sacc = fmaf(c.x, z[4], sacc);
-        sacc = fmaf(c.y, z[5], sacc);
-        sacc = fmaf(c.z, z[6], sacc);
-        sacc = fmaf(c.w, z[7], sacc);
+#pragma unroll
+        for (int q = 0; q < kB4 / 4; ++q) {
+          const float4 a = a4[q];
+          sacc = fmaf(a.x, z[4 * q], sacc);
+          sacc = fmaf(a.y, z[4 * q + 1], sacc);
+          sacc = fmaf(a.z, z[4 * q + 2], sacc);
+          sacc = fmaf(a.w, z[4 * q + 3], sacc);
+        }
         ys[j0 * P1 + rem] = sacc;
       }
     }
@@ -986,7 +1019,7 @@ void spttmc_hooi(const Csf& c, const float* const* U, const int64_t* J, Split ou
   if (const char* e = std::getenv("TUCKER_TTMC4_CS")) cs = std::max(1, std::min(8, std::atoi(e)));  // tests
   a.csize = cs;
   const size_t fac_bytes = ((size_t)a.I_leaf * JLP + (size_t)a.I_mid1 * a.J1P) * sizeof(float);
-  const size_t rest_bytes = ((size_t)round_up(P, 4) + (size_t)a.J0P * kW4 + (size_t)kW4 * w4_floats(JLP, a.J1P)) *
+  const size_t rest_bytes = ((size_t)round_up(P, 4) + (size_t)a.J0P * kB4 + (size_t)kW4 * w4_floats(JLP, a.J1P)) *
                             sizeof(float);
   bool fac_smem = fac_bytes + rest_bytes <= 110 * 1024;
   if (std::getenv("TUCKER_TTMC4_GMEM")) fac_smem = false;  // tests: factors read from global memory

@@ -57,7 +57,9 @@ def test_config5_ttmc_sampled_rows(c5):
         Yo = O.ttm_chain_unfold(T, c["U0"], n)
         Y = t.debug_ttmc(n)[rows].astype(np.float64)
         for r in range(len(rows)):
-            assert O.rel_frobenius(Y[r], Yo[r]) < 1e-4, (n, rows[r])
+            e = O.rel_frobenius(Y[r], Yo[r])
+            print(f"config5 Y_({n + 1}) row {rows[r]} ({int(np.sum(c['idx'][n] == rows[r]))} nnz): rel err {e:.3e}")
+            assert e < 1e-4, (n, rows[r])
 
 
 def test_config5_hooi_sweep_properties(c5):
@@ -117,8 +119,9 @@ def test_config5_hooi_5_sweeps_vs_cached_oracle(c5, golden_dir, record_property)
     t.set_factors(c["U0"])
     fits = t.hooi_sweep(5)
     G, U, fit = t.core_and_fit()
-    np.testing.assert_allclose(fits, ref["fits"], atol=1e-5)
-    assert abs(fit - ref["fits"][-1]) < 1e-5
+    print("config5 HOOI fits GPU   ", " ".join(f"{f:.8f}" for f in fits))
+    print("config5 HOOI fits oracle", " ".join(f"{f:.8f}" for f in ref["fits"]))
+    record_property("config5_fit_diff", [float(x) for x in np.asarray(fits) - ref["fits"]])
     Uo = [ref["U_mode1"].astype(np.float64), ref["U_mode2"].astype(np.float64), ref["U_mode3"].astype(np.float64)]
     dist, bound = [], []
     for n in range(3):
@@ -131,6 +134,8 @@ def test_config5_hooi_5_sweeps_vs_cached_oracle(c5, golden_dir, record_property)
               f"rel gap {last['rel_gap']:.3e}")
     record_property("config5_projector_distance", [float(x) for x in dist])
     record_property("config5_kappa_bound", [float(x) for x in bound])
+    np.testing.assert_allclose(fits, ref["fits"], atol=1e-5)
+    assert abs(fit - ref["fits"][-1]) < 1e-5
     for n in range(3):
         assert dist[n] < bound[n], (n, dist[n], bound[n])
     # core after aligning each factor to the oracle's basis (reading A3)
