@@ -1704,7 +1704,12 @@ __global__ void k_seed_basis(double* __restrict__ basis, int64_t d, int LB, int 
 bool eig_fused(double* S, int64_t d, int J, EigSlot& slot, EigWs& ws, const EigOpts& o, double* out_V,
                double* theta_dev, int* info_dev, cudaStream_t st, const float* hint) {
   const int k = choose_block(J, d, o.oversample);
-  const int grid = num_sms();  // one CTA per SM (cooperative: all co-resident)
+  // one CTA per SM (cooperative: all co-resident); a small problem (d <= 256) runs on 32:
+  // its products are latency-bound, and fewer CTAs make every grid barrier cheaper (measured
+  // at config 4, d = 200: 63.6 ms of eigensolves per step on 148 CTAs, 56.7 ms on 32, 62.5 on 64)
+  int grid = num_sms();
+  if (d <= 256) grid = std::min(grid, 32);
+  if (const char* e = std::getenv("TUCKER_EIG_GRID")) grid = std::max(1, std::min(num_sms(), std::atoi(e)));  // experiments
   const size_t smem = eig_fused_smem(k, (int)d, grid);
   if (smem > SMEM_LIMIT) fail(TUCKER_E_ARG, "eig_fused: block too large for shared memory");
   smem_optin((const void*)k_eig_fused, smem);

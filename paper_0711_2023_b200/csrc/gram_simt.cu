@@ -31,9 +31,11 @@ __device__ __forceinline__ void dmma8(double& c0, double& c1, double a, double b
 // CTA = one 64x64 upper-triangle tile (bi <= bj) x one split (K chunks z, z +
 // splits, ...); 8 warps, warp w owns tile rows 8w..8w+7 against all 8 column
 // tiles.  Operands staged as fp64 (hi + lo) in shared memory.
+// ktile: operand in the K-tile-major layout (lda = its row count, rows >= lda read as 0)
 __global__ void __launch_bounds__(256) k_syrk_dmma(const float* __restrict__ hi, const float* __restrict__ lo,
                                                    int64_t lda, int nchunks, int ntiles, int splits,
-                                                   const int2* __restrict__ tiles, double* __restrict__ part) {
+                                                   const int2* __restrict__ tiles, double* __restrict__ part,
+                                                   int ktile) {
   __shared__ double As[DT * DSP], Bs[DT * DSP];
   const int tile = blockIdx.x % ntiles, z = blockIdx.x / ntiles;
   const int2 bij = tiles[tile];
@@ -42,10 +44,12 @@ __global__ void __launch_bounds__(256) k_syrk_dmma(const float* __restrict__ hi,
   double acc[8][2];
 #pragma unroll
   for (int j = 0; j < 8; ++j) acc[j][0] = acc[j][1] = 0.0;
-  const float* hA = hi + (int64_t)bij.x * DT * lda;
-  const float* lA = lo + (int64_t)bij.x * DT * lda;
-  const float* hB = hi + (int64_t)bij.y * DT * lda;
-  const float* lB = lo + (int64_t)bij.y * DT * lda;
+  const int64_t rstride = ktile ? DKC : lda;  // element (r, k): ktile (k / 32) 32 lda + 32 r + k % 32
+  const float* hA = hi + (int64_t)bij.x * DT * rstride;
+  const float* lA = lo + (int64_t)bij.x * DT * rstride;
+  const float* hB = hi + (int64_t)bij.y * DT * rstride;
+  const float* lB = lo + (int64_t)bij.y * DT * rstride;
+  const int64_t ra = (int64_t)bij.x * DT, rb = (int64_t)bij.y * DT;
   // the next chunk's operands are prefetched into registers while the
   // current chunk's DMMAs run (one smem buffer); diagonal tiles load A only
   const bool diag = bij.x == bij.y;
@@ -56,12 +60,23 @@ __global__ void __launch_bounds__(256) k_syrk_dmma(const float* __restrict__ hi,
 #pragma unroll
     for (int u = 0; u < PER; ++u) {
       const int e = threadIdx.x + 256 * u, r = e >> 5, kk = e & 31;
-      const int64_t o = (int64_t)r * lda + k0 + kk;
-      pah[u] = __ldg(hA + o);
-      pal[u] = __ldg(lA + o);
-      if (!diag) {
-        pbh[u] = __ldg(hB + o);
-        pbl[u] = __ldg(lB + o);
+      if (ktile) {
+        const int64_t o = (int64_t)(k0 / DKC) * DKC * lda + (int64_t)r * DKC + kk;
+        const bool va = ra + r < lda, vb = rb + r < lda;
+        pah[u] = va ? __ldg(hA + o) : 0.f;
+        pal[u] = va ? __ldg(lA + o) : 0.f;
+        if (!diag) {
+          pbh[u] = vb ? __ldg(hB + o) : 0.f;
+          pbl[u] = vb ? __ldg(lB + o) : 0.f;
+        }
+      } else {
+        const int64_t o = (int64_t)r * lda + k0 + kk;
+        pah[u] = __ldg(hA + o);
+        pal[u] = __ldg(lA + o);
+        if (!diag) {
+          pbh[u] = __ldg(hB + o);
+          pbl[u] = __ldg(lB + o);
+        }
       }
     }
   };
@@ -118,7 +133,8 @@ void gram_syrk_dmma(const Split& A, double* S, int64_t lds, GramWs& ws, cudaStre
   const int64_t d = A.rows;
   const int nb = (int)ceil_div(d, DT);
   const int ntiles = nb * (nb + 1) / 2;
-  if (A.ld % DKC != 0 || A.K() % DKC != 0) fail(TUCKER_E_ARG, "gram_syrk_dmma: ld and K must be multiples of 32");
+  if ((!A.ktile && A.ld % DKC != 0) || A.K() % DKC != 0)
+    fail(TUCKER_E_ARG, "gram_syrk_dmma: ld and K must be multiples of 32");
   const int nchunks = (int)(A.K() / DKC);
   int nsm = 148;
   {
@@ -136,7 +152,7 @@ void gram_syrk_dmma(const Split& A, double* S, int64_t lds, GramWs& ws, cudaStre
   TK_CUDA(cudaMemcpyAsync(ws.scratch.p, tiles.data(), sizeof(int2) * tiles.size(), cudaMemcpyHostToDevice, st));
   ws.partial.ensure((size_t)splits * ntiles * DT * DT);
   TK_LAUNCH(k_syrk_dmma, (unsigned)(ntiles * splits), 256, 0, st, A.hi, A.lo, A.ld, nchunks, ntiles, splits,
-            (const int2*)ws.scratch.p, ws.partial.p);
+            (const int2*)ws.scratch.p, ws.partial.p, A.ktile ? 1 : 0);
   TK_LAUNCH(k_syrk_dmma_reduce, dim3(8, (unsigned)ntiles), 256, 0, st, (const double*)ws.partial.p,
             (const int2*)ws.scratch.p, ntiles, splits, d, S, lds);
 }

@@ -57,6 +57,7 @@ struct SyrkArgs {
   int nkt;             // K-tiles in A
   int splits;          // split z takes the K-tiles z, z + splits, z + 2 splits, ...
   double* partial;     // [split][tile][128][128]
+  int ktile;           // operand in the K-tile-major layout (3D tensor map: col, row, K-tile)
 };
 
 __global__ void __launch_bounds__(NUM_THREADS, 1)
@@ -109,13 +110,23 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         const uint32_t ph = (uint32_t)((i / STAGES) & 1);
         mbar_wait(&empty_bar[s], ph ^ 1);
         uint8_t* st = smem + s * STAGE_BYTES;
-        const int kcol = (split + i * p.splits) * TKE;
+        const int kt = split + i * p.splits;
         mbar_expect_tx(&full_bar[s], diag ? 2 * OPB : 4 * OPB);
-        tma_load_2d(st, &map_hi, &full_bar[s], kcol, bij.x * TM);
-        tma_load_2d(st + OPB, &map_lo, &full_bar[s], kcol, bij.x * TM);
-        if (!diag) {
-          tma_load_2d(st + 2 * OPB, &map_hi, &full_bar[s], kcol, bij.y * TM);
-          tma_load_2d(st + 3 * OPB, &map_lo, &full_bar[s], kcol, bij.y * TM);
+        if (p.ktile) {  // rows past the operand's last row are zero-filled by TMA (out of bounds)
+          tma_load_3d(st, &map_hi, &full_bar[s], 0, bij.x * TM, kt);
+          tma_load_3d(st + OPB, &map_lo, &full_bar[s], 0, bij.x * TM, kt);
+          if (!diag) {
+            tma_load_3d(st + 2 * OPB, &map_hi, &full_bar[s], 0, bij.y * TM, kt);
+            tma_load_3d(st + 3 * OPB, &map_lo, &full_bar[s], 0, bij.y * TM, kt);
+          }
+        } else {
+          const int kcol = kt * TKE;
+          tma_load_2d(st, &map_hi, &full_bar[s], kcol, bij.x * TM);
+          tma_load_2d(st + OPB, &map_lo, &full_bar[s], kcol, bij.x * TM);
+          if (!diag) {
+            tma_load_2d(st + 2 * OPB, &map_hi, &full_bar[s], kcol, bij.y * TM);
+            tma_load_2d(st + 3 * OPB, &map_lo, &full_bar[s], kcol, bij.y * TM);
+          }
         }
       }
     }
@@ -220,6 +231,22 @@ EncodeTiledFn encode_fn() {
   return fn;
 }
 
+// K-tile-major operand: dims (32 columns, ldr rows, nkt K-tiles); boxes of 32 x 128 x 1;
+// rows >= ldr read as zero (out-of-bounds fill), so no padding rows are stored or read
+CUtensorMap make_map_ktile(const float* base, int64_t ldr, int64_t nkt) {
+  CUtensorMap m;
+  std::memset(&m, 0, sizeof(m));
+  const cuuint64_t gdim[3] = {(cuuint64_t)TKE, (cuuint64_t)ldr, (cuuint64_t)nkt};
+  const cuuint64_t gstride[2] = {(cuuint64_t)(TKE * 4), (cuuint64_t)(ldr * TKE * 4)};
+  const cuuint32_t box[3] = {(cuuint32_t)TKE, (cuuint32_t)TM, 1};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  const CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, (void*)base, gdim, gstride,
+                                 box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                 CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) fail(TUCKER_E_CUDA, "cuTensorMapEncodeTiled (3D) failed (" + std::to_string((int)r) + ")");
+  return m;
+}
+
 CUtensorMap make_map(const float* base, int64_t rows_pad, int64_t ld, int64_t kext) {
   CUtensorMap m;
   std::memset(&m, 0, sizeof(m));
@@ -241,7 +268,8 @@ void gram_syrk_tc(const Split& A, double* S, int64_t lds, GramWs& ws, cudaStream
   smem_optin((const void*)k_syrk_tc, smem_bytes);
   const int64_t d = A.rows;
   const int64_t rows_pad = round_up(d, TM);
-  if (A.ld % TKE != 0 || A.K() % TKE != 0) fail(TUCKER_E_ARG, "gram_syrk_tc: ld and K must be multiples of 32");
+  if ((!A.ktile && A.ld % TKE != 0) || A.K() % TKE != 0)
+    fail(TUCKER_E_ARG, "gram_syrk_tc: ld and K must be multiples of 32");
   const int nb = (int)(rows_pad / TM);
   const int ntiles = nb * (nb + 1) / 2;
   const int nkt = (int)(A.K() / TKE);
@@ -261,14 +289,15 @@ void gram_syrk_tc(const Split& A, double* S, int64_t lds, GramWs& ws, cudaStream
   TK_CUDA(cudaMemcpyAsync(ws.scratch.p, tiles.data(), sizeof(int2) * tiles.size(),
                           cudaMemcpyHostToDevice, st));
   ws.partial.ensure((size_t)splits * ntiles * TM * TN);
-  const CUtensorMap mhi = make_map(A.hi, rows_pad, A.ld, A.K());
-  const CUtensorMap mlo = make_map(A.lo, rows_pad, A.ld, A.K());
+  const CUtensorMap mhi = A.ktile ? make_map_ktile(A.hi, A.ld, nkt) : make_map(A.hi, rows_pad, A.ld, A.K());
+  const CUtensorMap mlo = A.ktile ? make_map_ktile(A.lo, A.ld, nkt) : make_map(A.lo, rows_pad, A.ld, A.K());
   SyrkArgs a;
   a.tiles = (const int2*)ws.scratch.p;
   a.ntiles = ntiles;
   a.nkt = nkt;
   a.splits = splits;
   a.partial = ws.partial.p;
+  a.ktile = A.ktile ? 1 : 0;
   TK_LAUNCH(k_syrk_tc, (unsigned)(ntiles * splits), NUM_THREADS, (size_t)smem_bytes, st, mhi, mlo, a);
   TK_LAUNCH(k_syrk_reduce, dim3(16, (unsigned)ntiles), 256, 0, st, (const double*)ws.partial.p,
             (const int2*)ws.scratch.p, ntiles, splits, d, S, lds);

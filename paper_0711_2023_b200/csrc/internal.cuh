@@ -73,6 +73,10 @@ struct Split {
   // Gram K extent when the view covers part of each row (a K-range shard of
   // Y^T whose pointers are offset by a multiple of 32 columns); 0 = ld
   int64_t kext = 0;
+  // K-tile-major layout (MP's W): element (r, c) at (c / 32) * 32 ld + 32 r + c % 32,
+  // ld = rows rounded up to 8, kext = columns rounded up to 32.  Each 32-column K-tile
+  // of a 128-row block is one contiguous 16 KB box for TMA.
+  bool ktile = false;
   int64_t K() const { return kext > 0 ? kext : ld; }
 };
 

@@ -853,41 +853,79 @@ struct SpmmArgs {
   int64_t s_lo, s_hi, s_all;  // slices (mid index) of this rank of s_all; W columns start at col_off for s_lo
 };
 
-// GL lanes per fiber (GL = 8/16/32 by J: several fibers per warp, so the
-// dependent fib_ptr -> leaf -> U-row chains of short fibers overlap), QL row
-// elements per lane, two nonzeros in flight.
-template <int GL, int QL>
-__global__ void __launch_bounds__(256) k_spmm_mp(SpmmArgs p) {
-  const int gl = threadIdx.x & (GL - 1);
-  const int64_t grp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / GL;
-  const int64_t ngrp = ((int64_t)gridDim.x * blockDim.x) / GL;
+// One lane per fiber (MP's leaf SpMM, Fig. 7 X_s U_m): t_f = sum_{x in f} x U[leaf(x), :]
+// in registers, 4*QV columns per pass (U rows read as 128-bit vectors when 4 | J),
+// then written split (hi, lo) into W's K-tile-major layout at row root(f), columns
+// col_off + (slice(f) - s_lo) J + j.  Fibers are consecutive per warp, so a warp's
+// leaf ids / values come from one contiguous CSF range.
+template <int QV>
+__global__ void __launch_bounds__(256, 4) k_spmm_w(SpmmArgs p) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   const bool sharded = p.s_lo > 0 || p.s_hi < p.s_all;
-  for (int64_t f = grp; f < p.nfib; f += ngrp) {
+  const bool vec = (p.J & 3) == 0;                          // 128-bit U row loads
+  const bool vst = vec && (p.col_off & 3) == 0;              // 128-bit W stores (4-aligned columns)
+  const int64_t kt_stride = 32 * p.ldW;
+  for (int64_t f = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; f < p.nfib; f += stride) {
     int64_t mk = __ldg(p.fib_mid0 + f);
     if (p.fib_mid1) mk = mk * p.I_mid1 + __ldg(p.fib_mid1 + f);
+    if (sharded && (mk < p.s_lo || mk >= p.s_hi)) continue;  // another rank's slice
     const int64_t root = __ldg(p.fib_root + f);
     const int e0 = __ldg(p.fib_ptr + f), e1 = __ldg(p.fib_ptr + f + 1);
-    if (sharded && (mk < p.s_lo || mk >= p.s_hi)) continue;  // another rank's slice
-    float t[QL];
+    const int64_t c0 = p.col_off + (mk - p.s_lo) * p.J;
+    for (int jb = 0; jb < p.J; jb += 4 * QV) {
+      float t[4 * QV];
 #pragma unroll
-    for (int q = 0; q < QL; ++q) t[q] = 0.f;
-    for (int e = e0; e < e1; e += 2) {
-      const bool two = e + 1 < e1;
-      const float x0 = __ldg(p.val + e), x1 = two ? __ldg(p.val + e + 1) : 0.f;
-      const int l0 = __ldg(p.leaf_id + e), l1 = two ? __ldg(p.leaf_id + e + 1) : l0;
-      const float* r0 = p.U + (int64_t)l0 * p.J;
-      const float* r1 = p.U + (int64_t)l1 * p.J;
+      for (int j = 0; j < 4 * QV; ++j) t[j] = 0.f;
+      // the fiber's leaf ids / values two at a time (both loads in flight before the gathers)
+      for (int e = e0; e < e1; e += 2) {
+        const bool two = e + 1 < e1;
+        const float xa = __ldg(p.val + e), xb = two ? __ldg(p.val + e + 1) : 0.f;
+        const int la = __ldg(p.leaf_id + e), lb = two ? __ldg(p.leaf_id + e + 1) : la;
+        const float* ra = p.U + (int64_t)la * p.J + jb;
+        const float* rb = p.U + (int64_t)lb * p.J + jb;
+        if (vec) {
 #pragma unroll
-      for (int q = 0; q < QL; ++q) {
-        const int j = gl + GL * q;
-        if (j < p.J) t[q] += x0 * __ldg(r0 + j) + x1 * __ldg(r1 + j);
+          for (int q = 0; q < QV; ++q) {
+            if (jb + 4 * q < p.J) {
+              const float4 g = __ldg(reinterpret_cast<const float4*>(ra) + q);
+              const float4 k = __ldg(reinterpret_cast<const float4*>(rb) + q);
+              t[4 * q] = fmaf(xb, k.x, fmaf(xa, g.x, t[4 * q]));
+              t[4 * q + 1] = fmaf(xb, k.y, fmaf(xa, g.y, t[4 * q + 1]));
+              t[4 * q + 2] = fmaf(xb, k.z, fmaf(xa, g.z, t[4 * q + 2]));
+              t[4 * q + 3] = fmaf(xb, k.w, fmaf(xa, g.w, t[4 * q + 3]));
+            }
+          }
+        } else {
+#pragma unroll
+          for (int j = 0; j < 4 * QV; ++j)
+            if (jb + j < p.J) t[j] = fmaf(xb, __ldg(rb + j), fmaf(xa, __ldg(ra + j), t[j]));
+        }
       }
-    }
-    const int64_t base = root * p.ldW + p.col_off + (mk - p.s_lo) * p.J;
+      if (vst) {  // 4 | J and 4 | col_off: every 4-column group is aligned and inside one K-tile
 #pragma unroll
-    for (int q = 0; q < QL; ++q) {
-      const int j = gl + GL * q;
-      if (j < p.J) split_store(p.Whi, p.Wlo, base + j, t[q]);
+        for (int q = 0; q < QV; ++q) {
+          if (jb + 4 * q < p.J) {
+            const int64_t c = c0 + jb + 4 * q;
+            const int64_t off = (c >> 5) * kt_stride + root * 32 + (c & 31);
+            float h[4], l[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              h[u] = tf32_rna(t[4 * q + u]);
+              l[u] = tf32_rna(t[4 * q + u] - h[u]);
+            }
+            *reinterpret_cast<float4*>(p.Whi + off) = make_float4(h[0], h[1], h[2], h[3]);
+            *reinterpret_cast<float4*>(p.Wlo + off) = make_float4(l[0], l[1], l[2], l[3]);
+          }
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < 4 * QV; ++j) {
+          if (jb + j < p.J) {
+            const int64_t c = c0 + jb + j;
+            split_store(p.Whi, p.Wlo, (c >> 5) * kt_stride + root * 32 + (c & 31), t[j]);
+          }
+        }
+      }
     }
   }
 }
@@ -1210,11 +1248,12 @@ void spmm_mp(const Csf& c, const float* U_leaf, int64_t J_leaf, Split out, int64
   a.Wlo = out.lo;
   a.ldW = out.ld;
   a.col_off = col_off;
-  const int64_t blocks = std::min<int64_t>(ceil_div(c.nfib, 8), 148 * 32);
-  if (J_leaf <= 8) TK_LAUNCH((k_spmm_mp<8, 1>), (unsigned)blocks, 256, 0, st, a);
-  else if (J_leaf <= 32) TK_LAUNCH((k_spmm_mp<16, 2>), (unsigned)blocks, 256, 0, st, a);
-  else if (J_leaf <= 64) TK_LAUNCH((k_spmm_mp<16, 4>), (unsigned)blocks, 256, 0, st, a);
-  else TK_LAUNCH((k_spmm_mp<32, 4>), (unsigned)blocks, 256, 0, st, a);
+  if (!out.ktile) fail(TUCKER_E_ARG, "spmm_mp: W must be in the K-tile-major layout");
+  const unsigned blocks = (unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(c.nfib, 256), 148 * 16));
+  if (J_leaf <= 8) TK_LAUNCH((k_spmm_w<2>), blocks, 256, 0, st, a);
+  else if (J_leaf <= 16) TK_LAUNCH((k_spmm_w<4>), blocks, 256, 0, st, a);
+  else if (J_leaf <= 24) TK_LAUNCH((k_spmm_w<6>), blocks, 256, 0, st, a);
+  else TK_LAUNCH((k_spmm_w<8>), blocks, 256, 0, st, a);
 }
 
 }  // namespace tk

@@ -232,8 +232,9 @@ Split build_mp_w(tucker_handle* h, int n, int only_m = -1) {
     K += h->J[m] * (hi - lo);
   }
   const int64_t rows = h->dims[n];
-  const int64_t rows_pad = round_up(rows, 128), ld = round_up(K, 32);
-  const size_t need = (size_t)(rows_pad * ld);
+  // K-tile-major layout (Split::ktile): 32-column tiles of all rows, rows padded to 8
+  const int64_t ldr = round_up(rows, 8), kpad = round_up(K, 32);
+  const size_t need = (size_t)(ldr * kpad);
   auto& wk = h->wkeep[n][only_m + 1];
   const bool reuse = wk.need == need && wk.hi.p;
   if (!reuse && need > h->Whi.n) {
@@ -280,7 +281,9 @@ Split build_mp_w(tucker_handle* h, int n, int only_m = -1) {
   W.lo = wlo;
   W.rows = rows;
   W.cols = K;
-  W.ld = ld;
+  W.ld = ldr;
+  W.kext = kpad;
+  W.ktile = true;
   int64_t off = 0;
   for (int m = 0; m < h->order; ++m) {
     if (m == n || (only_m >= 0 && m != only_m)) continue;
