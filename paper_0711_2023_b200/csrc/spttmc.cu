@@ -851,6 +851,7 @@ struct SpmmArgs {
   float *Whi, *Wlo;
   int64_t ldW, col_off;
   int64_t s_lo, s_hi, s_all;  // slices (mid index) of this rank of s_all; W columns start at col_off for s_lo
+  int I_leaf;                  // rows of U (k_spmm_w's shared-memory table)
 };
 
 // One lane per fiber (MP's leaf SpMM, Fig. 7 X_s U_m): t_f = sum_{x in f} x U[leaf(x), :]
@@ -858,37 +859,102 @@ struct SpmmArgs {
 // then written split (hi, lo) into W's K-tile-major layout at row root(f), columns
 // col_off + (slice(f) - s_lo) J + j.  Fibers are consecutive per warp, so a warp's
 // leaf ids / values come from one contiguous CSF range.
-template <int QV>
-__global__ void __launch_bounds__(256, 4) k_spmm_w(SpmmArgs p) {
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+constexpr int kSpW = 4;  // warps per k_spmm_w block
+// SM: the factor table U (I_leaf x J) is staged in shared memory (dynamic; when it
+// fits) -- the per-nonzero row gathers then come from shared memory instead of L1
+constexpr int kSpNz = 128;  // staged nonzeros per warp batch (longer batches read global memory)
+template <int QV, bool SM>
+__global__ void __launch_bounds__(32 * kSpW, 6) k_spmm_w(SpmmArgs p) {
+  extern __shared__ __align__(16) float Us[];
+  // per warp: 32 fibers x 4 QV split values of one column pass, then written out with
+  // the warp's lanes over consecutive float4 slots: consecutive fibers of a CSF
+  // ordering are consecutive slices of one row, i.e. consecutive W columns, so each
+  // store instruction fills whole 128-byte K-tile row segments.  The batch's
+  // nonzeros (leaf ids, values) are staged with coalesced loads, and the next
+  // batch's fiber metadata is loaded while this batch computes.
+  __shared__ __align__(16) float st4[kSpW][32 * 4 * QV];
+  __shared__ int64_t srow[kSpW][32], scol[kSpW][32];
+  __shared__ int snz_l[kSpW][kSpNz];
+  __shared__ float snz_v[kSpW][kSpNz];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const unsigned full = 0xffffffffu;
   const bool sharded = p.s_lo > 0 || p.s_hi < p.s_all;
   const bool vec = (p.J & 3) == 0;                          // 128-bit U row loads
   const bool vst = vec && (p.col_off & 3) == 0;              // 128-bit W stores (4-aligned columns)
   const int64_t kt_stride = 32 * p.ldW;
-  for (int64_t f = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; f < p.nfib; f += stride) {
-    int64_t mk = __ldg(p.fib_mid0 + f);
-    if (p.fib_mid1) mk = mk * p.I_mid1 + __ldg(p.fib_mid1 + f);
-    if (sharded && (mk < p.s_lo || mk >= p.s_hi)) continue;  // another rank's slice
-    const int64_t root = __ldg(p.fib_root + f);
-    const int e0 = __ldg(p.fib_ptr + f), e1 = __ldg(p.fib_ptr + f + 1);
-    const int64_t c0 = p.col_off + (mk - p.s_lo) * p.J;
+  const int64_t nwarps = (int64_t)gridDim.x * kSpW;
+  const float* Ub = p.U;
+  if (SM) {
+    const int n = p.I_leaf * p.J;
+    for (int e = threadIdx.x; e < n; e += blockDim.x) Us[e] = __ldg(p.U + e);
+    __syncthreads();
+    Ub = Us;
+  }
+  struct Meta {
+    int64_t mk, root;
+    int e0, e1;
+  };
+  auto load_meta = [&](int64_t base) {
+    Meta m{0, 0, 0, 0};
+    const int64_t f = base + lane;
+    if (f < p.nfib) {
+      m.mk = __ldg(p.fib_mid0 + f);
+      if (p.fib_mid1) m.mk = m.mk * p.I_mid1 + __ldg(p.fib_mid1 + f);
+      m.root = __ldg(p.fib_root + f);
+      m.e0 = __ldg(p.fib_ptr + f);
+      m.e1 = __ldg(p.fib_ptr + f + 1);
+    } else {
+      m.e0 = m.e1 = -1;
+    }
+    return m;
+  };
+  int64_t base = (blockIdx.x * kSpW + warp) * 32LL;
+  Meta nx = load_meta(base);
+  for (; base < p.nfib; base += nwarps * 32) {
+    const Meta cm = nx;
+    nx = load_meta(base + nwarps * 32);  // in flight during this batch
+    bool ok = cm.e0 >= 0 && !(sharded && (cm.mk < p.s_lo || cm.mk >= p.s_hi));
+    // the batch's nonzeros [E0, E1) (contiguous in the CSF) staged with coalesced loads
+    const int last = __popc(__ballot_sync(full, cm.e0 >= 0)) - 1;
+    const int E0 = __shfl_sync(full, cm.e0, 0), E1 = __shfl_sync(full, cm.e1, last);
+    const bool staged = E1 - E0 <= kSpNz;
+    if (staged)
+      for (int e = E0 + lane; e < E1; e += 32) {
+        snz_l[warp][e - E0] = __ldg(p.leaf_id + e);
+        snz_v[warp][e - E0] = __ldg(p.val + e);
+      }
+    const int e0 = ok ? cm.e0 : 0, e1 = ok ? cm.e1 : 0;
+    const int64_t c0 = p.col_off + (cm.mk - p.s_lo) * p.J;
+    srow[warp][lane] = ok ? cm.root : -1;
+    scol[warp][lane] = c0;
+    __syncwarp();
     for (int jb = 0; jb < p.J; jb += 4 * QV) {
       float t[4 * QV];
 #pragma unroll
       for (int j = 0; j < 4 * QV; ++j) t[j] = 0.f;
-      // the fiber's leaf ids / values two at a time (both loads in flight before the gathers)
       for (int e = e0; e < e1; e += 2) {
         const bool two = e + 1 < e1;
-        const float xa = __ldg(p.val + e), xb = two ? __ldg(p.val + e + 1) : 0.f;
-        const int la = __ldg(p.leaf_id + e), lb = two ? __ldg(p.leaf_id + e + 1) : la;
-        const float* ra = p.U + (int64_t)la * p.J + jb;
-        const float* rb = p.U + (int64_t)lb * p.J + jb;
+        float xa, xb;
+        int la, lb;
+        if (staged) {
+          xa = snz_v[warp][e - E0];
+          la = snz_l[warp][e - E0];
+          xb = two ? snz_v[warp][e + 1 - E0] : 0.f;
+          lb = two ? snz_l[warp][e + 1 - E0] : la;
+        } else {
+          xa = __ldg(p.val + e);
+          la = __ldg(p.leaf_id + e);
+          xb = two ? __ldg(p.val + e + 1) : 0.f;
+          lb = two ? __ldg(p.leaf_id + e + 1) : la;
+        }
+        const float* ra = Ub + (int64_t)la * p.J + jb;
+        const float* rb = Ub + (int64_t)lb * p.J + jb;
         if (vec) {
 #pragma unroll
           for (int q = 0; q < QV; ++q) {
             if (jb + 4 * q < p.J) {
-              const float4 g = __ldg(reinterpret_cast<const float4*>(ra) + q);
-              const float4 k = __ldg(reinterpret_cast<const float4*>(rb) + q);
+              const float4 g = SM ? reinterpret_cast<const float4*>(ra)[q] : __ldg(reinterpret_cast<const float4*>(ra) + q);
+              const float4 k = SM ? reinterpret_cast<const float4*>(rb)[q] : __ldg(reinterpret_cast<const float4*>(rb) + q);
               t[4 * q] = fmaf(xb, k.x, fmaf(xa, g.x, t[4 * q]));
               t[4 * q + 1] = fmaf(xb, k.y, fmaf(xa, g.y, t[4 * q + 1]));
               t[4 * q + 2] = fmaf(xb, k.z, fmaf(xa, g.z, t[4 * q + 2]));
@@ -898,35 +964,45 @@ __global__ void __launch_bounds__(256, 4) k_spmm_w(SpmmArgs p) {
         } else {
 #pragma unroll
           for (int j = 0; j < 4 * QV; ++j)
-            if (jb + j < p.J) t[j] = fmaf(xb, __ldg(rb + j), fmaf(xa, __ldg(ra + j), t[j]));
+            if (jb + j < p.J) t[j] = fmaf(xb, rb[j], fmaf(xa, ra[j], t[j]));
         }
       }
-      if (vst) {  // 4 | J and 4 | col_off: every 4-column group is aligned and inside one K-tile
+      if (vst) {
+        float4* t4 = reinterpret_cast<float4*>(st4[warp] + lane * 4 * QV);
 #pragma unroll
-        for (int q = 0; q < QV; ++q) {
-          if (jb + 4 * q < p.J) {
-            const int64_t c = c0 + jb + 4 * q;
-            const int64_t off = (c >> 5) * kt_stride + root * 32 + (c & 31);
+        for (int q = 0; q < QV; ++q) t4[q] = make_float4(t[4 * q], t[4 * q + 1], t[4 * q + 2], t[4 * q + 3]);
+        __syncwarp();
+#pragma unroll
+        for (int u = 0; u < QV; ++u) {
+          const int slot = lane + 32 * u, k = slot / QV, q = slot - k * QV;
+          const int64_t r = srow[warp][k];
+          if (r >= 0 && jb + 4 * q < p.J) {
+            const int64_t c = scol[warp][k] + jb + 4 * q;
+            const int64_t off = (c >> 5) * kt_stride + r * 32 + (c & 31);
+            const float4 v = reinterpret_cast<const float4*>(st4[warp])[slot];
+            const float vv[4] = {v.x, v.y, v.z, v.w};
             float h[4], l[4];
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
-              h[u] = tf32_rna(t[4 * q + u]);
-              l[u] = tf32_rna(t[4 * q + u] - h[u]);
+            for (int w = 0; w < 4; ++w) {
+              h[w] = tf32_rna(vv[w]);
+              l[w] = tf32_rna(vv[w] - h[w]);
             }
             *reinterpret_cast<float4*>(p.Whi + off) = make_float4(h[0], h[1], h[2], h[3]);
             *reinterpret_cast<float4*>(p.Wlo + off) = make_float4(l[0], l[1], l[2], l[3]);
           }
         }
-      } else {
+        __syncwarp();
+      } else if (ok) {
 #pragma unroll
         for (int j = 0; j < 4 * QV; ++j) {
           if (jb + j < p.J) {
             const int64_t c = c0 + jb + j;
-            split_store(p.Whi, p.Wlo, (c >> 5) * kt_stride + root * 32 + (c & 31), t[j]);
+            split_store(p.Whi, p.Wlo, (c >> 5) * kt_stride + cm.root * 32 + (c & 31), t[j]);
           }
         }
       }
     }
+    __syncwarp();
   }
 }
 
@@ -1249,11 +1325,30 @@ void spmm_mp(const Csf& c, const float* U_leaf, int64_t J_leaf, Split out, int64
   a.ldW = out.ld;
   a.col_off = col_off;
   if (!out.ktile) fail(TUCKER_E_ARG, "spmm_mp: W must be in the K-tile-major layout");
-  const unsigned blocks = (unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(c.nfib, 256), 148 * 16));
-  if (J_leaf <= 8) TK_LAUNCH((k_spmm_w<2>), blocks, 256, 0, st, a);
-  else if (J_leaf <= 16) TK_LAUNCH((k_spmm_w<4>), blocks, 256, 0, st, a);
-  else if (J_leaf <= 24) TK_LAUNCH((k_spmm_w<6>), blocks, 256, 0, st, a);
-  else TK_LAUNCH((k_spmm_w<8>), blocks, 256, 0, st, a);
+  a.I_leaf = (int)c.I_leaf;
+  const size_t tab = (size_t)c.I_leaf * J_leaf * sizeof(float);
+  const bool sm = tab <= 48 * 1024;
+  int nsm = 148, dev = 0;
+  TK_CUDA(cudaGetDevice(&dev));
+  TK_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+  // persistent-ish grid (each block stages the table once), 6 blocks per SM
+  const unsigned blocks = (unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(c.nfib, 32 * kSpW), 6 * nsm));
+  const size_t smem = sm ? tab : 0;
+  auto go = [&](const void* fn) {
+    if (smem) smem_optin(fn, smem);
+    void* args[] = {&a};
+    TK_CUDA(cudaLaunchKernel(fn, dim3(blocks), dim3(32 * kSpW), args, smem, st));
+    if (g_launch_counter) ++(*g_launch_counter);
+    if (sync_check_enabled()) TK_CUDA(cudaStreamSynchronize(st));
+  };
+#define TK_SPW(qv)                                         \
+  if (sm) go((const void*)k_spmm_w<qv, true>);             \
+  else go((const void*)k_spmm_w<qv, false>);
+  if (J_leaf <= 8) { TK_SPW(2) }
+  else if (J_leaf <= 16) { TK_SPW(4) }
+  else if (J_leaf <= 24) { TK_SPW(6) }
+  else { TK_SPW(8) }
+#undef TK_SPW
 }
 
 }  // namespace tk
