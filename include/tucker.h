@@ -164,6 +164,12 @@ int tucker_debug_ttmc(tucker_handle* h, int mode, float* Y_out);
  * orientation), algo 1 = MP (M_n, I_n x I_n).  Row-major fp64. */
 int tucker_debug_gram(tucker_handle* h, int algo, int mode, double* S_out);
 
+/* Rows `rows[0..nrows)` (0-based) of the same Gram (algo 0 HOOI, 1 MP), fp64, into
+ * out (host, nrows x I_mode row-major): the Gram is formed on the device and only the
+ * requested rows are copied back -- for Grams too large to return (MP at config 5:
+ * 50000 x 50000).  E_ARG on bad arguments or rows out of range. */
+int tucker_debug_gram_rows(tucker_handle* h, int algo, int mode, int nrows, const int64_t* rows, double* out);
+
 /* Leading-J eigenvectors (descending, sign-canonical, fp32 row-major d x J) and
  * eigenvalues (fp64[J]) of a caller-provided symmetric fp64 d x d matrix, with
  * the library's eigensolver.  1 <= J <= min(d, 112). */

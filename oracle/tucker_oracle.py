@@ -374,6 +374,39 @@ def mp_gram_slices(T: SparseTensor, U, n: int) -> np.ndarray:
     return M
 
 
+def mp_gram_rows(T: SparseTensor, U, n: int, rows) -> np.ndarray:
+    """Rows `rows` of M_n (Fig. 7/8, Appendix) without forming M_n or W:
+    M_n[i, :] = sum_{m != n} sum_{slices s} P_s[i, :] P_s^T with P_s = X_s U_m, over the
+    slices s whose X_s has a nonzero in row i (the others contribute nothing).  For
+    tensors whose M_n (d x d) or W does not fit (BASELINE config 5: d = 50000).
+    Order 3."""
+    if T.N != 3:
+        raise ValueError("mp_gram_rows: order 3 only")
+    rows = np.asarray(rows, dtype=np.int64)
+    out = np.zeros((rows.size, T.dims[n]))
+    for m in range(3):
+        if m == n:
+            continue
+        o = 3 - n - m
+        Um = np.asarray(U[m], dtype=np.float64)
+        for k, i in enumerate(rows):
+            slices = np.unique(T.idx[o][T.idx[n] == i])  # slices with a nonzero in row i
+            sel = np.isin(T.idx[o], slices)
+            so, sn, sm = T.idx[o][sel], T.idx[n][sel], T.idx[m][sel]
+            # P_s for all those slices at once: rows (s, i'), a sparse x dense product (Eq. 1)
+            key = so * T.dims[n] + sn
+            uk, inv = np.unique(key, return_inverse=True)
+            Xs = sp.csr_matrix((T.vals[sel], (inv, sm)), shape=(uk.size, T.dims[m]))
+            P = Xs @ Um                                   # rows: fibers (s, i')
+            ks, ki = uk // T.dims[n], uk % T.dims[n]
+            mine = ki == i                                # the row i of each slice
+            Pi = np.zeros((T.dims[o], Um.shape[1]))
+            Pi[ks[mine]] = P[mine]
+            # M[i, i'] += <P_s[i], P_s[i']> for every fiber (s, i')
+            np.add.at(out[k], ki, np.einsum("fj,fj->f", P, Pi[ks]))
+    return out
+
+
 def mp_sweep(T: SparseTensor, U, core, diag=None):
     """One pass of Fig. 7/8's main loop: for n = 1..N, M_n as above with the
     freshest factors (Appendix: M2 uses the new A), then A(n) <- J_n leading

@@ -30,7 +30,7 @@ EXPORTS = [
     "tucker_debug_product", "tucker_debug_product_time", "tucker_csf_stats", "tucker_stats",
     "tucker_nccl_unique_id", "tucker_shard_bounds", "tucker_shard_info", "hooi_run", "mp_run",
     "tucker_hosvd", "sp_sweep", "sp_run", "tucker_set_factor", "tucker_set_allreduce",
-    "tucker_time_ttmc", "tucker_csf_layout",
+    "tucker_time_ttmc", "tucker_csf_layout", "tucker_debug_gram_rows",
 ]
 
 
@@ -70,6 +70,7 @@ def load(path: str = LIB_PATH) -> C.CDLL:
     lib.tucker_debug_product_time.argtypes = [C.c_int, C.c_int, C.c_int, C.POINTER(C.c_double)]
     lib.tucker_csf_stats.argtypes = [P, i64p]
     lib.tucker_csf_layout.argtypes = [P, i64p]
+    lib.tucker_debug_gram_rows.argtypes = [P, C.c_int, C.c_int, C.c_int, i64p, P]
     lib.tucker_time_ttmc.argtypes = [P, C.c_int, C.c_int, C.POINTER(C.c_float)]
     lib.tucker_nccl_unique_id.argtypes = [P]
     lib.tucker_hosvd.argtypes = [P, C.c_uint]
@@ -293,6 +294,15 @@ def tucker_debug_gram(h, algo, mode, I):
     S = np.zeros((I, I), dtype=np.float64)
     _check(lib().tucker_debug_gram(h, algo, mode, C.c_void_p(S.ctypes.data)), h)
     return S
+
+
+def tucker_debug_gram_rows(h, algo, mode, rows, I):
+    """Rows of the fp64 Gram (algo 0 HOOI, 1 MP) the next update of `mode` would use."""
+    rows = np.ascontiguousarray(rows, dtype=np.int64)
+    out = np.zeros((rows.size, I), dtype=np.float64)
+    _check(lib().tucker_debug_gram_rows(h, algo, mode, int(rows.size), rows.ctypes.data_as(C.POINTER(C.c_int64)),
+                                        C.c_void_p(out.ctypes.data)), h)
+    return out
 
 
 def tucker_debug_eig(h, S, J):
@@ -529,6 +539,9 @@ class Tucker:
 
     def debug_gram(self, algo, mode):
         return tucker_debug_gram(self.h, algo, mode, self.dims[mode])
+
+    def debug_gram_rows(self, algo, mode, rows):
+        return tucker_debug_gram_rows(self.h, algo, mode, rows, self.dims[mode])
 
     def debug_eig(self, S, J):
         return tucker_debug_eig(self.h, S, J)

@@ -228,7 +228,9 @@ struct MvPlan {
 };
 __host__ __device__ inline MvPlan mv_plan(int d, int G) {
   const int LS = (d + 63) / 64 * 64;
-  MvPlan best{1, (d + 7) / 8, 1, LS};
+  // d > 64 G (e.g. MP's d = 50000 at config 5): 64-row blocks over the full K range,
+  // more blocks than CTAs -- every CTA loops over its blocks (matvec)
+  MvPlan best{8, (d + 63) / 64, 1, LS};
   long long bc = -1;
   for (int m8 = 8; m8 >= 1; --m8) {
     const int MT = 8 * m8;
@@ -373,8 +375,8 @@ __device__ void matvec(const Ctx& x, double* mpart, const double* S, const doubl
   const int LS = x.ls, LB = x.lb;
   const int n8 = (n + 7) >> 3;
   const int RPX = (x.d + 8 * pl.m8 - 1) / (8 * pl.m8) * (8 * pl.m8);  // rows covered by the plan
-  if (x.cta < pl.RB * pl.KB) {
-    const int rb = x.cta / pl.KB, kb = x.cta - rb * pl.KB;
+  for (int t = x.cta; t < pl.RB * pl.KB; t += x.G) {  // one pass unless the plan has more blocks than CTAs
+    const int rb = t / pl.KB, kb = t - rb * pl.KB;
     PhaseA a;
     a.S = S;
     a.Y = Y;

@@ -153,6 +153,8 @@ struct EigWs {
   DBuf<long long> fprof;        // eig_fused per-phase ns (accumulated over solves)
   bool fprof_init = false;
   DBuf<double> cq, ct, H, R;    // cholqr2 (Y^T Y route)
+  DBuf<double> bL, bQ, bSQ, bY0, bY1, bT, sH, sV, sC, sTh, sRes;  // eig_large work blocks
+  DBuf<int> sInfo;
   DenseWs dense;
   int64_t stat_outer = 0, stat_matvec = 0, stat_sweeps = 0;
 };
@@ -173,6 +175,19 @@ void eig_layout(int64_t d, int64_t* ls, int64_t* rows);
 bool eig_fused(double* S, int64_t d, int J, EigSlot& slot, EigWs& ws, const EigOpts& o, double* out_V,
                double* theta_dev, int* info_dev, cudaStream_t st, const float* hint = nullptr);
 size_t eig_fused_smem(int k, int d, int G);
+// d > kFusedMaxD (the persistent solver keeps each CTA's rows of the block in shared
+// memory): the same method as a host-driven kernel sequence (eig_large.cu); S row
+// stride ls, same outputs and info record as eig_fused.  Synchronises the stream.
+constexpr int64_t kFusedMaxD = 8192;
+bool eig_large(const double* S, int64_t d, int64_t ls, int J, EigSlot& slot, EigWs& ws, const EigOpts& o,
+               double* out_V, double* theta_dev, int* info_dev, cudaStream_t st, const float* hint = nullptr);
+// MP's multislice Gram without the dense W (mp_sparse.cu): M (fp64, upper triangle, row
+// stride ls) += sum over the slices [s_lo, s_hi) of the order-3 CSF c (root = the slice
+// mode o, mid = n, leaf = m) of P_s P_s^T, P_s = X_s U_m; P rows are staged in Pbuf
+// (at most max_p_floats floats per batch of slices).  mp_sparse_mirror fills the lower triangle.
+void mp_sparse_term(const Csf& c, const float* U_leaf, int64_t J, int64_t s_lo, int64_t s_hi, double* M, int64_t ls,
+                    DBuf<float>& Pbuf, size_t max_p_floats, cudaStream_t st);
+void mp_sparse_mirror(double* M, int64_t d, int64_t ls, cudaStream_t st);
 // unit test of the fused solver's k x k routines (one CTA); see tucker_debug_smalldense
 void eig_unit_mv(const double* S, const double* Y, int d, int n, double alpha, double* Out, double gamma,
                  const double* D, cudaStream_t st);

@@ -45,6 +45,7 @@ struct tucker_handle {
   int Y_mode = -1;
   bool Y_transposed = false;
   DBuf<double> S, V, Ufull, G64, scal;
+  DBuf<float> Pmp;  // MP sparse multislice Gram: P rows of a batch of slices
   DBuf<float> G32, Ytmp;
   bool G_valid = false;
   EigSlot slots[3][kMaxOrder];  // warm starts: [0] HOOI, [1] MP, [2] SP
@@ -306,6 +307,13 @@ void solve_eig(tucker_handle* h, int64_t d, int J, EigSlot& slot, const float* h
   h->theta_d.ensure((size_t)J);
   h->info_d.ensure(16 * (kMaxOrder + 1));  // per record: 8 ints + 4 doubles
   h->rec_slot[rec] = &slot;
+  static const bool force_large = std::getenv("TUCKER_EIG_LARGE") != nullptr;  // tests
+  if (d > kFusedMaxD || force_large) {  // MP's M_n at config 5 (d = 50000): the host-driven variant
+    int64_t ls = 0, rows = 0;
+    eig_layout(d, &ls, &rows);
+    eig_large(h->S.p, d, ls, J, slot, h->eig, eig_opts(h), h->V.p, h->theta_d.p, h->info_d.p + 16 * rec, h->st, hint);
+    return;
+  }
   eig_fused(h->S.p, d, J, slot, h->eig, eig_opts(h), h->V.p, h->theta_d.p, h->info_d.p + 16 * rec, h->st, hint);
 }
 
@@ -360,6 +368,50 @@ struct SweepEvents {
   }
 };
 
+void factor_from_S(tucker_handle* h, int n, const Split& A, bool transposed, EigSlot& slot, bool partial_gram);
+
+// MP's multislice Gram without the dense W (order 3, tensors whose W_n would not fit):
+// h->S = sum over the terms m != n (only_m >= 0: that term) of sum_s P_s P_s^T, built
+// slice by slice from the orderings (root o, mid n, leaf m) (mp_sparse.cu); sharded:
+// this rank's slices, summed by an fp64 allreduce.  Returns the d x 0 Split view the
+// factor step needs (rows = I_n).
+bool mp_use_sparse(tucker_handle* h, int n, int only_m) {
+  if (h->order != 3) return false;
+  if (const char* e = std::getenv("TUCKER_MP_SPARSE")) return std::atoi(e) != 0;  // tests / experiments
+  int64_t K = 0;
+  for (int m = 0; m < h->order; ++m) {
+    if (m == n || (only_m >= 0 && m != only_m)) continue;
+    const Csf& c = *h->csfs[h->mp_csf[n][m]];
+    K += h->J[m] * c.I_mid0;
+  }
+  size_t free_b = 0, total_b = 0;
+  TK_CUDA(cudaMemGetInfo(&free_b, &total_b));
+  const double wbytes = 8.0 * (double)round_up(h->dims[n], 8) * (double)round_up(K, 32);
+  return wbytes > 0.4 * (double)free_b;
+}
+
+Split build_mp_gram_sparse(tucker_handle* h, int n, int only_m) {
+  const int64_t d = h->dims[n];
+  const int64_t lds = ensure_S(h, d);
+  int64_t ls = 0, rows = 0;
+  eig_layout(d, &ls, &rows);
+  TK_CUDA(cudaMemsetAsync(h->S.p, 0, (size_t)(rows * ls) * sizeof(double), h->st));
+  size_t free_b = 0, total_b = 0;
+  TK_CUDA(cudaMemGetInfo(&free_b, &total_b));
+  const size_t max_p = std::max<size_t>((size_t)1 << 24, std::min<size_t>(free_b / 3, (size_t)16 << 30) / sizeof(float));
+  for (int m = 0; m < h->order; ++m) {
+    if (m == n || (only_m >= 0 && m != only_m)) continue;
+    const int o = 3 - n - m;
+    const Csf& c = *h->csfs[h->mp_csf[o][m]];  // root o (the slice), mid n, leaf m
+    const int64_t lo = h->sharded ? h->mp_lo[n][m] : 0, hi = h->sharded ? h->mp_hi[n][m] : c.I_root;
+    mp_sparse_term(c, h->U[m].p, h->J[m], lo, hi, h->S.p, lds, h->Pmp, max_p, h->st);
+  }
+  mp_sparse_mirror(h->S.p, d, lds, h->st);
+  Split A;
+  A.rows = d;
+  return A;
+}
+
 // U_n from the eigenvectors of the Gram of the split matrix A (= Y, Y^T or W)
 // Sharded: a partial Gram (MP: this rank's W columns; HOOI Y^T Y route: this
 // rank's K range of Y^T, rounded out to 32 columns -- the other ranks' columns
@@ -385,6 +437,13 @@ void update_factor(tucker_handle* h, int n, const Split& A, bool transposed, Eig
   }
   if (partial_gram) dist_allreduce_f64(h->comm, h->S.p, d * lds, h->st);
   if (ev_gram) TK_CUDA(cudaEventRecord(ev_gram, h->st));
+  factor_from_S(h, n, A, transposed, slot, partial_gram);
+}
+
+// U_n from the Gram already in h->S (I_n x I_n, or prod J x prod J on the Y^T Y route)
+void factor_from_S(tucker_handle* h, int n, const Split& A, bool transposed, EigSlot& slot, bool partial_gram) {
+  const int64_t d = A.rows;
+  const int J = (int)h->J[n];
   solve_eig(h, d, J, slot, transposed ? nullptr : h->U[n].p, n);
   if (!transposed) {
     canon_to_f32(h->V.p, J, d, J, h->U[n].p, h->st);
@@ -403,6 +462,27 @@ void update_factor(tucker_handle* h, int n, const Split& A, bool transposed, Eig
     cholqr2(h->Ufull.p, J, I, J, h->eig, h->st);
     canon_to_f32(h->Ufull.p, J, I, J, h->U[n].p, h->st);
   }
+}
+
+// One MP / SP factor update of mode n (only_m >= 0: the single term of Slice
+// Projection): the dense-W route (SpMM + Gram) or, when W_n would not fit, the sparse
+// multislice Gram; ev_proj / ev_gram are recorded after the W build / the Gram.
+void mp_update(tucker_handle* h, int n, int only_m, EigSlot& slot, cudaEvent_t ev_proj, cudaEvent_t ev_gram) {
+  if (mp_use_sparse(h, n, only_m)) {
+    TK_CUDA(cudaEventRecord(ev_proj, h->st));
+    Split A = build_mp_gram_sparse(h, n, only_m);
+    if (h->sharded) {
+      int64_t ls = 0, rows = 0;
+      eig_layout(A.rows, &ls, &rows);
+      dist_allreduce_f64(h->comm, h->S.p, A.rows * ls, h->st);
+    }
+    TK_CUDA(cudaEventRecord(ev_gram, h->st));
+    factor_from_S(h, n, A, false, slot, h->sharded);
+    return;
+  }
+  Split W = only_m >= 0 ? build_mp_w(h, n, only_m) : build_mp_w(h, n);
+  TK_CUDA(cudaEventRecord(ev_proj, h->st));
+  update_factor(h, n, W, false, slot, ev_gram, h->sharded);
 }
 
 // G_(N) = U_N^T Y_(N) from h->Y (must be the projection of the last mode with
@@ -780,9 +860,7 @@ int mp_sweep(tucker_handle* h, int sweeps, double* fit_per_sweep, float* stage_m
     for (int s = 0; s < sweeps; ++s) {
       for (int n = 0; n < N; ++n) {
         TK_CUDA(cudaEventRecord(ev.e[4 * n], h->st));
-        Split W = build_mp_w(h, n);
-        TK_CUDA(cudaEventRecord(ev.e[4 * n + 1], h->st));
-        update_factor(h, n, W, false, h->slots[1][n], ev.e[4 * n + 2], h->sharded);
+        mp_update(h, n, -1, h->slots[1][n], ev.e[4 * n + 1], ev.e[4 * n + 2]);
         TK_CUDA(cudaEventRecord(ev.e[4 * n + 3], h->st));
       }
       h->G_valid = false;
@@ -826,9 +904,7 @@ int sp_sweep(tucker_handle* h, int sweeps, double* fits, double* gnorms, float* 
     for (int s = 0; s < sweeps; ++s) {
       for (int n = 0; n < N; ++n) {
         TK_CUDA(cudaEventRecord(ev.e[4 * n], h->st));
-        Split W = build_mp_w(h, n, (n + N - 1) % N);
-        TK_CUDA(cudaEventRecord(ev.e[4 * n + 1], h->st));
-        update_factor(h, n, W, false, h->slots[2][n], ev.e[4 * n + 2], h->sharded);
+        mp_update(h, n, (n + N - 1) % N, h->slots[2][n], ev.e[4 * n + 1], ev.e[4 * n + 2]);
         TK_CUDA(cudaEventRecord(ev.e[4 * n + 3], h->st));
       }
       TK_CUDA(cudaEventRecord(ev.e[4 * N], h->st));
@@ -955,19 +1031,45 @@ int tucker_debug_gram(tucker_handle* h, int algo, int mode, double* S_out) {
   if (!h || !S_out || mode < 0 || mode >= h->order || algo < 0 || algo > 1) return TUCKER_E_ARG;
   return guarded(h, [&]() -> int {
     Split A;
+    const bool sparse = algo == 1 && mp_use_sparse(h, mode, -1);
     if (algo == 0) {
       project_hooi(h, mode, false);
       h->G_valid = false;
       A = h->Y;
-    } else {
+    } else if (!sparse) {
       A = build_mp_w(h, mode);
     }
-    const int64_t d = A.rows;
+    const int64_t d = h->dims[mode];
     const int64_t lds = ensure_S(h, d);
-    gram_syrk(A, h->S.p, lds, h->gram, h->st);
+    if (sparse) build_mp_gram_sparse(h, mode, -1);
+    else gram_syrk(A, h->S.p, lds, h->gram, h->st);
     const bool od = (h->opts.flags & TUCKER_OUTPUT_ON_DEVICE) != 0;
     TK_CUDA(cudaMemcpy2DAsync(S_out, d * sizeof(double), h->S.p, lds * sizeof(double), d * sizeof(double), d,
                               od ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, h->st));
+    TK_CUDA(cudaStreamSynchronize(h->st));
+    return TUCKER_OK;
+  });
+}
+
+int tucker_debug_gram_rows(tucker_handle* h, int algo, int mode, int nrows, const int64_t* rows, double* out) {
+  if (!h || !rows || !out || nrows < 1 || mode < 0 || mode >= h->order || algo < 0 || algo > 1) return TUCKER_E_ARG;
+  for (int r = 0; r < nrows; ++r)
+    if (rows[r] < 0 || rows[r] >= h->dims[mode]) return TUCKER_E_ARG;
+  return guarded(h, [&]() -> int {
+    const int64_t d = h->dims[mode];
+    const int64_t lds = ensure_S(h, d);
+    if (algo == 0) {
+      project_hooi(h, mode, false);
+      h->G_valid = false;
+      gram_syrk(h->Y, h->S.p, lds, h->gram, h->st);
+    } else if (mp_use_sparse(h, mode, -1)) {
+      build_mp_gram_sparse(h, mode, -1);
+    } else {
+      gram_syrk(build_mp_w(h, mode), h->S.p, lds, h->gram, h->st);
+    }
+    for (int r = 0; r < nrows; ++r)
+      TK_CUDA(cudaMemcpyAsync(out + (int64_t)r * d, h->S.p + rows[r] * lds, d * sizeof(double),
+                              cudaMemcpyDeviceToHost, h->st));
     TK_CUDA(cudaStreamSynchronize(h->st));
     return TUCKER_OK;
   });

@@ -507,3 +507,15 @@ def test_hooi_large_exact_multilinear_rank():
     assert out["fit"] > 1 - 1e-6
     for n in range(3):
         assert O.projector_distance(out["U"][n], A[n]) < 1e-8
+
+
+@pytest.mark.parametrize("dims,core", [((7, 9, 5), (2, 3, 2)), ((11, 4, 13), (3, 2, 4))])
+def test_mp_gram_rows_is_a_row_of_the_slice_loop(dims, core):
+    """mp_gram_rows (MP's M_n rows without forming M_n) against the literal Fig. 7 slice
+    loop mp_gram_slices (P9), including rows with no nonzero (zero rows)."""
+    X, T = rand_sparse(dims, 0.2, 48)
+    U = rand_factors(dims, core, 49)
+    for n in range(3):
+        M = O.mp_gram_slices(T, U, n)
+        rows = list(range(dims[n]))
+        np.testing.assert_allclose(O.mp_gram_rows(T, U, n, rows), M, rtol=1e-12, atol=1e-12)
