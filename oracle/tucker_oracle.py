@@ -374,12 +374,12 @@ def mp_gram_slices(T: SparseTensor, U, n: int) -> np.ndarray:
     return M
 
 
-def mp_gram_rows(T: SparseTensor, U, n: int, rows) -> np.ndarray:
+def mp_gram_rows(T: SparseTensor, U, n: int, rows, chunk: int = 2_000_000) -> np.ndarray:
     """Rows `rows` of M_n (Fig. 7/8, Appendix) without forming M_n or W:
-    M_n[i, :] = sum_{m != n} sum_{slices s} P_s[i, :] P_s^T with P_s = X_s U_m, over the
-    slices s whose X_s has a nonzero in row i (the others contribute nothing).  For
-    tensors whose M_n (d x d) or W does not fit (BASELINE config 5: d = 50000).
-    Order 3."""
+    M_n[i, :] = sum_{m != n} sum_{slices s} P_s[i, :] P_s^T with P_s = X_s U_m (Eq. 1),
+    the slices s fixing the third mode o.  The slices are visited in chunks of at most
+    `chunk` nonzeros so that memory stays bounded (BASELINE config 5: d = 50000, 2e8
+    nonzeros).  Order 3."""
     if T.N != 3:
         raise ValueError("mp_gram_rows: order 3 only")
     rows = np.asarray(rows, dtype=np.int64)
@@ -389,21 +389,29 @@ def mp_gram_rows(T: SparseTensor, U, n: int, rows) -> np.ndarray:
             continue
         o = 3 - n - m
         Um = np.asarray(U[m], dtype=np.float64)
-        for k, i in enumerate(rows):
-            slices = np.unique(T.idx[o][T.idx[n] == i])  # slices with a nonzero in row i
-            sel = np.isin(T.idx[o], slices)
-            so, sn, sm = T.idx[o][sel], T.idx[n][sel], T.idx[m][sel]
-            # P_s for all those slices at once: rows (s, i'), a sparse x dense product (Eq. 1)
-            key = so * T.dims[n] + sn
-            uk, inv = np.unique(key, return_inverse=True)
-            Xs = sp.csr_matrix((T.vals[sel], (inv, sm)), shape=(uk.size, T.dims[m]))
-            P = Xs @ Um                                   # rows: fibers (s, i')
-            ks, ki = uk // T.dims[n], uk % T.dims[n]
-            mine = ki == i                                # the row i of each slice
-            Pi = np.zeros((T.dims[o], Um.shape[1]))
-            Pi[ks[mine]] = P[mine]
-            # M[i, i'] += <P_s[i], P_s[i']> for every fiber (s, i')
-            np.add.at(out[k], ki, np.einsum("fj,fj->f", P, Pi[ks]))
+        order = np.argsort(T.idx[o], kind="stable")
+        so_all = T.idx[o][order]
+        bounds = np.searchsorted(so_all, np.arange(T.dims[o] + 1))  # nonzeros of slice s
+        s0 = 0
+        while s0 < T.dims[o]:
+            s1 = max(s0 + 1, int(np.searchsorted(bounds, bounds[s0] + chunk, side="right")) - 1)
+            s1 = min(s1, T.dims[o])
+            sel = order[bounds[s0]:bounds[s1]]
+            if sel.size:
+                so, sn, sm = T.idx[o][sel], T.idx[n][sel], T.idx[m][sel]
+                key = (so - s0) * T.dims[n] + sn
+                uk, inv = np.unique(key, return_inverse=True)    # fibers (s, i')
+                Xs = sp.csr_matrix((T.vals[sel], (inv, sm)), shape=(uk.size, T.dims[m]))
+                P = Xs @ Um                                      # row (s, i') of P_s
+                ks, ki = uk // T.dims[n], uk % T.dims[n]
+                for k, i in enumerate(rows):
+                    mine = np.flatnonzero(ki == i)               # P_s[i] of the chunk's slices
+                    if mine.size == 0:
+                        continue
+                    Pi = np.zeros((s1 - s0, Um.shape[1]))
+                    Pi[ks[mine]] = P[mine]
+                    np.add.at(out[k], ki, np.einsum("fj,fj->f", P, Pi[ks]))
+            s0 = s1
     return out
 
 

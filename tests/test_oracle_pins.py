@@ -519,3 +519,5 @@ def test_mp_gram_rows_is_a_row_of_the_slice_loop(dims, core):
         M = O.mp_gram_slices(T, U, n)
         rows = list(range(dims[n]))
         np.testing.assert_allclose(O.mp_gram_rows(T, U, n, rows), M, rtol=1e-12, atol=1e-12)
+        # slices visited in chunks of a few nonzeros: the same rows
+        np.testing.assert_allclose(O.mp_gram_rows(T, U, n, rows, chunk=7), M, rtol=1e-12, atol=1e-12)
