@@ -4,9 +4,9 @@
 // collectives the sweep uses, and the contiguous work-balanced shard bounds.
 //
 // Exchange steps (one per mode, all sums of disjoint or partial terms):
-//   HOOI, Y Y^T route: rows of Y_(n) are disjoint across ranks -> allreduce Y
+//   HOOI, Y Y^T route: rows of Y_(n) are disjoint across ranks -> allgatherv Y
 //   HOOI, Y^T Y route: partial Gram over the rank's K range -> allreduce S (fp64);
-//                      rows of U = Y V Theta^{-1/2} disjoint -> allreduce U
+//                      rows of U = Y V Theta^{-1/2} disjoint -> allgatherv U
 //   HOOI core:         G = U_N^T Y_(N) partial when Y was not gathered -> allreduce G
 //   MP:                partial M_n over the rank's slices -> allreduce M_n (fp64)
 #include <dlfcn.h>
@@ -27,6 +27,9 @@ struct NcclApi {
   ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
   ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
                             cudaStream_t) = nullptr;
+  ncclResult_t (*Broadcast)(const void*, void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*GroupStart)() = nullptr;
+  ncclResult_t (*GroupEnd)() = nullptr;
   ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
   const char* (*GetErrorString)(ncclResult_t) = nullptr;
 };
@@ -47,6 +50,9 @@ NcclApi& api() {
     a.GetUniqueId = (decltype(a.GetUniqueId))sym("ncclGetUniqueId");
     a.CommInitRank = (decltype(a.CommInitRank))sym("ncclCommInitRank");
     a.AllReduce = (decltype(a.AllReduce))sym("ncclAllReduce");
+    a.Broadcast = (decltype(a.Broadcast))sym("ncclBroadcast");
+    a.GroupStart = (decltype(a.GroupStart))sym("ncclGroupStart");
+    a.GroupEnd = (decltype(a.GroupEnd))sym("ncclGroupEnd");
     a.CommDestroy = (decltype(a.CommDestroy))sym("ncclCommDestroy");
     a.GetErrorString = (decltype(a.GetErrorString))sym("ncclGetErrorString");
     a.lib = l;
@@ -114,6 +120,35 @@ static void allreduce(void* comm, void* p, int64_t n, int dtype, cudaStream_t st
   // cudaMemcpy, whose DMA can still be in flight when it returns): wait for the
   // whole device before the handle's stream reads the buffer
   TK_CUDA(cudaDeviceSynchronize());
+}
+
+// Every rank owns the contiguous element range [off[r], off[r + 1]) of `base` and
+// receives everybody's: one ncclBroadcast per rank, rooted at the owner, in place, in
+// one NCCL group (an allgather with unequal counts; each byte crosses the fabric once,
+// half of what an allreduce of the zero-padded buffer moves).  Host collectives: the
+// other ranks' ranges are zero in this rank's buffer, so the allreduce callback is the
+// same gather.
+static void allgatherv(void* comm, void* base, const int64_t* off, int world, int dtype, cudaStream_t st) {
+  auto* c = static_cast<DistComm*>(comm);
+  if (!c->nccl) {
+    allreduce(comm, (char*)base + off[0] * (dtype ? 8 : 4), off[world] - off[0], dtype, st);
+    return;
+  }
+  const size_t es = dtype ? 8 : 4;
+  check(api().GroupStart(), "ncclGroupStart");
+  for (int r = 0; r < world; ++r) {
+    const int64_t n = off[r + 1] - off[r];
+    if (n <= 0) continue;
+    void* p = (char*)base + off[r] * es;
+    check(api().Broadcast(p, p, (size_t)n, dtype ? ncclFloat64 : ncclFloat32, r, c->nccl, st), "ncclBroadcast");
+  }
+  check(api().GroupEnd(), "ncclGroupEnd");
+}
+void dist_allgatherv_f32(void* comm, float* base, const int64_t* off, int world, cudaStream_t st) {
+  allgatherv(comm, base, off, world, 0, st);
+}
+void dist_allgatherv_f64(void* comm, double* base, const int64_t* off, int world, cudaStream_t st) {
+  allgatherv(comm, base, off, world, 1, st);
 }
 
 void dist_allreduce_f32(void* comm, float* p, int64_t n, cudaStream_t st) { allreduce(comm, p, n, 0, st); }

@@ -99,6 +99,9 @@ void* dist_comm_host();  // TUCKER_HOST_COLLECTIVES: sums through a host callbac
 void dist_comm_set_callback(void* comm, void* fn, void* user);
 void dist_allreduce_f32(void* comm, float* p, int64_t n, cudaStream_t st);
 void dist_allreduce_f64(void* comm, double* p, int64_t n, cudaStream_t st);
+// rank r owns elements [off[r], off[r + 1]) of base (off has world + 1 entries); all ranks get all
+void dist_allgatherv_f32(void* comm, float* base, const int64_t* off, int world, cudaStream_t st);
+void dist_allgatherv_f64(void* comm, double* base, const int64_t* off, int world, cudaStream_t st);
 void dist_unique_id(void* out128);
 void shard_bounds(const double* w, int64_t n, int world, int64_t* bounds);
 

@@ -65,6 +65,7 @@ struct tucker_handle {
   void* comm = nullptr;
   bool sharded = false;
   int64_t hooi_lo[kMaxOrder] = {0, 0, 0, 0}, hooi_hi[kMaxOrder] = {-1, -1, -1, -1};  // root slices of mode n
+  std::vector<int64_t> hooi_bounds[kMaxOrder];  // every rank's root-slice bounds of mode n (world + 1)
   int64_t mp_lo[kMaxOrder][kMaxOrder] = {}, mp_hi[kMaxOrder][kMaxOrder] = {};       // slices of MP term (n, m)
   bool Y_partial = false;  // h->Y holds only this rank's rows (Y^T Y route, not gathered)
 };
@@ -206,9 +207,11 @@ void project_hooi(tucker_handle* h, int n, bool transposed) {
   h->Y_partial = false;
   if (h->sharded) {
     if (!transposed) {
-      // Y Y^T route: the ranks' rows of Y_(n) are disjoint -> the sum gathers Y
-      dist_allreduce_f32(h->comm, h->Yhi.p, (int64_t)need, h->st);
-      dist_allreduce_f32(h->comm, h->Ylo.p, (int64_t)need, h->st);
+      // Y Y^T route: the ranks' rows of Y_(n) are disjoint -> allgather them
+      std::vector<int64_t> off(h->hooi_bounds[n].size());
+      for (size_t r = 0; r < off.size(); ++r) off[r] = h->hooi_bounds[n][r] * ld;
+      dist_allgatherv_f32(h->comm, h->Yhi.p, off.data(), h->opts.world, h->st);
+      dist_allgatherv_f32(h->comm, h->Ylo.p, off.data(), h->opts.world, h->st);
     } else {
       h->Y_partial = true;  // Y^T Y route: partial Gram over this rank's K range instead
     }
@@ -457,8 +460,12 @@ void factor_from_S(tucker_handle* h, int n, const Split& A, bool transposed, Eig
     MatRef b;
     b.t = Elt::F64; b.p = h->V.p; b.ld = J; b.trans = false;
     dgemm(I, J, d, 1.0, a, b, 0.0, h->Ufull.p, J, 0.0, nullptr, 0, h->eig.dense, h->st);
-    // sharded: rows of U outside this rank's shard are zero (Y was) -> the sum gathers U
-    if (partial_gram) dist_allreduce_f64(h->comm, h->Ufull.p, I * J, h->st);
+    // sharded: this rank computed the rows of its shard (the others are zero: Y was) -> allgather
+    if (partial_gram) {
+      std::vector<int64_t> off(h->hooi_bounds[n].size());
+      for (size_t r = 0; r < off.size(); ++r) off[r] = h->hooi_bounds[n][r] * J;
+      dist_allgatherv_f64(h->comm, h->Ufull.p, off.data(), h->opts.world, h->st);
+    }
     cholqr2(h->Ufull.p, J, I, J, h->eig, h->st);
     canon_to_f32(h->Ufull.p, J, I, J, h->U[n].p, h->st);
   }
@@ -549,6 +556,7 @@ void make_shards(tucker_handle* h) {
     shard_bounds(w.data(), c.I_root, W, b.data());
     h->hooi_lo[n] = b[r];
     h->hooi_hi[n] = b[r + 1];
+    h->hooi_bounds[n] = b;
     for (int m = 0; m < h->order; ++m) {
       if (m == n) continue;
       const Csf& t = *h->csfs[h->mp_csf[n][m]];

@@ -153,3 +153,72 @@ def test_world2_sharded_sweep_matches_unsharded(capi):
             for n in range(len(dims)):
                 d = O.projector_distance(np.asarray(U[n], np.float64), np.asarray(rU[n], np.float64))
                 assert d < 1e-5, (dims, algo, n, d)
+
+
+# ---------------------------------------------------------------------------------
+# Config 5 at full size, HOOI, sharded over world 2 and 4 on one GPU through host
+# collectives: every rank holds the full 2e8-nonzero tensor, computes only its shard
+# (Zipf-skewed, work-balanced slice ranges), and the library's exchange steps (Y row
+# allgather, partial Gram / core sums) go through gloo.  The sharded sweep must
+# reproduce the unsharded one: fits to 1e-6 and factors within the fp32 conditioning
+# bound of config 5 (tests/test_gpu_config5.py: kappa 2^-21 with the kappa of the
+# cached oracle's first sweep), since the partial Grams are summed in another order.
+
+def _c5_rank(rank, world, port, q):
+    import torch
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from cuda.bindings import runtime as rt
+    from paper_0711_2023_b200 import capi
+    from synth import make_config
+
+    def allreduce(ptr, n, dt, stream):
+        host = np.empty(n, dtype=np.float32 if dt == 0 else np.float64)
+        e1, = rt.cudaMemcpy(host.ctypes.data, ptr, host.nbytes, rt.cudaMemcpyKind.cudaMemcpyDeviceToHost)
+        dist.all_reduce(torch.from_numpy(host))
+        e2, = rt.cudaMemcpy(ptr, host.ctypes.data, host.nbytes, rt.cudaMemcpyKind.cudaMemcpyHostToDevice)
+        return 0 if (e1 == rt.cudaError_t.cudaSuccess and e2 == rt.cudaError_t.cudaSuccess) else 1
+
+    c = make_config(5, device="cuda")
+    with capi.Tucker(c["dims"], c["core"], c["idx"], c["vals"], c["U0"], rank=rank, world=world,
+                     host_collectives=True) as t:
+        cb = capi.tucker_set_allreduce(t.h, allreduce)  # noqa: F841 (kept alive)
+        shards = t.shard_info()[0]
+        fits = t.hooi_sweep(1)
+        G, U, fit = t.core_and_fit()
+    if rank == 0:
+        q.put((shards, fits, U, fit))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_config5_hooi_sharded_world(capi, golden_dir, world):
+    import json
+    import torch.multiprocessing as tmp
+    from oracle import tucker_oracle as O
+    from synth import make_config
+    ctx = tmp.get_context("spawn")
+    q = ctx.Queue()
+    port = 29800 + 10 * world + (os.getpid() % 500)
+    procs = [ctx.Process(target=_c5_rank, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    shards, fits, U, fit = q.get(timeout=1500)
+    for p in procs:
+        p.join(timeout=300)
+        assert p.exitcode == 0
+    c = make_config(5, device="cuda")
+    with capi.Tucker(c["dims"], c["core"], c["idx"], c["vals"], c["U0"]) as t:
+        rfits = t.hooi_sweep(1)
+        _, rU, rfit = t.core_and_fit()
+    diag = json.loads(str(np.load(os.path.join(golden_dir, "config5_hooi_oracle.npz"))["diag"]))[:3]
+    print(f"config5 world {world}: rank-0 shards {shards}, fit {fit:.9f} vs unsharded {rfit:.9f}")
+    assert abs(fit - rfit) < 1e-6 and abs(fits[0] - rfits[0]) < 1e-6
+    for n in range(3):
+        kap = diag[n]["l1"] / (diag[n]["lJ"] - diag[n]["lJ1"])
+        d = O.projector_distance(np.asarray(U[n], np.float64), np.asarray(rU[n], np.float64))
+        print(f"  mode {n + 1}: projector distance sharded vs unsharded {d:.3e} (bound {max(1e-4, kap * 2.0 ** -21):.3e})")
+        assert d < max(1e-4, kap * 2.0 ** -21)
