@@ -158,6 +158,7 @@ struct EigWs {
   DBuf<double> cq, ct, H, R;    // cholqr2 (Y^T Y route)
   DBuf<double> bL, bQ, bSQ, bY0, bY1, bT, sH, sV, sC, sTh, sRes;  // eig_large work blocks
   DBuf<int> sInfo;
+  DBuf<double> small;  // eig_small scratch
   DenseWs dense;
   int64_t stat_outer = 0, stat_matvec = 0, stat_sweeps = 0;
 };
@@ -182,6 +183,12 @@ size_t eig_fused_smem(int k, int d, int G);
 // memory): the same method as a host-driven kernel sequence (eig_large.cu); S row
 // stride ls, same outputs and info record as eig_fused.  Synchronises the stream.
 constexpr int64_t kFusedMaxD = 8192;
+// Direct dense solver for d <= kSmallMaxD (eig_small.cu): Householder tridiagonalisation
+// in one 4-CTA cluster, bisection + inverse iteration, back-transformation.  V (n x m,
+// ld m), theta (m, descending), info record as eig_fused; scratch is a work buffer.
+constexpr int64_t kSmallMaxD = 256;
+void eig_small(const double* S, int64_t n, int64_t lds, int m, double* V, double* theta, int* info, DBuf<double>& scratch,
+               cudaStream_t st);
 bool eig_large(const double* S, int64_t d, int64_t ls, int J, EigSlot& slot, EigWs& ws, const EigOpts& o,
                double* out_V, double* theta_dev, int* info_dev, cudaStream_t st, const float* hint = nullptr);
 // MP's multislice Gram without the dense W (mp_sparse.cu): M (fp64, upper triangle, row

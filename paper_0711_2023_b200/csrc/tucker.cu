@@ -310,7 +310,16 @@ void solve_eig(tucker_handle* h, int64_t d, int J, EigSlot& slot, const float* h
   h->theta_d.ensure((size_t)J);
   h->info_d.ensure(16 * (kMaxOrder + 1));  // per record: 8 ints + 4 doubles
   h->rec_slot[rec] = &slot;
-  static const bool force_large = std::getenv("TUCKER_EIG_LARGE") != nullptr;  // tests
+  const bool force_large = std::getenv("TUCKER_EIG_LARGE") != nullptr;  // tests
+  // the direct dense solver (eig_small.cu) is correct but measured slower than the fused
+  // iterative solver at d = 200 (~4 ms vs 0.7-1.4 ms per solve): experiments only
+  const bool small = std::getenv("TUCKER_EIG_SMALL") != nullptr;
+  if (small && d <= kSmallMaxD && d >= 3 && !force_large) {
+    int64_t ls = 0, rows = 0;
+    eig_layout(d, &ls, &rows);
+    eig_small(h->S.p, d, ls, J, h->V.p, h->theta_d.p, h->info_d.p + 16 * rec, h->eig.small, h->st);
+    return;
+  }
   if (d > kFusedMaxD || force_large) {  // MP's M_n at config 5 (d = 50000): the host-driven variant
     int64_t ls = 0, rows = 0;
     eig_layout(d, &ls, &rows);

@@ -81,3 +81,38 @@ def test_split_k_product(capi, d, n):
     assert np.max(np.abs(out - ref)) / scale < 1e-14 * max(d, 16), (d, n)
     out0 = capi.tucker_debug_product(S, Y)
     assert np.max(np.abs(out0 - S @ Y)) / scale < 1e-14 * max(d, 16)
+
+
+@pytest.mark.parametrize("d,J,kind", [(3, 1, "spread"), (17, 5, "spread"), (100, 10, "outlier"), (200, 20, "outlier"),
+                                      (256, 112, "outlier"), (200, 50, "repeated"), (150, 30, "clustered")])
+def test_small_dense_eigensolver(monkeypatch, d, J, kind):
+    """eig_small (d <= 256: Householder tridiagonalisation in a 4-CTA cluster, bisection,
+    inverse iteration, back-transformation) against LAPACK: eigenvalues to 1e-12 relative
+    to ||S||, the leading-J subspace to 1e-9, orthonormal vectors -- including eigenvalues
+    repeated inside the leading set and a tight cluster around the J / J+1 boundary."""
+    from oracle import tucker_oracle as O
+    from paper_0711_2023_b200 import capi
+    from synth import random_orthonormal, uniform_distinct_coo
+    monkeypatch.setenv("TUCKER_EIG_SMALL", "1")  # the direct solver (experiments; not the default path)
+    rng = np.random.default_rng(d + 7 * J)
+    Q = np.linalg.qr(rng.standard_normal((d, d)))[0]
+    w = np.sort(rng.uniform(0.1, 1.0, d))[::-1].copy()
+    if kind == "outlier":
+        w[0] = 60.0
+    elif kind == "repeated":
+        w[:J] = np.repeat(np.linspace(5.0, 2.0, J // 5), 5)  # 5-fold eigenvalues, gap to J+1
+    elif kind == "clustered":
+        w[:J + 5] = 1.0 + 1e-4 * np.arange(J + 5)[::-1]        # relative gaps 1e-4
+        w = np.sort(w)[::-1]
+    S = (Q * w) @ Q.T
+    dims, core = (8, 8, 8), (2, 2, 2)
+    idx, vals = uniform_distinct_coo(dims, 50, np.random.default_rng(1))
+    U0 = [random_orthonormal(I, c, np.random.default_rng(2)) for I, c in zip(dims, core)]
+    with capi.Tucker(dims, core, idx, vals, U0) as t:
+        U, ev, rc = t.debug_eig(S, J)
+    Uo, wo = O.leading_eigenvectors(S, J)
+    assert rc == 0
+    np.testing.assert_allclose(ev, wo[:J], rtol=0, atol=1e-12 * wo[0])
+    assert np.abs(U.astype(np.float64).T @ U - np.eye(J)).max() < 1e-6
+    tol = 1e-9 if kind != "clustered" else 1e-5  # fp32 factor output; clustered: gap 1e-4
+    assert O.projector_distance(U, Uo) < max(tol, 1e-6)

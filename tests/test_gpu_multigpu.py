@@ -164,6 +164,43 @@ def test_world2_sharded_sweep_matches_unsharded(capi):
 # bound of config 5 (tests/test_gpu_config5.py: kappa 2^-21 with the kappa of the
 # cached oracle's first sweep), since the partial Grams are summed in another order.
 
+def _release_device_memory():
+    """Return this process's cached device memory (torch's cache and the library's
+    stream-ordered pool, which keeps freed blocks) before ranks that each need tens of
+    GB start on the same GPU."""
+    import gc
+
+    import torch
+    from cuda.bindings import runtime as rt
+    gc.collect()
+    torch.cuda.empty_cache()
+    err, pool = rt.cudaDeviceGetDefaultMemPool(0)
+    if err == rt.cudaError_t.cudaSuccess:
+        rt.cudaMemPoolTrimTo(pool, 0)
+
+
+def _get_or_fail(q, procs, timeout):
+    """The rank-0 result, or a failure as soon as a rank dies (instead of waiting out
+    the timeout while the survivors block in a collective)."""
+    import queue
+    import time
+    t0 = time.time()
+    while time.time() - t0 < timeout:
+        try:
+            return q.get(timeout=5)
+        except queue.Empty:
+            dead = [p.exitcode for p in procs if p.exitcode not in (None, 0)]
+            if dead:
+                for p in procs:
+                    if p.is_alive():
+                        p.kill()
+                pytest.fail(f"a rank exited with {dead}")
+    for p in procs:
+        if p.is_alive():
+            p.kill()
+    pytest.fail("timeout waiting for rank 0")
+
+
 def _c5_rank(rank, world, port, q):
     import torch
     import torch.distributed as dist
@@ -203,10 +240,11 @@ def test_config5_hooi_sharded_world(capi, golden_dir, world):
     ctx = tmp.get_context("spawn")
     q = ctx.Queue()
     port = 29800 + 10 * world + (os.getpid() % 500)
+    _release_device_memory()
     procs = [ctx.Process(target=_c5_rank, args=(r, world, port, q)) for r in range(world)]
     for p in procs:
         p.start()
-    shards, fits, U, fit = q.get(timeout=1500)
+    shards, fits, U, fit = _get_or_fail(q, procs, 1500)
     for p in procs:
         p.join(timeout=300)
         assert p.exitcode == 0
