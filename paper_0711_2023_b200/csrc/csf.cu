@@ -8,6 +8,8 @@
 #include <cub/cub.cuh>
 
 #include <cstdlib>
+#include <vector>
+#include <algorithm>
 #include <map>
 #include <mutex>
 
@@ -361,13 +363,13 @@ __global__ void k_pair_count(const int32_t* __restrict__ fib_ptr, int64_t f0, in
 // warp per fiber: pairs (a, b >= a) in row-major triangle order
 __global__ void k_pair_emit(const int32_t* __restrict__ fib_ptr, const int32_t* __restrict__ leaf,
                             const float* __restrict__ val, int64_t f0, int64_t nf,
-                            const int64_t* __restrict__ off, int64_t I, int64_t* __restrict__ key,
+                            const int64_t* __restrict__ off, int64_t base, int64_t I, int64_t* __restrict__ key,
                             double* __restrict__ pv) {
   const int lane = threadIdx.x & 31;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   for (int64_t f = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; f < nf; f += nw) {
     const int64_t e0 = fib_ptr[f0 + f], L = fib_ptr[f0 + f + 1] - e0;
-    int64_t o = off[f];
+    int64_t o = off[f] - base;
     for (int64_t a = 0; a < L; ++a) {
       const int64_t ia = leaf[e0 + a];
       const double xa = (double)val[e0 + a];
@@ -385,9 +387,9 @@ __global__ void k_pair_scatter(const int64_t* __restrict__ ukey, const double* _
                                int64_t lds) {
   const int64_t n = *nruns;
   for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n; r += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t i = ukey[r] / I, j = ukey[r] - i * I;
-    S[i * lds + j] = sum[r];
-    S[j * lds + i] = sum[r];
+    const int64_t i = ukey[r] / I, j = ukey[r] - i * I;  // i <= j; keys unique within a chunk
+    S[i * lds + j] += sum[r];
+    if (i != j) S[j * lds + i] += sum[r];
   }
 }
 
@@ -404,30 +406,48 @@ void sparse_gram(const Csf& c, int64_t f0, int64_t f1, double* S, int64_t lds, c
   TK_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, bytes, cnt.p, off.p, nf + 1, st));
   tmp.ensure(bytes);
   TK_CUDA(cub::DeviceScan::ExclusiveSum(tmp.p, bytes, cnt.p, off.p, nf + 1, st));
-  int64_t P = 0;
-  TK_CUDA(cudaMemcpyAsync(&P, off.p + nf, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  // fibers in chunks of at most kPairChunk pairs (the sort's memory: 6 x 8 B per pair); each
+  // chunk's pairs are sorted, reduced by key and added to S, chunks in fiber order
+  // (deterministic).  A dense 10 % tensor (the paper's Table 2 at 1000^3) has 5e9 pairs per mode.
+  constexpr int64_t kPairChunk = (int64_t)1 << 27;
+  std::vector<int64_t> offh((size_t)nf + 1);
+  TK_CUDA(cudaMemcpyAsync(offh.data(), off.p, offh.size() * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
   TK_CUDA(cudaStreamSynchronize(st));
-  if (P > ((int64_t)1 << 31) - 1)
-    fail(TUCKER_E_OOM, "tucker_hosvd: X_(n) X_(n)^T has " + std::to_string(P) +
-                           " fiber pairs (> 2^31); dense-block sparse Gram not implemented");
-  DBuf<int64_t> key((size_t)P), key2((size_t)P), ukey((size_t)P);
-  DBuf<double> pv((size_t)P), pv2((size_t)P), sum((size_t)P);
+  int64_t Pmax = 0;
+  for (int64_t a = 0; a < nf;) {
+    int64_t b = a + 1;
+    while (b < nf && offh[b + 1] - offh[a] <= kPairChunk) ++b;
+    Pmax = std::max(Pmax, offh[b] - offh[a]);
+    a = b;
+  }
+  if (Pmax > ((int64_t)1 << 31) - 1)
+    fail(TUCKER_E_OOM, "tucker_hosvd: one fiber of X_(n) has more than 2^31 pairs");
+  DBuf<int64_t> key((size_t)Pmax), key2((size_t)Pmax), ukey((size_t)Pmax);
+  DBuf<double> pv((size_t)Pmax), pv2((size_t)Pmax), sum((size_t)Pmax);
   DBuf<int> nruns(1);
-  TK_LAUNCH(k_pair_emit, grid_for(nf * 32), 256, 0, st, c.fib_ptr.p, c.leaf_id.p, c.val.p, f0, nf, off.p, I,
-            key.p, pv.p);
   int bits = 1;
   while (((int64_t)1 << bits) < I * I) ++bits;
-  bytes = 0;
-  TK_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, bytes, key.p, key2.p, pv.p, pv2.p, P, 0, bits, st));
-  tmp.ensure(bytes);
-  TK_CUDA(cub::DeviceRadixSort::SortPairs(tmp.p, bytes, key.p, key2.p, pv.p, pv2.p, P, 0, bits, st));
-  bytes = 0;
-  TK_CUDA(cub::DeviceReduce::ReduceByKey(nullptr, bytes, key2.p, ukey.p, pv2.p, sum.p, nruns.p,
-                                         cub::Sum(), P, st));
-  tmp.ensure(bytes);
-  TK_CUDA(cub::DeviceReduce::ReduceByKey(tmp.p, bytes, key2.p, ukey.p, pv2.p, sum.p, nruns.p, cub::Sum(),
-                                         P, st));
-  TK_LAUNCH(k_pair_scatter, grid_for(P), 256, 0, st, ukey.p, sum.p, nruns.p, I, S, lds);
+  for (int64_t a = 0; a < nf;) {
+    int64_t b = a + 1;
+    while (b < nf && offh[b + 1] - offh[a] <= kPairChunk) ++b;
+    const int64_t P = offh[b] - offh[a];
+    if (P > 0) {
+      TK_LAUNCH(k_pair_emit, grid_for((b - a) * 32), 256, 0, st, c.fib_ptr.p, c.leaf_id.p, c.val.p, f0 + a, b - a,
+                off.p + a, offh[a], I, key.p, pv.p);
+      bytes = 0;
+      TK_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, bytes, key.p, key2.p, pv.p, pv2.p, (int)P, 0, bits, st));
+      tmp.ensure(bytes);
+      TK_CUDA(cub::DeviceRadixSort::SortPairs(tmp.p, bytes, key.p, key2.p, pv.p, pv2.p, (int)P, 0, bits, st));
+      bytes = 0;
+      TK_CUDA(cub::DeviceReduce::ReduceByKey(nullptr, bytes, key2.p, ukey.p, pv2.p, sum.p, nruns.p, cub::Sum(),
+                                             (int)P, st));
+      tmp.ensure(bytes);
+      TK_CUDA(cub::DeviceReduce::ReduceByKey(tmp.p, bytes, key2.p, ukey.p, pv2.p, sum.p, nruns.p, cub::Sum(),
+                                             (int)P, st));
+      TK_LAUNCH(k_pair_scatter, grid_for(P), 256, 0, st, ukey.p, sum.p, nruns.p, I, S, lds);
+    }
+    a = b;
+  }
   TK_CUDA(cudaStreamSynchronize(st));  // the scratch buffers go out of scope
 }
 

@@ -15,6 +15,7 @@ from .generators import (  # noqa: F401
     CONFIGS,
     bernoulli_dense,
     bernoulli_coo,
+    bernoulli_coo_slabs,
     make_config,
     random_orthonormal,
     sp_random_init,

@@ -1,0 +1,63 @@
+"""the paper's Table 2 workloads at paper scale on one GPU
+(500^3, 750^3, 1000^3 at 10 % density: 12.5M / 42.2M / 100M nonzeros, cores 50^3 /
+75^3 / 100^3; Table 1), end to end through the C-ABI from host buffers
+(tucker_init + HO-SVD / pseudo HO-SVD init + sweeps until Delta_fit < 1e-4 (Eq. 10)
+or Delta_G < 1e-4 (SP, Eq. 11) + core/fit), next to the printed fits and MATLAB run
+times (one 2007 Opteron core; context only).  Inputs: the paper's
+Bernoulli(0.1) x U(0,1] recipe (synth.bernoulli_coo_slabs).  One JSON line per size.
+    python tools/paper_scale.py [500 750 1000]"""
+import json
+import os
+import sys
+import time
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np  # noqa: E402
+
+import __graft_entry__  # noqa: E402
+__graft_entry__.build()
+from paper_0711_2023_b200 import capi  # noqa: E402
+from synth import bernoulli_coo_slabs, random_orthonormal, sp_random_init  # noqa: E402
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+g = json.load(open(os.path.join(ROOT, "tests", "golden", "paper_fits.json")))
+PAPER_TIME = {500: {"hosvd": "00:03:44", "hooi": "00:09:52", "sp": "00:10:21", "mp": "00:13:55"},
+              750: {"hosvd": "00:14:42", "hooi": "00:42:45", "sp": "00:34:39", "mp": "00:51:33"},
+              1000: {"hosvd": "01:10:13", "hooi": "04:01:36", "sp": "01:43:20", "mp": "02:21:30"}}
+sizes = [int(a) for a in sys.argv[1:]] or [500, 750, 1000]
+for I in sizes:
+    case = g[f"table2_{I}cube_J{I // 10}"]
+    dims, core = tuple(case["dims"]), tuple(case["core"])
+    t0 = time.time()
+    idx, vals = bernoulli_coo_slabs(dims, case["density"], seed=I)
+    gen_s = time.time() - t0
+    U0 = [random_orthonormal(n, j, np.random.default_rng(60 + k)) for k, (n, j) in enumerate(zip(dims, core))]
+    out = {"workload": f"PAPER Table 2: {I}^3, density 0.1, core {I // 10}^3", "nnz": int(vals.size),
+           "gen_s": gen_s, "paper_fit_pct": {k: case[k] for k in ("hosvd", "hooi", "sp", "mp")},
+           "paper_time": PAPER_TIME.get(I)}
+    rest = range(1, 3)
+
+    def run(algo):
+        t0 = time.time()
+        h = capi.Tucker(dims, core, idx, vals, U0)
+        try:
+            if algo == "hosvd":
+                h.hosvd()
+                n = 0
+            elif algo == "sp":
+                C0 = sp_random_init(dims[-1], core[-1], np.random.default_rng(7)).astype(np.float32)
+                h.set_factor(2, C0, check=False)
+                n = len(h.sp_run(50, 1e-4))
+            else:
+                h.hosvd(rest)  # HOOI: HO-SVD of modes 2..N; MP: pseudo HO-SVD (same eigenvectors)
+                n = len(getattr(h, algo + "_run")(50, 1e-4))
+            _, _, fit = h.core_and_fit(want_core=False, want_factors=False)
+        finally:
+            h.close()
+        return 100 * fit, n, time.time() - t0
+
+    for algo in ("hosvd", "hooi", "sp", "mp"):
+        fit, n, s = run(algo)
+        out[algo] = {"fit_pct": round(fit, 4), "sweeps": n, "seconds": round(s, 3),
+                     "delta_pp": round(fit - case[algo], 4)}
+    print(json.dumps(out), flush=True)
