@@ -87,8 +87,9 @@ void tucker_default_opts(tucker_opts* opts);
  *           P:911-1114; SURVEY reading A18).
  *   dims    I_1..I_N, each >= 1 and I_n < 2^31, with prod_n I_n < 2^64 (the
  *           sort keys pack every coordinate into 64 bits; TUCKER_E_ARG otherwise).
- *   core    J_1..J_N, 1 <= J_n <= min(I_n, 112) (this build's eigensolver
- *           block limit) and J_n <= prod_{q != n} J_q (Y_(n) has at most that
+ *   core    J_1..J_N, 1 <= J_n <= min(I_n, 240) (the eigensolvers' block k = J + p
+ *           <= 256; J_n > 112 runs the host-driven solver, core sizes > 128 the
+ *           tcgen05 SpTTMc in 128-column windows) and J_n <= prod_{q != n} J_q (Y_(n) has at most that
  *           rank, so no J_n-dimensional dominant subspace exists beyond it);
  *           TUCKER_E_ARG otherwise.
  *   nnz     number of COO entries (>= 1).

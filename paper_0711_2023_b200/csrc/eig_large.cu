@@ -71,6 +71,14 @@ __global__ void k_copy_block(const double* __restrict__ src, int lds, double* __
   }
 }
 
+// W[:, j] *= lambda_j^{-1/2} (k x k, row-major), 0 for lambda_j <= 0
+__global__ void k_scale_rsqrt_cols(double* W, int k, const double* __restrict__ lam) {
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < k * k; e += gridDim.x * blockDim.x) {
+    const double l = lam[e % k];
+    W[e] *= l > 0 ? 1.0 / sqrt(l) : 0.0;
+  }
+}
+
 inline unsigned grid_of(int64_t n) { return (unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(n, 256), 148 * 8)); }
 
 MatRef f64m(const double* p, int64_t ld, bool trans = false) {
@@ -86,7 +94,29 @@ MatRef f64m(const double* p, int64_t ld, bool trans = false) {
 
 bool eig_large(const double* S, int64_t d, int64_t ls, int J, EigSlot& slot, EigWs& ws, const EigOpts& o,
                double* out_V, double* theta_dev, int* info_dev, cudaStream_t st, const float* hint) {
-  const int k = std::min<int64_t>(kMaxBlock, std::min<int64_t>(d, J + std::max(8, std::min(J, 10))));
+  const int k = (int)std::min<int64_t>(kSmallMaxD, std::min<int64_t>(d, J + std::max(8, std::min(J, 10))));
+  // blocks wider than the one-CTA Jacobi / CholQR (k > kMaxBlock): the Rayleigh-Ritz problem on the
+  // direct dense solver (eig_small) and orthonormalisation by SVQB, Q <- Q W Lambda^{-1/2} with
+  // Q^T Q = W Lambda W^T (twice; columns get re-mixed, which the next Rayleigh-Ritz step undoes)
+  auto orth = [&](double* Qb, int kk) {
+    if (kk <= kMaxBlock) {
+      cholqr2(Qb, kk, d, kk, ws, st);
+      return;
+    }
+    for (int pass = 0; pass < 2; ++pass) {
+      dgemm(kk, kk, d, 1.0, f64m(Qb, kk, true), f64m(Qb, kk), 0.0, ws.sH.p, kk, 0.0, nullptr, 0, ws.dense, st);
+      eig_small(ws.sH.p, kk, kk, kk, ws.sV.p, ws.sTh.p, ws.sInfo.p, ws.small, st);
+      TK_LAUNCH(k_scale_rsqrt_cols, grid_of((int64_t)kk * kk), 256, 0, st, ws.sV.p, kk, ws.sTh.p);
+      dgemm(d, kk, kk, 1.0, f64m(Qb, kk), f64m(ws.sV.p, kk), 0.0, ws.bT.p == Qb ? ws.bY1.p : ws.bT.p, kk, 0.0,
+            nullptr, 0, ws.dense, st);
+      double* out = ws.bT.p == Qb ? ws.bY1.p : ws.bT.p;
+      TK_LAUNCH(k_copy_block, grid_of(d * kk), 256, 0, st, out, kk, Qb, kk, d, 0, kk);
+    }
+  };
+  auto rr_eig = [&](int ka) {
+    if (ka <= kMaxBlock) eig_unit(1, ws.sH.p, ka, ws.sV.p, ws.sTh.p, ws.sInfo.p, 40, 0.0, st);
+    else eig_small(ws.sH.p, ka, ka, ka, ws.sV.p, ws.sTh.p, ws.sInfo.p, ws.small, st);
+  };
   const double tol = o.tol;
   // work blocks d x k (fp64): L (locked, first nl columns valid), Q (active), SQ, Y0, Y1, T
   ws.bL.ensure((size_t)d * k);
@@ -100,7 +130,7 @@ bool eig_large(const double* S, int64_t d, int64_t ls, int J, EigSlot& slot, Eig
   ws.sC.ensure((size_t)k * k);
   ws.sTh.ensure((size_t)k);
   ws.sRes.ensure((size_t)k);
-  ws.sInfo.ensure(8);
+  ws.sInfo.ensure(16);
   double *L = ws.bL.p, *Q = ws.bQ.p, *SQ = ws.bSQ.p, *Y0 = ws.bY0.p, *Y1 = ws.bY1.p, *T = ws.bT.p;
   // start: the slot's basis of the last solve (same d, k), else the hint + pseudo-random columns
   const bool warm = slot.valid && slot.d == d && slot.k == k && slot.basis.n >= (size_t)d * k;
@@ -109,7 +139,7 @@ bool eig_large(const double* S, int64_t d, int64_t ls, int J, EigSlot& slot, Eig
   } else {
     TK_LAUNCH(k_seed_large, grid_of(d * k), 256, 0, st, Q, d, k, hint, J, 0x1a29e5ull + (uint64_t)d * 131 + J);
   }
-  cholqr2(Q, k, d, k, ws, st);
+  orth(Q, k);
 
   int nl = 0;  // locked columns (leading Ritz pairs, descending)
   std::vector<double> th((size_t)k), res((size_t)k), lth;
@@ -123,7 +153,7 @@ bool eig_large(const double* S, int64_t d, int64_t ls, int J, EigSlot& slot, Eig
     dgemm(d, ka, d, 1.0, f64m(S, ls), f64m(Q, ka), 0.0, SQ, ka, 0.0, nullptr, 0, ws.dense, st);
     ++products;
     dgemm(ka, ka, d, 1.0, f64m(Q, ka, true), f64m(SQ, ka), 0.0, ws.sH.p, ka, 0.0, nullptr, 0, ws.dense, st);
-    eig_unit(1, ws.sH.p, ka, ws.sV.p, ws.sTh.p, ws.sInfo.p, 40, 0.0, st);
+    rr_eig(ka);
     dgemm(d, ka, ka, 1.0, f64m(Q, ka), f64m(ws.sV.p, ka), 0.0, T, ka, 0.0, nullptr, 0, ws.dense, st);
     std::swap(Q, T);
     dgemm(d, ka, ka, 1.0, f64m(SQ, ka), f64m(ws.sV.p, ka), 0.0, T, ka, 0.0, nullptr, 0, ws.dense, st);
@@ -198,7 +228,7 @@ bool eig_large(const double* S, int64_t d, int64_t ls, int J, EigSlot& slot, Eig
       dgemm(nl, kn, d, 1.0, f64m(L, k, true), f64m(Q, kn), 0.0, ws.sC.p, kn, 0.0, nullptr, 0, ws.dense, st);
       dgemm(d, kn, nl, -1.0, f64m(L, k), f64m(ws.sC.p, kn), 1.0, Q, kn, 0.0, nullptr, 0, ws.dense, st);
     }
-    cholqr2(Q, kn, d, kn, ws, st);
+    orth(Q, kn);
   }
   // result: V = [L | leading active Ritz vectors] (J columns, descending), theta
   std::vector<double> thJ((size_t)J);

@@ -7,7 +7,8 @@
 namespace tk {
 
 constexpr int kMaxOrder = 4;
-constexpr int kMaxJ = 112;       // per-mode core size limit of this build (eigensolver block <= 116)
+constexpr int kMaxJ = 240;       // per-mode core size limit (eigensolver block k = J + p <= 256)
+constexpr int kMaxJFused = 112;  // the persistent eigensolver's limit (block <= 116); larger J: eig_large
 constexpr int kMaxBlock = 116;   // eigensolver block size k limit (Jacobi in shared memory)
 
 // ---------------------------------------------------------------------------

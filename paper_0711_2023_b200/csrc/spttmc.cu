@@ -78,13 +78,13 @@ struct FVec<4> {
 
 template <int VW, int QV, int UN>
 __device__ __forceinline__ void gather_rows(const int* l, const float* x, int n,
-                                            const float* __restrict__ Uleaf, int Jl, int lane,
+                                            const float* __restrict__ Uleaf, int ldl, int Jl, int lane,
                                             float (&t)[QV][VW]) {
   using V = typename FVec<VW>::T;
   V g[UN][QV];
 #pragma unroll
   for (int u = 0; u < UN; ++u) {
-    const V* r = reinterpret_cast<const V*>(Uleaf + (int64_t)l[u] * Jl);
+    const V* r = reinterpret_cast<const V*>(Uleaf + (int64_t)l[u] * ldl);
 #pragma unroll
     for (int q = 0; q < QV; ++q) {
       const int v = lane + 32 * q;
@@ -135,7 +135,7 @@ __device__ __forceinline__ void leaf_stage_s(int nf, const int* fptr, const int*
           l[u] = u < n ? sl[e + u - E0] : 0;
           x[u] = u < n ? sv[e + u - E0] : 0.f;
         }
-        gather_rows<VW, QV, UN>(l, x, n, Uleaf, Jl, lane, t);
+        gather_rows<VW, QV, UN>(l, x, n, Uleaf, Jl, Jl, lane, t);
       }
     } else {
       for (int e = e0; e < e1; e += UN) {
@@ -145,7 +145,7 @@ __device__ __forceinline__ void leaf_stage_s(int nf, const int* fptr, const int*
           l[u] = u < n ? __ldg(leaf_id + e + u) : 0;
           x[u] = u < n ? __ldg(val + e + u) : 0.f;
         }
-        gather_rows<VW, QV, UN>(l, x, n, Uleaf, Jl, lane, t);
+        gather_rows<VW, QV, UN>(l, x, n, Uleaf, Jl, Jl, lane, t);
       }
     }
 #pragma unroll
@@ -229,6 +229,9 @@ struct Ttmc3Args {
   int64_t ldY;
   int transposed;
   int64_t sa, sb;  // Kolda strides of (mid index a, leaf index b) in the output column
+  // k_spttmc3_tc column windows (J_mid or J_leaf > 128): Umid / Uleaf point at column a0 / b0 of
+  // factors with row strides ldm / ldl; Jm / Jl are the window widths
+  int ldm, ldl, a0, b0;
 };
 
 template <int RA, int RB, int VW>
@@ -460,7 +463,7 @@ __global__ void __launch_bounds__(256) k_spttmc3_tc(Ttmc3Args p) {
               l[u] = u < n ? sl[e + u - E0] : 0;
               x[u] = u < n ? sv[e + u - E0] : 0.f;
             }
-            gather_rows<VW, QV, 4>(l, x, n, p.Uleaf, p.Jl, lane, t);
+            gather_rows<VW, QV, 4>(l, x, n, p.Uleaf, p.ldl, p.Jl, lane, t);
           }
         } else {
           for (int e = e0; e < e1; e += 4) {
@@ -470,7 +473,7 @@ __global__ void __launch_bounds__(256) k_spttmc3_tc(Ttmc3Args p) {
               l[u] = u < n ? __ldg(p.leaf_id + e + u) : 0;
               x[u] = u < n ? __ldg(p.val + e + u) : 0.f;
             }
-            gather_rows<VW, QV, 4>(l, x, n, p.Uleaf, p.Jl, lane, t);
+            gather_rows<VW, QV, 4>(l, x, n, p.Uleaf, p.ldl, p.Jl, lane, t);
           }
         }
       }
@@ -509,7 +512,7 @@ __global__ void __launch_bounds__(256) k_spttmc3_tc(Ttmc3Args p) {
       }
       // A: rows a (mid index) straight from the U_mid rows of the chunk's fibers
       if (k < nf) {
-        const float* mr = p.Umid + (int64_t)fmid[k] * p.Jm;
+        const float* mr = p.Umid + (int64_t)fmid[k] * p.ldm;
         for (int a = warp; a < p.Jm; a += 8) st_split1(Ahi, Alo, k_sw128(a, k), __ldg(mr + a));
       }
     }
@@ -544,7 +547,7 @@ __global__ void __launch_bounds__(256) k_spttmc3_tc(Ttmc3Args p) {
           if (slot >= 0) {
             p.part[(int64_t)slot * p.Jm * p.Jl + a * p.Jl + bcol] = racc[j];
           } else {
-            const int64_t col = a * p.sa + bcol * p.sb;
+            const int64_t col = (p.a0 + a) * p.sa + (p.b0 + bcol) * p.sb;
             const int64_t off = p.transposed ? col * p.ldY + i : (int64_t)i * p.ldY + col;
             split_store(p.Yhi, p.Ylo, off, racc[j]);
           }
@@ -562,7 +565,7 @@ __global__ void __launch_bounds__(256) k_spttmc3_tc(Ttmc3Args p) {
 __global__ void __launch_bounds__(256) k_spttmc3_reduce(const int32_t* __restrict__ red,
                                                         const float* __restrict__ part, int Jm, int Jl,
                                                         int64_t sa, int64_t sb, float* Yhi, float* Ylo,
-                                                        int64_t ldY, int transposed) {
+                                                        int64_t ldY, int transposed, int a0, int b0) {
   const int r = blockIdx.y;
   const int i = red[3 * r], s0 = red[3 * r + 1], ns = red[3 * r + 2];
   const int P = Jm * Jl;
@@ -571,7 +574,7 @@ __global__ void __launch_bounds__(256) k_spttmc3_reduce(const int32_t* __restric
   float y = 0.f;
   for (int s = 0; s < ns; ++s) y += __ldcs(part + (int64_t)(s0 + s) * P + c);
   const int a = c / Jl, b = c - a * Jl;
-  const int64_t col = a * sa + b * sb;
+  const int64_t col = (a0 + a) * sa + (b0 + b) * sb;
   const int64_t off = transposed ? col * ldY + i : (int64_t)i * ldY + col;
   split_store(Yhi, Ylo, off, y);
 }
@@ -1061,10 +1064,25 @@ void spttmc_hooi(const Csf& c, const float* const* U, const int64_t* J, Split ou
     // 42 ms, 0.28 vs 0.31 ms).  TUCKER_TTMC=tc|simt forces one (tests).
     const char* fe = std::getenv("TUCKER_TTMC");
     const int force = !fe ? 0 : (std::strcmp(fe, "tc") == 0 ? 1 : (std::strcmp(fe, "simt") == 0 ? -1 : 0));
-    const bool use_tc = a.Jm <= 128 && a.Jl <= 128 &&
-                        (force == 1 || (force == 0 && (int64_t)a.Jm * a.Jl >= 8192));
-    if (use_tc) {
+    a.ldm = a.Jm;
+    a.ldl = a.Jl;
+    a.a0 = a.b0 = 0;
+    const bool wide = a.Jm > 128 || a.Jl > 128;  // tcgen05 in 128 x 128 column windows
+    const bool use_tc = wide || (force == 1 || (force == 0 && (int64_t)a.Jm * a.Jl >= 8192));
+    const int Jm_full = a.Jm, Jl_full = a.Jl;
+    const float* Umid_full = a.Umid;
+    const float* Uleaf_full = a.Uleaf;
+    for (int a0 = 0; use_tc && a0 < Jm_full; a0 += 128)
+     for (int b0 = 0; b0 < Jl_full; b0 += 128) {
+      a.a0 = a0;
+      a.b0 = b0;
+      a.Jm = std::min(128, Jm_full - a0);
+      a.Jl = std::min(128, Jl_full - b0);
+      a.Umid = Umid_full + a0;
+      a.Uleaf = Uleaf_full + b0;
+      launched = false;
       const int NA = (a.Jl + 31) / 32;
+      const int VW = (Jl_full % 4 == 0 && b0 % 4 == 0) ? 4 : (Jl_full % 2 == 0 ? 2 : 1);
 #define TK_TC(na, vw)                                                                          \
   if (!launched && NA == na && VW == vw) {                                                     \
     smem_optin((const void*)k_spttmc3_tc<na, vw>, TcTile<na>::SMEM);                          \
@@ -1074,6 +1092,19 @@ void spttmc_hooi(const Csf& c, const float* const* U, const int64_t* J, Split ou
       TK_TC(1, 1) TK_TC(1, 2) TK_TC(1, 4) TK_TC(2, 1) TK_TC(2, 2) TK_TC(2, 4)
       TK_TC(3, 1) TK_TC(3, 2) TK_TC(3, 4) TK_TC(4, 1) TK_TC(4, 2) TK_TC(4, 4)
 #undef TK_TC
+      if (!launched) fail(TUCKER_E_ARG, "spttmc: no tcgen05 instance for this core size");
+      if (c.nred > 0) {  // split slices: this window's partial tiles, summed in slot order
+        const dim3 gr((unsigned)ceil_div((int64_t)a.Jm * a.Jl, 256), (unsigned)c.nred);
+        TK_LAUNCH(k_spttmc3_reduce, gr, 256, 0, st, c.red.p, c.part.p, a.Jm, a.Jl, a.sa, a.sb, a.Yhi, a.Ylo, ldY,
+                  (int)transposed, a0, b0);
+      }
+    }
+    if (use_tc) {
+      a.a0 = a.b0 = 0;
+      a.Jm = Jm_full;
+      a.Jl = Jl_full;
+      a.Umid = Umid_full;
+      a.Uleaf = Uleaf_full;
     }
 #define TK_S3V(ra, rb, vw) \
   if (VW == vw) TK_LAUNCH((k_spttmc3<ra, rb, vw>), g, 256, 0, st, a);
@@ -1087,10 +1118,10 @@ void spttmc_hooi(const Csf& c, const float* const* U, const int64_t* J, Split ou
 #undef TK_S3
 #undef TK_S3V
     if (!launched) fail(TUCKER_E_ARG, "spttmc: unsupported core size");
-    if (c.nred > 0) {
+    if (c.nred > 0 && !use_tc) {
       const dim3 gr((unsigned)ceil_div((int64_t)a.Jm * a.Jl, 256), (unsigned)c.nred);
       TK_LAUNCH(k_spttmc3_reduce, gr, 256, 0, st, c.red.p, c.part.p, a.Jm, a.Jl, a.sa, a.sb, a.Yhi,
-                a.Ylo, ldY, (int)transposed);
+                a.Ylo, ldY, (int)transposed, 0, 0);
     }
     return;
   }

@@ -320,7 +320,7 @@ void solve_eig(tucker_handle* h, int64_t d, int J, EigSlot& slot, const float* h
     eig_small(h->S.p, d, ls, J, h->V.p, h->theta_d.p, h->info_d.p + 16 * rec, h->eig.small, h->st);
     return;
   }
-  if (d > kFusedMaxD || force_large) {  // MP's M_n at config 5 (d = 50000): the host-driven variant
+  if (d > kFusedMaxD || force_large || J > kMaxJFused) {  // config 5 MP (d = 50000), J > 112: host-driven
     int64_t ls = 0, rows = 0;
     eig_layout(d, &ls, &rows);
     eig_large(h->S.p, d, ls, J, slot, h->eig, eig_opts(h), h->V.p, h->theta_d.p, h->info_d.p + 16 * rec, h->st, hint);
@@ -527,7 +527,7 @@ double core_from_y(tucker_handle* h) {
 
 double compute_core(tucker_handle* h) {
   const int n = h->order - 1;
-  const bool tr = prod_J_except(h, n) < h->dims[n];
+  const bool tr = prod_J_except(h, n) < h->dims[n] && h->J[n] <= kMaxBlock;
   project_hooi(h, n, tr);
   return core_from_y(h);
 }
@@ -839,7 +839,8 @@ int hooi_sweep(tucker_handle* h, int sweeps, double* fit_per_sweep, float* stage
     SweepEvents ev(4 * N + 2);
     for (int s = 0; s < sweeps; ++s) {
       for (int n = 0; n < N; ++n) {
-        const bool tr = prod_J_except(h, n) < h->dims[n];  // Y^T Y is the smaller Gram
+        // Y^T Y is the smaller Gram; its back-transform's CholQR2 handles J_n <= kMaxBlock
+        const bool tr = prod_J_except(h, n) < h->dims[n] && h->J[n] <= kMaxBlock;
         TK_CUDA(cudaEventRecord(ev.e[4 * n], h->st));
         project_hooi(h, n, tr);
         TK_CUDA(cudaEventRecord(ev.e[4 * n + 1], h->st));
@@ -1163,7 +1164,7 @@ int tucker_debug_product_time(int d, int n, int reps, double* us) {
 int tucker_time_ttmc(tucker_handle* h, int mode, int reps, float* ms_out) {
   if (!h || !ms_out || mode < 0 || mode >= h->order || reps < 1) return TUCKER_E_ARG;
   return guarded(h, [&]() -> int {
-    const bool tr = prod_J_except(h, mode) < h->dims[mode];
+    const bool tr = prod_J_except(h, mode) < h->dims[mode] && h->J[mode] <= kMaxBlock;
     project_hooi(h, mode, tr);  // untimed: buffers, first-touch
     SweepEvents ev(2);
     TK_CUDA(cudaEventRecord(ev.e[0], h->st));

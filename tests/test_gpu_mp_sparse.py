@@ -127,3 +127,46 @@ def test_large_eigensolver_parity(capi, monkeypatch, d, J, gap):
     assert rc == 0
     assert O.projector_distance(U, Uo) < 1e-5
     np.testing.assert_allclose(ev, wo[:J], rtol=1e-9)
+
+
+def test_core_sizes_above_112(capi):
+    """J_n > 112 (the paper's Table 2 cores go to 200^3): the host-driven eigensolver with
+    the Rayleigh-Ritz problem on the direct dense solver and SVQB orthonormalisation
+    (k > 116), and the tcgen05 SpTTMc in 128-column windows (J_mid, J_leaf > 128).
+    HOOI and MP sweeps vs the oracle."""
+    from oracle import tucker_oracle as O
+    dims, nnz, core = (260, 250, 240), 300_000, (130, 125, 120)
+    idx, vals, U0 = case(dims, nnz, core, seed=23, fseed=24)
+    T = O.SparseTensor(dims, idx, vals)
+    with capi.Tucker(dims, core, idx, vals, U0) as t:
+        for n in range(3):
+            assert O.rel_frobenius(t.debug_ttmc(n), O.ttm_chain_unfold(T, U0, n)) < 1e-4, n
+        fh = t.hooi_sweep(2)
+        _, Uh, _ = t.core_and_fit()
+        t.set_factors(U0)
+        fm = t.mp_sweep(2)
+        _, Um, _ = t.core_and_fit()
+    rh, rm = O.run_hooi(T, U0, core, 2), O.run_mp(T, U0, core, 2)
+    np.testing.assert_allclose(fh, rh["fits"], atol=1e-5)
+    np.testing.assert_allclose(fm, rm["fits"], atol=1e-5)
+    for n in range(3):
+        assert O.projector_distance(Uh[n], rh["U"][n]) < 1e-4, ("hooi", n)
+        assert O.projector_distance(Um[n], rm["U"][n]) < 1e-4, ("mp", n)
+
+
+@pytest.mark.parametrize("d,J", [(500, 150), (1200, 200)])
+def test_eig_wide_block(capi, d, J):
+    rng = np.random.default_rng(d + J)
+    Q = np.linalg.qr(rng.standard_normal((d, d)))[0]
+    w = np.sort(rng.uniform(0.1, 1.0, d))[::-1].copy()
+    w[0] = 80.0
+    w[:J] += 0.3
+    S = (Q * w) @ Q.T
+    dims, core = (8, 8, 8), (2, 2, 2)
+    idx, vals, U0 = case(dims, 50, core)
+    with capi.Tucker(dims, core, idx, vals, U0) as t:
+        U, ev, rc = t.debug_eig(S, J)
+    Uo, wo = O.leading_eigenvectors(S, J)
+    assert rc == 0
+    assert O.projector_distance(U, Uo) < 1e-5
+    np.testing.assert_allclose(ev, wo[:J], rtol=1e-9)

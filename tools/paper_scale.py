@@ -23,8 +23,10 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 g = json.load(open(os.path.join(ROOT, "tests", "golden", "paper_fits.json")))
 PAPER_TIME = {500: {"hosvd": "00:03:44", "hooi": "00:09:52", "sp": "00:10:21", "mp": "00:13:55"},
               750: {"hosvd": "00:14:42", "hooi": "00:42:45", "sp": "00:34:39", "mp": "00:51:33"},
-              1000: {"hosvd": "01:10:13", "hooi": "04:01:36", "sp": "01:43:20", "mp": "02:21:30"}}
-sizes = [int(a) for a in sys.argv[1:]] or [500, 750, 1000]
+              1000: {"hosvd": "01:10:13", "hooi": "04:01:36", "sp": "01:43:20", "mp": "02:21:30"},
+              1250: {"sp": "03:16:32", "mp": "05:05:11"}, 1500: {"sp": "06:01:47", "mp": "09:28:49"},
+              1750: {"sp": "09:58:36", "mp": "16:14:01"}, 2000: {"sp": "15:35:21", "mp": "25:43:17"}}
+sizes = [int(a) for a in sys.argv[1:]] or [500, 750, 1000, 1250, 1500, 1750, 2000]
 for I in sizes:
     case = g[f"table2_{I}cube_J{I // 10}"]
     dims, core = tuple(case["dims"]), tuple(case["core"])
@@ -32,9 +34,12 @@ for I in sizes:
     idx, vals = bernoulli_coo_slabs(dims, case["density"], seed=I)
     gen_s = time.time() - t0
     U0 = [random_orthonormal(n, j, np.random.default_rng(60 + k)) for k, (n, j) in enumerate(zip(dims, core))]
+    algos = [a for a in ("hosvd", "hooi", "sp", "mp") if a in case] + (["hooi"] if I > 1000 else [])
     out = {"workload": f"PAPER Table 2: {I}^3, density 0.1, core {I // 10}^3", "nnz": int(vals.size),
-           "gen_s": gen_s, "paper_fit_pct": {k: case[k] for k in ("hosvd", "hooi", "sp", "mp")},
-           "paper_time": PAPER_TIME.get(I)}
+           "gen_s": gen_s, "paper_fit_pct": {k: case[k] for k in ("hosvd", "hooi", "sp", "mp") if k in case},
+           "paper_time": PAPER_TIME.get(I),
+           "note": "HOOI beyond 1000^3 is not in the paper (MATLAB ran out of RAM, P:1233-1241): reported only"
+                   if I > 1000 else ""}
     rest = range(1, 3)
 
     def run(algo):
@@ -56,8 +61,8 @@ for I in sizes:
             h.close()
         return 100 * fit, n, time.time() - t0
 
-    for algo in ("hosvd", "hooi", "sp", "mp"):
+    for algo in algos:
         fit, n, s = run(algo)
         out[algo] = {"fit_pct": round(fit, 4), "sweeps": n, "seconds": round(s, 3),
-                     "delta_pp": round(fit - case[algo], 4)}
+                     "delta_pp": round(fit - case[algo], 4) if algo in case else None}
     print(json.dumps(out), flush=True)
