@@ -911,50 +911,21 @@ __global__ void __launch_bounds__(32 * kSpW, 6) k_spmm_w(SpmmArgs p) {
     }
     return m;
   };
-  // a batch's nonzeros [E0, E1) (contiguous in the CSF) in registers, 4 per lane, coalesced
-  struct Nz {
-    int E0, E1;
-    int l[kSpNz / 32];
-    float v[kSpNz / 32];
-  };
-  auto load_nz = [&](const Meta& m) {
-    Nz z;
-    const unsigned bal = __ballot_sync(full, m.e0 >= 0);
-    const int last = bal ? __popc(bal) - 1 : 0;
-    z.E0 = __shfl_sync(full, m.e0, 0);
-    z.E1 = bal ? __shfl_sync(full, m.e1, last) : z.E0;
-    const bool st4 = z.E1 - z.E0 <= kSpNz;
-#pragma unroll
-    for (int j = 0; j < kSpNz / 32; ++j) {
-      const int e = z.E0 + lane + 32 * j;
-      const bool in = st4 && e < z.E1;
-      z.l[j] = in ? __ldg(p.leaf_id + e) : 0;
-      z.v[j] = in ? __ldg(p.val + e) : 0.f;
-    }
-    return z;
-  };
-  // pipeline: fiber metadata two batches ahead, nonzeros one batch ahead (both in registers)
   int64_t base = (blockIdx.x * kSpW + warp) * 32LL;
-  Meta cur = load_meta(base);
-  Nz zc = load_nz(cur);
-  Meta nxt = load_meta(base + nwarps * 32);
+  Meta nx = load_meta(base);
   for (; base < p.nfib; base += nwarps * 32) {
-    const Meta cm = cur;
-    const int E0 = zc.E0, E1 = zc.E1;
-    const bool staged = E1 - E0 <= kSpNz;
-#pragma unroll
-    for (int j = 0; j < kSpNz / 32; ++j) {
-      const int e = E0 + lane + 32 * j;
-      if (staged && e < E1) {
-        snz_l[warp][e - E0] = zc.l[j];
-        snz_v[warp][e - E0] = zc.v[j];
-      }
-    }
-    // next batch's nonzeros and the batch after's metadata: in flight during this batch
-    cur = nxt;
-    zc = load_nz(cur);
-    nxt = load_meta(base + 2 * nwarps * 32);
+    const Meta cm = nx;
+    nx = load_meta(base + nwarps * 32);  // in flight during this batch
     bool ok = cm.e0 >= 0 && !(sharded && (cm.mk < p.s_lo || cm.mk >= p.s_hi));
+    // the batch's nonzeros [E0, E1) (contiguous in the CSF) staged with coalesced loads
+    const int last = __popc(__ballot_sync(full, cm.e0 >= 0)) - 1;
+    const int E0 = __shfl_sync(full, cm.e0, 0), E1 = __shfl_sync(full, cm.e1, last);
+    const bool staged = E1 - E0 <= kSpNz;
+    if (staged)
+      for (int e = E0 + lane; e < E1; e += 32) {
+        snz_l[warp][e - E0] = __ldg(p.leaf_id + e);
+        snz_v[warp][e - E0] = __ldg(p.val + e);
+      }
     const int e0 = ok ? cm.e0 : 0, e1 = ok ? cm.e1 : 0;
     const int64_t c0 = p.col_off + (cm.mk - p.s_lo) * p.J;
     srow[warp][lane] = ok ? cm.root : -1;
