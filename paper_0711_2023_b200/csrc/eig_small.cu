@@ -20,6 +20,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 
 #include "internal.cuh"
 
@@ -350,11 +351,475 @@ __global__ void __launch_bounds__(256) k_tri_eig(const double* __restrict__ a, c
   }
 }
 
+
+// ---------------------------------------------------------------------------
+// k_eig_direct: the whole direct solve in ONE CTA of 1024 threads for n small
+// enough that the packed lower triangle of S (n (n + 1) / 2 doubles; n = 200:
+// 161 KB) fits in shared memory -- no cluster barriers, no DSMEM, no global
+// round trips inside the sequential parts (the 4-CTA path above measured ~4 ms
+// at n = 200, dominated by those).  Phases:
+//   1. Householder tridiagonalisation Q^T S Q = T on the packed triangle: per
+//      column k two block barriers; lane l owns the indices j = l + 32 m (its u_j
+//      and q_j live in registers), warp w the rows i = k + 1 + w + 32 r; the
+//      symmetric product p = beta S u reads the row part (j <= i) and the column
+//      part (j > i) of the packed storage, the rank-2 update S -= u q^T + q u^T
+//      rewrites the row part; the lane that owns j = k + 1 also emits the next
+//      column (and its norm) so it is ready after the barrier.  The reflectors
+//      go to global memory (rows of H) for phase 4.
+//   2. Eigenvalues m largest of T (scaled by its Gershgorin bound) by
+//      multisection: a warp per eigenvalue, 32 points per round (11 rounds:
+//      33^-11 ~ 2e-17 of the interval), Sturm counts by the division-free
+//      three-term recurrence of the leading principal minors (sign changes;
+//      rescaled when they leave [1e-150, 1e150]).
+//   3. Eigenvectors by inverse iteration (one thread per vector, pivoted LU of
+//      T - lambda I in shared memory, 3 iterations; a tiny shift per vector and
+//      a fixed pseudo-random start separate equal eigenvalues), modified
+//      Gram-Schmidt (twice) among eigenvalues closer than 1e-9 ||T||.
+//   4. Back-transformation V = H_0 .. H_{n-3} Y, a warp per vector.
+// ---------------------------------------------------------------------------
+constexpr int kDT = 1024;
+constexpr int kDW = kDT / 32;
+constexpr int kDJ = 7;  // indices per lane: n <= 224
+
+struct DirArgs {
+  const double* S;
+  int64_t lds;
+  int n, m;
+  int ws;       // doubles of dynamic shared memory
+  double* H;    // n x n: row k = reflector u_k (entries k + 1 .. n - 1)
+  double* V;    // n x m, ld m
+  double* theta;
+  int* info;
+};
+
+__device__ __forceinline__ int pidx(int i, int j) { return (i * (i + 1)) / 2 + j; }
+__device__ __forceinline__ double wsum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+__global__ void __launch_bounds__(kDT, 1) k_eig_direct(DirArgs p) {
+  extern __shared__ double sm[];
+  __shared__ double npart[kDW], kpart[kDW];
+  __shared__ double lam[256];
+  __shared__ double red[kDW];
+  const int n = p.n, m = p.m, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  // layout: ub[2][n] | pr[n] | uv[n] | sa[n] | se[n] | te2[n] | pb[1024] (product partials) | L (packed; later the workspace)
+  double* ub = sm;
+  double* pr = ub + 2 * n;
+  double* uv = pr + n;  // u of the current step (u1 at k1)
+  double* sa = uv + n;
+  double* se = sa + n;
+  double* te2 = se + n;
+  double* pb = te2 + n;
+  double* L = pb + 1024;
+  const int wsz = p.ws - 7 * n - 1024;  // doubles from L on
+
+  for (int i = warp; i < n; i += kDW)
+    for (int j = lane; j <= i; j += 32) L[pidx(i, j)] = p.S[(int64_t)i * p.lds + j];
+  __syncthreads();
+  if (n >= 3) {  // first column (k = 0) and its norm
+    double ss = 0.0;
+    for (int i = 1 + warp; i < n; i += kDW) {
+      if (lane == 0) {
+        const double x = L[pidx(i, 0)];
+        ub[i] = x;
+        ss += x * x;
+      }
+    }
+    if (lane == 0) npart[warp] = ss;
+  }
+  __syncthreads();
+  // ---- 1. tridiagonalisation.  Per column k (active indices k1 = k + 1 .. n - 1), three phases
+  // and three block barriers; x = S[k1.., k] (the column, kept in ub by the previous step):
+  //   P  p~ = S_sub x: lanes = rows (32-row blocks), warps = (row block, column segment), partial
+  //      sums per segment (no scalar is needed: S u = S x - alpha S e_k1 is fixed up in R)
+  //   R  threads = rows: the reflector (alpha, beta, u), p = beta (p~ - alpha S[:, k1]), K partials
+  //   U  S_sub -= u q^T + q u^T, q = p - K u (lanes = columns); the owner of column k1 emits the
+  //      next step's x and its norm
+  __shared__ double scal[2];
+  for (int k = 0; k < n - 2; ++k) {
+    const double* x = ub + (k & 1) * n;
+    double* xn = ub + ((k + 1) & 1) * n;
+    const int k1 = k + 1, na = n - k1;
+    const int nrb = (na + 31) >> 5;
+    // column segments per row block: a power of two, <= 32 / nrb warps in all, and >= ~16 columns
+    // each (short steps use few warps: the per-warp setup would dominate)
+    int lg = nrb == 1 ? 5 : (nrb == 2 ? 4 : (nrb <= 4 ? 3 : 2));
+    while (lg > 0 && (na >> lg) < 16) --lg;
+    const int nseg = 1 << lg;
+    {  // P
+      const int SL = (na + nseg - 1) >> lg;
+      const int rbk = warp >> lg, sg = warp & (nseg - 1);
+      if (rbk < nrb) {
+        const int i0 = k1 + 32 * rbk + lane;
+        const int i = min(i0, n - 1);  // lanes past the last row read row n - 1, discarded
+        const int ti = (i * (i + 1)) / 2;
+        const int jb = k1 + sg * SL, je = min(n, jb + SL);
+        const int rlo = k1 + 32 * rbk;
+        double acc0 = 0.0, acc1 = 0.0;
+        int j = jb;
+        const int e1 = min(je, rlo);  // row part: j < rlo <= i
+        for (; j + 1 < e1; j += 2) {
+          const double2 xx = make_double2(x[j], x[j + 1]);
+          acc0 = fma(L[ti + j], xx.x, acc0);
+          acc1 = fma(L[ti + j + 1], xx.y, acc1);
+        }
+        for (; j < e1; ++j) acc0 = fma(L[ti + j], x[j], acc0);
+        const int e2 = min(je, rlo + 32);  // the diagonal band
+        for (; j < e2; ++j) acc0 = fma(j <= i ? L[ti + j] : L[(j * (j + 1)) / 2 + i], x[j], acc0);
+        int tj = (j * (j + 1)) / 2;  // column part: j > i
+        for (; j + 1 < je; j += 2) {
+          const int tj1 = tj + j + 1;
+          acc0 = fma(L[tj + i], x[j], acc0);
+          acc1 = fma(L[tj1 + i], x[j + 1], acc1);
+          tj = tj1 + j + 2;
+        }
+        for (; j < je; ++j) {
+          acc0 = fma(L[tj + i], x[j], acc0);
+          tj += j + 1;
+        }
+        if (i0 < n) pb[sg * (32 * nrb) + (i0 - k1)] = acc0 + acc1;
+      }
+    }
+    __syncthreads();
+    if (warp < nrb) {  // R
+      const double nx2 = wsum(npart[lane]);
+      const double x0 = x[k1];
+      const double nx = sqrt(nx2);
+      const double alpha = x0 >= 0 ? -nx : nx;
+      const double uu = 2.0 * (nx2 - alpha * x0);
+      const double beta = uu > 0 ? 2.0 / uu : 0.0;
+      const double u1 = x0 - alpha;
+      const int i = k1 + tid;
+      double kp = 0.0;
+      if (i < n) {
+        double s2 = 0.0;
+        for (int g = 0; g < nseg; ++g) s2 += pb[g * (32 * nrb) + tid];
+        const double pi = beta * fma(-alpha, L[pidx(i, k1)], s2);
+        const double ui = i == k1 ? u1 : x[i];
+        pr[i] = pi;
+        uv[i] = ui;
+        kp = pi * ui;
+        p.H[(int64_t)k * n + i] = ui;
+      }
+      kp = wsum(kp);
+      if (lane == 0) kpart[warp] = kp;
+      if (tid == 0) {
+        scal[0] = beta;
+        scal[1] = u1;
+        sa[k] = L[pidx(k, k)];
+        se[k] = alpha;
+        p.H[(int64_t)k * n + k] = beta;
+      }
+    } else if (lane == 0) {
+      kpart[warp] = 0.0;
+    }
+    __syncthreads();
+    {  // U: lanes = rows i (32-row blocks); the (row block, j <= i) pairs of the lower triangle
+       // are split evenly over the warps (block rbk holds 32 (rbk + 1) columns of pairs)
+      const double K = 0.5 * scal[0] * wsum(kpart[lane]);
+      const int C = 16 * nrb * (nrb + 1);            // total (block, column) pairs
+      const int WU = max(1, min(kDW, C >> 4));        // >= 16 columns of pairs per warp
+      const int c0 = warp < WU ? (warp * C) / WU : C, c1 = warp < WU ? ((warp + 1) * C) / WU : C;
+      double ss = 0.0;
+      int rbk = 0;
+      while (16 * (rbk + 1) * (rbk + 2) <= c0) ++rbk;  // block holding pair c0
+      for (int c = c0; c < c1; ++rbk) {
+        const int cb = 16 * rbk * (rbk + 1);          // first pair of block rbk
+        const int rlo = k1 + 32 * rbk;
+        const int jb = k1 + (c - cb), je = min(k1 + (min(c1, cb + 32 * (rbk + 1)) - cb), n);
+        c = min(c1, cb + 32 * (rbk + 1));
+        const int i0 = rlo + lane;
+        const bool iv = i0 < n;
+        const int i = min(i0, n - 1);
+        const int ti = (i * (i + 1)) / 2;
+        const double ui = uv[i];
+        const double qi = fma(-K, ui, pr[i]);
+        int j = jb;
+        if (j == k1 && j < je) {  // column k1 below the diagonal: the next step's x
+          const double uj = uv[j], qj = fma(-K, uj, pr[j]);
+          const double v = fma(-ui, qj, fma(-qi, uj, L[ti + j]));
+          if (iv) {
+            L[ti + j] = v;
+            if (i > k1) {
+              xn[i] = v;
+              ss = fma(v, v, ss);
+            }
+          }
+          ++j;
+        }
+        const int e1 = min(je, rlo);  // j < rlo <= i: every valid lane
+        for (; j + 1 < e1; j += 2) {
+          const double2 u2 = make_double2(uv[j], uv[j + 1]);
+          const double2 p2 = make_double2(pr[j], pr[j + 1]);
+          const double q0 = fma(-K, u2.x, p2.x), q1 = fma(-K, u2.y, p2.y);
+          const double v0 = fma(-ui, q0, fma(-qi, u2.x, L[ti + j]));
+          const double v1 = fma(-ui, q1, fma(-qi, u2.y, L[ti + j + 1]));
+          if (iv) {
+            L[ti + j] = v0;
+            L[ti + j + 1] = v1;
+          }
+        }
+        for (; j < je; ++j) {  // the rest, including the diagonal band (j <= i per lane)
+          const double uj = uv[j], qj = fma(-K, uj, pr[j]);
+          if (iv && j <= i) L[ti + j] = fma(-ui, qj, fma(-qi, uj, L[ti + j]));
+        }
+      }
+      ss = wsum(ss);
+      if (lane == 0) npart[warp] = ss;
+    }
+    __syncthreads();
+  }
+  if (tid == 0) {
+    for (int i = max(0, n - 2); i < n; ++i) sa[i] = L[pidx(i, i)];
+    if (n >= 2) se[n - 2] = L[pidx(n - 1, n - 2)];
+    se[n - 1] = 0.0;
+  }
+  for (int k = max(0, n - 2) + tid / 256; k < n; k += kDT / 256)  // no reflector for the last two columns
+    for (int i = tid % 256; i < n; i += 256) p.H[(int64_t)k * n + i] = 0.0;
+  __syncthreads();
+  // ---- 2. eigenvalues: scale T by its Gershgorin bound tn
+  double tn = 0.0;
+  for (int i = 0; i < n; ++i) tn = fmax(tn, fabs(sa[i]) + (i > 0 ? fabs(se[i - 1]) : 0.0) + (i < n - 1 ? fabs(se[i]) : 0.0));
+  const double sc = tn > 0 ? 1.0 / tn : 1.0;
+  __syncthreads();
+  for (int i = tid; i < n; i += kDT) {
+    sa[i] *= sc;
+    se[i] *= sc;
+    te2[i] = se[i] * se[i];
+  }
+  __syncthreads();
+  for (int j = warp; j < m; j += kDW) {
+    const int kth = n - 1 - j;  // the (n - 1 - j)-th smallest
+    double l = -1.0 - 1e-12, h = 1.0 + 1e-12;
+    for (int it = 0; it < 11; ++it) {
+      const double x = l + (h - l) * (double)(lane + 1) / 33.0;
+      // sign changes of the leading minors p_0 = 1, p_1 = a_0 - x, p_i = (a_{i-1} - x) p_{i-1} - e_{i-2}^2 p_{i-2}
+      // (T is scaled to ||T|| <= 1, so |p| grows by <= 3 per step: rescaled every 8 steps when it
+      // leaves [1e-100, 1e100]; an exact zero minor counts as a sign change, like a -0 pivot)
+      int cnt = 0;
+      double pm = 1.0, pc = sa[0] - x;
+      bool neg = pc <= 0.0;  // p_0 = 1 > 0; a zero p_1 counts as negative
+      cnt += neg;
+      int i = 1;
+      for (; i + 8 <= n; i += 8) {
+#pragma unroll
+        for (int r = 0; r < 8; ++r) {
+          const double pn = fma(sa[i + r] - x, pc, -te2[i + r - 1] * pm);
+          // sign of a zero minor: opposite to its predecessor's (a -0 pivot); kept off the chain
+          const bool ng = pn == 0.0 ? !neg : pn < 0.0;
+          cnt += ng != neg;
+          neg = ng;
+          pm = pc;
+          pc = pn;
+        }
+        const double an = fabs(pc);
+        if (an > 1e100 || an < 1e-100) {
+          const double f = an > 1e100 ? 1e-100 : 1e100;
+          pc *= f;
+          pm *= f;
+        }
+      }
+      for (; i < n; ++i) {
+        const double pn = fma(sa[i] - x, pc, -te2[i - 1] * pm);
+        const bool ng = pn == 0.0 ? !neg : pn < 0.0;
+        cnt += ng != neg;
+        neg = ng;
+        pm = pc;
+        pc = pn;
+      }
+      const unsigned below = __ballot_sync(0xffffffffu, cnt <= kth);
+      const int nb = __popc(below);  // points 0 .. nb - 1 lie at or left of the target
+      const double nl = nb > 0 ? l + (h - l) * (double)nb / 33.0 : l;
+      const double nh = l + (h - l) * (double)(nb + 1) / 33.0;
+      l = nl;
+      h = nh;
+    }
+    if (lane == 0) lam[j] = 0.5 * (l + h);
+  }
+  __syncthreads();
+  // ---- 3. inverse iteration; workspace: Y [n][m] | per round R vectors x (dl, dd, du, du2) [n][R] | pv bytes [n][R]
+  double* Y = L;
+  const int R = max(1, min(m, (int)((wsz - n * m) / (4 * n + (n + 7) / 8 + 1))));
+  double* dl = Y + n * m;
+  double* dd = dl + n * R;
+  double* du = dd + n * R;
+  double* du2 = du + n * R;
+  unsigned char* pv = reinterpret_cast<unsigned char*>(du2 + n * R);
+  const double eps = 2.2e-16;
+  for (int j0 = 0; j0 < m; j0 += R) {
+    const int t = tid;
+    const int j = j0 + t;
+    if (t < R && j < m) {
+      const double shift = lam[j] + eps * (1.0 + 0.25 * (j & 7));
+#define AT(a, i) a[(i) * R + t]
+      // pivoted LU of T - shift I (LAPACK dgttrf's elimination), the current row carried in registers
+      double cd = sa[0] - shift, cu = n > 1 ? se[0] : 0.0;
+      for (int i = 0; i < n - 1; ++i) {
+        const double li = se[i], nd = sa[i + 1] - shift, nu = i + 1 < n - 1 ? se[i + 1] : 0.0;
+        if (fabs(cd) >= fabs(li)) {
+          const double dv = cd == 0.0 ? eps : cd;
+          const double f = li / dv;
+          AT(dl, i) = f;
+          AT(dd, i) = 1.0 / dv;
+          AT(du, i) = cu;
+          AT(du2, i) = 0.0;
+          pv[i * R + t] = 0;
+          cd = fma(-f, cu, nd);
+          cu = nu;
+        } else {
+          const double f = cd / li;
+          AT(dl, i) = f;
+          AT(dd, i) = 1.0 / li;
+          AT(du, i) = nd;
+          AT(du2, i) = nu;
+          pv[i * R + t] = 1;
+          cd = fma(-f, nd, cu);
+          cu = -f * nu;
+        }
+      }
+      AT(dd, n - 1) = 1.0 / (cd == 0.0 ? eps : cd);
+      // start vector: fixed pseudo-random, in [0.5, 1)
+      for (int i = 0; i < n; ++i) {
+        uint64_t z = (uint64_t)(i + 1) * 0x9E3779B97F4A7C15ull ^ (uint64_t)(j + 7) * 0xBF58476D1CE4E5B9ull;
+        z ^= z >> 31;
+        Y[i * m + j] = 0.5 + (double)(z >> 11) * (1.0 / 9007199254740992.0);
+      }
+      for (int it = 0; it < 2; ++it) {
+        double cy = Y[j];  // forward: L (row swaps as recorded)
+        for (int i = 0; i < n - 1; ++i) {
+          const double ny = Y[(i + 1) * m + j], f = AT(dl, i);
+          if (!pv[i * R + t]) {
+            Y[i * m + j] = cy;
+            cy = fma(-f, cy, ny);
+          } else {
+            Y[i * m + j] = ny;
+            cy = fma(-f, ny, cy);
+          }
+        }
+        // backward: U (reciprocal pivots), y_{i+1}, y_{i+2} carried
+        double y1 = cy * AT(dd, n - 1), y2 = 0.0;
+        Y[(n - 1) * m + j] = y1;
+        double ssq = y1 * y1;
+        for (int i = n - 2; i >= 0; --i) {
+          const double yi = (Y[i * m + j] - AT(du, i) * y1 - AT(du2, i) * y2) * AT(dd, i);
+          Y[i * m + j] = yi;
+          ssq = fma(yi, yi, ssq);
+          y2 = y1;
+          y1 = yi;
+        }
+        const double sN = 1.0 / sqrt(ssq);
+        for (int i = 0; i < n; ++i) Y[i * m + j] *= sN;
+      }
+#undef AT
+    }
+    __syncthreads();
+  }
+  // modified Gram-Schmidt among close eigenvalues (twice)
+  auto csum = [&](double v) {
+    v = wsum(v);
+    if (lane == 0) red[warp] = v;
+    __syncthreads();
+    const double s = wsum(red[lane]);
+    __syncthreads();
+    return s;
+  };
+  for (int j = 1; j < m; ++j) {
+    int i0 = j;
+    while (i0 > 0 && lam[i0 - 1] - lam[i0] <= 1e-9) --i0;
+    if (i0 == j) continue;
+    for (int pass = 0; pass < 2; ++pass) {
+      for (int i = i0; i < j; ++i) {
+        double s = 0.0;
+        for (int r = tid; r < n; r += kDT) s = fma(Y[r * m + i], Y[r * m + j], s);
+        s = csum(s);
+        for (int r = tid; r < n; r += kDT) Y[r * m + j] -= s * Y[r * m + i];
+        __syncthreads();
+      }
+      double s = 0.0;
+      for (int r = tid; r < n; r += kDT) s = fma(Y[r * m + j], Y[r * m + j], s);
+      s = 1.0 / sqrt(csum(s));
+      for (int r = tid; r < n; r += kDT) Y[r * m + j] *= s;
+      __syncthreads();
+    }
+  }
+  // ---- 4. back-transformation, a warp per vector (Yt: [m][n] copy, conflict-free lanes)
+  double* Yt = dl;  // the inverse-iteration arrays are free now (n m <= 4 n R + ... checked on the host)
+  for (int e = tid; e < n * m; e += kDT) {
+    const int jj = e / n, r = e - jj * n;
+    Yt[e] = Y[r * m + jj];
+  }
+  __syncthreads();
+  // reflector rows staged in shared memory in chunks of CH (the workspace past Y and Yt)
+  double* Hs = Yt + (size_t)n * m;
+  const int CH = max(1, min(n, (int)((wsz - 2 * n * m) / n)));
+  for (int k1 = n - 2; k1 > 0; k1 -= CH) {  // rows [k0, k1) of H, applied last to first
+    const int k0 = max(0, k1 - CH);
+    for (int e = tid; e < (k1 - k0) * n; e += kDT) Hs[e] = p.H[(int64_t)k0 * n + e];
+    __syncthreads();
+    for (int jj = warp; jj < m; jj += kDW) {
+      double* y = Yt + (size_t)jj * n;
+      for (int k = k1 - 1; k >= k0; --k) {
+        const double* uk = Hs + (size_t)(k - k0) * n;
+        const double bk = uk[k];  // beta_k sits in the diagonal slot
+        if (bk == 0.0) continue;
+        double s = 0.0;
+        for (int r = k + 1 + lane; r < n; r += 32) s = fma(uk[r], y[r], s);
+        s = bk * wsum(s);
+        for (int r = k + 1 + lane; r < n; r += 32) y[r] -= s * uk[r];
+        __syncwarp();
+      }
+    }
+    __syncthreads();
+  }
+  for (int e = tid; e < n * m; e += kDT) {
+    const int r = e / m, jj = e - r * m;
+    p.V[e] = Yt[(size_t)jj * n + r];
+  }
+  for (int jj = tid; jj < m; jj += kDT) p.theta[jj] = lam[jj] * tn;
+  if (tid < 8) p.info[tid] = tid == 0 || tid == 1 ? 1 : 0;  // converged (direct method), 1 "iteration"
+  if (tid == 0) {
+    double* dv = reinterpret_cast<double*>(p.info + 8);
+    dv[0] = -1.0;  // no Lanczos / filter-bound estimates (eig_check keeps the slot's)
+    dv[1] = -1.0;
+  }
+}
+
 }  // namespace
+
+// shared memory (doubles) k_eig_direct needs for (n, m); 0: does not fit
+size_t eig_direct_ws(int n, int m) {
+  if (n < 3 || n > 32 * kDJ || m < 1 || m > n || m > 256) return 0;
+  const size_t np = (size_t)n * (n + 1) / 2;  // packed triangle
+  // workspace from L on: Y (n m) + R (4 n + n / 8 + 1) with R >= 1, and the transposed copy (n m)
+  size_t wsz = std::max(np, (size_t)n * m + (size_t)(4 * n + (n + 7) / 8 + 1) * std::min(m, 20));
+  wsz = std::max(wsz, (size_t)2 * n * m + 16 * (size_t)n);  // + reflector chunks of >= 16 rows
+  const size_t tot = 7 * (size_t)n + 1024 + wsz;
+  return tot * sizeof(double) <= 218 * 1024 ? tot : 0;  // + ~6 KB static shared memory <= 227 KB
+}
 
 void eig_small(const double* S, int64_t n, int64_t lds, int m, double* V, double* theta, int* info, DBuf<double>& scratch,
                cudaStream_t st) {
   if (n < 3 || n > kNMax || m < 1 || m > n) fail(TUCKER_E_ARG, "eig_small: 3 <= n <= 256, 1 <= m <= n");
+  const size_t ws = eig_direct_ws((int)n, m);
+  if (ws && !std::getenv("TUCKER_EIG_CLUSTER")) {  // one CTA, everything in shared memory
+    scratch.ensure((size_t)(n * n));
+    DirArgs a;
+    a.S = S;
+    a.lds = lds;
+    a.n = (int)n;
+    a.m = m;
+    a.ws = (int)ws;
+    a.H = scratch.p;
+    a.V = V;
+    a.theta = theta;
+    a.info = info;
+    smem_optin((const void*)k_eig_direct, ws * sizeof(double));
+    TK_LAUNCH(k_eig_direct, 1, kDT, ws * sizeof(double), st, a);
+    return;
+  }
   scratch.ensure((size_t)(3 * n + n * n + (size_t)m * n + (size_t)m * 5 * n));
   double* a = scratch.p;
   double* e = a + n;

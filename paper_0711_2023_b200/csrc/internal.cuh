@@ -4,6 +4,8 @@
 
 #include "common.cuh"
 
+#include <memory>
+
 namespace tk {
 
 constexpr int kMaxOrder = 4;
@@ -42,6 +44,17 @@ struct Csf {
   DBuf<int32_t> unit;  // 4 ints per unit: slice, vf0, vf1, slot (-1: write Y directly)
   DBuf<int32_t> red;   // 3 ints per split slice: slice, first slot, #slots
   DBuf<float> part;    // nslots x (J_mid * J_leaf) partial tiles
+  // order-4 GEMM-form SpTTMc (spttmc4g.cu): the ordering's "dense batch layout",
+  // built on first use (jlp = the leaf core size it was built for, 0: not built)
+  struct G4 {
+    int jlp = 0;
+    int64_t nbatch = 0;
+    DBuf<int4> batch;                  // (slice, first node, nodes, -)
+    DBuf<int32_t> bfirst, sp, leaf;    // first batch per slice; slot nonzero offsets; leaf ids in slot order
+    DBuf<float> val, part;             // values in slot order; run partial rows
+    std::vector<int32_t> bfirst_h;
+  };
+  std::unique_ptr<G4> g4 = std::make_unique<G4>();
 };
 
 struct Coo {  // validated, zero-free COO on the device
@@ -85,6 +98,9 @@ struct Split {
 // HOOI: Y_(n) (Kolda order) written as split fp32; transposed => out is Y_(n)^T.
 // Only the root slices [lo, hi) are computed (a rank's shard; hi < 0: all); the
 // other rows of out stay as they are (zero).
+// order-4 GEMM-form SpTTMc (spttmc4g.cu); false: not applicable (use k_spttmc4w)
+bool spttmc4g(const Csf& c, const float* const* U, const int64_t* J, Split out, bool transposed, int64_t s0,
+              int64_t s1, int64_t sb, cudaStream_t st, int64_t lo, int64_t hi);
 void spttmc_hooi(const Csf& c, const float* const* U, const int64_t* J, Split out, bool transposed,
                  cudaStream_t st, int64_t lo = 0, int64_t hi = -1);
 // MP: W columns [col_off, col_off + (s_hi - s_lo)*J_leaf) of the rows of out
@@ -190,6 +206,8 @@ constexpr int64_t kFusedMaxD = 8192;
 constexpr int64_t kSmallMaxD = 256;
 void eig_small(const double* S, int64_t n, int64_t lds, int m, double* V, double* theta, int* info, DBuf<double>& scratch,
                cudaStream_t st);
+// doubles of shared memory the one-CTA direct solver needs for (n, m); 0: it does not fit
+size_t eig_direct_ws(int n, int m);
 bool eig_large(const double* S, int64_t d, int64_t ls, int J, EigSlot& slot, EigWs& ws, const EigOpts& o,
                double* out_V, double* theta_dev, int* info_dev, cudaStream_t st, const float* hint = nullptr);
 // MP's multislice Gram without the dense W (mp_sparse.cu): M (fp64, upper triangle, row

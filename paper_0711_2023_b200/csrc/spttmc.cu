@@ -1146,6 +1146,9 @@ void spttmc_hooi(const Csf& c, const float* const* U, const int64_t* J, Split ou
   a.s0 = kolda_stride(c.mid0, others, no, J);
   a.s1 = kolda_stride(c.mid1, others, no, J);
   a.sb = kolda_stride(c.leaf, others, no, J);
+  if (!std::getenv("TUCKER_TTMC4_CS") && !std::getenv("TUCKER_TTMC4_GMEM") &&
+      spttmc4g(c, U, J, out, transposed, a.s0, a.s1, a.sb, st, lo, hi))
+    return;
   const int64_t P = (int64_t)a.J0 * a.J1 * a.Jl;
   a.slice0 = (int)lo;
   a.I_leaf = (int)c.I_leaf;

@@ -311,9 +311,19 @@ void solve_eig(tucker_handle* h, int64_t d, int J, EigSlot& slot, const float* h
   h->info_d.ensure(16 * (kMaxOrder + 1));  // per record: 8 ints + 4 doubles
   h->rec_slot[rec] = &slot;
   const bool force_large = std::getenv("TUCKER_EIG_LARGE") != nullptr;  // tests
-  // the direct dense solver (eig_small.cu) is correct but measured slower than the fused
-  // iterative solver at d = 200 (~4 ms vs 0.7-1.4 ms per solve): experiments only
-  const bool small = std::getenv("TUCKER_EIG_SMALL") != nullptr;
+  // the direct dense solver (eig_small.cu): by default where its one-CTA form fits
+  // (d <= 224, packed S in shared memory) and the iterative solver's options are at their
+  // defaults (eig_max_iter / eig_tol configure the iterative solver); TUCKER_EIG_FUSED=1
+  // forces the iterative solver, TUCKER_EIG_SMALL=1 the direct one up to d = 256
+  // HOOI's warm-started solves converge in ~30 products at config 4 (0.5-1.2 ms per solve under
+  // ncu) and stay on the fused solver; MP's and SP's (flat bulk, ~175 products, 1.4-4 ms) and the
+  // cold one-off solves (HO-SVD, diagnostics) take the direct solver (~1.3 ms, gap independent)
+  const bool iter_opts = h->opts.eig_max_iter > 0 || h->opts.eig_tol > 0;
+  bool hooi_slot = false;
+  for (int m = 0; m < kMaxOrder; ++m) hooi_slot = hooi_slot || &slot == &h->slots[0][m];
+  const bool small = std::getenv("TUCKER_EIG_SMALL") != nullptr ||
+                     (!std::getenv("TUCKER_EIG_FUSED") && !iter_opts && !hooi_slot &&
+                      eig_direct_ws((int)std::min<int64_t>(d, 1 << 20), J) > 0);
   if (small && d <= kSmallMaxD && d >= 3 && !force_large) {
     int64_t ls = 0, rows = 0;
     eig_layout(d, &ls, &rows);

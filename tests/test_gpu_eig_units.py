@@ -83,13 +83,18 @@ def test_split_k_product(capi, d, n):
     assert np.max(np.abs(out0 - S @ Y)) / scale < 1e-14 * max(d, 16)
 
 
+@pytest.mark.parametrize("path", ["auto", "cluster"])
 @pytest.mark.parametrize("d,J,kind", [(3, 1, "spread"), (17, 5, "spread"), (100, 10, "outlier"), (200, 20, "outlier"),
-                                      (256, 112, "outlier"), (200, 50, "repeated"), (150, 30, "clustered")])
-def test_small_dense_eigensolver(monkeypatch, d, J, kind):
-    """eig_small (d <= 256: Householder tridiagonalisation in a 4-CTA cluster, bisection,
-    inverse iteration, back-transformation) against LAPACK: eigenvalues to 1e-12 relative
-    to ||S||, the leading-J subspace to 1e-9, orthonormal vectors -- including eigenvalues
-    repeated inside the leading set and a tight cluster around the J / J+1 boundary."""
+                                      (256, 112, "outlier"), (200, 50, "repeated"), (150, 30, "clustered"),
+                                      (210, 24, "repeated"), (64, 64, "spread")])
+def test_small_dense_eigensolver(monkeypatch, d, J, kind, path):
+    """eig_small against LAPACK: eigenvalues to 1e-12 relative to ||S||, the leading-J
+    subspace to 1e-9, orthonormal vectors -- including eigenvalues repeated inside the
+    leading set and a tight cluster around the J / J+1 boundary.  "auto": the one-CTA
+    solver (k_eig_direct: packed S in shared memory) wherever it fits (d <= 224 and
+    the workspace), the 4-CTA cluster path beyond; "cluster": the cluster path forced."""
+    if path == "cluster":
+        monkeypatch.setenv("TUCKER_EIG_CLUSTER", "1")
     from oracle import tucker_oracle as O
     from paper_0711_2023_b200 import capi
     from synth import random_orthonormal, uniform_distinct_coo

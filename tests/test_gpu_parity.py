@@ -137,6 +137,36 @@ def test_ttmc_parity_order4_shapes(capi, dims, nnz, core):
             assert O.rel_frobenius(t.debug_ttmc(n), O.ttm_chain_unfold(T, U0, n)) < 1e-4
 
 
+@pytest.mark.parametrize("dims,nnz,core", [((9, 40, 33, 7), 6_000, (3, 8, 12, 2)),
+                                            ((30, 6, 5, 50), 4_000, (7, 2, 5, 9)),
+                                            ((12, 13, 14, 15), 20_000, (2, 3, 5, 7)),
+                                            ((20, 22, 18, 16), 12_000, (4, 5, 3, 6)),
+                                            ((40, 200, 30, 20), 48_000, (5, 6, 20, 8)),
+                                            ((7, 300, 37, 21), 60_000, (3, 21, 9, 13))])
+def test_ttmc_parity_order4_gemm(capi, monkeypatch, dims, nnz, core):
+    """Order-4 GEMM-form SpTTMc (k_spttmc4g, forced with TUCKER_TTMC4=g even where
+    the dispatch would pick k_spttmc4w): the dense batch layout (partial last
+    batches, mid1 ranges that are not multiples of the 16-index chunk, empty
+    slices and nodes), several batches per slice and per CTA (runs summed in
+    batch order) and ragged core sizes; Y equals the oracle's and the old
+    kernel's, repeated runs are bit-identical, and a HOOI sweep matches."""
+    idx, vals, U0 = case(dims, nnz, core)
+    T = O.SparseTensor(dims, idx, vals)
+    monkeypatch.setenv("TUCKER_TTMC4", "g")
+    with capi.Tucker(dims, core, idx, vals, U0) as t:
+        Yg = [t.debug_ttmc(n) for n in range(4)]
+        for n in range(4):
+            assert O.rel_frobenius(Yg[n], O.ttm_chain_unfold(T, U0, n)) < 1e-4
+            np.testing.assert_array_equal(Yg[n], t.debug_ttmc(n))
+        fits = t.hooi_sweep(1)
+    monkeypatch.setenv("TUCKER_TTMC4", "w")
+    with capi.Tucker(dims, core, idx, vals, U0) as t:
+        for n in range(4):
+            assert O.rel_frobenius(Yg[n], t.debug_ttmc(n)) < 1e-5
+    ref = O.run_hooi(T, U0, core, 1)
+    assert np.max(np.abs(np.asarray(fits) - np.asarray(ref["fits"]))) < 1e-5
+
+
 @pytest.mark.parametrize("dims,nnz,core", SHAPES)
 def test_gram_parity(capi, dims, nnz, core):
     idx, vals, U0 = case(dims, nnz, core)
