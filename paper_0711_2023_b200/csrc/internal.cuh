@@ -45,12 +45,13 @@ struct Csf {
   DBuf<int32_t> red;   // 3 ints per split slice: slice, first slot, #slots
   DBuf<float> part;    // nslots x (J_mid * J_leaf) partial tiles
   // order-4 GEMM-form SpTTMc (spttmc4g.cu): the ordering's "dense batch layout",
-  // built on first use (jlp = the leaf core size it was built for, 0: not built)
+  // built on first use
   struct G4 {
-    int jlp = 0;
+    int nb_ = 0, kch = 0;              // nodes per batch, mid1 indices per chunk (0: not built)
     int64_t nbatch = 0;
     DBuf<int4> batch;                  // (slice, first node, nodes, -)
-    DBuf<int32_t> bfirst, sp, leaf;    // first batch per slice; slot nonzero offsets; leaf ids in slot order
+    DBuf<int32_t> bfirst, sp, tgt, leaf;  // first batch per slice; slot nonzero offsets (slots sorted by count per
+                                          // chunk) and their (b_local, v) targets; leaf ids in slot order
     DBuf<float> val, part;             // values in slot order; run partial rows
     std::vector<int32_t> bfirst_h;
   };

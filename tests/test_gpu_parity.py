@@ -143,16 +143,18 @@ def test_ttmc_parity_order4_shapes(capi, dims, nnz, core):
                                             ((20, 22, 18, 16), 12_000, (4, 5, 3, 6)),
                                             ((40, 200, 30, 20), 48_000, (5, 6, 20, 8)),
                                             ((7, 300, 37, 21), 60_000, (3, 21, 9, 13))])
-def test_ttmc_parity_order4_gemm(capi, monkeypatch, dims, nnz, core):
-    """Order-4 GEMM-form SpTTMc (k_spttmc4g, forced with TUCKER_TTMC4=g even where
-    the dispatch would pick k_spttmc4w): the dense batch layout (partial last
+@pytest.mark.parametrize("kern", ["g", "t"])
+def test_ttmc_parity_order4_gemm(capi, monkeypatch, dims, nnz, core, kern):
+    """Order-4 GEMM-form SpTTMc (k_spttmc4g on the FMA pipes, k_spttmc4t with level 2
+    on tcgen05 in 3xTF32; forced with TUCKER_TTMC4=g / t even where the dispatch
+    would pick k_spttmc4w): the dense batch layout (partial last
     batches, mid1 ranges that are not multiples of the 16-index chunk, empty
     slices and nodes), several batches per slice and per CTA (runs summed in
     batch order) and ragged core sizes; Y equals the oracle's and the old
     kernel's, repeated runs are bit-identical, and a HOOI sweep matches."""
     idx, vals, U0 = case(dims, nnz, core)
     T = O.SparseTensor(dims, idx, vals)
-    monkeypatch.setenv("TUCKER_TTMC4", "g")
+    monkeypatch.setenv("TUCKER_TTMC4", kern)
     with capi.Tucker(dims, core, idx, vals, U0) as t:
         Yg = [t.debug_ttmc(n) for n in range(4)]
         for n in range(4):
