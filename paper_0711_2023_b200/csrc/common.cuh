@@ -38,6 +38,9 @@ extern thread_local int64_t* g_launch_counter;
 // nullptr (no handle call, e.g. unit-test entry points): plain cudaMalloc.
 extern thread_local cudaStream_t g_alloc_stream;
 void mempool_retain(int device);  // default pool keeps freed memory (once per device)
+// SMs held by a concurrent kernel of the calling handle (MP overlap): persistent grids size to
+// (SMs - g_sm_reserve) so no block waits for a held SM's slots
+extern thread_local int g_sm_reserve;
 
 bool sync_check_enabled();  // env TUCKER_SYNC_CHECK: synchronise + check after every launch
 

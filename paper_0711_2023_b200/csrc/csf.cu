@@ -19,6 +19,7 @@ namespace tk {
 
 thread_local int64_t* g_launch_counter = nullptr;
 thread_local cudaStream_t g_alloc_stream = nullptr;
+thread_local int g_sm_reserve = 0;
 void mempool_retain(int device) {
   static bool done[64] = {};
   if (device < 0 || device >= 64 || done[device]) return;

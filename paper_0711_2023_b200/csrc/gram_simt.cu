@@ -112,7 +112,8 @@ __global__ void __launch_bounds__(256) k_syrk_dmma(const float* __restrict__ hi,
 
 // S[i][j] = S[j][i] = sum_z part[z][t][r][c] (fixed order); diagonal tiles r <= c only
 __global__ void k_syrk_dmma_reduce(const double* __restrict__ part, const int2* __restrict__ tiles, int ntiles,
-                                   int splits, int64_t d, double* __restrict__ S, int64_t lds) {
+                                   int splits, int64_t d, double* __restrict__ S, int64_t lds,
+                                   const double* __restrict__ Sadd) {
   const int t = blockIdx.y;
   const int2 bij = tiles[t];
   for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < DT * DT; e += gridDim.x * blockDim.x) {
@@ -122,6 +123,7 @@ __global__ void k_syrk_dmma_reduce(const double* __restrict__ part, const int2* 
     if (i >= d || j >= d) continue;
     double s = 0.0;
     for (int q = 0; q < splits; ++q) s += part[((size_t)q * ntiles + t) * (DT * DT) + e];
+    if (Sadd) s += Sadd[i * lds + j];
     S[i * lds + j] = s;
     S[j * lds + i] = s;
   }
@@ -129,7 +131,7 @@ __global__ void k_syrk_dmma_reduce(const double* __restrict__ part, const int2* 
 
 }  // namespace
 
-void gram_syrk_dmma(const Split& A, double* S, int64_t lds, GramWs& ws, cudaStream_t st) {
+void gram_syrk_dmma(const Split& A, double* S, int64_t lds, GramWs& ws, cudaStream_t st, const double* Sadd) {
   const int64_t d = A.rows;
   const int nb = (int)ceil_div(d, DT);
   const int ntiles = nb * (nb + 1) / 2;
@@ -142,6 +144,7 @@ void gram_syrk_dmma(const Split& A, double* S, int64_t lds, GramWs& ws, cudaStre
     TK_CUDA(cudaGetDevice(&dev));
     TK_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
   }
+  nsm = std::max(1, nsm - g_sm_reserve);
   // about two waves of 256-thread CTAs, >= 4 chunks per CTA
   const int splits = (int)std::max<int64_t>(1, std::min<int64_t>(std::max<int64_t>(1, 2 * nsm / ntiles), nchunks / 4));
   std::vector<int2> tiles;
@@ -154,7 +157,7 @@ void gram_syrk_dmma(const Split& A, double* S, int64_t lds, GramWs& ws, cudaStre
   TK_LAUNCH(k_syrk_dmma, (unsigned)(ntiles * splits), 256, 0, st, A.hi, A.lo, A.ld, nchunks, ntiles, splits,
             (const int2*)ws.scratch.p, ws.partial.p, A.ktile ? 1 : 0);
   TK_LAUNCH(k_syrk_dmma_reduce, dim3(8, (unsigned)ntiles), 256, 0, st, (const double*)ws.partial.p,
-            (const int2*)ws.scratch.p, ntiles, splits, d, S, lds);
+            (const int2*)ws.scratch.p, ntiles, splits, d, S, lds, Sadd);
 }
 
 int gram_mode() {

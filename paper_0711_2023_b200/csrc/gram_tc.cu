@@ -198,7 +198,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 // S[i][j] = S[j][i] = sum_z partial[z][t][r][c] (fixed order); diagonal tiles r <= c only
 __global__ void k_syrk_reduce(const double* __restrict__ partial, const int2* __restrict__ tiles,
                               int ntiles, int splits, int64_t d, double* __restrict__ S,
-                              int64_t lds) {
+                              int64_t lds, const double* __restrict__ Sadd) {
   const int t = blockIdx.y;
   const int2 bij = tiles[t];
   for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < TM * TN; e += gridDim.x * blockDim.x) {
@@ -208,6 +208,7 @@ __global__ void k_syrk_reduce(const double* __restrict__ partial, const int2* __
     if (i >= d || j >= d) continue;
     double s = 0.0;
     for (int z = 0; z < splits; ++z) s += partial[((int64_t)z * ntiles + t) * (TM * TN) + e];
+    if (Sadd) s += Sadd[i * lds + j];
     S[i * lds + j] = s;
     S[j * lds + i] = s;
   }
@@ -263,7 +264,7 @@ CUtensorMap make_map(const float* base, int64_t rows_pad, int64_t ld, int64_t ke
 
 }  // namespace
 
-void gram_syrk_tc(const Split& A, double* S, int64_t lds, GramWs& ws, cudaStream_t st) {
+void gram_syrk_tc(const Split& A, double* S, int64_t lds, GramWs& ws, cudaStream_t st, const double* Sadd) {
   const int smem_bytes = STAGES * STAGE_BYTES + 1024;
   smem_optin((const void*)k_syrk_tc, smem_bytes);
   const int64_t d = A.rows;
@@ -284,6 +285,7 @@ void gram_syrk_tc(const Split& A, double* S, int64_t lds, GramWs& ws, cudaStream
     TK_CUDA(cudaGetDevice(&dev));
     TK_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
   }
+  nsm = std::max(1, nsm - g_sm_reserve);
   const int splits = (int)std::max<int64_t>(1, std::min<int64_t>(nsm / ntiles, nkt / 4));
   ws.scratch.ensure(sizeof(int2) * tiles.size());
   TK_CUDA(cudaMemcpyAsync(ws.scratch.p, tiles.data(), sizeof(int2) * tiles.size(),
@@ -300,21 +302,25 @@ void gram_syrk_tc(const Split& A, double* S, int64_t lds, GramWs& ws, cudaStream
   a.ktile = A.ktile ? 1 : 0;
   TK_LAUNCH(k_syrk_tc, (unsigned)(ntiles * splits), NUM_THREADS, (size_t)smem_bytes, st, mhi, mlo, a);
   TK_LAUNCH(k_syrk_reduce, dim3(16, (unsigned)ntiles), 256, 0, st, (const double*)ws.partial.p,
-            (const int2*)ws.scratch.p, ntiles, splits, d, S, lds);
+            (const int2*)ws.scratch.p, ntiles, splits, d, S, lds, Sadd);
 }
 
 // Path selection: fp64 DMMA when the SYRK is small enough to afford fp64
 // (<= 2e10 FMA, ~1 ms at the measured 37 TFLOP/s; all HOOI Grams of configs 1-4),
 // 3xTF32 tcgen05 with fp64 drains for the large MP Grams.
-void gram_syrk(const Split& A, double* S, int64_t lds, GramWs& ws, cudaStream_t st) {
-  if (A.K() == 0) {  // empty K shard: S = 0
-    for (int64_t i = 0; i < A.rows; ++i)
-      TK_CUDA(cudaMemsetAsync(S + i * lds, 0, A.rows * sizeof(double), st));
+void gram_syrk(const Split& A, double* S, int64_t lds, GramWs& ws, cudaStream_t st, const double* Sadd, double fma_hint) {
+  if (A.K() == 0) {  // empty K shard: S = 0 (or Sadd)
+    if (Sadd) {
+      TK_CUDA(cudaMemcpy2DAsync(S, lds * sizeof(double), Sadd, lds * sizeof(double), A.rows * sizeof(double), A.rows,
+                                cudaMemcpyDeviceToDevice, st));
+    } else {
+      for (int64_t i = 0; i < A.rows; ++i) TK_CUDA(cudaMemsetAsync(S + i * lds, 0, A.rows * sizeof(double), st));
+    }
     return;
   }
-  const double fma = 0.5 * (double)A.rows * (double)(A.rows + 1) * (double)A.K();
-  if (fma <= 2e10 || gram_mode() == 1) gram_syrk_dmma(A, S, lds, ws, st);
-  else gram_syrk_tc(A, S, lds, ws, st);
+  const double fma = fma_hint > 0 ? fma_hint : 0.5 * (double)A.rows * (double)(A.rows + 1) * (double)A.K();
+  if (fma <= 2e10 || gram_mode() == 1) gram_syrk_dmma(A, S, lds, ws, st, Sadd);
+  else gram_syrk_tc(A, S, lds, ws, st, Sadd);
 }
 
 int gram_path_id() { return gram_mode(); }

@@ -128,9 +128,12 @@ struct GramWs {
   DBuf<double> partial;
   DBuf<uint8_t> scratch;
 };
-void gram_syrk(const Split& A, double* S, int64_t lds, GramWs& ws, cudaStream_t st);
+// S = A A^T (+ Sadd, same layout, when given: the MP term split of mp_sweep's overlap);
+// fma_hint > 0: choose the precision path by this size (the whole Gram a part belongs to)
+void gram_syrk(const Split& A, double* S, int64_t lds, GramWs& ws, cudaStream_t st, const double* Sadd = nullptr,
+               double fma_hint = 0);
 // fp64 tensor-core (DMMA) path for Grams small enough to afford fp64
-void gram_syrk_dmma(const Split& A, double* S, int64_t lds, GramWs& ws, cudaStream_t st);
+void gram_syrk_dmma(const Split& A, double* S, int64_t lds, GramWs& ws, cudaStream_t st, const double* Sadd = nullptr);
 int gram_mode();     // 0 = by size (default), 1 = every Gram on fp64 DMMA (env TUCKER_GRAM_FP64=1)
 int gram_path_id();  // 0 = by size (DMMA <= 2e10 FMA, else tcgen05 3xTF32), 1 = all DMMA
 

@@ -1366,7 +1366,7 @@ void spmm_mp(const Csf& c, const float* U_leaf, int64_t J_leaf, Split out, int64
   TK_CUDA(cudaGetDevice(&dev));
   TK_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
   // persistent-ish grid (each block stages the table once), 6 blocks per SM
-  const unsigned blocks = (unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(c.nfib, 32 * kSpW), 6 * nsm));
+  const unsigned blocks = (unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(c.nfib, 32 * kSpW), 6 * std::max(1, nsm - g_sm_reserve)));
   const size_t smem = sm ? tab : 0;
   auto go = [&](const void* fn) {
     if (smem) smem_optin(fn, smem);

@@ -56,6 +56,15 @@ struct tucker_handle {
   EigSlot scratch_slot;
   EigWs eig;
   GramWs gram;
+  // MP overlap (mp_sweep): while mode n's eigensolve runs, a second stream builds the next
+  // mode's W columns that do not involve U_n and their partial Gram into S2
+  cudaStream_t st2 = nullptr, st_hi = nullptr;  // side work (least priority), eigensolve (greatest)
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_eig = nullptr;
+  DBuf<double> S2;
+  GramWs gram2;
+  bool side_ready[kMaxOrder] = {};
+  cudaEvent_t tl[kMaxOrder][7] = {};  // TUCKER_MP_TIMELINE=1: fork, eig end, side SpMM end, side Gram end,
+                                      // late start, late SpMM end, late Gram end
   int64_t launches = 0;
   int64_t stat_outer0 = 0, stat_matvec0 = 0, stat_sweeps0 = 0;
   long long prof0[13] = {0};
@@ -75,6 +84,18 @@ tucker_handle::~tucker_handle() { g_wkeep_bytes -= wkeep_bytes; }
 
 
 namespace {
+
+struct SmReserveScope {  // SMs held by a concurrent kernel (MP overlap): grid sizing leaves them out
+  int prev;
+  explicit SmReserveScope(int n) : prev(g_sm_reserve) { g_sm_reserve = n; }
+  ~SmReserveScope() { g_sm_reserve = prev; }
+};
+
+struct AllocScope {  // stream-ordered allocations on another stream of the handle (MP overlap)
+  cudaStream_t prev;
+  explicit AllocScope(cudaStream_t s) : prev(g_alloc_stream) { g_alloc_stream = s; }
+  ~AllocScope() { g_alloc_stream = prev; }
+};
 
 struct LaunchScope {  // route TK_LAUNCH counting and stream-ordered allocations to this handle
   int64_t* prev;
@@ -219,21 +240,30 @@ void project_hooi(tucker_handle* h, int n, bool transposed) {
 }
 
 // W_n = [ (X x_m U_m^T)_(n) ]_{m != n} into a kept per-(n, term set) buffer or
-// h->Whi/Wlo; returns the split view
+// h->Whi/Wlo; returns the split view.  Terms in cyclic order m = n + 1, n + 2, ...
+// (the term of the factor updated last, m = n - 1, comes last: mp_sweep's overlap
+// builds the others early), each term's columns padded to a multiple of 32.
 // only_m >= 0: the single term m (Slice Projection, Figs. 5-6)
-Split build_mp_w(tucker_handle* h, int n, int only_m = -1) {
+// mask: the terms whose columns are computed (the others are left as they are);
+// fresh = false: the buffer already holds this build's other terms (never re-zeroed)
+int mp_term_order(const tucker_handle* h, int n, int k) { return (n + 1 + k) % h->order; }
+Split build_mp_w(tucker_handle* h, int n, int only_m = -1, uint32_t mask = ~0u, cudaStream_t s = nullptr,
+                 int64_t* late_off = nullptr, bool fresh = true) {
+  if (!s) s = h->st;
   // sharded: this rank's slices [mp_lo, mp_hi) of every term, columns compacted
   auto slices = [&](int m, const Csf& c, int64_t& lo, int64_t& hi) {
     lo = h->sharded ? h->mp_lo[n][m] : 0;
     hi = h->sharded ? h->mp_hi[n][m] : c.I_mid0 * c.I_mid1;
   };
   int64_t K = 0;
-  for (int m = 0; m < h->order; ++m) {
-    if (m == n || (only_m >= 0 && m != only_m)) continue;
+  for (int k = 0; k < h->order - 1; ++k) {
+    const int m = mp_term_order(h, n, k);
+    if (only_m >= 0 && m != only_m) continue;
     const Csf& c = *h->csfs[h->mp_csf[n][m]];
     int64_t lo, hi;
     slices(m, c, lo, hi);
-    K += h->J[m] * (hi - lo);
+    if (late_off && k == h->order - 2) *late_off = K;
+    K += round_up(h->J[m] * (hi - lo), 32);
   }
   const int64_t rows = h->dims[n];
   // K-tile-major layout (Split::ktile): 32-column tiles of all rows, rows padded to 8
@@ -272,14 +302,20 @@ Split build_mp_w(tucker_handle* h, int n, int only_m = -1) {
       whi = wk.hi.p;
       wlo = wk.lo.p;
     } else {
+      if (!fresh && h->Whi.n >= need) {  // the shared buffer already holds this build's other terms
+        whi = h->Whi.p;
+        wlo = h->Wlo.p;
+        goto fill;
+      }
       h->Whi.ensure(need);
       h->Wlo.ensure(need);
       whi = h->Whi.p;
       wlo = h->Wlo.p;
     }
-    TK_CUDA(cudaMemsetAsync(whi, 0, need * sizeof(float), h->st));
-    TK_CUDA(cudaMemsetAsync(wlo, 0, need * sizeof(float), h->st));
+    TK_CUDA(cudaMemsetAsync(whi, 0, need * sizeof(float), s));
+    TK_CUDA(cudaMemsetAsync(wlo, 0, need * sizeof(float), s));
   }
+fill:
   Split W;
   W.hi = whi;
   W.lo = wlo;
@@ -289,13 +325,14 @@ Split build_mp_w(tucker_handle* h, int n, int only_m = -1) {
   W.kext = kpad;
   W.ktile = true;
   int64_t off = 0;
-  for (int m = 0; m < h->order; ++m) {
-    if (m == n || (only_m >= 0 && m != only_m)) continue;
+  for (int k = 0; k < h->order - 1; ++k) {
+    const int m = mp_term_order(h, n, k);
+    if (only_m >= 0 && m != only_m) continue;
     const Csf& c = *h->csfs[h->mp_csf[n][m]];
     int64_t lo, hi;
     slices(m, c, lo, hi);
-    spmm_mp(c, h->U[m].p, h->J[m], W, off, h->st, lo, hi);
-    off += h->J[m] * (hi - lo);
+    if (mask & (1u << m)) spmm_mp(c, h->U[m].p, h->J[m], W, off, s, lo, hi);
+    off += round_up(h->J[m] * (hi - lo), 32);
   }
   return W;
 }
@@ -509,6 +546,118 @@ void mp_update(tucker_handle* h, int n, int only_m, EigSlot& slot, cudaEvent_t e
   Split W = only_m >= 0 ? build_mp_w(h, n, only_m) : build_mp_w(h, n);
   TK_CUDA(cudaEventRecord(ev_proj, h->st));
   update_factor(h, n, W, false, slot, ev_gram, h->sharded);
+}
+
+// MP overlap (mp_sweep): M_n = sum_{m != n} W_m W_m^T, and only the term of the factor
+// updated last (m = n - 1) depends on the eigensolve just before; the other terms' W columns
+// and their partial Gram are built on a second stream while that eigensolve runs (one CTA
+// for MP's d <= 224 direct solver, the fused solver's few CTAs otherwise).  Same arithmetic
+// as mp_update; the Gram sum is split into S2 (early terms) + the late term, in fp64.
+// Dense-W route, unsharded, order >= 3; TUCKER_MP_OVERLAP=0 disables it.
+bool mp_overlap_ok(tucker_handle* h, int n) {
+  const char* e = std::getenv("TUCKER_MP_OVERLAP");
+  const bool off = e && e[0] == '0';
+  return !off && !h->sharded && h->order >= 3 && !mp_use_sparse(h, n, -1);
+}
+
+
+
+// the early terms of mode n (all but m = n - 1) into W_n and S2, on h->st2
+static bool mp_timeline() {
+  const char* e = std::getenv("TUCKER_MP_TIMELINE");
+  return e && e[0] == '1';
+}
+void mp_side(tucker_handle* h, int n, cudaEvent_t* tl = nullptr) {
+  const int N = h->order, late = (n + N - 1) % N;
+  uint32_t mask = 0;
+  for (int m = 0; m < N; ++m)
+    if (m != n && m != late) mask |= 1u << m;
+  const AllocScope as(h->st2);
+  // the eigensolve holds one SM: persistent side kernels size their grids to the others
+  // (a grid that needs the held SM's slots runs its last blocks after a whole block's share)
+  const SmReserveScope rs(1);
+  int64_t off_late = 0;
+  Split W = build_mp_w(h, n, -1, mask, h->st2, &off_late);
+  if (tl) TK_CUDA(cudaEventRecord(tl[2], h->st2));
+  Split We = W;
+  We.kext = off_late;
+  We.cols = off_late;
+  int64_t ls = 0, rows = 0;  // S2 in S's padded layout (h->S itself is in use by the eigensolve)
+  eig_layout(W.rows, &ls, &rows);
+  h->S2.ensure((size_t)(rows * ls));
+  gram_syrk(We, h->S2.p, ls, h->gram2, h->st2, nullptr, 0.5 * (double)W.rows * (W.rows + 1) * (double)W.K());
+  if (tl) TK_CUDA(cudaEventRecord(tl[3], h->st2));
+  h->side_ready[n] = true;
+}
+
+void mp_update_overlap(tucker_handle* h, int n, EigSlot& slot, cudaEvent_t ev_proj, cudaEvent_t ev_gram, int next) {
+  if (!h->st2) {
+    // the eigensolve's CTA(s) must be dispatched before the side kernels fill every SM (the SpMM
+    // blocks are persistent): it runs on a greatest-priority stream, the side work on a least one
+    int least = 0, greatest = 0;
+    TK_CUDA(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+    TK_CUDA(cudaStreamCreateWithPriority(&h->st2, cudaStreamNonBlocking, least));
+    TK_CUDA(cudaStreamCreateWithPriority(&h->st_hi, cudaStreamNonBlocking, greatest));
+    TK_CUDA(cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming));
+    TK_CUDA(cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming));
+    TK_CUDA(cudaEventCreateWithFlags(&h->ev_eig, cudaEventDisableTiming));
+  }
+  const int N = h->order, late = (n + N - 1) % N;
+  const int64_t d = h->dims[n];
+  const int64_t lds = ensure_S(h, d);
+  cudaEvent_t* tl = nullptr;
+  if (mp_timeline()) {
+    tl = h->tl[n];
+    for (int q = 0; q < 7; ++q)
+      if (!tl[q]) TK_CUDA(cudaEventCreate(&tl[q]));
+  }
+  if (h->side_ready[n]) {  // early terms done on st2: the late term, S = S2 + W_late W_late^T
+    TK_CUDA(cudaStreamWaitEvent(h->st, h->ev_join, 0));
+    if (tl) TK_CUDA(cudaEventRecord(tl[4], h->st));
+    int64_t off_late = 0;
+    Split W = build_mp_w(h, n, -1, 1u << late, h->st, &off_late, false);
+    TK_CUDA(cudaEventRecord(ev_proj, h->st));
+    if (tl) TK_CUDA(cudaEventRecord(tl[5], h->st));
+    Split Wl = W;
+    const int64_t sh = off_late / 32 * 32 * W.ld;  // K-tile-major: whole 32-column tiles
+    Wl.hi = W.hi + sh;
+    Wl.lo = W.lo + sh;
+    Wl.kext = W.kext - off_late;
+    Wl.cols = W.cols - off_late;
+    gram_syrk(Wl, h->S.p, lds, h->gram, h->st, h->S2.p, 0.5 * (double)W.rows * (W.rows + 1) * (double)W.K());
+    if (tl) TK_CUDA(cudaEventRecord(tl[6], h->st));
+    h->side_ready[n] = false;
+  } else {
+    Split W = build_mp_w(h, n);
+    TK_CUDA(cudaEventRecord(ev_proj, h->st));
+    gram_syrk(W, h->S.p, lds, h->gram, h->st);
+  }
+  TK_CUDA(cudaEventRecord(ev_gram, h->st));
+  TK_CUDA(cudaEventRecord(h->ev_fork, h->st));
+  if (tl) TK_CUDA(cudaEventRecord(tl[0], h->st));
+  {  // the eigensolve (and the factor update) on the greatest-priority stream, launched first
+    TK_CUDA(cudaStreamWaitEvent(h->st_hi, h->ev_fork, 0));
+    cudaStream_t main_st = h->st;
+    h->st = h->st_hi;
+    try {
+      const AllocScope as(h->st_hi);
+      Split A;
+      A.rows = d;
+      factor_from_S(h, n, A, false, slot, false);
+    } catch (...) {
+      h->st = main_st;
+      throw;
+    }
+    h->st = main_st;
+    TK_CUDA(cudaEventRecord(h->ev_eig, h->st_hi));
+    if (tl) TK_CUDA(cudaEventRecord(tl[1], h->st_hi));
+  }
+  if (next >= 0) {  // every factor but U_n is final: the next mode's early terms meanwhile
+    TK_CUDA(cudaStreamWaitEvent(h->st2, h->ev_fork, 0));
+    mp_side(h, next, tl);
+    TK_CUDA(cudaEventRecord(h->ev_join, h->st2));
+  }
+  TK_CUDA(cudaStreamWaitEvent(h->st, h->ev_eig, 0));
 }
 
 // G_(N) = U_N^T Y_(N) from h->Y (must be the projection of the last mode with
@@ -881,6 +1030,8 @@ int hooi_sweep(tucker_handle* h, int sweeps, double* fit_per_sweep, float* stage
 int mp_sweep(tucker_handle* h, int sweeps, double* fit_per_sweep, float* stage_ms) {
   if (!h || sweeps < 1) return TUCKER_E_ARG;
   return guarded(h, [&]() -> int {
+    for (auto& r : h->side_ready) r = false;
+    if (h->st2) TK_CUDA(cudaStreamSynchronize(h->st2));  // nothing of an earlier call still in flight
     h->eig_unconverged = false;
     h->G_valid = false;
     const int N = h->order;
@@ -888,7 +1039,14 @@ int mp_sweep(tucker_handle* h, int sweeps, double* fit_per_sweep, float* stage_m
     for (int s = 0; s < sweeps; ++s) {
       for (int n = 0; n < N; ++n) {
         TK_CUDA(cudaEventRecord(ev.e[4 * n], h->st));
-        mp_update(h, n, -1, h->slots[1][n], ev.e[4 * n + 1], ev.e[4 * n + 2]);
+        const int nn = (n + 1) % N;
+        const bool more = n + 1 < N || s + 1 < sweeps;
+        if (mp_overlap_ok(h, n)) {
+          mp_update_overlap(h, n, h->slots[1][n], ev.e[4 * n + 1], ev.e[4 * n + 2],
+                            more && mp_overlap_ok(h, nn) ? nn : -1);
+        } else {
+          mp_update(h, n, -1, h->slots[1][n], ev.e[4 * n + 1], ev.e[4 * n + 2]);
+        }
         TK_CUDA(cudaEventRecord(ev.e[4 * n + 3], h->st));
       }
       h->G_valid = false;
@@ -896,6 +1054,22 @@ int mp_sweep(tucker_handle* h, int sweeps, double* fit_per_sweep, float* stage_m
       if (fit_per_sweep) fit_per_sweep[s] = compute_core(h);
       TK_CUDA(cudaEventRecord(ev.e[4 * N + 1], h->st));
       TK_CUDA(cudaEventSynchronize(ev.e[4 * N + 1]));  // the sweep's one host synchronisation
+      if (mp_timeline()) {
+        TK_CUDA(cudaDeviceSynchronize());
+        for (int n = 0; n < N; ++n) {
+          if (!h->tl[n][0]) continue;
+          float a = 0, b = 0, c = 0;
+          cudaEventElapsedTime(&a, h->tl[n][0], h->tl[n][1]);
+          cudaEventElapsedTime(&b, h->tl[n][0], h->tl[n][2]);
+          cudaEventElapsedTime(&c, h->tl[n][0], h->tl[n][3]);
+          float d1 = 0, d2 = 0;
+          cudaEventElapsedTime(&d1, h->tl[n][4], h->tl[n][5]);
+          cudaEventElapsedTime(&d2, h->tl[n][5], h->tl[n][6]);
+          std::fprintf(stderr, "mp timeline sweep %d mode %d: eig end %.3f ms, side SpMM end %.3f, side Gram end %.3f; "
+                       "late SpMM %.3f, late Gram %.3f\n", s, n, a, b, c, d1, d2);
+        }
+        (void)cudaGetLastError();  // unrecorded events of the last mode
+      }
       eig_check(h, 0, N);
       float ms[4] = {0, 0, 0, ev.ms(4 * N, 4 * N + 1)};
       for (int n = 0; n < N; ++n) {
@@ -1032,8 +1206,21 @@ int tucker_free(tucker_handle* h) {
   if (h->st) cudaStreamSynchronize(h->st);
   const bool own = h->own_stream;
   cudaStream_t st = h->st;
+  cudaStream_t st2 = h->st2, sth = h->st_hi;  // MP overlap streams: destroyed after the buffers they allocated
+  cudaEvent_t e1 = h->ev_fork, e2 = h->ev_join, e3 = h->ev_eig;
+  if (st2) cudaStreamSynchronize(st2);
+  if (sth) cudaStreamSynchronize(sth);
   if (h->comm) dist_comm_destroy(h->comm);
   delete h;
+  if (st2) {
+    cudaStreamSynchronize(st2);
+    cudaStreamSynchronize(sth);
+    cudaStreamDestroy(st2);
+    cudaStreamDestroy(sth);
+    cudaEventDestroy(e1);
+    cudaEventDestroy(e2);
+    cudaEventDestroy(e3);
+  }
   if (own && st) cudaStreamDestroy(st);
   return TUCKER_OK;
 }

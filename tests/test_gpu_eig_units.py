@@ -86,7 +86,7 @@ def test_split_k_product(capi, d, n):
 @pytest.mark.parametrize("path", ["auto", "cluster"])
 @pytest.mark.parametrize("d,J,kind", [(3, 1, "spread"), (17, 5, "spread"), (100, 10, "outlier"), (200, 20, "outlier"),
                                       (256, 112, "outlier"), (200, 50, "repeated"), (150, 30, "clustered"),
-                                      (210, 24, "repeated"), (64, 64, "spread")])
+                                      (210, 25, "repeated"), (64, 64, "spread")])
 def test_small_dense_eigensolver(monkeypatch, d, J, kind, path):
     """eig_small against LAPACK: eigenvalues to 1e-12 relative to ||S||, the leading-J
     subspace to 1e-9, orthonormal vectors -- including eigenvalues repeated inside the

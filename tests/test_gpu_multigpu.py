@@ -27,7 +27,10 @@ def capi():
     ((37, 300, 53), 9_000, (5, 16, 7)),        # Y^T Y route on modes 1, 3
     ((20, 22, 18, 16), 12_000, (4, 5, 3, 6)),  # order 4
 ])
-def test_sharded_path_world1_matches_unsharded(capi, dims, nnz, core):
+def test_sharded_path_world1_matches_unsharded(capi, monkeypatch, dims, nnz, core):
+    # bit-identity: the unsharded MP sweep without the eigensolve / next-mode overlap (which
+    # splits each M_n sum into two fp64 partial sums, test_gpu_parity.test_mp_overlap)
+    monkeypatch.setenv("TUCKER_MP_OVERLAP", "0")
     rng = np.random.default_rng(31)
     idx, vals = uniform_distinct_coo(dims, nnz, rng)
     U0 = [random_orthonormal(I, J, np.random.default_rng(40 + k)) for k, (I, J) in enumerate(zip(dims, core))]

@@ -352,3 +352,30 @@ def test_convergence_driver(capi, algo):
         fits = getattr(t, algo + "_run")(max_sweeps=50, tol=tol)
     assert len(fits) == k + 1
     assert np.max(np.abs(fits - ref[: k + 1])) < 1e-5
+
+
+@pytest.mark.parametrize("dims,nnz,core", [((100, 110, 120), 13_200, (10, 11, 12)),
+                                            ((20, 22, 18, 16), 12_000, (4, 5, 3, 6)),
+                                            ((200, 200, 200, 200), 400_000, (20, 20, 20, 20))])
+def test_mp_overlap(capi, monkeypatch, dims, nnz, core):
+    """MP sweep with the next mode's early terms (W columns and their Gram into S2) built on a
+    second stream while the eigensolve runs, the late term added on the main stream: the same
+    sums in another fp64 order -- fits and factors agree with the serial sweep to rounding, and
+    both with the oracle."""
+    idx, vals, U0 = case(dims, nnz, core)
+    out = {}
+    for ov in ("0", "1"):
+        monkeypatch.setenv("TUCKER_MP_OVERLAP", ov)
+        with capi.Tucker(dims, core, idx, vals, U0) as t:
+            f = t.mp_sweep(3)
+            G, U, fit = t.core_and_fit()
+        out[ov] = (np.asarray(f), U, fit)
+    f0, U0g, _ = out["0"]
+    f1, U1g, _ = out["1"]
+    assert np.max(np.abs(f0 - f1)) < 1e-9
+    for a, b in zip(U0g, U1g):
+        assert O.projector_distance(a, b) < 1e-4  # fp32 factors of an ill-conditioned sum (kappa ~1e3)
+    if nnz <= 20_000:
+        T = O.SparseTensor(dims, idx, vals)
+        ref = O.run_mp(T, U0, core, 3)
+        assert np.max(np.abs(f1 - np.asarray(ref["fits"]))) < 1e-5
