@@ -187,19 +187,35 @@ def spttmc_table(capi, configs, local, stream, pk, cpk):
     return rows
 
 
-def gram_flops(c):
+def mp_overlap_on(c):
+    """The library's MP overlap (TUCKER_MP_OVERLAP, default on; dense-W route, order >= 3):
+    the main stream's projection / Gram stages then hold only the late term (m = n - 1) of
+    each mode; the other terms run beside the previous mode's eigensolve."""
+    return os.environ.get("TUCKER_MP_OVERLAP", "1") != "0" and len(c["dims"]) >= 3 and c["nnz"] < 1e8
+
+
+def gram_flops(c, late_only=False):
     """Algorithmic flops of the Gram (SYRK, upper triangle incl. diagonal) per
-    HOOI sweep and per MP sweep: d(d+1)K with d x K the Gram operand."""
+    HOOI sweep and per MP sweep: d(d+1)K with d x K the Gram operand (MP: only
+    the late term's K when late_only)."""
     dims, J, N = c["dims"], c["core"], len(c["dims"])
     h = m = 0.0
     for n in range(N):
         P = int(np.prod([J[q] for q in range(N) if q != n]))
         d, K = (dims[n], P) if P >= dims[n] else (P, dims[n])
         h += d * (d + 1.0) * K
-        Kw = sum(J[q] * int(np.prod([dims[r] for r in range(N) if r not in (n, q)]))
-                 for q in range(N) if q != n)
+        terms = [(n - 1) % N] if late_only else [q for q in range(N) if q != n]
+        Kw = sum(J[q] * int(np.prod([dims[r] for r in range(N) if r not in (n, q)])) for q in terms)
         m += dims[n] * (dims[n] + 1.0) * Kw
     return h, m
+
+
+def direct_eig_flops(d, J):
+    """Algorithmic fp64 flops of one direct dense solve (k_eig_direct): Householder
+    tridiagonalisation 4/3 d^3 (symmetric product + rank-2 update per column),
+    back-transformation of J vectors 4 d^2 J / 2 (reflectors of decreasing length);
+    the O(d J) bisection / inverse-iteration work is not counted."""
+    return 4.0 / 3.0 * d ** 3 + 2.0 * d * d * J
 
 
 def cpu_oracle_sample(c):
@@ -448,35 +464,52 @@ def run_ours(args):
               "gram": (stage_acc[1] + stage_acc_mp[1]) / args.steps,
               "eig": (stage_acc[2] + stage_acc_mp[2]) / args.steps,
               "core+fit": (stage_acc[3] + stage_acc_mp[3]) / args.steps}
-    eig_ms = shares["eig"]
+    # HOOI solves: the warm-started fused solver (k_eig_fused, its own flop count); MP solves at
+    # d <= 224: the one-CTA direct solver (k_eig_direct, direct_eig_flops)
+    eig_ms_h = stage_acc[2] / args.steps
+    eig_ms_m = stage_acc_mp[2] / args.steps
     eig_flops = st.get("eig_flops", 0) / args.steps
-    launches_eig = 2 * N * S  # one k_eig_fused launch per factor update
+    launches_eig = N * S  # one launch per factor update
     fp64_peak = cpk.get("dmma_tflops") or 148 * 64 * 2 * 1.965e9 / 1e12
-    achieved = eig_flops / (eig_ms / 1e3) / 1e12 if eig_ms > 0 else 0.0
+    peak_note = ("fp64 DMMA measured (tools/peaks.cu, profiles/measured_compute_peaks.json)"
+                 if cpk.get("dmma_tflops") else
+                 "fp64 nominal: 148 SMs x 64 FMA/clk x 2 x 1.965 GHz (B200_PROFILING clock)")
     try:  # per-launch DRAM bytes from the committed ncu --set full captures
         traffic_all = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
     except Exception:
         traffic_all = {}
-    roof_eig = {"kernel": "k_eig_fused (persistent eigensolver: DMMA products, Jacobi RR, CholQR)",
-                "bound": "alu",
-                "peak_note": ("fp64 DMMA measured (tools/peaks.cu, profiles/measured_compute_peaks.json)"
-                              if cpk.get("dmma_tflops") else
-                              "fp64 nominal: 148 SMs x 64 FMA/clk x 2 x 1.965 GHz (B200_PROFILING clock)"),
-                "achieved": achieved, "peak": fp64_peak, "unit": "TFLOP/s", "frac": achieved / fp64_peak,
-                "traffic": traffic_all.get("k_eig_fused"), "flops_per_launch": eig_flops / launches_eig,
-                "ms_per_launch": eig_ms / launches_eig, "launches_per_step": launches_eig,
-                "products_per_solve": st.get("eig_matvec", 0) / args.steps / launches_eig}
+    ach_h = eig_flops / (eig_ms_h / 1e3) / 1e12 if eig_ms_h > 0 else 0.0
+    roof_eig_h = {"kernel": "k_eig_fused (HOOI: persistent warm-started subspace iteration, 32 CTAs at d <= 256)",
+                  "bound": "alu", "peak_note": peak_note,
+                  "achieved": ach_h, "peak": fp64_peak, "unit": "TFLOP/s", "frac": ach_h / fp64_peak,
+                  "traffic": traffic_all.get("k_eig_fused"), "flops_per_launch": eig_flops / launches_eig,
+                  "ms_per_launch": eig_ms_h / launches_eig, "launches_per_step": launches_eig,
+                  "products_per_solve": st.get("eig_matvec", 0) / args.steps / launches_eig}
+    dflops = sum(direct_eig_flops(dims[n], core[n]) for n in range(N)) * S
+    ach_m = dflops / (eig_ms_m / 1e3) / 1e12 if eig_ms_m > 0 else 0.0
+    roof_eig = {"kernel": "k_eig_direct (MP: one-CTA dense solve -- Householder tridiagonalisation in shared "
+                          "memory, multisection, inverse iteration, back-transformation)",
+                "bound": "alu", "peak_note": peak_note + "; the kernel runs on ONE SM by design (beside the "
+                "overlapped next-mode work on the other 147): frac_one_sm is against 1/148 of that peak",
+                "achieved": ach_m, "peak": fp64_peak, "unit": "TFLOP/s", "frac": ach_m / fp64_peak,
+                "frac_one_sm": ach_m / (fp64_peak / 148.0),
+                "traffic": traffic_all.get("k_eig_direct"), "flops_per_launch": dflops / launches_eig,
+                "ms_per_launch": eig_ms_m / launches_eig, "launches_per_step": launches_eig,
+                "note": "latency bound: 198 dependent Householder steps (three block barriers each) at d = 200"}
     phases = {k: v / args.steps for k, v in st.get("eig_phase_ms", {}).items()}
     if any(v > 0 for v in phases.values()):  # only in TK_EIG_PROFILE builds (tools/eig_profile.sh)
         roof_eig["eig_phase_ms_per_step"] = phases
     # the Gram SYRK: 3xTF32 on tcgen05 (MP) / fp64 DMMA (HOOI <= 2e10 FMA)
-    hflops, mflops = gram_flops(c)
+    ovl = mp_overlap_on(c)
+    hflops, mflops = gram_flops(c, late_only=ovl)
     gram_ms = shares["gram"]
     gram_flops_step = S * (hflops + mflops)
     g_ach = gram_flops_step / (gram_ms / 1e3) / 1e12 if gram_ms > 0 else 0.0
     tf32_peak = cpk.get("tcgen05_tf32_tflops") or pk["bf16_tflops"] * (1.1 / 2.25)
     g_peak = tf32_peak / 3.0
     roof_gram = {"kernel": "k_syrk_tc (tcgen05 3xTF32 SYRK, fp64 drain) + k_syrk_dmma", "bound": "tensor",
+                 "note": ("main-stream Grams: HOOI's and MP's late term (the other MP terms run overlapped)"
+                          if ovl else "all Grams"),
                  "peak_note": ("measured tcgen05 kind::tf32 issue peak / 3 products (profiles/measured_compute_peaks.json)"
                                if cpk.get("tcgen05_tf32_tflops") else
                                "measured bf16 burst x tf32/bf16 nominal (1.1/2.25) / 3 products"),
@@ -500,16 +533,20 @@ def run_ours(args):
     sp_nnz_bytes = 0.0
     for n in range(N):
         for m in range(N):
-            if m != n:
+            if m != n and (not ovl or m == (n - 1) % N):
                 sp_nnz_bytes += 8.0 * c["nnz"] + 16.0 * layout[n]["fibers"] + 8.0 * layout[n]["fibers"] * core[m]
     spmm_ms = shares["spmm"] / S
     roof_spmm = {"kernel": "k_spmm_w (MP leaf SpMM into the K-tile-major W)", "bound": "hbm", "unit": "GB/s",
                  "achieved": sp_nnz_bytes / (spmm_ms / 1e3) / 1e9 if spmm_ms > 0 else None, "peak": pk["hbm_gbs"],
                  "alg_bytes": sp_nnz_bytes, "ms_per_sweep": spmm_ms,
-                 "note": "fibers of the (n, o, m) orderings approximated by the HOOI ordering's fiber count"}
+                 "note": "fibers of the (n, o, m) orderings approximated by the HOOI ordering's fiber count" +
+                         ("; main-stream SpMMs only (MP's late term per mode)" if ovl else "")}
     roof_spmm["frac"] = roof_spmm["achieved"] / roof_spmm["peak"] if roof_spmm["achieved"] else None
     dom = max(shares, key=shares.get)
-    roof = dict({"spttmc": roof_sp, "spmm": roof_spmm, "gram": roof_gram, "eig": roof_eig}.get(dom, roof_eig))
+    if dom == "eig" and eig_ms_h > eig_ms_m:
+        roof = dict(roof_eig_h)
+    else:
+        roof = dict({"spttmc": roof_sp, "spmm": roof_spmm, "gram": roof_gram, "eig": roof_eig}.get(dom, roof_eig))
     roof["dominant_stage"] = dom
     roof["stage_ms_per_step"] = shares
 
@@ -543,6 +580,8 @@ def run_ours(args):
                 "d2h_bytes_per_step": int(d2h)},
         "roofline": roof,
         "roofline_eig": roof_eig,
+        "roofline_eig_hooi": roof_eig_h,
+        "mp_overlap": ovl,
         "roofline_gram": roof_gram,
         "roofline_spttmc": roof_sp,
         "roofline_spmm": roof_spmm,

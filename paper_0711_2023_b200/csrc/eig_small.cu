@@ -399,6 +399,220 @@ __device__ __forceinline__ double wsum(double v) {
   return v;
 }
 
+// phases 2-4 of the direct solve: T = (sa, se) (overwritten: scaled), reflectors in rows of H
+// (u_k on entries k + 1 .. n - 1; beta_k in H[k][k], or beta[k] when beta != nullptr), a
+// shared-memory workspace L of wsz doubles; V (n x m, ld m), theta (m), info record
+__device__ void eig_tail(int n, int m, double* sa, double* se, double* te2, double* L, int wsz, double* lam,
+                         double* red, const double* Hg, const double* betag, double* Vout, double* theta_out,
+                         int* info_out) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  // ---- 2. eigenvalues: scale T by its Gershgorin bound tn
+  double tn = 0.0;
+  for (int i = 0; i < n; ++i) tn = fmax(tn, fabs(sa[i]) + (i > 0 ? fabs(se[i - 1]) : 0.0) + (i < n - 1 ? fabs(se[i]) : 0.0));
+  const double sc = tn > 0 ? 1.0 / tn : 1.0;
+  __syncthreads();
+  for (int i = tid; i < n; i += kDT) {
+    sa[i] *= sc;
+    se[i] *= sc;
+    te2[i] = se[i] * se[i];
+  }
+  __syncthreads();
+  for (int j = warp; j < m; j += kDW) {
+    const int kth = n - 1 - j;  // the (n - 1 - j)-th smallest
+    double l = -1.0 - 1e-12, h = 1.0 + 1e-12;
+    for (int it = 0; it < 11; ++it) {
+      const double x = l + (h - l) * (double)(lane + 1) / 33.0;
+      // sign changes of the leading minors p_0 = 1, p_1 = a_0 - x, p_i = (a_{i-1} - x) p_{i-1} - e_{i-2}^2 p_{i-2}
+      // (T is scaled to ||T|| <= 1, so |p| grows by <= 3 per step: rescaled every 8 steps when it
+      // leaves [1e-100, 1e100]; an exact zero minor counts as a sign change, like a -0 pivot)
+      int cnt = 0;
+      double pm = 1.0, pc = sa[0] - x;
+      bool neg = pc <= 0.0;  // p_0 = 1 > 0; a zero p_1 counts as negative
+      cnt += neg;
+      int i = 1;
+      for (; i + 8 <= n; i += 8) {
+#pragma unroll
+        for (int r = 0; r < 8; ++r) {
+          const double pn = fma(sa[i + r] - x, pc, -te2[i + r - 1] * pm);
+          // sign of a zero minor: opposite to its predecessor's (a -0 pivot); kept off the chain
+          const bool ng = pn == 0.0 ? !neg : pn < 0.0;
+          cnt += ng != neg;
+          neg = ng;
+          pm = pc;
+          pc = pn;
+        }
+        const double an = fabs(pc);
+        if (an > 1e100 || an < 1e-100) {
+          const double f = an > 1e100 ? 1e-100 : 1e100;
+          pc *= f;
+          pm *= f;
+        }
+      }
+      for (; i < n; ++i) {
+        const double pn = fma(sa[i] - x, pc, -te2[i - 1] * pm);
+        const bool ng = pn == 0.0 ? !neg : pn < 0.0;
+        cnt += ng != neg;
+        neg = ng;
+        pm = pc;
+        pc = pn;
+      }
+      const unsigned below = __ballot_sync(0xffffffffu, cnt <= kth);
+      const int nb = __popc(below);  // points 0 .. nb - 1 lie at or left of the target
+      const double nl = nb > 0 ? l + (h - l) * (double)nb / 33.0 : l;
+      const double nh = l + (h - l) * (double)(nb + 1) / 33.0;
+      l = nl;
+      h = nh;
+    }
+    if (lane == 0) lam[j] = 0.5 * (l + h);
+  }
+  __syncthreads();
+  // ---- 3. inverse iteration; workspace: Y [n][m] | per round R vectors x (dl, dd, du, du2) [n][R] | pv bytes [n][R]
+  double* Y = L;
+  const int R = max(1, min(m, (int)((wsz - n * m) / (4 * n + (n + 7) / 8 + 1))));
+  double* dl = Y + n * m;
+  double* dd = dl + n * R;
+  double* du = dd + n * R;
+  double* du2 = du + n * R;
+  unsigned char* pv = reinterpret_cast<unsigned char*>(du2 + n * R);
+  const double eps = 2.2e-16;
+  for (int j0 = 0; j0 < m; j0 += R) {
+    const int t = tid;
+    const int j = j0 + t;
+    if (t < R && j < m) {
+      const double shift = lam[j] + eps * (1.0 + 0.25 * (j & 7));
+#define AT(a, i) a[(i) * R + t]
+      // pivoted LU of T - shift I (LAPACK dgttrf's elimination), the current row carried in registers
+      double cd = sa[0] - shift, cu = n > 1 ? se[0] : 0.0;
+      for (int i = 0; i < n - 1; ++i) {
+        const double li = se[i], nd = sa[i + 1] - shift, nu = i + 1 < n - 1 ? se[i + 1] : 0.0;
+        if (fabs(cd) >= fabs(li)) {
+          const double dv = cd == 0.0 ? eps : cd;
+          const double f = li / dv;
+          AT(dl, i) = f;
+          AT(dd, i) = 1.0 / dv;
+          AT(du, i) = cu;
+          AT(du2, i) = 0.0;
+          pv[i * R + t] = 0;
+          cd = fma(-f, cu, nd);
+          cu = nu;
+        } else {
+          const double f = cd / li;
+          AT(dl, i) = f;
+          AT(dd, i) = 1.0 / li;
+          AT(du, i) = nd;
+          AT(du2, i) = nu;
+          pv[i * R + t] = 1;
+          cd = fma(-f, nd, cu);
+          cu = -f * nu;
+        }
+      }
+      AT(dd, n - 1) = 1.0 / (cd == 0.0 ? eps : cd);
+      // start vector: fixed pseudo-random, in [0.5, 1)
+      for (int i = 0; i < n; ++i) {
+        uint64_t z = (uint64_t)(i + 1) * 0x9E3779B97F4A7C15ull ^ (uint64_t)(j + 7) * 0xBF58476D1CE4E5B9ull;
+        z ^= z >> 31;
+        Y[i * m + j] = 0.5 + (double)(z >> 11) * (1.0 / 9007199254740992.0);
+      }
+      for (int it = 0; it < 2; ++it) {
+        double cy = Y[j];  // forward: L (row swaps as recorded)
+        for (int i = 0; i < n - 1; ++i) {
+          const double ny = Y[(i + 1) * m + j], f = AT(dl, i);
+          if (!pv[i * R + t]) {
+            Y[i * m + j] = cy;
+            cy = fma(-f, cy, ny);
+          } else {
+            Y[i * m + j] = ny;
+            cy = fma(-f, ny, cy);
+          }
+        }
+        // backward: U (reciprocal pivots), y_{i+1}, y_{i+2} carried
+        double y1 = cy * AT(dd, n - 1), y2 = 0.0;
+        Y[(n - 1) * m + j] = y1;
+        double ssq = y1 * y1;
+        for (int i = n - 2; i >= 0; --i) {
+          const double yi = (Y[i * m + j] - AT(du, i) * y1 - AT(du2, i) * y2) * AT(dd, i);
+          Y[i * m + j] = yi;
+          ssq = fma(yi, yi, ssq);
+          y2 = y1;
+          y1 = yi;
+        }
+        const double sN = 1.0 / sqrt(ssq);
+        for (int i = 0; i < n; ++i) Y[i * m + j] *= sN;
+      }
+#undef AT
+    }
+    __syncthreads();
+  }
+  // modified Gram-Schmidt among close eigenvalues (twice)
+  auto csum = [&](double v) {
+    v = wsum(v);
+    if (lane == 0) red[warp] = v;
+    __syncthreads();
+    const double s = wsum(red[lane]);
+    __syncthreads();
+    return s;
+  };
+  for (int j = 1; j < m; ++j) {
+    int i0 = j;
+    while (i0 > 0 && lam[i0 - 1] - lam[i0] <= 1e-9) --i0;
+    if (i0 == j) continue;
+    for (int pass = 0; pass < 2; ++pass) {
+      for (int i = i0; i < j; ++i) {
+        double s = 0.0;
+        for (int r = tid; r < n; r += kDT) s = fma(Y[r * m + i], Y[r * m + j], s);
+        s = csum(s);
+        for (int r = tid; r < n; r += kDT) Y[r * m + j] -= s * Y[r * m + i];
+        __syncthreads();
+      }
+      double s = 0.0;
+      for (int r = tid; r < n; r += kDT) s = fma(Y[r * m + j], Y[r * m + j], s);
+      s = 1.0 / sqrt(csum(s));
+      for (int r = tid; r < n; r += kDT) Y[r * m + j] *= s;
+      __syncthreads();
+    }
+  }
+  // ---- 4. back-transformation, a warp per vector (Yt: [m][n] copy, conflict-free lanes)
+  double* Yt = dl;  // the inverse-iteration arrays are free now (n m <= 4 n R + ... checked on the host)
+  for (int e = tid; e < n * m; e += kDT) {
+    const int jj = e / n, r = e - jj * n;
+    Yt[e] = Y[r * m + jj];
+  }
+  __syncthreads();
+  // reflector rows staged in shared memory in chunks of CH (the workspace past Y and Yt)
+  double* Hs = Yt + (size_t)n * m;
+  const int CH = max(1, min(n, (int)((wsz - 2 * n * m) / n)));
+  for (int k1 = n - 2; k1 > 0; k1 -= CH) {  // rows [k0, k1) of H, applied last to first
+    const int k0 = max(0, k1 - CH);
+    for (int e = tid; e < (k1 - k0) * n; e += kDT) Hs[e] = Hg[(int64_t)k0 * n + e];
+    __syncthreads();
+    for (int jj = warp; jj < m; jj += kDW) {
+      double* y = Yt + (size_t)jj * n;
+      for (int k = k1 - 1; k >= k0; --k) {
+        const double* uk = Hs + (size_t)(k - k0) * n;
+        const double bk = betag ? betag[k] : uk[k];  // beta_k: separate, or in the diagonal slot
+        if (bk == 0.0) continue;
+        double s = 0.0;
+        for (int r = k + 1 + lane; r < n; r += 32) s = fma(uk[r], y[r], s);
+        s = bk * wsum(s);
+        for (int r = k + 1 + lane; r < n; r += 32) y[r] -= s * uk[r];
+        __syncwarp();
+      }
+    }
+    __syncthreads();
+  }
+  for (int e = tid; e < n * m; e += kDT) {
+    const int r = e / m, jj = e - r * m;
+    Vout[e] = Yt[(size_t)jj * n + r];
+  }
+  for (int jj = tid; jj < m; jj += kDT) theta_out[jj] = lam[jj] * tn;
+  if (tid < 8) info_out[tid] = tid == 0 || tid == 1 ? 1 : 0;  // converged (direct method), 1 "iteration"
+  if (tid == 0) {
+    double* dv = reinterpret_cast<double*>(info_out + 8);
+    dv[0] = -1.0;  // no Lanczos / filter-bound estimates (eig_check keeps the slot's)
+    dv[1] = -1.0;
+  }
+}
+
 __global__ void __launch_bounds__(kDT, 1) k_eig_direct(DirArgs p) {
   extern __shared__ double sm[];
   __shared__ double npart[kDW], kpart[kDW];
@@ -580,214 +794,31 @@ __global__ void __launch_bounds__(kDT, 1) k_eig_direct(DirArgs p) {
   for (int k = max(0, n - 2) + tid / 256; k < n; k += kDT / 256)  // no reflector for the last two columns
     for (int i = tid % 256; i < n; i += 256) p.H[(int64_t)k * n + i] = 0.0;
   __syncthreads();
-  // ---- 2. eigenvalues: scale T by its Gershgorin bound tn
-  double tn = 0.0;
-  for (int i = 0; i < n; ++i) tn = fmax(tn, fabs(sa[i]) + (i > 0 ? fabs(se[i - 1]) : 0.0) + (i < n - 1 ? fabs(se[i]) : 0.0));
-  const double sc = tn > 0 ? 1.0 / tn : 1.0;
-  __syncthreads();
-  for (int i = tid; i < n; i += kDT) {
-    sa[i] *= sc;
-    se[i] *= sc;
-    te2[i] = se[i] * se[i];
-  }
-  __syncthreads();
-  for (int j = warp; j < m; j += kDW) {
-    const int kth = n - 1 - j;  // the (n - 1 - j)-th smallest
-    double l = -1.0 - 1e-12, h = 1.0 + 1e-12;
-    for (int it = 0; it < 11; ++it) {
-      const double x = l + (h - l) * (double)(lane + 1) / 33.0;
-      // sign changes of the leading minors p_0 = 1, p_1 = a_0 - x, p_i = (a_{i-1} - x) p_{i-1} - e_{i-2}^2 p_{i-2}
-      // (T is scaled to ||T|| <= 1, so |p| grows by <= 3 per step: rescaled every 8 steps when it
-      // leaves [1e-100, 1e100]; an exact zero minor counts as a sign change, like a -0 pivot)
-      int cnt = 0;
-      double pm = 1.0, pc = sa[0] - x;
-      bool neg = pc <= 0.0;  // p_0 = 1 > 0; a zero p_1 counts as negative
-      cnt += neg;
-      int i = 1;
-      for (; i + 8 <= n; i += 8) {
-#pragma unroll
-        for (int r = 0; r < 8; ++r) {
-          const double pn = fma(sa[i + r] - x, pc, -te2[i + r - 1] * pm);
-          // sign of a zero minor: opposite to its predecessor's (a -0 pivot); kept off the chain
-          const bool ng = pn == 0.0 ? !neg : pn < 0.0;
-          cnt += ng != neg;
-          neg = ng;
-          pm = pc;
-          pc = pn;
-        }
-        const double an = fabs(pc);
-        if (an > 1e100 || an < 1e-100) {
-          const double f = an > 1e100 ? 1e-100 : 1e100;
-          pc *= f;
-          pm *= f;
-        }
-      }
-      for (; i < n; ++i) {
-        const double pn = fma(sa[i] - x, pc, -te2[i - 1] * pm);
-        const bool ng = pn == 0.0 ? !neg : pn < 0.0;
-        cnt += ng != neg;
-        neg = ng;
-        pm = pc;
-        pc = pn;
-      }
-      const unsigned below = __ballot_sync(0xffffffffu, cnt <= kth);
-      const int nb = __popc(below);  // points 0 .. nb - 1 lie at or left of the target
-      const double nl = nb > 0 ? l + (h - l) * (double)nb / 33.0 : l;
-      const double nh = l + (h - l) * (double)(nb + 1) / 33.0;
-      l = nl;
-      h = nh;
-    }
-    if (lane == 0) lam[j] = 0.5 * (l + h);
-  }
-  __syncthreads();
-  // ---- 3. inverse iteration; workspace: Y [n][m] | per round R vectors x (dl, dd, du, du2) [n][R] | pv bytes [n][R]
-  double* Y = L;
-  const int R = max(1, min(m, (int)((wsz - n * m) / (4 * n + (n + 7) / 8 + 1))));
-  double* dl = Y + n * m;
-  double* dd = dl + n * R;
-  double* du = dd + n * R;
-  double* du2 = du + n * R;
-  unsigned char* pv = reinterpret_cast<unsigned char*>(du2 + n * R);
-  const double eps = 2.2e-16;
-  for (int j0 = 0; j0 < m; j0 += R) {
-    const int t = tid;
-    const int j = j0 + t;
-    if (t < R && j < m) {
-      const double shift = lam[j] + eps * (1.0 + 0.25 * (j & 7));
-#define AT(a, i) a[(i) * R + t]
-      // pivoted LU of T - shift I (LAPACK dgttrf's elimination), the current row carried in registers
-      double cd = sa[0] - shift, cu = n > 1 ? se[0] : 0.0;
-      for (int i = 0; i < n - 1; ++i) {
-        const double li = se[i], nd = sa[i + 1] - shift, nu = i + 1 < n - 1 ? se[i + 1] : 0.0;
-        if (fabs(cd) >= fabs(li)) {
-          const double dv = cd == 0.0 ? eps : cd;
-          const double f = li / dv;
-          AT(dl, i) = f;
-          AT(dd, i) = 1.0 / dv;
-          AT(du, i) = cu;
-          AT(du2, i) = 0.0;
-          pv[i * R + t] = 0;
-          cd = fma(-f, cu, nd);
-          cu = nu;
-        } else {
-          const double f = cd / li;
-          AT(dl, i) = f;
-          AT(dd, i) = 1.0 / li;
-          AT(du, i) = nd;
-          AT(du2, i) = nu;
-          pv[i * R + t] = 1;
-          cd = fma(-f, nd, cu);
-          cu = -f * nu;
-        }
-      }
-      AT(dd, n - 1) = 1.0 / (cd == 0.0 ? eps : cd);
-      // start vector: fixed pseudo-random, in [0.5, 1)
-      for (int i = 0; i < n; ++i) {
-        uint64_t z = (uint64_t)(i + 1) * 0x9E3779B97F4A7C15ull ^ (uint64_t)(j + 7) * 0xBF58476D1CE4E5B9ull;
-        z ^= z >> 31;
-        Y[i * m + j] = 0.5 + (double)(z >> 11) * (1.0 / 9007199254740992.0);
-      }
-      for (int it = 0; it < 2; ++it) {
-        double cy = Y[j];  // forward: L (row swaps as recorded)
-        for (int i = 0; i < n - 1; ++i) {
-          const double ny = Y[(i + 1) * m + j], f = AT(dl, i);
-          if (!pv[i * R + t]) {
-            Y[i * m + j] = cy;
-            cy = fma(-f, cy, ny);
-          } else {
-            Y[i * m + j] = ny;
-            cy = fma(-f, ny, cy);
-          }
-        }
-        // backward: U (reciprocal pivots), y_{i+1}, y_{i+2} carried
-        double y1 = cy * AT(dd, n - 1), y2 = 0.0;
-        Y[(n - 1) * m + j] = y1;
-        double ssq = y1 * y1;
-        for (int i = n - 2; i >= 0; --i) {
-          const double yi = (Y[i * m + j] - AT(du, i) * y1 - AT(du2, i) * y2) * AT(dd, i);
-          Y[i * m + j] = yi;
-          ssq = fma(yi, yi, ssq);
-          y2 = y1;
-          y1 = yi;
-        }
-        const double sN = 1.0 / sqrt(ssq);
-        for (int i = 0; i < n; ++i) Y[i * m + j] *= sN;
-      }
-#undef AT
-    }
-    __syncthreads();
-  }
-  // modified Gram-Schmidt among close eigenvalues (twice)
-  auto csum = [&](double v) {
-    v = wsum(v);
-    if (lane == 0) red[warp] = v;
-    __syncthreads();
-    const double s = wsum(red[lane]);
-    __syncthreads();
-    return s;
-  };
-  for (int j = 1; j < m; ++j) {
-    int i0 = j;
-    while (i0 > 0 && lam[i0 - 1] - lam[i0] <= 1e-9) --i0;
-    if (i0 == j) continue;
-    for (int pass = 0; pass < 2; ++pass) {
-      for (int i = i0; i < j; ++i) {
-        double s = 0.0;
-        for (int r = tid; r < n; r += kDT) s = fma(Y[r * m + i], Y[r * m + j], s);
-        s = csum(s);
-        for (int r = tid; r < n; r += kDT) Y[r * m + j] -= s * Y[r * m + i];
-        __syncthreads();
-      }
-      double s = 0.0;
-      for (int r = tid; r < n; r += kDT) s = fma(Y[r * m + j], Y[r * m + j], s);
-      s = 1.0 / sqrt(csum(s));
-      for (int r = tid; r < n; r += kDT) Y[r * m + j] *= s;
-      __syncthreads();
-    }
-  }
-  // ---- 4. back-transformation, a warp per vector (Yt: [m][n] copy, conflict-free lanes)
-  double* Yt = dl;  // the inverse-iteration arrays are free now (n m <= 4 n R + ... checked on the host)
-  for (int e = tid; e < n * m; e += kDT) {
-    const int jj = e / n, r = e - jj * n;
-    Yt[e] = Y[r * m + jj];
-  }
-  __syncthreads();
-  // reflector rows staged in shared memory in chunks of CH (the workspace past Y and Yt)
-  double* Hs = Yt + (size_t)n * m;
-  const int CH = max(1, min(n, (int)((wsz - 2 * n * m) / n)));
-  for (int k1 = n - 2; k1 > 0; k1 -= CH) {  // rows [k0, k1) of H, applied last to first
-    const int k0 = max(0, k1 - CH);
-    for (int e = tid; e < (k1 - k0) * n; e += kDT) Hs[e] = p.H[(int64_t)k0 * n + e];
-    __syncthreads();
-    for (int jj = warp; jj < m; jj += kDW) {
-      double* y = Yt + (size_t)jj * n;
-      for (int k = k1 - 1; k >= k0; --k) {
-        const double* uk = Hs + (size_t)(k - k0) * n;
-        const double bk = uk[k];  // beta_k sits in the diagonal slot
-        if (bk == 0.0) continue;
-        double s = 0.0;
-        for (int r = k + 1 + lane; r < n; r += 32) s = fma(uk[r], y[r], s);
-        s = bk * wsum(s);
-        for (int r = k + 1 + lane; r < n; r += 32) y[r] -= s * uk[r];
-        __syncwarp();
-      }
-    }
-    __syncthreads();
-  }
-  for (int e = tid; e < n * m; e += kDT) {
-    const int r = e / m, jj = e - r * m;
-    p.V[e] = Yt[(size_t)jj * n + r];
-  }
-  for (int jj = tid; jj < m; jj += kDT) p.theta[jj] = lam[jj] * tn;
-  if (tid < 8) p.info[tid] = tid == 0 || tid == 1 ? 1 : 0;  // converged (direct method), 1 "iteration"
-  if (tid == 0) {
-    double* dv = reinterpret_cast<double*>(p.info + 8);
-    dv[0] = -1.0;  // no Lanczos / filter-bound estimates (eig_check keeps the slot's)
-    dv[1] = -1.0;
-  }
+  eig_tail(n, m, sa, se, te2, L, wsz, lam, red, p.H, nullptr, p.V, p.theta, p.info);
 }
 
 }  // namespace
+
+// the 4-CTA cluster tridiagonalisation (k_tridiag: T = (a, e), reflectors in rows of H, beta)
+// followed by the one-CTA phases 2-4 (TUCKER_EIG_HYBRID=1, d <= 256)
+__global__ void __launch_bounds__(kDT, 1) k_tri_tail(const double* __restrict__ a, const double* __restrict__ e, int n,
+                                                   int m, int ws, const double* __restrict__ H,
+                                                   const double* __restrict__ beta, double* V, double* theta,
+                                                   int* info) {
+  extern __shared__ double sm[];
+  __shared__ double lam[256];
+  __shared__ double red[kDW];
+  double* sa = sm;
+  double* se = sa + n;
+  double* te2 = se + n;
+  double* L = te2 + n;
+  for (int i = threadIdx.x; i < n; i += kDT) {
+    sa[i] = a[i];
+    se[i] = i < n - 1 ? e[i] : 0.0;
+  }
+  __syncthreads();
+  eig_tail(n, m, sa, se, te2, L, ws - 3 * n, lam, red, H, beta, V, theta, info);
+}
 
 // shared memory (doubles) k_eig_direct needs for (n, m); 0: does not fit
 size_t eig_direct_ws(int n, int m) {
@@ -821,6 +852,7 @@ void eig_small(const double* S, int64_t n, int64_t lds, int m, double* V, double
     return;
   }
   scratch.ensure((size_t)(3 * n + n * n + (size_t)m * n + (size_t)m * 5 * n));
+  const bool hybrid = std::getenv("TUCKER_EIG_HYBRID") != nullptr;
   double* a = scratch.p;
   double* e = a + n;
   double* beta = e + n;
@@ -838,6 +870,16 @@ void eig_small(const double* S, int64_t n, int64_t lds, int m, double* V, double
   const size_t smem = (size_t)kRows * kNMax * sizeof(double);
   smem_optin((const void*)k_tridiag, smem);
   TK_LAUNCH(k_tridiag, kCl, kNT, smem, st, p);
+  if (hybrid) {
+    const size_t wsz = std::max<size_t>((size_t)n * m + (size_t)(4 * n + (n + 7) / 8 + 1) * std::min(m, 20),
+                                        (size_t)2 * n * m + 16 * (size_t)n);
+    const size_t ws = 3 * (size_t)n + wsz;
+    if (ws * sizeof(double) <= 218 * 1024) {
+      smem_optin((const void*)k_tri_tail, ws * sizeof(double));
+      TK_LAUNCH(k_tri_tail, 1, kDT, ws * sizeof(double), st, a, e, (int)n, m, (int)ws, H, beta, V, theta, info);
+      return;
+    }
+  }
   TK_LAUNCH(k_tri_eig, 1, 256, 0, st, a, e, (int)n, H, beta, m, Y, F, V, theta, info);
 }
 
