@@ -407,8 +407,15 @@ __device__ void eig_tail(int n, int m, double* sa, double* se, double* te2, doub
                          int* info_out) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   // ---- 2. eigenvalues: scale T by its Gershgorin bound tn
-  double tn = 0.0;
-  for (int i = 0; i < n; ++i) tn = fmax(tn, fabs(sa[i]) + (i > 0 ? fabs(se[i - 1]) : 0.0) + (i < n - 1 ? fabs(se[i]) : 0.0));
+  double tn = 0.0;  // max_i |a_i| + |e_i-1| + |e_i|: per-thread maxima, warp max, then the 32 warp maxima
+  for (int i = tid; i < n; i += kDT) tn = fmax(tn, fabs(sa[i]) + (i > 0 ? fabs(se[i - 1]) : 0.0) + (i < n - 1 ? fabs(se[i]) : 0.0));
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) tn = fmax(tn, __shfl_xor_sync(0xffffffffu, tn, o));
+  if (lane == 0) red[warp] = tn;
+  __syncthreads();
+  tn = red[lane];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) tn = fmax(tn, __shfl_xor_sync(0xffffffffu, tn, o));
   const double sc = tn > 0 ? 1.0 / tn : 1.0;
   __syncthreads();
   for (int i = tid; i < n; i += kDT) {
@@ -420,7 +427,7 @@ __device__ void eig_tail(int n, int m, double* sa, double* se, double* te2, doub
   for (int j = warp; j < m; j += kDW) {
     const int kth = n - 1 - j;  // the (n - 1 - j)-th smallest
     double l = -1.0 - 1e-12, h = 1.0 + 1e-12;
-    for (int it = 0; it < 11; ++it) {
+    for (int it = 0; it < 7; ++it) {  // 33^-7 ~ 2e-11 of the interval: the shift of inverse iteration
       const double x = l + (h - l) * (double)(lane + 1) / 33.0;
       // sign changes of the leading minors p_0 = 1, p_1 = a_0 - x, p_i = (a_{i-1} - x) p_{i-1} - e_{i-2}^2 p_{i-2}
       // (T is scaled to ||T|| <= 1, so |p| grows by <= 3 per step: rescaled every 8 steps when it
@@ -487,18 +494,20 @@ __device__ void eig_tail(int n, int m, double* sa, double* se, double* te2, doub
         const double li = se[i], nd = sa[i + 1] - shift, nu = i + 1 < n - 1 ? se[i + 1] : 0.0;
         if (fabs(cd) >= fabs(li)) {
           const double dv = cd == 0.0 ? eps : cd;
-          const double f = li / dv;
+          const double rv = 1.0 / dv;
+          const double f = li * rv;
           AT(dl, i) = f;
-          AT(dd, i) = 1.0 / dv;
+          AT(dd, i) = rv;
           AT(du, i) = cu;
           AT(du2, i) = 0.0;
           pv[i * R + t] = 0;
           cd = fma(-f, cu, nd);
           cu = nu;
         } else {
-          const double f = cd / li;
+          const double rl = 1.0 / li;
+          const double f = cd * rl;
           AT(dl, i) = f;
-          AT(dd, i) = 1.0 / li;
+          AT(dd, i) = rl;
           AT(du, i) = nd;
           AT(du2, i) = nu;
           pv[i * R + t] = 1;
@@ -513,9 +522,30 @@ __device__ void eig_tail(int n, int m, double* sa, double* se, double* te2, doub
         z ^= z >> 31;
         Y[i * m + j] = 0.5 + (double)(z >> 11) * (1.0 / 9007199254740992.0);
       }
+      // the solves read 8 steps' operands into registers before computing them (no load waits
+      // behind the previous step's store: the chain is the register recurrence only)
       for (int it = 0; it < 2; ++it) {
         double cy = Y[j];  // forward: L (row swaps as recorded)
-        for (int i = 0; i < n - 1; ++i) {
+        int i = 0;
+        for (; i + 8 <= n - 1; i += 8) {
+          double ny[8], fv[8];
+          bool sw[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            ny[u] = Y[(i + u + 1) * m + j];
+            fv[u] = AT(dl, i + u);
+            sw[u] = pv[(i + u) * R + t] != 0;
+          }
+          double out[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            out[u] = sw[u] ? ny[u] : cy;
+            cy = sw[u] ? fma(-fv[u], ny[u], cy) : fma(-fv[u], cy, ny[u]);
+          }
+#pragma unroll
+          for (int u = 0; u < 8; ++u) Y[(i + u) * m + j] = out[u];
+        }
+        for (; i < n - 1; ++i) {
           const double ny = Y[(i + 1) * m + j], f = AT(dl, i);
           if (!pv[i * R + t]) {
             Y[i * m + j] = cy;
@@ -529,7 +559,28 @@ __device__ void eig_tail(int n, int m, double* sa, double* se, double* te2, doub
         double y1 = cy * AT(dd, n - 1), y2 = 0.0;
         Y[(n - 1) * m + j] = y1;
         double ssq = y1 * y1;
-        for (int i = n - 2; i >= 0; --i) {
+        i = n - 2;
+        for (; i >= 7; i -= 8) {
+          double yv[8], uv1[8], uv2[8], rv[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            yv[u] = Y[(i - u) * m + j];
+            uv1[u] = AT(du, i - u);
+            uv2[u] = AT(du2, i - u);
+            rv[u] = AT(dd, i - u);
+          }
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const double yi = (yv[u] - uv1[u] * y1 - uv2[u] * y2) * rv[u];
+            yv[u] = yi;
+            ssq = fma(yi, yi, ssq);
+            y2 = y1;
+            y1 = yi;
+          }
+#pragma unroll
+          for (int u = 0; u < 8; ++u) Y[(i - u) * m + j] = yv[u];
+        }
+        for (; i >= 0; --i) {
           const double yi = (Y[i * m + j] - AT(du, i) * y1 - AT(du2, i) * y2) * AT(dd, i);
           Y[i * m + j] = yi;
           ssq = fma(yi, yi, ssq);
@@ -537,7 +588,18 @@ __device__ void eig_tail(int n, int m, double* sa, double* se, double* te2, doub
           y1 = yi;
         }
         const double sN = 1.0 / sqrt(ssq);
-        for (int i = 0; i < n; ++i) Y[i * m + j] *= sN;
+        for (int i2 = 0; i2 < n; ++i2) Y[i2 * m + j] *= sN;
+      }
+      // the eigenvalue as the Rayleigh quotient y^T T y of the converged vector (the bisection
+      // bracket is only ~2e-11 ||T|| narrow; the quotient's error is O(residual^2))
+      {
+        double rq = 0.0, yp = Y[j];
+        for (int i2 = 0; i2 < n; ++i2) {
+          const double yn = i2 + 1 < n ? Y[(i2 + 1) * m + j] : 0.0;
+          rq = fma(yp, fma(sa[i2], yp, 2.0 * se[i2] * yn), rq);
+          yp = yn;
+        }
+        lam[j] = rq;
       }
 #undef AT
     }
@@ -578,23 +640,94 @@ __device__ void eig_tail(int n, int m, double* sa, double* se, double* te2, doub
     Yt[e] = Y[r * m + jj];
   }
   __syncthreads();
-  // reflector rows staged in shared memory in chunks of CH (the workspace past Y and Yt)
+  // reflector rows staged in shared memory in chunks of CH (the workspace past Y and Yt, minus
+  // room for the blocks' T factors), applied in blocks of kWB as compact-WY products
+  // H_k0 .. H_k0+b-1 = I - V T V^T (T upper triangular, LAPACK dlarft forward / columnwise):
+  // one warp-wide reduction per block instead of per reflector
+  constexpr int kWB = 8;
   double* Hs = Yt + (size_t)n * m;
-  const int CH = max(1, min(n, (int)((wsz - 2 * n * m) / n)));
+  // per chunk row: n doubles of Hs, 1 beta, kWB^2 / kWB = 8 of T (+ one spare block)
+  const int CH = max(kWB, min(n, (int)((wsz - 2 * n * m - 64) / (n + 9)) / kWB * kWB));
+  double* Tb = Hs + (size_t)CH * n;          // T factors of the chunk's blocks (kWB x kWB each)
+  double* bet = Tb + (size_t)(CH / kWB + 1) * kWB * kWB;  // the chunk's betas
   for (int k1 = n - 2; k1 > 0; k1 -= CH) {  // rows [k0, k1) of H, applied last to first
     const int k0 = max(0, k1 - CH);
-    for (int e = tid; e < (k1 - k0) * n; e += kDT) Hs[e] = Hg[(int64_t)k0 * n + e];
+    for (int r = tid; r < k1 - k0; r += kDT) {
+      const int k = k0 + r;
+      bet[r] = betag ? betag[k] : Hg[(int64_t)k * n + k];
+    }
+    for (int e = tid; e < (k1 - k0) * n; e += kDT) {
+      const int r = e / n, c = e - r * n;  // reflector k = k0 + r lives on entries c > k
+      Hs[e] = c > k0 + r ? Hg[(int64_t)k0 * n + e] : 0.0;
+    }
+    __syncthreads();
+    // T factors: blocks [kb0, kb0 + b) from the chunk's top down; dots of the block's columns
+    const int nblk = (k1 - k0 + kWB - 1) / kWB;
+    for (int q = warp; q < nblk * kWB * kWB; q += kDW) {
+      const int blk = q / (kWB * kWB), ij = q - blk * (kWB * kWB), a = ij / kWB, c = ij - a * kWB;
+      const int kb1 = k1 - blk * kWB, kb0 = max(k0, kb1 - kWB);
+      const int bsz = kb1 - kb0;
+      double dotv = 0.0;
+      if (a < c && c < bsz) {
+        const double* va = Hs + (size_t)(kb0 + a - k0) * n;
+        const double* vc = Hs + (size_t)(kb0 + c - k0) * n;
+        for (int r = lane; r < n; r += 32) dotv = fma(va[r], vc[r], dotv);
+        dotv = wsum(dotv);
+      }
+      if (lane == 0) Tb[blk * kWB * kWB + ij] = dotv;  // V_a . V_c above the diagonal, for now
+    }
+    __syncthreads();
+    for (int blk = tid; blk < nblk; blk += kDT) {  // T(0:i, i) = -beta_i T(0:i, 0:i) (V(:, 0:i)^T v_i)
+      const int kb1 = k1 - blk * kWB, kb0 = max(k0, kb1 - kWB);
+      const int bsz = kb1 - kb0;
+      double* T = Tb + blk * kWB * kWB;
+      double dv[kWB][kWB];
+#pragma unroll
+      for (int a = 0; a < kWB; ++a)
+#pragma unroll
+        for (int c = 0; c < kWB; ++c) dv[a][c] = T[a * kWB + c];
+      for (int i = 0; i < kWB; ++i) {
+        const double bi = i < bsz ? bet[kb0 + i - k0] : 0.0;
+        for (int a = 0; a < i; ++a) {
+          double t = 0.0;
+          for (int l = a; l < i; ++l) t = fma(T[a * kWB + l], dv[l][i], t);
+          T[a * kWB + i] = -bi * t;
+        }
+        T[i * kWB + i] = bi;
+        for (int a = i + 1; a < kWB; ++a) T[a * kWB + i] = 0.0;
+      }
+    }
     __syncthreads();
     for (int jj = warp; jj < m; jj += kDW) {
       double* y = Yt + (size_t)jj * n;
-      for (int k = k1 - 1; k >= k0; --k) {
-        const double* uk = Hs + (size_t)(k - k0) * n;
-        const double bk = betag ? betag[k] : uk[k];  // beta_k: separate, or in the diagonal slot
-        if (bk == 0.0) continue;
-        double s = 0.0;
-        for (int r = k + 1 + lane; r < n; r += 32) s = fma(uk[r], y[r], s);
-        s = bk * wsum(s);
-        for (int r = k + 1 + lane; r < n; r += 32) y[r] -= s * uk[r];
+      for (int blk = 0; blk < nblk; ++blk) {  // the chunk's last block first
+        const int kb1 = k1 - blk * kWB, kb0 = max(k0, kb1 - kWB);
+        const double* V = Hs + (size_t)(kb0 - k0) * n;
+        const double* T = Tb + blk * kWB * kWB;
+        double w[kWB];
+#pragma unroll
+        for (int l = 0; l < kWB; ++l) w[l] = 0.0;
+        for (int r = kb0 + 1 + lane; r < n; r += 32) {
+          const double yr = y[r];
+#pragma unroll
+          for (int l = 0; l < kWB; ++l) w[l] = fma(V[(size_t)l * n + r], yr, w[l]);  // rows past the block: zero T
+        }
+#pragma unroll
+        for (int l = 0; l < kWB; ++l) w[l] = wsum(w[l]);
+        double w2[kWB];
+#pragma unroll
+        for (int a = 0; a < kWB; ++a) {
+          double t = 0.0;
+#pragma unroll
+          for (int c = 0; c < kWB; ++c) t = fma(T[a * kWB + c], w[c], t);
+          w2[a] = t;
+        }
+        for (int r = kb0 + 1 + lane; r < n; r += 32) {
+          double yr = y[r];
+#pragma unroll
+          for (int l = 0; l < kWB; ++l) yr = fma(-V[(size_t)l * n + r], w2[l], yr);
+          y[r] = yr;
+        }
         __syncwarp();
       }
     }
@@ -827,6 +960,7 @@ size_t eig_direct_ws(int n, int m) {
   // workspace from L on: Y (n m) + R (4 n + n / 8 + 1) with R >= 1, and the transposed copy (n m)
   size_t wsz = std::max(np, (size_t)n * m + (size_t)(4 * n + (n + 7) / 8 + 1) * std::min(m, 20));
   wsz = std::max(wsz, (size_t)2 * n * m + 16 * (size_t)n);  // + reflector chunks of >= 16 rows
+  wsz = std::max(wsz, (size_t)2 * n * m + 8 * (size_t)(n + 9) + 64);  // >= one block of 8 rows with its T
   const size_t tot = 7 * (size_t)n + 1024 + wsz;
   return tot * sizeof(double) <= 218 * 1024 ? tot : 0;  // + ~6 KB static shared memory <= 227 KB
 }
@@ -871,8 +1005,9 @@ void eig_small(const double* S, int64_t n, int64_t lds, int m, double* V, double
   smem_optin((const void*)k_tridiag, smem);
   TK_LAUNCH(k_tridiag, kCl, kNT, smem, st, p);
   if (hybrid) {
-    const size_t wsz = std::max<size_t>((size_t)n * m + (size_t)(4 * n + (n + 7) / 8 + 1) * std::min(m, 20),
-                                        (size_t)2 * n * m + 16 * (size_t)n);
+    const size_t wsz = std::max<size_t>(std::max<size_t>((size_t)n * m + (size_t)(4 * n + (n + 7) / 8 + 1) * std::min(m, 20),
+                                                         (size_t)2 * n * m + 16 * (size_t)n),
+                                        (size_t)2 * n * m + 8 * (size_t)(n + 9) + 64);
     const size_t ws = 3 * (size_t)n + wsz;
     if (ws * sizeof(double) <= 218 * 1024) {
       smem_optin((const void*)k_tri_tail, ws * sizeof(double));
