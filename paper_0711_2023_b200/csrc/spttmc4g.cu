@@ -73,6 +73,10 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       : "memory");
 }
 
+__device__ __forceinline__ void bulk_prefetch_l2(const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+}
+
 // CTA c of G owns batches [c nb / G, (c + 1) nb / G)
 __host__ __device__ inline int cta_first(int c, int nb, int G) { return (int)(((int64_t)c * nb) / G); }
 
@@ -331,6 +335,8 @@ __global__ void __launch_bounds__(256) k_spttmc4g_reduce(const float* __restrict
 constexpr int kTKC = 32;  // mid1 indices per chunk (one 128-byte swizzle row of K)
 
 struct G4tArgs {
+  int maxck;                // k_spttmc4s: chunk bounds held in shared memory (>= chunks per CTA + 1)
+  int dbg;                  // timing experiments (TUCKER_TTMC4_DBG): 1 skip leaf, 2 skip transpose, 4 skip MMAs, 8 skip level 3
   int bres;                 // the B operands (U_mid1^T split) of every chunk resident in shared memory
   const int4* batch;
   const int32_t* node_mid0;
@@ -626,6 +632,311 @@ __global__ void __launch_bounds__(kNT, 1) k_spttmc4t(G4tArgs p) {
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(64));
 }
 
+// ---------------------------------------------------------------------------
+// k_spttmc4s: k_spttmc4t's arithmetic with the per-chunk phases on separate warp groups, so
+// they overlap: warps 0-7 (leaf) build the plain fiber sums of chunk q + 1 into one of two T
+// buffers while warps 8-11 (transpose) write chunk q's split K-major operands and one of them
+// issues its tcgen05 MMAs; mbarriers hand the T buffers back and forth.  At a batch's end the
+// transpose warps read Z out of TMEM into shared memory and the leaf warps run level 3 (Y in
+// registers, as before) before the next batch.
+// ---------------------------------------------------------------------------
+constexpr int kSL = 256, kSX = 256, kSNT = kSL + kSX;  // leaf threads, transpose threads
+constexpr int kCapS = 1024;                            // staged nonzeros per chunk buffer
+
+__device__ __forceinline__ void named_sync(int id, int n) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+
+template <int CL>
+__global__ void __launch_bounds__(kSNT, 1) k_spttmc4s(G4tArgs p) {
+  extern __shared__ uint8_t sms_raw[];
+  uint8_t* sms = sms_raw + ((1024u - (tc::smem_u32(sms_raw) & 1023u)) & 1023u);
+  constexpr int kST = 3;  // bulk-copy stages (chunk data arrives two chunks ahead)
+  __shared__ __align__(8) uint64_t full[kST], tpf[2], tpe[2], mma_done;
+  __shared__ int st_e0[kST], st_ok[kST];
+  __shared__ uint32_t tmem_slot;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  constexpr int JLP = 4 * CL, NB = 256 / JLP;
+  constexpr int nslot = NB * kTKC;
+  const int J0 = p.J0, J0P = p.J0P, J1 = p.J1;
+  const int P1 = J1 * JLP;
+  // layout: A_hi[2 tiles] A_lo[2 tiles] | B_hi B_lo | Tp[2] | Zs | Uls | u0t[3] | stage[3] | chunk bounds
+  uint8_t* Ahi = sms;
+  uint8_t* Alo = Ahi + 2 * kTA;
+  uint8_t* Bhi = Alo + 2 * kTA;
+  uint8_t* Blo = Bhi + kTB;
+  float* Tp = reinterpret_cast<float*>(Blo + kTB);
+  float* Zs = Tp + 2 * kTKC * kTpLd;
+  float* Uls = Zs + ((NB * P1 + 3) & ~3);
+  float* u0t = Uls + p.I_leaf * JLP;
+  const int U0S = (NB * J0P + 3) & ~3;
+  int* stg = reinterpret_cast<int*>(u0t + 3 * U0S);  // u0t[3]: batch b's rows in u0t[(b - b0) % 3]
+  const int SB = 2 * p.SPC + 2 * kCapS;
+  int* bnd = stg + kST * SB;  // nonzero offset of every chunk of this CTA (+ the end)
+
+  const int b0 = p.b_lo + cta_first(blockIdx.x, p.nb, gridDim.x);
+  const int b1 = p.b_lo + cta_first(blockIdx.x + 1, p.nb, gridDim.x);
+  if (b0 >= b1) return;
+  const int64_t ck0 = (int64_t)b0 * p.NCH, nck = (int64_t)(b1 - b0) * p.NCH;
+  for (int64_t i = tid; i <= nck; i += kSNT) bnd[i] = __ldg(p.sp + (ck0 + i) * p.SPC);
+  // chunks q + 2 .. q + 5 are prefetched into L2 ahead of their bulk copies into shared memory
+  // (a chunk's work is ~1 us: two chunks of shared-memory lookahead do not cover HBM latency)
+  auto prefetch = [&](int64_t q) {
+    if (q >= nck) return;
+    bulk_prefetch_l2(p.sp + (ck0 + q) * p.SPC, (uint32_t)(p.SPC * 4));
+    bulk_prefetch_l2(p.tgt + (ck0 + q) * p.SPC, (uint32_t)(p.SPC * 4));
+    const int E0r = bnd[q] & ~3, E1r = (bnd[q + 1] + 3) & ~3;
+    if (E1r > E0r) {
+      bulk_prefetch_l2(p.leaf + E0r, (uint32_t)(4 * (E1r - E0r)));
+      bulk_prefetch_l2(p.val + E0r, (uint32_t)(4 * (E1r - E0r)));
+    }
+  };
+  auto issue = [&](int64_t q, int E0, int E1) {
+    const int buf = (int)(q % kST);
+    int* sb = stg + buf * SB;
+    const int E0r = E0 & ~3, E1r = (E1 + 3) & ~3;
+    const int n = E1r - E0r;
+    const bool ok = n <= kCapS;
+    st_e0[buf] = E0r;
+    st_ok[buf] = ok ? 1 : 0;
+    tc::mbar_expect_tx(&full[buf], (uint32_t)(p.SPC * 8 + (ok ? 8 * n : 0)));
+    bulk_g2s(sb, p.sp + (ck0 + q) * p.SPC, (uint32_t)(p.SPC * 4), &full[buf]);
+    bulk_g2s(sb + p.SPC, p.tgt + (ck0 + q) * p.SPC, (uint32_t)(p.SPC * 4), &full[buf]);
+    if (ok && n > 0) {
+      bulk_g2s(sb + 2 * p.SPC, p.leaf + E0r, (uint32_t)(4 * n), &full[buf]);
+      bulk_g2s(sb + 2 * p.SPC + kCapS, p.val + E0r, (uint32_t)(4 * n), &full[buf]);
+    }
+  };
+  if (tid == 0) {
+    for (int b = 0; b < kST; ++b) tc::mbar_init(&full[b], 1);
+    for (int b = 0; b < 2; ++b) {
+      tc::mbar_init(&tpf[b], kSL / 32);
+      tc::mbar_init(&tpe[b], kSX / 32);
+    }
+    tc::mbar_init(&mma_done, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 8) {  // (k_spttmc4s: the first transpose warp)
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(tc::smem_u32(&tmem_slot)), "r"(64));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  for (int e = tid; e < p.I_leaf * JLP; e += kSNT) {
+    const int r = e / JLP, j = e - r * JLP;
+    Uls[e] = j < p.Jl ? __ldg(p.Ul + (int64_t)r * p.Jl + j) : 0.f;
+  }
+  for (int o = tid * 16; o < 4 * kTA + 2 * kTB; o += kSNT * 16) *reinterpret_cast<float4*>(sms + o) = make_float4(0.f, 0.f, 0.f, 0.f);
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
+  const uint32_t tmem = tmem_slot;
+
+  if (warp < 8) {
+    // ================= leaf group: T chunks, then level 3 at each batch's end
+    if (tid == 0) {
+      for (int64_t q = 0; q < kST && q < nck; ++q) issue(q, bnd[q], bnd[q + 1]);
+      for (int64_t q = kST; q < kST + 4; ++q) prefetch(q);
+    }
+    // U_mid0 rows of batch b: loaded one batch ahead into u0t[(b - b0) % 3] (the transpose warps
+    // read batch b's at its end, at most one batch behind)
+    auto load_u0 = [&](int b) {
+      if (b >= b1) return;
+      const int4 bt = p.batch[b];
+      float* u0b = u0t + ((b - b0) % 3) * U0S;
+      for (int e = tid; e < NB * J0P; e += kSL) {
+        const int v = e / J0P, a = e - v * J0P;
+        u0b[e] = (v < bt.z && a < J0) ? __ldg(p.U0 + (int64_t)__ldg(p.node_mid0 + bt.y + v) * J0 + a) : 0.f;
+      }
+    };
+    load_u0(b0);
+    int64_t q = 0;
+    for (int b = b0; b < b1; ++b) {
+      const int4 bt = p.batch[b];
+      load_u0(b + 1);
+      for (int kc = 0; kc < p.NCH; ++kc, ++q) {
+        const int tb = (int)(q & 1);
+        const uint32_t use = (uint32_t)(q >> 1);
+        const int sbuf = (int)(q % kST);
+        tc::mbar_wait(&full[sbuf], (uint32_t)((q / kST) & 1));
+        tc::mbar_wait(&tpe[tb], (use & 1) ^ 1);  // the transpose warps are done with T[tb]
+        const int* sb = stg + sbuf * SB;
+        const int E0r = st_e0[sbuf];
+        const bool ok = st_ok[sbuf] != 0;
+        float* T = Tp + tb * kTKC * kTpLd;
+        for (int sl = tid; sl < ((p.dbg & 1) ? 0 : nslot); sl += kSL) {
+          const int e0 = sb[sl], e1 = sb[sl + 1];
+          const int tg = sb[p.SPC + sl];
+          const int v = tg % NB, bl = tg / NB;
+          float4 t[CL];
+#pragma unroll
+          for (int c = 0; c < CL; ++c) t[c] = make_float4(0.f, 0.f, 0.f, 0.f);
+          for (int e = e0; e < e1; ++e) {
+            int l;
+            float x;
+            if (ok) {
+              l = sb[2 * p.SPC + e - E0r];
+              x = __int_as_float(sb[2 * p.SPC + kCapS + e - E0r]);
+            } else {
+              l = __ldg(p.leaf + e);
+              x = __ldg(p.val + e);
+            }
+            const float4* r4 = reinterpret_cast<const float4*>(Uls + l * JLP);
+#pragma unroll
+            for (int c = 0; c < CL; ++c) {
+              const float4 g = r4[c];
+              t[c].x = fmaf(x, g.x, t[c].x);
+              t[c].y = fmaf(x, g.y, t[c].y);
+              t[c].z = fmaf(x, g.z, t[c].z);
+              t[c].w = fmaf(x, g.w, t[c].w);
+            }
+          }
+          float4* Tw = reinterpret_cast<float4*>(T + bl * kTpLd + v * JLP);
+#pragma unroll
+          for (int c = 0; c < CL; ++c) Tw[c] = t[c];
+        }
+        named_sync(1, kSL);  // T[tb] written; stage buffer tb free
+        if (tid == 0 && q + kST < nck) {  // stage buffer sbuf is free: chunk q + 3 into it
+          issue(q + kST, bnd[q + kST], bnd[q + kST + 1]);
+          prefetch(q + kST + 4);
+        }
+        if (lane == 0) tc::mbar_arrive(&tpf[tb]);
+      }
+    }
+  } else {
+    // ================= transpose group: operands, MMAs, Z out of TMEM
+    const int xt = tid - kSL, xw = xt >> 5;  // warp xw of the group: TMEM lane quarter xw & 3, Z tile xw >> 2
+    const uint32_t sA = tc::smem_u32(Ahi), sAl = tc::smem_u32(Alo), sB = tc::smem_u32(Bhi), sBl = tc::smem_u32(Blo);
+    const int k = lane;
+    uint32_t o4[2][4];  // in-atom offsets of rows h + u at column k, h = 0 / 4
+#pragma unroll
+    for (int hh = 0; hh < 2; ++hh)
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int r = 4 * hh + u;
+        o4[hh][u] = (uint32_t)(r * 128 + ((((k >> 2) ^ r) << 4) | ((k & 3) << 2)));
+      }
+    uint32_t mphase = 0;
+    bool pending = false;
+    int64_t q = 0;
+    constexpr int rows = NB * JLP;
+    constexpr int kYC = 2, kYA = 24;  // Y columns xt + 256 u (J1 JLP <= 512), rows a < J0 <= 24
+    float yacc[kYC][kYA];
+#pragma unroll
+    for (int u = 0; u < kYC; ++u)
+#pragma unroll
+      for (int a = 0; a < kYA; ++a) yacc[u][a] = 0.f;
+    int run0 = b0;
+    for (int b = b0; b < b1; ++b) {
+      const int4 bt = p.batch[b];
+      for (int kc = 0; kc < p.NCH; ++kc, ++q) {
+        const int tb = (int)(q & 1);
+        tc::mbar_wait(&tpf[tb], (uint32_t)((q >> 1) & 1));
+        if (pending) {  // the previous chunk's MMAs have read A and B
+          tc::mbar_wait(&mma_done, mphase & 1);
+          ++mphase;
+          pending = false;
+        }
+        const float* T = Tp + tb * kTKC * kTpLd;
+        for (int r4 = xw; r4 < ((p.dbg & 2) ? 0 : rows / 4); r4 += kSX / 32) {
+          const float4 v4 = *reinterpret_cast<const float4*>(T + k * kTpLd + 4 * r4);
+          const int r0 = 4 * r4;
+          const uint32_t base = (uint32_t)((r0 >> 7) * kTA + ((r0 & 127) >> 3) * 1024);
+          const int hh = r4 & 1;
+          t_split(Ahi, Alo, base + o4[hh][0], v4.x);
+          t_split(Ahi, Alo, base + o4[hh][1], v4.y);
+          t_split(Ahi, Alo, base + o4[hh][2], v4.z);
+          t_split(Ahi, Alo, base + o4[hh][3], v4.w);
+        }
+        {
+          const int bb = kc * kTKC + k;
+          for (int r = xw; r < 32; r += kSX / 32) {
+            const float u = (r < J1 && bb < p.I_mid1) ? __ldg(p.U1 + (int64_t)bb * J1 + r) : 0.f;
+            t_split(Bhi, Blo, t_sw128(r, k), u);
+          }
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(&tpe[tb]);  // T[tb] may be refilled
+        named_sync(2, kSX);                          // every operand write is done
+        if (xt == 0 && !(p.dbg & 4)) {
+          tc::tc_fence_after();
+#pragma unroll
+          for (int mt = 0; mt < 2; ++mt) {
+            const uint32_t d = tmem + 32 * mt;
+#pragma unroll
+            for (int ks = 0; ks < kTKC / 8; ++ks) {
+              const uint32_t o = (uint32_t)(ks * 32);
+              const uint32_t ah = sA + mt * kTA + o, al = sAl + mt * kTA + o;
+              tc::umma_tf32(d, tc::sw128_desc(ah), tc::sw128_desc(sB + o), kTIdesc, (kc > 0 || ks > 0) ? 1u : 0u);
+              tc::umma_tf32(d, tc::sw128_desc(ah), tc::sw128_desc(sBl + o), kTIdesc, 1u);
+              tc::umma_tf32(d, tc::sw128_desc(al), tc::sw128_desc(sB + o), kTIdesc, 1u);
+            }
+          }
+          tc::umma_commit(&mma_done);
+        }
+        if (xt == 0 && (p.dbg & 4)) tc::mbar_arrive(&mma_done);
+        pending = true;
+      }
+      // the batch's Z: TMEM row (v, c) of tile mt -> Zs[v][b' JLP + c]
+      tc::mbar_wait(&mma_done, mphase & 1);
+      ++mphase;
+      pending = false;
+      tc::tc_fence_after();
+      {
+        const int mt = xw >> 2, lq = xw & 3;
+        float z[32];
+        tc::tmem_ld32(tmem + ((uint32_t)(32 * lq) << 16) + (uint32_t)(32 * mt), z);
+        tc::tmem_wait_ld();
+        const int r = mt * 128 + lq * 32 + lane;
+        const int v = r / JLP, c = r - v * JLP;
+        if (v < bt.z) {
+#pragma unroll
+          for (int bp = 0; bp < 32; ++bp)
+            if (bp < J1) Zs[v * P1 + bp * JLP + c] = z[bp];
+        }
+      }
+      tc::tc_fence_before();
+      named_sync(2, kSX);  // Zs complete
+      // ---- level 3: Y[a][col] += sum_v U_mid0[a_v][a] Z_v[col] (registers of the transpose warps)
+      const float* u0b = u0t + ((b - b0) % 3) * U0S;
+      const bool run_end = b + 1 == b1 || p.batch[b + 1].x != bt.x;
+#pragma unroll
+      for (int u = 0; u < kYC; ++u) {
+        const int col = xt + kSX * u;
+        if (col < P1) {
+          for (int v = 0; v < ((p.dbg & 8) ? 0 : bt.z); ++v) {
+            const float zz = Zs[v * P1 + col];
+            const float4* u4 = reinterpret_cast<const float4*>(u0b + v * J0P);
+#pragma unroll
+            for (int a4 = 0; a4 < kYA / 4; ++a4) {
+              if (4 * a4 < J0) {
+                const float4 w = u4[a4];
+                yacc[u][4 * a4] = fmaf(w.x, zz, yacc[u][4 * a4]);
+                yacc[u][4 * a4 + 1] = fmaf(w.y, zz, yacc[u][4 * a4 + 1]);
+                yacc[u][4 * a4 + 2] = fmaf(w.z, zz, yacc[u][4 * a4 + 2]);
+                yacc[u][4 * a4 + 3] = fmaf(w.w, zz, yacc[u][4 * a4 + 3]);
+              }
+            }
+          }
+          if (run_end) {
+            float* dst = p.part + (int64_t)(run0 - p.b_lo) * J0 * P1 + col;
+#pragma unroll
+            for (int a = 0; a < kYA; ++a) {
+              if (a < J0) dst[(int64_t)a * P1] = yacc[u][a];
+              yacc[u][a] = 0.f;
+            }
+          }
+        }
+      }
+      if (run_end) run0 = b + 1;
+      named_sync(2, kSX);  // Zs consumed before the next batch's Z
+    }
+  }
+  tc::tc_fence_before();
+  __syncthreads();
+  if (warp == 8) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(64));
+}
+
 // ---- dense batch layout builder ----
 __global__ void k_g4_node(const int32_t* __restrict__ slice_ptr, int64_t nslice, const int32_t* __restrict__ bfirst,
                           int64_t nnode, int NB, int NCH, int SPC, int32_t* __restrict__ node_base) {
@@ -719,6 +1030,14 @@ static size_t g4t_smem(const Csf& c, int J0, int Jl, int NB, int SPC, bool bres)
   const int64_t fl = (int64_t)kTKC * kTpLd + c.I_leaf * JLP + round_up((int64_t)NB * J0P, 4);
   const size_t b = bres ? 1024 + (size_t)ceil_div(c.I_mid1, kTKC) * 2 * kTB : 0;
   return 1024 + 4 * kTA + 2 * kTB + (size_t)(fl + 2 * (2 * SPC + 2 * kCap)) * 4 + b;
+}
+
+// bytes of dynamic shared memory of k_spttmc4s
+static size_t g4s_smem(const Csf& c, int J0, int J1, int Jl, int NB, int SPC, int maxck) {
+  const int JLP = (int)round_up(Jl, 4), J0P = (int)round_up(J0, 4);
+  const int64_t fl = 2 * (int64_t)kTKC * kTpLd + round_up((int64_t)NB * J1 * JLP, 4) + c.I_leaf * JLP +
+                     3 * round_up((int64_t)NB * J0P, 4);
+  return 1024 + 4 * kTA + 2 * kTB + (size_t)(fl + 3 * (2 * SPC + 2 * kCapS)) * 4 + (size_t)maxck * 4;
 }
 
 // The dense batch layout of ordering c for (NB nodes per batch, KCH mid1 indices per chunk),
@@ -816,9 +1135,15 @@ bool spttmc4g(const Csf& c, const float* const* U, const int64_t* J, Split out, 
   // default: the FMA kernel (measured at config 4: 0.51 ms per mode vs 0.65 ms for the tcgen05
   // kernel, whose per-chunk phases -- leaf, transpose, MMA issue -- are latency / barrier bound
   // with one 8-warp CTA per SM; tensor pipe 6 % busy)
-  const bool use_tc = fc == 't' ? tc_ok : false;
+  // (the transpose warps hold Y: J1 JLP <= 2 x 256 columns, J0 <= 24 rows; >= 3 chunks per batch keep
+  // the leaf warps within one batch of them, so two U_mid0 buffers suffice)
+  const int maxck_est = 1024;  // bound on chunks per CTA (4 KB of bounds), checked at launch
+  const bool s_ok = J1 <= 32 && J0 <= 24 && (int64_t)J1 * JLP <= 2 * kSX && ceil_div(c.I_mid1, kTKC) >= 3 &&
+                    g4s_smem(c, J0, J1, Jl, NBt, SPCt, maxck_est) <= 220 * 1024;
+  const bool use_s = fc == 's' ? s_ok : false;
+  const bool use_tc = use_s || (fc == 't' ? tc_ok : false);
   if (!use_tc && !g_ok) return false;
-  if (fc == 't' && !tc_ok) return false;
+  if ((fc == 't' && !tc_ok) || (fc == 's' && !s_ok)) return false;
   const int NB = use_tc ? NBt : NBg, KCH = use_tc ? kTKC : kKCH, SPC = use_tc ? SPCt : SPCg;
   const int NCH = (int)ceil_div(c.I_mid1, KCH);
   if (!g4_layout(c, NB, KCH, st)) return false;
@@ -858,6 +1183,21 @@ bool spttmc4g(const Csf& c, const float* const* U, const int64_t* J, Split out, 
       a.nb = nb;
       a.part = g.part.p;
       a.bres = bres ? 1 : 0;
+      a.dbg = std::getenv("TUCKER_TTMC4_DBG") ? std::atoi(std::getenv("TUCKER_TTMC4_DBG")) : 0;
+      if (use_s) {
+        a.maxck = (int)(ceil_div(nb, G) * NCH + 8);
+        if (a.maxck > maxck_est) fail(TUCKER_E_ARG, "spttmc4s: too many chunks per CTA");
+        const size_t smem_s = g4s_smem(c, J0, J1, Jl, NB, SPC, a.maxck);
+        switch (CL) {
+#define TK_G4S(cl)                                                     \
+  case cl:                                                             \
+    smem_optin((const void*)k_spttmc4s<cl>, smem_s);                   \
+    TK_LAUNCH(k_spttmc4s<cl>, (unsigned)G, kSNT, smem_s, st, a);       \
+    break;
+          TK_G4S(1) TK_G4S(2) TK_G4S(3) TK_G4S(4) TK_G4S(5) TK_G4S(6) TK_G4S(7) TK_G4S(8)
+#undef TK_G4S
+        }
+      } else {
       const size_t smem = g4t_smem(c, J0, Jl, NB, SPC, bres);
       switch (CL) {
 #define TK_G4T(cl)                                                     \
@@ -867,6 +1207,7 @@ bool spttmc4g(const Csf& c, const float* const* U, const int64_t* J, Split out, 
     break;
         TK_G4T(1) TK_G4T(2) TK_G4T(3) TK_G4T(4) TK_G4T(5) TK_G4T(6) TK_G4T(7) TK_G4T(8)
 #undef TK_G4T
+      }
       }
     } else {
       G4Args a;

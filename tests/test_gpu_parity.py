@@ -143,7 +143,7 @@ def test_ttmc_parity_order4_shapes(capi, dims, nnz, core):
                                             ((20, 22, 18, 16), 12_000, (4, 5, 3, 6)),
                                             ((40, 200, 30, 20), 48_000, (5, 6, 20, 8)),
                                             ((7, 300, 37, 21), 60_000, (3, 21, 9, 13))])
-@pytest.mark.parametrize("kern", ["g", "t"])
+@pytest.mark.parametrize("kern", ["g", "t", "s"])
 def test_ttmc_parity_order4_gemm(capi, monkeypatch, dims, nnz, core, kern):
     """Order-4 GEMM-form SpTTMc (k_spttmc4g on the FMA pipes, k_spttmc4t with level 2
     on tcgen05 in 3xTF32; forced with TUCKER_TTMC4=g / t even where the dispatch

@@ -4,7 +4,7 @@ mkdir -p gpurun_out
 python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build.log 2>&1 || { cat gpurun_out/build.log; exit 1; }
 if [ -n "$TESTS" ]; then timeout ${TEST_TIMEOUT:-1200} python -m pytest tests -m gpu -x -q -rs -k "$TESTS" > gpurun_out/it_tests.log 2>&1; echo "tests rc=$?" >> gpurun_out/it_tests.log; fi
 if [ -n "$TTMC" ]; then
-  for c in $TTMC; do timeout 300 python tools/ttmc_time.py $c 20 >> gpurun_out/it_ttmc.log 2>&1; TUCKER_TTMC4=g timeout 300 python tools/ttmc_time.py $c 20 | sed "s/^/g: /" >> gpurun_out/it_ttmc.log 2>&1; done
+  for c in $TTMC; do timeout 300 python tools/ttmc_time.py $c 20 >> gpurun_out/it_ttmc.log 2>&1; TUCKER_TTMC4=g timeout 300 python tools/ttmc_time.py $c 20 | sed "s/^/g: /" >> gpurun_out/it_ttmc.log 2>&1; TUCKER_TTMC4=s timeout 300 python tools/ttmc_time.py $c 20 | sed "s/^/s: /" >> gpurun_out/it_ttmc.log 2>&1; done
 fi
 [ -n "$MICRO" ] && ./tools/lds_uniform_bench > gpurun_out/it_micro.log 2>&1
 if [ -n "$BENCH" ]; then timeout 900 python bench.py $BENCH > gpurun_out/it_bench.log 2>&1; echo "bench rc=$?" >> gpurun_out/it_bench.log; fi
