@@ -191,7 +191,9 @@ def mp_overlap_on(c):
     """The library's MP overlap (TUCKER_MP_OVERLAP, default on; dense-W route, order >= 3):
     the main stream's projection / Gram stages then hold only the late term (m = n - 1) of
     each mode; the other terms run beside the previous mode's eigensolve."""
-    return os.environ.get("TUCKER_MP_OVERLAP", "1") != "0" and len(c["dims"]) >= 3 and c["nnz"] < 1e8
+    # (only beside the one-CTA direct eigensolver: MP Grams of d <= 224 -- config 4, not config 2's d = 1000)
+    return (os.environ.get("TUCKER_MP_OVERLAP", "1") != "0" and len(c["dims"]) >= 3 and c["nnz"] < 1e8
+            and max(c["dims"]) <= 224)
 
 
 def gram_flops(c, late_only=False):

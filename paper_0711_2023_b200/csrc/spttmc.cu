@@ -1011,6 +1011,72 @@ __global__ void __launch_bounds__(32 * kSpW, 6) k_spmm_w(SpmmArgs p) {
 
 inline int rtile(int J) { return (J + 15) / 16; }  // 1..8
 
+// MP leaf SpMM for wide factor rows (J > 24) or factor tables too large for shared memory
+// (config 2: U 1000 x 50 = 200 KB): lanes over the J columns instead of lane per fiber, so the
+// U row gathers are coalesced (one 128-byte line per 32 columns of a row) and each store
+// instruction writes 32 consecutive W columns of one row (one K-tile row segment).  A warp takes
+// 32 consecutive fibers (metadata loaded coalesced, broadcast by shuffles) and walks them four
+// at a time so four fibers' gathers are in flight together.
+constexpr int kSpC = 8;  // warps per block
+__global__ void __launch_bounds__(32 * kSpC) k_spmm_wc(SpmmArgs p) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const unsigned full = 0xffffffffu;
+  const bool sharded = p.s_lo > 0 || p.s_hi < p.s_all;
+  const int64_t kt_stride = 32 * p.ldW;
+  const int64_t nwarps = (int64_t)gridDim.x * kSpC;
+  for (int64_t base = (blockIdx.x * (int64_t)kSpC + warp) * 32; base < p.nfib; base += nwarps * 32) {
+    const int64_t f = base + lane;
+    int64_t mk = 0, root = -1;
+    int e0 = 0, e1 = 0;
+    if (f < p.nfib) {
+      mk = __ldg(p.fib_mid0 + f);
+      if (p.fib_mid1) mk = mk * p.I_mid1 + __ldg(p.fib_mid1 + f);
+      root = __ldg(p.fib_root + f);
+      e0 = __ldg(p.fib_ptr + f);
+      e1 = __ldg(p.fib_ptr + f + 1);
+      if (sharded && (mk < p.s_lo || mk >= p.s_hi)) e1 = e0 = 0, root = -1;
+    }
+    const int nf = (int)(p.nfib - base < 32 ? p.nfib - base : 32);
+    for (int k0 = 0; k0 < nf; k0 += 4) {
+      int ke0[4], ke1[4];
+      int64_t kr[4], kc[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int kk = min(k0 + u, 31);
+        ke0[u] = __shfl_sync(full, e0, kk);
+        ke1[u] = k0 + u < nf ? __shfl_sync(full, e1, kk) : ke0[u];
+        kr[u] = __shfl_sync(full, root, kk);
+        kc[u] = p.col_off + (__shfl_sync(full, mk, kk) - p.s_lo) * p.J;
+      }
+      for (int jb = 0; jb < p.J; jb += 32) {
+        const int j = jb + lane;
+        float acc[4] = {0.f, 0.f, 0.f, 0.f};
+        int lmax = 0;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) lmax = max(lmax, ke1[u] - ke0[u]);
+        for (int t = 0; t < lmax; ++t) {
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            if (t < ke1[u] - ke0[u]) {
+              const int e = ke0[u] + t;
+              const int l = __ldg(p.leaf_id + e);
+              const float x = __ldg(p.val + e);
+              if (j < p.J) acc[u] = fmaf(x, __ldg(p.U + (int64_t)l * p.J + j), acc[u]);
+            }
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          if (k0 + u < nf && kr[u] >= 0 && j < p.J) {
+            const int64_t c = kc[u] + j;
+            split_store(p.Whi, p.Wlo, (c >> 5) * kt_stride + kr[u] * 32 + (c & 31), acc[u]);
+          }
+        }
+      }
+    }
+  }
+}
+
 }  // namespace
 
 // Kolda stride of mode `m` among the modes `others` (ascending lower-fastest).
@@ -1375,6 +1441,13 @@ void spmm_mp(const Csf& c, const float* U_leaf, int64_t J_leaf, Split out, int64
     if (g_launch_counter) ++(*g_launch_counter);
     if (sync_check_enabled()) TK_CUDA(cudaStreamSynchronize(st));
   };
+  if (J_leaf >= 32 && J_leaf <= 64 && !sm) {  // rows gathered from global memory: column lanes (k_spmm_wc;
+    // measured: config 2 (J = 50) 0.85 -> ~0.2 ms per term; config 3 J = 100 keeps the lane-per-fiber kernel)
+    const unsigned cblocks = (unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(c.nfib, 32 * kSpC),
+                                                                            8 * std::max(1, nsm - g_sm_reserve)));
+    TK_LAUNCH(k_spmm_wc, cblocks, 32 * kSpC, 0, st, a);
+    return;
+  }
 #define TK_SPW(qv)                                         \
   if (sm) go((const void*)k_spmm_w<qv, true>);             \
   else go((const void*)k_spmm_w<qv, false>);

@@ -559,6 +559,14 @@ bool mp_overlap_ok(tucker_handle* h, int n) {
   const bool off = e && e[0] == '0';
   return !off && !h->sharded && h->order >= 3 && !mp_use_sparse(h, n, -1);
 }
+// mode n's MP eigensolve is the one-CTA direct solver (solve_eig's rule): only then is there a
+// GPU to share -- the fused solver is a cooperative grid over every SM (config 2's d = 1000)
+bool mp_eig_direct(tucker_handle* h, int n) {
+  const int64_t d = h->dims[n];
+  const bool iter_opts = h->opts.eig_max_iter > 0 || h->opts.eig_tol > 0;
+  return !std::getenv("TUCKER_EIG_FUSED") && !iter_opts && d >= 3 && d <= kSmallMaxD &&
+         eig_direct_ws((int)d, (int)h->J[n]) > 0;
+}
 
 
 
@@ -1043,7 +1051,7 @@ int mp_sweep(tucker_handle* h, int sweeps, double* fit_per_sweep, float* stage_m
         const bool more = n + 1 < N || s + 1 < sweeps;
         if (mp_overlap_ok(h, n)) {
           mp_update_overlap(h, n, h->slots[1][n], ev.e[4 * n + 1], ev.e[4 * n + 2],
-                            more && mp_overlap_ok(h, nn) ? nn : -1);
+                            more && mp_overlap_ok(h, nn) && mp_eig_direct(h, n) ? nn : -1);
         } else {
           mp_update(h, n, -1, h->slots[1][n], ev.e[4 * n + 1], ev.e[4 * n + 2]);
         }
