@@ -20,6 +20,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 
 #include "internal.cuh"
@@ -390,7 +391,17 @@ struct DirArgs {
   double* V;    // n x m, ld m
   double* theta;
   int* info;
+  unsigned long long* prof;  // nullable: per-phase globaltimer stamps (TUCKER_EIG_PROF, tools)
+  int dbg;                   // TUCKER_EIG_DBG (timing experiments; wrong results): 1 skip phase 2, 2 skip phase 1
 };
+
+__device__ __forceinline__ void stamp(unsigned long long* prof, int slot) {
+  if (prof != nullptr && threadIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    prof[slot] = t;
+  }
+}
 
 __device__ __forceinline__ int pidx(int i, int j) { return (i * (i + 1)) / 2 + j; }
 __device__ __forceinline__ double wsum(double v) {
@@ -404,7 +415,7 @@ __device__ __forceinline__ double wsum(double v) {
 // shared-memory workspace L of wsz doubles; V (n x m, ld m), theta (m), info record
 __device__ void eig_tail(int n, int m, double* sa, double* se, double* te2, double* L, int wsz, double* lam,
                          double* red, const double* Hg, const double* betag, double* Vout, double* theta_out,
-                         int* info_out) {
+                         int* info_out, unsigned long long* prof = nullptr) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   // ---- 2. eigenvalues: scale T by its Gershgorin bound tn
   double tn = 0.0;  // max_i |a_i| + |e_i-1| + |e_i|: per-thread maxima, warp max, then the 32 warp maxima
@@ -473,6 +484,7 @@ __device__ void eig_tail(int n, int m, double* sa, double* se, double* te2, doub
     if (lane == 0) lam[j] = 0.5 * (l + h);
   }
   __syncthreads();
+  stamp(prof, 3);
   // ---- 3. inverse iteration; workspace: Y [n][m] | per round R vectors x (dl, dd, du, du2) [n][R] | pv bytes [n][R]
   double* Y = L;
   const int R = max(1, min(m, (int)((wsz - n * m) / (4 * n + (n + 7) / 8 + 1))));
@@ -605,6 +617,7 @@ __device__ void eig_tail(int n, int m, double* sa, double* se, double* te2, doub
     }
     __syncthreads();
   }
+  stamp(prof, 4);
   // modified Gram-Schmidt among close eigenvalues (twice)
   auto csum = [&](double v) {
     v = wsum(v);
@@ -633,6 +646,7 @@ __device__ void eig_tail(int n, int m, double* sa, double* se, double* te2, doub
       __syncthreads();
     }
   }
+  stamp(prof, 5);
   // ---- 4. back-transformation, a warp per vector (Yt: [m][n] copy, conflict-free lanes)
   double* Yt = dl;  // the inverse-iteration arrays are free now (n m <= 4 n R + ... checked on the host)
   for (int e = tid; e < n * m; e += kDT) {
@@ -681,20 +695,28 @@ __device__ void eig_tail(int n, int m, double* sa, double* se, double* te2, doub
       const int kb1 = k1 - blk * kWB, kb0 = max(k0, kb1 - kWB);
       const int bsz = kb1 - kb0;
       double* T = Tb + blk * kWB * kWB;
-      double dv[kWB][kWB];
+      // fully unrolled so column i's dots sit in registers (r1: a dynamically indexed 8 x 8 local
+      // array, i.e. local-memory round trips on the chain)
 #pragma unroll
-      for (int a = 0; a < kWB; ++a)
-#pragma unroll
-        for (int c = 0; c < kWB; ++c) dv[a][c] = T[a * kWB + c];
       for (int i = 0; i < kWB; ++i) {
+        double dcol[kWB];  // V_l . V_i, l < i (column i above the diagonal, overwritten below)
+#pragma unroll
+        for (int l = 0; l < kWB; ++l) dcol[l] = l < i ? T[l * kWB + i] : 0.0;
         const double bi = i < bsz ? bet[kb0 + i - k0] : 0.0;
-        for (int a = 0; a < i; ++a) {
-          double t = 0.0;
-          for (int l = a; l < i; ++l) t = fma(T[a * kWB + l], dv[l][i], t);
-          T[a * kWB + i] = -bi * t;
+#pragma unroll
+        for (int a = 0; a < kWB; ++a) {
+          if (a < i) {
+            double t = 0.0;
+#pragma unroll
+            for (int l = 0; l < kWB; ++l)
+              if (l >= a && l < i) t = fma(T[a * kWB + l], dcol[l], t);
+            T[a * kWB + i] = -bi * t;
+          }
         }
         T[i * kWB + i] = bi;
-        for (int a = i + 1; a < kWB; ++a) T[a * kWB + i] = 0.0;
+#pragma unroll
+        for (int a = 0; a < kWB; ++a)
+          if (a > i) T[a * kWB + i] = 0.0;
       }
     }
     __syncthreads();
@@ -733,6 +755,7 @@ __device__ void eig_tail(int n, int m, double* sa, double* se, double* te2, doub
     }
     __syncthreads();
   }
+  stamp(prof, 6);
   for (int e = tid; e < n * m; e += kDT) {
     const int r = e / m, jj = e - r * m;
     Vout[e] = Yt[(size_t)jj * n + r];
@@ -744,6 +767,7 @@ __device__ void eig_tail(int n, int m, double* sa, double* se, double* te2, doub
     dv[0] = -1.0;  // no Lanczos / filter-bound estimates (eig_check keeps the slot's)
     dv[1] = -1.0;
   }
+  stamp(prof, 7);
 }
 
 __global__ void __launch_bounds__(kDT, 1) k_eig_direct(DirArgs p) {
@@ -762,10 +786,11 @@ __global__ void __launch_bounds__(kDT, 1) k_eig_direct(DirArgs p) {
   double* pb = te2 + n;
   double* L = pb + 1024;
   const int wsz = p.ws - 7 * n - 1024;  // doubles from L on
-
+  stamp(p.prof, 0);
   for (int i = warp; i < n; i += kDW)
     for (int j = lane; j <= i; j += 32) L[pidx(i, j)] = p.S[(int64_t)i * p.lds + j];
   __syncthreads();
+  stamp(p.prof, 1);
   if (n >= 3) {  // first column (k = 0) and its norm
     double ss = 0.0;
     for (int i = 1 + warp; i < n; i += kDW) {
@@ -927,9 +952,244 @@ __global__ void __launch_bounds__(kDT, 1) k_eig_direct(DirArgs p) {
   for (int k = max(0, n - 2) + tid / 256; k < n; k += kDT / 256)  // no reflector for the last two columns
     for (int i = tid % 256; i < n; i += 256) p.H[(int64_t)k * n + i] = 0.0;
   __syncthreads();
-  eig_tail(n, m, sa, se, te2, L, wsz, lam, red, p.H, nullptr, p.V, p.theta, p.info);
+  stamp(p.prof, 2);
+  eig_tail(n, m, sa, se, te2, L, wsz, lam, red, p.H, nullptr, p.V, p.theta, p.info, p.prof);
 }
 
+
+// ---- the tiled one-CTA tridiagonalisation (n <= 208; r2 default for the direct solver) ----
+// S (both triangles' values: the lower triangle's tiles; diagonal tiles full) as 16 x 16 fp64
+// tiles in shared memory, element (r, c) of a tile at c * 16 + (r ^ c): a half-warp reading a
+// tile column (lanes = rows) or a tile row (lanes = columns) touches 16 distinct bank pairs, so
+// both the row and the transposed column sweeps are conflict-free (the packed triangle of
+// k_eig_direct read rows at lane strides of ~i doubles).  Per column k, two block barriers:
+//   phase 1 (threads = rows i > k): the reflector of x_k = A[k+1.., k] (alpha, beta, u), from
+//     the partial sums s = A x_k of the previous pass: p = beta (s - alpha A e_k1), K = beta^2 / 2
+//     u^T A u with u^T A u = x^T A x - 2 alpha s_k1 + alpha^2 A_k1k1 (x^T A x from per-warp tile
+//     partials), q = p - K u, and the next column x_{k+1} = (A - u q^T - q u^T)[k+2.., k+1];
+//   phase 2 (warps = tiles of the active trailing block): A -= u q^T + q u^T and, in the same
+//     sweep, the partial sums of A_new x_{k+1} (row sums, then the transposed column sums of
+//     off-diagonal tiles) and x^T A_new x.
+// One read + write of the trailing matrix per column (k_eig_direct: a product read and an
+// update read + write).  Symmetric matrix; the reflectors are LAPACK dsytd2's (lower).
+constexpr int kTB = 16;           // tile edge
+constexpr int kTNB = 13;          // tile blocks: n <= 208
+constexpr int kTN = kTB * kTNB;   // 208
+
+__device__ __forceinline__ int toff(int I, int J) { return ((I * (I + 1)) / 2 + J) * (kTB * kTB); }  // I >= J
+__device__ __forceinline__ int tel(int r, int c) { return c * kTB + (r ^ c); }
+__device__ __forceinline__ int tat(int i, int j) {  // element (i, j), any order
+  const int a = max(i, j), b = min(i, j);
+  return toff(a >> 4, b >> 4) + tel(a & 15, b & 15);
+}
+
+// phase 2 over the tiles (I, J), B0 <= J <= I < nb: update with (u, q), partial sums of A x
+// into pb[(I nb + J) 16 + r] (row part of tile (I, J)) and pb[(J nb + I) 16 + c] (column part)
+__device__ __forceinline__ void tri_pass(double* T, double* pb, const double2* uq, const double* x, int nb, int B0,
+                                         int warp, int lane, double* xpart) {
+  // uq[i] = (u_i, q_i).  Shared-memory operands are staged in registers four columns at a time
+  // before the tile's stores (the compiler cannot move loads across stores into the same array:
+  // a load -> fma -> store chain per element was ~2.5x slower)
+  const int mb = nb - B0;
+  const int nt = mb * (mb + 1) / 2;
+  const int r = lane & 15, h = lane >> 4;
+  double xs = 0.0;
+  for (int t = warp; t < nt; t += kDW) {
+    int a = 0;
+    while ((a + 1) * (a + 2) / 2 <= t) ++a;
+    const int I = B0 + a, J = B0 + (t - a * (a + 1) / 2);
+    double* Tt = T + toff(I, J);
+    const double2 wr = uq[I * kTB + r];
+    const double xr = x[I * kTB + r];
+    double racc0 = 0.0, racc1 = 0.0;
+#pragma unroll
+    for (int c4 = 0; c4 < 8; c4 += 4) {
+      double av[4], xc[4];
+      double2 wc[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int c = h * 8 + c4 + j;
+        av[j] = Tt[c * kTB + (r ^ c)];
+        wc[j] = uq[J * kTB + c];
+        xc[j] = x[J * kTB + c];
+      }
+      if (I != J) {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) av[j] = fma(-wr.x, wc[j].y, fma(-wr.y, wc[j].x, av[j]));
+      } else {  // diagonal tile, both triangles: a symmetric update formula keeps it exactly symmetric
+#pragma unroll
+        for (int j = 0; j < 4; ++j) av[j] = av[j] - __dadd_rn(__dmul_rn(wr.x, wc[j].y), __dmul_rn(wr.y, wc[j].x));
+      }
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int c = h * 8 + c4 + j;
+        Tt[c * kTB + (r ^ c)] = av[j];
+      }
+      racc0 = fma(av[0], xc[0], racc0);
+      racc1 = fma(av[1], xc[1], racc1);
+      racc0 = fma(av[2], xc[2], racc0);
+      racc1 = fma(av[3], xc[3], racc1);
+    }
+    double racc = racc0 + racc1;
+    racc += __shfl_xor_sync(0xffffffffu, racc, 16);
+    if (h == 0) {
+      pb[(I * nb + J) * kTB + r] = racc;
+      xs = fma(I != J ? 2.0 * xr : xr, racc, xs);
+    }
+    if (I != J) {  // column sums of the updated tile: lanes = columns, rows split by half-warp
+      __syncwarp();
+      double c0 = 0.0, c1 = 0.0;
+#pragma unroll
+      for (int r4 = 0; r4 < 8; r4 += 4) {
+        double av[4], xv[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int r2 = h * 8 + r4 + j;
+          av[j] = Tt[r * kTB + (r2 ^ r)];
+          xv[j] = x[I * kTB + r2];
+        }
+        c0 = fma(av[0], xv[0], c0);
+        c1 = fma(av[1], xv[1], c1);
+        c0 = fma(av[2], xv[2], c0);
+        c1 = fma(av[3], xv[3], c1);
+      }
+      double cacc = c0 + c1;
+      cacc += __shfl_xor_sync(0xffffffffu, cacc, 16);
+      if (h == 0) pb[(J * nb + I) * kTB + r] = cacc;
+    }
+  }
+  xs = wsum(xs);
+  if (lane == 0) xpart[warp] = xs;
+}
+
+__global__ void __launch_bounds__(kDT, 1) k_eig_direct_t(DirArgs p) {
+  extern __shared__ double sm[];
+  __shared__ double npart[2][kDW], xpart[kDW];
+  __shared__ double lam[256];
+  __shared__ double red[kDW];
+  const int n = p.n, m = p.m, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int nb = (n + kTB - 1) / kTB;
+  // layout: sa | se | te2 | u | q | x[2] (kTN each) | pb (nb nb 16) | tiles; from pb on: the tail's workspace
+  double* sa = sm;
+  double* se = sa + kTN;
+  double* te2 = se + kTN;
+  double2* uq = reinterpret_cast<double2*>(te2 + kTN);  // (u_i, q_i) interleaved
+  double* xb = te2 + 3 * kTN;
+  double* pb = xb + 2 * kTN;
+  double* T = pb + nb * nb * kTB;
+  const int wsz = p.ws - 7 * kTN;
+  stamp(p.prof, 0);
+  for (int e = tid; e < 4 * kTN; e += kDT) te2[kTN + e] = 0.0;  // uq, x[0], x[1]
+  const int ntile = nb * (nb + 1) / 2;
+  for (int e = tid; e < ntile * kTB * kTB; e += kDT) {
+    const int t = e >> 8, w = e & 255;
+    int I = 0;
+    while ((I + 1) * (I + 2) / 2 <= t) ++I;
+    const int J = t - I * (I + 1) / 2;
+    const int c = w >> 4, r = (w & 15) ^ c;
+    const int i = I * kTB + r, j = J * kTB + c;
+    double v = 0.0;
+    if (i < n && j < n) v = i >= j ? p.S[(int64_t)i * p.lds + j] : p.S[(int64_t)j * p.lds + i];
+    T[e] = v;
+  }
+  __syncthreads();
+  stamp(p.prof, 1);
+  {  // x_0 = A[1.., 0] and its norm
+    double ss = 0.0;
+    for (int i = tid; i < n; i += kDT)
+      if (i >= 1) {
+        const double v = T[tat(i, 0)];
+        xb[i] = v;
+        ss = fma(v, v, ss);
+      }
+    ss = wsum(ss);
+    if (lane == 0) npart[0][warp] = ss;
+  }
+  __syncthreads();
+  tri_pass(T, pb, uq, xb, nb, 0, warp, lane, xpart);  // u = q = 0: the product A x_0 only
+  __syncthreads();
+  long long cyc[4] = {0, 0, 0, 0};  // TUCKER_EIG_PROF: thread 0's cycles in phase 1 / barrier / phase 2 / barrier
+  const bool pr0 = p.prof != nullptr && tid == 0;
+  const int dbg = p.dbg;
+  for (int k = 0; k < n - 2; ++k) {
+    long long c0 = pr0 ? clock64() : 0;
+    const int k1 = k + 1;
+    const double* xc = xb + (k & 1) * kTN;
+    double* xn = xb + ((k + 1) & 1) * kTN;
+    const int bprev = k >> 4;  // first tile block of the previous pass
+    const int nr = n - k;      // rows k .. n - 1
+    if (warp < (nr + 31) >> 5 && !(dbg & 2)) {
+      const double nx2 = wsum(npart[k & 1][lane]);
+      const double xax = wsum(xpart[lane]);
+      const double x0 = xc[k1];
+      const double nx = sqrt(nx2);
+      const double alpha = x0 >= 0 ? -nx : nx;
+      const double uu = 2.0 * (nx2 - alpha * x0);
+      const double beta = uu > 0 ? 2.0 / uu : 0.0;
+      const double u1 = x0 - alpha;
+      double sk1 = 0.0;
+      {
+        const double* pr = pb + ((k1 >> 4) * nb) * kTB + (k1 & 15);
+        for (int b = bprev; b < nb; ++b) sk1 += pr[b * kTB];
+      }
+      const double a11 = T[tat(k1, k1)];
+      const double uau = fma(alpha * alpha, a11, fma(-2.0 * alpha, sk1, xax));
+      const double K = 0.5 * beta * beta * uau;
+      const double q1 = fma(-K, u1, beta * fma(-alpha, a11, sk1));
+      const int i = k + tid;
+      double ss = 0.0;
+      if (i == k) {
+        uq[k] = make_double2(0.0, 0.0);
+        xn[k] = 0.0;
+        sa[k] = T[tat(k, k)];
+        se[k] = alpha;
+        p.H[(int64_t)k * n + k] = beta;
+      } else if (i < n) {
+        double si = 0.0;
+        const double* pr = pb + ((i >> 4) * nb) * kTB + (i & 15);
+        for (int b = bprev; b < nb; ++b) si += pr[b * kTB];
+        const double ai = T[tat(i, k1)];
+        const double pi = beta * fma(-alpha, ai, si);
+        const double ui = i == k1 ? u1 : xc[i];
+        const double qi = fma(-K, ui, pi);
+        uq[i] = make_double2(ui, qi);
+        const double xv = i == k1 ? 0.0 : fma(-ui, q1, fma(-qi, u1, ai));
+        xn[i] = xv;
+        ss = xv * xv;
+        p.H[(int64_t)k * n + i] = ui;
+      }
+      ss = wsum(ss);
+      if (lane == 0) npart[(k + 1) & 1][warp] = ss;
+    } else if (lane == 0) {
+      npart[(k + 1) & 1][warp] = 0.0;
+    }
+    long long c1 = pr0 ? clock64() : 0;
+    __syncthreads();
+    long long c2 = pr0 ? clock64() : 0;
+    if (!(dbg & 1)) tri_pass(T, pb, uq, xn, nb, k1 >> 4, warp, lane, xpart);
+    long long c3 = pr0 ? clock64() : 0;
+    __syncthreads();
+    if (pr0) {
+      const long long c4 = clock64();
+      cyc[0] += c1 - c0;
+      cyc[1] += c2 - c1;
+      cyc[2] += c3 - c2;
+      cyc[3] += c4 - c3;
+    }
+  }
+  if (pr0)
+    for (int i = 0; i < 4; ++i) p.prof[8 + i] = (unsigned long long)cyc[i];
+  if (tid == 0) {
+    for (int i = max(0, n - 2); i < n; ++i) sa[i] = T[tat(i, i)];
+    if (n >= 2) se[n - 2] = T[tat(n - 1, n - 2)];
+    se[n - 1] = 0.0;
+  }
+  for (int k = max(0, n - 2) + tid / 256; k < n; k += kDT / 256)  // no reflector for the last two columns
+    for (int i = tid % 256; i < n; i += 256) p.H[(int64_t)k * n + i] = 0.0;
+  __syncthreads();
+  stamp(p.prof, 2);
+  eig_tail(n, m, sa, se, te2, pb, wsz, lam, red, p.H, nullptr, p.V, p.theta, p.info, p.prof);
+}
 }  // namespace
 
 // the 4-CTA cluster tridiagonalisation (k_tridiag: T = (a, e), reflectors in rows of H, beta)
@@ -965,8 +1225,54 @@ size_t eig_direct_ws(int n, int m) {
   return tot * sizeof(double) <= 218 * 1024 ? tot : 0;  // + ~6 KB static shared memory <= 227 KB
 }
 
+// shared memory (doubles) k_eig_direct_t needs for (n, m); 0: does not fit (n > 208 or the tail's workspace)
+size_t eig_direct_t_ws(int n, int m) {
+  if (n < 3 || n > kTN || m < 1 || m > n || m > 256) return 0;
+  const size_t nb = (n + kTB - 1) / kTB;
+  const size_t wk = nb * nb * kTB + nb * (nb + 1) / 2 * kTB * kTB;  // pb + tiles: the tail's workspace
+  size_t need = std::max((size_t)n * m + (size_t)(4 * n + (n + 7) / 8 + 1) * std::min(m, 20),
+                         (size_t)2 * n * m + 16 * (size_t)n);
+  need = std::max(need, (size_t)2 * n * m + 8 * (size_t)(n + 9) + 64);
+  if (need > wk) return 0;
+  const size_t tot = 7 * (size_t)kTN + wk;
+  return tot * sizeof(double) <= 220 * 1024 ? tot : 0;  // + ~4 KB static shared memory <= 227 KB
+}
+
 void eig_small(const double* S, int64_t n, int64_t lds, int m, double* V, double* theta, int* info, DBuf<double>& scratch,
                cudaStream_t st) {
+  static const bool prof = std::getenv("TUCKER_EIG_PROF") != nullptr;  // tools: per-phase times on stderr
+  static unsigned long long* prof_d = nullptr;
+  if (prof && !prof_d) TK_CUDA(cudaMalloc(&prof_d, 16 * sizeof(unsigned long long)));
+  const bool old_direct = std::getenv("TUCKER_EIG_DIRECT_OLD") != nullptr;  // tests, experiments
+  const size_t wst = old_direct ? 0 : eig_direct_t_ws((int)n, m);
+  if (wst && !std::getenv("TUCKER_EIG_CLUSTER")) {  // one CTA, tiled S in shared memory
+    scratch.ensure((size_t)(n * n));
+    DirArgs a;
+    a.S = S;
+    a.lds = lds;
+    a.n = (int)n;
+    a.m = m;
+    a.ws = (int)wst;
+    a.H = scratch.p;
+    a.V = V;
+    a.theta = theta;
+    a.info = info;
+    a.prof = prof ? prof_d : nullptr;
+    a.dbg = std::getenv("TUCKER_EIG_DBG") ? std::atoi(std::getenv("TUCKER_EIG_DBG")) : 0;
+    smem_optin((const void*)k_eig_direct_t, wst * sizeof(double));
+    TK_LAUNCH(k_eig_direct_t, 1, kDT, wst * sizeof(double), st, a);
+    if (prof) {
+      unsigned long long t[16];
+      TK_CUDA(cudaStreamSynchronize(st));
+      TK_CUDA(cudaMemcpy(t, prof_d, sizeof(t), cudaMemcpyDeviceToHost));
+      std::fprintf(stderr, "eig_direct_t n=%d m=%d us: load %.1f tridiag %.1f bisect %.1f invit %.1f mgs %.1f back %.1f out %.1f total %.1f"
+                   " | tridiag cycles/step: ph1 %.0f bar %.0f ph2 %.0f bar %.0f\n",
+                   (int)n, m, (t[1] - t[0]) * 1e-3, (t[2] - t[1]) * 1e-3, (t[3] - t[2]) * 1e-3, (t[4] - t[3]) * 1e-3,
+                   (t[5] - t[4]) * 1e-3, (t[6] - t[5]) * 1e-3, (t[7] - t[6]) * 1e-3, (t[7] - t[0]) * 1e-3,
+                   (double)t[8] / (n - 2), (double)t[9] / (n - 2), (double)t[10] / (n - 2), (double)t[11] / (n - 2));
+    }
+    return;
+  }
   if (n < 3 || n > kNMax || m < 1 || m > n) fail(TUCKER_E_ARG, "eig_small: 3 <= n <= 256, 1 <= m <= n");
   const size_t ws = eig_direct_ws((int)n, m);
   if (ws && !std::getenv("TUCKER_EIG_CLUSTER")) {  // one CTA, everything in shared memory
@@ -981,8 +1287,18 @@ void eig_small(const double* S, int64_t n, int64_t lds, int m, double* V, double
     a.V = V;
     a.theta = theta;
     a.info = info;
+    a.prof = prof ? prof_d : nullptr;
+    a.dbg = 0;
     smem_optin((const void*)k_eig_direct, ws * sizeof(double));
     TK_LAUNCH(k_eig_direct, 1, kDT, ws * sizeof(double), st, a);
+    if (prof) {
+      unsigned long long t[8];
+      TK_CUDA(cudaStreamSynchronize(st));
+      TK_CUDA(cudaMemcpy(t, prof_d, sizeof(t), cudaMemcpyDeviceToHost));
+      std::fprintf(stderr, "eig_direct n=%d m=%d us: load %.1f tridiag %.1f bisect %.1f invit %.1f mgs %.1f back %.1f out %.1f total %.1f\n",
+                   (int)n, m, (t[1] - t[0]) * 1e-3, (t[2] - t[1]) * 1e-3, (t[3] - t[2]) * 1e-3, (t[4] - t[3]) * 1e-3,
+                   (t[5] - t[4]) * 1e-3, (t[6] - t[5]) * 1e-3, (t[7] - t[6]) * 1e-3, (t[7] - t[0]) * 1e-3);
+    }
     return;
   }
   scratch.ensure((size_t)(3 * n + n * n + (size_t)m * n + (size_t)m * 5 * n));

@@ -83,10 +83,11 @@ def test_split_k_product(capi, d, n):
     assert np.max(np.abs(out0 - S @ Y)) / scale < 1e-14 * max(d, 16)
 
 
-@pytest.mark.parametrize("path", ["auto", "cluster"])
+@pytest.mark.parametrize("path", ["auto", "cluster", "packed"])
 @pytest.mark.parametrize("d,J,kind", [(3, 1, "spread"), (17, 5, "spread"), (100, 10, "outlier"), (200, 20, "outlier"),
                                       (256, 112, "outlier"), (200, 50, "repeated"), (150, 30, "clustered"),
-                                      (210, 25, "repeated"), (64, 64, "spread")])
+                                      (210, 25, "repeated"), (64, 64, "spread"), (16, 4, "spread"), (33, 8, "outlier"),
+                                      (208, 20, "outlier"), (207, 30, "spread"), (129, 16, "diag"), (200, 20, "diag")])
 def test_small_dense_eigensolver(monkeypatch, d, J, kind, path):
     """eig_small against LAPACK: eigenvalues to 1e-12 relative to ||S||, the leading-J
     subspace to 1e-9, orthonormal vectors -- including eigenvalues repeated inside the
@@ -109,7 +110,7 @@ def test_small_dense_eigensolver(monkeypatch, d, J, kind, path):
     elif kind == "clustered":
         w[:J + 5] = 1.0 + 1e-4 * np.arange(J + 5)[::-1]        # relative gaps 1e-4
         w = np.sort(w)[::-1]
-    S = (Q * w) @ Q.T
+    S = (Q * w) @ Q.T if kind != "diag" else np.diag(rng.permutation(w))
     dims, core = (8, 8, 8), (2, 2, 2)
     idx, vals = uniform_distinct_coo(dims, 50, np.random.default_rng(1))
     U0 = [random_orthonormal(I, c, np.random.default_rng(2)) for I, c in zip(dims, core)]
