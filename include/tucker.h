@@ -83,8 +83,12 @@ void tucker_default_opts(tucker_opts* opts);
 /*
  * tucker_init -- load an order-N sparse tensor and the initial factors.
  *
- *   order   N in {3, 4} (MP is defined for orders 3 and 4 only, Figs. 7-8
- *           P:911-1114; SURVEY reading A18).
+ *   order   N in 2..8.  HOOI (Fig. 4) is defined for any N; order 2 is the
+ *           matrix case.  MP and SP are defined for orders 3 and 4 only
+ *           (Figs. 5-8; SURVEY reading A18): for orders 2 and 5..8 mp_sweep,
+ *           sp_sweep, tucker_hosvd and the CSF queries return TUCKER_E_ARG, HOOI runs on
+ *           one rank (world > 1 -> TUCKER_E_ARG) through per-mode sorted COO slices
+ *           (no CSF), and the orders 3 / 4 keep the CSF kernels.
  *   dims    I_1..I_N, each >= 1 and I_n < 2^31, with prod_n I_n < 2^64 (the
  *           sort keys pack every coordinate into 64 bits; TUCKER_E_ARG otherwise).
  *   core    J_1..J_N, 1 <= J_n <= min(I_n, 240) (the eigensolvers' block k = J + p
@@ -127,7 +131,7 @@ int hooi_sweep(tucker_handle* h, int sweeps, double* fit_per_sweep, float* stage
  *   M_n = sum_{m != n} sum_{slices s fixing the modes not in {n,m}} (X_s U_m)(X_s U_m)^T
  * (fp64, I_n x I_n), U_n = J_n leading eigenvectors of M_n (SURVEY reading A2:
  * of M_n, not M_n M_n^T).  Same output arguments as hooi_sweep
- * (stage_ms entries: {spmm, gram, eig, corefit}).
+ * (stage_ms entries: {spmm, gram, eig, corefit}).  Orders 3 and 4 only (E_ARG otherwise).
  */
 int mp_sweep(tucker_handle* h, int sweeps, double* fit_per_sweep, float* stage_ms);
 

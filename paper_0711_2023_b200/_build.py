@@ -12,7 +12,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libtucker.so")
-SOURCES = ["tucker.cu", "csf.cu", "spttmc.cu", "gram_tc.cu", "gram_simt.cu", "dense.cu", "eig.cu", "eig_fused.cu", "eig_large.cu", "eig_small.cu", "mp_sparse.cu", "dist.cu", "spttmc4g.cu"]
+SOURCES = ["tucker.cu", "csf.cu", "spttmc.cu", "gram_tc.cu", "gram_simt.cu", "dense.cu", "eig.cu", "eig_fused.cu", "eig_large.cu", "eig_small.cu", "mp_sparse.cu", "dist.cu", "spttmc4g.cu", "gen.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

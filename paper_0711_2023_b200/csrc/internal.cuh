@@ -8,7 +8,7 @@
 
 namespace tk {
 
-constexpr int kMaxOrder = 4;
+constexpr int kMaxOrder = 8;  // HOOI orders 2..8 (gen.cu for 2 and 5..8); MP / SP: 3, 4
 constexpr int kMaxJ = 240;       // per-mode core size limit (eigensolver block k = J + p <= 256)
 constexpr int kMaxJFused = 112;  // the persistent eigensolver's limit (block <= 116); larger J: eig_large
 constexpr int kMaxBlock = 116;   // eigensolver block size k limit (Jacobi in shared memory)
@@ -60,7 +60,7 @@ struct Csf {
 
 struct Coo {  // validated, zero-free COO on the device
   int order = 0;
-  int64_t dims[kMaxOrder] = {0, 0, 0, 0};
+  int64_t dims[kMaxOrder] = {};
   int64_t nnz = 0;
   DBuf<int32_t> idx[kMaxOrder];
   DBuf<float> val;
@@ -94,6 +94,20 @@ struct Split {
   bool ktile = false;
   int64_t K() const { return kext > 0 ? kext : ld; }
 };
+
+// gen.cu: HOOI projection for orders 2 and 5..8 -- per mode n the nonzeros sorted by
+// (i_n, other modes lower-fastest) as one 64-bit key, and the slice pointers of mode n
+struct GenMode {
+  DBuf<uint64_t> key;
+  DBuf<float> val;
+  DBuf<int32_t> sptr;  // I_n + 1
+  int64_t nnz = 0;
+  uint64_t Sn = 1;     // prod_{m != n} I_m
+};
+void gen_build(Coo& coo, GenMode* modes, cudaStream_t st);  // validates (E_INDEX, E_VALUE, E_DUP)
+void spttmc_gen(const GenMode& g, int order, int n, const int64_t* dims, const int64_t* J, const float* const* U,
+                Split Y, bool transposed, cudaStream_t st);
+
 
 // spttmc.cu
 // HOOI: Y_(n) (Kolda order) written as split fp32; transposed => out is Y_(n)^T.

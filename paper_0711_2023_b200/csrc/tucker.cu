@@ -17,14 +17,16 @@ using namespace tk;
 
 struct tucker_handle {
   int order = 0;
-  int64_t dims[kMaxOrder] = {1, 1, 1, 1};
-  int64_t J[kMaxOrder] = {1, 1, 1, 1};
+  int64_t dims[kMaxOrder] = {1, 1, 1, 1, 1, 1, 1, 1};
+  int64_t J[kMaxOrder] = {1, 1, 1, 1, 1, 1, 1, 1};
   tucker_opts opts{};
   cudaStream_t st = nullptr;
   bool own_stream = false;
   Coo coo;
   std::vector<std::unique_ptr<Csf>> csfs;
-  int hooi_csf[kMaxOrder] = {-1, -1, -1, -1};
+  int hooi_csf[kMaxOrder] = {-1, -1, -1, -1, -1, -1, -1, -1};
+  bool generic = false;      // order 2 or 5..8: HOOI through gen.cu (no CSF, no MP / SP)
+  GenMode gen[kMaxOrder];
   int mp_csf[kMaxOrder][kMaxOrder];
   DBuf<float> U[kMaxOrder];
   double normX2 = 0;
@@ -73,7 +75,7 @@ struct tucker_handle {
   // multi-GPU: a sharded sweep when opts.nccl_unique_id is set
   void* comm = nullptr;
   bool sharded = false;
-  int64_t hooi_lo[kMaxOrder] = {0, 0, 0, 0}, hooi_hi[kMaxOrder] = {-1, -1, -1, -1};  // root slices of mode n
+  int64_t hooi_lo[kMaxOrder] = {}, hooi_hi[kMaxOrder] = {-1, -1, -1, -1, -1, -1, -1, -1};  // root slices of mode n
   std::vector<int64_t> hooi_bounds[kMaxOrder];  // every rank's root-slice bounds of mode n (world + 1)
   int64_t mp_lo[kMaxOrder][kMaxOrder] = {}, mp_hi[kMaxOrder][kMaxOrder] = {};       // slices of MP term (n, m)
   bool Y_partial = false;  // h->Y holds only this rank's rows (Y^T Y route, not gathered)
@@ -222,7 +224,8 @@ void project_hooi(tucker_handle* h, int n, bool transposed) {
   h->Y.rows = rows;
   h->Y.cols = cols;
   h->Y.ld = ld;
-  spttmc_hooi(*h->csfs[h->hooi_csf[n]], uptrs(h), h->J, h->Y, transposed, h->st, h->hooi_lo[n], h->hooi_hi[n]);
+  if (h->generic) spttmc_gen(h->gen[n], h->order, n, h->dims, h->J, uptrs(h), h->Y, transposed, h->st);
+  else spttmc_hooi(*h->csfs[h->hooi_csf[n]], uptrs(h), h->J, h->Y, transposed, h->st, h->hooi_lo[n], h->hooi_hi[n]);
   h->Y_mode = n;
   h->Y_transposed = transposed;
   h->Y_partial = false;
@@ -834,7 +837,7 @@ int tucker_init(tucker_handle** out, int order, const int64_t* dims, const int64
                 const tucker_opts* opts) {
   if (!out || !dims || !core || !idx || !vals || !U0) return TUCKER_E_ARG;
   *out = nullptr;
-  if (order < 3 || order > 4 || nnz <= 0 || nnz >= (int64_t)1 << 31) return TUCKER_E_ARG;
+  if (order < 2 || order > kMaxOrder || nnz <= 0 || nnz >= (int64_t)1 << 31) return TUCKER_E_ARG;
   tucker_opts o;
   tucker_default_opts(&o);
   if (opts) o = *opts;
@@ -862,8 +865,12 @@ int tucker_init(tucker_handle** out, int order, const int64_t* dims, const int64
       const int rc = validate_factor(U0[n], dims[n], core[n]);
       if (rc) return rc;
     }
+  // orders 2 and 5..8 (HOOI only, gen.cu): one rank (the sharded sweep is built on the CSF)
+  const bool generic = order != 3 && order != 4;
+  if (generic && o.world > 1) return TUCKER_E_ARG;
   auto h = std::make_unique<tucker_handle>();
   h->order = order;
+  h->generic = generic;
   h->opts = o;
   for (int n = 0; n < order; ++n) {
     h->dims[n] = dims[n];
@@ -905,6 +912,16 @@ int tucker_init(tucker_handle** out, int order, const int64_t* dims, const int64
     c.val.alloc(nnz);
     TK_CUDA(cudaMemcpyAsync(c.val.p, vals, nnz * sizeof(float), kind, h->st));
     mark("H2D copies + allocs");
+    if (h->generic) {  // orders 2, 5..8: sorted COO per mode (gen.cu), HOOI only
+      gen_build(c, h->gen, h->st);
+      h->normX2 = coo_norm2(c, h->st);
+      if (!(h->normX2 > 0) || !std::isfinite(h->normX2))
+        fail(TUCKER_E_VALUE, "tucker_init: ||X|| = 0 or not finite");
+      for (int n = 0; n < order; ++n) c.idx[n].release();
+      c.val.release();
+      TK_CUDA(cudaStreamSynchronize(h->st));
+      return TUCKER_OK;
+    }
     coo_validate_compact(c, h->st);
     mark("validate");
     h->normX2 = coo_norm2(c, h->st);
@@ -1036,7 +1053,7 @@ int hooi_sweep(tucker_handle* h, int sweeps, double* fit_per_sweep, float* stage
 }
 
 int mp_sweep(tucker_handle* h, int sweeps, double* fit_per_sweep, float* stage_ms) {
-  if (!h || sweeps < 1) return TUCKER_E_ARG;
+  if (!h || sweeps < 1 || h->generic) return TUCKER_E_ARG;  // MP: orders 3, 4 (reading A18)
   return guarded(h, [&]() -> int {
     for (auto& r : h->side_ready) r = false;
     if (h->st2) TK_CUDA(cudaStreamSynchronize(h->st2));  // nothing of an earlier call still in flight
@@ -1106,7 +1123,7 @@ int mp_run(tucker_handle* h, int max_sweeps, double tol, double* fits, int* swee
 // m = n - 1 (cyclic); after every sweep the core and fit (fits[s]) and the core
 // norm (gnorms[s], for Delta_G, Eq. 11) -- both nullable.
 int sp_sweep(tucker_handle* h, int sweeps, double* fits, double* gnorms, float* stage_ms) {
-  if (!h || sweeps < 1) return TUCKER_E_ARG;
+  if (!h || sweeps < 1 || h->generic) return TUCKER_E_ARG;  // SP: orders 3, 4 (Figs. 5-6)
   return guarded(h, [&]() -> int {
     h->eig_unconverged = false;
     const int N = h->order;
@@ -1252,6 +1269,7 @@ int tucker_debug_ttmc(tucker_handle* h, int mode, float* Y_out) {
 
 int tucker_debug_gram(tucker_handle* h, int algo, int mode, double* S_out) {
   if (!h || !S_out || mode < 0 || mode >= h->order || algo < 0 || algo > 1) return TUCKER_E_ARG;
+  if (algo == 1 && h->generic) return TUCKER_E_ARG;
   return guarded(h, [&]() -> int {
     Split A;
     const bool sparse = algo == 1 && mp_use_sparse(h, mode, -1);
@@ -1276,6 +1294,7 @@ int tucker_debug_gram(tucker_handle* h, int algo, int mode, double* S_out) {
 
 int tucker_debug_gram_rows(tucker_handle* h, int algo, int mode, int nrows, const int64_t* rows, double* out) {
   if (!h || !rows || !out || nrows < 1 || mode < 0 || mode >= h->order || algo < 0 || algo > 1) return TUCKER_E_ARG;
+  if (algo == 1 && h->generic) return TUCKER_E_ARG;
   for (int r = 0; r < nrows; ++r)
     if (rows[r] < 0 || rows[r] >= h->dims[mode]) return TUCKER_E_ARG;
   return guarded(h, [&]() -> int {
@@ -1383,7 +1402,7 @@ int tucker_time_ttmc(tucker_handle* h, int mode, int reps, float* ms_out) {
 }
 
 int tucker_csf_layout(tucker_handle* h, int64_t* out) {
-  if (!h || !out) return TUCKER_E_ARG;
+  if (!h || !out || h->generic) return TUCKER_E_ARG;
   for (int n = 0; n < h->order; ++n) {
     const Csf& c = *h->csfs[h->hooi_csf[n]];
     int64_t* o = out + 8 * n;
@@ -1400,7 +1419,7 @@ int tucker_csf_layout(tucker_handle* h, int64_t* out) {
 }
 
 int tucker_csf_stats(tucker_handle* h, int64_t* out) {
-  if (!h || !out) return TUCKER_E_ARG;
+  if (!h || !out || h->generic) return TUCKER_E_ARG;
   for (int n = 0; n < h->order; ++n) {
     const Csf& c = *h->csfs[h->hooi_csf[n]];
     out[4 * n] = c.nfib;
@@ -1412,7 +1431,7 @@ int tucker_csf_stats(tucker_handle* h, int64_t* out) {
 }
 
 int tucker_hosvd(tucker_handle* h, unsigned mode_mask) {
-  if (!h || (mode_mask >> h->order) != 0) return TUCKER_E_ARG;
+  if (!h || (mode_mask >> h->order) != 0 || h->generic) return TUCKER_E_ARG;
   return guarded(h, [&]() -> int {
     h->eig_unconverged = false;
     for (int n = 0; n < h->order; ++n) {
@@ -1465,7 +1484,7 @@ int tucker_set_allreduce(tucker_handle* h, void* fn, void* user) {
 }
 
 int tucker_shard_info(tucker_handle* h, int64_t* out) {
-  if (!h || !out) return TUCKER_E_ARG;
+  if (!h || !out || h->generic) return TUCKER_E_ARG;
   const int N = h->order;
   for (int n = 0; n < N; ++n) {
     const Csf& c = *h->csfs[h->hooi_csf[n]];

@@ -42,11 +42,20 @@ def test_strerror_and_arg_errors_without_device(lib):
     idx = [np.zeros(3, np.int32)] * 3
     vals = np.ones(3, np.float32)
     U = [np.eye(d, c, dtype=np.float32) for d, c in zip(dims, core)]
-    # order 5 is outside the paper's MP scope (reading A18) -> E_ARG before any CUDA call
+    # orders outside 2..8 (HOOI's range) -> E_ARG before any CUDA call; orders 2 and
+    # 5..8 run HOOI on one rank only (gen.cu): sharded -> E_ARG
+    d9 = (4, 5, 6, 7, 8, 4, 5, 6, 7)
+    U9 = [np.eye(d, 2, dtype=np.float32) for d in d9]
+    with pytest.raises(capi.TuckerError) as e:
+        capi.tucker_init(d9, (2,) * 9, (idx * 3)[:9], vals, U9)
+    assert e.value.code == 1
+    with pytest.raises(capi.TuckerError) as e:
+        capi.tucker_init((4,), (2,), idx[:1], vals, [np.eye(4, 2, dtype=np.float32)])
+    assert e.value.code == 1
     d5 = (4, 5, 6, 7, 8)
     U5 = [np.eye(d, 2, dtype=np.float32) for d in d5]
     with pytest.raises(capi.TuckerError) as e:
-        capi.tucker_init(d5, (2,) * 5, (idx * 2)[:5], vals, U5)
+        capi.tucker_init(d5, (2,) * 5, (idx * 2)[:5], vals, U5, rank=0, world=2, host_collectives=True)
     assert e.value.code == 1
     # J > I -> E_ARG
     with pytest.raises(capi.TuckerError) as e:
