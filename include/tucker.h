@@ -209,6 +209,17 @@ int tucker_debug_product_time(int d, int n, int reps, double* us);
  * arguments. */
 int tucker_time_ttmc(tucker_handle* h, int mode, int reps, float* ms_out);
 
+/* Measurement: kernel time of mp_sweep's overlapped streams (MP overlap: while mode n's
+ * eigensolve runs on its own stream, a side stream builds the next mode's W terms that do not
+ * involve U_n and their Gram; the main stream adds the late term m = n - 1), summed over the
+ * sweeps since the last reset from CUDA events on the stream each kernel runs on.
+ * ms[5] / counts[5]: [0] side SpMM (counts in terms = k_spmm_w launches), [1] side Gram (calls),
+ * [2] main-stream SpMM (late term, or a whole build when nothing was prepared; terms),
+ * [3] main-stream Gram (calls), [4] eigensolve + factor update (calls).  The streams overlap, so
+ * the sums exceed the sweep's wall time.  The side work of a call's last mode is counted only if
+ * it had finished at the sweep's end.  All zero when the overlap is off.  E_ARG on null pointers. */
+int tucker_mp_overlap_times(tucker_handle* h, double* ms, int64_t* counts, int reset);
+
 /* Sparse layout of the handle, for the CSF ordering mode n's HOOI projection
  * uses (out has 4 N entries): out[4n] = fibers, out[4n + 1] = nonzeros,
  * out[4n + 2] = virtual fibers of the SpTTMc work plan and out[4n + 3] = its

@@ -30,7 +30,7 @@ EXPORTS = [
     "tucker_debug_product", "tucker_debug_product_time", "tucker_csf_stats", "tucker_stats",
     "tucker_nccl_unique_id", "tucker_shard_bounds", "tucker_shard_info", "hooi_run", "mp_run",
     "tucker_hosvd", "sp_sweep", "sp_run", "tucker_set_factor", "tucker_set_allreduce",
-    "tucker_time_ttmc", "tucker_csf_layout", "tucker_debug_gram_rows",
+    "tucker_time_ttmc", "tucker_csf_layout", "tucker_debug_gram_rows", "tucker_mp_overlap_times",
 ]
 
 
@@ -72,6 +72,7 @@ def load(path: str = LIB_PATH) -> C.CDLL:
     lib.tucker_csf_layout.argtypes = [P, i64p]
     lib.tucker_debug_gram_rows.argtypes = [P, C.c_int, C.c_int, C.c_int, i64p, P]
     lib.tucker_time_ttmc.argtypes = [P, C.c_int, C.c_int, C.POINTER(C.c_float)]
+    lib.tucker_mp_overlap_times.argtypes = [P, C.POINTER(C.c_double), i64p, C.c_int]
     lib.tucker_nccl_unique_id.argtypes = [P]
     lib.tucker_hosvd.argtypes = [P, C.c_uint]
     lib.tucker_set_allreduce.argtypes = [P, P, P]
@@ -375,6 +376,16 @@ def tucker_time_ttmc(h, mode, reps=5):
     ms = C.c_float(0)
     _check(lib().tucker_time_ttmc(h, mode, reps, C.byref(ms)), h)
     return ms.value
+
+
+def tucker_mp_overlap_times(h, reset=False):
+    """Kernel time (ms) and counts of mp_sweep's overlapped streams since the last reset:
+    dict(side_spmm, side_gram, main_spmm, main_gram, eig) -> (ms, count)."""
+    ms = (C.c_double * 5)()
+    cnt = (C.c_int64 * 5)()
+    _check(lib().tucker_mp_overlap_times(h, ms, cnt, 1 if reset else 0), h)
+    keys = ("side_spmm", "side_gram", "main_spmm", "main_gram", "eig")
+    return {k: (float(ms[i]), int(cnt[i])) for i, k in enumerate(keys)}
 
 
 def tucker_csf_fibers(h, order=3):

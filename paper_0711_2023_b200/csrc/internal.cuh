@@ -54,6 +54,9 @@ struct Csf {
                                           // chunk) and their (b_local, v) targets; leaf ids in slot order
     DBuf<float> val, part;             // values in slot order; run partial rows
     std::vector<int32_t> bfirst_h;
+    // sibling-mode lists (HOOI partial-contraction reuse): nodes grouped by mid0
+    bool sib_built = false;
+    DBuf<int32_t> sib_ptr, sib_node, node_root;
   };
   std::unique_ptr<G4> g4 = std::make_unique<G4>();
 };
@@ -114,10 +117,18 @@ void spttmc_gen(const GenMode& g, int order, int n, const int64_t* dims, const i
 // Only the root slices [lo, hi) are computed (a rank's shard; hi < 0: all); the
 // other rows of out stay as they are (zero).
 // order-4 GEMM-form SpTTMc (spttmc4g.cu); false: not applicable (use k_spttmc4w)
+// zout (nullable): Z_v = U_mid1^T T_v of every node, [nnode][J_mid1 round_up(J_leaf, 4)], kept for
+// the sibling mode (FMA kernel only)
 bool spttmc4g(const Csf& c, const float* const* U, const int64_t* J, Split out, bool transposed, int64_t s0,
-              int64_t s1, int64_t sb, cudaStream_t st, int64_t lo, int64_t hi);
+              int64_t s1, int64_t sb, cudaStream_t st, int64_t lo, int64_t hi, float* zout = nullptr);
+bool spttmc4g_fma_default(const Csf& c, const int64_t* J);  // spttmc4g would run the FMA kernel by default
+// Y_(c.mid0) from the kept Z of ordering c (strides: Kolda positions of root, mid1, leaf in mode mid0's unfolding)
+void spttmc4_sibling(const Csf& c, const float* Z, const float* Uroot, const int64_t* J, Split out, bool transposed,
+                     int64_t sr, int64_t s1, int64_t sb, cudaStream_t st);
+void spttmc_hooi_sibling(const Csf& c, const float* Z, const float* const* U, const int64_t* J, Split out,
+                         bool transposed, cudaStream_t st);
 void spttmc_hooi(const Csf& c, const float* const* U, const int64_t* J, Split out, bool transposed,
-                 cudaStream_t st, int64_t lo = 0, int64_t hi = -1);
+                 cudaStream_t st, int64_t lo = 0, int64_t hi = -1, float* zout = nullptr);
 // MP: W columns [col_off, col_off + (s_hi - s_lo)*J_leaf) of the rows of out
 // (out pre-zeroed): W[i_root, col_off + (mk - s_lo)*J_leaf + j] = sum_{x in fiber} x U_leaf[i_leaf, j]
 // for the slices mk (the mid index) in [s_lo, s_hi) (a rank's shard; s_hi < 0: all).

@@ -1087,8 +1087,18 @@ static int64_t kolda_stride(int m, const int* others, int nothers, const int64_t
   return s;
 }
 
+// Mode c.mid0 from the Z kept by mode c.root's projection (spttmc4g.cu, k_spttmc4_sib)
+void spttmc_hooi_sibling(const Csf& c, const float* Z, const float* const* U, const int64_t* J, Split out,
+                         bool transposed, cudaStream_t st) {
+  int others[3], no = 0;
+  for (int m = 0; m < c.order; ++m)
+    if (m != c.mid0) others[no++] = m;
+  spttmc4_sibling(c, Z, U[c.root], J, out, transposed, kolda_stride(c.root, others, no, J),
+                  kolda_stride(c.mid1, others, no, J), kolda_stride(c.leaf, others, no, J), st);
+}
+
 void spttmc_hooi(const Csf& c, const float* const* U, const int64_t* J, Split out, bool transposed,
-                 cudaStream_t st, int64_t lo, int64_t hi) {
+                 cudaStream_t st, int64_t lo, int64_t hi, float* zout) {
   if (hi < 0) hi = c.I_root;
   if (hi <= lo) return;  // empty shard: Y stays zero
   int others[3], no = 0;
@@ -1213,8 +1223,9 @@ void spttmc_hooi(const Csf& c, const float* const* U, const int64_t* J, Split ou
   a.s1 = kolda_stride(c.mid1, others, no, J);
   a.sb = kolda_stride(c.leaf, others, no, J);
   if (!std::getenv("TUCKER_TTMC4_CS") && !std::getenv("TUCKER_TTMC4_GMEM") &&
-      spttmc4g(c, U, J, out, transposed, a.s0, a.s1, a.sb, st, lo, hi))
+      spttmc4g(c, U, J, out, transposed, a.s0, a.s1, a.sb, st, lo, hi, zout))
     return;
+  if (zout) fail(TUCKER_E_STATE, "spttmc_hooi: Z is kept by the GEMM-form kernel only");
   const int64_t P = (int64_t)a.J0 * a.J1 * a.Jl;
   a.slice0 = (int)lo;
   a.I_leaf = (int)c.I_leaf;

@@ -63,6 +63,7 @@ struct G4Args {
   int I_leaf, I_mid1;
   int b_lo, nb;             // batches [b_lo, b_lo + nb) of this launch
   float* part;              // [nb][J0 * J1 * JLP] partial rows of runs (index: run's first batch - b_lo)
+  float* zout;              // nullable: Z_v of every node, [nnode][J1 * JLP] (kept for the sibling mode)
 };
 
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
@@ -256,6 +257,10 @@ __global__ void __launch_bounds__(kNT, 1) k_spttmc4g(G4Args p) {
 #pragma unroll
       for (int c = 0; c < 4; ++c) acc[r][c] = 0.f;
     __syncthreads();
+    if (p.zout) {  // the batch's Z rows are contiguous (node-major) in TZ and in zout
+      float* zo = p.zout + (int64_t)bt.y * P1;
+      for (int e = tid; e < bt.z * P1; e += kNT) zo[e] = TZ[e];
+    }
     const bool run_end = b + 1 == b1 || p.batch[b + 1].x != bt.x;
     for (int col = tid; col < P1; col += kNT) {
       for (int a0 = 0; a0 < J0; a0 += 4) {
@@ -1113,8 +1118,25 @@ static bool g4_layout(const Csf& c, int NB, int KCH, cudaStream_t st) {
 // not applicable (the caller falls back to k_spttmc4w).  Default: the FMA kernel (k_spttmc4g);
 // TUCKER_TTMC4=t selects the tcgen05 kernel (k_spttmc4t), =g the FMA kernel even where the
 // density test would reject it, =w disables both (tests).
+// True when spttmc4g would take the default FMA kernel on ordering c (the kernel that can keep Z)
+bool spttmc4g_fma_default(const Csf& c, const int64_t* J) {
+  const char* fe = std::getenv("TUCKER_TTMC4");
+  const char fc = fe ? fe[0] : 0;  // 'g' forces the FMA kernel (tests); any other choice has no Z
+  if ((fc != 0 && fc != 'g') || std::getenv("TUCKER_TTMC4_CS") || std::getenv("TUCKER_TTMC4_GMEM")) return false;
+  if (c.order != 4) return false;
+  const int J0 = (int)J[c.mid0], J1 = (int)J[c.mid1], Jl = (int)J[c.leaf];
+  const int JLP = (int)round_up(Jl, 4), J1P = (int)round_up(J1, 4), CL = JLP / 4;
+  if (CL > 8 || J0 > 256) return false;
+  if (fc == 0 && (double)c.nnode * (double)round_up(c.I_mid1, 32) > 2.5 * (double)c.nfib) return false;
+  const int NBg = kNT / CL;
+  const int SPCg = (int)round_up((int64_t)NBg * kKCH + 1, 4);
+  if (!(J1P <= 24 && g4_smem(c, J0, J1, Jl, NBg, SPCg) <= 220 * 1024)) return false;
+  const int64_t nbatch_est = c.nnode / NBg + c.I_root;
+  return (nbatch_est * ceil_div(c.I_mid1, kKCH) * SPCg + 8) < ((int64_t)1 << 31);
+}
+
 bool spttmc4g(const Csf& c, const float* const* U, const int64_t* J, Split out, bool transposed, int64_t s0,
-              int64_t s1, int64_t sb, cudaStream_t st, int64_t lo, int64_t hi) {
+              int64_t s1, int64_t sb, cudaStream_t st, int64_t lo, int64_t hi, float* zout) {
   const char* fe = std::getenv("TUCKER_TTMC4");
   const char fc = fe ? fe[0] : 0;
   if (fc == 'w' || c.order != 4) return false;
@@ -1143,6 +1165,7 @@ bool spttmc4g(const Csf& c, const float* const* U, const int64_t* J, Split out, 
   const bool use_s = fc == 's' ? s_ok : false;
   const bool use_tc = use_s || (fc == 't' ? tc_ok : false);
   if (!use_tc && !g_ok) return false;
+  if (zout && use_tc) fail(TUCKER_E_STATE, "spttmc4g: Z is kept by the FMA kernel only");
   if ((fc == 't' && !tc_ok) || (fc == 's' && !s_ok)) return false;
   const int NB = use_tc ? NBt : NBg, KCH = use_tc ? kTKC : kKCH, SPC = use_tc ? SPCt : SPCg;
   const int NCH = (int)ceil_div(c.I_mid1, KCH);
@@ -1234,6 +1257,7 @@ bool spttmc4g(const Csf& c, const float* const* U, const int64_t* J, Split out, 
       a.b_lo = blo;
       a.nb = nb;
       a.part = g.part.p;
+      a.zout = zout;
       const size_t smem = g4_smem(c, J0, J1, Jl, NB, SPC);
       bool launched = false;
 #define TK_G4(j1p)                                                                  \
@@ -1252,6 +1276,145 @@ bool spttmc4g(const Csf& c, const float* const* U, const int64_t* J, Split out, 
               std::max(nb, 1), G, J1, Jl, JLP, (int)P, s0, s1, sb, out.hi, out.lo, out.ld, (int)transposed);
   }
   return true;
+}
+
+
+// ---------------------------------------------------------------------------
+// Sibling mode from the kept Z (HOOI partial-contraction reuse, order 4).
+// Ordering (p; q; x; y): Z_v = X x_x U_x^T x_y U_y^T restricted to node v = (i_p, i_q).
+// Mode p's row is Y_(p)[i_p] = sum_{i_q} U_q[i_q] (x) Z_v (level 3 above); the same Z gives
+// mode q: Y_(q)[i_q] = sum_{i_p} U_p[i_p] (x) Z_v (Fig. 4 P:618-627 with Eq. 1 applied in
+// another order), valid while U_x and U_y are unchanged -- in a Gauss-Seidel sweep exactly
+// when q = p + 1.  Thread = one Z column and 16 U_p columns; the nodes of i_q in ascending
+// i_p, one fixed-order sum per output (deterministic).  kSibJ: U_p columns per thread (one
+// tile covers J_p <= 24, so Z is read once; larger J_p in tiles of 16).
+// ---------------------------------------------------------------------------
+constexpr int kSibT = 128, kSibN = 32, kSibU = 8;
+template <int kSibJ>
+__global__ void __launch_bounds__(kSibT) k_spttmc4_sib(const float* __restrict__ Z, const int32_t* __restrict__ sib_ptr,
+                                                      const int32_t* __restrict__ sib_node,
+                                                      const int32_t* __restrict__ node_root,
+                                                      const float* __restrict__ Ur, int Jr, int J1, int Jl, int JLP,
+                                                      int64_t sr, int64_t s1, int64_t sb, float* __restrict__ Yhi,
+                                                      float* __restrict__ Ylo, int64_t ldY, int transposed) {
+  __shared__ __align__(16) float us[kSibN][kSibJ];
+  __shared__ int nd[kSibN];
+  const int P1 = J1 * JLP;
+  const int col = blockIdx.x * kSibT + threadIdx.x;
+  const int a = blockIdx.y;
+  const int jr0 = blockIdx.z * kSibJ;
+  const bool live = col < P1;
+  float y[kSibJ];
+#pragma unroll
+  for (int t = 0; t < kSibJ; ++t) y[t] = 0.f;
+  const int k0 = sib_ptr[a], k1 = sib_ptr[a + 1];
+  for (int kb = k0; kb < k1; kb += kSibN) {
+    const int n = min(kSibN, k1 - kb);
+    __syncthreads();
+    if (threadIdx.x < n) nd[threadIdx.x] = sib_node[kb + threadIdx.x];
+    for (int e = threadIdx.x; e < n * kSibJ; e += kSibT) {
+      const int k = e / kSibJ, t = e - k * kSibJ;
+      const int v = sib_node[kb + k];
+      us[k][t] = jr0 + t < Jr ? __ldg(Ur + (int64_t)node_root[v] * Jr + jr0 + t) : 0.f;
+    }
+    __syncthreads();
+    if (live) {
+      int k = 0;
+      for (; k + kSibU <= n; k += kSibU) {
+        float z[kSibU];
+#pragma unroll
+        for (int u = 0; u < kSibU; ++u) z[u] = __ldg(Z + (int64_t)nd[k + u] * P1 + col);
+#pragma unroll
+        for (int u = 0; u < kSibU; ++u)
+#pragma unroll
+          for (int t4 = 0; t4 < kSibJ / 4; ++t4) {
+            const float4 g = *reinterpret_cast<const float4*>(&us[k + u][4 * t4]);
+            y[4 * t4] = fmaf(g.x, z[u], y[4 * t4]);
+            y[4 * t4 + 1] = fmaf(g.y, z[u], y[4 * t4 + 1]);
+            y[4 * t4 + 2] = fmaf(g.z, z[u], y[4 * t4 + 2]);
+            y[4 * t4 + 3] = fmaf(g.w, z[u], y[4 * t4 + 3]);
+          }
+      }
+      for (; k < n; ++k) {
+        const float z = __ldg(Z + (int64_t)nd[k] * P1 + col);
+#pragma unroll
+        for (int t = 0; t < kSibJ; ++t) y[t] = fmaf(us[k][t], z, y[t]);
+      }
+    }
+  }
+  if (!live) return;
+  const int r = col / JLP, c = col - r * JLP;
+  if (c >= Jl) return;
+#pragma unroll
+  for (int t = 0; t < kSibJ; ++t) {
+    if (jr0 + t >= Jr) break;
+    const int64_t ycol = (jr0 + t) * sr + r * s1 + c * sb;
+    const int64_t off = transposed ? ycol * ldY + a : (int64_t)a * ldY + ycol;
+    const float h = tf32_rna_g4(y[t]);
+    Yhi[off] = h;
+    Ylo[off] = tf32_rna_g4(y[t] - h);
+  }
+}
+
+__global__ void k_sib_node_root(const int32_t* __restrict__ slice_ptr, int64_t nslice, int64_t nnode,
+                                int32_t* __restrict__ node_root, int32_t* __restrict__ id) {
+  const int64_t nd = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (nd >= nnode) return;
+  int64_t lo = 0, hi = nslice;
+  while (hi - lo > 1) {
+    const int64_t m = (lo + hi) / 2;
+    if (slice_ptr[m] <= nd) lo = m;
+    else hi = m;
+  }
+  node_root[nd] = (int32_t)lo;
+  id[nd] = (int32_t)nd;
+}
+__global__ void k_sib_ptr(const int32_t* __restrict__ key, int64_t nnode, int64_t I, int32_t* __restrict__ ptr) {
+  const int64_t a = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (a > I) return;
+  int64_t lo = 0, hi = nnode;  // first position with key >= a
+  while (lo < hi) {
+    const int64_t m = (lo + hi) / 2;
+    if (key[m] < a) lo = m + 1;
+    else hi = m;
+  }
+  ptr[a] = (int32_t)lo;
+}
+
+void spttmc4_sibling(const Csf& c, const float* Z, const float* Uroot, const int64_t* J, Split out, bool transposed,
+                     int64_t sr, int64_t s1, int64_t sb, cudaStream_t st) {
+  Csf::G4& g = *c.g4;
+  if (!g.sib_built) {  // nodes grouped by mid0 (stable: ascending root inside a group)
+    const int64_t nn = std::max<int64_t>(1, c.nnode);
+    g.node_root.alloc(nn);
+    g.sib_node.alloc(nn);
+    g.sib_ptr.alloc(c.I_mid0 + 1);
+    DBuf<int32_t> id(nn), key2(nn);
+    if (c.nnode)
+      TK_LAUNCH(k_sib_node_root, (unsigned)ceil_div(c.nnode, 256), 256, 0, st, c.slice_ptr.p, c.I_root, c.nnode,
+                g.node_root.p, id.p);
+    size_t sbytes = 0;
+    TK_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, sbytes, c.node_mid0.p, key2.p, id.p, g.sib_node.p, (int)c.nnode, 0,
+                                            bits_needed((uint64_t)c.I_mid0), st));
+    DBuf<uint8_t> stmp(sbytes);
+    TK_CUDA(cub::DeviceRadixSort::SortPairs(stmp.p, sbytes, c.node_mid0.p, key2.p, id.p, g.sib_node.p, (int)c.nnode, 0,
+                                            bits_needed((uint64_t)c.I_mid0), st));
+    TK_LAUNCH(k_sib_ptr, (unsigned)ceil_div(c.I_mid0 + 1, 256), 256, 0, st, (const int32_t*)key2.p, c.nnode, c.I_mid0,
+              g.sib_ptr.p);
+    TK_CUDA(cudaStreamSynchronize(st));  // the temporaries go out of scope
+    g.sib_built = true;
+  }
+  const int Jr = (int)J[c.root], J1 = (int)J[c.mid1], Jl = (int)J[c.leaf];
+  const int JLP = (int)round_up(Jl, 4);
+  const int JT = Jr <= 8 ? 8 : (Jr <= 16 ? 16 : (Jr <= 24 ? 24 : 16));
+  const dim3 gr((unsigned)ceil_div((int64_t)J1 * JLP, kSibT), (unsigned)c.I_mid0, (unsigned)ceil_div(Jr, JT));
+#define TK_SIB(jt)                                                                                                   \
+  if (JT == jt)                                                                                                      \
+    TK_LAUNCH(k_spttmc4_sib<jt>, gr, kSibT, 0, st, Z, (const int32_t*)g.sib_ptr.p, (const int32_t*)g.sib_node.p,     \
+              (const int32_t*)g.node_root.p, Uroot, Jr, J1, Jl, JLP, sr, s1, sb, out.hi, out.lo, out.ld,            \
+              (int)transposed);
+  TK_SIB(8) TK_SIB(16) TK_SIB(24)
+#undef TK_SIB
 }
 
 }  // namespace tk

@@ -79,6 +79,23 @@ struct tucker_handle {
   std::vector<int64_t> hooi_bounds[kMaxOrder];  // every rank's root-slice bounds of mode n (world + 1)
   int64_t mp_lo[kMaxOrder][kMaxOrder] = {}, mp_hi[kMaxOrder][kMaxOrder] = {};       // slices of MP term (n, m)
   bool Y_partial = false;  // h->Y holds only this rank's rows (Y^T Y route, not gathered)
+  // HOOI partial-contraction reuse (order 4, one rank, GEMM-form SpTTMc): mode p's projection on the
+  // ordering (p; p + 1; x; y) keeps Z = X x_x U_x^T x_y U_y^T per node (i_p, i_{p+1}); mode p + 1 is
+  // then one small kernel over Z.  valid: Z was built with the current U_x and U_y.
+  struct Memo {
+    int csf = -1, root = -1, sib = -1;
+    DBuf<float> Z;
+    bool valid = false;
+  };
+  Memo memo[2];
+  int64_t memo_hits = 0;
+  // MP overlap accounting (tucker_mp_overlap_times): kernel time by stream, summed at each sweep's
+  // end from the tl events.  [0] side SpMM, [1] side Gram, [2] late / whole SpMM (main stream),
+  // [3] late / whole Gram, [4] eigensolve + factor (its own stream).  cnt: SpMM in terms (= launches),
+  // the others in calls.
+  double ov_ms[5] = {};
+  int64_t ov_cnt[5] = {};
+  unsigned tl_rec[kMaxOrder] = {};  // this sweep's recorded groups: 1 fork/eig, 2 side, 4 late
 };
 // kept W buffers of all live handles in this process (budget: a quarter of the device)
 static std::atomic<size_t> g_wkeep_bytes{0};
@@ -199,6 +216,15 @@ const float* const* uptrs(tucker_handle* h) {
   return p;
 }
 
+// factor n was rewritten (n < 0: all): the kept Z products that used it are stale
+void memo_invalidate(tucker_handle* h, int n) {
+  for (auto& m : h->memo) {
+    if (m.csf < 0) continue;
+    const Csf& c = *h->csfs[m.csf];
+    if (n < 0 || n == c.mid1 || n == c.leaf) m.valid = false;
+  }
+}
+
 EigOpts eig_opts(const tucker_handle* h) {
   EigOpts o;
   o.oversample = h->opts.eig_oversample;
@@ -224,8 +250,26 @@ void project_hooi(tucker_handle* h, int n, bool transposed) {
   h->Y.rows = rows;
   h->Y.cols = cols;
   h->Y.ld = ld;
-  if (h->generic) spttmc_gen(h->gen[n], h->order, n, h->dims, h->J, uptrs(h), h->Y, transposed, h->st);
-  else spttmc_hooi(*h->csfs[h->hooi_csf[n]], uptrs(h), h->J, h->Y, transposed, h->st, h->hooi_lo[n], h->hooi_hi[n]);
+  tucker_handle::Memo* mroot = nullptr;
+  tucker_handle::Memo* msib = nullptr;
+  for (auto& m : h->memo) {
+    if (m.csf >= 0 && m.root == n) mroot = &m;
+    if (m.csf >= 0 && m.sib == n && m.valid) msib = &m;
+  }
+  if (h->generic) {
+    spttmc_gen(h->gen[n], h->order, n, h->dims, h->J, uptrs(h), h->Y, transposed, h->st);
+  } else if (msib) {  // Y_(n) from the Z kept by mode n - 1's projection
+    spttmc_hooi_sibling(*h->csfs[msib->csf], msib->Z.p, uptrs(h), h->J, h->Y, transposed, h->st);
+    ++h->memo_hits;
+  } else if (mroot) {
+    const Csf& c = *h->csfs[mroot->csf];
+    mroot->Z.ensure((size_t)std::max<int64_t>(1, c.nnode) * h->J[c.mid1] * round_up(h->J[c.leaf], 4));
+    mroot->valid = false;
+    spttmc_hooi(c, uptrs(h), h->J, h->Y, transposed, h->st, h->hooi_lo[n], h->hooi_hi[n], mroot->Z.p);
+    mroot->valid = true;
+  } else {
+    spttmc_hooi(*h->csfs[h->hooi_csf[n]], uptrs(h), h->J, h->Y, transposed, h->st, h->hooi_lo[n], h->hooi_hi[n]);
+  }
   h->Y_mode = n;
   h->Y_transposed = transposed;
   h->Y_partial = false;
@@ -506,6 +550,7 @@ void update_factor(tucker_handle* h, int n, const Split& A, bool transposed, Eig
 void factor_from_S(tucker_handle* h, int n, const Split& A, bool transposed, EigSlot& slot, bool partial_gram) {
   const int64_t d = A.rows;
   const int J = (int)h->J[n];
+  memo_invalidate(h, n);
   solve_eig(h, d, J, slot, transposed ? nullptr : h->U[n].p, n);
   if (!transposed) {
     canon_to_f32(h->V.p, J, d, J, h->U[n].p, h->st);
@@ -616,12 +661,10 @@ void mp_update_overlap(tucker_handle* h, int n, EigSlot& slot, cudaEvent_t ev_pr
   const int N = h->order, late = (n + N - 1) % N;
   const int64_t d = h->dims[n];
   const int64_t lds = ensure_S(h, d);
-  cudaEvent_t* tl = nullptr;
-  if (mp_timeline()) {
-    tl = h->tl[n];
-    for (int q = 0; q < 7; ++q)
-      if (!tl[q]) TK_CUDA(cudaEventCreate(&tl[q]));
-  }
+  cudaEvent_t* tl = h->tl[n];  // always on: seven event records per mode
+  for (int q = 0; q < 7; ++q)
+    if (!tl[q]) TK_CUDA(cudaEventCreate(&tl[q]));
+  h->tl_rec[n] = 0;
   if (h->side_ready[n]) {  // early terms done on st2: the late term, S = S2 + W_late W_late^T
     TK_CUDA(cudaStreamWaitEvent(h->st, h->ev_join, 0));
     if (tl) TK_CUDA(cudaEventRecord(tl[4], h->st));
@@ -638,10 +681,15 @@ void mp_update_overlap(tucker_handle* h, int n, EigSlot& slot, cudaEvent_t ev_pr
     gram_syrk(Wl, h->S.p, lds, h->gram, h->st, h->S2.p, 0.5 * (double)W.rows * (W.rows + 1) * (double)W.K());
     if (tl) TK_CUDA(cudaEventRecord(tl[6], h->st));
     h->side_ready[n] = false;
+    h->tl_rec[n] |= 4u;
   } else {
+    TK_CUDA(cudaEventRecord(tl[4], h->st));
     Split W = build_mp_w(h, n);
     TK_CUDA(cudaEventRecord(ev_proj, h->st));
+    TK_CUDA(cudaEventRecord(tl[5], h->st));
     gram_syrk(W, h->S.p, lds, h->gram, h->st);
+    TK_CUDA(cudaEventRecord(tl[6], h->st));
+    h->tl_rec[n] |= 8u;  // whole build: N - 1 terms
   }
   TK_CUDA(cudaEventRecord(ev_gram, h->st));
   TK_CUDA(cudaEventRecord(h->ev_fork, h->st));
@@ -662,11 +710,13 @@ void mp_update_overlap(tucker_handle* h, int n, EigSlot& slot, cudaEvent_t ev_pr
     h->st = main_st;
     TK_CUDA(cudaEventRecord(h->ev_eig, h->st_hi));
     if (tl) TK_CUDA(cudaEventRecord(tl[1], h->st_hi));
+    h->tl_rec[n] |= 1u;
   }
   if (next >= 0) {  // every factor but U_n is final: the next mode's early terms meanwhile
     TK_CUDA(cudaStreamWaitEvent(h->st2, h->ev_fork, 0));
     mp_side(h, next, tl);
     TK_CUDA(cudaEventRecord(h->ev_join, h->st2));
+    h->tl_rec[n] |= 2u;
   }
   TK_CUDA(cudaStreamWaitEvent(h->st, h->ev_eig, 0));
 }
@@ -965,6 +1015,42 @@ int tucker_init(tucker_handle** out, int order, const int64_t* dims, const int64
       h->sharded = true;
       make_shards(h.get());
     }
+    // HOOI partial-contraction reuse (order 4, one rank; TUCKER_HOOI_MEMO=0 disables): modes
+    // (0, 1) share Z = X x_2 U_2^T x_3 U_3^T, modes (2, 3) share Z = X x_0 U_0^T x_1 U_1^T.
+    // Mode p takes the ordering (p; p + 1; x; y) with the cheaper leaf; (2; 3; x; y) is an extra
+    // ordering (the MP orderings keep their mids ascending).  Only where the GEMM-form kernel
+    // (the one that keeps Z) runs by default and Z fits an eighth of the free memory.
+    {
+      const char* me = std::getenv("TUCKER_HOOI_MEMO");
+      const bool want = order == 4 && !h->sharded && !(me && me[0] == '0');
+      for (int pr = 0; want && pr < 2; ++pr) {
+        const int p = 2 * pr, q = p + 1, x = pr == 0 ? 2 : 0, y = pr == 0 ? 3 : 1;
+        // leaf: the smaller J (ties: the higher mode), as in the HOOI flop model (nnode is the same)
+        const int leaf = h->J[x] < h->J[y] ? x : y, mid1 = leaf == x ? y : x;
+        int ci = -1;
+        if (pr == 0) {
+          ci = h->mp_csf[p][leaf];  // mids ascending = (1, mid1)
+        } else {
+          auto cs = std::make_unique<Csf>();
+          csf_build(c, *cs, p, q, mid1, leaf, h->st);
+          mark("csf_build (memo)");
+          ci = (int)h->csfs.size();
+          h->csfs.push_back(std::move(cs));
+        }
+        const Csf& cm = *h->csfs[ci];
+        size_t fr = 0, tot = 0;
+        TK_CUDA(cudaMemGetInfo(&fr, &tot));
+        const double zbytes = 4.0 * (double)cm.nnode * (double)h->J[mid1] * (double)round_up(h->J[leaf], 4);
+        if (cm.mid0 != q || !spttmc4g_fma_default(cm, h->J) || zbytes > (double)fr / 8) {
+          if (pr == 1) h->csfs.pop_back();
+          continue;
+        }
+        h->memo[pr].csf = ci;
+        h->memo[pr].root = p;
+        h->memo[pr].sib = q;
+        h->hooi_csf[p] = ci;
+      }
+    }
     for (int n = 0; n < order; ++n) {  // order 4: Jm = J_mid0 J_mid1 (the partial row is prod_{q != n} J_q)
       Csf& ch = *h->csfs[h->hooi_csf[n]];
       const int64_t Jm = h->J[ch.mid0] * (order == 4 ? h->J[ch.mid1] : 1);
@@ -1008,6 +1094,7 @@ int tucker_set_factors(tucker_handle* h, const float* const* U) {
                               on_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, h->st));
     TK_CUDA(cudaStreamSynchronize(h->st));
     h->G_valid = false;
+    memo_invalidate(h, -1);
     for (auto& row : h->slots)
       for (auto& s : row) s.valid = false;
     return TUCKER_OK;
@@ -1079,6 +1166,35 @@ int mp_sweep(tucker_handle* h, int sweeps, double* fit_per_sweep, float* stage_m
       if (fit_per_sweep) fit_per_sweep[s] = compute_core(h);
       TK_CUDA(cudaEventRecord(ev.e[4 * N + 1], h->st));
       TK_CUDA(cudaEventSynchronize(ev.e[4 * N + 1]));  // the sweep's one host synchronisation
+      for (int n = 0; n < N; ++n) {  // overlap accounting (events of this sweep; all but the last side are complete)
+        const unsigned rec = h->tl_rec[n];
+        h->tl_rec[n] = 0;
+        cudaEvent_t* t = h->tl[n];
+        float v = 0;
+        if ((rec & 1u) && cudaEventElapsedTime(&v, t[0], t[1]) == cudaSuccess) {
+          h->ov_ms[4] += v;
+          ++h->ov_cnt[4];
+        }
+        if (rec & 12u) {
+          float a = 0, b = 0;
+          if (cudaEventElapsedTime(&a, t[4], t[5]) == cudaSuccess && cudaEventElapsedTime(&b, t[5], t[6]) == cudaSuccess) {
+            h->ov_ms[2] += a;
+            h->ov_cnt[2] += (rec & 8u) ? N - 1 : 1;
+            h->ov_ms[3] += b;
+            ++h->ov_cnt[3];
+          }
+        }
+        if ((rec & 2u) && cudaEventQuery(t[3]) == cudaSuccess) {  // the last mode's side work may still run
+          float a = 0, b = 0;
+          if (cudaEventElapsedTime(&a, t[0], t[2]) == cudaSuccess && cudaEventElapsedTime(&b, t[2], t[3]) == cudaSuccess) {
+            h->ov_ms[0] += a;
+            h->ov_cnt[0] += N - 2;
+            h->ov_ms[1] += b;
+            ++h->ov_cnt[1];
+          }
+        }
+        (void)cudaGetLastError();
+      }
       if (mp_timeline()) {
         TK_CUDA(cudaDeviceSynchronize());
         for (int n = 0; n < N; ++n) {
@@ -1191,6 +1307,7 @@ int tucker_set_factor(tucker_handle* h, int n, const float* U, int check) {
                             on_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, h->st));
     TK_CUDA(cudaStreamSynchronize(h->st));
     h->G_valid = false;
+    memo_invalidate(h, n);
     for (auto& row : h->slots) row[n].valid = false;  // the next solve of mode n starts from U
     return TUCKER_OK;
   });
@@ -1389,6 +1506,9 @@ int tucker_time_ttmc(tucker_handle* h, int mode, int reps, float* ms_out) {
   if (!h || !ms_out || mode < 0 || mode >= h->order || reps < 1) return TUCKER_E_ARG;
   return guarded(h, [&]() -> int {
     const bool tr = prod_J_except(h, mode) < h->dims[mode] && h->J[mode] <= kMaxBlock;
+    // the sweep's path: a sibling mode of the partial-contraction reuse reads the Z its root mode kept
+    for (auto& m : h->memo)
+      if (m.csf >= 0 && m.sib == mode && !m.valid) project_hooi(h, m.root, false);
     project_hooi(h, mode, tr);  // untimed: buffers, first-touch
     SweepEvents ev(2);
     TK_CUDA(cudaEventRecord(ev.e[0], h->st));
@@ -1451,6 +1571,7 @@ int tucker_hosvd(tucker_handle* h, unsigned mode_mask) {
       sparse_gram(c, f0, f1, h->S.p, lds, h->st);
       if (h->sharded) dist_allreduce_f64(h->comm, h->S.p, d * lds, h->st);
       h->scratch_slot.valid = false;
+      memo_invalidate(h, n);
       solve_eig(h, d, J, h->scratch_slot, h->U[n].p);
       canon_to_f32(h->V.p, J, d, J, h->U[n].p, h->st);
       TK_CUDA(cudaStreamSynchronize(h->st));
@@ -1499,6 +1620,19 @@ int tucker_shard_info(tucker_handle* h, int64_t* out) {
       const Csf& t = *h->csfs[h->mp_csf[n][m]];
       o[0] = h->sharded ? h->mp_lo[n][m] : 0;
       o[1] = h->sharded ? h->mp_hi[n][m] : t.I_mid0 * t.I_mid1;
+    }
+  }
+  return TUCKER_OK;
+}
+
+int tucker_mp_overlap_times(tucker_handle* h, double* ms, int64_t* counts, int reset) {
+  if (!h || !ms || !counts) return TUCKER_E_ARG;
+  for (int q = 0; q < 5; ++q) {
+    ms[q] = h->ov_ms[q];
+    counts[q] = h->ov_cnt[q];
+    if (reset) {
+      h->ov_ms[q] = 0;
+      h->ov_cnt[q] = 0;
     }
   }
   return TUCKER_OK;
