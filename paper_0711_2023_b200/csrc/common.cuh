@@ -41,6 +41,9 @@ void mempool_retain(int device);  // default pool keeps freed memory (once per d
 // SMs held by a concurrent kernel of the calling handle (MP overlap): persistent grids size to
 // (SMs - g_sm_reserve) so no block waits for a held SM's slots
 extern thread_local int g_sm_reserve;
+// when set, the one-CTA direct eigensolver records this event right after its kernel (the MP overlap's
+// accounting: the solver kernel's own time, apart from the small kernels queued behind it)
+extern thread_local cudaEvent_t g_eig_kernel_event;
 
 bool sync_check_enabled();  // env TUCKER_SYNC_CHECK: synchronise + check after every launch
 

@@ -20,6 +20,7 @@ namespace tk {
 thread_local int64_t* g_launch_counter = nullptr;
 thread_local cudaStream_t g_alloc_stream = nullptr;
 thread_local int g_sm_reserve = 0;
+thread_local cudaEvent_t g_eig_kernel_event = nullptr;
 void mempool_retain(int device) {
   static bool done[64] = {};
   if (device < 0 || device >= 64 || done[device]) return;

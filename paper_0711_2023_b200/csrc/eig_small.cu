@@ -1261,6 +1261,7 @@ void eig_small(const double* S, int64_t n, int64_t lds, int m, double* V, double
     a.dbg = std::getenv("TUCKER_EIG_DBG") ? std::atoi(std::getenv("TUCKER_EIG_DBG")) : 0;
     smem_optin((const void*)k_eig_direct_t, wst * sizeof(double));
     TK_LAUNCH(k_eig_direct_t, 1, kDT, wst * sizeof(double), st, a);
+    if (g_eig_kernel_event) TK_CUDA(cudaEventRecord(g_eig_kernel_event, st));
     if (prof) {
       unsigned long long t[16];
       TK_CUDA(cudaStreamSynchronize(st));
@@ -1291,6 +1292,7 @@ void eig_small(const double* S, int64_t n, int64_t lds, int m, double* V, double
     a.dbg = 0;
     smem_optin((const void*)k_eig_direct, ws * sizeof(double));
     TK_LAUNCH(k_eig_direct, 1, kDT, ws * sizeof(double), st, a);
+    if (g_eig_kernel_event) TK_CUDA(cudaEventRecord(g_eig_kernel_event, st));
     if (prof) {
       unsigned long long t[8];
       TK_CUDA(cudaStreamSynchronize(st));

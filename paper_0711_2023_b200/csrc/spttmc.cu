@@ -1189,8 +1189,10 @@ void spttmc_hooi(const Csf& c, const float* const* U, const int64_t* J, Split ou
     TK_S3V(ra, rb, 1) TK_S3V(ra, rb, 2) TK_S3V(ra, rb, 4)                      \
     launched = true;                                                           \
   }
+    // (8, 1): J_mid in (64, 128] with J_leaf <= 16 (config 3 mode 2: 100 x 10) -- without it the
+    // dispatch fell through to (8, 2) and did twice the Kronecker FMAs on zero-padded columns
     TK_S3(1, 1) TK_S3(2, 1) TK_S3(1, 2) TK_S3(2, 2) TK_S3(4, 1) TK_S3(1, 4) TK_S3(4, 2)
-    TK_S3(2, 4) TK_S3(4, 4) TK_S3(8, 2) TK_S3(2, 8) TK_S3(8, 4) TK_S3(4, 8) TK_S3(8, 8)
+    TK_S3(2, 4) TK_S3(4, 4) TK_S3(8, 1) TK_S3(8, 2) TK_S3(2, 8) TK_S3(8, 4) TK_S3(4, 8) TK_S3(8, 8)
 #undef TK_S3
 #undef TK_S3V
     if (!launched) fail(TUCKER_E_ARG, "spttmc: unsupported core size");

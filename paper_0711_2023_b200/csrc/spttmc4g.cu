@@ -1289,7 +1289,7 @@ bool spttmc4g(const Csf& c, const float* const* U, const int64_t* J, Split out, 
 // i_p, one fixed-order sum per output (deterministic).  kSibJ: U_p columns per thread (one
 // tile covers J_p <= 24, so Z is read once; larger J_p in tiles of 16).
 // ---------------------------------------------------------------------------
-constexpr int kSibT = 128, kSibN = 32, kSibU = 8;
+constexpr int kSibT = 64, kSibN = 32, kSibU = 16;
 template <int kSibJ>
 __global__ void __launch_bounds__(kSibT) k_spttmc4_sib(const float* __restrict__ Z, const int32_t* __restrict__ sib_ptr,
                                                       const int32_t* __restrict__ sib_node,

@@ -65,7 +65,7 @@ struct tucker_handle {
   DBuf<double> S2;
   GramWs gram2;
   bool side_ready[kMaxOrder] = {};
-  cudaEvent_t tl[kMaxOrder][7] = {};  // TUCKER_MP_TIMELINE=1: fork, eig end, side SpMM end, side Gram end,
+  cudaEvent_t tl[kMaxOrder][8] = {};  // TUCKER_MP_TIMELINE=1: fork, eig end, side SpMM end, side Gram end,
                                       // late start, late SpMM end, late Gram end
   int64_t launches = 0;
   int64_t stat_outer0 = 0, stat_matvec0 = 0, stat_sweeps0 = 0;
@@ -99,7 +99,12 @@ struct tucker_handle {
 };
 // kept W buffers of all live handles in this process (budget: a quarter of the device)
 static std::atomic<size_t> g_wkeep_bytes{0};
-tucker_handle::~tucker_handle() { g_wkeep_bytes -= wkeep_bytes; }
+tucker_handle::~tucker_handle() {
+  g_wkeep_bytes -= wkeep_bytes;
+  for (auto& row : tl)
+    for (auto& e : row)
+      if (e) cudaEventDestroy(e);
+}
 
 
 namespace {
@@ -662,7 +667,7 @@ void mp_update_overlap(tucker_handle* h, int n, EigSlot& slot, cudaEvent_t ev_pr
   const int64_t d = h->dims[n];
   const int64_t lds = ensure_S(h, d);
   cudaEvent_t* tl = h->tl[n];  // always on: seven event records per mode
-  for (int q = 0; q < 7; ++q)
+  for (int q = 0; q < 8; ++q)
     if (!tl[q]) TK_CUDA(cudaEventCreate(&tl[q]));
   h->tl_rec[n] = 0;
   if (h->side_ready[n]) {  // early terms done on st2: the late term, S = S2 + W_late W_late^T
@@ -698,15 +703,19 @@ void mp_update_overlap(tucker_handle* h, int n, EigSlot& slot, cudaEvent_t ev_pr
     TK_CUDA(cudaStreamWaitEvent(h->st_hi, h->ev_fork, 0));
     cudaStream_t main_st = h->st;
     h->st = h->st_hi;
+    TK_CUDA(cudaEventRecord(tl[7], h->st_hi));  // (re-recorded right after the direct solver's kernel)
+    g_eig_kernel_event = tl[7];
     try {
       const AllocScope as(h->st_hi);
       Split A;
       A.rows = d;
       factor_from_S(h, n, A, false, slot, false);
     } catch (...) {
+      g_eig_kernel_event = nullptr;
       h->st = main_st;
       throw;
     }
+    g_eig_kernel_event = nullptr;
     h->st = main_st;
     TK_CUDA(cudaEventRecord(h->ev_eig, h->st_hi));
     if (tl) TK_CUDA(cudaEventRecord(tl[1], h->st_hi));
@@ -1171,7 +1180,11 @@ int mp_sweep(tucker_handle* h, int sweeps, double* fit_per_sweep, float* stage_m
         h->tl_rec[n] = 0;
         cudaEvent_t* t = h->tl[n];
         float v = 0;
-        if ((rec & 1u) && cudaEventElapsedTime(&v, t[0], t[1]) == cudaSuccess) {
+        // [4]: fork -> the solver kernel's end when the one-CTA direct solver ran (t[7] re-recorded
+        // after it; the small kernels behind it wait for SM slots beside the side work), else -> t[1]
+        if ((rec & 1u) && cudaEventElapsedTime(&v, t[0], t[7]) == cudaSuccess) {
+          float w = 0;
+          if (v < 1e-3f && cudaEventElapsedTime(&w, t[0], t[1]) == cudaSuccess) v = w;
           h->ov_ms[4] += v;
           ++h->ov_cnt[4];
         }

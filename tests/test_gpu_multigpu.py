@@ -31,6 +31,9 @@ def test_sharded_path_world1_matches_unsharded(capi, monkeypatch, dims, nnz, cor
     # bit-identity: the unsharded MP sweep without the eigensolve / next-mode overlap (which
     # splits each M_n sum into two fp64 partial sums, test_gpu_parity.test_mp_overlap)
     monkeypatch.setenv("TUCKER_MP_OVERLAP", "0")
+    # ... and without the one-rank order-4 path that sums in another order (HOOI's reuse of Z for
+    # modes 2 and 4; against the oracle in test_gpu_memo.py)
+    monkeypatch.setenv("TUCKER_HOOI_MEMO", "0")
     rng = np.random.default_rng(31)
     idx, vals = uniform_distinct_coo(dims, nnz, rng)
     U0 = [random_orthonormal(I, J, np.random.default_rng(40 + k)) for k, (I, J) in enumerate(zip(dims, core))]
