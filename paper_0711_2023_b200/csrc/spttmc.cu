@@ -217,6 +217,47 @@ __device__ __forceinline__ void kron_stage(int nf, const float* T, const float* 
   }
 }
 
+// Small cores (16 RA x 16 RB <= 512 outputs per slice): the 16 x 16 thread grid above leaves each
+// thread 1-2 accumulators, i.e. ~3 shared loads and loop overhead per 1-2 FMAs in all 8 warps for every
+// fiber (ncu at config 3 mode 1, 25 x 10 outputs: issue 83 %, FMA 36 %).  Here each warp runs the
+// Kronecker update of the fibers it produced in the leaf stage itself (fl = warp, warp + 8, ...: no
+// block barrier between the stages), lane = a BR x 4 block of the tile (two vector loads per 4 BR
+// FMAs), and the 8 per-warp partial tiles are summed in warp order at the end (deterministic).
+template <int RA, int RB>
+struct KronSmall {
+  static constexpr int JLP = 16 * RB, JMP = 16 * RA;
+  static constexpr int CB = JLP / 4;        // 4-column blocks per row
+  static constexpr int RBK = 32 / CB;       // row blocks
+  static constexpr bool on = RA * RB <= 2;
+  static constexpr int BR = on ? JMP / RBK : 1;  // rows per lane: 2 or 4
+};
+template <int RA, int RB>
+__device__ __forceinline__ void kron_small(int nf, const float* T, const float* M,
+                                           float (&acc)[KronSmall<RA, RB>::BR][4]) {
+  using K = KronSmall<RA, RB>;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int cb = lane % K::CB, rb = lane / K::CB;
+  for (int fl = warp; fl < nf; fl += 8) {
+    const float4 b = *reinterpret_cast<const float4*>(T + fl * K::JLP + 4 * cb);
+    float a[K::BR];
+    const float* mr = M + fl * K::JMP + rb * K::BR;
+    if constexpr (K::BR == 4) {
+      const float4 v = *reinterpret_cast<const float4*>(mr);
+      a[0] = v.x; a[1] = v.y; a[2] = v.z; a[3] = v.w;
+    } else {
+      const float2 v = *reinterpret_cast<const float2*>(mr);
+      a[0] = v.x; a[1] = v.y;
+    }
+#pragma unroll
+    for (int r = 0; r < K::BR; ++r) {
+      acc[r][0] += a[r] * b.x;
+      acc[r][1] += a[r] * b.y;
+      acc[r][2] += a[r] * b.z;
+      acc[r][3] += a[r] * b.w;
+    }
+  }
+}
+
 struct Ttmc3Args {
   const int32_t *slice_ptr, *fib_ptr, *fib_mid, *leaf_id;
   const int32_t* unit;  // work units (slice, f0, f1, slot) or null: one CTA per slice
@@ -256,6 +297,12 @@ __global__ void __launch_bounds__(256) k_spttmc3(Ttmc3Args p) {
   for (int r = 0; r < RA; ++r)
 #pragma unroll
     for (int c = 0; c < RB; ++c) acc[r][c] = 0.f;
+  using KS = KronSmall<RA, RB>;
+  float acc2[KS::BR][4];  // small cores: this warp's partial BR x 4 block (kron_small)
+#pragma unroll
+  for (int r = 0; r < KS::BR; ++r)
+#pragma unroll
+    for (int c = 0; c < 4; ++c) acc2[r][c] = 0.f;
   __shared__ int fptr[kFC + 1], fmid[kFC];
   __shared__ int sl[kNS];
   __shared__ float sv[kNS];
@@ -287,11 +334,36 @@ __global__ void __launch_bounds__(256) k_spttmc3(Ttmc3Args p) {
     __syncthreads();
     leaf_stage_s<JLP, JMP, VW>(nf, fptr, fmid, staged ? sl : nullptr, sv, p.leaf_id, p.val, p.Umid, p.Jm,
                            p.Uleaf, p.Jl, T, M);
-    __syncthreads();
-    kron_stage<RA, RB>(nf, T, M, acc);
+    if constexpr (KS::on) {
+      __syncwarp();  // each warp consumes the T / M rows it wrote (fl = warp + 8 k in both stages)
+      kron_small<RA, RB>(nf, T, M, acc2);
+    } else {
+      __syncthreads();
+      kron_stage<RA, RB>(nf, T, M, acc);
+    }
     __syncthreads();
   }
   const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  if constexpr (KS::on) {  // the 8 warps' partial tiles, summed in warp order
+    __shared__ __align__(16) float red[8][JMP * JLP];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int cb = lane % KS::CB, rb = lane / KS::CB;
+#pragma unroll
+    for (int r = 0; r < KS::BR; ++r)
+      *reinterpret_cast<float4*>(&red[warp][(rb * KS::BR + r) * JLP + 4 * cb]) =
+          make_float4(acc2[r][0], acc2[r][1], acc2[r][2], acc2[r][3]);
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < RA; ++r)
+#pragma unroll
+      for (int c = 0; c < RB; ++c) {
+        const int e = (ty * RA + r) * JLP + kron_col<RA, RB>(tx, c);
+        float v = 0.f;
+#pragma unroll
+        for (int w = 0; w < 8; ++w) v += red[w][e];
+        acc[r][c] = v;
+      }
+  }
 #pragma unroll
   for (int r = 0; r < RA; ++r)
 #pragma unroll

@@ -106,3 +106,27 @@ def test_memo_off_when_sparse(capi):
     idx, vals, U0 = case(dims, nnz, core)
     with capi.Tucker(dims, core, idx, vals, U0) as t:
         assert not memo_active(t)
+
+
+def test_mp_overlap_times(capi):
+    """tucker_mp_overlap_times: counts follow the overlap's structure (order 4, d <= 208: the one-CTA
+    solver beside the side stream) -- per sweep N solves and N main-stream Grams, N (N - 1) SpMM terms
+    split between the side and main streams -- and every counted time is positive; reset zeroes them."""
+    dims, nnz, core = (24, 20, 32, 18), 33_000, (5, 3, 6, 4)
+    idx, vals, U0 = case(dims, nnz, core)
+    N, S = 4, 3
+    with capi.Tucker(dims, core, idx, vals, U0) as t:
+        t.mp_sweep(S)
+        ov = capi.tucker_mp_overlap_times(t.h)
+        assert ov["eig"][1] == N * S and ov["main_gram"][1] == N * S
+        # sweep 0 mode 0 builds all N - 1 terms on the main stream; every other mode only the late term
+        assert ov["main_spmm"][1] == (N - 1) + (N * S - 1)
+        # the side work of the call's last mode is never launched; all others have finished by a sweep's end
+        # except possibly the one prepared for the next sweep's first mode (counted only if finished)
+        assert N * S - 1 - (S - 1) <= ov["side_gram"][1] <= N * S - 1
+        assert ov["side_spmm"][1] == ov["side_gram"][1] * (N - 2)
+        for k, (ms, cnt) in ov.items():
+            assert ms > 0 and cnt > 0, k
+        capi.tucker_mp_overlap_times(t.h, reset=True)
+        ov = capi.tucker_mp_overlap_times(t.h)
+        assert all(ms == 0 and cnt == 0 for ms, cnt in ov.values())
