@@ -219,10 +219,10 @@ __device__ __forceinline__ void kron_stage(int nf, const float* T, const float* 
 
 // Small cores (16 RA x 16 RB <= 512 outputs per slice): the 16 x 16 thread grid above leaves each
 // thread 1-2 accumulators, i.e. ~3 shared loads and loop overhead per 1-2 FMAs in all 8 warps for every
-// fiber (ncu at config 3 mode 1, 25 x 10 outputs: issue 83 %, FMA 36 %).  Here each warp runs the
-// Kronecker update of the fibers it produced in the leaf stage itself (fl = warp, warp + 8, ...: no
-// block barrier between the stages), lane = a BR x 4 block of the tile (two vector loads per 4 BR
-// FMAs), and the 8 per-warp partial tiles are summed in warp order at the end (deterministic).
+// fiber (ncu at config 3 mode 1, 25 x 10 outputs: issue 83 %, FMA 36 %).  Here a chunk is 128 fibers,
+// each warp runs the Kronecker update of 16 of them, lane = a BR x 4 block of the tile (two vector
+// loads per 4 BR FMAs), and the 8 per-warp partial tiles are summed in warp order at the end
+// (deterministic).
 template <int RA, int RB>
 struct KronSmall {
   static constexpr int JLP = 16 * RB, JMP = 16 * RA;
@@ -231,13 +231,15 @@ struct KronSmall {
   static constexpr bool on = RA * RB <= 2;
   static constexpr int BR = on ? JMP / RBK : 1;  // rows per lane: 2 or 4
 };
+constexpr int kFCS = 128;  // fibers per chunk on the small-core path
 template <int RA, int RB>
 __device__ __forceinline__ void kron_small(int nf, const float* T, const float* M,
                                            float (&acc)[KronSmall<RA, RB>::BR][4]) {
   using K = KronSmall<RA, RB>;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int cb = lane % K::CB, rb = lane / K::CB;
-  for (int fl = warp; fl < nf; fl += 8) {
+  const int fl1 = min(nf, (warp + 1) * (kFCS / 8));
+  for (int fl = warp * (kFCS / 8); fl < fl1; ++fl) {
     const float4 b = *reinterpret_cast<const float4*>(T + fl * K::JLP + 4 * cb);
     float a[K::BR];
     const float* mr = M + fl * K::JMP + rb * K::BR;
@@ -255,6 +257,48 @@ __device__ __forceinline__ void kron_small(int nf, const float* T, const float* 
       acc[r][2] += a[r] * b.z;
       acc[r][3] += a[r] * b.w;
     }
+  }
+}
+
+// Small-core leaf stage, one LANE per fiber (the warp-per-fiber stage above keeps 5 of 32 lanes busy at
+// J_leaf = 10 and spends ~60 instructions per fiber): t_f in registers, the U_leaf rows read as VW-float
+// vectors (L1 / L2 hits: the table is I x J_leaf floats), then one padded row of T.
+template <int JLP, int VW>
+__device__ __forceinline__ void leaf_lane(int t, const int* fptr, const int* sl, const float* sv, int E0,
+                                          const int32_t* __restrict__ leaf_id, const float* __restrict__ val,
+                                          const float* __restrict__ Uleaf, int Jl, float* T) {
+  using V = typename FVec<VW>::T;
+  constexpr int NV = JLP / VW;
+  float tt[JLP];
+#pragma unroll
+  for (int j = 0; j < JLP; ++j) tt[j] = 0.f;
+  const int e0 = fptr[t], e1 = fptr[t + 1];
+  for (int e = e0; e < e1; ++e) {
+    int l;
+    float x;
+    if (sl) {
+      l = sl[e - E0];
+      x = sv[e - E0];
+    } else {
+      l = __ldg(leaf_id + e);
+      x = __ldg(val + e);
+    }
+    const V* r = reinterpret_cast<const V*>(Uleaf + (int64_t)l * Jl);
+#pragma unroll
+    for (int v = 0; v < NV; ++v)
+      if (v * VW < Jl) FVec<VW>::fma(x, __ldg(r + v), tt + v * VW);
+  }
+  float4* Tw = reinterpret_cast<float4*>(T + t * JLP);
+#pragma unroll
+  for (int q = 0; q < JLP / 4; ++q) Tw[q] = make_float4(tt[4 * q], tt[4 * q + 1], tt[4 * q + 2], tt[4 * q + 3]);
+}
+// the chunk's U_mid rows (zero padded to JMP <= 32), a warp per row, by the upper four warps
+template <int JMP>
+__device__ __forceinline__ void mid_rows(int nf, const int* fmid, const float* __restrict__ Umid, int Jm, float* M) {
+  const int w = (threadIdx.x >> 5) - 4, lane = threadIdx.x & 31;
+  for (int fl = w; fl < nf; fl += 4) {
+    const float* mr = Umid + (int64_t)fmid[fl] * Jm;
+    if (lane < JMP) M[fl * JMP + lane] = lane < Jm ? __ldg(mr + lane) : 0.f;
   }
 }
 
@@ -278,8 +322,9 @@ struct Ttmc3Args {
 template <int RA, int RB, int VW>
 __global__ void __launch_bounds__(256) k_spttmc3(Ttmc3Args p) {
   constexpr int JLP = 16 * RB, JMP = 16 * RA;
-  __shared__ __align__(16) float T[kFC * JLP];
-  __shared__ __align__(16) float M[kFC * JMP];
+  constexpr int FC = KronSmall<RA, RB>::on ? kFCS : kFC;  // fibers per chunk
+  __shared__ __align__(16) float T[FC * JLP];
+  __shared__ __align__(16) float M[FC * JMP];
   int i, f0, f1, slot = -1;
   if (p.unit) {
     const int4 u = reinterpret_cast<const int4*>(p.unit)[blockIdx.x];
@@ -303,17 +348,17 @@ __global__ void __launch_bounds__(256) k_spttmc3(Ttmc3Args p) {
   for (int r = 0; r < KS::BR; ++r)
 #pragma unroll
     for (int c = 0; c < 4; ++c) acc2[r][c] = 0.f;
-  __shared__ int fptr[kFC + 1], fmid[kFC];
+  __shared__ int fptr[FC + 1], fmid[FC];
   __shared__ int sl[kNS];
   __shared__ float sv[kNS];
   // chunk metadata prefetched into registers one chunk ahead
   int nx_ptr = 0, nx_mid = 0;
-  if (f0 < f1 && threadIdx.x <= min(kFC, f1 - f0)) {
+  if (f0 < f1 && threadIdx.x <= min(FC, f1 - f0)) {
     nx_ptr = __ldg(p.fib_ptr + f0 + threadIdx.x);
-    if (threadIdx.x < min(kFC, f1 - f0)) nx_mid = __ldg(p.fib_mid + f0 + threadIdx.x);
+    if (threadIdx.x < min(FC, f1 - f0)) nx_mid = __ldg(p.fib_mid + f0 + threadIdx.x);
   }
-  for (int fc = f0; fc < f1; fc += kFC) {
-    const int nf = min(kFC, f1 - fc);
+  for (int fc = f0; fc < f1; fc += FC) {
+    const int nf = min(FC, f1 - fc);
     if (threadIdx.x <= nf) fptr[threadIdx.x] = nx_ptr;
     if (threadIdx.x < nf) fmid[threadIdx.x] = nx_mid;
     __syncthreads();
@@ -325,19 +370,26 @@ __global__ void __launch_bounds__(256) k_spttmc3(Ttmc3Args p) {
         sv[e - E0] = __ldg(p.val + e);
       }
     // next chunk's metadata: in flight during this chunk's stages
-    const int fn = fc + kFC;
+    const int fn = fc + FC;
     if (fn < f1) {
-      const int nfn = min(kFC, f1 - fn);
+      const int nfn = min(FC, f1 - fn);
       if (threadIdx.x <= nfn) nx_ptr = __ldg(p.fib_ptr + fn + threadIdx.x);
       if (threadIdx.x < nfn) nx_mid = __ldg(p.fib_mid + fn + threadIdx.x);
     }
     __syncthreads();
-    leaf_stage_s<JLP, JMP, VW>(nf, fptr, fmid, staged ? sl : nullptr, sv, p.leaf_id, p.val, p.Umid, p.Jm,
-                           p.Uleaf, p.Jl, T, M);
     if constexpr (KS::on) {
-      __syncwarp();  // each warp consumes the T / M rows it wrote (fl = warp + 8 k in both stages)
+      // lower four warps: one lane per fiber (t_f); upper four: the fibers' U_mid rows
+      if (threadIdx.x < kFCS) {
+        if ((int)threadIdx.x < nf)
+          leaf_lane<JLP, VW>(threadIdx.x, fptr, staged ? sl : nullptr, sv, E0, p.leaf_id, p.val, p.Uleaf, p.Jl, T);
+      } else {
+        mid_rows<JMP>(nf, fmid, p.Umid, p.Jm, M);
+      }
+      __syncthreads();
       kron_small<RA, RB>(nf, T, M, acc2);
     } else {
+      leaf_stage_s<JLP, JMP, VW>(nf, fptr, fmid, staged ? sl : nullptr, sv, p.leaf_id, p.val, p.Umid, p.Jm,
+                                 p.Uleaf, p.Jl, T, M);
       __syncthreads();
       kron_stage<RA, RB>(nf, T, M, acc);
     }
